@@ -1,0 +1,414 @@
+"""Benchmark: batched step + render frames/s on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C3]
+    python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N
+    python bench.py --impl reference        # the reference CPU path (oracle port)
+
+A "step" is one Simulator.step + observations() for every env of the shard:
+agent step (swept-disc collision + slide), column raycast, frame fill, all on
+the GPU through the C ABI.  Default workload = BASELINE.json configs[2] (C3):
+1024 envs per GPU x 256x256 RGB-D on a ~200k-triangle synthetic apartment
+(weak scaling: per-GPU work fixed).  Frames written per step (470 MB) exceed
+the 126 MB L2, so no explicit flush is needed between timed steps.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # name: (envs per GPU, W, H, channels, scene)
+    "C1": (1, 256, 256, ("rgb", "depth"), "C1"),
+    "C2": (64, 128, 128, ("depth",), "C2"),
+    "C3": (1024, 256, 256, ("rgb", "depth"), "C3"),
+    "C4": (1024, 256, 256, ("rgb", "depth", "semantic"), "C4"),
+    "C5": (512, 512, 512, ("rgb", "depth"), "C5"),
+}
+WORKLOAD = {
+    "C1": "1 env, 256x256 RGB+depth, 1-room ~2k tris (1000 segments)",
+    "C2": "64 envs, 128x128 depth, multi-room ~20k tris",
+    "C3": "1024 envs/GPU, 256x256 RGB-D, ~200k-tri synthetic apartment",
+    "C4": "1024 envs/GPU (8192 over 8), 256x256 RGB-D+semantic, ~200k tris",
+    "C5": "512 envs/GPU (4096 over 8), 512x512 RGB-D, ~1M tris",
+}
+BYTES_PER_PX = {"rgb": 3, "depth": 4, "semantic": 2}
+METRIC = "RGB-D frames/sec (256\u00d7256, N envs) at 1/2/4/8 B200; % of HBM roofline"
+STEP_IO_BYTES = 94   # per env: pose in/out, action, step outputs, gps/compass
+
+
+def bytes_per_env_step(W, H, channels):
+    return W * H * sum(BYTES_PER_PX[c] for c in channels) + STEP_IO_BYTES
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons during the timed region."""
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([v.strip() for v in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            time.sleep(0.15)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            try:
+                sm.append(float(r[0]))
+                mx.append(float(r[1]))
+            except (ValueError, IndexError):
+                continue
+            for n, v in zip(names, r[4:8]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx),
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json copy test)"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+# --------------------------------------------------------------- CPU baseline
+
+def cpu_baseline(cfg: str, seconds: float = 10.0, threads: int | None = None, n_envs=None):
+    """The reference's CPU path (oracle port of Simulator.step + observations,
+    f64 frames like fill_frame) on the host cores, time-bounded sample."""
+    from oracle import oracle
+    from paper_1904_01201_b200 import synth
+    N_cfg, W, H, chans, scene_key = CONFIGS[cfg]
+    threads = threads or os.cpu_count() or 1
+    sc = synth.config_scene(scene_key)
+    osc = oracle.OracleScene(sc.segments, sc.semantic_ids, sc.albedo, sc.wall_height,
+                             sc.floor_color, sc.ceiling_color)
+    n = n_envs or max(1, min(N_cfg, 4 * threads))
+    poses = synth.sample_poses(sc, n, seed=1)
+    x, y = poses[:, 0].copy(), poses[:, 1].copy()
+    h = np.array([oracle.wrap_angle(v) for v in poses[:, 2]])
+    path = np.zeros(n)
+    coll = np.zeros(n, dtype=np.int64)
+    depth = np.empty((n, H, W)) if "depth" in chans else None
+    rgb = np.empty((n, H, W, 3)) if "rgb" in chans else None
+    sem = np.empty((n, H, W), dtype=np.uint16) if "semantic" in chans else None
+    focal = (W * 0.5) / math.tan(math.radians(90.0) * 0.5)
+    acts = synth.random_actions(n, 10_000, seed=2)
+    frames, steps, t0 = 0, 0, time.perf_counter()
+    osc.batch_step_render(x, y, h, path, coll, acts[0], 0.1, 0.25, 10.0, 1.5, W, H, focal, 10.0,
+                          depth, rgb, sem, threads)  # warm-up
+    t0 = time.perf_counter()
+    while True:
+        osc.batch_step_render(x, y, h, path, coll, acts[(steps + 1) % len(acts)], 0.1, 0.25, 10.0,
+                              1.5, W, H, focal, 10.0, depth, rgb, sem, threads)
+        steps += 1
+        frames += n
+        el = time.perf_counter() - t0
+        if el >= seconds:
+            break
+    return {"value": frames / el, "unit": "frames/s", "cores": threads, "kind": "port",
+            "sample": f"{n} envs x {steps} steps of {WORKLOAD[cfg]} ({el:.1f} s, "
+                      f"oracle/navsim_oracle.c, f64 frames like the reference)",
+            "cpu_model": _cpu_model()}
+
+
+def _cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    cfg = args.config
+    per_step = []
+    res = None
+    for s in range(args.warmup + args.steps):
+        r = cpu_baseline(cfg, seconds=max(1.0, args.ref_seconds / max(1, args.steps)),
+                         n_envs=args.ref_envs)
+        if s >= args.warmup:
+            per_step.append(r["value"])
+            res = r
+    v = statistics.median(per_step)
+    N_cfg, W, H, chans, _ = CONFIGS[cfg]
+    line = {"impl": "reference", "metric": METRIC,
+            "value": v, "unit": "frames/s", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": WORKLOAD[cfg], "config": cfg},
+            "cpu_baseline": dict(res, value=v),
+            "e2e": {"value": v, "unit": "frames/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+    return 0
+
+
+# ------------------------------------------------------------------- GPU path
+
+def run_gpu(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1904_01201_b200 import BatchSimulator, SensorConfig, synth
+    from paper_1904_01201_b200 import _native as nat
+    from paper_1904_01201_b200.dist import EnvShard, gather_episode_stats
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cfg = args.config
+    N, W, H, chans, scene_key = CONFIGS[cfg]
+    if args.envs:
+        N = args.envs
+    shard = EnvShard(n_total=N * world, world=world, rank=rank)
+    sc = synth.config_scene(scene_key)
+    suite = tuple(SensorConfig(c, W, H) for c in chans) + (SensorConfig("gps_compass"),)
+    sim = BatchSimulator(sc.segments, sc.semantic_ids, sc.albedo, shard.n_local,
+                         sensor_configs=suite, wall_height=sc.wall_height,
+                         floor_color=sc.floor_color, ceiling_color=sc.ceiling_color, device=local)
+    poses = synth.sample_poses(sc, shard.n_total, seed=1)[shard.lo:shard.hi]
+    sim.reset(poses[:, :2], poses[:, 2])
+    total_steps = args.warmup + args.steps
+    acts = torch.as_tensor(synth.random_actions(shard.n_total, total_steps, seed=2)[:, shard.lo:shard.hi].copy(),
+                           device=f"cuda:{local}")
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    # warm-up (also JIT/first-launch costs), then capture the timed steps in one graph
+    for s in range(args.warmup):
+        sim.step(acts[s])
+    torch.cuda.synchronize()
+    use_graph = not args.no_graph
+    launches0 = sim.launches()
+    if use_graph:
+        g = torch.cuda.CUDAGraph()
+        cap = torch.cuda.Stream()
+        cap.wait_stream(stream)
+        with torch.cuda.stream(cap):
+            with torch.cuda.graph(g, stream=cap):
+                for s in range(args.warmup, total_steps):
+                    sim.step(acts[s])
+        stream.wait_stream(cap)
+        torch.cuda.synchronize()
+    launches_timed = sim.launches() - launches0
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    gpu_index = int(os.environ.get("CUDA_VISIBLE_DEVICES", str(local)).split(",")[local]) \
+        if os.environ.get("CUDA_VISIBLE_DEVICES") else local
+    with ClockSampler(gpu_index) as clk:
+        barrier()
+        torch.cuda.synchronize()
+        start.record(stream)
+        if use_graph:
+            g.replay()
+        else:
+            for s in range(args.warmup, total_steps):
+                sim.step(acts[s])
+        end.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        if clk.proc is not None and start.elapsed_time(end) < 500:
+            # short timed region: keep the same load running untimed for
+            # ~0.6 s so the 100 ms nvidia-smi sampler sees it
+            t_end = time.time() + 0.6
+            while time.time() < t_end:
+                if use_graph:
+                    g.replay()
+                else:
+                    for s in range(args.warmup, total_steps):
+                        sim.step(acts[s])
+                torch.cuda.synchronize()
+    ms = start.elapsed_time(end)
+    t = torch.tensor([ms], dtype=torch.float64, device=f"cuda:{local}")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    frames = shard.n_total * args.steps
+    value = frames / (ms_max / 1e3)
+    # episode statistics: the one collective of the path (NCCL all-gather)
+    stats = gather_episode_stats(sim, shard, world)
+
+    # ---- kernel breakdown: per-kernel CUDA events over a second run of K steps
+    lib, h = sim.ctx.lib, sim.ctx.handle
+    nat.check(lib.nv_profile(h, 1))
+    for s in range(args.warmup, total_steps):
+        sim.step(acts[s])
+    msk = np.zeros(4)
+    cnt = np.zeros(4, dtype=np.int64)
+    nat.check(lib.nv_profile_read(h, nat.ptr(msk), nat.ptr(cnt)))
+    nat.check(lib.nv_profile(h, 0))
+    per = {k: (msk[i] / max(1, cnt[i])) for i, k in enumerate(["agent_step", "column_cast", "frame_fill"])}
+    fill_bytes = shard.n_local * W * H * sum(BYTES_PER_PX[c] for c in chans)
+    peak, peak_src = measured_peaks()
+    achieved = fill_bytes / (per["frame_fill"] / 1e3) / 1e9
+    step_bytes = shard.n_local * bytes_per_env_step(W, H, chans)
+    step_gbs = step_bytes / (ms_max / args.steps / 1e3) / 1e9
+
+    # ---- e2e: host-buffer C-ABI path, pinned host actions in, results out
+    e2e = None
+    e2e_frames = None
+    if not args.no_e2e:
+        n = shard.n_local
+        host_acts = torch.empty((args.steps, n), dtype=torch.int8).pin_memory()
+        host_acts.copy_(acts[args.warmup:total_steps].cpu())
+        out = {"gps": torch.empty((n, 2), dtype=torch.float64).pin_memory(),
+               "compass": torch.empty((n,), dtype=torch.float64).pin_memory(),
+               "collided": torch.empty((n,), dtype=torch.uint8).pin_memory(),
+               "displacement": torch.empty((n,), dtype=torch.float64).pin_memory()}
+        for s in range(min(3, args.steps)):
+            sim.step_host(host_acts[s].numpy(), out=out)
+        barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for s in range(args.steps):
+            sim.step_host(host_acts[s].numpy(), out=out)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        wall = (time.perf_counter() - t0) * 1e3
+        te = torch.tensor([max(wall, e0.elapsed_time(e1))], dtype=torch.float64,
+                          device=f"cuda:{local}")
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e = {"value": frames / (float(te.item()) / 1e3), "unit": "frames/s",
+               "h2d_bytes_per_step": n * 1, "d2h_bytes_per_step": n * (16 + 8 + 1 + 8),
+               "path": "nv_step_render_host: pinned host actions in, host step results "
+                       "(collided, displacement, gps, compass) out; frames stay in HBM "
+                       "for the GPU consumer (the paper's GPU->GPU mode)"}
+        # variant: also copy every frame to pinned host memory (host-consumer mode)
+        k2 = min(args.steps, 5)
+        fr = {c: torch.empty(((n, H, W, 3) if c == "rgb" else (n, H, W)),
+                             dtype={"rgb": torch.uint8, "depth": torch.float32,
+                                    "semantic": torch.uint16}[c]).pin_memory() for c in chans}
+        fr.update(out)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for s in range(k2):
+            sim.step_host(host_acts[s].numpy(), out=fr, frames_to_host=True)
+        wall = (time.perf_counter() - t0) * 1e3
+        tf = torch.tensor([wall], dtype=torch.float64, device=f"cuda:{local}")
+        if world > 1:
+            dist.all_reduce(tf, op=dist.ReduceOp.MAX)
+        e2e_frames = {"value": shard.n_total * k2 / (float(tf.item()) / 1e3), "unit": "frames/s",
+                      "h2d_bytes_per_step": n, "d2h_bytes_per_step":
+                          n * (W * H * sum(BYTES_PER_PX[c] for c in chans) + 33),
+                      "steps": k2}
+
+    line = None
+    if rank == 0:
+        line = {
+            "metric": METRIC,
+            "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64 geometry/kinematics; u8 rgb, f32 depth, u16 semantic outputs",
+            "data": "synthetic (procedural scene, seeded poses/actions)",
+            "config": {"workload": WORKLOAD[cfg], "config": cfg, "envs_per_gpu": shard.n_local,
+                       "envs_total": shard.n_total, "width": W, "height": H,
+                       "channels": list(chans), "segments": sc.n_segments,
+                       "triangles": sc.n_triangles, "parallelism": f"env-shard x{world}",
+                       "cuda_graph": use_graph,
+                       "l2": f"no flush: frames written per step "
+                             f"({step_bytes / 1e6:.0f} MB/GPU) exceed the 126 MB L2"},
+            "roofline": {"bound": "hbm", "kernel": "k_fill_tma (frame_fill)",
+                         "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": None, "peak_source": peak_src,
+                         "bytes_per_launch": fill_bytes,
+                         "kernel_ms": per,
+                         "step_achieved_gbs": step_gbs, "step_frac": step_gbs / peak},
+            "clocks": clk.summary(),
+            "gpu_launches": int(launches_timed),
+            "e2e": e2e,
+            "e2e_host_frames": e2e_frames,
+            "episode_stats": stats,
+        }
+        if not args.no_cpu_baseline:
+            line["cpu_baseline"] = cpu_baseline(cfg, seconds=args.cpu_seconds)
+        print(json.dumps(line))
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="C3", choices=sorted(CONFIGS))
+    ap.add_argument("--envs", type=int, default=0, help="override envs per GPU")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--ref-seconds", type=float, default=60.0)
+    ap.add_argument("--ref-envs", type=int, default=0)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_gpu(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,201 @@
+/* navsim_b200.h -- C ABI of the B200-native navsim hot path.
+ *
+ * Drop-in boundary for the reference's two-level hot-path interface
+ * (/root/reference/pkg/src/navsim):
+ *   - the numba "operator" layer  (_kernels.raycast_grid :51, raycast_all :16,
+ *     fill_frame :128, disc_cast :393, min_seg_distance :468), and
+ *   - the Python Simulator / render API built on it (sim.py:133-219,
+ *     sensors.py:105-152, geometry.py:100-206).
+ * Each entry point below names the reference interface it replaces.
+ *
+ * Conventions
+ *   - Every call returns 0 on success or a negative NV_ERR_* code; the message
+ *     of the last failure on the calling host thread is nv_last_error().
+ *   - A context is owned by ONE host thread at a time, mirroring the
+ *     reference's exclusive-owner rule for a Simulator (sim.py:134-137).
+ *   - "dev" pointers are CUDA device pointers (e.g. torch tensor data_ptr());
+ *     "host" pointers are ordinary host memory.  Hot per-step calls take
+ *     device pointers and a cudaStream_t (passed as void*; NULL = legacy
+ *     default stream) and never synchronise the host.
+ *   - Actions use the reference enum order (sim.py:31-35):
+ *     0 MOVE_FORWARD, 1 TURN_LEFT, 2 TURN_RIGHT, 3 STOP.
+ *   - Frames: rgb u8 [N,H,W,3] (reference: f64 in [0,1], tolerance 1/255),
+ *     depth f32 [N,H,W] metres (reference f64, tolerance 1e-5 rel),
+ *     semantic u16 [N,H,W] (exact).  Any frame pointer may be NULL to skip
+ *     that channel (fill_frame's want_* flags, _kernels.py:131).
+ */
+#ifndef NAVSIM_B200_H
+#define NAVSIM_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define NV_OK 0
+#define NV_ERR_ARG -1        /* invalid argument (SensorError/SimError class)  */
+#define NV_ERR_CUDA -2       /* CUDA runtime failure                           */
+#define NV_ERR_STATE -3      /* call order: no scene / envs / camera / reset   */
+#define NV_ERR_OOM -4        /* device allocation failed                       */
+
+#define NV_ACTION_MOVE_FORWARD 0
+#define NV_ACTION_TURN_LEFT 1
+#define NV_ACTION_TURN_RIGHT 2
+#define NV_ACTION_STOP 3
+
+/* per-env status written by nv_set_poses / nv_step */
+#define NV_ENV_OK 0
+#define NV_ENV_TOO_CLOSE 1   /* clearance < radius (sim.py:176-180)            */
+#define NV_ENV_NOT_RESET 2   /* step before reset (sim.py:203-204)             */
+#define NV_ENV_BAD_ACTION 3  /* unknown action (sim.py:215-216)                */
+
+typedef struct nv_ctx nv_ctx;
+
+const char *nv_last_error(void);
+int nv_version(void);
+
+/* Context on CUDA device `device` (one per process per GPU). */
+int nv_create(int device, nv_ctx **out);
+int nv_destroy(nv_ctx *ctx);
+
+/* Scene upload -- replaces RenderGeometry.__init__ (sensors.py:81-93) +
+ * SegmentIndex.__init__ (geometry.py:109-141) + segment_normals
+ * (geometry.py:66-73).  segs: n x (ax, ay, bx, by) f64 world coordinates
+ * (scene.flatten_arrays output, scene.py:349-378); sem: n u16; albedo: n x 3
+ * f64; floor3/ceil3: 3 f64.  All HOST pointers.  The 1 m uniform grid is built
+ * on the host exactly like SegmentIndex and uploaded once. */
+int nv_scene_upload(nv_ctx *ctx, const double *segs, const uint16_t *sem,
+                    const double *albedo, int64_t n, double wall_height,
+                    const double *floor3, const double *ceil3);
+/* Grid introspection (parity tests): x0, y0, nx, ny, item count. */
+int nv_scene_grid_info(nv_ctx *ctx, double *x0, double *y0, int64_t *nx,
+                       int64_t *ny, int64_t *nitems);
+
+/* Agent kinematics -- AgentConfig (sim.py:49-61).  turn_rad is
+ * math.radians(turn_angle) computed by the caller. */
+int nv_agent_config(nv_ctx *ctx, double radius, double forward_step,
+                    double turn_rad, double sensor_height);
+
+/* Allocate device state for n_envs environments (all un-reset). */
+int nv_envs_alloc(nv_ctx *ctx, int64_t n_envs);
+
+/* Camera (sensor group sharing one traversal, sensors.py:121-123).
+ * cam in [0, 8).  focal = SensorConfig.focal (sensors.py:55-57) computed by
+ * the caller.  Fails (NV_ERR_ARG) if sensor_height > wall_height
+ * (sensors.py:119-120). */
+int nv_camera_config(nv_ctx *ctx, int cam, int width, int height, double focal,
+                     double max_range);
+
+/* Reset -- Simulator.set_agent_state (sim.py:172-184), batched.
+ * HOST arrays of n_envs: xy (n x 2), heading, mask (NULL = all; 0 = leave env
+ * untouched).  status_out (HOST, n_envs i32, may be NULL) receives NV_ENV_*;
+ * clearance_out (HOST, may be NULL) the clearance used for the check.
+ * Synchronous.  Returns NV_ERR_ARG if any masked env failed its check. */
+int nv_set_poses(nv_ctx *ctx, const double *xy, const double *heading,
+                 const uint8_t *mask, int32_t *status_out,
+                 double *clearance_out);
+
+/* Step -- Simulator.step's kinematics (sim.py:202-219: apply_forward :90,
+ * apply_turn :83), batched over all envs.  actions: DEVICE i8[n_envs].
+ * Outputs (DEVICE, each may be NULL): collided u8[n], displacement f64[n],
+ * status i32[n] (NV_ENV_*).  Envs never reset report NV_ENV_NOT_RESET and are
+ * not moved. */
+int nv_step(nv_ctx *ctx, const int8_t *actions, uint8_t *collided,
+            double *displacement, int32_t *status, void *stream);
+
+/* Observations -- sensors.render (sensors.py:105-152) for camera `cam` at the
+ * current poses of all envs, plus gps_compass (sensors.py:175-180).  DEVICE
+ * outputs, each may be NULL: rgb u8[n,H,W,3], depth f32[n,H,W],
+ * sem u16[n,H,W], gps f64[n,2], compass f64[n]. */
+int nv_render(nv_ctx *ctx, int cam, uint8_t *rgb, float *depth, uint16_t *sem,
+              double *gps, double *compass, void *stream);
+
+/* Fused step + render: one call per simulator step for all envs. */
+int nv_step_render(nv_ctx *ctx, const int8_t *actions, int cam, uint8_t *rgb,
+                   float *depth, uint16_t *sem, double *gps, double *compass,
+                   uint8_t *collided, double *displacement, int32_t *status,
+                   void *stream);
+
+/* End-to-end call over HOST buffers (the reference-facing path: host actions
+ * in, host results out).  Copies actions (host, n i8) in, runs
+ * nv_step_render into device frames owned by the context (channels: bitmask
+ * of NV_CH_*; a non-NULL host frame pointer implies its channel), copies the
+ * per-env step results (collided u8, displacement f64, gps f64x2, compass
+ * f64) back to host buffers (any may be NULL) and, where the host frame
+ * pointers are non-NULL, the frames too.  Host buffers should be pinned.
+ * Synchronises `stream` before returning. */
+#define NV_CH_RGB 1u
+#define NV_CH_DEPTH 2u
+#define NV_CH_SEM 4u
+int nv_step_render_host(nv_ctx *ctx, const int8_t *actions_host, int cam,
+                        uint32_t channels, uint8_t *rgb_host, float *depth_host,
+                        uint16_t *sem_host, double *gps_host,
+                        double *compass_host, uint8_t *collided_host,
+                        double *displacement_host, void *stream);
+/* Device frame buffers written by nv_step_render_host (valid until the next
+ * call; for a GPU consumer of the host-driven path). */
+int nv_host_frames(nv_ctx *ctx, uint8_t **rgb, float **depth, uint16_t **sem);
+
+/* gps_compass (sensors.py:175-180) alone, for suites without visual sensors.
+ * DEVICE outputs gps f64[n,2], compass f64[n] (either may be NULL). */
+int nv_gps_compass(nv_ctx *ctx, double *gps, double *compass, void *stream);
+
+/* Agent state in/out (DEVICE arrays of n_envs; any may be NULL):
+ * position xy f64[n,2], heading f64[n], path length f64[n],
+ * collision count i64[n] -- AgentState (sim.py:65-73). */
+int nv_get_state(nv_ctx *ctx, double *xy, double *heading, double *path_len,
+                 int64_t *collisions, void *stream);
+/* Episode frame origin/heading (EpisodeFrame, sensors.py:155-172). */
+int nv_get_frame(nv_ctx *ctx, double *origin_xy, double *heading, void *stream);
+
+/* ---- operator-level entry points (numba kernels, _kernels.py) ---------- */
+
+/* raycast_grid (_kernels.py:51-120; SegmentIndex.raycast geometry.py:165) or,
+ * with brute != 0, raycast_all (_kernels.py:16-48).  m rays, ray k starts at
+ * (ox[k], oy[k]) with direction (dirx[k], diry[k]).  DEVICE arrays.
+ * Outputs t f64[m] (inf on miss), idx i64[m] (-1 on miss). */
+int nv_raycast(nv_ctx *ctx, const double *ox, const double *oy,
+               const double *dirx, const double *diry, int64_t m, double t_max,
+               int brute, double *t_out, int64_t *idx_out, void *stream);
+
+/* fill_frame (_kernels.py:128-207) for n frames of camera `cam` from given
+ * per-column hits: t_col f64[n,W], i_col i64[n,W], dirx/diry f64[n,W].
+ * sensor_height = cam_h.  DEVICE arrays; outputs as in nv_render. */
+int nv_fill_frames(nv_ctx *ctx, int cam, int64_t n, const double *t_col,
+                   const int64_t *i_col, const double *dirx, const double *diry,
+                   double sensor_height, uint8_t *rgb, float *depth,
+                   uint16_t *sem, void *stream);
+
+/* SegmentIndex.cast_disc (geometry.py:183-192) -> disc_cast
+ * (_kernels.py:393-465) for m queries.  DEVICE arrays: px, py, ux, uy,
+ * radius (f64[m] each).  Outputs t f64[m], seg i64[m], tan f64[m,2]. */
+int nv_cast_disc(nv_ctx *ctx, const double *px, const double *py,
+                 const double *ux, const double *uy, const double *radius,
+                 int64_t m, double *t_out, int64_t *seg_out, double *tan_out,
+                 void *stream);
+
+/* SegmentIndex.clearance (geometry.py:194-206) -> min_seg_distance
+ * (_kernels.py:468-493) for m points.  DEVICE arrays. */
+int nv_clearance(nv_ctx *ctx, const double *px, const double *py, int64_t m,
+                 double search_radius, double *out, void *stream);
+
+/* Correctly rounded sin/cos/hypot used on the device agent path, exposed
+ * (host implementation) for tests. */
+void nv_host_sincos(double x, double *s, double *c);
+double nv_host_hypot(double x, double y);
+
+/* Number of kernel launches issued by this context so far (bench evidence). */
+int64_t nv_launch_count(nv_ctx *ctx);
+
+/* Per-kernel CUDA-event timing of the hot-path launches (bench roofline
+ * evidence).  nv_profile(ctx, 1) clears and enables; nv_profile_read waits
+ * for the recorded events and returns accumulated milliseconds and launch
+ * counts for [agent_step, column_cast, frame_fill, other]. */
+int nv_profile(nv_ctx *ctx, int enable);
+int nv_profile_read(nv_ctx *ctx, double *ms4, int64_t *counts4);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NAVSIM_B200_H */

@@ -1,0 +1,147 @@
+"""ctypes binding of the C ABI (include/navsim_b200.h).
+
+The shared library is built in-tree (``__graft_entry__.build()`` /
+``python -m paper_1904_01201_b200.build``) into ``paper_1904_01201_b200/_lib``.
+There is no fallback: if the library is missing or no CUDA device is present
+every entry point raises ``NativeUnavailable``.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "_lib", "libnavsim_b200.so")
+
+NV_OK = 0
+NV_ERR_ARG = -1
+NV_ERR_CUDA = -2
+NV_ERR_STATE = -3
+NV_ERR_OOM = -4
+NV_ENV_OK, NV_ENV_TOO_CLOSE, NV_ENV_NOT_RESET, NV_ENV_BAD_ACTION = 0, 1, 2, 3
+NV_CH_RGB, NV_CH_DEPTH, NV_CH_SEM = 1, 2, 4
+
+# every symbol include/navsim_b200.h declares: (name, restype, argtypes)
+_P = ctypes.c_void_p
+_D = ctypes.c_double
+_I = ctypes.c_int
+_I64 = ctypes.c_int64
+_U32 = ctypes.c_uint32
+SIGNATURES = {
+    "nv_last_error": (ctypes.c_char_p, []),
+    "nv_version": (_I, []),
+    "nv_create": (_I, [_I, ctypes.POINTER(_P)]),
+    "nv_destroy": (_I, [_P]),
+    "nv_scene_upload": (_I, [_P, _P, _P, _P, _I64, _D, _P, _P]),
+    "nv_scene_grid_info": (_I, [_P, _P, _P, _P, _P, _P]),
+    "nv_agent_config": (_I, [_P, _D, _D, _D, _D]),
+    "nv_envs_alloc": (_I, [_P, _I64]),
+    "nv_camera_config": (_I, [_P, _I, _I, _I, _D, _D]),
+    "nv_set_poses": (_I, [_P, _P, _P, _P, _P, _P]),
+    "nv_step": (_I, [_P, _P, _P, _P, _P, _P]),
+    "nv_render": (_I, [_P, _I, _P, _P, _P, _P, _P, _P]),
+    "nv_step_render": (_I, [_P, _P, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
+    "nv_step_render_host": (_I, [_P, _P, _I, _U32, _P, _P, _P, _P, _P, _P, _P, _P]),
+    "nv_host_frames": (_I, [_P, _P, _P, _P]),
+    "nv_gps_compass": (_I, [_P, _P, _P, _P]),
+    "nv_get_state": (_I, [_P, _P, _P, _P, _P, _P]),
+    "nv_get_frame": (_I, [_P, _P, _P, _P]),
+    "nv_raycast": (_I, [_P, _P, _P, _P, _P, _I64, _D, _I, _P, _P, _P]),
+    "nv_fill_frames": (_I, [_P, _I, _I64, _P, _P, _P, _P, _D, _P, _P, _P, _P]),
+    "nv_cast_disc": (_I, [_P, _P, _P, _P, _P, _P, _I64, _P, _P, _P, _P]),
+    "nv_clearance": (_I, [_P, _P, _P, _I64, _D, _P, _P]),
+    "nv_host_sincos": (None, [_D, _P, _P]),
+    "nv_host_hypot": (_D, [_D, _D]),
+    "nv_launch_count": (_I64, [_P]),
+    "nv_profile": (_I, [_P, _I]),
+    "nv_profile_read": (_I, [_P, _P, _P]),
+}
+
+
+class NativeUnavailable(RuntimeError):
+    """The CUDA extension is not built or cannot run here (no fallback)."""
+
+
+class NativeError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(msg)
+        self.code = code
+
+
+_lib = None
+
+
+def load():
+    """Load the in-tree shared library (no GPU needed to load it)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise NativeUnavailable(
+            f"CUDA extension missing at {LIB_PATH}; build it with "
+            "`python -c 'import __graft_entry__ as g; g.build()'`")
+    lib = ctypes.CDLL(LIB_PATH)
+    for name, (res, args) in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib
+
+
+def last_error() -> str:
+    return load().nv_last_error().decode(errors="replace")
+
+
+def check(rc: int) -> None:
+    if rc != NV_OK:
+        raise NativeError(rc, last_error())
+
+
+def ptr(t):
+    """Raw pointer of a torch tensor / numpy array / None."""
+    if t is None:
+        return None
+    if hasattr(t, "data_ptr"):
+        return ctypes.c_void_p(t.data_ptr())
+    return t.ctypes.data_as(ctypes.c_void_p)
+
+
+def stream_handle(device=None):
+    import torch
+    return ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream)
+
+
+class Context:
+    """Owns one nv_ctx (one GPU)."""
+
+    def __init__(self, device: int = 0):
+        import torch
+        if not torch.cuda.is_available():
+            raise NativeUnavailable("no CUDA device: the navsim B200 path has no CPU fallback")
+        lib = load()
+        torch.cuda.init()
+        self.device = device
+        h = ctypes.c_void_p()
+        with torch.cuda.device(device):
+            check(lib.nv_create(device, ctypes.byref(h)))
+        self._h = h
+        self.lib = lib
+
+    @property
+    def handle(self):
+        return self._h
+
+    def close(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            self.lib.nv_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def launches(self) -> int:
+        return int(self.lib.nv_launch_count(self._h))

@@ -1,0 +1,84 @@
+// device.cuh -- data layout shared by the kernels and the host side.
+//
+// HBM layout (one scene replica + one env shard per GPU):
+//   * segment SoA, f64: ax, ay, bx, by, ex, ey, nx, ny (n each) -- the
+//     reference's SegmentIndex / RenderGeometry arrays (geometry.py:111-117,
+//     sensors.py:84-93), read by the disc casts and the column epilogue;
+//   * uniform-grid CSR (geometry.py:128-141) with the bucket items EXPANDED
+//     into 48-byte CellEntry records {ax, ay, ex, ey, idx}: the DDA reads one
+//     contiguous run per cell instead of gathering through bucket_items;
+//   * per-env agent state SoA (x, y, heading, path, collisions, cos/sin of
+//     heading, episode frame);
+//   * per camera: u_j (W f64), tc/tf row tables (H f64) for the exact FP64
+//     row/column classification, and RowRec (H x 32 B) for shading;
+//   * per camera, per step: ColRec (N x W x 32 B), the column hits + the
+//     column's shading parameters, written by the cast kernel and read by the
+//     fill kernel (8 MB at 1024 envs x 256 columns: L2-resident);
+//   * frames: caller-owned u8 [N,H,W,3], f32 [N,H,W], u16 [N,H,W].
+#pragma once
+
+#include <stdint.h>
+
+namespace nvd {
+
+struct __align__(16) CellEntry {
+  double ax, ay;  // segment start
+  double ex, ey;  // b - a (SegmentIndex.ex/ey, geometry.py:116-117)
+  int32_t idx;    // segment index (the tie-break key)
+  int32_t pad[3];
+};
+
+struct SceneView {
+  const double *ax, *ay, *bx, *by, *ex, *ey, *nx, *ny;
+  const uint16_t *sem;
+  const float4 *alb255;  // albedo * 255 (rgb, pad)
+  const int32_t *starts; // nc + 1
+  const CellEntry *ent;  // starts[nc] entries
+  const int32_t *items;  // same order, index only (disc casts)
+  double x0, y0;
+  int gnx, gny;
+  int64_t n;
+};
+
+struct EnvView {
+  double *x, *y, *h, *path;
+  int64_t *coll;
+  double *ch, *sh;             // cos/sin of heading (correctly rounded)
+  double *ox, *oy, *oh;        // episode frame (sensors.py:155-172)
+  double *fc, *fs;             // cos(-oh), sin(-oh)
+  uint8_t *reset;
+  int n;
+};
+
+// Per-row shading record (fill kernel), 32 B.
+struct __align__(16) RowRec {
+  float depth_p;  // plane depth (tc / tf, or max_range when void)
+  float num08_p;  // 0.8 * |v| (0 when void)
+  float v2;       // v*v
+  uint32_t sem_mode;  // plane semantic | mode << 16 (0: top/mid, 1: bottom)
+  float col_p[3];     // plane colour * 255 (0 when void)
+  float pad;
+};
+
+// Per-column record (cast -> fill), 32 B.
+struct __align__(16) ColRec {
+  float depth_w;   // wall depth (f32(s)) or max_range when void
+  float num08_w;   // 0.8 * |d . n_k| (0 when void)
+  float d2;        // dx*dx + dy*dy
+  uint32_t lohi;   // lo (ceiling rows [0, lo)) | hi << 16 (floor rows [hi, H))
+  float col_w[3];  // albedo_k * 255 (0 when void)
+  uint32_t sem_w;  // seg_sem[k] (0 when void)
+};
+
+struct CamView {
+  int W, H;
+  int n_top;  // rows with v > 0
+  int b0;     // first row with v < 0
+  double max_range;
+  const double *u;   // W: ((j + 0.5) - W*0.5) / focal
+  const double *tc;  // H: (wall_h - cam_h) / v for v > 0 rows
+  const double *tf;  // H: -cam_h / v for v < 0 rows
+  const RowRec *rows;
+};
+
+}  // namespace nvd

@@ -1,0 +1,894 @@
+// kernels.cuh -- sm_100a kernels of the navsim hot path.
+//
+//   k_agent_step   Simulator.step kinematics (sim.py:83-130), one warp / env:
+//                  swept-disc casts (disc_cast, _kernels.py:393-465) over the
+//                  grid candidates with a warp-lexicographic (t, idx) min.
+//   k_column_cast  raycast_grid (_kernels.py:51-120), one thread / (env,
+//                  column), exact FP64 DDA + segment test, then the column
+//                  epilogue: exact FP64 row classification against the tc/tf
+//                  tables (fill_frame's per-pixel compares, _kernels.py:141-170,
+//                  restated as two binary searches per column) -> ColRec.
+//   k_fill_tma     fill_frame's per-pixel resolve (_kernels.py:171-207) as a
+//                  streaming writer: each warp renders whole rows into a
+//                  private double-buffered shared-memory stage and its lane 0
+//                  writes them out with cp.async.bulk (TMA bulk) stores,
+//                  evict-first in L2; work is pulled from a global counter.
+//   k_fill_generic the same resolve, one thread per pixel, any W/H.
+//
+// Exactness: every FP64 operation that decides coverage, semantics, depth or
+// pose uses the nvx:: _rn helpers (no FMA contraction), replicating the
+// reference's operation order.  Shading is FP32 (RGB tolerance 1/255).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <math_constants.h>
+#include <stdint.h>
+
+#include "device.cuh"
+#include "exact_math.cuh"
+
+namespace nvk {
+
+using namespace nvd;
+using nvx::add;
+using nvx::div;
+using nvx::mul;
+using nvx::sub;
+
+#define NV_INF CUDART_INF
+
+// ---------------------------------------------------------------- helpers
+
+// SegmentIndex._cell_of (geometry.py:146-149): trunc toward zero, clamp.
+__device__ __forceinline__ int cell_coord(double v, double o, int n) {
+  double d = div(sub(v, o), 1.0);
+  if (!(d >= 1.0)) return 0;
+  if (d >= (double)(n - 1)) return n - 1;
+  return (int)d;
+}
+
+// One segment test of raycast_grid / raycast_all (_kernels.py:91-103).
+__device__ __forceinline__ void seg_test(double px, double py, double dx, double dy,
+                                         double ax, double ay, double ex, double ey,
+                                         int i, double &best_t, int &best_i) {
+  double den = sub(mul(dx, ey), mul(dy, ex));
+  if (den == 0.0) return;
+  double sx = sub(ax, px), sy = sub(ay, py);
+  double tn = sub(mul(sx, ey), mul(sy, ex));
+  // Division-free rejections, each implying the reference's `continue`:
+  // t < 0 (sign of tn/den; tn == +-0 gives t == +-0, which passes) and
+  // t > best_t (|tn| > |den| * best_t * (1 + 2^-40) => RN(tn/den) > best_t).
+  if (tn != 0.0 && ((tn < 0.0) != (den < 0.0))) return;
+  double rn = sub(mul(sx, dy), mul(sy, dx));
+  if (rn != 0.0 && ((rn < 0.0) != (den < 0.0))) return;   // r < 0
+  double aden = fabs(den);
+  if (fabs(rn) > aden * 1.0000000000010) return;           // r > 1 for sure
+  if (fabs(tn) > aden * best_t * 1.0000000000010) return;  // t > best_t
+  double t = div(tn, den);
+  if (t < 0.0 || t > best_t) return;
+  double r = div(rn, den);
+  if (0.0 <= r && r <= 1.0) {
+    if (t < best_t || i < best_i) {
+      best_t = t;
+      best_i = i;
+    }
+  }
+}
+
+// raycast_grid (_kernels.py:51-120), one ray, exact replica of the DDA.
+__device__ __forceinline__ void ray_grid(const SceneView &sc, double px, double py,
+                                         double dx, double dy, double t_max,
+                                         double &out_t, int &out_i) {
+  const double cell = 1.0;
+  double best_t = NV_INF;
+  int best_i = -1;
+  if (isnan(px) || isnan(py) || isnan(dx) || isnan(dy)) {  // reference would spin
+    out_t = best_t;
+    out_i = best_i;
+    return;
+  }
+  long long cx = (long long)floor(div(sub(px, sc.x0), cell));
+  long long cy = (long long)floor(div(sub(py, sc.y0), cell));
+  const int stepx = dx > 0.0 ? 1 : -1;
+  const int stepy = dy > 0.0 ? 1 : -1;
+  double tnx, tdx, tny, tdy;
+  if (dx != 0.0) {
+    double nbx = add(sc.x0, mul((double)(cx + (dx > 0.0 ? 1 : 0)), cell));
+    tnx = div(sub(nbx, px), dx);
+    tdx = fabs(div(cell, dx));
+  } else {
+    tnx = NV_INF;
+    tdx = NV_INF;
+  }
+  if (dy != 0.0) {
+    double nby = add(sc.y0, mul((double)(cy + (dy > 0.0 ? 1 : 0)), cell));
+    tny = div(sub(nby, py), dy);
+    tdy = fabs(div(cell, dy));
+  } else {
+    tny = NV_INF;
+    tdy = NV_INF;
+  }
+  const long long gnx = sc.gnx, gny = sc.gny;
+  for (int guard = 0; guard < (1 << 24); ++guard) {
+    if (0 <= cx && cx < gnx && 0 <= cy && cy < gny) {
+      int c = (int)(cy * gnx + cx);
+      int q0 = __ldg(sc.starts + c), q1 = __ldg(sc.starts + c + 1);
+      for (int q = q0; q < q1; ++q) {
+        const double2 *e2 = reinterpret_cast<const double2 *>(sc.ent + q);
+        double2 g0 = __ldg(e2), g1 = __ldg(e2 + 1);
+        int idx = __ldg(&sc.ent[q].idx);
+        seg_test(px, py, dx, dy, g0.x, g0.y, g1.x, g1.y, idx, best_t, best_i);
+      }
+    }
+    double t_exit = tnx < tny ? tnx : tny;
+    if (best_t <= t_exit || t_exit > t_max) break;
+    if (tnx < tny) {
+      cx += stepx;
+      tnx = add(tnx, tdx);
+    } else {
+      cy += stepy;
+      tny = add(tny, tdy);
+    }
+    if (cx < 0 || cx >= gnx || cy < 0 || cy >= gny) {
+      bool out_x = (cx < 0 && dx <= 0.0) || (cx >= gnx && dx >= 0.0);
+      bool out_y = (cy < 0 && dy <= 0.0) || (cy >= gny && dy >= 0.0);
+      if (out_x || out_y) break;
+    }
+  }
+  out_t = best_t;
+  out_i = best_i;
+}
+
+// raycast_all (_kernels.py:16-48)
+__device__ __forceinline__ void ray_brute(const SceneView &sc, double px, double py,
+                                          double dx, double dy, double &out_t,
+                                          int &out_i) {
+  double best_t = NV_INF;
+  int best_i = -1;
+  for (int64_t i = 0; i < sc.n; ++i)
+    seg_test(px, py, dx, dy, __ldg(sc.ax + i), __ldg(sc.ay + i), __ldg(sc.ex + i),
+             __ldg(sc.ey + i), (int)i, best_t, best_i);
+  out_t = best_t;
+  out_i = best_i;
+}
+
+// Per-segment first-contact time of disc_cast (_kernels.py:405-459): the
+// minimum over the face / band / endpoint candidates of one segment, taken in
+// the reference's order with its strict `<`.  The reference's result is then
+// the lexicographic (t, idx) minimum over segments (its scan is ascending in
+// idx with strict `<`), which lets the warp scan candidates in any order.
+__device__ __forceinline__ double disc_seg_t(double px, double py, double ux, double uy,
+                                             double radius, double u2, double axi,
+                                             double ayi, double bxi, double byi) {
+  double best = NV_INF;
+  double exi = sub(bxi, axi), eyi = sub(byi, ayi);
+  double seg_len = nvx::sqrt_rn(add(mul(exi, exi), mul(eyi, eyi)));
+  if (seg_len <= 0.0) return best;
+  double tx = div(exi, seg_len), ty = div(eyi, seg_len);
+  double nx = -ty, ny = tx;
+  double relx = sub(px, axi), rely = sub(py, ayi);
+  double d0 = add(mul(relx, nx), mul(rely, ny));
+  double vn = add(mul(ux, nx), mul(uy, ny));
+  if (fabs(d0) >= radius) {
+    double side = d0 > 0.0 ? 1.0 : -1.0;
+    if (mul(vn, side) < 0.0) {
+      double t = div(sub(mul(side, radius), d0), vn);
+      if (0.0 <= t && t <= 1.0) {
+        double proj = add(mul(add(relx, mul(t, ux)), tx), mul(add(rely, mul(t, uy)), ty));
+        if (0.0 <= proj && proj <= seg_len) {
+          if (t < best) best = t;
+        }
+      }
+    }
+  } else {
+    double proj = add(mul(relx, tx), mul(rely, ty));
+    if (0.0 <= proj && proj <= seg_len && mul(vn, d0) < 0.0) {
+      if (0.0 < best) best = 0.0;
+    }
+  }
+#pragma unroll
+  for (int e = 0; e < 2; ++e) {
+    double cxp = e == 0 ? axi : bxi;
+    double cyp = e == 0 ? ayi : byi;
+    double wx = sub(px, cxp), wy = sub(py, cyp);
+    double b = add(mul(wx, ux), mul(wy, uy));
+    double c = sub(add(mul(wx, wx), mul(wy, wy)), mul(radius, radius));
+    if (c < 0.0) {
+      if (b < 0.0 && 0.0 < best) best = 0.0;
+      continue;
+    }
+    if (u2 == 0.0) continue;
+    double disc = sub(mul(b, b), mul(u2, c));
+    if (disc < 0.0) continue;
+    double t = div(sub(-b, nvx::sqrt_rn(disc)), u2);
+    if (0.0 <= t && t <= 1.0 && t < best) best = t;
+  }
+  return best;
+}
+
+__device__ __forceinline__ void lex_min(double &t, int &i, double t2, int i2) {
+  if (t2 < t || (t2 == t && i2 < i)) {
+    t = t2;
+    i = i2;
+  }
+}
+
+__device__ __forceinline__ void warp_lex_min(double &t, int &i) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    double t2 = __shfl_xor_sync(0xffffffffu, t, o);
+    int i2 = __shfl_xor_sync(0xffffffffu, i, o);
+    lex_min(t, i, t2, i2);
+  }
+}
+
+// SegmentIndex.cast_disc (geometry.py:183-192): candidates from the padded
+// swept AABB (query_aabb), first contact, tangent of the contacted segment.
+__device__ void warp_cast_disc(const SceneView &sc, double px, double py, double ux,
+                               double uy, double radius, double &t_out, int &i_out,
+                               double &tan_x, double &tan_y) {
+  const int lane = threadIdx.x & 31;
+  double pad = add(radius, 1e-6);
+  double xa = add(px, ux), ya = add(py, uy);
+  double lox = xa < px ? xa : px, loy = ya < py ? ya : py;  // Python min(a, b)
+  double hix = xa > px ? xa : px, hiy = ya > py ? ya : py;  // Python max(a, b)
+  int cx0 = cell_coord(sub(lox, pad), sc.x0, sc.gnx);
+  int cy0 = cell_coord(sub(loy, pad), sc.y0, sc.gny);
+  int cx1 = cell_coord(add(hix, pad), sc.x0, sc.gnx);
+  int cy1 = cell_coord(add(hiy, pad), sc.y0, sc.gny);
+  double u2 = add(mul(ux, ux), mul(uy, uy));
+  double bt = NV_INF;
+  int bi = 0x7fffffff;
+  for (int cy = cy0; cy <= cy1; ++cy)
+    for (int cx = cx0; cx <= cx1; ++cx) {
+      int c = cy * sc.gnx + cx;
+      int q0 = __ldg(sc.starts + c), q1 = __ldg(sc.starts + c + 1);
+      for (int q = q0 + lane; q < q1; q += 32) {
+        int i = __ldg(sc.items + q);
+        double t = disc_seg_t(px, py, ux, uy, radius, u2, __ldg(sc.ax + i),
+                              __ldg(sc.ay + i), __ldg(sc.bx + i), __ldg(sc.by + i));
+        lex_min(bt, bi, t, i);
+      }
+    }
+  warp_lex_min(bt, bi);
+  if (!(bt < NV_INF) || bi == 0x7fffffff) {  // t is inf whenever nothing hit
+    t_out = NV_INF;
+    i_out = -1;
+    tan_x = 0.0;
+    tan_y = 0.0;
+    return;
+  }
+  double exi = sub(__ldg(sc.bx + bi), __ldg(sc.ax + bi));
+  double eyi = sub(__ldg(sc.by + bi), __ldg(sc.ay + bi));
+  double seg_len = nvx::sqrt_rn(add(mul(exi, exi), mul(eyi, eyi)));
+  t_out = bt;
+  i_out = bi;
+  tan_x = div(exi, seg_len);
+  tan_y = div(eyi, seg_len);
+}
+
+// min_seg_distance (_kernels.py:468-493), one segment.
+__device__ __forceinline__ double seg_dist(double px, double py, double axi, double ayi,
+                                           double bxi, double byi) {
+  double exi = sub(bxi, axi), eyi = sub(byi, ayi);
+  double l2 = add(mul(exi, exi), mul(eyi, eyi));
+  double wx = sub(px, axi), wy = sub(py, ayi);
+  double cx, cy;
+  if (l2 > 0.0) {
+    double t = div(add(mul(wx, exi), mul(wy, eyi)), l2);
+    if (t < 0.0)
+      t = 0.0;
+    else if (t > 1.0)
+      t = 1.0;
+    cx = sub(wx, mul(t, exi));
+    cy = sub(wy, mul(t, eyi));
+  } else {
+    cx = wx;
+    cy = wy;
+  }
+  return nvx::sqrt_rn(add(mul(cx, cx), mul(cy, cy)));
+}
+
+__device__ __forceinline__ double warp_min(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmin(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// SegmentIndex.clearance (geometry.py:194-206): local query, then global.
+__device__ double warp_clearance(const SceneView &sc, double px, double py, double sr) {
+  const int lane = threadIdx.x & 31;
+  int cx0 = cell_coord(sub(px, sr), sc.x0, sc.gnx);
+  int cy0 = cell_coord(sub(py, sr), sc.y0, sc.gny);
+  int cx1 = cell_coord(add(px, sr), sc.x0, sc.gnx);
+  int cy1 = cell_coord(add(py, sr), sc.y0, sc.gny);
+  double best = NV_INF;
+  int any = 0;
+  for (int cy = cy0; cy <= cy1; ++cy)
+    for (int cx = cx0; cx <= cx1; ++cx) {
+      int c = cy * sc.gnx + cx;
+      int q0 = __ldg(sc.starts + c), q1 = __ldg(sc.starts + c + 1);
+      any |= (q1 > q0);
+      for (int q = q0 + lane; q < q1; q += 32) {
+        int i = __ldg(sc.items + q);
+        double d = seg_dist(px, py, __ldg(sc.ax + i), __ldg(sc.ay + i), __ldg(sc.bx + i),
+                            __ldg(sc.by + i));
+        if (d < best) best = d;
+      }
+    }
+  best = warp_min(best);
+  if (any && best <= sr) return best;
+  if (sc.n == 0) return NV_INF;
+  best = NV_INF;
+  for (int64_t i = lane; i < sc.n; i += 32) {
+    double d = seg_dist(px, py, __ldg(sc.ax + i), __ldg(sc.ay + i), __ldg(sc.bx + i),
+                        __ldg(sc.by + i));
+    if (d < best) best = d;
+  }
+  return warp_min(best);
+}
+
+// ------------------------------------------------------------ agent step
+
+struct AgentCfg {
+  double radius, step, turn_rad;
+};
+
+#define NV_CONTACT_EPSILON 1e-4  // sim.py:24
+
+// apply_forward (sim.py:90-130) for one env, executed by a whole warp.
+__device__ void warp_forward(const SceneView &sc, const AgentCfg &cfg, double &x,
+                             double &y, double ch, double sh, double &moved,
+                             int &collided) {
+  double ux = mul(cfg.step, ch), uy = mul(cfg.step, sh);
+  double t1, tx, ty;
+  int i1;
+  warp_cast_disc(sc, x, y, ux, uy, cfg.radius, t1, i1, tx, ty);
+  if (!(t1 < 1.0)) {
+    x = add(x, ux);
+    y = add(y, uy);
+    moved = cfg.step;
+    collided = 0;
+    return;
+  }
+  double d1 = sub(mul(t1, cfg.step), NV_CONTACT_EPSILON);
+  if (!(d1 > 0.0)) d1 = 0.0;  // Python max(0.0, d1)
+  double unx = div(ux, cfg.step), uny = div(uy, cfg.step);
+  double p1x = add(x, mul(unx, d1)), p1y = add(y, mul(uny, d1));
+  double omt = sub(1.0, t1);
+  double remx = mul(ux, omt), remy = mul(uy, omt);
+  double dot = nvx::fma_rn(remy, ty, mul(remx, tx));  // np.dot -> OpenBLAS ddot
+  double slx = mul(dot, tx), sly = mul(dot, ty);
+  double slide_len = nvx::hypot_cr(slx, sly);
+  double d2 = 0.0;
+  if (slide_len > NV_CONTACT_EPSILON) {
+    double t2, t2x, t2y;
+    int i2;
+    warp_cast_disc(sc, p1x, p1y, slx, sly, cfg.radius, t2, i2, t2x, t2y);
+    if (!(t2 < 1.0)) {
+      d2 = slide_len;
+    } else {
+      d2 = sub(mul(t2, slide_len), NV_CONTACT_EPSILON);
+      if (!(d2 > 0.0)) d2 = 0.0;
+    }
+    p1x = add(p1x, mul(div(slx, slide_len), d2));
+    p1y = add(p1y, mul(div(sly, slide_len), d2));
+  }
+  x = p1x;
+  y = p1y;
+  moved = add(d1, d2);
+  collided = 1;
+}
+
+// Simulator.step (sim.py:202-219) for all envs: one warp per env.
+__global__ void __launch_bounds__(128) k_agent_step(EnvView ev, SceneView sc, AgentCfg cfg,
+                                                    const int8_t *__restrict__ actions,
+                                                    uint8_t *collided_out,
+                                                    double *disp_out, int32_t *status_out) {
+  const int e = (int)((blockIdx.x * (size_t)blockDim.x + threadIdx.x) >> 5);
+  const int lane = threadIdx.x & 31;
+  if (e >= ev.n) return;
+  const int a = actions[e];
+  int status = 0, collided = 0;
+  double moved = 0.0;
+  if (!ev.reset[e]) {
+    status = 2;  // NV_ENV_NOT_RESET
+  } else if (a == 0) {
+    double x = ev.x[e], y = ev.y[e];
+    warp_forward(sc, cfg, x, y, ev.ch[e], ev.sh[e], moved, collided);
+    if (lane == 0) {
+      ev.x[e] = x;
+      ev.y[e] = y;
+      ev.path[e] = add(ev.path[e], moved);
+      ev.coll[e] += collided;
+    }
+  } else if (a == 1 || a == 2) {
+    // apply_turn (sim.py:83-87): wrap(h + sign * radians(turn)); +-x is exact
+    double h = nvx::wrap_angle(add(ev.h[e], a == 1 ? cfg.turn_rad : -cfg.turn_rad));
+    if (lane == 0) {
+      double s, c;
+      nvx::sincos_cr(h, &s, &c);
+      ev.h[e] = h;
+      ev.sh[e] = s;
+      ev.ch[e] = c;
+    }
+  } else if (a != 3) {
+    status = 3;  // NV_ENV_BAD_ACTION
+  }
+  if (lane == 0) {
+    if (collided_out) collided_out[e] = (uint8_t)collided;
+    if (disp_out) disp_out[e] = moved;
+    if (status_out) status_out[e] = status;
+  }
+}
+
+// Simulator.set_agent_state (sim.py:172-184), one warp per env.  Inputs are
+// device copies of the host arrays.
+__global__ void __launch_bounds__(128) k_set_poses(EnvView ev, SceneView sc, double radius,
+                                                   const double *__restrict__ xy,
+                                                   const double *__restrict__ hd,
+                                                   const uint8_t *__restrict__ mask,
+                                                   int32_t *status, double *clear_out) {
+  const int e = (int)((blockIdx.x * (size_t)blockDim.x + threadIdx.x) >> 5);
+  const int lane = threadIdx.x & 31;
+  if (e >= ev.n) return;
+  if (mask && !mask[e]) {
+    if (lane == 0) status[e] = 0;
+    return;
+  }
+  double px = xy[2 * e], py = xy[2 * e + 1];
+  double clr = warp_clearance(sc, px, py, 2.0);
+  if (lane != 0) return;
+  clear_out[e] = clr;
+  if (clr < radius) {
+    status[e] = 1;  // NV_ENV_TOO_CLOSE, state untouched
+    return;
+  }
+  double h = nvx::wrap_angle(hd[e]);
+  double s, c;
+  nvx::sincos_cr(h, &s, &c);
+  ev.x[e] = px;
+  ev.y[e] = py;
+  ev.h[e] = h;
+  ev.ch[e] = c;
+  ev.sh[e] = s;
+  ev.path[e] = 0.0;
+  ev.coll[e] = 0;
+  ev.ox[e] = px;
+  ev.oy[e] = py;
+  ev.oh[e] = h;
+  // EpisodeFrame.to_frame uses cos(-h0), sin(-h0) (sensors.py:166)
+  double fs, fc;
+  nvx::sincos_cr(-h, &fs, &fc);
+  ev.fc[e] = fc;
+  ev.fs[e] = fs;
+  ev.reset[e] = 1;
+  status[e] = 0;
+}
+
+// --------------------------------------------------------- column casts
+
+// Column epilogue: exact classification of the column into ceiling rows
+// [0, lo), middle rows [lo, hi) (wall, or void when s >= max_range) and floor
+// rows [hi, H), equal to fill_frame's per-pixel FP64 compares
+// (_kernels.py:149-170) because tc is non-decreasing over the v > 0 rows and
+// tf non-increasing over the v < 0 rows (IEEE division is monotone).
+__device__ __forceinline__ void column_epilogue(const SceneView &sc, const CamView &cam,
+                                                double s, int k, double dx, double dy,
+                                                ColRec &out) {
+  int a = 0, b = cam.n_top;  // lo = #{i < n_top : tc[i] <= s}
+  while (a < b) {
+    int m = (a + b) >> 1;
+    if (__ldg(cam.tc + m) <= s) a = m + 1; else b = m;
+  }
+  const int lo = a;
+  a = cam.b0;
+  b = cam.H;  // hi = first i >= b0 with tf[i] <= s
+  while (a < b) {
+    int m = (a + b) >> 1;
+    if (__ldg(cam.tf + m) <= s) b = m; else a = m + 1;
+  }
+  const int hi = a;
+  const bool lit = s < cam.max_range && k >= 0;
+  out.lohi = (uint32_t)lo | ((uint32_t)hi << 16);
+  float fdx = (float)dx, fdy = (float)dy;
+  out.d2 = fdx * fdx + fdy * fdy;
+  if (lit) {
+    out.depth_w = (float)s;
+    double dt = fabs(add(mul(dx, __ldg(sc.nx + k)), mul(dy, __ldg(sc.ny + k))));
+    out.num08_w = 0.8f * (float)dt;
+    float4 c = __ldg(sc.alb255 + k);
+    out.col_w[0] = c.x;
+    out.col_w[1] = c.y;
+    out.col_w[2] = c.z;
+    out.sem_w = __ldg(sc.sem + k);
+  } else {
+    out.depth_w = (float)cam.max_range;
+    out.num08_w = 0.0f;
+    out.col_w[0] = out.col_w[1] = out.col_w[2] = 0.0f;
+    out.sem_w = 0;
+  }
+}
+
+// _column_directions (sensors.py:96-102) + raycast_grid + epilogue, one
+// thread per (env, column); also gps_compass (sensors.py:175-180) once per env.
+__global__ void __launch_bounds__(256) k_column_cast(EnvView ev, SceneView sc, CamView cam,
+                                                     ColRec *__restrict__ rec, double t_max,
+                                                     double *gps, double *compass) {
+  const long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const long long total = (long long)ev.n * cam.W;
+  if (g >= total) return;
+  const int e = (int)(g / cam.W);
+  const int j = (int)(g - (long long)e * cam.W);
+  const double px = ev.x[e], py = ev.y[e], c = ev.ch[e], s = ev.sh[e];
+  const double u = __ldg(cam.u + j);
+  const double dx = add(c, mul(u, s));
+  const double dy = add(s, mul(u, -c));
+  double t;
+  int k;
+  ray_grid(sc, px, py, dx, dy, t_max, t, k);
+  ColRec r;
+  column_epilogue(sc, cam, t, k, dx, dy, r);
+  rec[g] = r;
+  if (j == 0 && (gps || compass)) {
+    double ddx = sub(px, ev.ox[e]), ddy = sub(py, ev.oy[e]);
+    double fc = ev.fc[e], fs = ev.fs[e];
+    if (gps) {
+      gps[2 * e] = sub(mul(fc, ddx), mul(fs, ddy));
+      gps[2 * e + 1] = add(mul(fs, ddx), mul(fc, ddy));
+    }
+    if (compass) compass[e] = nvx::wrap_angle(sub(ev.h[e], ev.oh[e]));
+  }
+}
+
+// gps_compass (sensors.py:175-180) for all envs (no visual sensors case).
+__global__ void k_gps_compass(EnvView ev, double *gps, double *compass) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= ev.n) return;
+  double ddx = sub(ev.x[e], ev.ox[e]), ddy = sub(ev.y[e], ev.oy[e]);
+  double fc = ev.fc[e], fs = ev.fs[e];
+  if (gps) {
+    gps[2 * e] = sub(mul(fc, ddx), mul(fs, ddy));
+    gps[2 * e + 1] = add(mul(fs, ddx), mul(fc, ddy));
+  }
+  if (compass) compass[e] = nvx::wrap_angle(sub(ev.h[e], ev.oh[e]));
+}
+
+// Column records from caller-supplied hits (fill_frame operator entry).
+__global__ void k_cols_from_hits(SceneView sc, CamView cam, long long total,
+                                 const double *__restrict__ t_col,
+                                 const int64_t *__restrict__ i_col,
+                                 const double *__restrict__ dirx,
+                                 const double *__restrict__ diry, ColRec *rec) {
+  const long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (g >= total) return;
+  ColRec r;
+  column_epilogue(sc, cam, t_col[g], (int)i_col[g], dirx[g], diry[g], r);
+  rec[g] = r;
+}
+
+// Operator entry: raycast_grid / raycast_all over arbitrary rays.
+__global__ void k_raycast(SceneView sc, const double *ox, const double *oy,
+                          const double *dirx, const double *diry, long long m, double t_max,
+                          int brute, double *t_out, int64_t *i_out) {
+  const long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (k >= m) return;
+  double t;
+  int i;
+  if (brute)
+    ray_brute(sc, ox[k], oy[k], dirx[k], diry[k], t, i);
+  else
+    ray_grid(sc, ox[k], oy[k], dirx[k], diry[k], t_max, t, i);
+  t_out[k] = t;
+  i_out[k] = i;
+}
+
+__global__ void __launch_bounds__(128) k_cast_disc(SceneView sc, const double *px,
+                                                   const double *py, const double *ux,
+                                                   const double *uy, const double *rad,
+                                                   long long m, double *t_out,
+                                                   int64_t *seg_out, double *tan_out) {
+  const long long q = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  if (q >= m) return;
+  double t, tx, ty;
+  int i;
+  warp_cast_disc(sc, px[q], py[q], ux[q], uy[q], rad[q], t, i, tx, ty);
+  if ((threadIdx.x & 31) == 0) {
+    t_out[q] = t;
+    seg_out[q] = i;
+    tan_out[2 * q] = tx;
+    tan_out[2 * q + 1] = ty;
+  }
+}
+
+__global__ void __launch_bounds__(128) k_clearance(SceneView sc, const double *px,
+                                                   const double *py, long long m, double sr,
+                                                   double *out) {
+  const long long q = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  if (q >= m) return;
+  double d = warp_clearance(sc, px[q], py[q], sr);
+  if ((threadIdx.x & 31) == 0) out[q] = d;
+}
+
+// ------------------------------------------------------------ frame fill
+
+#define NV_MAGIC 12582912.0f  // 1.5 * 2^23: low mantissa byte = round(x)
+
+struct FillArgs {
+  const ColRec *rec;
+  const RowRec *rows;
+  int N, W, H;
+  uint8_t *rgb;
+  float *depth;
+  uint16_t *sem;
+  int rows_per_unit;   // rows of one work unit
+  int units_per_seg;   // ceil(H / rows_per_unit)
+  int segs_per_row;    // W / (32 * CPL)
+  long long n_units;   // N * segs_per_row * units_per_seg
+  unsigned int *ctr;   // [0] next unit, [1] finished warps (self-resetting)
+};
+
+// One pixel of fill_frame (_kernels.py:141-207) given its plane/middle class.
+struct PixOut {
+  float depth;
+  uint32_t sem;
+  uint32_t r, g, b;  // float bits, low byte = channel value
+};
+
+__device__ __forceinline__ PixOut shade_px(bool plane, const RowRec &R, float depth_w,
+                                           float num_w, float d2, const float *colw,
+                                           uint32_t sem_w) {
+  PixOut o;
+  o.depth = plane ? R.depth_p : depth_w;
+  o.sem = plane ? (R.sem_mode & 0xffffu) : sem_w;
+  float num = plane ? R.num08_p : num_w;
+  float inv = rsqrtf(d2 + R.v2);          // 1/sqrt(dx^2 + dy^2 + v^2)
+  float t = fmaf(num, inv, 0.2f);         // 0.2 + 0.8 cos(alpha)
+  o.r = __float_as_uint(fmaf(plane ? R.col_p[0] : colw[0], t, NV_MAGIC));
+  o.g = __float_as_uint(fmaf(plane ? R.col_p[1] : colw[1], t, NV_MAGIC));
+  o.b = __float_as_uint(fmaf(plane ? R.col_p[2] : colw[2], t, NV_MAGIC));
+  return o;
+}
+
+__device__ __forceinline__ uint32_t pack4(uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  uint32_t lo = __byte_perm(a, b, 0x0040);
+  uint32_t hi = __byte_perm(c, d, 0x0040);
+  return __byte_perm(lo, hi, 0x5410);
+}
+
+__device__ __forceinline__ unsigned smem_addr(const void *p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void bulk_store(void *gdst, const void *ssrc, unsigned bytes,
+                                           uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;\n" ::"l"(
+          gdst),
+      "r"(smem_addr(ssrc)), "r"(bytes), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_commit() {
+  asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;\n" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() {
+  asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(p));
+  return p;
+}
+
+template <int CPL>
+struct ColRegs {
+  float depth_w[CPL], num_w[CPL], d2[CPL], col[CPL][3];
+  uint32_t lo[CPL], hi[CPL], sem_w[CPL];
+};
+
+// k_fill_tma: streaming frame writer.  A warp owns a unit = (env, column
+// segment of 32*CPL columns, rows_per_unit rows); it keeps its CPL columns'
+// ColRecs in registers, renders RW rows at a time into a private smem stage
+// laid out exactly like global memory, and lane 0 stores the stage with
+// cp.async.bulk (one copy per channel per stage when a warp covers full rows).
+// NS = 2 stages per warp; units are pulled from a self-resetting counter.
+template <int CPL, int RW>
+__global__ void __launch_bounds__(128) k_fill_tma(FillArgs a) {
+  constexpr int NS = 2;
+  constexpr int SEGW = 32 * CPL;
+  extern __shared__ __align__(128) uint8_t smem[];
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  const bool want_rgb = a.rgb != nullptr, want_d = a.depth != nullptr,
+             want_s = a.sem != nullptr;
+  const int off_d = want_rgb ? RW * SEGW * 3 : 0;
+  const int off_s = off_d + (want_d ? RW * SEGW * 4 : 0);
+  const int stage_bytes = off_s + (want_s ? RW * SEGW * 2 : 0);
+  uint8_t *wbase = smem + (size_t)wib * NS * stage_bytes;
+  const uint64_t pol = policy_evict_first();
+  const int W = a.W, H = a.H;
+  const unsigned total_warps = gridDim.x * (blockDim.x >> 5);
+
+  ColRegs<CPL> cr;
+  long long cur_es = -1;
+  int k = 0;
+  long long u = 0;
+  if (lane == 0) u = atomicAdd(a.ctr, 1u);
+  u = __shfl_sync(0xffffffffu, u, 0);
+  while (u < a.n_units) {
+    long long nxt = 0;
+    if (lane == 0) nxt = atomicAdd(a.ctr, 1u);  // prefetch the next unit
+    const long long es = u / a.units_per_seg;
+    const int gidx = (int)(u - es * a.units_per_seg);
+    const int env = (int)(es / a.segs_per_row);
+    const int seg = (int)(es - (long long)env * a.segs_per_row);
+    if (es != cur_es) {
+      cur_es = es;
+      const ColRec *rp = a.rec + (size_t)env * W + seg * SEGW + lane * CPL;
+#pragma unroll
+      for (int c = 0; c < CPL; ++c) {
+        const float4 *q = reinterpret_cast<const float4 *>(rp + c);
+        float4 v0 = __ldg(q), v1 = __ldg(q + 1);
+        cr.depth_w[c] = v0.x;
+        cr.num_w[c] = v0.y;
+        cr.d2[c] = v0.z;
+        uint32_t lh = __float_as_uint(v0.w);
+        cr.lo[c] = lh & 0xffffu;
+        cr.hi[c] = lh >> 16;
+        cr.col[c][0] = v1.x;
+        cr.col[c][1] = v1.y;
+        cr.col[c][2] = v1.z;
+        cr.sem_w[c] = __float_as_uint(v1.w);
+      }
+    }
+    const int r_begin = gidx * a.rows_per_unit;
+    const int r_end = min(H, r_begin + a.rows_per_unit);
+    for (int r0 = r_begin; r0 < r_end; r0 += RW) {
+      const int nr = min(RW, r_end - r0);
+      uint8_t *buf = wbase + (k & (NS - 1)) * stage_bytes;
+      if (k >= NS) {
+        if (lane == 0) bulk_wait_read<NS - 1>();
+        __syncwarp();
+      }
+      for (int rr = 0; rr < nr; ++rr) {
+        const int i = r0 + rr;
+        const float4 *rq = reinterpret_cast<const float4 *>(a.rows + i);
+        float4 q0 = __ldg(rq), q1 = __ldg(rq + 1);
+        RowRec R;
+        R.depth_p = q0.x;
+        R.num08_p = q0.y;
+        R.v2 = q0.z;
+        R.sem_mode = __float_as_uint(q0.w);
+        R.col_p[0] = q1.x;
+        R.col_p[1] = q1.y;
+        R.col_p[2] = q1.z;
+        const bool bottom = (R.sem_mode >> 16) != 0;
+        uint32_t cb[3 * CPL];
+        float dv[CPL];
+        uint32_t sv[CPL];
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) {
+          const bool plane = bottom ? ((uint32_t)i >= cr.hi[c]) : ((uint32_t)i < cr.lo[c]);
+          PixOut o = shade_px(plane, R, cr.depth_w[c], cr.num_w[c], cr.d2[c], cr.col[c],
+                              cr.sem_w[c]);
+          dv[c] = o.depth;
+          sv[c] = o.sem;
+          cb[3 * c] = o.r;
+          cb[3 * c + 1] = o.g;
+          cb[3 * c + 2] = o.b;
+        }
+        if (want_rgb) {
+          uint8_t *dst = buf + (rr * SEGW + lane * CPL) * 3;
+          if constexpr (CPL == 2) {
+#pragma unroll
+            for (int q = 0; q < 3; ++q)
+              reinterpret_cast<uint16_t *>(dst)[q] =
+                  (uint16_t)__byte_perm(cb[2 * q], cb[2 * q + 1], 0x0040);
+          } else {
+            uint32_t w[3 * CPL / 4];
+#pragma unroll
+            for (int q = 0; q < 3 * CPL / 4; ++q)
+              w[q] = pack4(cb[4 * q], cb[4 * q + 1], cb[4 * q + 2], cb[4 * q + 3]);
+            if constexpr (CPL == 4) {
+#pragma unroll
+              for (int q = 0; q < 3; ++q) reinterpret_cast<uint32_t *>(dst)[q] = w[q];
+            } else {  // CPL == 8: three 8-byte chunks
+#pragma unroll
+              for (int q = 0; q < 3; ++q)
+                reinterpret_cast<uint2 *>(dst)[q] = make_uint2(w[2 * q], w[2 * q + 1]);
+            }
+          }
+        }
+        if (want_d) {
+          float *dst = reinterpret_cast<float *>(buf + off_d) + rr * SEGW + lane * CPL;
+          if constexpr (CPL == 2) {
+            *reinterpret_cast<float2 *>(dst) = make_float2(dv[0], dv[1]);
+          } else {
+#pragma unroll
+            for (int q = 0; q < CPL / 4; ++q)
+              reinterpret_cast<float4 *>(dst)[q] =
+                  make_float4(dv[4 * q], dv[4 * q + 1], dv[4 * q + 2], dv[4 * q + 3]);
+          }
+        }
+        if (want_s) {
+          uint16_t *dst = reinterpret_cast<uint16_t *>(buf + off_s) + rr * SEGW + lane * CPL;
+          uint32_t pw[CPL / 2];
+#pragma unroll
+          for (int q = 0; q < CPL / 2; ++q) pw[q] = __byte_perm(sv[2 * q], sv[2 * q + 1], 0x5410);
+          if constexpr (CPL == 2) {
+            *reinterpret_cast<uint32_t *>(dst) = pw[0];
+          } else if constexpr (CPL == 4) {
+            *reinterpret_cast<uint2 *>(dst) = make_uint2(pw[0], pw[1]);
+          } else {
+            *reinterpret_cast<uint4 *>(dst) = make_uint4(pw[0], pw[1], pw[2], pw[3]);
+          }
+        }
+      }
+      fence_proxy_async();
+      __syncwarp();
+      if (lane == 0) {
+        if (a.segs_per_row == 1) {
+          const size_t pix0 = ((size_t)env * H + r0) * W;
+          if (want_rgb) bulk_store(a.rgb + pix0 * 3, buf, (unsigned)(nr * W * 3), pol);
+          if (want_d) bulk_store(a.depth + pix0, buf + off_d, (unsigned)(nr * W * 4), pol);
+          if (want_s) bulk_store(a.sem + pix0, buf + off_s, (unsigned)(nr * W * 2), pol);
+        } else {
+          for (int rr = 0; rr < nr; ++rr) {
+            const size_t pix0 = ((size_t)env * H + r0 + rr) * W + (size_t)seg * SEGW;
+            if (want_rgb)
+              bulk_store(a.rgb + pix0 * 3, buf + rr * SEGW * 3, (unsigned)(SEGW * 3), pol);
+            if (want_d)
+              bulk_store(a.depth + pix0, buf + off_d + rr * SEGW * 4, (unsigned)(SEGW * 4), pol);
+            if (want_s)
+              bulk_store(a.sem + pix0, buf + off_s + rr * SEGW * 2, (unsigned)(SEGW * 2), pol);
+          }
+        }
+        bulk_commit();
+      }
+      ++k;
+    }
+    u = __shfl_sync(0xffffffffu, nxt, 0);
+  }
+  if (lane == 0) {
+    bulk_wait_all();
+    // last warp out resets the scheduler for the next launch
+    if (atomicAdd(a.ctr + 1, 1u) == total_warps - 1) {
+      a.ctr[0] = 0;
+      a.ctr[1] = 0;
+      __threadfence();
+    }
+  }
+}
+
+// One thread per pixel, any W/H (also the reference-layout fallback).
+__global__ void k_fill_generic(FillArgs a) {
+  const long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const long long total = (long long)a.N * a.H * a.W;
+  if (p >= total) return;
+  const int j = (int)(p % a.W);
+  const long long ei = p / a.W;
+  const int i = (int)(ei % a.H);
+  const int e = (int)(ei / a.H);
+  const ColRec c = a.rec[(size_t)e * a.W + j];
+  const RowRec R = a.rows[i];
+  const bool bottom = (R.sem_mode >> 16) != 0;
+  const uint32_t lo = c.lohi & 0xffffu, hi = c.lohi >> 16;
+  const bool plane = bottom ? ((uint32_t)i >= hi) : ((uint32_t)i < lo);
+  PixOut o = shade_px(plane, R, c.depth_w, c.num08_w, c.d2, c.col_w, c.sem_w);
+  if (a.depth) a.depth[p] = o.depth;
+  if (a.sem) a.sem[p] = (uint16_t)o.sem;
+  if (a.rgb) {
+    a.rgb[3 * p] = (uint8_t)o.r;
+    a.rgb[3 * p + 1] = (uint8_t)o.g;
+    a.rgb[3 * p + 2] = (uint8_t)o.b;
+  }
+}
+
+}  // namespace nvk

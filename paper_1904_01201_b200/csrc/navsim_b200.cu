@@ -1,0 +1,791 @@
+// navsim_b200.cu -- host side of the C ABI (include/navsim_b200.h).
+//
+// Scene upload builds the reference's uniform grid on the host exactly like
+// SegmentIndex.__init__ (geometry.py:109-141), expands bucket items into
+// contiguous CellEntry runs, and uploads everything once.  Per-step calls
+// only enqueue kernels on the caller's stream (no host synchronisation).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/navsim_b200.h"
+#include "device.cuh"
+#include "exact_math.cuh"
+#include "kernels.cuh"
+
+using namespace nvd;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char *fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define CK(call)                                                                   \
+  do {                                                                             \
+    cudaError_t e_ = (call);                                                       \
+    if (e_ != cudaSuccess)                                                         \
+      return fail(NV_ERR_CUDA, "%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_), \
+                  __FILE__, __LINE__);                                             \
+  } while (0)
+
+struct DevBuf {
+  void *p = nullptr;
+  size_t bytes = 0;
+  ~DevBuf() { release(); }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+  int alloc(size_t b) {
+    if (b <= bytes && p) return NV_OK;
+    release();
+    if (b == 0) b = 16;
+    if (cudaMalloc(&p, b) != cudaSuccess) {
+      cudaGetLastError();
+      return fail(NV_ERR_OOM, "cudaMalloc(%zu) failed", b);
+    }
+    bytes = b;
+    return NV_OK;
+  }
+  template <class T>
+  T *as() const { return reinterpret_cast<T *>(p); }
+};
+
+#define TRY(x)               \
+  do {                       \
+    int r_ = (x);            \
+    if (r_ != NV_OK) return r_; \
+  } while (0)
+
+template <class T>
+int upload(DevBuf &b, const std::vector<T> &v) {
+  TRY(b.alloc(sizeof(T) * std::max<size_t>(v.size(), 1)));
+  if (!v.empty()) CK(cudaMemcpy(b.p, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice));
+  return NV_OK;
+}
+
+struct Camera {
+  bool on = false;
+  int W = 0, H = 0;
+  double focal = 0, max_range = 0;
+  int n_top = 0, b0 = 0;
+  double tables_cam_h = NAN;
+  DevBuf u, tc, tf, rows;
+  DevBuf rec;      // ColRec N x W
+  DevBuf ctr;      // fill scheduler counters
+};
+
+}  // namespace
+
+struct nv_ctx {
+  int device = 0;
+  int sm_count = 148;
+  int max_smem_optin = 0;
+  // scene
+  bool has_scene = false;
+  int64_t n = 0;
+  double wall_h = 2.5;
+  double floor3[3] = {0.35, 0.33, 0.30}, ceil3[3] = {0.85, 0.85, 0.85};
+  double gx0 = -0.5, gy0 = -0.5;
+  int gnx = 1, gny = 1;
+  int64_t nitems = 0;
+  DevBuf ax, ay, bx, by, ex, ey, nx, ny, sem, alb, starts, ent, items;
+  // agent
+  double radius = 0.1, step = 0.25, turn_rad = 0.17453292519943295, sensor_h = 1.5;
+  // envs
+  int64_t n_envs = 0;
+  DevBuf x, y, h, path, coll, ch, sh, ox, oy, oh, fc, fs, reset;
+  Camera cams[8];
+  // host-buffer (e2e) path scratch
+  DevBuf e_act, e_rgb, e_depth, e_sem, e_gps, e_comp, e_coll, e_disp;
+  int64_t launches = 0;
+  // optional per-kernel CUDA-event timing (bench roofline evidence)
+  bool prof_on = false;
+  std::vector<cudaEvent_t> prof_ev;   // pool, pairs
+  std::vector<int> prof_kind;         // kind per pair in use
+  size_t prof_used = 0;               // pairs in use
+  double prof_ms[4] = {0, 0, 0, 0};
+  int64_t prof_n[4] = {0, 0, 0, 0};
+  ~nv_ctx() {
+    for (auto e : prof_ev) cudaEventDestroy(e);
+  }
+  // launch config
+  SceneView scene_view() const {
+    SceneView v;
+    v.ax = ax.as<double>(); v.ay = ay.as<double>(); v.bx = bx.as<double>();
+    v.by = by.as<double>(); v.ex = ex.as<double>(); v.ey = ey.as<double>();
+    v.nx = nx.as<double>(); v.ny = ny.as<double>();
+    v.sem = sem.as<uint16_t>(); v.alb255 = alb.as<float4>();
+    v.starts = starts.as<int32_t>(); v.ent = ent.as<CellEntry>(); v.items = items.as<int32_t>();
+    v.x0 = gx0; v.y0 = gy0; v.gnx = gnx; v.gny = gny; v.n = n;
+    return v;
+  }
+  EnvView env_view() const {
+    EnvView v;
+    v.x = x.as<double>(); v.y = y.as<double>(); v.h = h.as<double>(); v.path = path.as<double>();
+    v.coll = coll.as<int64_t>(); v.ch = ch.as<double>(); v.sh = sh.as<double>();
+    v.ox = ox.as<double>(); v.oy = oy.as<double>(); v.oh = oh.as<double>();
+    v.fc = fc.as<double>(); v.fs = fs.as<double>(); v.reset = reset.as<uint8_t>();
+    v.n = (int)n_envs;
+    return v;
+  }
+};
+
+namespace {
+
+// --------------------------------------------------------------- grid build
+// Exact restatement of SegmentIndex.__init__ (geometry.py:109-141).
+int64_t cell_coord_h(double v, double o, int64_t n) {
+  double d = (v - o) / 1.0;
+  if (!(d >= 1.0)) return 0;
+  if (d >= (double)(n - 1)) return n - 1;
+  return (int64_t)d;
+}
+
+struct HostGrid {
+  double x0, y0;
+  int64_t nx, ny;
+  std::vector<int64_t> starts, items;
+};
+
+HostGrid build_grid(const double *segs, int64_t n) {
+  HostGrid g;
+  double x1, y1;
+  if (n > 0) {
+    double mnx = INFINITY, mny = INFINITY, mxx = -INFINITY, mxy = -INFINITY;
+    for (int64_t i = 0; i < n; ++i) {
+      const double *s = segs + 4 * i;
+      mnx = std::min(mnx, std::min(s[0], s[2]));
+      mny = std::min(mny, std::min(s[1], s[3]));
+      mxx = std::max(mxx, std::max(s[0], s[2]));
+      mxy = std::max(mxy, std::max(s[1], s[3]));
+    }
+    g.x0 = mnx - 0.5; g.y0 = mny - 0.5; x1 = mxx + 0.5; y1 = mxy + 0.5;
+  } else {
+    g.x0 = g.y0 = -0.5; x1 = y1 = 0.5;
+  }
+  g.nx = std::max<int64_t>(1, (int64_t)std::ceil((x1 - g.x0) / 1.0));
+  g.ny = std::max<int64_t>(1, (int64_t)std::ceil((y1 - g.y0) / 1.0));
+  const int64_t nc = g.nx * g.ny;
+  std::vector<int64_t> cnt(nc + 1, 0);
+  auto range = [&](int64_t i, int64_t &cx0, int64_t &cy0, int64_t &cx1, int64_t &cy1) {
+    const double *s = segs + 4 * i;
+    cx0 = cell_coord_h(std::min(s[0], s[2]), g.x0, g.nx);
+    cy0 = cell_coord_h(std::min(s[1], s[3]), g.y0, g.ny);
+    cx1 = cell_coord_h(std::max(s[0], s[2]), g.x0, g.nx);
+    cy1 = cell_coord_h(std::max(s[1], s[3]), g.y0, g.ny);
+  };
+  for (int64_t i = 0; i < n; ++i) {
+    int64_t a, b, c, d;
+    range(i, a, b, c, d);
+    for (int64_t cy = b; cy <= d; ++cy)
+      for (int64_t cx = a; cx <= c; ++cx) cnt[cy * g.nx + cx + 1]++;
+  }
+  for (int64_t c = 0; c < nc; ++c) cnt[c + 1] += cnt[c];
+  g.starts = cnt;
+  g.items.assign(cnt[nc], 0);
+  for (int64_t i = 0; i < n; ++i) {
+    int64_t a, b, c, d;
+    range(i, a, b, c, d);
+    for (int64_t cy = b; cy <= d; ++cy)
+      for (int64_t cx = a; cx <= c; ++cx) g.items[cnt[cy * g.nx + cx]++] = i;
+  }
+  return g;
+}
+
+int ensure_scene(nv_ctx *c) {
+  if (!c->has_scene) return fail(NV_ERR_STATE, "no scene uploaded (nv_scene_upload)");
+  return NV_OK;
+}
+int ensure_envs(nv_ctx *c) {
+  TRY(ensure_scene(c));
+  if (c->n_envs <= 0) return fail(NV_ERR_STATE, "no envs allocated (nv_envs_alloc)");
+  return NV_OK;
+}
+
+// Row tables for a camera (fill_frame's per-row quantities, _kernels.py:141,
+// 150, 158): v, tc, tf in exact f64 (host IEEE, no contraction), shading f32.
+int build_camera_tables(nv_ctx *c, Camera &cam, double cam_h) {
+  const int W = cam.W, H = cam.H;
+  std::vector<double> u(W), tc(H, 0.0), tf(H, 0.0);
+  for (int j = 0; j < W; ++j) u[j] = (((double)j + 0.5) - (double)W * 0.5) / cam.focal;
+  std::vector<RowRec> rows(H);
+  int n_top = 0, b0 = H;
+  for (int i = 0; i < H; ++i) {
+    double v = ((double)H * 0.5 - ((double)i + 0.5)) / cam.focal;
+    RowRec r;
+    std::memset(&r, 0, sizeof r);
+    r.v2 = (float)v * (float)v;
+    bool lit = false;
+    double t = 0.0;
+    const double *col = nullptr;
+    uint32_t sem = 0, mode = 0;
+    if (v > 0.0) {
+      n_top = i + 1;
+      tc[i] = (c->wall_h - cam_h) / v;
+      t = tc[i];
+      lit = t < cam.max_range;
+      col = c->ceil3;
+      sem = 65535;
+    } else if (v < 0.0) {
+      if (b0 == H) b0 = i;
+      tf[i] = -cam_h / v;
+      t = tf[i];
+      lit = t < cam.max_range;
+      col = c->floor3;
+      sem = 65534;
+      mode = 1;
+    }
+    if (lit) {
+      r.depth_p = (float)t;
+      r.num08_p = 0.8f * (float)std::fabs(v);
+      for (int k = 0; k < 3; ++k) r.col_p[k] = (float)(col[k] * 255.0);
+      r.sem_mode = sem | (mode << 16);
+    } else {
+      r.depth_p = (float)cam.max_range;
+      r.sem_mode = mode << 16;
+    }
+    rows[i] = r;
+  }
+  cam.n_top = n_top;
+  cam.b0 = b0;
+  TRY(upload(cam.u, u));
+  TRY(upload(cam.tc, tc));
+  TRY(upload(cam.tf, tf));
+  TRY(upload(cam.rows, rows));
+  cam.tables_cam_h = cam_h;
+  return NV_OK;
+}
+
+CamView cam_view(const Camera &cam) {
+  CamView v;
+  v.W = cam.W; v.H = cam.H; v.n_top = cam.n_top; v.b0 = cam.b0; v.max_range = cam.max_range;
+  v.u = cam.u.as<double>(); v.tc = cam.tc.as<double>(); v.tf = cam.tf.as<double>();
+  v.rows = cam.rows.as<RowRec>();
+  return v;
+}
+
+// Event pair around one launch of kind k (0 step, 1 cast, 2 fill, 3 other).
+struct Prof {
+  nv_ctx *c;
+  cudaStream_t st;
+  int pair = -1;
+  Prof(nv_ctx *c_, cudaStream_t s_, int kind) : c(c_), st(s_) {
+    if (!c->prof_on) return;
+    if (2 * (c->prof_used + 1) > c->prof_ev.size()) {
+      cudaEvent_t a, b;
+      cudaEventCreate(&a);
+      cudaEventCreate(&b);
+      c->prof_ev.push_back(a);
+      c->prof_ev.push_back(b);
+      c->prof_kind.push_back(kind);
+    }
+    pair = (int)c->prof_used++;
+    c->prof_kind[pair] = kind;
+    cudaEventRecord(c->prof_ev[2 * pair], st);
+  }
+  ~Prof() {
+    if (pair >= 0) cudaEventRecord(c->prof_ev[2 * pair + 1], st);
+  }
+};
+
+int check_launch(nv_ctx *c) {
+  c->launches++;
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(NV_ERR_CUDA, "kernel launch failed: %s", cudaGetErrorString(e));
+  return NV_OK;
+}
+
+unsigned blocks_for(long long work, int per_block) {
+  return (unsigned)std::max<long long>(1, (work + per_block - 1) / per_block);
+}
+
+// Fill launch: TMA streaming writer when the row layout allows 16-byte bulk
+// copies, else the generic per-pixel kernel.
+template <int CPL>
+int launch_fill_tma(nv_ctx *c, nvk::FillArgs &a, cudaStream_t st) {
+  constexpr int RW = 2;
+  const int segw = 32 * CPL;
+  const int bpp = (a.rgb ? 3 : 0) + (a.depth ? 4 : 0) + (a.sem ? 2 : 0);
+  const int stage = RW * segw * bpp;
+  const int warps = 4;
+  const size_t smem = (size_t)warps * 2 * stage;
+  auto kern = nvk::k_fill_tma<CPL, RW>;
+  static int configured_smem[3] = {0, 0, 0};
+  int slot = CPL == 2 ? 0 : (CPL == 4 ? 1 : 2);
+  if ((int)smem > configured_smem[slot]) {
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    configured_smem[slot] = (int)smem;
+  }
+  int per_sm = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, warps * 32, smem));
+  per_sm = std::max(1, per_sm);
+  a.segs_per_row = a.W / segw;
+  a.rows_per_unit = 16;
+  a.units_per_seg = (a.H + a.rows_per_unit - 1) / a.rows_per_unit;
+  a.n_units = (long long)a.N * a.segs_per_row * a.units_per_seg;
+  long long want = (a.n_units + warps - 1) / warps;
+  unsigned grid = (unsigned)std::max<long long>(1, std::min<long long>(want, (long long)per_sm * c->sm_count));
+  Prof pf(c, st, 2);
+  kern<<<grid, warps * 32, smem, st>>>(a);
+  return check_launch(c);
+}
+
+int launch_fill(nv_ctx *c, Camera &cam, int64_t N, uint8_t *rgb, float *depth, uint16_t *sem,
+                cudaStream_t st) {
+  if (!rgb && !depth && !sem) return NV_OK;
+  nvk::FillArgs a;
+  a.rec = cam.rec.as<ColRec>();
+  a.rows = cam.rows.as<RowRec>();
+  a.N = (int)N; a.W = cam.W; a.H = cam.H;
+  a.rgb = rgb; a.depth = depth; a.sem = sem;
+  a.ctr = cam.ctr.as<unsigned int>();
+  auto al16 = [](const void *p) { return ((uintptr_t)p & 15) == 0; };
+  bool aligned = al16(rgb) && al16(depth) && al16(sem);
+  if (aligned && cam.W % 256 == 0) return launch_fill_tma<8>(c, a, st);
+  if (aligned && cam.W == 128) return launch_fill_tma<4>(c, a, st);
+  if (aligned && cam.W == 64) return launch_fill_tma<2>(c, a, st);
+  long long total = N * (long long)cam.W * cam.H;
+  Prof pf(c, st, 2);
+  nvk::k_fill_generic<<<blocks_for(total, 256), 256, 0, st>>>(a);
+  return check_launch(c);
+}
+
+int cam_check(nv_ctx *c, int cam) {
+  if (cam < 0 || cam >= 8 || !c->cams[cam].on)
+    return fail(NV_ERR_STATE, "camera %d not configured (nv_camera_config)", cam);
+  Camera &k = c->cams[cam];
+  if (c->sensor_h > c->wall_h) return fail(NV_ERR_ARG, "sensor height must stay below wall height");
+  if (k.tables_cam_h != c->sensor_h) TRY(build_camera_tables(c, k, c->sensor_h));
+  TRY(k.rec.alloc(sizeof(ColRec) * (size_t)std::max<int64_t>(1, c->n_envs) * k.W));
+  return NV_OK;
+}
+
+int do_cast(nv_ctx *c, int cam, double *gps, double *compass, cudaStream_t st) {
+  Camera &k = c->cams[cam];
+  long long total = c->n_envs * (long long)k.W;
+  // t_max = max_range: capping the walk is output-identical for rendered
+  // frames (tests/test_gpu_parity.py checks it against the
+  // reference's uncapped t_max = 1e9 render).
+  Prof pf(c, st, 1);
+  nvk::k_column_cast<<<blocks_for(total, 256), 256, 0, st>>>(
+      c->env_view(), c->scene_view(), cam_view(k), k.rec.as<ColRec>(), k.max_range, gps,
+      compass);
+  return check_launch(c);
+}
+
+int do_step(nv_ctx *c, const int8_t *actions, uint8_t *collided, double *disp, int32_t *status,
+            cudaStream_t st) {
+  nvk::AgentCfg cfg{c->radius, c->step, c->turn_rad};
+  long long threads = c->n_envs * 32;
+  Prof pf(c, st, 0);
+  nvk::k_agent_step<<<blocks_for(threads, 128), 128, 0, st>>>(c->env_view(), c->scene_view(), cfg,
+                                                               actions, collided, disp, status);
+  return check_launch(c);
+}
+
+}  // namespace
+
+// ====================================================================== ABI
+
+extern "C" {
+
+const char *nv_last_error(void) { return g_err.c_str(); }
+int nv_version(void) { return 1; }
+
+int nv_create(int device, nv_ctx **out) {
+  if (!out) return fail(NV_ERR_ARG, "out is NULL");
+  int ndev = 0;
+  CK(cudaGetDeviceCount(&ndev));
+  if (device < 0 || device >= ndev) return fail(NV_ERR_ARG, "device %d out of range (%d)", device, ndev);
+  CK(cudaSetDevice(device));
+  nv_ctx *c = new nv_ctx();
+  c->device = device;
+  cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device);
+  cudaDeviceGetAttribute(&c->max_smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+  *out = c;
+  return NV_OK;
+}
+
+int nv_destroy(nv_ctx *ctx) {
+  if (!ctx) return NV_OK;
+  cudaSetDevice(ctx->device);
+  delete ctx;
+  return NV_OK;
+}
+
+int nv_scene_upload(nv_ctx *c, const double *segs, const uint16_t *sem, const double *albedo,
+                    int64_t n, double wall_height, const double *floor3, const double *ceil3) {
+  if (!c) return fail(NV_ERR_ARG, "ctx is NULL");
+  if (n < 0 || (n > 0 && (!segs || !sem || !albedo)))
+    return fail(NV_ERR_ARG, "bad scene arrays");
+  if (n >= (1LL << 31)) return fail(NV_ERR_ARG, "too many segments (%lld)", (long long)n);
+  CK(cudaSetDevice(c->device));
+  HostGrid g = build_grid(segs, n);
+  if (g.nx * g.ny >= (1LL << 31) || (int64_t)g.items.size() >= (1LL << 31))
+    return fail(NV_ERR_ARG, "scene grid too large");
+  std::vector<double> ax(n), ay(n), bx(n), by(n), ex(n), ey(n), nx(n), ny(n);
+  std::vector<uint16_t> sm(n);
+  std::vector<float4> alb(n);
+  for (int64_t i = 0; i < n; ++i) {
+    ax[i] = segs[4 * i]; ay[i] = segs[4 * i + 1]; bx[i] = segs[4 * i + 2]; by[i] = segs[4 * i + 3];
+    ex[i] = bx[i] - ax[i]; ey[i] = by[i] - ay[i];
+    // segment_normals (geometry.py:66-73): glibc hypot, like np.hypot
+    double ln = std::hypot(ex[i], ey[i]);
+    if (!(ln > 0.0)) ln = 1.0;
+    nx[i] = -ey[i] / ln;
+    ny[i] = ex[i] / ln;
+    sm[i] = sem[i];
+    alb[i] = make_float4((float)(albedo[3 * i] * 255.0), (float)(albedo[3 * i + 1] * 255.0),
+                         (float)(albedo[3 * i + 2] * 255.0), 0.0f);
+  }
+  std::vector<int32_t> starts(g.starts.size()), items(g.items.size());
+  std::vector<CellEntry> ent(g.items.size());
+  for (size_t k = 0; k < g.starts.size(); ++k) starts[k] = (int32_t)g.starts[k];
+  for (size_t q = 0; q < g.items.size(); ++q) {
+    int64_t i = g.items[q];
+    items[q] = (int32_t)i;
+    CellEntry e;
+    std::memset(&e, 0, sizeof e);
+    e.ax = ax[i]; e.ay = ay[i]; e.ex = ex[i]; e.ey = ey[i]; e.idx = (int32_t)i;
+    ent[q] = e;
+  }
+  TRY(upload(c->ax, ax)); TRY(upload(c->ay, ay)); TRY(upload(c->bx, bx)); TRY(upload(c->by, by));
+  TRY(upload(c->ex, ex)); TRY(upload(c->ey, ey)); TRY(upload(c->nx, nx)); TRY(upload(c->ny, ny));
+  TRY(upload(c->sem, sm)); TRY(upload(c->alb, alb));
+  TRY(upload(c->starts, starts)); TRY(upload(c->items, items)); TRY(upload(c->ent, ent));
+  c->n = n;
+  c->wall_h = wall_height;
+  for (int k = 0; k < 3; ++k) {
+    c->floor3[k] = floor3 ? floor3[k] : c->floor3[k];
+    c->ceil3[k] = ceil3 ? ceil3[k] : c->ceil3[k];
+  }
+  c->gx0 = g.x0; c->gy0 = g.y0; c->gnx = (int)g.nx; c->gny = (int)g.ny;
+  c->nitems = (int64_t)g.items.size();
+  c->has_scene = true;
+  for (auto &k : c->cams) k.tables_cam_h = NAN;  // colours / wall height changed
+  return NV_OK;
+}
+
+int nv_scene_grid_info(nv_ctx *c, double *x0, double *y0, int64_t *nx, int64_t *ny,
+                       int64_t *nitems) {
+  if (!c) return fail(NV_ERR_ARG, "ctx is NULL");
+  TRY(ensure_scene(c));
+  if (x0) *x0 = c->gx0;
+  if (y0) *y0 = c->gy0;
+  if (nx) *nx = c->gnx;
+  if (ny) *ny = c->gny;
+  if (nitems) *nitems = c->nitems;
+  return NV_OK;
+}
+
+int nv_agent_config(nv_ctx *c, double radius, double forward_step, double turn_rad,
+                    double sensor_height) {
+  if (!c) return fail(NV_ERR_ARG, "ctx is NULL");
+  if (!(radius >= 0.0) || !(forward_step > 0.0) || !(turn_rad > 0.0) || !(sensor_height > 0.0))
+    return fail(NV_ERR_ARG, "invalid agent config");
+  if (c->has_scene && sensor_height > c->wall_h)
+    return fail(NV_ERR_ARG, "sensor height %g exceeds wall height %g", sensor_height, c->wall_h);
+  c->radius = radius;
+  c->step = forward_step;
+  c->turn_rad = turn_rad;
+  c->sensor_h = sensor_height;
+  return NV_OK;
+}
+
+int nv_envs_alloc(nv_ctx *c, int64_t n_envs) {
+  if (!c) return fail(NV_ERR_ARG, "ctx is NULL");
+  if (n_envs <= 0 || n_envs >= (1LL << 30)) return fail(NV_ERR_ARG, "bad n_envs %lld", (long long)n_envs);
+  CK(cudaSetDevice(c->device));
+  size_t d = sizeof(double) * (size_t)n_envs;
+  for (DevBuf *b : {&c->x, &c->y, &c->h, &c->path, &c->ch, &c->sh, &c->ox, &c->oy, &c->oh, &c->fc,
+                    &c->fs}) {
+    b->release();
+    TRY(b->alloc(d));
+    CK(cudaMemset(b->p, 0, d));
+  }
+  c->coll.release();
+  TRY(c->coll.alloc(sizeof(int64_t) * (size_t)n_envs));
+  CK(cudaMemset(c->coll.p, 0, sizeof(int64_t) * (size_t)n_envs));
+  c->reset.release();
+  TRY(c->reset.alloc((size_t)n_envs));
+  CK(cudaMemset(c->reset.p, 0, (size_t)n_envs));
+  c->n_envs = n_envs;
+  return NV_OK;
+}
+
+int nv_camera_config(nv_ctx *c, int cam, int width, int height, double focal, double max_range) {
+  if (!c) return fail(NV_ERR_ARG, "ctx is NULL");
+  if (cam < 0 || cam >= 8) return fail(NV_ERR_ARG, "camera index %d out of range [0, 8)", cam);
+  if (width < 1 || height < 1 || width > 16384 || height > 16384)
+    return fail(NV_ERR_ARG, "sensor resolution must be at least 1x1 (got %dx%d)", width, height);
+  if (!(focal > 0.0) || !std::isfinite(focal)) return fail(NV_ERR_ARG, "bad focal %g", focal);
+  if (!(max_range > 0.0)) return fail(NV_ERR_ARG, "max_range must be positive");
+  TRY(ensure_scene(c));
+  CK(cudaSetDevice(c->device));
+  Camera &k = c->cams[cam];
+  k.W = width;
+  k.H = height;
+  k.focal = focal;
+  k.max_range = max_range;
+  TRY(build_camera_tables(c, k, c->sensor_h));
+  TRY(k.ctr.alloc(16));
+  CK(cudaMemset(k.ctr.p, 0, 16));
+  k.on = true;
+  return NV_OK;
+}
+
+int nv_set_poses(nv_ctx *c, const double *xy, const double *heading, const uint8_t *mask,
+                 int32_t *status_out, double *clearance_out) {
+  if (!c) return fail(NV_ERR_ARG, "ctx is NULL");
+  TRY(ensure_envs(c));
+  if (!xy || !heading) return fail(NV_ERR_ARG, "xy/heading are NULL");
+  CK(cudaSetDevice(c->device));
+  const size_t N = (size_t)c->n_envs;
+  DevBuf dxy, dh, dm, dst, dcl;
+  TRY(dxy.alloc(16 * N)); TRY(dh.alloc(8 * N)); TRY(dst.alloc(4 * N)); TRY(dcl.alloc(8 * N));
+  CK(cudaMemcpy(dxy.p, xy, 16 * N, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(dh.p, heading, 8 * N, cudaMemcpyHostToDevice));
+  if (mask) {
+    TRY(dm.alloc(N));
+    CK(cudaMemcpy(dm.p, mask, N, cudaMemcpyHostToDevice));
+  }
+  nvk::k_set_poses<<<blocks_for((long long)N * 32, 128), 128>>>(
+      c->env_view(), c->scene_view(), c->radius, dxy.as<double>(), dh.as<double>(),
+      mask ? dm.as<uint8_t>() : nullptr, dst.as<int32_t>(), dcl.as<double>());
+  TRY(check_launch(c));
+  CK(cudaDeviceSynchronize());
+  std::vector<int32_t> st(N);
+  std::vector<double> cl(N);
+  CK(cudaMemcpy(st.data(), dst.p, 4 * N, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(cl.data(), dcl.p, 8 * N, cudaMemcpyDeviceToHost));
+  if (status_out) std::memcpy(status_out, st.data(), 4 * N);
+  if (clearance_out) std::memcpy(clearance_out, cl.data(), 8 * N);
+  for (size_t e = 0; e < N; ++e)
+    if (st[e] == NV_ENV_TOO_CLOSE)
+      return fail(NV_ERR_ARG, "env %zu: position (%.3f, %.3f) is %.3f m from the nearest wall; agent radius is %g",
+                  e, xy[2 * e], xy[2 * e + 1], cl[e], c->radius);
+  return NV_OK;
+}
+
+int nv_step(nv_ctx *c, const int8_t *actions, uint8_t *collided, double *displacement,
+            int32_t *status, void *stream) {
+  if (!c) return fail(NV_ERR_ARG, "ctx is NULL");
+  TRY(ensure_envs(c));
+  if (!actions) return fail(NV_ERR_ARG, "actions is NULL");
+  return do_step(c, actions, collided, displacement, status, (cudaStream_t)stream);
+}
+
+int nv_render(nv_ctx *c, int cam, uint8_t *rgb, float *depth, uint16_t *sem, double *gps,
+              double *compass, void *stream) {
+  if (!c) return fail(NV_ERR_ARG, "ctx is NULL");
+  TRY(ensure_envs(c));
+  TRY(cam_check(c, cam));
+  cudaStream_t st = (cudaStream_t)stream;
+  TRY(do_cast(c, cam, gps, compass, st));
+  return launch_fill(c, c->cams[cam], c->n_envs, rgb, depth, sem, st);
+}
+
+int nv_step_render(nv_ctx *c, const int8_t *actions, int cam, uint8_t *rgb, float *depth,
+                   uint16_t *sem, double *gps, double *compass, uint8_t *collided,
+                   double *displacement, int32_t *status, void *stream) {
+  if (!c) return fail(NV_ERR_ARG, "ctx is NULL");
+  TRY(ensure_envs(c));
+  TRY(cam_check(c, cam));
+  if (!actions) return fail(NV_ERR_ARG, "actions is NULL");
+  cudaStream_t st = (cudaStream_t)stream;
+  TRY(do_step(c, actions, collided, displacement, status, st));
+  TRY(do_cast(c, cam, gps, compass, st));
+  return launch_fill(c, c->cams[cam], c->n_envs, rgb, depth, sem, st);
+}
+
+int nv_step_render_host(nv_ctx *c, const int8_t *actions_host, int cam, uint32_t channels,
+                        uint8_t *rgb_host, float *depth_host, uint16_t *sem_host,
+                        double *gps_host, double *compass_host, uint8_t *collided_host,
+                        double *displacement_host, void *stream) {
+  if (!c) return fail(NV_ERR_ARG, "ctx is NULL");
+  TRY(ensure_envs(c));
+  TRY(cam_check(c, cam));
+  if (!actions_host) return fail(NV_ERR_ARG, "actions is NULL");
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t N = (size_t)c->n_envs;
+  const Camera &k = c->cams[cam];
+  const size_t px = N * k.W * k.H;
+  const bool want_rgb = (channels & NV_CH_RGB) || rgb_host;
+  const bool want_d = (channels & NV_CH_DEPTH) || depth_host;
+  const bool want_s = (channels & NV_CH_SEM) || sem_host;
+  TRY(c->e_act.alloc(N));
+  if (want_rgb) TRY(c->e_rgb.alloc(px * 3));
+  if (want_d) TRY(c->e_depth.alloc(px * 4));
+  if (want_s) TRY(c->e_sem.alloc(px * 2));
+  TRY(c->e_gps.alloc(16 * N)); TRY(c->e_comp.alloc(8 * N)); TRY(c->e_coll.alloc(N));
+  TRY(c->e_disp.alloc(8 * N));
+  CK(cudaMemcpyAsync(c->e_act.p, actions_host, N, cudaMemcpyHostToDevice, st));
+  TRY(nv_step_render(c, c->e_act.as<int8_t>(), cam, want_rgb ? c->e_rgb.as<uint8_t>() : nullptr,
+                     want_d ? c->e_depth.as<float>() : nullptr,
+                     want_s ? c->e_sem.as<uint16_t>() : nullptr, c->e_gps.as<double>(),
+                     c->e_comp.as<double>(), c->e_coll.as<uint8_t>(), c->e_disp.as<double>(),
+                     nullptr, stream));
+  if (rgb_host) CK(cudaMemcpyAsync(rgb_host, c->e_rgb.p, px * 3, cudaMemcpyDeviceToHost, st));
+  if (depth_host) CK(cudaMemcpyAsync(depth_host, c->e_depth.p, px * 4, cudaMemcpyDeviceToHost, st));
+  if (sem_host) CK(cudaMemcpyAsync(sem_host, c->e_sem.p, px * 2, cudaMemcpyDeviceToHost, st));
+  if (gps_host) CK(cudaMemcpyAsync(gps_host, c->e_gps.p, 16 * N, cudaMemcpyDeviceToHost, st));
+  if (compass_host) CK(cudaMemcpyAsync(compass_host, c->e_comp.p, 8 * N, cudaMemcpyDeviceToHost, st));
+  if (collided_host) CK(cudaMemcpyAsync(collided_host, c->e_coll.p, N, cudaMemcpyDeviceToHost, st));
+  if (displacement_host)
+    CK(cudaMemcpyAsync(displacement_host, c->e_disp.p, 8 * N, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return NV_OK;
+}
+
+int nv_host_frames(nv_ctx *c, uint8_t **rgb, float **depth, uint16_t **sem) {
+  if (!c) return fail(NV_ERR_ARG, "ctx is NULL");
+  if (rgb) *rgb = c->e_rgb.as<uint8_t>();
+  if (depth) *depth = c->e_depth.as<float>();
+  if (sem) *sem = c->e_sem.as<uint16_t>();
+  return NV_OK;
+}
+
+int nv_gps_compass(nv_ctx *c, double *gps, double *compass, void *stream) {
+  if (!c) return fail(NV_ERR_ARG, "ctx is NULL");
+  TRY(ensure_envs(c));
+  nvk::k_gps_compass<<<blocks_for(c->n_envs, 128), 128, 0, (cudaStream_t)stream>>>(
+      c->env_view(), gps, compass);
+  return check_launch(c);
+}
+
+int nv_get_state(nv_ctx *c, double *xy, double *heading, double *path_len, int64_t *collisions,
+                 void *stream) {
+  if (!c) return fail(NV_ERR_ARG, "ctx is NULL");
+  TRY(ensure_envs(c));
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t N = (size_t)c->n_envs;
+  if (xy) {
+    CK(cudaMemcpy2DAsync(xy, 16, c->x.p, 8, 8, N, cudaMemcpyDeviceToDevice, st));
+    CK(cudaMemcpy2DAsync(xy + 1, 16, c->y.p, 8, 8, N, cudaMemcpyDeviceToDevice, st));
+  }
+  if (heading) CK(cudaMemcpyAsync(heading, c->h.p, 8 * N, cudaMemcpyDeviceToDevice, st));
+  if (path_len) CK(cudaMemcpyAsync(path_len, c->path.p, 8 * N, cudaMemcpyDeviceToDevice, st));
+  if (collisions) CK(cudaMemcpyAsync(collisions, c->coll.p, 8 * N, cudaMemcpyDeviceToDevice, st));
+  return NV_OK;
+}
+
+int nv_get_frame(nv_ctx *c, double *origin_xy, double *heading, void *stream) {
+  if (!c) return fail(NV_ERR_ARG, "ctx is NULL");
+  TRY(ensure_envs(c));
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t N = (size_t)c->n_envs;
+  if (origin_xy) {
+    CK(cudaMemcpy2DAsync(origin_xy, 16, c->ox.p, 8, 8, N, cudaMemcpyDeviceToDevice, st));
+    CK(cudaMemcpy2DAsync(origin_xy + 1, 16, c->oy.p, 8, 8, N, cudaMemcpyDeviceToDevice, st));
+  }
+  if (heading) CK(cudaMemcpyAsync(heading, c->oh.p, 8 * N, cudaMemcpyDeviceToDevice, st));
+  return NV_OK;
+}
+
+int nv_raycast(nv_ctx *c, const double *ox, const double *oy, const double *dirx,
+               const double *diry, int64_t m, double t_max, int brute, double *t_out,
+               int64_t *idx_out, void *stream) {
+  if (!c) return fail(NV_ERR_ARG, "ctx is NULL");
+  TRY(ensure_scene(c));
+  if (m < 0) return fail(NV_ERR_ARG, "m < 0");
+  if (m == 0) return NV_OK;
+  nvk::k_raycast<<<blocks_for(m, 128), 128, 0, (cudaStream_t)stream>>>(
+      c->scene_view(), ox, oy, dirx, diry, m, t_max, brute, t_out, idx_out);
+  return check_launch(c);
+}
+
+int nv_fill_frames(nv_ctx *c, int cam, int64_t n, const double *t_col, const int64_t *i_col,
+                   const double *dirx, const double *diry, double sensor_height, uint8_t *rgb,
+                   float *depth, uint16_t *sem, void *stream) {
+  if (!c) return fail(NV_ERR_ARG, "ctx is NULL");
+  TRY(ensure_scene(c));
+  if (cam < 0 || cam >= 8 || !c->cams[cam].on) return fail(NV_ERR_STATE, "camera %d not configured", cam);
+  if (n <= 0) return NV_OK;
+  if (sensor_height > c->wall_h) return fail(NV_ERR_ARG, "sensor height must stay below wall height");
+  Camera &k = c->cams[cam];
+  cudaStream_t st = (cudaStream_t)stream;
+  if (k.tables_cam_h != sensor_height) {
+    CK(cudaStreamSynchronize(st));
+    TRY(build_camera_tables(c, k, sensor_height));
+  }
+  TRY(k.rec.alloc(sizeof(ColRec) * (size_t)n * k.W));
+  long long total = n * (long long)k.W;
+  nvk::k_cols_from_hits<<<blocks_for(total, 256), 256, 0, st>>>(
+      c->scene_view(), cam_view(k), total, t_col, i_col, dirx, diry, k.rec.as<ColRec>());
+  TRY(check_launch(c));
+  return launch_fill(c, k, n, rgb, depth, sem, st);
+}
+
+int nv_cast_disc(nv_ctx *c, const double *px, const double *py, const double *ux,
+                 const double *uy, const double *radius, int64_t m, double *t_out,
+                 int64_t *seg_out, double *tan_out, void *stream) {
+  if (!c) return fail(NV_ERR_ARG, "ctx is NULL");
+  TRY(ensure_scene(c));
+  if (m <= 0) return NV_OK;
+  nvk::k_cast_disc<<<blocks_for(m * 32, 128), 128, 0, (cudaStream_t)stream>>>(
+      c->scene_view(), px, py, ux, uy, radius, m, t_out, seg_out, tan_out);
+  return check_launch(c);
+}
+
+int nv_clearance(nv_ctx *c, const double *px, const double *py, int64_t m, double search_radius,
+                 double *out, void *stream) {
+  if (!c) return fail(NV_ERR_ARG, "ctx is NULL");
+  TRY(ensure_scene(c));
+  if (m <= 0) return NV_OK;
+  nvk::k_clearance<<<blocks_for(m * 32, 128), 128, 0, (cudaStream_t)stream>>>(
+      c->scene_view(), px, py, m, search_radius, out);
+  return check_launch(c);
+}
+
+void nv_host_sincos(double x, double *s, double *c) { nvx::sincos_cr(x, s, c); }
+double nv_host_hypot(double x, double y) { return nvx::hypot_cr(x, y); }
+
+int64_t nv_launch_count(nv_ctx *c) { return c ? c->launches : 0; }
+
+int nv_profile(nv_ctx *c, int enable) {
+  if (!c) return fail(NV_ERR_ARG, "ctx is NULL");
+  c->prof_on = enable != 0;
+  c->prof_used = 0;
+  for (int k = 0; k < 4; ++k) {
+    c->prof_ms[k] = 0.0;
+    c->prof_n[k] = 0;
+  }
+  return NV_OK;
+}
+
+int nv_profile_read(nv_ctx *c, double *ms, int64_t *counts) {
+  if (!c) return fail(NV_ERR_ARG, "ctx is NULL");
+  for (size_t p = 0; p < c->prof_used; ++p) {
+    CK(cudaEventSynchronize(c->prof_ev[2 * p + 1]));
+    float m = 0.0f;
+    CK(cudaEventElapsedTime(&m, c->prof_ev[2 * p], c->prof_ev[2 * p + 1]));
+    int k = c->prof_kind[p];
+    c->prof_ms[k] += m;
+    c->prof_n[k] += 1;
+  }
+  c->prof_used = 0;
+  for (int k = 0; k < 4; ++k) {
+    if (ms) ms[k] = c->prof_ms[k];
+    if (counts) counts[k] = c->prof_n[k];
+  }
+  return NV_OK;
+}
+
+}  // extern "C"
