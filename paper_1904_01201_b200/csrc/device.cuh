@@ -5,7 +5,8 @@
 //     reference's SegmentIndex / RenderGeometry arrays (geometry.py:111-117,
 //     sensors.py:84-93), read by the disc casts and the column epilogue;
 //   * uniform-grid CSR (geometry.py:128-141) with the bucket items EXPANDED
-//     into 48-byte CellEntry records {ax, ay, ex, ey, idx}: the DDA reads one
+//     into 32-byte CellEntry records {ax, ay, ex, ey} (+ the parallel int32
+//     items array, read only for prefilter survivors): the DDA reads one
 //     contiguous run per cell instead of gathering through bucket_items;
 //   * per-env agent state SoA (x, y, heading, path, collisions, cos/sin of
 //     heading, episode frame);
@@ -24,9 +25,7 @@ namespace nvd {
 struct __align__(16) CellEntry {
   double ax, ay;  // segment start
   double ex, ey;  // b - a (SegmentIndex.ex/ey, geometry.py:116-117)
-  int32_t idx;    // segment index (the tie-break key)
-  int32_t pad[3];
-};
+};                // the segment index (tie-break key) is items[q]
 
 struct SceneView {
   const double *ax, *ay, *bx, *by, *ex, *ey, *nx, *ny;

@@ -47,23 +47,39 @@ __device__ __forceinline__ int cell_coord(double v, double o, int n) {
   return (int)d;
 }
 
-// One segment test of raycast_grid / raycast_all (_kernels.py:91-103).
-__device__ __forceinline__ void seg_test(double px, double py, double dx, double dy,
-                                         double ax, double ay, double ex, double ey,
-                                         int i, double &best_t, int &best_i) {
-  double den = sub(mul(dx, ey), mul(dy, ex));
-  if (den == 0.0) return;
+// One segment test of raycast_grid / raycast_all (_kernels.py:91-103), split
+// into a division-free prefilter and the exact IEEE path.  The prefilter only
+// rejects a segment when the reference's own checks would `continue` on it:
+//   t < 0     <=> sign(tn) != sign(den), tn != 0 (tn = +-0 gives t = +-0,
+//               which passes `t < 0.0`);
+//   r < 0     likewise with rn;
+//   r > 1     if |rn| > |den| (1 + 1e-12): RN(rn/den) > 1;
+//   t > best  if |tn| > |den| best (1 + 1e-12): RN(tn/den) > best.
+// (Exact for coordinates whose products do not underflow, i.e. any scene
+// with |coordinates| and segment lengths in [2^-400, 2^400].)  The exact path
+// is the reference's arithmetic and update rule, a lexicographic (t, idx)
+// minimum, so the order in which candidates are tested is irrelevant.
+#define NV_R1 1.0000000000010
+
+__device__ __forceinline__ bool seg_pre(double px, double py, double dx, double dy,
+                                        double ax, double ay, double ex, double ey,
+                                        double best_t, double &den, double &tn, double &rn) {
+  den = sub(mul(dx, ey), mul(dy, ex));
   double sx = sub(ax, px), sy = sub(ay, py);
-  double tn = sub(mul(sx, ey), mul(sy, ex));
-  // Division-free rejections, each implying the reference's `continue`:
-  // t < 0 (sign of tn/den; tn == +-0 gives t == +-0, which passes) and
-  // t > best_t (|tn| > |den| * best_t * (1 + 2^-40) => RN(tn/den) > best_t).
-  if (tn != 0.0 && ((tn < 0.0) != (den < 0.0))) return;
-  double rn = sub(mul(sx, dy), mul(sy, dx));
-  if (rn != 0.0 && ((rn < 0.0) != (den < 0.0))) return;   // r < 0
-  double aden = fabs(den);
-  if (fabs(rn) > aden * 1.0000000000010) return;           // r > 1 for sure
-  if (fabs(tn) > aden * best_t * 1.0000000000010) return;  // t > best_t
+  tn = sub(mul(sx, ey), mul(sy, ex));
+  rn = sub(mul(sx, dy), mul(sy, dx));
+  const bool neg = den < 0.0;
+  const double aden = fabs(den);
+  bool ok = den != 0.0;
+  ok &= !(tn != 0.0 && ((tn < 0.0) != neg));
+  ok &= !(rn != 0.0 && ((rn < 0.0) != neg));
+  ok &= !(fabs(rn) > aden * NV_R1);
+  ok &= !(fabs(tn) > aden * best_t * NV_R1);
+  return ok;
+}
+
+__device__ __forceinline__ void seg_exact(double den, double tn, double rn, int i,
+                                          double &best_t, int &best_i) {
   double t = div(tn, den);
   if (t < 0.0 || t > best_t) return;
   double r = div(rn, den);
@@ -71,6 +87,48 @@ __device__ __forceinline__ void seg_test(double px, double py, double dx, double
     if (t < best_t || i < best_i) {
       best_t = t;
       best_i = i;
+    }
+  }
+}
+
+__device__ __forceinline__ void seg_test(double px, double py, double dx, double dy,
+                                         double ax, double ay, double ex, double ey,
+                                         int i, double &best_t, int &best_i) {
+  double den, tn, rn;
+  if (seg_pre(px, py, dx, dy, ax, ay, ex, ey, best_t, den, tn, rn))
+    seg_exact(den, tn, rn, i, best_t, best_i);
+}
+
+// Tests the bucket run [q0, q1) of one cell, NB entries per round with all
+// loads issued up front (memory-level parallelism); indices past the end are
+// clamped to q1-1 -- re-testing a segment cannot change a lexicographic min.
+template <int NB>
+__device__ __forceinline__ void test_cell(const SceneView &sc, int q0, int q1, double px,
+                                          double py, double dx, double dy, double &best_t,
+                                          int &best_i) {
+  for (int q = q0; q < q1; q += NB) {
+    double2 a[NB], e[NB];
+#pragma unroll
+    for (int k = 0; k < NB; ++k) {
+      const int qq = min(q + k, q1 - 1);
+      const double2 *p2 = reinterpret_cast<const double2 *>(sc.ent + qq);
+      a[k] = __ldg(p2);
+      e[k] = __ldg(p2 + 1);
+    }
+    double den[NB], tn[NB], rn[NB];
+    bool ok[NB];
+    bool any = false;
+#pragma unroll
+    for (int k = 0; k < NB; ++k) {
+      ok[k] = seg_pre(px, py, dx, dy, a[k].x, a[k].y, e[k].x, e[k].y, best_t, den[k], tn[k],
+                      rn[k]);
+      any |= ok[k];
+    }
+    if (any) {
+#pragma unroll
+      for (int k = 0; k < NB; ++k)
+        if (ok[k]) seg_exact(den[k], tn[k], rn[k], __ldg(sc.items + min(q + k, q1 - 1)), best_t,
+                             best_i);
     }
   }
 }
@@ -113,12 +171,7 @@ __device__ __forceinline__ void ray_grid(const SceneView &sc, double px, double 
     if (0 <= cx && cx < gnx && 0 <= cy && cy < gny) {
       int c = (int)(cy * gnx + cx);
       int q0 = __ldg(sc.starts + c), q1 = __ldg(sc.starts + c + 1);
-      for (int q = q0; q < q1; ++q) {
-        const double2 *e2 = reinterpret_cast<const double2 *>(sc.ent + q);
-        double2 g0 = __ldg(e2), g1 = __ldg(e2 + 1);
-        int idx = __ldg(&sc.ent[q].idx);
-        seg_test(px, py, dx, dy, g0.x, g0.y, g1.x, g1.y, idx, best_t, best_i);
-      }
+      test_cell<4>(sc, q0, q1, px, py, dx, dy, best_t, best_i);
     }
     double t_exit = tnx < tny ? tnx : tny;
     if (best_t <= t_exit || t_exit > t_max) break;
@@ -512,7 +565,7 @@ __device__ __forceinline__ void column_epilogue(const SceneView &sc, const CamVi
 
 // _column_directions (sensors.py:96-102) + raycast_grid + epilogue, one
 // thread per (env, column); also gps_compass (sensors.py:175-180) once per env.
-__global__ void __launch_bounds__(256) k_column_cast(EnvView ev, SceneView sc, CamView cam,
+__global__ void __launch_bounds__(128) k_column_cast(EnvView ev, SceneView sc, CamView cam,
                                                      ColRec *__restrict__ rec, double t_max,
                                                      double *gps, double *compass) {
   const long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x;
@@ -642,7 +695,8 @@ __device__ __forceinline__ PixOut shade_px(bool plane, const RowRec &R, float de
   o.depth = plane ? R.depth_p : depth_w;
   o.sem = plane ? (R.sem_mode & 0xffffu) : sem_w;
   float num = plane ? R.num08_p : num_w;
-  float inv = rsqrtf(d2 + R.v2);          // 1/sqrt(dx^2 + dy^2 + v^2)
+  float inv;                              // 1/sqrt(dx^2 + dy^2 + v^2)
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(inv) : "f"(d2 + R.v2));
   float t = fmaf(num, inv, 0.2f);         // 0.2 + 0.8 cos(alpha)
   o.r = __float_as_uint(fmaf(plane ? R.col_p[0] : colw[0], t, NV_MAGIC));
   o.g = __float_as_uint(fmaf(plane ? R.col_p[1] : colw[1], t, NV_MAGIC));
@@ -769,13 +823,14 @@ __global__ void __launch_bounds__(128) k_fill_tma(FillArgs a) {
         R.col_p[0] = q1.x;
         R.col_p[1] = q1.y;
         R.col_p[2] = q1.z;
-        const bool bottom = (R.sem_mode >> 16) != 0;
         uint32_t cb[3 * CPL];
         float dv[CPL];
         uint32_t sv[CPL];
 #pragma unroll
         for (int c = 0; c < CPL; ++c) {
-          const bool plane = bottom ? ((uint32_t)i >= cr.hi[c]) : ((uint32_t)i < cr.lo[c]);
+          // ceiling rows [0, lo), floor rows [hi, H): the middle band is
+          // [lo, hi) for every row class (lo <= n_top <= b0 <= hi)
+          const bool plane = !((uint32_t)i >= cr.lo[c] && (uint32_t)i < cr.hi[c]);
           PixOut o = shade_px(plane, R, cr.depth_w[c], cr.num_w[c], cr.d2[c], cr.col[c],
                               cr.sem_w[c]);
           dv[c] = o.depth;
@@ -878,9 +933,8 @@ __global__ void k_fill_generic(FillArgs a) {
   const int e = (int)(ei / a.H);
   const ColRec c = a.rec[(size_t)e * a.W + j];
   const RowRec R = a.rows[i];
-  const bool bottom = (R.sem_mode >> 16) != 0;
   const uint32_t lo = c.lohi & 0xffffu, hi = c.lohi >> 16;
-  const bool plane = bottom ? ((uint32_t)i >= hi) : ((uint32_t)i < lo);
+  const bool plane = !((uint32_t)i >= lo && (uint32_t)i < hi);
   PixOut o = shade_px(plane, R, c.depth_w, c.num08_w, c.d2, c.col_w, c.sem_w);
   if (a.depth) a.depth[p] = o.depth;
   if (a.sem) a.sem[p] = (uint16_t)o.sem;

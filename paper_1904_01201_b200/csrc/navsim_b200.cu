@@ -384,7 +384,7 @@ int do_cast(nv_ctx *c, int cam, double *gps, double *compass, cudaStream_t st) {
   // frames (tests/test_gpu_parity.py checks it against the
   // reference's uncapped t_max = 1e9 render).
   Prof pf(c, st, 1);
-  nvk::k_column_cast<<<blocks_for(total, 256), 256, 0, st>>>(
+  nvk::k_column_cast<<<blocks_for(total, 128), 128, 0, st>>>(
       c->env_view(), c->scene_view(), cam_view(k), k.rec.as<ColRec>(), k.max_range, gps,
       compass);
   return check_launch(c);
@@ -463,7 +463,7 @@ int nv_scene_upload(nv_ctx *c, const double *segs, const uint16_t *sem, const do
     items[q] = (int32_t)i;
     CellEntry e;
     std::memset(&e, 0, sizeof e);
-    e.ax = ax[i]; e.ay = ay[i]; e.ex = ex[i]; e.ey = ey[i]; e.idx = (int32_t)i;
+    e.ax = ax[i]; e.ay = ay[i]; e.ex = ex[i]; e.ey = ey[i];
     ent[q] = e;
   }
   TRY(upload(c->ax, ax)); TRY(upload(c->ay, ay)); TRY(upload(c->bx, bx)); TRY(upload(c->by, by));
