@@ -34,6 +34,8 @@ struct SceneView {
   const int32_t *starts; // nc + 1
   const CellEntry *ent;  // starts[nc] entries
   const int32_t *items;  // same order, index only (disc casts)
+  const float4 *entf;    // same order, f32 endpoints (a - X0c, b - X0c), X0c = x0 + cx
+  const float *cellb;    // per cell: max |endpoint - X0c|_1 over its items
   double x0, y0;
   int gnx, gny;
   int64_t n;
@@ -49,14 +51,16 @@ struct EnvView {
   int n;
 };
 
-// Per-row shading record (fill kernel), 32 B.
+// Per-row shading record (fill kernel), 32 B.  Plane (floor / ceiling)
+// parameters of the row, void-substituted when the plane depth >= max_range;
+// colour/shading values are f16 pairs splatted over both halves so the fill
+// kernel can blend them with per-pixel wall values two pixels at a time.
 struct __align__(16) RowRec {
-  float depth_p;  // plane depth (tc / tf, or max_range when void)
-  float num08_p;  // 0.8 * |v| (0 when void)
-  float v2;       // v*v
-  uint32_t sem_mode;  // plane semantic | mode << 16 (0: top/mid, 1: bottom)
-  float col_p[3];     // plane colour * 255 (0 when void)
-  float pad;
+  float depth_p;  // plane depth (tc / tf), or max_range when void
+  uint32_t sem2;  // plane semantic, splatted (s | s << 16)
+  uint32_t num2;  // half2 splat of 0.8 * |v| (0 when void)
+  uint32_t r2, g2, b2;  // half2 splats of the plane colour * 255 (0 when void)
+  uint32_t pad[2];
 };
 
 // Per-column record (cast -> fill), 32 B.
@@ -78,6 +82,7 @@ struct CamView {
   const double *tc;  // H: (wall_h - cam_h) / v for v > 0 rows
   const double *tf;  // H: -cam_h / v for v < 0 rows
   const RowRec *rows;
+  const uint16_t *inv;  // H x W f16: 1/sqrt(1 + u_j^2 + v_i^2) (env-independent)
 };
 
 }  // namespace nvd

@@ -133,6 +133,67 @@ __device__ __forceinline__ void test_cell(const SceneView &sc, int q0, int q1, d
   }
 }
 
+// FP32 prefilter for one cell of the DDA (side test).  The ray's line
+// crosses segment [a, b] iff a and b are not strictly on the same side:
+// with s_a = d x (a - p) and s_b = d x (b - p), the reference's
+// r = rn/den = s_a / (s_a - s_b), so both s_a, s_b > 0 (or both < 0) means
+// r < 0 or r > 1 (or den == 0) and the reference skips the segment.
+// Entries are stored in f32 relative to the cell anchor (X0c, Y0c) =
+// (x0 + cx, y0 + cy); the ray origin is rebased to the same anchor in f64
+// and rounded once.  E = 2^-18 |d|_1 (A + |p_rel|_1) bounds the f32 error of
+// s_a, s_b (conversions, products, sums; ~8x over the worst case) and the
+// reference's own f64 rounding, so a segment is skipped only when it is
+// certain that the reference skips it.  Survivors -- the segments the ray's
+// line actually crosses, plus a hairline margin -- take the exact FP64 test,
+// so the result is bit-identical to the unfiltered DDA.
+#define NV_K32 0x1p-18f
+
+struct CellF {
+  float cp, E;  // d x p_rel, error bound
+};
+
+__device__ __forceinline__ CellF cell_f32(const SceneView &sc, int cx, int cy, int c, double px,
+                                          double py, float dxf, float dyf, float sd) {
+  const double X0 = add(sc.x0, (double)cx), Y0 = add(sc.y0, (double)cy);
+  const float pxr = (float)sub(px, X0), pyr = (float)sub(py, Y0);
+  CellF f;
+  f.cp = fmaf(dxf, pyr, -(dyf * pxr));
+  f.E = NV_K32 * sd * (__ldg(sc.cellb + c) + fabsf(pxr) + fabsf(pyr) + 1e-30f);
+  return f;
+}
+
+// Tests the bucket run [q0, q1) of one cell: NB f32 side tests per round
+// (loads issued up front), then the exact FP64 test for the survivors.
+template <int NB>
+__device__ __forceinline__ void test_cell_f32(const SceneView &sc, int q0, int q1,
+                                              const CellF &cf, double px, double py, double dx,
+                                              double dy, float dxf, float dyf, double &best_t,
+                                              int &best_i) {
+  for (int q = q0; q < q1; q += NB) {
+    float4 e[NB];
+#pragma unroll
+    for (int k = 0; k < NB; ++k) e[k] = __ldg(sc.entf + min(q + k, q1 - 1));
+    unsigned keep = 0;
+#pragma unroll
+    for (int k = 0; k < NB; ++k) {
+      const float sa = fmaf(dxf, e[k].y, -(dyf * e[k].x)) - cf.cp;
+      const float sb = fmaf(dxf, e[k].w, -(dyf * e[k].z)) - cf.cp;
+      const bool skip = fminf(sa, sb) > cf.E || fmaxf(sa, sb) < -cf.E;
+      keep |= (skip ? 0u : 1u) << k;
+    }
+    while (keep) {
+      const int k = __ffs(keep) - 1;
+      keep &= keep - 1;
+      const int qq = min(q + k, q1 - 1);
+      const double2 *p2 = reinterpret_cast<const double2 *>(sc.ent + qq);
+      const double2 a2 = __ldg(p2), e2 = __ldg(p2 + 1);
+      double den, tn, rn;
+      if (seg_pre(px, py, dx, dy, a2.x, a2.y, e2.x, e2.y, best_t, den, tn, rn))
+        seg_exact(den, tn, rn, __ldg(sc.items + qq), best_t, best_i);
+    }
+  }
+}
+
 // raycast_grid (_kernels.py:51-120), one ray, exact replica of the DDA.
 __device__ __forceinline__ void ray_grid(const SceneView &sc, double px, double py,
                                          double dx, double dy, double t_max,
@@ -167,11 +228,16 @@ __device__ __forceinline__ void ray_grid(const SceneView &sc, double px, double 
     tdy = NV_INF;
   }
   const long long gnx = sc.gnx, gny = sc.gny;
+  const float dxf = (float)dx, dyf = (float)dy;
+  const float sd = (fabsf(dxf) + fabsf(dyf)) * (1.0f + 0x1p-20f);
   for (int guard = 0; guard < (1 << 24); ++guard) {
     if (0 <= cx && cx < gnx && 0 <= cy && cy < gny) {
       int c = (int)(cy * gnx + cx);
       int q0 = __ldg(sc.starts + c), q1 = __ldg(sc.starts + c + 1);
-      test_cell<4>(sc, q0, q1, px, py, dx, dy, best_t, best_i);
+      if (q1 > q0) {
+        const CellF cf = cell_f32(sc, (int)cx, (int)cy, c, px, py, dxf, dyf, sd);
+        test_cell_f32<4>(sc, q0, q1, cf, px, py, dx, dy, dxf, dyf, best_t, best_i);
+      }
     }
     double t_exit = tnx < tny ? tnx : tny;
     if (best_t <= t_exit || t_exit > t_max) break;
@@ -665,11 +731,26 @@ __global__ void __launch_bounds__(128) k_clearance(SceneView sc, const double *p
 
 // ------------------------------------------------------------ frame fill
 
-#define NV_MAGIC 12582912.0f  // 1.5 * 2^23: low mantissa byte = round(x)
+// ---- fill: packed-f16 shading --------------------------------------------
+//
+// Per pixel (fill_frame, _kernels.py:171-207): the pixel is a plane pixel
+// (ceiling rows [0, lo), floor rows [hi, H)) or a middle-band pixel (wall, or
+// void when s >= max_range); lo/hi were classified exactly in FP64 by the
+// column epilogue.  Depth (f32) and semantic (u16) are selected exactly.  RGB
+// is shaded in f16 pairs, two pixels per instruction:
+//   t   = 0.2 + (0.8 cos-numerator) * inv      inv = 1/|(d, v)| from a table
+//   c8  = round(col255 * t)                    via HFMA2(col255, t, 1024): the
+//                                              low byte of the f16 result
+// Worst-case error vs the reference's f64 rgb: 0.5 (rounding) + 0.0625 (f16
+// col255) + 255 * 1e-3 (t) < 0.85 of one 8-bit step (tolerance: 1 step).
+
+#define NV_H2_POINT2 0x32663266u   // (0.2, 0.2) in f16
+#define NV_H2_1024 0x64006400u     // (1024, 1024): low byte of 1024+x = round(x)
 
 struct FillArgs {
   const ColRec *rec;
   const RowRec *rows;
+  const uint16_t *inv;  // H x W f16 shading table
   int N, W, H;
   uint8_t *rgb;
   float *depth;
@@ -681,33 +762,19 @@ struct FillArgs {
   unsigned int *ctr;   // [0] next unit, [1] finished warps (self-resetting)
 };
 
-// One pixel of fill_frame (_kernels.py:141-207) given its plane/middle class.
-struct PixOut {
-  float depth;
-  uint32_t sem;
-  uint32_t r, g, b;  // float bits, low byte = channel value
-};
-
-__device__ __forceinline__ PixOut shade_px(bool plane, const RowRec &R, float depth_w,
-                                           float num_w, float d2, const float *colw,
-                                           uint32_t sem_w) {
-  PixOut o;
-  o.depth = plane ? R.depth_p : depth_w;
-  o.sem = plane ? (R.sem_mode & 0xffffu) : sem_w;
-  float num = plane ? R.num08_p : num_w;
-  float inv;                              // 1/sqrt(dx^2 + dy^2 + v^2)
-  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(inv) : "f"(d2 + R.v2));
-  float t = fmaf(num, inv, 0.2f);         // 0.2 + 0.8 cos(alpha)
-  o.r = __float_as_uint(fmaf(plane ? R.col_p[0] : colw[0], t, NV_MAGIC));
-  o.g = __float_as_uint(fmaf(plane ? R.col_p[1] : colw[1], t, NV_MAGIC));
-  o.b = __float_as_uint(fmaf(plane ? R.col_p[2] : colw[2], t, NV_MAGIC));
-  return o;
+__device__ __forceinline__ uint32_t h2_fma(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t d;
+  asm("fma.rn.f16x2 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
 }
-
-__device__ __forceinline__ uint32_t pack4(uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
-  uint32_t lo = __byte_perm(a, b, 0x0040);
-  uint32_t hi = __byte_perm(c, d, 0x0040);
-  return __byte_perm(lo, hi, 0x5410);
+__device__ __forceinline__ uint32_t h2_pack(float lo, float hi) {
+  uint32_t d;
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(d) : "f"(hi), "f"(lo));
+  return d;
+}
+// (a & m) | (b & ~m): per-half select with a 0xFFFF-granular mask
+__device__ __forceinline__ uint32_t sel_mask(uint32_t a, uint32_t b, uint32_t m) {
+  return (a & m) | (b & ~m);
 }
 
 __device__ __forceinline__ unsigned smem_addr(const void *p) {
@@ -741,16 +808,95 @@ __device__ __forceinline__ uint64_t policy_evict_first() {
   return p;
 }
 
+// A lane's CPL columns (CPL/2 pixel pairs) in registers, packed.
 template <int CPL>
 struct ColRegs {
-  float depth_w[CPL], num_w[CPL], d2[CPL], col[CPL][3];
-  uint32_t lo[CPL], hi[CPL], sem_w[CPL];
+  float dw[CPL];                 // wall depth (or max_range)
+  uint32_t lo[CPL], hi[CPL];     // plane rows: i < lo or i >= hi
+  uint32_t nw[CPL / 2], rw[CPL / 2], gw[CPL / 2], bw[CPL / 2];  // f16 pairs
+  uint32_t sw[CPL / 2];          // semantic pairs
 };
+
+template <int CPL>
+__device__ __forceinline__ void load_cols(const ColRec *rp, ColRegs<CPL> &cr) {
+#pragma unroll
+  for (int k = 0; k < CPL / 2; ++k) {
+    const float4 *q = reinterpret_cast<const float4 *>(rp + 2 * k);
+    float4 a0 = __ldg(q), a1 = __ldg(q + 1), b0 = __ldg(q + 2), b1 = __ldg(q + 3);
+    cr.dw[2 * k] = a0.x;
+    cr.dw[2 * k + 1] = b0.x;
+    uint32_t l0 = __float_as_uint(a0.w), l1 = __float_as_uint(b0.w);
+    cr.lo[2 * k] = l0 & 0xffffu;
+    cr.hi[2 * k] = l0 >> 16;
+    cr.lo[2 * k + 1] = l1 & 0xffffu;
+    cr.hi[2 * k + 1] = l1 >> 16;
+    cr.nw[k] = h2_pack(a0.y, b0.y);
+    cr.rw[k] = h2_pack(a1.x, b1.x);
+    cr.gw[k] = h2_pack(a1.y, b1.y);
+    cr.bw[k] = h2_pack(a1.z, b1.z);
+    cr.sw[k] = (__float_as_uint(a1.w) & 0xffffu) | (__float_as_uint(b1.w) << 16);
+  }
+}
+
+// Shade one pixel pair (columns 2k, 2k+1 of the lane) of row i.
+struct PairOut {
+  uint32_t r, g, b, s;  // f16 pairs (low byte of each half = value), sem pair
+  float d0, d1;
+};
+
+__device__ __forceinline__ PairOut shade_pair(uint32_t i, const RowRec &R, uint32_t lo0,
+                                              uint32_t hi0, uint32_t lo1, uint32_t hi1, float dw0,
+                                              float dw1, uint32_t nw, uint32_t rw, uint32_t gw,
+                                              uint32_t bw, uint32_t sw, uint32_t inv2) {
+  const bool in0 = i >= lo0 && i < hi0;  // middle band (wall / void)
+  const bool in1 = i >= lo1 && i < hi1;
+  const uint32_t m = (in0 ? 0x0000ffffu : 0u) | (in1 ? 0xffff0000u : 0u);
+  PairOut o;
+  o.d0 = in0 ? dw0 : R.depth_p;
+  o.d1 = in1 ? dw1 : R.depth_p;
+  o.s = sel_mask(sw, R.sem2, m);
+  const uint32_t num = sel_mask(nw, R.num2, m);
+  const uint32_t t = h2_fma(num, inv2, NV_H2_POINT2);
+  o.r = h2_fma(sel_mask(rw, R.r2, m), t, NV_H2_1024);
+  o.g = h2_fma(sel_mask(gw, R.g2, m), t, NV_H2_1024);
+  o.b = h2_fma(sel_mask(bw, R.b2, m), t, NV_H2_1024);
+  return o;
+}
+
+// Two pixel pairs (4 pixels) -> 12 interleaved RGB bytes (3 words).
+__device__ __forceinline__ void pack_rgb4(const PairOut &p, const PairOut &q, uint32_t &w0,
+                                          uint32_t &w1, uint32_t &w2) {
+  const uint32_t rg0 = __byte_perm(p.r, p.g, 0x6240);  // r0 g0 r1 g1
+  const uint32_t rg1 = __byte_perm(q.r, q.g, 0x6240);  // r2 g2 r3 g3
+  w0 = __byte_perm(rg0, p.b, 0x2410);                  // r0 g0 b0 r1
+  const uint32_t t = __byte_perm(rg0, p.b, 0x3263);    // g1 b1 . .
+  w1 = __byte_perm(t, rg1, 0x5410);                    // g1 b1 r2 g2
+  w2 = __byte_perm(rg1, q.b, 0x6324);                  // b2 r3 g3 b3
+}
+
+// Row record + this lane's CPL shading-table entries of row i.
+template <int CPL>
+__device__ __forceinline__ void load_row(const FillArgs &a, uint32_t i, int col0, uint4 &q0,
+                                         uint4 &q1, uint32_t (&iv)[CPL / 2]) {
+  const uint4 *rq = reinterpret_cast<const uint4 *>(a.rows + i);
+  q0 = __ldg(rq);
+  q1 = __ldg(rq + 1);
+  const uint16_t *ip = a.inv + (size_t)i * a.W + col0;
+  if constexpr (CPL == 8) {
+    uint4 v = __ldg(reinterpret_cast<const uint4 *>(ip));
+    iv[0] = v.x; iv[1] = v.y; iv[2] = v.z; iv[3] = v.w;
+  } else if constexpr (CPL == 4) {
+    uint2 v = __ldg(reinterpret_cast<const uint2 *>(ip));
+    iv[0] = v.x; iv[1] = v.y;
+  } else {
+    iv[0] = __ldg(reinterpret_cast<const uint32_t *>(ip));
+  }
+}
 
 // k_fill_tma: streaming frame writer.  A warp owns a unit = (env, column
 // segment of 32*CPL columns, rows_per_unit rows); it keeps its CPL columns'
-// ColRecs in registers, renders RW rows at a time into a private smem stage
-// laid out exactly like global memory, and lane 0 stores the stage with
+// parameters in registers, renders RW rows at a time into a private smem
+// stage laid out exactly like global memory, and lane 0 stores the stage with
 // cp.async.bulk (one copy per channel per stage when a warp covers full rows).
 // NS = 2 stages per warp; units are pulled from a self-resetting counter.
 template <int CPL, int RW>
@@ -783,27 +929,16 @@ __global__ void __launch_bounds__(128) k_fill_tma(FillArgs a) {
     const int gidx = (int)(u - es * a.units_per_seg);
     const int env = (int)(es / a.segs_per_row);
     const int seg = (int)(es - (long long)env * a.segs_per_row);
+    const int col0 = seg * SEGW + lane * CPL;
     if (es != cur_es) {
       cur_es = es;
-      const ColRec *rp = a.rec + (size_t)env * W + seg * SEGW + lane * CPL;
-#pragma unroll
-      for (int c = 0; c < CPL; ++c) {
-        const float4 *q = reinterpret_cast<const float4 *>(rp + c);
-        float4 v0 = __ldg(q), v1 = __ldg(q + 1);
-        cr.depth_w[c] = v0.x;
-        cr.num_w[c] = v0.y;
-        cr.d2[c] = v0.z;
-        uint32_t lh = __float_as_uint(v0.w);
-        cr.lo[c] = lh & 0xffffu;
-        cr.hi[c] = lh >> 16;
-        cr.col[c][0] = v1.x;
-        cr.col[c][1] = v1.y;
-        cr.col[c][2] = v1.z;
-        cr.sem_w[c] = __float_as_uint(v1.w);
-      }
+      load_cols<CPL>(a.rec + (size_t)env * W + col0, cr);
     }
     const int r_begin = gidx * a.rows_per_unit;
     const int r_end = min(H, r_begin + a.rows_per_unit);
+    uint4 pq0, pq1;
+    uint32_t piv[CPL / 2];
+    load_row<CPL>(a, (uint32_t)r_begin, col0, pq0, pq1, piv);
     for (int r0 = r_begin; r0 < r_end; r0 += RW) {
       const int nr = min(RW, r_end - r0);
       uint8_t *buf = wbase + (k & (NS - 1)) * stage_bytes;
@@ -812,45 +947,40 @@ __global__ void __launch_bounds__(128) k_fill_tma(FillArgs a) {
         __syncwarp();
       }
       for (int rr = 0; rr < nr; ++rr) {
-        const int i = r0 + rr;
-        const float4 *rq = reinterpret_cast<const float4 *>(a.rows + i);
-        float4 q0 = __ldg(rq), q1 = __ldg(rq + 1);
+        const uint32_t i = (uint32_t)(r0 + rr);
+        // this row's loads were issued one row ahead (software pipelining)
         RowRec R;
-        R.depth_p = q0.x;
-        R.num08_p = q0.y;
-        R.v2 = q0.z;
-        R.sem_mode = __float_as_uint(q0.w);
-        R.col_p[0] = q1.x;
-        R.col_p[1] = q1.y;
-        R.col_p[2] = q1.z;
-        uint32_t cb[3 * CPL];
-        float dv[CPL];
-        uint32_t sv[CPL];
+        R.depth_p = __uint_as_float(pq0.x);
+        R.sem2 = pq0.y;
+        R.num2 = pq0.z;
+        R.r2 = pq0.w;
+        R.g2 = pq1.x;
+        R.b2 = pq1.y;
+        uint32_t iv[CPL / 2];
 #pragma unroll
-        for (int c = 0; c < CPL; ++c) {
-          // ceiling rows [0, lo), floor rows [hi, H): the middle band is
-          // [lo, hi) for every row class (lo <= n_top <= b0 <= hi)
-          const bool plane = !((uint32_t)i >= cr.lo[c] && (uint32_t)i < cr.hi[c]);
-          PixOut o = shade_px(plane, R, cr.depth_w[c], cr.num_w[c], cr.d2[c], cr.col[c],
-                              cr.sem_w[c]);
-          dv[c] = o.depth;
-          sv[c] = o.sem;
-          cb[3 * c] = o.r;
-          cb[3 * c + 1] = o.g;
-          cb[3 * c + 2] = o.b;
+        for (int c = 0; c < CPL / 2; ++c) iv[c] = piv[c];
+        {
+          const uint32_t inext = min(i + 1, (uint32_t)(r_end - 1));
+          load_row<CPL>(a, inext, col0, pq0, pq1, piv);
         }
+        PairOut po[CPL / 2];
+#pragma unroll
+        for (int c = 0; c < CPL / 2; ++c)
+          po[c] = shade_pair(i, R, cr.lo[2 * c], cr.hi[2 * c], cr.lo[2 * c + 1],
+                             cr.hi[2 * c + 1], cr.dw[2 * c], cr.dw[2 * c + 1], cr.nw[c], cr.rw[c],
+                             cr.gw[c], cr.bw[c], cr.sw[c], iv[c]);
         if (want_rgb) {
           uint8_t *dst = buf + (rr * SEGW + lane * CPL) * 3;
           if constexpr (CPL == 2) {
-#pragma unroll
-            for (int q = 0; q < 3; ++q)
-              reinterpret_cast<uint16_t *>(dst)[q] =
-                  (uint16_t)__byte_perm(cb[2 * q], cb[2 * q + 1], 0x0040);
+            uint16_t *d16 = reinterpret_cast<uint16_t *>(dst);
+            d16[0] = (uint16_t)__byte_perm(po[0].r, po[0].g, 0x0040);  // r0 g0
+            d16[1] = (uint16_t)__byte_perm(po[0].b, po[0].r, 0x0060);  // b0 r1
+            d16[2] = (uint16_t)__byte_perm(po[0].g, po[0].b, 0x0062);  // g1 b1
           } else {
             uint32_t w[3 * CPL / 4];
 #pragma unroll
-            for (int q = 0; q < 3 * CPL / 4; ++q)
-              w[q] = pack4(cb[4 * q], cb[4 * q + 1], cb[4 * q + 2], cb[4 * q + 3]);
+            for (int q = 0; q < CPL / 4; ++q)
+              pack_rgb4(po[2 * q], po[2 * q + 1], w[3 * q], w[3 * q + 1], w[3 * q + 2]);
             if constexpr (CPL == 4) {
 #pragma unroll
               for (int q = 0; q < 3; ++q) reinterpret_cast<uint32_t *>(dst)[q] = w[q];
@@ -864,25 +994,22 @@ __global__ void __launch_bounds__(128) k_fill_tma(FillArgs a) {
         if (want_d) {
           float *dst = reinterpret_cast<float *>(buf + off_d) + rr * SEGW + lane * CPL;
           if constexpr (CPL == 2) {
-            *reinterpret_cast<float2 *>(dst) = make_float2(dv[0], dv[1]);
+            *reinterpret_cast<float2 *>(dst) = make_float2(po[0].d0, po[0].d1);
           } else {
 #pragma unroll
             for (int q = 0; q < CPL / 4; ++q)
               reinterpret_cast<float4 *>(dst)[q] =
-                  make_float4(dv[4 * q], dv[4 * q + 1], dv[4 * q + 2], dv[4 * q + 3]);
+                  make_float4(po[2 * q].d0, po[2 * q].d1, po[2 * q + 1].d0, po[2 * q + 1].d1);
           }
         }
         if (want_s) {
           uint16_t *dst = reinterpret_cast<uint16_t *>(buf + off_s) + rr * SEGW + lane * CPL;
-          uint32_t pw[CPL / 2];
-#pragma unroll
-          for (int q = 0; q < CPL / 2; ++q) pw[q] = __byte_perm(sv[2 * q], sv[2 * q + 1], 0x5410);
           if constexpr (CPL == 2) {
-            *reinterpret_cast<uint32_t *>(dst) = pw[0];
+            *reinterpret_cast<uint32_t *>(dst) = po[0].s;
           } else if constexpr (CPL == 4) {
-            *reinterpret_cast<uint2 *>(dst) = make_uint2(pw[0], pw[1]);
+            *reinterpret_cast<uint2 *>(dst) = make_uint2(po[0].s, po[1].s);
           } else {
-            *reinterpret_cast<uint4 *>(dst) = make_uint4(pw[0], pw[1], pw[2], pw[3]);
+            *reinterpret_cast<uint4 *>(dst) = make_uint4(po[0].s, po[1].s, po[2].s, po[3].s);
           }
         }
       }
@@ -922,22 +1049,25 @@ __global__ void __launch_bounds__(128) k_fill_tma(FillArgs a) {
   }
 }
 
-// One thread per pixel, any W/H (also the reference-layout fallback).
+// One thread per pixel, any W/H; the same f16 arithmetic as k_fill_tma (one
+// half of each pair), so both paths produce identical frames.
 __global__ void k_fill_generic(FillArgs a) {
   const long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   const long long total = (long long)a.N * a.H * a.W;
   if (p >= total) return;
   const int j = (int)(p % a.W);
   const long long ei = p / a.W;
-  const int i = (int)(ei % a.H);
+  const uint32_t i = (uint32_t)(ei % a.H);
   const int e = (int)(ei / a.H);
   const ColRec c = a.rec[(size_t)e * a.W + j];
   const RowRec R = a.rows[i];
   const uint32_t lo = c.lohi & 0xffffu, hi = c.lohi >> 16;
-  const bool plane = !((uint32_t)i >= lo && (uint32_t)i < hi);
-  PixOut o = shade_px(plane, R, c.depth_w, c.num08_w, c.d2, c.col_w, c.sem_w);
-  if (a.depth) a.depth[p] = o.depth;
-  if (a.sem) a.sem[p] = (uint16_t)o.sem;
+  const uint32_t inv = a.inv[(size_t)i * a.W + j];
+  PairOut o = shade_pair(i, R, lo, hi, lo, hi, c.depth_w, c.depth_w, h2_pack(c.num08_w, 0.f),
+                         h2_pack(c.col_w[0], 0.f), h2_pack(c.col_w[1], 0.f),
+                         h2_pack(c.col_w[2], 0.f), c.sem_w & 0xffffu, inv);
+  if (a.depth) a.depth[p] = o.d0;
+  if (a.sem) a.sem[p] = (uint16_t)o.s;
   if (a.rgb) {
     a.rgb[3 * p] = (uint8_t)o.r;
     a.rgb[3 * p + 1] = (uint8_t)o.g;

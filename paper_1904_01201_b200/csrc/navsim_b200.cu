@@ -4,6 +4,7 @@
 // SegmentIndex.__init__ (geometry.py:109-141), expands bucket items into
 // contiguous CellEntry runs, and uploads everything once.  Per-step calls
 // only enqueue kernels on the caller's stream (no host synchronisation).
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -86,7 +87,7 @@ struct Camera {
   double focal = 0, max_range = 0;
   int n_top = 0, b0 = 0;
   double tables_cam_h = NAN;
-  DevBuf u, tc, tf, rows;
+  DevBuf u, tc, tf, rows, inv;
   DevBuf rec;      // ColRec N x W
   DevBuf ctr;      // fill scheduler counters
 };
@@ -105,7 +106,7 @@ struct nv_ctx {
   double gx0 = -0.5, gy0 = -0.5;
   int gnx = 1, gny = 1;
   int64_t nitems = 0;
-  DevBuf ax, ay, bx, by, ex, ey, nx, ny, sem, alb, starts, ent, items;
+  DevBuf ax, ay, bx, by, ex, ey, nx, ny, sem, alb, starts, ent, items, entf, cellb;
   // agent
   double radius = 0.1, step = 0.25, turn_rad = 0.17453292519943295, sensor_h = 1.5;
   // envs
@@ -133,6 +134,7 @@ struct nv_ctx {
     v.nx = nx.as<double>(); v.ny = ny.as<double>();
     v.sem = sem.as<uint16_t>(); v.alb255 = alb.as<float4>();
     v.starts = starts.as<int32_t>(); v.ent = ent.as<CellEntry>(); v.items = items.as<int32_t>();
+    v.entf = entf.as<float4>(); v.cellb = cellb.as<float>();
     v.x0 = gx0; v.y0 = gy0; v.gnx = gnx; v.gny = gny; v.n = n;
     return v;
   }
@@ -219,23 +221,32 @@ int ensure_envs(nv_ctx *c) {
   return NV_OK;
 }
 
+uint16_t f2h(float x) { return __half_as_ushort(__float2half_rn(x)); }
+uint32_t h2splat(float x) {
+  uint32_t h = f2h(x);
+  return h | (h << 16);
+}
+
 // Row tables for a camera (fill_frame's per-row quantities, _kernels.py:141,
-// 150, 158): v, tc, tf in exact f64 (host IEEE, no contraction), shading f32.
+// 150, 158): v, tc, tf in exact f64 (host IEEE, no contraction); the f16
+// shading table inv[i][j] = 1/sqrt(|d_j|^2 + v_i^2), |d_j|^2 = 1 + u_j^2
+// (column directions have unit forward component, sensors.py:96-102), is the
+// same for every env and heading.
 int build_camera_tables(nv_ctx *c, Camera &cam, double cam_h) {
   const int W = cam.W, H = cam.H;
-  std::vector<double> u(W), tc(H, 0.0), tf(H, 0.0);
+  std::vector<double> u(W), tc(H, 0.0), tf(H, 0.0), vv(H);
   for (int j = 0; j < W; ++j) u[j] = (((double)j + 0.5) - (double)W * 0.5) / cam.focal;
   std::vector<RowRec> rows(H);
   int n_top = 0, b0 = H;
   for (int i = 0; i < H; ++i) {
     double v = ((double)H * 0.5 - ((double)i + 0.5)) / cam.focal;
+    vv[i] = v;
     RowRec r;
     std::memset(&r, 0, sizeof r);
-    r.v2 = (float)v * (float)v;
     bool lit = false;
     double t = 0.0;
     const double *col = nullptr;
-    uint32_t sem = 0, mode = 0;
+    uint32_t sem = 0;
     if (v > 0.0) {
       n_top = i + 1;
       tc[i] = (c->wall_h - cam_h) / v;
@@ -250,25 +261,30 @@ int build_camera_tables(nv_ctx *c, Camera &cam, double cam_h) {
       lit = t < cam.max_range;
       col = c->floor3;
       sem = 65534;
-      mode = 1;
     }
     if (lit) {
       r.depth_p = (float)t;
-      r.num08_p = 0.8f * (float)std::fabs(v);
-      for (int k = 0; k < 3; ++k) r.col_p[k] = (float)(col[k] * 255.0);
-      r.sem_mode = sem | (mode << 16);
+      r.sem2 = sem | (sem << 16);
+      r.num2 = h2splat(0.8f * (float)std::fabs(v));
+      r.r2 = h2splat((float)(col[0] * 255.0));
+      r.g2 = h2splat((float)(col[1] * 255.0));
+      r.b2 = h2splat((float)(col[2] * 255.0));
     } else {
       r.depth_p = (float)cam.max_range;
-      r.sem_mode = mode << 16;
     }
     rows[i] = r;
   }
+  std::vector<uint16_t> inv((size_t)H * W);
+  for (int i = 0; i < H; ++i)
+    for (int j = 0; j < W; ++j)
+      inv[(size_t)i * W + j] = f2h((float)(1.0 / std::sqrt(1.0 + u[j] * u[j] + vv[i] * vv[i])));
   cam.n_top = n_top;
   cam.b0 = b0;
   TRY(upload(cam.u, u));
   TRY(upload(cam.tc, tc));
   TRY(upload(cam.tf, tf));
   TRY(upload(cam.rows, rows));
+  TRY(upload(cam.inv, inv));
   cam.tables_cam_h = cam_h;
   return NV_OK;
 }
@@ -278,6 +294,7 @@ CamView cam_view(const Camera &cam) {
   v.W = cam.W; v.H = cam.H; v.n_top = cam.n_top; v.b0 = cam.b0; v.max_range = cam.max_range;
   v.u = cam.u.as<double>(); v.tc = cam.tc.as<double>(); v.tf = cam.tf.as<double>();
   v.rows = cam.rows.as<RowRec>();
+  v.inv = cam.inv.as<uint16_t>();
   return v;
 }
 
@@ -353,6 +370,7 @@ int launch_fill(nv_ctx *c, Camera &cam, int64_t N, uint8_t *rgb, float *depth, u
   nvk::FillArgs a;
   a.rec = cam.rec.as<ColRec>();
   a.rows = cam.rows.as<RowRec>();
+  a.inv = cam.inv.as<uint16_t>();
   a.N = (int)N; a.W = cam.W; a.H = cam.H;
   a.rgb = rgb; a.depth = depth; a.sem = sem;
   a.ctr = cam.ctr.as<unsigned int>();
@@ -457,19 +475,35 @@ int nv_scene_upload(nv_ctx *c, const double *segs, const uint16_t *sem, const do
   }
   std::vector<int32_t> starts(g.starts.size()), items(g.items.size());
   std::vector<CellEntry> ent(g.items.size());
+  std::vector<float4> entf(g.items.size());
+  std::vector<float> cellb((size_t)(g.nx * g.ny), 0.f);
   for (size_t k = 0; k < g.starts.size(); ++k) starts[k] = (int32_t)g.starts[k];
-  for (size_t q = 0; q < g.items.size(); ++q) {
-    int64_t i = g.items[q];
-    items[q] = (int32_t)i;
-    CellEntry e;
-    std::memset(&e, 0, sizeof e);
-    e.ax = ax[i]; e.ay = ay[i]; e.ex = ex[i]; e.ey = ey[i];
-    ent[q] = e;
-  }
+  for (int64_t cy = 0; cy < g.ny; ++cy)
+    for (int64_t cx = 0; cx < g.nx; ++cx) {
+      const int64_t c = cy * g.nx + cx;
+      // cell anchor, the same IEEE sums the device forms (kernels.cuh cell_bounds)
+      const double X0 = g.x0 + (double)cx, Y0 = g.y0 + (double)cy;
+      float amax = 0.f;
+      for (int64_t q = g.starts[c]; q < g.starts[c + 1]; ++q) {
+        int64_t i = g.items[q];
+        items[q] = (int32_t)i;
+        CellEntry e;
+        e.ax = ax[i]; e.ay = ay[i]; e.ex = ex[i]; e.ey = ey[i];
+        ent[q] = e;
+        // endpoints a and a + e (the segment the reference's arithmetic tests)
+        float4 f = make_float4((float)(ax[i] - X0), (float)(ay[i] - Y0),
+                               (float)(ax[i] + ex[i] - X0), (float)(ay[i] + ey[i] - Y0));
+        entf[q] = f;
+        amax = std::max(amax, std::max(std::fabs(f.x) + std::fabs(f.y), std::fabs(f.z) + std::fabs(f.w)));
+      }
+      // 2^-20 relative slack covers the f32 rounding of the stored values
+      cellb[c] = amax * (1.0f + 0x1p-20f);
+    }
   TRY(upload(c->ax, ax)); TRY(upload(c->ay, ay)); TRY(upload(c->bx, bx)); TRY(upload(c->by, by));
   TRY(upload(c->ex, ex)); TRY(upload(c->ey, ey)); TRY(upload(c->nx, nx)); TRY(upload(c->ny, ny));
   TRY(upload(c->sem, sm)); TRY(upload(c->alb, alb));
   TRY(upload(c->starts, starts)); TRY(upload(c->items, items)); TRY(upload(c->ent, ent));
+  TRY(upload(c->entf, entf)); TRY(upload(c->cellb, cellb));
   c->n = n;
   c->wall_h = wall_height;
   for (int k = 0; k < 3; ++k) {

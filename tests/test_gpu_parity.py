@@ -264,3 +264,31 @@ def test_device_sincos_matches_host(nb):
         lib.nv_host_sincos(nb.wrap_angle(h), ctypes.byref(s), ctypes.byref(c))
         assert xy[e, 0] == 0.0 + 0.25 * c.value
         assert xy[e, 1] == 50.0 + 0.25 * s.value
+
+
+@pytest.mark.parametrize("cfg", ["C1", "C2", "C3"])
+def test_raycast_stress_vs_oracle(nb, oracle_mod, cfg):
+    """Random and adversarial rays (aimed exactly at segment endpoints, along
+    segments, axis-aligned) through the device DDA (f32 prefilter + exact
+    FP64 test) vs the oracle's raycast_grid: bit-identical (t, idx)."""
+    from paper_1904_01201_b200 import synth
+    sc = synth.config_scene(cfg)
+    osc = _oracle_scene(oracle_mod, sc)
+    idx = nb.SegmentIndex(sc.segments)
+    rng = np.random.default_rng(11)
+    poses = synth.sample_poses(sc, 24, seed=99)
+    segs = sc.segments
+    for (x, y, h) in poses:
+        th = rng.uniform(-math.pi, math.pi, 1024)
+        dirs = [np.stack([np.cos(th), np.sin(th)], 1)]
+        near = segs[np.argsort(np.hypot(segs[:, 0] - x, segs[:, 1] - y))[:256]]
+        dirs.append(near[:, 0:2] - [x, y])                  # exactly at endpoints a
+        dirs.append(near[:, 2:4] - [x, y])                  # exactly at endpoints b
+        dirs.append(near[:, 2:4] - near[:, 0:2])            # parallel to segments
+        dirs.append(np.array([[1, 0], [0, 1], [-1, 0], [0, -1], [1, 1], [-1, 1]], float))
+        d = np.concatenate(dirs)
+        for t_max in (1e9, 10.0):
+            tg, ig = idx.raycast((x, y), d, t_max=t_max)
+            to, io = osc.raycast((x, y), d, t_max=t_max)
+            assert np.array_equal(ig, io)
+            assert np.array_equal(tg, to)
