@@ -222,6 +222,7 @@ def run_gpu(args):
                          floor_color=sc.floor_color, ceiling_color=sc.ceiling_color, device=local)
     poses = synth.sample_poses(sc, shard.n_total, seed=1)[shard.lo:shard.hi]
     sim.reset(poses[:, :2], poses[:, 2])
+    nat.check(sim.ctx.lib.nv_set_fused(sim.ctx.handle, 1 if args.fused else 0))
     total_steps = args.warmup + args.steps
     acts = torch.as_tensor(synth.random_actions(shard.n_total, total_steps, seed=2)[:, shard.lo:shard.hi].copy(),
                            device=f"cuda:{local}")
@@ -293,10 +294,20 @@ def run_gpu(args):
     cnt = np.zeros(4, dtype=np.int64)
     nat.check(lib.nv_profile_read(h, nat.ptr(msk), nat.ptr(cnt)))
     nat.check(lib.nv_profile(h, 0))
-    per = {k: (msk[i] / max(1, cnt[i])) for i, k in enumerate(["agent_step", "column_cast", "frame_fill"])}
-    fill_bytes = shard.n_local * W * H * sum(BYTES_PER_PX[c] for c in chans)
+    names = ["agent_step", "column_cast", "frame_fill", "step_render_fused"]
+    per = {k: (msk[i] / cnt[i]) for i, k in enumerate(names) if cnt[i] > 0}
+    fused = "step_render_fused" in per
+    frame_bytes = shard.n_local * W * H * sum(BYTES_PER_PX[c] for c in chans)
+    # dominant kernel: the fused step+render megakernel (algorithmic bytes = the
+    # frames it writes + the per-env step I/O), else the frame fill
+    if fused:
+        dom, dom_bytes, dom_ms = ("k_step_render (fused agent step + column cast + frame fill)",
+                                  shard.n_local * bytes_per_env_step(W, H, chans),
+                                  per["step_render_fused"])
+    else:
+        dom, dom_bytes, dom_ms = "k_fill_tma (frame_fill)", frame_bytes, per["frame_fill"]
     peak, peak_src = measured_peaks()
-    achieved = fill_bytes / (per["frame_fill"] / 1e3) / 1e9
+    achieved = dom_bytes / (dom_ms / 1e3) / 1e9
     step_bytes = shard.n_local * bytes_per_env_step(W, H, chans)
     step_gbs = step_bytes / (ms_max / args.steps / 1e3) / 1e9
 
@@ -364,13 +375,13 @@ def run_gpu(args):
                        "envs_total": shard.n_total, "width": W, "height": H,
                        "channels": list(chans), "segments": sc.n_segments,
                        "triangles": sc.n_triangles, "parallelism": f"env-shard x{world}",
-                       "cuda_graph": use_graph,
+                       "cuda_graph": use_graph, "fused_megakernel": fused,
                        "l2": f"no flush: frames written per step "
                              f"({step_bytes / 1e6:.0f} MB/GPU) exceed the 126 MB L2"},
-            "roofline": {"bound": "hbm", "kernel": "k_fill_tma (frame_fill)",
+            "roofline": {"bound": "hbm", "kernel": dom,
                          "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": None, "peak_source": peak_src,
-                         "bytes_per_launch": fill_bytes,
+                         "bytes_per_launch": dom_bytes,
                          "kernel_ms": per,
                          "step_achieved_gbs": step_gbs, "step_frac": step_gbs / peak},
             "clocks": clk.summary(),
@@ -397,6 +408,7 @@ def main():
     ap.add_argument("--envs", type=int, default=0, help="override envs per GPU")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--fused", action="store_true", help="one megakernel launch per step (experimental)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)

@@ -111,11 +111,17 @@ int nv_step(nv_ctx *ctx, const int8_t *actions, uint8_t *collided,
 int nv_render(nv_ctx *ctx, int cam, uint8_t *rgb, float *depth, uint16_t *sem,
               double *gps, double *compass, void *stream);
 
-/* Fused step + render: one call per simulator step for all envs. */
+/* Fused step + render: one call per simulator step for all envs.  When the
+ * frame layout allows (W in {64, 128, 256k}, 16-byte aligned outputs) this is
+ * ONE persistent kernel launch (step, cast and fill tasks overlapped through
+ * a dependency-tracked queue); otherwise three launches. */
 int nv_step_render(nv_ctx *ctx, const int8_t *actions, int cam, uint8_t *rgb,
                    float *depth, uint16_t *sem, double *gps, double *compass,
                    uint8_t *collided, double *displacement, int32_t *status,
                    void *stream);
+
+/* Enable (default) / disable the single-launch megakernel of nv_step_render. */
+int nv_set_fused(nv_ctx *ctx, int on);
 
 /* End-to-end call over HOST buffers (the reference-facing path: host actions
  * in, host results out).  Copies actions (host, n i8) in, runs
@@ -191,7 +197,7 @@ int64_t nv_launch_count(nv_ctx *ctx);
 /* Per-kernel CUDA-event timing of the hot-path launches (bench roofline
  * evidence).  nv_profile(ctx, 1) clears and enables; nv_profile_read waits
  * for the recorded events and returns accumulated milliseconds and launch
- * counts for [agent_step, column_cast, frame_fill, other]. */
+ * counts for [agent_step, column_cast, frame_fill, step_render (fused)]. */
 int nv_profile(nv_ctx *ctx, int enable);
 int nv_profile_read(nv_ctx *ctx, double *ms4, int64_t *counts4);
 

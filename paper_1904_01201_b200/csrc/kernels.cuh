@@ -499,15 +499,12 @@ __device__ void warp_forward(const SceneView &sc, const AgentCfg &cfg, double &x
   collided = 1;
 }
 
-// Simulator.step (sim.py:202-219) for all envs: one warp per env.
-__global__ void __launch_bounds__(128) k_agent_step(EnvView ev, SceneView sc, AgentCfg cfg,
-                                                    const int8_t *__restrict__ actions,
-                                                    uint8_t *collided_out,
-                                                    double *disp_out, int32_t *status_out) {
-  const int e = (int)((blockIdx.x * (size_t)blockDim.x + threadIdx.x) >> 5);
+// Simulator.step (sim.py:202-219) for env e, executed by one warp.
+__device__ __forceinline__ void warp_agent_step(const EnvView &ev, const SceneView &sc,
+                                                const AgentCfg &cfg, int e, int a,
+                                                uint8_t *collided_out, double *disp_out,
+                                                int32_t *status_out) {
   const int lane = threadIdx.x & 31;
-  if (e >= ev.n) return;
-  const int a = actions[e];
   int status = 0, collided = 0;
   double moved = 0.0;
   if (!ev.reset[e]) {
@@ -539,6 +536,16 @@ __global__ void __launch_bounds__(128) k_agent_step(EnvView ev, SceneView sc, Ag
     if (disp_out) disp_out[e] = moved;
     if (status_out) status_out[e] = status;
   }
+}
+
+// Simulator.step for all envs: one warp per env.
+__global__ void __launch_bounds__(128) k_agent_step(EnvView ev, SceneView sc, AgentCfg cfg,
+                                                    const int8_t *__restrict__ actions,
+                                                    uint8_t *collided_out,
+                                                    double *disp_out, int32_t *status_out) {
+  const int e = (int)((blockIdx.x * (size_t)blockDim.x + threadIdx.x) >> 5);
+  if (e >= ev.n) return;
+  warp_agent_step(ev, sc, cfg, e, actions[e], collided_out, disp_out, status_out);
 }
 
 // Simulator.set_agent_state (sim.py:172-184), one warp per env.  Inputs are
@@ -629,17 +636,20 @@ __device__ __forceinline__ void column_epilogue(const SceneView &sc, const CamVi
   }
 }
 
-// _column_directions (sensors.py:96-102) + raycast_grid + epilogue, one
-// thread per (env, column); also gps_compass (sensors.py:175-180) once per env.
-__global__ void __launch_bounds__(128) k_column_cast(EnvView ev, SceneView sc, CamView cam,
-                                                     ColRec *__restrict__ rec, double t_max,
-                                                     double *gps, double *compass) {
-  const long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  const long long total = (long long)ev.n * cam.W;
-  if (g >= total) return;
-  const int e = (int)(g / cam.W);
-  const int j = (int)(g - (long long)e * cam.W);
-  const double px = ev.x[e], py = ev.y[e], c = ev.ch[e], s = ev.sh[e];
+// _column_directions (sensors.py:96-102) + raycast_grid + epilogue for one
+// (env, column); column 0 also writes gps_compass (sensors.py:175-180).
+// COH: agent state was written earlier in the same launch (megakernel), so it
+// is read through L2 (ld.global.cg) rather than the non-coherent path.
+template <bool COH>
+__device__ __forceinline__ void cast_column(const EnvView &ev, const SceneView &sc,
+                                            const CamView &cam, int e, int j, ColRec *rec,
+                                            double t_max, double *gps, double *compass) {
+  double px, py, c, s;
+  if (COH) {
+    px = __ldcg(ev.x + e); py = __ldcg(ev.y + e); c = __ldcg(ev.ch + e); s = __ldcg(ev.sh + e);
+  } else {
+    px = ev.x[e]; py = ev.y[e]; c = ev.ch[e]; s = ev.sh[e];
+  }
   const double u = __ldg(cam.u + j);
   const double dx = add(c, mul(u, s));
   const double dy = add(s, mul(u, -c));
@@ -648,7 +658,7 @@ __global__ void __launch_bounds__(128) k_column_cast(EnvView ev, SceneView sc, C
   ray_grid(sc, px, py, dx, dy, t_max, t, k);
   ColRec r;
   column_epilogue(sc, cam, t, k, dx, dy, r);
-  rec[g] = r;
+  rec[(size_t)e * cam.W + j] = r;
   if (j == 0 && (gps || compass)) {
     double ddx = sub(px, ev.ox[e]), ddy = sub(py, ev.oy[e]);
     double fc = ev.fc[e], fs = ev.fs[e];
@@ -656,8 +666,23 @@ __global__ void __launch_bounds__(128) k_column_cast(EnvView ev, SceneView sc, C
       gps[2 * e] = sub(mul(fc, ddx), mul(fs, ddy));
       gps[2 * e + 1] = add(mul(fs, ddx), mul(fc, ddy));
     }
-    if (compass) compass[e] = nvx::wrap_angle(sub(ev.h[e], ev.oh[e]));
+    if (compass) {
+      const double h = COH ? __ldcg(ev.h + e) : ev.h[e];
+      compass[e] = nvx::wrap_angle(sub(h, ev.oh[e]));
+    }
   }
+}
+
+// One thread per (env, column).
+__global__ void __launch_bounds__(128) k_column_cast(EnvView ev, SceneView sc, CamView cam,
+                                                     ColRec *__restrict__ rec, double t_max,
+                                                     double *gps, double *compass) {
+  const long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const long long total = (long long)ev.n * cam.W;
+  if (g >= total) return;
+  const int e = (int)(g / cam.W);
+  const int j = (int)(g - (long long)e * cam.W);
+  cast_column<false>(ev, sc, cam, e, j, rec, t_max, gps, compass);
 }
 
 // gps_compass (sensors.py:175-180) for all envs (no visual sensors case).
@@ -817,12 +842,17 @@ struct ColRegs {
   uint32_t sw[CPL / 2];          // semantic pairs
 };
 
-template <int CPL>
+template <int CPL, bool COH>
 __device__ __forceinline__ void load_cols(const ColRec *rp, ColRegs<CPL> &cr) {
 #pragma unroll
   for (int k = 0; k < CPL / 2; ++k) {
     const float4 *q = reinterpret_cast<const float4 *>(rp + 2 * k);
-    float4 a0 = __ldg(q), a1 = __ldg(q + 1), b0 = __ldg(q + 2), b1 = __ldg(q + 3);
+    float4 a0, a1, b0, b1;
+    if (COH) {  // written earlier in this launch: read through L2
+      a0 = __ldcg(q); a1 = __ldcg(q + 1); b0 = __ldcg(q + 2); b1 = __ldcg(q + 3);
+    } else {
+      a0 = __ldg(q); a1 = __ldg(q + 1); b0 = __ldg(q + 2); b1 = __ldg(q + 3);
+    }
     cr.dw[2 * k] = a0.x;
     cr.dw[2 * k + 1] = b0.x;
     uint32_t l0 = __float_as_uint(a0.w), l1 = __float_as_uint(b0.w);
@@ -893,160 +923,283 @@ __device__ __forceinline__ void load_row(const FillArgs &a, uint32_t i, int col0
   }
 }
 
-// k_fill_tma: streaming frame writer.  A warp owns a unit = (env, column
-// segment of 32*CPL columns, rows_per_unit rows); it keeps its CPL columns'
-// parameters in registers, renders RW rows at a time into a private smem
-// stage laid out exactly like global memory, and lane 0 stores the stage with
-// cp.async.bulk (one copy per channel per stage when a warp covers full rows).
-// NS = 2 stages per warp; units are pulled from a self-resetting counter.
+// Per-warp state of the streaming writer: a private ring of NS smem stages.
+template <int CPL, int RW>
+struct FillWarp {
+  static constexpr int NS = 2;
+  static constexpr int SEGW = 32 * CPL;
+  uint8_t *wbase;
+  int off_d, off_s, stage_bytes;
+  bool want_rgb, want_d, want_s;
+  uint64_t pol;
+  int k;  // stages issued so far
+  __device__ __forceinline__ void init(const FillArgs &a, uint8_t *smem, int wib) {
+    want_rgb = a.rgb != nullptr;
+    want_d = a.depth != nullptr;
+    want_s = a.sem != nullptr;
+    off_d = want_rgb ? RW * SEGW * 3 : 0;
+    off_s = off_d + (want_d ? RW * SEGW * 4 : 0);
+    stage_bytes = off_s + (want_s ? RW * SEGW * 2 : 0);
+    wbase = smem + (size_t)wib * NS * stage_bytes;
+    pol = policy_evict_first();
+    k = 0;
+  }
+};
+
+// Render one unit = (env, column segment of 32*CPL columns, rows
+// [gidx*rpu, ...)) of fill_frame: the lane's CPL columns' parameters sit in
+// registers; RW rows at a time are rendered into a smem stage laid out exactly
+// like global memory, which lane 0 writes out with cp.async.bulk (one copy
+// per channel per stage when a warp covers full rows), evict-first in L2.
+// COH: the column records were written earlier in the same launch.
+template <int CPL, int RW, bool COH>
+__device__ __forceinline__ void fill_unit(const FillArgs &a, FillWarp<CPL, RW> &fw, int env,
+                                          int seg, int gidx) {
+  constexpr int NS = FillWarp<CPL, RW>::NS;
+  constexpr int SEGW = FillWarp<CPL, RW>::SEGW;
+  const int lane = threadIdx.x & 31;
+  const int W = a.W, H = a.H;
+  const int col0 = seg * SEGW + lane * CPL;
+  ColRegs<CPL> cr;
+  load_cols<CPL, COH>(a.rec + (size_t)env * W + col0, cr);
+  const int r_begin = gidx * a.rows_per_unit;
+  const int r_end = min(H, r_begin + a.rows_per_unit);
+  uint4 pq0, pq1;
+  uint32_t piv[CPL / 2];
+  load_row<CPL>(a, (uint32_t)r_begin, col0, pq0, pq1, piv);
+  for (int r0 = r_begin; r0 < r_end; r0 += RW) {
+    const int nr = min(RW, r_end - r0);
+    uint8_t *buf = fw.wbase + (fw.k & (NS - 1)) * fw.stage_bytes;
+    if (fw.k >= NS) {
+      if (lane == 0) bulk_wait_read<NS - 1>();
+      __syncwarp();
+    }
+    for (int rr = 0; rr < nr; ++rr) {
+      const uint32_t i = (uint32_t)(r0 + rr);
+      // this row's loads were issued one row ahead (software pipelining)
+      RowRec R;
+      R.depth_p = __uint_as_float(pq0.x);
+      R.sem2 = pq0.y;
+      R.num2 = pq0.z;
+      R.r2 = pq0.w;
+      R.g2 = pq1.x;
+      R.b2 = pq1.y;
+      uint32_t iv[CPL / 2];
+#pragma unroll
+      for (int c = 0; c < CPL / 2; ++c) iv[c] = piv[c];
+      load_row<CPL>(a, min(i + 1, (uint32_t)(r_end - 1)), col0, pq0, pq1, piv);
+      PairOut po[CPL / 2];
+#pragma unroll
+      for (int c = 0; c < CPL / 2; ++c)
+        po[c] = shade_pair(i, R, cr.lo[2 * c], cr.hi[2 * c], cr.lo[2 * c + 1], cr.hi[2 * c + 1],
+                           cr.dw[2 * c], cr.dw[2 * c + 1], cr.nw[c], cr.rw[c], cr.gw[c], cr.bw[c],
+                           cr.sw[c], iv[c]);
+      if (fw.want_rgb) {
+        uint8_t *dst = buf + (rr * SEGW + lane * CPL) * 3;
+        if constexpr (CPL == 2) {
+          uint16_t *d16 = reinterpret_cast<uint16_t *>(dst);
+          d16[0] = (uint16_t)__byte_perm(po[0].r, po[0].g, 0x0040);  // r0 g0
+          d16[1] = (uint16_t)__byte_perm(po[0].b, po[0].r, 0x0060);  // b0 r1
+          d16[2] = (uint16_t)__byte_perm(po[0].g, po[0].b, 0x0062);  // g1 b1
+        } else {
+          uint32_t w[3 * CPL / 4];
+#pragma unroll
+          for (int q = 0; q < CPL / 4; ++q)
+            pack_rgb4(po[2 * q], po[2 * q + 1], w[3 * q], w[3 * q + 1], w[3 * q + 2]);
+          if constexpr (CPL == 4) {
+#pragma unroll
+            for (int q = 0; q < 3; ++q) reinterpret_cast<uint32_t *>(dst)[q] = w[q];
+          } else {  // CPL == 8: three 8-byte chunks
+#pragma unroll
+            for (int q = 0; q < 3; ++q)
+              reinterpret_cast<uint2 *>(dst)[q] = make_uint2(w[2 * q], w[2 * q + 1]);
+          }
+        }
+      }
+      if (fw.want_d) {
+        float *dst = reinterpret_cast<float *>(buf + fw.off_d) + rr * SEGW + lane * CPL;
+        if constexpr (CPL == 2) {
+          *reinterpret_cast<float2 *>(dst) = make_float2(po[0].d0, po[0].d1);
+        } else {
+#pragma unroll
+          for (int q = 0; q < CPL / 4; ++q)
+            reinterpret_cast<float4 *>(dst)[q] =
+                make_float4(po[2 * q].d0, po[2 * q].d1, po[2 * q + 1].d0, po[2 * q + 1].d1);
+        }
+      }
+      if (fw.want_s) {
+        uint16_t *dst = reinterpret_cast<uint16_t *>(buf + fw.off_s) + rr * SEGW + lane * CPL;
+        if constexpr (CPL == 2) {
+          *reinterpret_cast<uint32_t *>(dst) = po[0].s;
+        } else if constexpr (CPL == 4) {
+          *reinterpret_cast<uint2 *>(dst) = make_uint2(po[0].s, po[1].s);
+        } else {
+          *reinterpret_cast<uint4 *>(dst) = make_uint4(po[0].s, po[1].s, po[2].s, po[3].s);
+        }
+      }
+    }
+    fence_proxy_async();
+    __syncwarp();
+    if (lane == 0) {
+      if (a.segs_per_row == 1) {
+        const size_t pix0 = ((size_t)env * H + r0) * W;
+        if (fw.want_rgb) bulk_store(a.rgb + pix0 * 3, buf, (unsigned)(nr * W * 3), fw.pol);
+        if (fw.want_d) bulk_store(a.depth + pix0, buf + fw.off_d, (unsigned)(nr * W * 4), fw.pol);
+        if (fw.want_s) bulk_store(a.sem + pix0, buf + fw.off_s, (unsigned)(nr * W * 2), fw.pol);
+      } else {
+        for (int rr = 0; rr < nr; ++rr) {
+          const size_t pix0 = ((size_t)env * H + r0 + rr) * W + (size_t)seg * SEGW;
+          if (fw.want_rgb)
+            bulk_store(a.rgb + pix0 * 3, buf + rr * SEGW * 3, (unsigned)(SEGW * 3), fw.pol);
+          if (fw.want_d)
+            bulk_store(a.depth + pix0, buf + fw.off_d + rr * SEGW * 4, (unsigned)(SEGW * 4),
+                       fw.pol);
+          if (fw.want_s)
+            bulk_store(a.sem + pix0, buf + fw.off_s + rr * SEGW * 2, (unsigned)(SEGW * 2), fw.pol);
+        }
+      }
+      bulk_commit();
+    }
+    ++fw.k;
+  }
+}
+
+// Drains this warp's bulk stores and, for the last warp of the grid, resets
+// the self-resetting work counter for the next launch.
+__device__ __forceinline__ void finish_grid(unsigned int *ctr) {
+  if ((threadIdx.x & 31) == 0) {
+    bulk_wait_all();
+    const unsigned total_warps = gridDim.x * (blockDim.x >> 5);
+    if (atomicAdd(ctr + 1, 1u) == total_warps - 1) {
+      ctr[0] = 0;
+      ctr[1] = 0;
+      __threadfence();
+    }
+  }
+}
+
+// k_fill_tma: streaming frame writer over all units of a frame batch; units
+// are pulled from a self-resetting global counter (one prefetched ahead).
 template <int CPL, int RW>
 __global__ void __launch_bounds__(128) k_fill_tma(FillArgs a) {
-  constexpr int NS = 2;
-  constexpr int SEGW = 32 * CPL;
   extern __shared__ __align__(128) uint8_t smem[];
   const int lane = threadIdx.x & 31;
-  const int wib = threadIdx.x >> 5;
-  const bool want_rgb = a.rgb != nullptr, want_d = a.depth != nullptr,
-             want_s = a.sem != nullptr;
-  const int off_d = want_rgb ? RW * SEGW * 3 : 0;
-  const int off_s = off_d + (want_d ? RW * SEGW * 4 : 0);
-  const int stage_bytes = off_s + (want_s ? RW * SEGW * 2 : 0);
-  uint8_t *wbase = smem + (size_t)wib * NS * stage_bytes;
-  const uint64_t pol = policy_evict_first();
-  const int W = a.W, H = a.H;
-  const unsigned total_warps = gridDim.x * (blockDim.x >> 5);
-
-  ColRegs<CPL> cr;
-  long long cur_es = -1;
-  int k = 0;
+  FillWarp<CPL, RW> fw;
+  fw.init(a, smem, threadIdx.x >> 5);
   long long u = 0;
   if (lane == 0) u = atomicAdd(a.ctr, 1u);
   u = __shfl_sync(0xffffffffu, u, 0);
   while (u < a.n_units) {
     long long nxt = 0;
-    if (lane == 0) nxt = atomicAdd(a.ctr, 1u);  // prefetch the next unit
+    if (lane == 0) nxt = atomicAdd(a.ctr, 1u);
     const long long es = u / a.units_per_seg;
     const int gidx = (int)(u - es * a.units_per_seg);
     const int env = (int)(es / a.segs_per_row);
     const int seg = (int)(es - (long long)env * a.segs_per_row);
-    const int col0 = seg * SEGW + lane * CPL;
-    if (es != cur_es) {
-      cur_es = es;
-      load_cols<CPL>(a.rec + (size_t)env * W + col0, cr);
-    }
-    const int r_begin = gidx * a.rows_per_unit;
-    const int r_end = min(H, r_begin + a.rows_per_unit);
-    uint4 pq0, pq1;
-    uint32_t piv[CPL / 2];
-    load_row<CPL>(a, (uint32_t)r_begin, col0, pq0, pq1, piv);
-    for (int r0 = r_begin; r0 < r_end; r0 += RW) {
-      const int nr = min(RW, r_end - r0);
-      uint8_t *buf = wbase + (k & (NS - 1)) * stage_bytes;
-      if (k >= NS) {
-        if (lane == 0) bulk_wait_read<NS - 1>();
-        __syncwarp();
-      }
-      for (int rr = 0; rr < nr; ++rr) {
-        const uint32_t i = (uint32_t)(r0 + rr);
-        // this row's loads were issued one row ahead (software pipelining)
-        RowRec R;
-        R.depth_p = __uint_as_float(pq0.x);
-        R.sem2 = pq0.y;
-        R.num2 = pq0.z;
-        R.r2 = pq0.w;
-        R.g2 = pq1.x;
-        R.b2 = pq1.y;
-        uint32_t iv[CPL / 2];
-#pragma unroll
-        for (int c = 0; c < CPL / 2; ++c) iv[c] = piv[c];
-        {
-          const uint32_t inext = min(i + 1, (uint32_t)(r_end - 1));
-          load_row<CPL>(a, inext, col0, pq0, pq1, piv);
-        }
-        PairOut po[CPL / 2];
-#pragma unroll
-        for (int c = 0; c < CPL / 2; ++c)
-          po[c] = shade_pair(i, R, cr.lo[2 * c], cr.hi[2 * c], cr.lo[2 * c + 1],
-                             cr.hi[2 * c + 1], cr.dw[2 * c], cr.dw[2 * c + 1], cr.nw[c], cr.rw[c],
-                             cr.gw[c], cr.bw[c], cr.sw[c], iv[c]);
-        if (want_rgb) {
-          uint8_t *dst = buf + (rr * SEGW + lane * CPL) * 3;
-          if constexpr (CPL == 2) {
-            uint16_t *d16 = reinterpret_cast<uint16_t *>(dst);
-            d16[0] = (uint16_t)__byte_perm(po[0].r, po[0].g, 0x0040);  // r0 g0
-            d16[1] = (uint16_t)__byte_perm(po[0].b, po[0].r, 0x0060);  // b0 r1
-            d16[2] = (uint16_t)__byte_perm(po[0].g, po[0].b, 0x0062);  // g1 b1
-          } else {
-            uint32_t w[3 * CPL / 4];
-#pragma unroll
-            for (int q = 0; q < CPL / 4; ++q)
-              pack_rgb4(po[2 * q], po[2 * q + 1], w[3 * q], w[3 * q + 1], w[3 * q + 2]);
-            if constexpr (CPL == 4) {
-#pragma unroll
-              for (int q = 0; q < 3; ++q) reinterpret_cast<uint32_t *>(dst)[q] = w[q];
-            } else {  // CPL == 8: three 8-byte chunks
-#pragma unroll
-              for (int q = 0; q < 3; ++q)
-                reinterpret_cast<uint2 *>(dst)[q] = make_uint2(w[2 * q], w[2 * q + 1]);
-            }
-          }
-        }
-        if (want_d) {
-          float *dst = reinterpret_cast<float *>(buf + off_d) + rr * SEGW + lane * CPL;
-          if constexpr (CPL == 2) {
-            *reinterpret_cast<float2 *>(dst) = make_float2(po[0].d0, po[0].d1);
-          } else {
-#pragma unroll
-            for (int q = 0; q < CPL / 4; ++q)
-              reinterpret_cast<float4 *>(dst)[q] =
-                  make_float4(po[2 * q].d0, po[2 * q].d1, po[2 * q + 1].d0, po[2 * q + 1].d1);
-          }
-        }
-        if (want_s) {
-          uint16_t *dst = reinterpret_cast<uint16_t *>(buf + off_s) + rr * SEGW + lane * CPL;
-          if constexpr (CPL == 2) {
-            *reinterpret_cast<uint32_t *>(dst) = po[0].s;
-          } else if constexpr (CPL == 4) {
-            *reinterpret_cast<uint2 *>(dst) = make_uint2(po[0].s, po[1].s);
-          } else {
-            *reinterpret_cast<uint4 *>(dst) = make_uint4(po[0].s, po[1].s, po[2].s, po[3].s);
-          }
-        }
-      }
-      fence_proxy_async();
-      __syncwarp();
-      if (lane == 0) {
-        if (a.segs_per_row == 1) {
-          const size_t pix0 = ((size_t)env * H + r0) * W;
-          if (want_rgb) bulk_store(a.rgb + pix0 * 3, buf, (unsigned)(nr * W * 3), pol);
-          if (want_d) bulk_store(a.depth + pix0, buf + off_d, (unsigned)(nr * W * 4), pol);
-          if (want_s) bulk_store(a.sem + pix0, buf + off_s, (unsigned)(nr * W * 2), pol);
-        } else {
-          for (int rr = 0; rr < nr; ++rr) {
-            const size_t pix0 = ((size_t)env * H + r0 + rr) * W + (size_t)seg * SEGW;
-            if (want_rgb)
-              bulk_store(a.rgb + pix0 * 3, buf + rr * SEGW * 3, (unsigned)(SEGW * 3), pol);
-            if (want_d)
-              bulk_store(a.depth + pix0, buf + off_d + rr * SEGW * 4, (unsigned)(SEGW * 4), pol);
-            if (want_s)
-              bulk_store(a.sem + pix0, buf + off_s + rr * SEGW * 2, (unsigned)(SEGW * 2), pol);
-          }
-        }
-        bulk_commit();
-      }
-      ++k;
-    }
+    fill_unit<CPL, RW, false>(a, fw, env, seg, gidx);
     u = __shfl_sync(0xffffffffu, nxt, 0);
   }
-  if (lane == 0) {
-    bulk_wait_all();
-    // last warp out resets the scheduler for the next launch
-    if (atomicAdd(a.ctr + 1, 1u) == total_warps - 1) {
-      a.ctr[0] = 0;
-      a.ctr[1] = 0;
-      __threadfence();
+  finish_grid(a.ctr);
+}
+
+// ----------------------------------------------------------- megakernel
+//
+// k_step_render: one launch per simulator step.  Persistent warps pull tasks
+// from a host-built queue in which every dependency precedes its dependents:
+//   STEP(e)      Simulator.step kinematics of env e            (one warp)
+//   CAST(e, c)   32 columns of env e: DDA + epilogue -> ColRec  (one warp)
+//   FILL(e, u)   one fill unit of env e                         (one warp)
+// The queue interleaves STEP(e + LS + LC), CAST(e + LC, *), FILL(e, *) so the
+// latency-bound casts run ahead of, and overlap with, the HBM-bound fill.
+// Per-env counters (step done, casts done, fills done) carry the
+// dependencies (release/acquire through L2); the last fill of an env resets
+// them for the next launch, the last warp resets the queue counter.
+// Every dequeued task's dependencies were dequeued earlier by running warps,
+// so waiting can never deadlock.
+enum : int { NV_TASK_STEP = 0, NV_TASK_CAST = 1, NV_TASK_FILL = 2 };
+
+struct MegaArgs {
+  EnvView ev;
+  SceneView sc;
+  CamView cam;
+  AgentCfg cfg;
+  FillArgs f;
+  const int8_t *actions;
+  uint8_t *collided;
+  double *disp;
+  int32_t *status;
+  double *gps, *compass;
+  double t_max;
+  const int2 *tasks;  // (type << 24 | sub, env)
+  int n_tasks;
+  int n_cast;         // cast tasks per env
+  int n_fill;         // fill tasks per env
+  unsigned int *envsync;  // 3 per env: step done, casts done, fills done
+};
+
+__device__ __forceinline__ unsigned ld_acquire(const unsigned *p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void wait_at_least(const unsigned *p, unsigned target) {
+  if ((threadIdx.x & 31) == 0) {
+    unsigned ns = 32;
+    while (ld_acquire(p) < target) {
+      __nanosleep(ns);
+      ns = min(ns * 2, 256u);
     }
   }
+  __syncwarp();
+}
+
+template <int CPL, int RW>
+__global__ void __launch_bounds__(128) k_step_render(MegaArgs m) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  const int lane = threadIdx.x & 31;
+  FillWarp<CPL, RW> fw;
+  fw.init(m.f, smem, threadIdx.x >> 5);
+  long long slot = 0;
+  if (lane == 0) slot = atomicAdd(m.f.ctr, 1u);
+  slot = __shfl_sync(0xffffffffu, slot, 0);
+  while (slot < m.n_tasks) {
+    long long nxt = 0;
+    if (lane == 0) nxt = atomicAdd(m.f.ctr, 1u);
+    const int2 t = __ldg(m.tasks + slot);
+    const int type = t.x >> 24, sub = t.x & 0xffffff, e = t.y;
+    unsigned *sync = m.envsync + 3 * (size_t)e;
+    if (type == NV_TASK_STEP) {
+      warp_agent_step(m.ev, m.sc, m.cfg, e, m.actions[e], m.collided, m.disp, m.status);
+      __syncwarp();
+      if (lane == 0) {
+        __threadfence();
+        atomicExch(sync, 1u);
+      }
+    } else if (type == NV_TASK_CAST) {
+      wait_at_least(sync, 1u);
+      const int j = sub * 32 + lane;
+      if (j < m.cam.W) cast_column<true>(m.ev, m.sc, m.cam, e, j, const_cast<ColRec *>(m.f.rec),
+                                         m.t_max, m.gps, m.compass);
+      __syncwarp();
+      if (lane == 0) {
+        __threadfence();
+        atomicAdd(sync + 1, 1u);
+      }
+    } else {
+      wait_at_least(sync + 1, (unsigned)m.n_cast);
+      const int seg = sub / m.f.units_per_seg;
+      const int gidx = sub - seg * m.f.units_per_seg;
+      fill_unit<CPL, RW, true>(m.f, fw, e, seg, gidx);
+      if (lane == 0 && atomicAdd(sync + 2, 1u) == (unsigned)m.n_fill - 1) {
+        sync[0] = 0;  // every task of env e is done: reset for the next launch
+        sync[1] = 0;
+        sync[2] = 0;
+      }
+    }
+    slot = __shfl_sync(0xffffffffu, nxt, 0);
+  }
+  finish_grid(m.f.ctr);
 }
 
 // One thread per pixel, any W/H; the same f16 arithmetic as k_fill_tma (one

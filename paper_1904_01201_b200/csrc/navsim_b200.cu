@@ -90,6 +90,11 @@ struct Camera {
   DevBuf u, tc, tf, rows, inv;
   DevBuf rec;      // ColRec N x W
   DevBuf ctr;      // fill scheduler counters
+  // fused step+render megakernel task queue (rebuilt when N or layout changes)
+  DevBuf tasks, envsync;
+  int64_t tasks_n = -1;
+  int tasks_key = -1;
+  int n_tasks = 0, n_cast = 0, n_fill = 0;
 };
 
 }  // namespace
@@ -116,6 +121,7 @@ struct nv_ctx {
   // host-buffer (e2e) path scratch
   DevBuf e_act, e_rgb, e_depth, e_sem, e_gps, e_comp, e_coll, e_disp;
   int64_t launches = 0;
+  bool fused = false;  // nv_step_render uses the megakernel when the layout allows (opt-in)
   // optional per-kernel CUDA-event timing (bench roofline evidence)
   bool prof_on = false;
   std::vector<cudaEvent_t> prof_ev;   // pool, pairs
@@ -333,6 +339,15 @@ unsigned blocks_for(long long work, int per_block) {
   return (unsigned)std::max<long long>(1, (work + per_block - 1) / per_block);
 }
 
+// Fill work decomposition shared by k_fill_tma and the megakernel.
+template <int CPL>
+void fill_layout(nvk::FillArgs &a) {
+  a.segs_per_row = a.W / (32 * CPL);
+  a.rows_per_unit = 16;
+  a.units_per_seg = (a.H + a.rows_per_unit - 1) / a.rows_per_unit;
+  a.n_units = (long long)a.N * a.segs_per_row * a.units_per_seg;
+}
+
 // Fill launch: TMA streaming writer when the row layout allows 16-byte bulk
 // copies, else the generic per-pixel kernel.
 template <int CPL>
@@ -353,14 +368,87 @@ int launch_fill_tma(nv_ctx *c, nvk::FillArgs &a, cudaStream_t st) {
   int per_sm = 0;
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, warps * 32, smem));
   per_sm = std::max(1, per_sm);
-  a.segs_per_row = a.W / segw;
-  a.rows_per_unit = 16;
-  a.units_per_seg = (a.H + a.rows_per_unit - 1) / a.rows_per_unit;
-  a.n_units = (long long)a.N * a.segs_per_row * a.units_per_seg;
+  fill_layout<CPL>(a);
   long long want = (a.n_units + warps - 1) / warps;
   unsigned grid = (unsigned)std::max<long long>(1, std::min<long long>(want, (long long)per_sm * c->sm_count));
   Prof pf(c, st, 2);
   kern<<<grid, warps * 32, smem, st>>>(a);
+  return check_launch(c);
+}
+
+// Task queue of the megakernel: STEP(e + LS + LC), CAST(e + LC, *), FILL(e, *)
+// per round, so every dependency is dequeued before its dependents.
+int build_tasks(Camera &cam, int64_t N, int n_cast, int n_fill, int key) {
+  if (cam.tasks_n == N && cam.tasks_key == key) return NV_OK;
+  const int64_t LS = std::min<int64_t>(32, N), LC = std::min<int64_t>(96, N);
+  std::vector<int2> t;
+  t.reserve((size_t)N * (1 + n_cast + n_fill));
+  for (int64_t r = 0; r < N + LS + LC; ++r) {
+    if (r < N) t.push_back(make_int2(nvk::NV_TASK_STEP << 24, (int)r));
+    const int64_t ec = r - LS;
+    if (ec >= 0 && ec < N)
+      for (int k = 0; k < n_cast; ++k) t.push_back(make_int2((nvk::NV_TASK_CAST << 24) | k, (int)ec));
+    const int64_t ef = r - LS - LC;
+    if (ef >= 0 && ef < N)
+      for (int k = 0; k < n_fill; ++k) t.push_back(make_int2((nvk::NV_TASK_FILL << 24) | k, (int)ef));
+  }
+  TRY(upload(cam.tasks, t));
+  TRY(cam.envsync.alloc(sizeof(uint32_t) * 3 * (size_t)N));
+  CK(cudaMemset(cam.envsync.p, 0, sizeof(uint32_t) * 3 * (size_t)N));
+  cam.n_tasks = (int)t.size();
+  cam.n_cast = n_cast;
+  cam.n_fill = n_fill;
+  cam.tasks_n = N;
+  cam.tasks_key = key;
+  return NV_OK;
+}
+
+template <int CPL>
+int launch_mega(nv_ctx *c, Camera &cam, const int8_t *actions, uint8_t *rgb, float *depth,
+                uint16_t *sem, double *gps, double *compass, uint8_t *collided, double *disp,
+                int32_t *status, cudaStream_t st) {
+  constexpr int RW = 2;
+  nvk::MegaArgs m;
+  m.ev = c->env_view();
+  m.sc = c->scene_view();
+  m.cam = cam_view(cam);
+  m.cfg = nvk::AgentCfg{c->radius, c->step, c->turn_rad};
+  nvk::FillArgs &a = m.f;
+  a.rec = cam.rec.as<ColRec>();
+  a.rows = cam.rows.as<RowRec>();
+  a.inv = cam.inv.as<uint16_t>();
+  a.N = (int)c->n_envs; a.W = cam.W; a.H = cam.H;
+  a.rgb = rgb; a.depth = depth; a.sem = sem;
+  a.ctr = cam.ctr.as<unsigned int>();
+  fill_layout<CPL>(a);
+  const int n_cast = (cam.W + 31) / 32;
+  const int n_fill = a.segs_per_row * a.units_per_seg;
+  TRY(build_tasks(cam, c->n_envs, n_cast, n_fill, CPL * 1000 + a.rows_per_unit));
+  m.actions = actions; m.collided = collided; m.disp = disp; m.status = status;
+  m.gps = gps; m.compass = compass;
+  m.t_max = cam.max_range;
+  m.tasks = cam.tasks.as<int2>();
+  m.n_tasks = cam.n_tasks;
+  m.n_cast = cam.n_cast;
+  m.n_fill = cam.n_fill;
+  m.envsync = cam.envsync.as<unsigned int>();
+  const int segw = 32 * CPL;
+  const int bpp = (rgb ? 3 : 0) + (depth ? 4 : 0) + (sem ? 2 : 0);
+  const int warps = 4;
+  const size_t smem = (size_t)warps * 2 * RW * segw * std::max(bpp, 1);
+  auto kern = nvk::k_step_render<CPL, RW>;
+  static int configured_smem[3] = {0, 0, 0};
+  int slot = CPL == 2 ? 0 : (CPL == 4 ? 1 : 2);
+  if ((int)smem > configured_smem[slot]) {
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    configured_smem[slot] = (int)smem;
+  }
+  int per_sm = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, warps * 32, smem));
+  per_sm = std::max(1, per_sm);
+  unsigned grid = (unsigned)((long long)per_sm * c->sm_count);
+  Prof pf(c, st, 3);
+  kern<<<grid, warps * 32, smem, st>>>(m);
   return check_launch(c);
 }
 
@@ -644,9 +732,29 @@ int nv_step_render(nv_ctx *c, const int8_t *actions, int cam, uint8_t *rgb, floa
   TRY(cam_check(c, cam));
   if (!actions) return fail(NV_ERR_ARG, "actions is NULL");
   cudaStream_t st = (cudaStream_t)stream;
+  Camera &k = c->cams[cam];
+  auto al16 = [](const void *p) { return ((uintptr_t)p & 15) == 0; };
+  const bool tma_ok = al16(rgb) && al16(depth) && al16(sem) && (rgb || depth || sem);
+  if (c->fused && tma_ok && c->n_envs < (1 << 24)) {
+    if (k.W % 256 == 0)
+      return launch_mega<8>(c, k, actions, rgb, depth, sem, gps, compass, collided, displacement,
+                            status, st);
+    if (k.W == 128)
+      return launch_mega<4>(c, k, actions, rgb, depth, sem, gps, compass, collided, displacement,
+                            status, st);
+    if (k.W == 64)
+      return launch_mega<2>(c, k, actions, rgb, depth, sem, gps, compass, collided, displacement,
+                            status, st);
+  }
   TRY(do_step(c, actions, collided, displacement, status, st));
   TRY(do_cast(c, cam, gps, compass, st));
-  return launch_fill(c, c->cams[cam], c->n_envs, rgb, depth, sem, st);
+  return launch_fill(c, k, c->n_envs, rgb, depth, sem, st);
+}
+
+int nv_set_fused(nv_ctx *c, int on) {
+  if (!c) return fail(NV_ERR_ARG, "ctx is NULL");
+  c->fused = on != 0;
+  return NV_OK;
 }
 
 int nv_step_render_host(nv_ctx *c, const int8_t *actions_host, int cam, uint32_t channels,
