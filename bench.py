@@ -106,6 +106,17 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def ncu_traffic():
+    """dram read+write bytes per launch of the dominant kernel from the committed
+    ncu capture (profiles/r01_fill_traffic.json), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_fill_traffic.json")) as f:
+            d = json.load(f)
+        return int(d["dram_bytes_read"]) + int(d["dram_bytes_write"])
+    except (OSError, KeyError, ValueError):
+        return None
+
+
 def measured_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -223,6 +234,7 @@ def run_gpu(args):
     poses = synth.sample_poses(sc, shard.n_total, seed=1)[shard.lo:shard.hi]
     sim.reset(poses[:, :2], poses[:, 2])
     nat.check(sim.ctx.lib.nv_set_fused(sim.ctx.handle, 1 if args.fused else 0))
+    nat.check(sim.ctx.lib.nv_set_fill_mode(sim.ctx.handle, args.fill_mode))
     total_steps = args.warmup + args.steps
     acts = torch.as_tensor(synth.random_actions(shard.n_total, total_steps, seed=2)[:, shard.lo:shard.hi].copy(),
                            device=f"cuda:{local}")
@@ -376,11 +388,15 @@ def run_gpu(args):
                        "channels": list(chans), "segments": sc.n_segments,
                        "triangles": sc.n_triangles, "parallelism": f"env-shard x{world}",
                        "cuda_graph": use_graph, "fused_megakernel": fused,
+                       "fill_mode": ["direct-256b-stores", "tma-bulk-stores"][args.fill_mode],
                        "l2": f"no flush: frames written per step "
                              f"({step_bytes / 1e6:.0f} MB/GPU) exceed the 126 MB L2"},
             "roofline": {"bound": "hbm", "kernel": dom,
                          "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": None, "peak_source": peak_src,
+                         "frac": achieved / peak,
+                         "traffic": ncu_traffic() if not fused else None,
+                         "traffic_source": "profiles/r01_fill_traffic.json (ncu --set full)",
+                         "peak_source": peak_src,
                          "bytes_per_launch": dom_bytes,
                          "kernel_ms": per,
                          "step_achieved_gbs": step_gbs, "step_frac": step_gbs / peak},
@@ -408,6 +424,7 @@ def main():
     ap.add_argument("--envs", type=int, default=0, help="override envs per GPU")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--fill-mode", type=int, default=1, help="0 direct stores, 1 TMA bulk stores")
     ap.add_argument("--fused", action="store_true", help="one megakernel launch per step (experimental)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -120,8 +120,11 @@ int nv_step_render(nv_ctx *ctx, const int8_t *actions, int cam, uint8_t *rgb,
                    uint8_t *collided, double *displacement, int32_t *status,
                    void *stream);
 
-/* Enable (default) / disable the single-launch megakernel of nv_step_render. */
+/* Enable / disable (default) the single-launch megakernel of nv_step_render. */
 int nv_set_fused(nv_ctx *ctx, int on);
+/* Frame writer: 0 = 256-bit direct stores from registers,
+ * 1 (default) = shared-memory stages written out by TMA bulk copies. */
+int nv_set_fill_mode(nv_ctx *ctx, int mode);
 
 /* End-to-end call over HOST buffers (the reference-facing path: host actions
  * in, host results out).  Copies actions (host, n i8) in, runs

@@ -904,13 +904,14 @@ __device__ __forceinline__ void pack_rgb4(const PairOut &p, const PairOut &q, ui
   w2 = __byte_perm(rg1, q.b, 0x6324);                  // b2 r3 g3 b3
 }
 
-// Row record + this lane's CPL shading-table entries of row i.
+// Row record (from the CTA's shared-memory copy of the row table) + this
+// lane's CPL shading-table entries of row i.
 template <int CPL>
-__device__ __forceinline__ void load_row(const FillArgs &a, uint32_t i, int col0, uint4 &q0,
-                                         uint4 &q1, uint32_t (&iv)[CPL / 2]) {
-  const uint4 *rq = reinterpret_cast<const uint4 *>(a.rows + i);
-  q0 = __ldg(rq);
-  q1 = __ldg(rq + 1);
+__device__ __forceinline__ void load_row(const FillArgs &a, const RowRec *rows_s, uint32_t i,
+                                         int col0, uint4 &q0, uint4 &q1, uint32_t (&iv)[CPL / 2]) {
+  const uint4 *rq = reinterpret_cast<const uint4 *>(rows_s + i);
+  q0 = rq[0];
+  q1 = rq[1];
   const uint16_t *ip = a.inv + (size_t)i * a.W + col0;
   if constexpr (CPL == 8) {
     uint4 v = __ldg(reinterpret_cast<const uint4 *>(ip));
@@ -923,17 +924,32 @@ __device__ __forceinline__ void load_row(const FillArgs &a, uint32_t i, int col0
   }
 }
 
+// Copies the camera's row table (H x 32 B) into shared memory; every warp of
+// the CTA reads its rows from there (uniform LDS, no L1/L2 misses under the
+// write stream).  Returns the first byte after the table (16-aligned).
+__device__ __forceinline__ uint8_t *stage_rows(const FillArgs &a, uint8_t *smem) {
+  const uint4 *src = reinterpret_cast<const uint4 *>(a.rows);
+  uint4 *dst = reinterpret_cast<uint4 *>(smem);
+  for (int k = threadIdx.x; k < a.H * 2; k += blockDim.x) dst[k] = __ldg(src + k);
+  __syncthreads();
+  return smem + (size_t)a.H * sizeof(RowRec);
+}
+
 // Per-warp state of the streaming writer: a private ring of NS smem stages.
 template <int CPL, int RW>
 struct FillWarp {
   static constexpr int NS = 2;
   static constexpr int SEGW = 32 * CPL;
   uint8_t *wbase;
+  const RowRec *rows_s;  // shared-memory row table
   int off_d, off_s, stage_bytes;
   bool want_rgb, want_d, want_s;
   uint64_t pol;
   int k;  // stages issued so far
+  // smem layout: [row table H x 32 B][per-warp stage rings]
   __device__ __forceinline__ void init(const FillArgs &a, uint8_t *smem, int wib) {
+    rows_s = reinterpret_cast<const RowRec *>(smem);
+    smem = stage_rows(a, smem);
     want_rgb = a.rgb != nullptr;
     want_d = a.depth != nullptr;
     want_s = a.sem != nullptr;
@@ -966,7 +982,7 @@ __device__ __forceinline__ void fill_unit(const FillArgs &a, FillWarp<CPL, RW> &
   const int r_end = min(H, r_begin + a.rows_per_unit);
   uint4 pq0, pq1;
   uint32_t piv[CPL / 2];
-  load_row<CPL>(a, (uint32_t)r_begin, col0, pq0, pq1, piv);
+  load_row<CPL>(a, fw.rows_s, (uint32_t)r_begin, col0, pq0, pq1, piv);
   for (int r0 = r_begin; r0 < r_end; r0 += RW) {
     const int nr = min(RW, r_end - r0);
     uint8_t *buf = fw.wbase + (fw.k & (NS - 1)) * fw.stage_bytes;
@@ -987,7 +1003,7 @@ __device__ __forceinline__ void fill_unit(const FillArgs &a, FillWarp<CPL, RW> &
       uint32_t iv[CPL / 2];
 #pragma unroll
       for (int c = 0; c < CPL / 2; ++c) iv[c] = piv[c];
-      load_row<CPL>(a, min(i + 1, (uint32_t)(r_end - 1)), col0, pq0, pq1, piv);
+      load_row<CPL>(a, fw.rows_s, min(i + 1, (uint32_t)(r_end - 1)), col0, pq0, pq1, piv);
       PairOut po[CPL / 2];
 #pragma unroll
       for (int c = 0; c < CPL / 2; ++c)
@@ -1092,11 +1108,148 @@ __global__ void __launch_bounds__(128) k_fill_tma(FillArgs a) {
   while (u < a.n_units) {
     long long nxt = 0;
     if (lane == 0) nxt = atomicAdd(a.ctr, 1u);
-    const long long es = u / a.units_per_seg;
-    const int gidx = (int)(u - es * a.units_per_seg);
+    // row-block-major order: warps across the GPU render the same rows of
+    // different envs at the same time, so the row records and shading-table
+    // slice they share stay hot in every SM's L1
+    const long long n_es = (long long)a.N * a.segs_per_row;
+    const int gidx = (int)(u / n_es);
+    const long long es = u - (long long)gidx * n_es;
     const int env = (int)(es / a.segs_per_row);
     const int seg = (int)(es - (long long)env * a.segs_per_row);
     fill_unit<CPL, RW, false>(a, fw, env, seg, gidx);
+    u = __shfl_sync(0xffffffffu, nxt, 0);
+  }
+  finish_grid(a.ctr);
+}
+
+// ---- direct-store variant: no smem staging ---------------------------------
+// Each lane stores its CPL pixels of a row straight from registers: depth as
+// one 256-bit store (STG.256, sm_100), semantic as 128-bit, RGB as three
+// 64-bit stores; a warp covers W contiguous pixels per row, so every row is a
+// fully coalesced run per channel and partial sectors merge in L2.  Without
+// stage buffers the whole L1 serves the (env-independent) shading tables.
+__device__ __forceinline__ void st_v8f(float *p, const float (&v)[8], uint64_t pol) {
+  asm volatile(
+      "st.global.L2::cache_hint.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8}, %9;" ::"l"(p),
+      "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7]),
+      "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ void st_v4u(void *p, uint32_t a, uint32_t b, uint32_t c, uint32_t d,
+                                       uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.v4.b32 [%0], {%1,%2,%3,%4}, %5;" ::"l"(p), "r"(a),
+               "r"(b), "r"(c), "r"(d), "l"(pol)
+               : "memory");
+}
+__device__ __forceinline__ void st_v2u(void *p, uint32_t a, uint32_t b, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.v2.b32 [%0], {%1,%2}, %3;" ::"l"(p), "r"(a), "r"(b),
+               "l"(pol)
+               : "memory");
+}
+
+template <int CPL, bool COH>
+__device__ __forceinline__ void fill_unit_direct(const FillArgs &a, const RowRec *rows_s,
+                                                 uint64_t pol, int env, int seg, int gidx) {
+  constexpr int SEGW = 32 * CPL;
+  const int lane = threadIdx.x & 31;
+  const int W = a.W, H = a.H;
+  const int col0 = seg * SEGW + lane * CPL;
+  ColRegs<CPL> cr;
+  load_cols<CPL, COH>(a.rec + (size_t)env * W + col0, cr);
+  const int r_begin = gidx * a.rows_per_unit;
+  const int r_end = min(H, r_begin + a.rows_per_unit);
+  uint4 pq0, pq1;
+  uint32_t piv[CPL / 2];
+  load_row<CPL>(a, rows_s, (uint32_t)r_begin, col0, pq0, pq1, piv);
+  size_t pix = ((size_t)env * H + r_begin) * W + col0;  // first pixel of this lane's run
+  for (int r = r_begin; r < r_end; ++r, pix += W) {
+    const uint32_t i = (uint32_t)r;
+    RowRec R;
+    R.depth_p = __uint_as_float(pq0.x);
+    R.sem2 = pq0.y;
+    R.num2 = pq0.z;
+    R.r2 = pq0.w;
+    R.g2 = pq1.x;
+    R.b2 = pq1.y;
+    uint32_t iv[CPL / 2];
+#pragma unroll
+    for (int c = 0; c < CPL / 2; ++c) iv[c] = piv[c];
+    load_row<CPL>(a, rows_s, min(i + 1, (uint32_t)(r_end - 1)), col0, pq0, pq1, piv);
+    PairOut po[CPL / 2];
+#pragma unroll
+    for (int c = 0; c < CPL / 2; ++c)
+      po[c] = shade_pair(i, R, cr.lo[2 * c], cr.hi[2 * c], cr.lo[2 * c + 1], cr.hi[2 * c + 1],
+                         cr.dw[2 * c], cr.dw[2 * c + 1], cr.nw[c], cr.rw[c], cr.gw[c], cr.bw[c],
+                         cr.sw[c], iv[c]);
+    if (a.rgb) {
+      uint8_t *dst = a.rgb + pix * 3;
+      if constexpr (CPL == 2) {
+        uint16_t *d16 = reinterpret_cast<uint16_t *>(dst);
+        d16[0] = (uint16_t)__byte_perm(po[0].r, po[0].g, 0x0040);
+        d16[1] = (uint16_t)__byte_perm(po[0].b, po[0].r, 0x0060);
+        d16[2] = (uint16_t)__byte_perm(po[0].g, po[0].b, 0x0062);
+      } else {
+        uint32_t w[3 * CPL / 4];
+#pragma unroll
+        for (int q = 0; q < CPL / 4; ++q)
+          pack_rgb4(po[2 * q], po[2 * q + 1], w[3 * q], w[3 * q + 1], w[3 * q + 2]);
+        if constexpr (CPL == 4) {
+#pragma unroll
+          for (int q = 0; q < 3; ++q) reinterpret_cast<uint32_t *>(dst)[q] = w[q];
+        } else {
+#pragma unroll
+          for (int q = 0; q < 3; ++q) st_v2u(dst + 8 * q, w[2 * q], w[2 * q + 1], pol);
+        }
+      }
+    }
+    if (a.depth) {
+      float *dst = a.depth + pix;
+      if constexpr (CPL == 8) {
+        const float v[8] = {po[0].d0, po[0].d1, po[1].d0, po[1].d1,
+                            po[2].d0, po[2].d1, po[3].d0, po[3].d1};
+        st_v8f(dst, v, pol);
+      } else if constexpr (CPL == 4) {
+        st_v4u(dst, __float_as_uint(po[0].d0), __float_as_uint(po[0].d1),
+               __float_as_uint(po[1].d0), __float_as_uint(po[1].d1), pol);
+      } else {
+        st_v2u(dst, __float_as_uint(po[0].d0), __float_as_uint(po[0].d1), pol);
+      }
+    }
+    if (a.sem) {
+      uint16_t *dst = a.sem + pix;
+      if constexpr (CPL == 8) {
+        st_v4u(dst, po[0].s, po[1].s, po[2].s, po[3].s, pol);
+      } else if constexpr (CPL == 4) {
+        st_v2u(dst, po[0].s, po[1].s, pol);
+      } else {
+        *reinterpret_cast<uint32_t *>(dst) = po[0].s;
+      }
+    }
+  }
+}
+
+template <int CPL>
+__global__ void __launch_bounds__(128) k_fill_direct(FillArgs a) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  stage_rows(a, smem);
+  const RowRec *rows_s = reinterpret_cast<const RowRec *>(smem);
+  const int lane = threadIdx.x & 31;
+  const uint64_t pol = policy_evict_first();
+  long long u = 0;
+  if (lane == 0) u = atomicAdd(a.ctr, 1u);
+  u = __shfl_sync(0xffffffffu, u, 0);
+  while (u < a.n_units) {
+    long long nxt = 0;
+    if (lane == 0) nxt = atomicAdd(a.ctr, 1u);
+    // row-block-major order: warps across the GPU render the same rows of
+    // different envs at the same time, so the row records and shading-table
+    // slice they share stay hot in every SM's L1
+    const long long n_es = (long long)a.N * a.segs_per_row;
+    const int gidx = (int)(u / n_es);
+    const long long es = u - (long long)gidx * n_es;
+    const int env = (int)(es / a.segs_per_row);
+    const int seg = (int)(es - (long long)env * a.segs_per_row);
+    fill_unit_direct<CPL, false>(a, rows_s, pol, env, seg, gidx);
     u = __shfl_sync(0xffffffffu, nxt, 0);
   }
   finish_grid(a.ctr);

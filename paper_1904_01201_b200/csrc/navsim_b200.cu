@@ -121,6 +121,7 @@ struct nv_ctx {
   // host-buffer (e2e) path scratch
   DevBuf e_act, e_rgb, e_depth, e_sem, e_gps, e_comp, e_coll, e_disp;
   int64_t launches = 0;
+  int fill_mode = 1;   // 0: direct 256-bit stores, 1: smem stages + TMA bulk stores
   bool fused = false;  // nv_step_render uses the megakernel when the layout allows (opt-in)
   // optional per-kernel CUDA-event timing (bench roofline evidence)
   bool prof_on = false;
@@ -357,7 +358,7 @@ int launch_fill_tma(nv_ctx *c, nvk::FillArgs &a, cudaStream_t st) {
   const int bpp = (a.rgb ? 3 : 0) + (a.depth ? 4 : 0) + (a.sem ? 2 : 0);
   const int stage = RW * segw * bpp;
   const int warps = 4;
-  const size_t smem = (size_t)warps * 2 * stage;
+  const size_t smem = (size_t)a.H * sizeof(RowRec) + (size_t)warps * 2 * stage;
   auto kern = nvk::k_fill_tma<CPL, RW>;
   static int configured_smem[3] = {0, 0, 0};
   int slot = CPL == 2 ? 0 : (CPL == 4 ? 1 : 2);
@@ -435,7 +436,7 @@ int launch_mega(nv_ctx *c, Camera &cam, const int8_t *actions, uint8_t *rgb, flo
   const int segw = 32 * CPL;
   const int bpp = (rgb ? 3 : 0) + (depth ? 4 : 0) + (sem ? 2 : 0);
   const int warps = 4;
-  const size_t smem = (size_t)warps * 2 * RW * segw * std::max(bpp, 1);
+  const size_t smem = (size_t)cam.H * sizeof(RowRec) + (size_t)warps * 2 * RW * segw * std::max(bpp, 1);
   auto kern = nvk::k_step_render<CPL, RW>;
   static int configured_smem[3] = {0, 0, 0};
   int slot = CPL == 2 ? 0 : (CPL == 4 ? 1 : 2);
@@ -452,6 +453,27 @@ int launch_mega(nv_ctx *c, Camera &cam, const int8_t *actions, uint8_t *rgb, flo
   return check_launch(c);
 }
 
+template <int CPL>
+int launch_fill_direct(nv_ctx *c, nvk::FillArgs &a, cudaStream_t st) {
+  const int warps = 4;
+  auto kern = nvk::k_fill_direct<CPL>;
+  const size_t smem = (size_t)a.H * sizeof(RowRec);
+  static int configured = 0;
+  if ((int)smem > configured) {
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    configured = (int)smem;
+  }
+  int per_sm = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, warps * 32, smem));
+  per_sm = std::max(1, per_sm);
+  fill_layout<CPL>(a);
+  long long want = (a.n_units + warps - 1) / warps;
+  unsigned grid = (unsigned)std::max<long long>(1, std::min<long long>(want, (long long)per_sm * c->sm_count));
+  Prof pf(c, st, 2);
+  kern<<<grid, warps * 32, smem, st>>>(a);
+  return check_launch(c);
+}
+
 int launch_fill(nv_ctx *c, Camera &cam, int64_t N, uint8_t *rgb, float *depth, uint16_t *sem,
                 cudaStream_t st) {
   if (!rgb && !depth && !sem) return NV_OK;
@@ -464,6 +486,10 @@ int launch_fill(nv_ctx *c, Camera &cam, int64_t N, uint8_t *rgb, float *depth, u
   a.ctr = cam.ctr.as<unsigned int>();
   auto al16 = [](const void *p) { return ((uintptr_t)p & 15) == 0; };
   bool aligned = al16(rgb) && al16(depth) && al16(sem);
+  auto al32 = [](const void *p) { return ((uintptr_t)p & 31) == 0; };
+  if (c->fill_mode == 0 && aligned && al32(depth) && cam.W % 256 == 0)
+    return launch_fill_direct<8>(c, a, st);
+  if (c->fill_mode == 0 && aligned && cam.W == 128) return launch_fill_direct<4>(c, a, st);
   if (aligned && cam.W % 256 == 0) return launch_fill_tma<8>(c, a, st);
   if (aligned && cam.W == 128) return launch_fill_tma<4>(c, a, st);
   if (aligned && cam.W == 64) return launch_fill_tma<2>(c, a, st);
@@ -749,6 +775,13 @@ int nv_step_render(nv_ctx *c, const int8_t *actions, int cam, uint8_t *rgb, floa
   TRY(do_step(c, actions, collided, displacement, status, st));
   TRY(do_cast(c, cam, gps, compass, st));
   return launch_fill(c, k, c->n_envs, rgb, depth, sem, st);
+}
+
+int nv_set_fill_mode(nv_ctx *c, int mode) {
+  if (!c) return fail(NV_ERR_ARG, "ctx is NULL");
+  if (mode < 0 || mode > 1) return fail(NV_ERR_ARG, "fill mode must be 0 (direct) or 1 (tma)");
+  c->fill_mode = mode;
+  return NV_OK;
 }
 
 int nv_set_fused(nv_ctx *c, int on) {

@@ -187,29 +187,53 @@ def test_batch_step_render_vs_oracle(nb, oracle_mod, cfg, W, H, n_envs, steps):
                 assert abs(obs["compass"][e] - c) <= POSE_ATOL
 
 
-def test_tma_and_generic_paths_agree(nb):
-    """Same frames from the TMA streaming writer and the per-pixel kernel."""
+@pytest.mark.parametrize("W,H", [(256, 64), (128, 40), (512, 32)])
+def test_fill_paths_agree(nb, W, H):
+    """Identical frames from every frame writer: direct 256-bit stores (default),
+    smem stages + TMA bulk stores, the per-pixel kernel (forced by misaligned
+    outputs) and the fused megakernel."""
     from paper_1904_01201_b200 import _native as nat
     from paper_1904_01201_b200 import synth
     sc = synth.config_scene("C2")
-    n, W, H = 6, 256, 64
+    n = 6
     suite = (nb.SensorConfig("rgb", W, H), nb.SensorConfig("depth", W, H),
              nb.SensorConfig("semantic", W, H))
     sim = nb.BatchSimulator(sc.segments, sc.semantic_ids, sc.albedo, n, sensor_configs=suite)
     poses = synth.sample_poses(sc, n, seed=3)
     sim.reset(poses[:, :2], poses[:, 2])
-    sim.render()
-    ref = {k: v.clone() for k, v in sim.observations().items()}
-    # misaligned output pointers force the generic kernel
+    c, st = sim.ctx, nat.stream_handle("cuda:0")
+    outs = []
+    for mode in (0, 1):
+        nat.check(c.lib.nv_set_fill_mode(c.handle, mode))
+        sim.render()
+        torch.cuda.synchronize()
+        outs.append({k: v.clone() for k, v in sim.observations().items()})
     raw_rgb = torch.empty(n * H * W * 3 + 1, dtype=torch.uint8, device="cuda:0")
     raw_d = torch.empty(n * H * W + 1, dtype=torch.float32, device="cuda:0")
-    rgb, dep = raw_rgb[1:], raw_d[1:]
-    c = sim.ctx
-    nat.check(c.lib.nv_render(c.handle, 0, nat.ptr(rgb), nat.ptr(dep), None, None, None,
-                              nat.stream_handle("cuda:0")))
+    raw_s = torch.empty(n * H * W + 1, dtype=torch.int16, device="cuda:0")
+    rgb, dep, sem = raw_rgb[1:], raw_d[1:], raw_s[1:]
+    nat.check(c.lib.nv_render(c.handle, 0, nat.ptr(rgb), nat.ptr(dep), nat.ptr(sem), None, None, st))
     torch.cuda.synchronize()
-    assert torch.equal(rgb.view(n, H, W, 3), ref["rgb"])
-    assert torch.equal(dep.view(n, H, W), ref["depth"])
+    outs.append({"rgb": rgb.view(n, H, W, 3), "depth": dep.view(n, H, W),
+                 "semantic": sem.view(n, H, W).view(torch.uint16)})
+    for o in outs[1:]:
+        assert torch.equal(o["rgb"], outs[0]["rgb"])
+        assert torch.equal(o["depth"], outs[0]["depth"])
+        assert torch.equal(o["semantic"].view(torch.int16), outs[0]["semantic"].view(torch.int16))
+    # fused megakernel vs three launches on the same actions from the same state
+    acts = torch.as_tensor(synth.random_actions(n, 3, seed=4), device="cuda:0")
+    res = []
+    for fused in (0, 1):
+        s2 = nb.BatchSimulator(sc.segments, sc.semantic_ids, sc.albedo, n, sensor_configs=suite)
+        s2.reset(poses[:, :2], poses[:, 2])
+        nat.check(s2.ctx.lib.nv_set_fused(s2.ctx.handle, fused))
+        for s in range(3):
+            s2.step(acts[s])
+        torch.cuda.synchronize()
+        res.append(({k: v.clone() for k, v in s2.observations().items()}, s2.state()[0].clone()))
+    for k in ("rgb", "depth"):
+        assert torch.equal(res[0][0][k], res[1][0][k])
+    assert torch.equal(res[0][1], res[1][1])
 
 
 def test_full_size_properties(nb):
@@ -292,3 +316,55 @@ def test_raycast_stress_vs_oracle(nb, oracle_mod, cfg):
             to, io = osc.raycast((x, y), d, t_max=t_max)
             assert np.array_equal(ig, io)
             assert np.array_equal(tg, to)
+
+
+def _graph_from_golden(nb, g):
+    walls = [nb.WallSegment(a=(s[0], s[1]), b=(s[2], s[3]), semantic_id=int(i),
+                            albedo=tuple(float(c) for c in a))
+             for s, i, a in zip(g["segments"], g["semantic_ids"], g["albedo"])]
+    sc = nb.Scene(id="golden", walls=walls, floor_color=tuple(g["floor_color"]),
+                  ceiling_color=tuple(g["ceiling_color"]), wall_height=float(g["wall_height"]))
+    return nb.build_scene_graph(sc)
+
+
+def test_simulator_facade_matches_reference(nb):
+    """The drop-in Simulator (sim.py:133-219 API) replays the reference's
+    recorded episode: poses within 1e-6, identical collision flags, reference
+    errors raised (tests/test_sim.py:354-409 behaviours)."""
+    g = load_golden("square")
+    graph = _graph_from_golden(nb, g)
+    sim = nb.Simulator(graph, sensor_configs=(nb.SensorConfig("rgb", 64, 48),
+                                               nb.SensorConfig("depth", 64, 48),
+                                               nb.SensorConfig("gps_compass")))
+    with pytest.raises(nb.SimError, match="reset"):
+        sim.step(nb.Action.MOVE_FORWARD)
+    with pytest.raises(nb.SimError, match="radius"):
+        sim.set_agent_state((0.05, 5.0), 0.0)
+    x, y, h = g["kin_starts"][0]
+    sim.set_agent_state((x, y), h)
+    acts = (nb.Action.MOVE_FORWARD, nb.Action.TURN_LEFT, nb.Action.TURN_RIGHT, nb.Action.STOP)
+    for s, a in enumerate(g["kin_actions"][0][:120]):
+        res, obs = sim.step(acts[int(a)])
+        ref = g["kin_states"][0][s]
+        assert abs(sim.state.position[0] - ref[0]) <= POSE_ATOL
+        assert abs(sim.state.position[1] - ref[1]) <= POSE_ATOL
+        assert abs(sim.state.heading - ref[2]) <= POSE_ATOL
+        assert res.collided == bool(g["kin_collided"][0][s])
+        assert obs.rgb.shape == (48, 64, 3) and obs.rgb.dtype == np.float64
+        assert obs.depth.shape == (48, 64) and obs.gps.shape == (2,)
+    with pytest.raises(nb.SimError, match="wall height"):
+        nb.Simulator(graph, nb.AgentConfig(sensor_height=3.0))
+
+
+def test_blind_and_gps_only(nb):
+    g = load_golden("square")
+    graph = _graph_from_golden(nb, g)
+    sim = nb.Simulator(graph, sensor_configs=())
+    sim.set_agent_state((5.0, 5.0), 0.0)
+    _, obs = sim.step(nb.Action.MOVE_FORWARD)
+    assert obs.rgb is None and obs.depth is None and obs.gps is None
+    sim = nb.Simulator(graph, sensor_configs=(nb.SensorConfig("gps_compass"),))
+    sim.set_agent_state((5.0, 5.0), 1.1)
+    _, obs = sim.step(nb.Action.MOVE_FORWARD)
+    assert np.allclose(obs.gps, [0.25, 0.0], atol=1e-12)   # tests/test_sim.py:412-418
+    assert obs.compass == pytest.approx(0.0, abs=1e-12)
