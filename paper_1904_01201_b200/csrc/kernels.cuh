@@ -358,14 +358,28 @@ __device__ void warp_cast_disc(const SceneView &sc, double px, double py, double
   double u2 = add(mul(ux, ux), mul(uy, uy));
   double bt = NV_INF;
   int bi = 0x7fffffff;
+  // f32 prefilter on the cell-relative endpoints: any contact (face, band or
+  // endpoint case of disc_cast) needs a point of the segment within `radius`
+  // of a point of the sweep, so the segment's box must meet the sweep's box
+  // grown by radius; the 1e-3 m slack dwarfs every f32/f64 rounding at these
+  // magnitudes.  Skipped segments are ones disc_cast finds no valid t for.
+  const float grow = (float)radius + 1e-3f;
   for (int cy = cy0; cy <= cy1; ++cy)
     for (int cx = cx0; cx <= cx1; ++cx) {
       int c = cy * sc.gnx + cx;
       int q0 = __ldg(sc.starts + c), q1 = __ldg(sc.starts + c + 1);
+      if (q0 == q1) continue;
+      const double X0 = add(sc.x0, (double)cx), Y0 = add(sc.y0, (double)cy);
+      const float sx0 = (float)sub(lox, X0) - grow, sx1 = (float)sub(hix, X0) + grow;
+      const float sy0 = (float)sub(loy, Y0) - grow, sy1 = (float)sub(hiy, Y0) + grow;
       for (int q = q0 + lane; q < q1; q += 32) {
+        const float4 f = __ldg(sc.entf + q);
+        if (fmaxf(f.x, f.z) < sx0 || fminf(f.x, f.z) > sx1 || fmaxf(f.y, f.w) < sy0 ||
+            fminf(f.y, f.w) > sy1)
+          continue;
         int i = __ldg(sc.items + q);
-        double t = disc_seg_t(px, py, ux, uy, radius, u2, __ldg(sc.ax + i),
-                              __ldg(sc.ay + i), __ldg(sc.bx + i), __ldg(sc.by + i));
+        double t = disc_seg_t(px, py, ux, uy, radius, u2, __ldg(sc.ax + i), __ldg(sc.ay + i),
+                              __ldg(sc.bx + i), __ldg(sc.by + i));
         lex_min(bt, bi, t, i);
       }
     }
