@@ -235,6 +235,7 @@ def run_gpu(args):
     sim.reset(poses[:, :2], poses[:, 2])
     nat.check(sim.ctx.lib.nv_set_fused(sim.ctx.handle, 1 if args.fused else 0))
     nat.check(sim.ctx.lib.nv_set_fill_mode(sim.ctx.handle, args.fill_mode))
+    nat.check(sim.ctx.lib.nv_set_cast_mode(sim.ctx.handle, args.cast_mode))
     total_steps = args.warmup + args.steps
     acts = torch.as_tensor(synth.random_actions(shard.n_total, total_steps, seed=2)[:, shard.lo:shard.hi].copy(),
                            device=f"cuda:{local}")
@@ -389,6 +390,7 @@ def run_gpu(args):
                        "triangles": sc.n_triangles, "parallelism": f"env-shard x{world}",
                        "cuda_graph": use_graph, "fused_megakernel": fused,
                        "fill_mode": ["direct-256b-stores", "tma-bulk-stores"][args.fill_mode],
+                       "cast_mode": ["dda", "binned"][args.cast_mode],
                        "l2": f"no flush: frames written per step "
                              f"({step_bytes / 1e6:.0f} MB/GPU) exceed the 126 MB L2"},
             "roofline": {"bound": "hbm", "kernel": dom,
@@ -425,6 +427,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--fill-mode", type=int, default=1, help="0 direct stores, 1 TMA bulk stores")
+    ap.add_argument("--cast-mode", type=int, default=0, help="0 per-column DDA, 1 binned")
     ap.add_argument("--fused", action="store_true", help="one megakernel launch per step (experimental)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -122,6 +122,11 @@ int nv_step_render(nv_ctx *ctx, const int8_t *actions, int cam, uint8_t *rgb,
 
 /* Enable / disable (default) the single-launch megakernel of nv_step_render. */
 int nv_set_fused(nv_ctx *ctx, int on);
+/* Column cast: 0 (default) = per-column DDA over the grid (raycast_grid's
+ * walk), 1 = binned: one CTA per env projects the frustum's segments to
+ * column spans and tests (segment, column) pairs exactly (raycast_all's
+ * lexicographic minimum, which the reference defines raycast_grid to equal). */
+int nv_set_cast_mode(nv_ctx *ctx, int mode);
 /* Frame writer: 0 = 256-bit direct stores from registers,
  * 1 (default) = shared-memory stages written out by TMA bulk copies. */
 int nv_set_fill_mode(nv_ctx *ctx, int mode);

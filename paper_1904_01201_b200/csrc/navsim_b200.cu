@@ -121,6 +121,7 @@ struct nv_ctx {
   // host-buffer (e2e) path scratch
   DevBuf e_act, e_rgb, e_depth, e_sem, e_gps, e_comp, e_coll, e_disp;
   int64_t launches = 0;
+  int cast_mode = 0;  // 0: per-column DDA (default), 1: binned (tile-binned segment setup)
   int fill_mode = 1;   // 0: direct 256-bit stores, 1: smem stages + TMA bulk stores
   bool fused = false;  // nv_step_render uses the megakernel when the layout allows (opt-in)
   // optional per-kernel CUDA-event timing (bench roofline evidence)
@@ -511,18 +512,37 @@ int cam_check(nv_ctx *c, int cam) {
 
 int do_cast(nv_ctx *c, int cam, double *gps, double *compass, cudaStream_t st) {
   Camera &k = c->cams[cam];
+  if (c->cast_mode == 1 && k.W <= 2048) {
+    const int ntiles = (k.W + NV_COLTILE - 1) / NV_COLTILE;
+    const size_t smem = (size_t)k.W * (8 + 8 + 8) + (size_t)NV_BIN_MAXCELLS * (16 + 4) +
+                        (size_t)((k.W + 3) & ~3) * 4 + (size_t)((ntiles + 3) & ~3) * 4 +
+                        (size_t)NV_HIT_CAP * 8 + 32;
+    static size_t configured = 0;
+    if (smem > configured) {
+      CK(cudaFuncSetAttribute(nvk::k_cast_binned, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)smem));
+      configured = smem;
+    }
+    Prof pf(c, st, 1);
+    nvk::k_cast_binned<<<(unsigned)c->n_envs, 128, smem, st>>>(
+        c->env_view(), c->scene_view(), cam_view(k), k.focal, k.rec.as<ColRec>(), gps, compass);
+    return check_launch(c);
+  }
   // t_max = max_range: capping the walk is output-identical for rendered
   // frames (tests/test_gpu_parity.py checks it against the
   // reference's uncapped t_max = 1e9 render).
-  // Non-persistent launch: a block's 4 warps are 128 adjacent columns of one
-  // env, which share their cells in L1 (a persistent packet-pulling variant
-  // measured 30 % slower: it loses that locality).
   const long long total = c->n_envs * (long long)k.W;
   Prof pf(c, st, 1);
   nvk::k_column_cast<<<blocks_for(total, 128), 128, 0, st>>>(
       c->env_view(), c->scene_view(), cam_view(k), k.rec.as<ColRec>(), k.max_range, gps,
       compass);
   return check_launch(c);
+}
+
+int nv_set_cast_mode_(nv_ctx *c, int mode) {
+  if (mode < 0 || mode > 1) return fail(NV_ERR_ARG, "cast mode must be 0 (dda) or 1 (binned)");
+  c->cast_mode = mode;
+  return NV_OK;
 }
 
 int do_step(nv_ctx *c, const int8_t *actions, uint8_t *collided, double *disp, int32_t *status,
@@ -778,6 +798,11 @@ int nv_step_render(nv_ctx *c, const int8_t *actions, int cam, uint8_t *rgb, floa
   TRY(do_step(c, actions, collided, displacement, status, st));
   TRY(do_cast(c, cam, gps, compass, st));
   return launch_fill(c, k, c->n_envs, rgb, depth, sem, st);
+}
+
+int nv_set_cast_mode(nv_ctx *c, int mode) {
+  if (!c) return fail(NV_ERR_ARG, "ctx is NULL");
+  return nv_set_cast_mode_(c, mode);
 }
 
 int nv_set_fill_mode(nv_ctx *c, int mode) {

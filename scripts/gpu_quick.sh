@@ -7,8 +7,8 @@ python -c "
 import json; d=json.load(open('gpurun_out/${TAG}_bench.json'))
 print('value', round(d['value']), 'ms/step', round(d['ms_per_step'],4), 'frac', round(d['roofline']['frac'],3), d['roofline']['kernel'][:14], 'kernel_ms', {k: round(v,4) for k,v in d['roofline']['kernel_ms'].items()}, 'e2e', d['e2e'] and round(d['e2e']['value']), 'clocks', d['clocks'])
 "
-timeout 600 python bench.py --steps 30 --warmup 5 --no-cpu-baseline --no-e2e --fill-mode 0 > gpurun_out/${1:-q}_bench_fused.json 2>/dev/null
+timeout 600 python bench.py --steps 30 --warmup 5 --no-cpu-baseline --no-e2e --cast-mode 1 > gpurun_out/${1:-q}_bench_fused.json 2>/dev/null
 python -c "
 import json; d=json.load(open('gpurun_out/${1:-q}_bench_fused.json'))
-print('DIRECT-FILL value', round(d['value']), 'ms/step', round(d['ms_per_step'],4), 'kernel_ms', {k: round(v,4) for k,v in d['roofline']['kernel_ms'].items()})
+print('BINNED-CAST value', round(d['value']), 'ms/step', round(d['ms_per_step'],4), 'kernel_ms', {k: round(v,4) for k,v in d['roofline']['kernel_ms'].items()})
 "
