@@ -11,7 +11,7 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libnavsim_b200.so")
+LIB_PATH = os.environ.get("NAVSIM_B200_LIB") or os.path.join(_HERE, "_lib", "libnavsim_b200.so")
 
 NV_OK = 0
 NV_ERR_ARG = -1

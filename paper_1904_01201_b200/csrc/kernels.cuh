@@ -41,7 +41,7 @@ using nvx::sub;
 
 // SegmentIndex._cell_of (geometry.py:146-149): trunc toward zero, clamp.
 __device__ __forceinline__ int cell_coord(double v, double o, int n) {
-  double d = div(sub(v, o), 1.0);
+  double d = sub(v, o);  // (v - o) / CELL with CELL = 1.0: division by 1 is exact
   if (!(d >= 1.0)) return 0;
   if (d >= (double)(n - 1)) return n - 1;
   return (int)d;
@@ -206,8 +206,9 @@ __device__ __forceinline__ void ray_grid(const SceneView &sc, double px, double 
     out_i = best_i;
     return;
   }
-  long long cx = (long long)floor(div(sub(px, sc.x0), cell));
-  long long cy = (long long)floor(div(sub(py, sc.y0), cell));
+  // (p - x0) / cell with cell = 1.0 is exact without the division
+  long long cx = (long long)floor(sub(px, sc.x0));
+  long long cy = (long long)floor(sub(py, sc.y0));
   const int stepx = dx > 0.0 ? 1 : -1;
   const int stepy = dy > 0.0 ? 1 : -1;
   double tnx, tdx, tny, tdy;
@@ -364,25 +365,73 @@ __device__ void warp_cast_disc(const SceneView &sc, double px, double py, double
   // grown by radius; the 1e-3 m slack dwarfs every f32/f64 rounding at these
   // magnitudes.  Skipped segments are ones disc_cast finds no valid t for.
   const float grow = (float)radius + 1e-3f;
-  for (int cy = cy0; cy <= cy1; ++cy)
-    for (int cx = cx0; cx <= cx1; ++cx) {
-      int c = cy * sc.gnx + cx;
-      int q0 = __ldg(sc.starts + c), q1 = __ldg(sc.starts + c + 1);
-      if (q0 == q1) continue;
-      const double X0 = add(sc.x0, (double)cx), Y0 = add(sc.y0, (double)cy);
+  const int ncx = cx1 - cx0 + 1, ncell = ncx * (cy1 - cy0 + 1);
+  if (ncell <= 32) {
+    // all query cells at once: lane k owns cell k's run; a warp prefix sum
+    // flattens the runs so every lane tests independent candidates
+    int cnt = 0, q0 = 0, cxk = 0, cyk = 0;
+    if (lane < ncell) {
+      cyk = cy0 + lane / ncx;
+      cxk = cx0 + lane % ncx;
+      const int c = cyk * sc.gnx + cxk;
+      q0 = __ldg(sc.starts + c);
+      cnt = __ldg(sc.starts + c + 1) - q0;
+    }
+    int incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
+    }
+    const int total = __shfl_sync(0xffffffffu, incl, 31);
+    for (int base = 0; base < total; base += 32) {
+      const int g = min(base + lane, total - 1);
+      int o = 0;
+#pragma unroll
+      for (int b = 16; b > 0; b >>= 1) {
+        const int v = __shfl_sync(0xffffffffu, incl, o + b - 1);
+        if (v <= g) o += b;
+      }
+      const int oq0 = __shfl_sync(0xffffffffu, q0, o);
+      const int oincl = __shfl_sync(0xffffffffu, incl, o);
+      const int ocnt = __shfl_sync(0xffffffffu, cnt, o);
+      const int ocx = __shfl_sync(0xffffffffu, cxk, o);
+      const int ocy = __shfl_sync(0xffffffffu, cyk, o);
+      if (base + lane >= total) continue;
+      const int q = oq0 + (g - (oincl - ocnt));
+      const double X0 = add(sc.x0, (double)ocx), Y0 = add(sc.y0, (double)ocy);
       const float sx0 = (float)sub(lox, X0) - grow, sx1 = (float)sub(hix, X0) + grow;
       const float sy0 = (float)sub(loy, Y0) - grow, sy1 = (float)sub(hiy, Y0) + grow;
-      for (int q = q0 + lane; q < q1; q += 32) {
-        const float4 f = __ldg(sc.entf + q);
-        if (fmaxf(f.x, f.z) < sx0 || fminf(f.x, f.z) > sx1 || fmaxf(f.y, f.w) < sy0 ||
-            fminf(f.y, f.w) > sy1)
-          continue;
-        int i = __ldg(sc.items + q);
-        double t = disc_seg_t(px, py, ux, uy, radius, u2, __ldg(sc.ax + i), __ldg(sc.ay + i),
-                              __ldg(sc.bx + i), __ldg(sc.by + i));
-        lex_min(bt, bi, t, i);
-      }
+      const float4 f = __ldg(sc.entf + q);
+      if (fmaxf(f.x, f.z) < sx0 || fminf(f.x, f.z) > sx1 || fmaxf(f.y, f.w) < sy0 ||
+          fminf(f.y, f.w) > sy1)
+        continue;
+      int i = __ldg(sc.items + q);
+      double t = disc_seg_t(px, py, ux, uy, radius, u2, __ldg(sc.ax + i), __ldg(sc.ay + i),
+                            __ldg(sc.bx + i), __ldg(sc.by + i));
+      lex_min(bt, bi, t, i);
     }
+  } else {
+    for (int cy = cy0; cy <= cy1; ++cy)
+      for (int cx = cx0; cx <= cx1; ++cx) {
+        int c = cy * sc.gnx + cx;
+        int q0 = __ldg(sc.starts + c), q1 = __ldg(sc.starts + c + 1);
+        if (q0 == q1) continue;
+        const double X0 = add(sc.x0, (double)cx), Y0 = add(sc.y0, (double)cy);
+        const float sx0 = (float)sub(lox, X0) - grow, sx1 = (float)sub(hix, X0) + grow;
+        const float sy0 = (float)sub(loy, Y0) - grow, sy1 = (float)sub(hiy, Y0) + grow;
+        for (int q = q0 + lane; q < q1; q += 32) {
+          const float4 f = __ldg(sc.entf + q);
+          if (fmaxf(f.x, f.z) < sx0 || fminf(f.x, f.z) > sx1 || fmaxf(f.y, f.w) < sy0 ||
+              fminf(f.y, f.w) > sy1)
+            continue;
+          int i = __ldg(sc.items + q);
+          double t = disc_seg_t(px, py, ux, uy, radius, u2, __ldg(sc.ax + i), __ldg(sc.ay + i),
+                                __ldg(sc.bx + i), __ldg(sc.by + i));
+          lex_min(bt, bi, t, i);
+        }
+      }
+  }
   warp_lex_min(bt, bi);
   if (!(bt < NV_INF) || bi == 0x7fffffff) {  // t is inf whenever nothing hit
     t_out = NV_INF;
@@ -850,7 +899,7 @@ __device__ __forceinline__ bool bin_cell(const SceneView &sc, const BinShared &S
 __global__ void __launch_bounds__(128) k_cast_binned(EnvView ev, SceneView sc, CamView cam,
                                                      double focal, ColRec *__restrict__ rec,
                                                      double *gps, double *compass) {
-  extern __shared__ __align__(16) uint8_t smem[];
+  extern __shared__ __align__(128) uint8_t smem[];
   const int W = cam.W;
   const int ntiles = (W + NV_COLTILE - 1) / NV_COLTILE;
   BinShared S;

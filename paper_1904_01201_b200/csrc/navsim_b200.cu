@@ -352,9 +352,12 @@ void fill_layout(nvk::FillArgs &a) {
 
 // Fill launch: TMA streaming writer when the row layout allows 16-byte bulk
 // copies, else the generic per-pixel kernel.
+#ifndef NV_FILL_RW
+#define NV_FILL_RW 2
+#endif
 template <int CPL>
 int launch_fill_tma(nv_ctx *c, nvk::FillArgs &a, cudaStream_t st) {
-  constexpr int RW = 2;
+  constexpr int RW = NV_FILL_RW;
   const int segw = 32 * CPL;
   const int bpp = (a.rgb ? 3 : 0) + (a.depth ? 4 : 0) + (a.sem ? 2 : 0);
   const int stage = RW * segw * bpp;

@@ -12,3 +12,10 @@ python -c "
 import json; d=json.load(open('gpurun_out/${1:-q}_bench_fused.json'))
 print('BINNED-CAST value', round(d['value']), 'ms/step', round(d['ms_per_step'],4), 'kernel_ms', {k: round(v,4) for k,v in d['roofline']['kernel_ms'].items()})
 "
+if [ -f paper_1904_01201_b200/_lib/libnavsim_b200_rw4.so ]; then
+NAVSIM_B200_LIB=$PWD/paper_1904_01201_b200/_lib/libnavsim_b200_rw4.so timeout 600 python bench.py --steps 30 --warmup 5 --no-cpu-baseline --no-e2e > gpurun_out/${1:-q}_bench_rw4.json 2>/dev/null
+python -c "
+import json; d=json.load(open('gpurun_out/${1:-q}_bench_rw4.json'))
+print('RW4 value', round(d['value']), 'ms/step', round(d['ms_per_step'],4), 'kernel_ms', {k: round(v,4) for k,v in d['roofline']['kernel_ms'].items()})
+"
+fi
