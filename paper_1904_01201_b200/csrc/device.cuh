@@ -20,6 +20,8 @@
 
 #include <stdint.h>
 
+#define NV_CHUNK 8  // entries per prefilter box (cast)
+
 namespace nvd {
 
 struct __align__(16) CellEntry {
@@ -36,6 +38,8 @@ struct SceneView {
   const int32_t *items;  // same order, index only (disc casts)
   const float4 *entf;    // same order, f32 endpoints (a - X0c, b - X0c), X0c = x0 + cx
   const float *cellb;    // per cell: max |endpoint - X0c|_1 over its items
+  const int4 *cells;     // per cell: {starts[c], starts[c+1], bits(bound), first chunk}
+  const float4 *chunks;  // per run of NV_CHUNK entries: f32 box (x0, y0, x1, y1), cell-relative
   double x0, y0;
   int gnx, gny;
   int64_t n;
@@ -82,7 +86,6 @@ struct CamView {
   const double *tc;  // H: (wall_h - cam_h) / v for v > 0 rows
   const double *tf;  // H: -cam_h / v for v < 0 rows
   const RowRec *rows;
-  const uint16_t *inv;  // H x W f16: 1/sqrt(1 + u_j^2 + v_i^2) (env-independent)
 };
 
 }  // namespace nvd

@@ -195,6 +195,16 @@ __device__ __forceinline__ void test_cell_f32(const SceneView &sc, int q0, int q
 }
 
 // raycast_grid (_kernels.py:51-120), one ray, exact replica of the DDA.
+// The walk is software-pipelined: the next cell's record {q0, q1, bound} is
+// loaded (one 16-byte load) before the current cell's entries are tested, so
+// the cell-to-cell latency overlaps the tests; the visit order and the
+// early-out are the reference's.
+#ifndef NV_CAST_NB
+#define NV_CAST_NB 8
+#endif
+#ifndef NV_CAST_CHUNKS
+#define NV_CAST_CHUNKS 1
+#endif
 __device__ __forceinline__ void ray_grid(const SceneView &sc, double px, double py,
                                          double dx, double dy, double t_max,
                                          double &out_t, int &out_i) {
@@ -231,24 +241,53 @@ __device__ __forceinline__ void ray_grid(const SceneView &sc, double px, double 
   const long long gnx = sc.gnx, gny = sc.gny;
   const float dxf = (float)dx, dyf = (float)dy;
   const float sd = (fabsf(dxf) + fabsf(dyf)) * (1.0f + 0x1p-20f);
+  const bool pos_dx = dxf >= 0.0f, pos_dy = dyf >= 0.0f;
+  (void)pos_dx; (void)pos_dy;
+  auto inb = [&](long long x, long long y) { return 0 <= x && x < gnx && 0 <= y && y < gny; };
+  int4 rec = make_int4(0, 0, 0, 0);
+  if (inb(cx, cy)) rec = __ldg(sc.cells + (cy * gnx + cx));
   for (int guard = 0; guard < (1 << 24); ++guard) {
-    if (0 <= cx && cx < gnx && 0 <= cy && cy < gny) {
-      int c = (int)(cy * gnx + cx);
-      int q0 = __ldg(sc.starts + c), q1 = __ldg(sc.starts + c + 1);
-      if (q1 > q0) {
-        const CellF cf = cell_f32(sc, (int)cx, (int)cy, c, px, py, dxf, dyf, sd);
-        test_cell_f32<4>(sc, q0, q1, cf, px, py, dx, dy, dxf, dyf, best_t, best_i);
-      }
-    }
-    double t_exit = tnx < tny ? tnx : tny;
-    if (best_t <= t_exit || t_exit > t_max) break;
+    const double t_exit = tnx < tny ? tnx : tny;
+    // the cell after this one (the reference advances to it unless it stops)
+    long long ncx = cx, ncy = cy;
+    double ntnx = tnx, ntny = tny;
     if (tnx < tny) {
-      cx += stepx;
-      tnx = add(tnx, tdx);
+      ncx += stepx;
+      ntnx = add(tnx, tdx);
     } else {
-      cy += stepy;
-      tny = add(tny, tdy);
+      ncy += stepy;
+      ntny = add(tny, tdy);
     }
+    int4 nrec = make_int4(0, 0, 0, 0);
+    if (!(t_exit > t_max) && inb(ncx, ncy)) nrec = __ldg(sc.cells + (ncy * gnx + ncx));
+    if (rec.y > rec.x) {
+      const double X0 = add(sc.x0, (double)cx), Y0 = add(sc.y0, (double)cy);
+      const float pxr = (float)sub(px, X0), pyr = (float)sub(py, Y0);
+      CellF cf;
+      cf.cp = fmaf(dxf, pyr, -(dyf * pxr));
+      cf.E = NV_K32 * sd * (__int_as_float(rec.z) + fabsf(pxr) + fabsf(pyr) + 1e-30f);
+#if NV_CAST_CHUNKS
+      // s(x, y) = d x ((x, y) - p) is linear, so over a run's box it is
+      // bounded by two corners; a run whose box lies beyond +-E on one side
+      // holds no entry the per-entry side test would keep.
+      for (int q = rec.x, ch = rec.w; q < rec.y; q += NV_CHUNK, ++ch) {
+        const float4 b = __ldg(sc.chunks + ch);
+        const float smin = fmaf(dxf, pos_dx ? b.y : b.w, -(dyf * (pos_dy ? b.z : b.x))) - cf.cp;
+        const float smax = fmaf(dxf, pos_dx ? b.w : b.y, -(dyf * (pos_dy ? b.x : b.z))) - cf.cp;
+        if (smin > cf.E || smax < -cf.E) continue;
+        test_cell_f32<NV_CAST_NB>(sc, q, min(q + NV_CHUNK, rec.y), cf, px, py, dx, dy, dxf, dyf,
+                                  best_t, best_i);
+      }
+#else
+      test_cell_f32<NV_CAST_NB>(sc, rec.x, rec.y, cf, px, py, dx, dy, dxf, dyf, best_t, best_i);
+#endif
+    }
+    if (best_t <= t_exit || t_exit > t_max) break;
+    cx = ncx;
+    cy = ncy;
+    tnx = ntnx;
+    tny = ntny;
+    rec = nrec;
     if (cx < 0 || cx >= gnx || cy < 0 || cy >= gny) {
       bool out_x = (cx < 0 && dx <= 0.0) || (cx >= gnx && dx >= 0.0);
       bool out_y = (cy < 0 && dy <= 0.0) || (cy >= gny && dy >= 0.0);
@@ -1178,7 +1217,8 @@ __global__ void __launch_bounds__(128) k_clearance(SceneView sc, const double *p
 // void when s >= max_range); lo/hi were classified exactly in FP64 by the
 // column epilogue.  Depth (f32) and semantic (u16) are selected exactly.  RGB
 // is shaded in f16 pairs, two pixels per instruction:
-//   t   = 0.2 + (0.8 cos-numerator) * inv      inv = 1/|(d, v)| from a table
+//   t   = 0.2 + (0.8 cos-numerator) * inv      inv = 1/|(d, v)| from the f16 table
+//                                              invh (env-independent; rows mirrored)
 //   c8  = round(col255 * t)                    via HFMA2(col255, t, 1024): the
 //                                              low byte of the f16 result
 // Worst-case error vs the reference's f64 rgb: 0.5 (rounding) + 0.0625 (f16
@@ -1190,7 +1230,6 @@ __global__ void __launch_bounds__(128) k_clearance(SceneView sc, const double *p
 struct FillArgs {
   const ColRec *rec;
   const RowRec *rows;
-  const uint16_t *inv;  // H x W f16 shading table
   int N, W, H;
   uint8_t *rgb;
   float *depth;
@@ -1200,6 +1239,8 @@ struct FillArgs {
   int segs_per_row;    // W / (32 * CPL)
   long long n_units;   // N * segs_per_row * units_per_seg
   unsigned int *ctr;   // [0] next unit, [1] finished warps (self-resetting)
+  const uint16_t *invh;  // ceil(H/2) x W f16 shading table 1/|(d_j, v_i)|, rows
+                         // mirrored (v_{H-1-i} = -v_i); env-independent
 };
 
 __device__ __forceinline__ uint32_t h2_fma(uint32_t a, uint32_t b, uint32_t c) {
@@ -1246,6 +1287,14 @@ __device__ __forceinline__ uint64_t policy_evict_first() {
   uint64_t p;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(p));
   return p;
+}
+
+// L1 prefetch of a lane's CPL column records (the next work unit's).
+template <int CPL>
+__device__ __forceinline__ void prefetch_cols(const ColRec *rp) {
+#pragma unroll
+  for (int k = 0; k < CPL * (int)sizeof(ColRec); k += 128)
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(reinterpret_cast<const char *>(rp) + k));
 }
 
 // A lane's CPL columns (CPL/2 pixel pairs) in registers, packed.
@@ -1319,20 +1368,27 @@ __device__ __forceinline__ void pack_rgb4(const PairOut &p, const PairOut &q, ui
   w2 = __byte_perm(rg1, q.b, 0x6324);                  // b2 r3 g3 b3
 }
 
-// Row record (from the CTA's shared-memory copy of the row table) + this
-// lane's CPL shading-table entries of row i.
-template <int CPL>
-__device__ __forceinline__ void load_row(const FillArgs &a, const RowRec *rows_s, uint32_t i,
-                                         int col0, uint4 &q0, uint4 &q1, uint32_t (&iv)[CPL / 2]) {
+// Row record of row i from the CTA's shared-memory copy of the row table.
+__device__ __forceinline__ void load_row(const RowRec *rows_s, uint32_t i, uint4 &q0, uint4 &q1) {
   const uint4 *rq = reinterpret_cast<const uint4 *>(rows_s + i);
   q0 = rq[0];
   q1 = rq[1];
-  const uint16_t *ip = a.inv + (size_t)i * a.W + col0;
+}
+
+// Shading-table row of image row i: the table holds rows [0, ceil(H/2)) and
+// row H-1-i equals row i (v_{H-1-i} = -v_i exactly).
+__device__ __forceinline__ uint32_t inv_row(uint32_t i, int H) {
+  return i < (uint32_t)(H >> 1) ? i : (uint32_t)(H - 1) - i;
+}
+
+// The lane's CPL shading-table entries (CPL/2 f16 pairs) from global memory.
+template <int CPL>
+__device__ __forceinline__ void load_inv_g(const uint16_t *ip, uint32_t (&iv)[CPL / 2]) {
   if constexpr (CPL == 8) {
-    uint4 v = __ldg(reinterpret_cast<const uint4 *>(ip));
+    const uint4 v = __ldg(reinterpret_cast<const uint4 *>(ip));
     iv[0] = v.x; iv[1] = v.y; iv[2] = v.z; iv[3] = v.w;
   } else if constexpr (CPL == 4) {
-    uint2 v = __ldg(reinterpret_cast<const uint2 *>(ip));
+    const uint2 v = __ldg(reinterpret_cast<const uint2 *>(ip));
     iv[0] = v.x; iv[1] = v.y;
   } else {
     iv[0] = __ldg(reinterpret_cast<const uint32_t *>(ip));
@@ -1383,9 +1439,11 @@ struct FillWarp {
 // like global memory, which lane 0 writes out with cp.async.bulk (one copy
 // per channel per stage when a warp covers full rows), evict-first in L2.
 // COH: the column records were written earlier in the same launch.
+// pf: the lane's column records of the warp's next unit (prefetched into L1
+// half-way through this one), or nullptr.
 template <int CPL, int RW, bool COH>
 __device__ __forceinline__ void fill_unit(const FillArgs &a, FillWarp<CPL, RW> &fw, int env,
-                                          int seg, int gidx) {
+                                          int seg, int gidx, const ColRec *pf = nullptr) {
   constexpr int NS = FillWarp<CPL, RW>::NS;
   constexpr int SEGW = FillWarp<CPL, RW>::SEGW;
   const int lane = threadIdx.x & 31;
@@ -1395,11 +1453,10 @@ __device__ __forceinline__ void fill_unit(const FillArgs &a, FillWarp<CPL, RW> &
   load_cols<CPL, COH>(a.rec + (size_t)env * W + col0, cr);
   const int r_begin = gidx * a.rows_per_unit;
   const int r_end = min(H, r_begin + a.rows_per_unit);
-  uint4 pq0, pq1;
-  uint32_t piv[CPL / 2];
-  load_row<CPL>(a, fw.rows_s, (uint32_t)r_begin, col0, pq0, pq1, piv);
+  const int r_pf = r_begin + ((r_end - r_begin) >> 1);
   for (int r0 = r_begin; r0 < r_end; r0 += RW) {
     const int nr = min(RW, r_end - r0);
+    if (pf && r0 <= r_pf && r_pf < r0 + RW) prefetch_cols<CPL>(pf);
     uint8_t *buf = fw.wbase + (fw.k & (NS - 1)) * fw.stage_bytes;
     if (fw.k >= NS) {
       if (lane == 0) bulk_wait_read<NS - 1>();
@@ -1407,7 +1464,8 @@ __device__ __forceinline__ void fill_unit(const FillArgs &a, FillWarp<CPL, RW> &
     }
     for (int rr = 0; rr < nr; ++rr) {
       const uint32_t i = (uint32_t)(r0 + rr);
-      // this row's loads were issued one row ahead (software pipelining)
+      uint4 pq0, pq1;
+      load_row(fw.rows_s, i, pq0, pq1);
       RowRec R;
       R.depth_p = __uint_as_float(pq0.x);
       R.sem2 = pq0.y;
@@ -1416,9 +1474,7 @@ __device__ __forceinline__ void fill_unit(const FillArgs &a, FillWarp<CPL, RW> &
       R.g2 = pq1.x;
       R.b2 = pq1.y;
       uint32_t iv[CPL / 2];
-#pragma unroll
-      for (int c = 0; c < CPL / 2; ++c) iv[c] = piv[c];
-      load_row<CPL>(a, fw.rows_s, min(i + 1, (uint32_t)(r_end - 1)), col0, pq0, pq1, piv);
+      load_inv_g<CPL>(a.invh + (size_t)inv_row(i, H) * W + col0, iv);
       PairOut po[CPL / 2];
 #pragma unroll
       for (int c = 0; c < CPL / 2; ++c)
@@ -1512,29 +1568,493 @@ __device__ __forceinline__ void finish_grid(unsigned int *ctr) {
 // k_fill_tma: streaming frame writer over all units of a frame batch; units
 // are pulled from a self-resetting global counter (one prefetched ahead).
 template <int CPL, int RW>
-__global__ void __launch_bounds__(128) k_fill_tma(FillArgs a) {
+#ifndef NV_FILL_MINB
+#define NV_FILL_MINB 5
+#endif
+__global__ void __launch_bounds__(128, NV_FILL_MINB) k_fill_tma(FillArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
   const int lane = threadIdx.x & 31;
   FillWarp<CPL, RW> fw;
   fw.init(a, smem, threadIdx.x >> 5);
-  long long u = 0;
-  if (lane == 0) u = atomicAdd(a.ctr, 1u);
+  // Units are claimed two ahead: the current one, the next one (whose column
+  // records are prefetched into L1 during the current one) and, in flight,
+  // the one after.  Row-block-major order: warps across the GPU render the
+  // same rows of different envs at the same time.
+  const long long n_es = (long long)a.N * a.segs_per_row;
+  long long u = 0, nxt = 0;
+  if (lane == 0) {
+    u = atomicAdd(a.ctr, 1u);
+    nxt = atomicAdd(a.ctr, 1u);
+  }
   u = __shfl_sync(0xffffffffu, u, 0);
+  nxt = __shfl_sync(0xffffffffu, nxt, 0);
   while (u < a.n_units) {
-    long long nxt = 0;
-    if (lane == 0) nxt = atomicAdd(a.ctr, 1u);
-    // row-block-major order: warps across the GPU render the same rows of
-    // different envs at the same time, so the row records and shading-table
-    // slice they share stay hot in every SM's L1
-    const long long n_es = (long long)a.N * a.segs_per_row;
+    long long after = 0;
+    if (lane == 0) after = atomicAdd(a.ctr, 1u);
     const int gidx = (int)(u / n_es);
     const long long es = u - (long long)gidx * n_es;
     const int env = (int)(es / a.segs_per_row);
     const int seg = (int)(es - (long long)env * a.segs_per_row);
-    fill_unit<CPL, RW, false>(a, fw, env, seg, gidx);
-    u = __shfl_sync(0xffffffffu, nxt, 0);
+    const ColRec *pf = nullptr;
+    if (nxt < a.n_units) {
+      const long long es2 = nxt - (nxt / n_es) * n_es;
+      const int env2 = (int)(es2 / a.segs_per_row);
+      const int seg2 = (int)(es2 - (long long)env2 * a.segs_per_row);
+      pf = a.rec + (size_t)env2 * a.W + seg2 * 32 * CPL + lane * CPL;
+    }
+    fill_unit<CPL, RW, false>(a, fw, env, seg, gidx, pf);
+    u = nxt;
+    nxt = __shfl_sync(0xffffffffu, after, 0);
   }
   finish_grid(a.ctr);
+}
+
+// ---- CTA-per-frame writer ---------------------------------------------------
+//
+// k_fill_cta: persistent, one CTA of NW warps per SM; a work item is one env's
+// whole frame.  The item's column records (W x 32 B) arrive in shared memory
+// by a TMA bulk copy issued one item ahead (mbarrier completion), so no warp
+// ever waits on L2 for them; the row table and (when it fits) the mirrored
+// half of the env-independent shading table 1/|(d_j, v_i)| sit in shared
+// memory for the whole launch.  Warp w renders column segment w % S, rows
+// [(w / S) * rpw, ...) of the frame through its own double-buffered stage,
+// written out by cp.async.bulk exactly like k_fill_tma.
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_addr(bar)),
+      "r"(parity)
+      : "memory");
+}
+// global -> shared bulk copy completing on an mbarrier (bytes % 16 == 0)
+__device__ __forceinline__ void bulk_load(void *sdst, const void *gsrc, unsigned bytes,
+                                          uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(smem_addr(sdst)),
+      "l"(gsrc), "r"(bytes), "r"(smem_addr(bar))
+      : "memory");
+}
+
+template <int CPL>
+__device__ __forceinline__ void load_cols_smem(const ColRec *rp, ColRegs<CPL> &cr) {
+#pragma unroll
+  for (int k = 0; k < CPL / 2; ++k) {
+    const float4 *q = reinterpret_cast<const float4 *>(rp + 2 * k);
+    const float4 a0 = q[0], a1 = q[1], b0 = q[2], b1 = q[3];
+    cr.dw[2 * k] = a0.x;
+    cr.dw[2 * k + 1] = b0.x;
+    uint32_t l0 = __float_as_uint(a0.w), l1 = __float_as_uint(b0.w);
+    cr.lo[2 * k] = l0 & 0xffffu;
+    cr.hi[2 * k] = l0 >> 16;
+    cr.lo[2 * k + 1] = l1 & 0xffffu;
+    cr.hi[2 * k + 1] = l1 >> 16;
+    cr.nw[k] = h2_pack(a0.y, b0.y);
+    cr.rw[k] = h2_pack(a1.x, b1.x);
+    cr.gw[k] = h2_pack(a1.y, b1.y);
+    cr.bw[k] = h2_pack(a1.z, b1.z);
+    cr.sw[k] = (__float_as_uint(a1.w) & 0xffffu) | (__float_as_uint(b1.w) << 16);
+  }
+}
+
+template <int CPL>
+__device__ __forceinline__ void load_inv_smem(const uint16_t *ip, uint32_t (&iv)[CPL / 2]) {
+  if constexpr (CPL == 8) {
+    const uint4 v = *reinterpret_cast<const uint4 *>(ip);
+    iv[0] = v.x; iv[1] = v.y; iv[2] = v.z; iv[3] = v.w;
+  } else if constexpr (CPL == 4) {
+    const uint2 v = *reinterpret_cast<const uint2 *>(ip);
+    iv[0] = v.x; iv[1] = v.y;
+  } else {
+    iv[0] = *reinterpret_cast<const uint32_t *>(ip);
+  }
+}
+
+struct FillCtaLayout {  // byte offsets into dynamic shared memory
+  int rows, inv, cols, bar, stages, stage_bytes;
+};
+
+template <int CPL, int RW, bool TAB>
+__global__ void __launch_bounds__(512, 1) k_fill_cta(FillArgs a, FillCtaLayout L) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  constexpr int NS = 2;
+  constexpr int SEGW = 32 * CPL;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int W = a.W, H = a.H;
+  const RowRec *rows_s = reinterpret_cast<const RowRec *>(smem + L.rows);
+  const uint16_t *inv_s = reinterpret_cast<const uint16_t *>(smem + L.inv);
+  ColRec *cols_s = reinterpret_cast<ColRec *>(smem + L.cols);  // 2 x W
+  uint64_t *bar = reinterpret_cast<uint64_t *>(smem + L.bar);   // 2
+  const unsigned col_bytes = (unsigned)W * sizeof(ColRec);
+  int e = blockIdx.x;
+  if (threadIdx.x == 0) {
+    mbar_init(bar, 1);
+    mbar_init(bar + 1, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    if (e < a.N) {
+      mbar_expect_tx(bar, col_bytes);
+      bulk_load(cols_s, a.rec + (size_t)e * W, col_bytes, bar);
+    }
+  }
+  {
+    const uint4 *src = reinterpret_cast<const uint4 *>(a.rows);
+    uint4 *dst = reinterpret_cast<uint4 *>(smem + L.rows);
+    for (int k = threadIdx.x; k < H * 2; k += blockDim.x) dst[k] = __ldg(src + k);
+    if (TAB) {
+      const uint4 *s2 = reinterpret_cast<const uint4 *>(a.invh);
+      uint4 *d2 = reinterpret_cast<uint4 *>(smem + L.inv);
+      const int n16 = ((H + 1) / 2) * W * 2 / 16;
+      for (int k = threadIdx.x; k < n16; k += blockDim.x) d2[k] = __ldg(s2 + k);
+    }
+  }
+  __syncthreads();
+  const bool want_rgb = a.rgb != nullptr, want_d = a.depth != nullptr, want_s = a.sem != nullptr;
+  const int off_d = want_rgb ? RW * SEGW * 3 : 0;
+  const int off_s = off_d + (want_d ? RW * SEGW * 4 : 0);
+  uint8_t *wbase = smem + L.stages + (size_t)warp * NS * L.stage_bytes;
+  const uint64_t pol = policy_evict_first();
+  const int S = a.segs_per_row;
+  const int seg = warp % S;
+  const int rpw = (H * S + nw - 1) / nw;
+  const int r_begin = (warp / S) * rpw;
+  const int r_end = min(H, r_begin + rpw);
+  const int col0 = seg * SEGW + lane * CPL;
+  int kst = 0;  // stages issued by this warp
+  for (int it = 0; e < a.N; ++it, e += gridDim.x) {
+    const int en = e + gridDim.x;
+    if (threadIdx.x == 0 && en < a.N) {  // prefetch the next item's column records
+      uint64_t *b = bar + ((it + 1) & 1);
+      mbar_expect_tx(b, col_bytes);
+      bulk_load(cols_s + ((it + 1) & 1) * W, a.rec + (size_t)en * W, col_bytes, b);
+    }
+    mbar_wait(bar + (it & 1), (unsigned)((it >> 1) & 1));
+    ColRegs<CPL> cr;
+    load_cols_smem<CPL>(cols_s + (it & 1) * W + col0, cr);
+    for (int r0 = r_begin; r0 < r_end; r0 += RW) {
+      const int nr = min(RW, r_end - r0);
+      uint8_t *buf = wbase + (kst & (NS - 1)) * L.stage_bytes;
+      if (kst >= NS) {
+        if (lane == 0) bulk_wait_read<NS - 1>();
+        __syncwarp();
+      }
+      for (int rr = 0; rr < nr; ++rr) {
+        const uint32_t i = (uint32_t)(r0 + rr);
+        uint4 pq0, pq1;
+        load_row(rows_s, i, pq0, pq1);
+        RowRec R;
+        R.depth_p = __uint_as_float(pq0.x);
+        R.sem2 = pq0.y;
+        R.num2 = pq0.z;
+        R.r2 = pq0.w;
+        R.g2 = pq1.x;
+        R.b2 = pq1.y;
+        uint32_t iv[CPL / 2];
+        if constexpr (TAB)
+          load_inv_smem<CPL>(inv_s + (size_t)inv_row(i, H) * W + col0, iv);
+        else
+          load_inv_g<CPL>(a.invh + (size_t)inv_row(i, H) * W + col0, iv);
+        PairOut po[CPL / 2];
+#pragma unroll
+        for (int c = 0; c < CPL / 2; ++c)
+          po[c] = shade_pair(i, R, cr.lo[2 * c], cr.hi[2 * c], cr.lo[2 * c + 1],
+                             cr.hi[2 * c + 1], cr.dw[2 * c], cr.dw[2 * c + 1], cr.nw[c], cr.rw[c],
+                             cr.gw[c], cr.bw[c], cr.sw[c], iv[c]);
+        if (want_rgb) {
+          uint8_t *dst = buf + (rr * SEGW + lane * CPL) * 3;
+          if constexpr (CPL == 2) {
+            uint16_t *d16 = reinterpret_cast<uint16_t *>(dst);
+            d16[0] = (uint16_t)__byte_perm(po[0].r, po[0].g, 0x0040);
+            d16[1] = (uint16_t)__byte_perm(po[0].b, po[0].r, 0x0060);
+            d16[2] = (uint16_t)__byte_perm(po[0].g, po[0].b, 0x0062);
+          } else {
+            uint32_t w[3 * CPL / 4];
+#pragma unroll
+            for (int q = 0; q < CPL / 4; ++q)
+              pack_rgb4(po[2 * q], po[2 * q + 1], w[3 * q], w[3 * q + 1], w[3 * q + 2]);
+            if constexpr (CPL == 4) {
+#pragma unroll
+              for (int q = 0; q < 3; ++q) reinterpret_cast<uint32_t *>(dst)[q] = w[q];
+            } else {
+#pragma unroll
+              for (int q = 0; q < 3; ++q)
+                reinterpret_cast<uint2 *>(dst)[q] = make_uint2(w[2 * q], w[2 * q + 1]);
+            }
+          }
+        }
+        if (want_d) {
+          float *dst = reinterpret_cast<float *>(buf + off_d) + rr * SEGW + lane * CPL;
+          if constexpr (CPL == 2) {
+            *reinterpret_cast<float2 *>(dst) = make_float2(po[0].d0, po[0].d1);
+          } else {
+#pragma unroll
+            for (int q = 0; q < CPL / 4; ++q)
+              reinterpret_cast<float4 *>(dst)[q] =
+                  make_float4(po[2 * q].d0, po[2 * q].d1, po[2 * q + 1].d0, po[2 * q + 1].d1);
+          }
+        }
+        if (want_s) {
+          uint16_t *dst = reinterpret_cast<uint16_t *>(buf + off_s) + rr * SEGW + lane * CPL;
+          if constexpr (CPL == 2) {
+            *reinterpret_cast<uint32_t *>(dst) = po[0].s;
+          } else if constexpr (CPL == 4) {
+            *reinterpret_cast<uint2 *>(dst) = make_uint2(po[0].s, po[1].s);
+          } else {
+            *reinterpret_cast<uint4 *>(dst) = make_uint4(po[0].s, po[1].s, po[2].s, po[3].s);
+          }
+        }
+      }
+      fence_proxy_async();
+      __syncwarp();
+      if (lane == 0) {
+        if (S == 1) {
+          const size_t pix0 = ((size_t)e * H + r0) * W;
+          if (want_rgb) bulk_store(a.rgb + pix0 * 3, buf, (unsigned)(nr * W * 3), pol);
+          if (want_d) bulk_store(a.depth + pix0, buf + off_d, (unsigned)(nr * W * 4), pol);
+          if (want_s) bulk_store(a.sem + pix0, buf + off_s, (unsigned)(nr * W * 2), pol);
+        } else {
+          for (int rr = 0; rr < nr; ++rr) {
+            const size_t pix0 = ((size_t)e * H + r0 + rr) * W + (size_t)seg * SEGW;
+            if (want_rgb)
+              bulk_store(a.rgb + pix0 * 3, buf + rr * SEGW * 3, (unsigned)(SEGW * 3), pol);
+            if (want_d)
+              bulk_store(a.depth + pix0, buf + off_d + rr * SEGW * 4, (unsigned)(SEGW * 4), pol);
+            if (want_s)
+              bulk_store(a.sem + pix0, buf + off_s + rr * SEGW * 2, (unsigned)(SEGW * 2), pol);
+          }
+        }
+        bulk_commit();
+      }
+      ++kst;
+    }
+    __syncthreads();  // column buffer (it & 1) is free for item it + 2
+  }
+  if (lane == 0) bulk_wait_all();
+}
+
+// ---- warp-specialised frame writer ------------------------------------------
+//
+// k_fill_ws: persistent, one CTA per SM = NW producer warps + 1 store warp; a
+// work item is one env's frame.  Producers render rows into a ring of NSLOT
+// shared-memory slots (a slot = R consecutive frame rows, all channels, laid
+// out exactly like the frame, so ONE bulk copy per channel writes it out);
+// the store warp's elected lane waits on the slot's `full` mbarrier, issues
+// the cp.async.bulk stores (evict-first), and releases the previous slot
+// through its `empty` mbarrier once the bulk engine has read it.  The same
+// lane prefetches the next item's column records into a double buffer with a
+// bulk copy.  Producers never touch L2 except through the store path: row
+// records, the shading table and column records are all shared-memory reads.
+
+#ifndef NV_WS_DEBUG
+#define NV_WS_DEBUG 0  // 1: producers skip rendering, 2: no bulk stores (bound studies)
+#endif
+struct FillWsLayout {  // byte offsets into dynamic shared memory + ring geometry
+  int rows, inv, cols, bars, slots;
+  int slot_bytes, nslot, slot_rows;
+};
+
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
+}
+
+template <int CPL, bool TAB, int RPW>
+__global__ void __launch_bounds__(544, 1) k_fill_ws(FillArgs a, FillWsLayout L) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  constexpr int SEGW = 32 * CPL;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nw = (blockDim.x >> 5) - 1;  // producer warps
+  const int W = a.W, H = a.H, S = a.segs_per_row, R = L.slot_rows, NSLOT = L.nslot;
+  const RowRec *rows_s = reinterpret_cast<const RowRec *>(smem + L.rows);
+  const uint16_t *inv_s = reinterpret_cast<const uint16_t *>(smem + L.inv);
+  ColRec *cols_s = reinterpret_cast<ColRec *>(smem + L.cols);  // 2 x W
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + L.bars);
+  uint64_t *empty = full + NSLOT;
+  uint64_t *colfull = empty + NSLOT;
+  uint64_t *colempty = colfull + 2;
+  uint8_t *slots = smem + L.slots;
+  const unsigned col_bytes = (unsigned)W * sizeof(ColRec);
+  const bool want_rgb = a.rgb != nullptr, want_d = a.depth != nullptr, want_s = a.sem != nullptr;
+  const int off_d = want_rgb ? R * W * 3 : 0;
+  const int off_s = off_d + (want_d ? R * W * 4 : 0);
+  const int slots_per_item = H / R;
+  if (threadIdx.x == 0) {
+    for (int k = 0; k < NSLOT; ++k) {
+      mbar_init(full + k, (unsigned)nw);
+      mbar_init(empty + k, 1);
+    }
+    for (int k = 0; k < 2; ++k) {
+      mbar_init(colfull + k, 1);
+      mbar_init(colempty + k, (unsigned)nw);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  {
+    const uint4 *src = reinterpret_cast<const uint4 *>(a.rows);
+    uint4 *dst = reinterpret_cast<uint4 *>(smem + L.rows);
+    for (int k = threadIdx.x; k < H * 2; k += blockDim.x) dst[k] = __ldg(src + k);
+    if (TAB) {
+      const uint4 *s2 = reinterpret_cast<const uint4 *>(a.invh);
+      uint4 *d2 = reinterpret_cast<uint4 *>(smem + L.inv);
+      const int n16 = ((H + 1) / 2) * W * 2 / 16;
+      for (int k = threadIdx.x; k < n16; k += blockDim.x) d2[k] = __ldg(s2 + k);
+    }
+  }
+  __syncthreads();
+  if (warp == nw) {
+    // ------------------------------------------------------------ store warp
+    if (lane != 0) return;
+    const uint64_t pol = policy_evict_first();
+    int e = blockIdx.x;
+    if (e < a.N) {
+      mbar_expect_tx(colfull, col_bytes);
+      bulk_load(cols_s, a.rec + (size_t)e * W, col_bytes, colfull);
+    }
+    unsigned k = 0, slot = 0, use = 0, prev = 0;
+    for (int it = 0; e < a.N; ++it, e += gridDim.x) {
+      const int en = e + gridDim.x;
+      if (en < a.N) {
+        const int j = it + 1;
+        if (j >= 2) mbar_wait(colempty + (j & 1), (unsigned)(((j >> 1) - 1) & 1));
+        mbar_expect_tx(colfull + (j & 1), col_bytes);
+        bulk_load(cols_s + (j & 1) * W, a.rec + (size_t)en * W, col_bytes, colfull + (j & 1));
+      }
+      for (int sl = 0; sl < slots_per_item; ++sl, ++k) {
+        mbar_wait(full + slot, use & 1u);
+        const uint8_t *buf = slots + (size_t)slot * L.slot_bytes;
+        const size_t pix0 = ((size_t)e * H + (size_t)sl * R) * W;
+#if NV_WS_DEBUG != 2
+        if (want_rgb) bulk_store(a.rgb + pix0 * 3, buf, (unsigned)(R * W * 3), pol);
+        if (want_d) bulk_store(a.depth + pix0, buf + off_d, (unsigned)(R * W * 4), pol);
+        if (want_s) bulk_store(a.sem + pix0, buf + off_s, (unsigned)(R * W * 2), pol);
+#else
+        (void)buf; (void)pix0; (void)pol;
+#endif
+        bulk_commit();
+        if (k >= 1) {
+          bulk_wait_read<1>();
+          mbar_arrive(empty + prev);
+        }
+        prev = slot;
+        if (++slot == (unsigned)NSLOT) {
+          slot = 0;
+          ++use;
+        }
+      }
+    }
+    bulk_wait_all();
+    return;
+  }
+  // -------------------------------------------------------------- producers
+  const int seg = warp % S;
+  const int rsub = warp / S;        // first row of this warp within a slot
+  const int rstride = nw / S;       // row stride between the warp's RPW rows
+  const int col0 = seg * SEGW + lane * CPL;
+  unsigned slot = 0, use = 0;
+  int e = blockIdx.x;
+  for (int it = 0; e < a.N; ++it, e += gridDim.x) {
+    mbar_wait(colfull + (it & 1), (unsigned)((it >> 1) & 1));
+    ColRegs<CPL> cr;
+    load_cols_smem<CPL>(cols_s + (it & 1) * W + col0, cr);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(colempty + (it & 1));
+    for (int sl = 0; sl < slots_per_item; ++sl) {
+      if (use >= 1) mbar_wait(empty + slot, (use - 1) & 1u);
+      uint8_t *buf = slots + (size_t)slot * L.slot_bytes;
+#pragma unroll
+      for (int rr = 0; rr < RPW; ++rr) {
+        const int rs = rsub + rr * rstride;  // row within the slot
+        const uint32_t i = (uint32_t)(sl * R + rs);
+#if NV_WS_DEBUG == 1
+        (void)buf; (void)i;
+        continue;
+#endif
+        uint4 pq0, pq1;
+        load_row(rows_s, i, pq0, pq1);
+        RowRec Rr;
+        Rr.depth_p = __uint_as_float(pq0.x);
+        Rr.sem2 = pq0.y;
+        Rr.num2 = pq0.z;
+        Rr.r2 = pq0.w;
+        Rr.g2 = pq1.x;
+        Rr.b2 = pq1.y;
+        uint32_t iv[CPL / 2];
+        if constexpr (TAB)
+          load_inv_smem<CPL>(inv_s + (size_t)inv_row(i, H) * W + col0, iv);
+        else
+          load_inv_g<CPL>(a.invh + (size_t)inv_row(i, H) * W + col0, iv);
+        PairOut po[CPL / 2];
+#pragma unroll
+        for (int c = 0; c < CPL / 2; ++c)
+          po[c] = shade_pair(i, Rr, cr.lo[2 * c], cr.hi[2 * c], cr.lo[2 * c + 1],
+                             cr.hi[2 * c + 1], cr.dw[2 * c], cr.dw[2 * c + 1], cr.nw[c], cr.rw[c],
+                             cr.gw[c], cr.bw[c], cr.sw[c], iv[c]);
+        const int px = rs * W + col0;  // pixel index within the slot
+        if (want_rgb) {
+          uint8_t *dst = buf + (size_t)px * 3;
+          if constexpr (CPL == 2) {
+            uint16_t *d16 = reinterpret_cast<uint16_t *>(dst);
+            d16[0] = (uint16_t)__byte_perm(po[0].r, po[0].g, 0x0040);
+            d16[1] = (uint16_t)__byte_perm(po[0].b, po[0].r, 0x0060);
+            d16[2] = (uint16_t)__byte_perm(po[0].g, po[0].b, 0x0062);
+          } else {
+            uint32_t w[3 * CPL / 4];
+#pragma unroll
+            for (int q = 0; q < CPL / 4; ++q)
+              pack_rgb4(po[2 * q], po[2 * q + 1], w[3 * q], w[3 * q + 1], w[3 * q + 2]);
+            if constexpr (CPL == 4) {
+#pragma unroll
+              for (int q = 0; q < 3; ++q) reinterpret_cast<uint32_t *>(dst)[q] = w[q];
+            } else {
+#pragma unroll
+              for (int q = 0; q < 3; ++q)
+                reinterpret_cast<uint2 *>(dst)[q] = make_uint2(w[2 * q], w[2 * q + 1]);
+            }
+          }
+        }
+        if (want_d) {
+          float *dst = reinterpret_cast<float *>(buf + off_d) + px;
+          if constexpr (CPL == 2) {
+            *reinterpret_cast<float2 *>(dst) = make_float2(po[0].d0, po[0].d1);
+          } else {
+#pragma unroll
+            for (int q = 0; q < CPL / 4; ++q)
+              reinterpret_cast<float4 *>(dst)[q] =
+                  make_float4(po[2 * q].d0, po[2 * q].d1, po[2 * q + 1].d0, po[2 * q + 1].d1);
+          }
+        }
+        if (want_s) {
+          uint16_t *dst = reinterpret_cast<uint16_t *>(buf + off_s) + px;
+          if constexpr (CPL == 2) {
+            *reinterpret_cast<uint32_t *>(dst) = po[0].s;
+          } else if constexpr (CPL == 4) {
+            *reinterpret_cast<uint2 *>(dst) = make_uint2(po[0].s, po[1].s);
+          } else {
+            *reinterpret_cast<uint4 *>(dst) = make_uint4(po[0].s, po[1].s, po[2].s, po[3].s);
+          }
+        }
+      }
+      fence_proxy_async();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(full + slot);
+      if (++slot == (unsigned)NSLOT) {
+        slot = 0;
+        ++use;
+      }
+    }
+  }
 }
 
 // ---- direct-store variant: no smem staging ---------------------------------
@@ -1542,7 +2062,7 @@ __global__ void __launch_bounds__(128) k_fill_tma(FillArgs a) {
 // one 256-bit store (STG.256, sm_100), semantic as 128-bit, RGB as three
 // 64-bit stores; a warp covers W contiguous pixels per row, so every row is a
 // fully coalesced run per channel and partial sectors merge in L2.  Without
-// stage buffers the whole L1 serves the (env-independent) shading tables.
+// stage buffers the whole L1 serves the column records.
 __device__ __forceinline__ void st_v8f(float *p, const float (&v)[8], uint64_t pol) {
   asm volatile(
       "st.global.L2::cache_hint.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8}, %9;" ::"l"(p),
@@ -1573,12 +2093,11 @@ __device__ __forceinline__ void fill_unit_direct(const FillArgs &a, const RowRec
   load_cols<CPL, COH>(a.rec + (size_t)env * W + col0, cr);
   const int r_begin = gidx * a.rows_per_unit;
   const int r_end = min(H, r_begin + a.rows_per_unit);
-  uint4 pq0, pq1;
-  uint32_t piv[CPL / 2];
-  load_row<CPL>(a, rows_s, (uint32_t)r_begin, col0, pq0, pq1, piv);
   size_t pix = ((size_t)env * H + r_begin) * W + col0;  // first pixel of this lane's run
   for (int r = r_begin; r < r_end; ++r, pix += W) {
     const uint32_t i = (uint32_t)r;
+    uint4 pq0, pq1;
+    load_row(rows_s, i, pq0, pq1);
     RowRec R;
     R.depth_p = __uint_as_float(pq0.x);
     R.sem2 = pq0.y;
@@ -1587,9 +2106,7 @@ __device__ __forceinline__ void fill_unit_direct(const FillArgs &a, const RowRec
     R.g2 = pq1.x;
     R.b2 = pq1.y;
     uint32_t iv[CPL / 2];
-#pragma unroll
-    for (int c = 0; c < CPL / 2; ++c) iv[c] = piv[c];
-    load_row<CPL>(a, rows_s, min(i + 1, (uint32_t)(r_end - 1)), col0, pq0, pq1, piv);
+    load_inv_g<CPL>(a.invh + (size_t)inv_row(i, H) * W + col0, iv);
     PairOut po[CPL / 2];
 #pragma unroll
     for (int c = 0; c < CPL / 2; ++c)
@@ -1783,7 +2300,7 @@ __global__ void k_fill_generic(FillArgs a) {
   const ColRec c = a.rec[(size_t)e * a.W + j];
   const RowRec R = a.rows[i];
   const uint32_t lo = c.lohi & 0xffffu, hi = c.lohi >> 16;
-  const uint32_t inv = a.inv[(size_t)i * a.W + j];
+  const uint32_t inv = a.invh[(size_t)inv_row(i, a.H) * a.W + j];
   PairOut o = shade_pair(i, R, lo, hi, lo, hi, c.depth_w, c.depth_w, h2_pack(c.num08_w, 0.f),
                          h2_pack(c.col_w[0], 0.f), h2_pack(c.col_w[1], 0.f),
                          h2_pack(c.col_w[2], 0.f), c.sem_w & 0xffffu, inv);

@@ -11,6 +11,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -87,7 +88,7 @@ struct Camera {
   double focal = 0, max_range = 0;
   int n_top = 0, b0 = 0;
   double tables_cam_h = NAN;
-  DevBuf u, tc, tf, rows, inv;
+  DevBuf u, tc, tf, rows, invh;
   DevBuf rec;      // ColRec N x W
   DevBuf ctr;      // fill scheduler counters
   // fused step+render megakernel task queue (rebuilt when N or layout changes)
@@ -111,7 +112,7 @@ struct nv_ctx {
   double gx0 = -0.5, gy0 = -0.5;
   int gnx = 1, gny = 1;
   int64_t nitems = 0;
-  DevBuf ax, ay, bx, by, ex, ey, nx, ny, sem, alb, starts, ent, items, entf, cellb;
+  DevBuf ax, ay, bx, by, ex, ey, nx, ny, sem, alb, starts, ent, items, entf, cellb, cells, chunks;
   // agent
   double radius = 0.1, step = 0.25, turn_rad = 0.17453292519943295, sensor_h = 1.5;
   // envs
@@ -122,7 +123,7 @@ struct nv_ctx {
   DevBuf e_act, e_rgb, e_depth, e_sem, e_gps, e_comp, e_coll, e_disp;
   int64_t launches = 0;
   int cast_mode = 0;  // 0: per-column DDA (default), 1: binned (tile-binned segment setup)
-  int fill_mode = 1;   // 0: direct 256-bit stores, 1: smem stages + TMA bulk stores
+  int fill_mode = 3;   // 0 direct stores, 1 per-warp TMA stages, 2 CTA per frame, 3 warp-specialised
   bool fused = false;  // nv_step_render uses the megakernel when the layout allows (opt-in)
   // optional per-kernel CUDA-event timing (bench roofline evidence)
   bool prof_on = false;
@@ -142,7 +143,8 @@ struct nv_ctx {
     v.nx = nx.as<double>(); v.ny = ny.as<double>();
     v.sem = sem.as<uint16_t>(); v.alb255 = alb.as<float4>();
     v.starts = starts.as<int32_t>(); v.ent = ent.as<CellEntry>(); v.items = items.as<int32_t>();
-    v.entf = entf.as<float4>(); v.cellb = cellb.as<float>();
+    v.entf = entf.as<float4>(); v.cellb = cellb.as<float>(); v.cells = cells.as<int4>();
+    v.chunks = chunks.as<float4>();
     v.x0 = gx0; v.y0 = gy0; v.gnx = gnx; v.gny = gny; v.n = n;
     return v;
   }
@@ -237,9 +239,9 @@ uint32_t h2splat(float x) {
 
 // Row tables for a camera (fill_frame's per-row quantities, _kernels.py:141,
 // 150, 158): v, tc, tf in exact f64 (host IEEE, no contraction); the f16
-// shading table inv[i][j] = 1/sqrt(|d_j|^2 + v_i^2), |d_j|^2 = 1 + u_j^2
+// shading table invh[i][j] = 1/sqrt(|d_j|^2 + v_i^2), |d_j|^2 = 1 + u_j^2
 // (column directions have unit forward component, sensors.py:96-102), is the
-// same for every env and heading.
+// same for every env and heading; rows i >= ceil(H/2) mirror row H-1-i.
 int build_camera_tables(nv_ctx *c, Camera &cam, double cam_h) {
   const int W = cam.W, H = cam.H;
   std::vector<double> u(W), tc(H, 0.0), tf(H, 0.0), vv(H);
@@ -282,17 +284,18 @@ int build_camera_tables(nv_ctx *c, Camera &cam, double cam_h) {
     }
     rows[i] = r;
   }
-  std::vector<uint16_t> inv((size_t)H * W);
-  for (int i = 0; i < H; ++i)
+  const int Hh = (H + 1) / 2;
+  std::vector<uint16_t> invh((size_t)Hh * W);
+  for (int i = 0; i < Hh; ++i)
     for (int j = 0; j < W; ++j)
-      inv[(size_t)i * W + j] = f2h((float)(1.0 / std::sqrt(1.0 + u[j] * u[j] + vv[i] * vv[i])));
+      invh[(size_t)i * W + j] = f2h((float)(1.0 / std::sqrt(1.0 + u[j] * u[j] + vv[i] * vv[i])));
+  TRY(upload(cam.invh, invh));
   cam.n_top = n_top;
   cam.b0 = b0;
   TRY(upload(cam.u, u));
   TRY(upload(cam.tc, tc));
   TRY(upload(cam.tf, tf));
   TRY(upload(cam.rows, rows));
-  TRY(upload(cam.inv, inv));
   cam.tables_cam_h = cam_h;
   return NV_OK;
 }
@@ -302,7 +305,6 @@ CamView cam_view(const Camera &cam) {
   v.W = cam.W; v.H = cam.H; v.n_top = cam.n_top; v.b0 = cam.b0; v.max_range = cam.max_range;
   v.u = cam.u.as<double>(); v.tc = cam.tc.as<double>(); v.tf = cam.tf.as<double>();
   v.rows = cam.rows.as<RowRec>();
-  v.inv = cam.inv.as<uint16_t>();
   return v;
 }
 
@@ -345,7 +347,12 @@ unsigned blocks_for(long long work, int per_block) {
 template <int CPL>
 void fill_layout(nvk::FillArgs &a) {
   a.segs_per_row = a.W / (32 * CPL);
-  a.rows_per_unit = 16;
+  static const int rpu = [] {  // tuning knob (rows per work unit), default 16
+    const char *e = getenv("NAVSIM_FILL_RPU");
+    const int v = e ? atoi(e) : 0;
+    return v >= 2 && v <= 256 ? v : 16;
+  }();
+  a.rows_per_unit = rpu;
   a.units_per_seg = (a.H + a.rows_per_unit - 1) / a.rows_per_unit;
   a.n_units = (long long)a.N * a.segs_per_row * a.units_per_seg;
 }
@@ -421,7 +428,7 @@ int launch_mega(nv_ctx *c, Camera &cam, const int8_t *actions, uint8_t *rgb, flo
   nvk::FillArgs &a = m.f;
   a.rec = cam.rec.as<ColRec>();
   a.rows = cam.rows.as<RowRec>();
-  a.inv = cam.inv.as<uint16_t>();
+  a.invh = cam.invh.as<uint16_t>();
   a.N = (int)c->n_envs; a.W = cam.W; a.H = cam.H;
   a.rgb = rgb; a.depth = depth; a.sem = sem;
   a.ctr = cam.ctr.as<unsigned int>();
@@ -478,13 +485,130 @@ int launch_fill_direct(nv_ctx *c, nvk::FillArgs &a, cudaStream_t st) {
   return check_launch(c);
 }
 
+// CTA-per-frame writer: the widest configuration that fits in shared memory,
+// preferring 16 warps with the shading table resident.
+template <int CPL>
+int launch_fill_cta(nv_ctx *c, nvk::FillArgs &a, cudaStream_t st) {
+  constexpr int RW = 2;
+  const int segw = 32 * CPL;
+  const int S = a.W / segw;
+  const int bpp = (a.rgb ? 3 : 0) + (a.depth ? 4 : 0) + (a.sem ? 2 : 0);
+  auto up = [](size_t x) { return (x + 127) & ~(size_t)127; };
+  nvk::FillCtaLayout L;
+  L.stage_bytes = (int)up((size_t)RW * segw * bpp);
+  const size_t rows_b = up((size_t)a.H * sizeof(RowRec));
+  const size_t inv_b = up((size_t)((a.H + 1) / 2) * a.W * 2);
+  const size_t cols_b = up((size_t)2 * a.W * sizeof(ColRec));
+  static const int cfg_nw[6] = {16, 16, 12, 12, 8, 8};
+  static const bool cfg_tab[6] = {true, false, true, false, true, false};
+  int nw = 0;
+  bool tab = false;
+  size_t smem = 0;
+  for (int k = 0; k < 6; ++k) {
+    if (cfg_nw[k] % S) continue;
+    const size_t tot = rows_b + (cfg_tab[k] ? inv_b : 0) + cols_b + 128 +
+                       (size_t)cfg_nw[k] * 2 * L.stage_bytes;
+    if ((int)tot <= c->max_smem_optin) {
+      nw = cfg_nw[k];
+      tab = cfg_tab[k];
+      smem = tot;
+      break;
+    }
+  }
+  if (!nw) return fail(NV_ERR_ARG, "frame layout too large for the CTA fill writer");
+  L.rows = 0;
+  L.inv = (int)rows_b;
+  L.cols = L.inv + (tab ? (int)inv_b : 0);
+  L.bar = L.cols + (int)cols_b;
+  L.stages = L.bar + 128;
+  a.segs_per_row = S;
+  auto kern = tab ? nvk::k_fill_cta<CPL, RW, true> : nvk::k_fill_cta<CPL, RW, false>;
+  static int configured[2][3] = {{0, 0, 0}, {0, 0, 0}};
+  int &cfgd = configured[tab ? 1 : 0][CPL == 2 ? 0 : (CPL == 4 ? 1 : 2)];
+  if ((int)smem > cfgd) {
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    cfgd = (int)smem;
+  }
+  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(a.N, c->sm_count));
+  Prof pf(c, st, 2);
+  kern<<<grid, nw * 32, smem, st>>>(a, L);
+  return check_launch(c);
+}
+
+// Warp-specialised writer: 16 producer warps + 1 store warp.  Preference
+// order: shading table resident, RPW (rows per producer warp per slot) = 2
+// with a ring of >= 2 slots, then RPW = 1 with 2..4 slots, then no table.
+template <int CPL, bool TAB, int RPW>
+int launch_ws_kernel(nv_ctx *c, nvk::FillArgs &a, const nvk::FillWsLayout &L, size_t smem,
+                     cudaStream_t st) {
+  auto kern = nvk::k_fill_ws<CPL, TAB, RPW>;
+  static int configured = 0;
+  if ((int)smem > configured) {
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    configured = (int)smem;
+  }
+  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(a.N, c->sm_count));
+  Prof pf(c, st, 2);
+  kern<<<grid, (16 + 1) * 32, smem, st>>>(a, L);
+  return check_launch(c);
+}
+
+template <int CPL>
+int launch_fill_ws(nv_ctx *c, nvk::FillArgs &a, cudaStream_t st) {
+  const int segw = 32 * CPL;
+  const int S = a.W / segw;
+  const int nw = 16;
+  const int bpp = (a.rgb ? 3 : 0) + (a.depth ? 4 : 0) + (a.sem ? 2 : 0);
+  auto up = [](size_t x) { return (x + 127) & ~(size_t)127; };
+  if (nw % S) return fail(NV_ERR_ARG, "frame layout unsupported by ws fill");
+  const size_t rows_b = up((size_t)a.H * sizeof(RowRec));
+  const size_t inv_b = up((size_t)((a.H + 1) / 2) * a.W * 2);
+  const size_t cols_b = up((size_t)2 * a.W * sizeof(ColRec));
+  const size_t bars_b = 128;
+  static const int force_rpw = [] {
+    const char *e = getenv("NAVSIM_WS_RPW");
+    return e ? atoi(e) : 0;
+  }();
+  struct Opt { bool tab; int rpw, nmin, nmax; };
+  static const Opt opts[] = {{true, 2, 2, 4}, {true, 1, 2, 4}, {false, 2, 2, 4}, {false, 1, 2, 4}};
+  nvk::FillWsLayout L;
+  bool tab = false;
+  int rpw = 0;
+  size_t smem = 0;
+  for (const Opt &o : opts) {
+    if (force_rpw && o.rpw != force_rpw) continue;
+    const int R = o.rpw * nw / S;
+    if (a.H % R) continue;
+    const size_t slot = up((size_t)R * a.W * bpp);
+    for (int ns = o.nmax; ns >= o.nmin && !rpw; --ns) {
+      const size_t tot = rows_b + (o.tab ? inv_b : 0) + cols_b + bars_b + (size_t)ns * slot;
+      if ((int)tot <= c->max_smem_optin) {
+        tab = o.tab; rpw = o.rpw; smem = tot;
+        L.nslot = ns; L.slot_rows = R; L.slot_bytes = (int)slot;
+      }
+    }
+    if (rpw) break;
+  }
+  if (!rpw) return fail(NV_ERR_ARG, "frame layout too large for the ws fill writer");
+  L.rows = 0;
+  L.inv = (int)rows_b;
+  L.cols = L.inv + (tab ? (int)inv_b : 0);
+  L.bars = L.cols + (int)cols_b;
+  L.slots = L.bars + (int)bars_b;
+  a.segs_per_row = S;
+  if (tab && rpw == 2) return launch_ws_kernel<CPL, true, 2>(c, a, L, smem, st);
+  if (tab) return launch_ws_kernel<CPL, true, 1>(c, a, L, smem, st);
+  if (rpw == 2) return launch_ws_kernel<CPL, false, 2>(c, a, L, smem, st);
+  return launch_ws_kernel<CPL, false, 1>(c, a, L, smem, st);
+}
+
 int launch_fill(nv_ctx *c, Camera &cam, int64_t N, uint8_t *rgb, float *depth, uint16_t *sem,
                 cudaStream_t st) {
   if (!rgb && !depth && !sem) return NV_OK;
   nvk::FillArgs a;
   a.rec = cam.rec.as<ColRec>();
   a.rows = cam.rows.as<RowRec>();
-  a.inv = cam.inv.as<uint16_t>();
+  a.invh = cam.invh.as<uint16_t>();
   a.N = (int)N; a.W = cam.W; a.H = cam.H;
   a.rgb = rgb; a.depth = depth; a.sem = sem;
   a.ctr = cam.ctr.as<unsigned int>();
@@ -494,6 +618,14 @@ int launch_fill(nv_ctx *c, Camera &cam, int64_t N, uint8_t *rgb, float *depth, u
   if (c->fill_mode == 0 && aligned && al32(depth) && cam.W % 256 == 0)
     return launch_fill_direct<8>(c, a, st);
   if (c->fill_mode == 0 && aligned && cam.W == 128) return launch_fill_direct<4>(c, a, st);
+  const bool ws_ok = cam.W <= 4096 && (cam.W % 256 == 0 ? cam.H % (16 / std::min(16, cam.W / 256)) == 0
+                                                          : cam.H % 16 == 0);
+  if (c->fill_mode == 3 && aligned && ws_ok && cam.W % 256 == 0) return launch_fill_ws<8>(c, a, st);
+  if (c->fill_mode == 3 && aligned && ws_ok && cam.W == 128) return launch_fill_ws<4>(c, a, st);
+  if (c->fill_mode == 3 && aligned && ws_ok && cam.W == 64) return launch_fill_ws<2>(c, a, st);
+  if (c->fill_mode == 2 && aligned && cam.W % 256 == 0) return launch_fill_cta<8>(c, a, st);
+  if (c->fill_mode == 2 && aligned && cam.W == 128) return launch_fill_cta<4>(c, a, st);
+  if (c->fill_mode == 2 && aligned && cam.W == 64) return launch_fill_cta<2>(c, a, st);
   if (aligned && cam.W % 256 == 0) return launch_fill_tma<8>(c, a, st);
   if (aligned && cam.W == 128) return launch_fill_tma<4>(c, a, st);
   if (aligned && cam.W == 64) return launch_fill_tma<2>(c, a, st);
@@ -644,6 +776,37 @@ int nv_scene_upload(nv_ctx *c, const double *segs, const uint16_t *sem, const do
   TRY(upload(c->sem, sm)); TRY(upload(c->alb, alb));
   TRY(upload(c->starts, starts)); TRY(upload(c->items, items)); TRY(upload(c->ent, ent));
   TRY(upload(c->entf, entf)); TRY(upload(c->cellb, cellb));
+  // Per cell: runs of NV_CHUNK entries (bucket order) with the f32 bounding box
+  // of their cell-relative endpoints; the cast rejects a whole run when the
+  // ray's line passes the box on one side (kernels.cuh ray_grid).  The cell
+  // bound grows to cover the box corners, so one error bound E serves both.
+  std::vector<int4> cells((size_t)(g.nx * g.ny));
+  std::vector<float4> chunks;
+  for (size_t k = 0; k < cells.size(); ++k) {
+    float b = cellb[k];
+    const int32_t q0 = starts[k], q1 = starts[k + 1];
+    const int32_t ch0 = (int32_t)chunks.size();
+    for (int32_t q = q0; q < q1; q += NV_CHUNK) {
+      float4 bx = make_float4(INFINITY, INFINITY, -INFINITY, -INFINITY);
+      for (int32_t r = q; r < std::min(q1, q + NV_CHUNK); ++r) {
+        const float4 f = entf[r];
+        bx.x = std::min(bx.x, std::min(f.x, f.z));
+        bx.y = std::min(bx.y, std::min(f.y, f.w));
+        bx.z = std::max(bx.z, std::max(f.x, f.z));
+        bx.w = std::max(bx.w, std::max(f.y, f.w));
+      }
+      chunks.push_back(bx);
+      const float cb = std::max(std::fabs(bx.x), std::fabs(bx.z)) +
+                       std::max(std::fabs(bx.y), std::fabs(bx.w));
+      b = std::max(b, cb * (1.0f + 0x1p-20f));
+    }
+    int bi;
+    std::memcpy(&bi, &b, 4);
+    cells[k] = make_int4(q0, q1, bi, ch0);
+  }
+  if (chunks.empty()) chunks.push_back(make_float4(0.f, 0.f, 0.f, 0.f));
+  TRY(upload(c->cells, cells));
+  TRY(upload(c->chunks, chunks));
   c->n = n;
   c->wall_h = wall_height;
   for (int k = 0; k < 3; ++k) {
@@ -810,7 +973,8 @@ int nv_set_cast_mode(nv_ctx *c, int mode) {
 
 int nv_set_fill_mode(nv_ctx *c, int mode) {
   if (!c) return fail(NV_ERR_ARG, "ctx is NULL");
-  if (mode < 0 || mode > 1) return fail(NV_ERR_ARG, "fill mode must be 0 (direct) or 1 (tma)");
+  if (mode < 0 || mode > 3)
+    return fail(NV_ERR_ARG, "fill mode must be 0 (direct), 1 (tma), 2 (cta) or 3 (ws)");
   c->fill_mode = mode;
   return NV_OK;
 }
