@@ -389,7 +389,7 @@ def run_gpu(args):
                        "channels": list(chans), "segments": sc.n_segments,
                        "triangles": sc.n_triangles, "parallelism": f"env-shard x{world}",
                        "cuda_graph": use_graph, "fused_megakernel": fused,
-                       "fill_mode": ["direct-256b-stores", "tma-bulk-stores", "cta-per-frame-tma", "warp-specialised-tma"][args.fill_mode],
+                       "fill_mode": {0: "direct-stores", 1: "per-warp-tma-stages", 3: "warp-specialised-tma"}.get(args.fill_mode),
                        "cast_mode": ["dda", "binned"][args.cast_mode],
                        "l2": f"no flush: frames written per step "
                              f"({step_bytes / 1e6:.0f} MB/GPU) exceed the 126 MB L2"},
@@ -426,7 +426,7 @@ def main():
     ap.add_argument("--envs", type=int, default=0, help="override envs per GPU")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-graph", action="store_true")
-    ap.add_argument("--fill-mode", type=int, default=3, help="0 direct stores, 1 TMA bulk stores, 2 CTA-per-frame TMA writer, 3 warp-specialised writer")
+    ap.add_argument("--fill-mode", type=int, default=3, help="0 direct stores, 1 per-warp TMA stages, 3 warp-specialised writer")
     ap.add_argument("--cast-mode", type=int, default=0, help="0 per-column DDA, 1 binned")
     ap.add_argument("--fused", action="store_true", help="one megakernel launch per step (experimental)")
     ap.add_argument("--no-e2e", action="store_true")

@@ -129,7 +129,6 @@ int nv_set_fused(nv_ctx *ctx, int on);
 int nv_set_cast_mode(nv_ctx *ctx, int mode);
 /* Frame writer: 0 = 256-bit direct stores from registers,
  * 1 = per-warp shared-memory stages written out by TMA bulk copies,
- * 2 = one CTA per frame (column records bulk-prefetched into smem),
  * 3 (default) = warp-specialised: 16 producer warps render rows into a ring of
  *     smem slots, one store warp writes each slot with one bulk copy per
  *     channel.  All modes produce identical frames. */

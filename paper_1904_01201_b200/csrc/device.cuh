@@ -77,6 +77,33 @@ struct __align__(16) ColRec {
   uint32_t sem_w;  // seg_sem[k] (0 when void)
 };
 
+// Column records live in two planes of 16-byte halves per camera,
+//   A = {depth_w, num08_w, d2, lohi},  B = {col_w[0..2], sem_w},
+// at index env * W + rec_pos(j): within each 32*CPL-column segment the record
+// of column seg*32*CPL + g*32*GW + l*GW + c (lane l, group g, column c of the
+// group, GW = min(CPL, 4)) sits at seg*32*CPL + (g*GW + c)*32 + l, so the 32
+// lanes of a fill warp read 32 consecutive halves (conflict-free shared-memory
+// rows, coalesced global loads).  cpl = 0: identity order.
+#if defined(__CUDACC__)
+#define NV_HDI __host__ __device__ __forceinline__
+#else
+#define NV_HDI static inline
+#endif
+NV_HDI int rec_pos(int j, int cpl) {
+  if (cpl <= 0) return j;
+  const int gw = cpl < 4 ? cpl : 4;
+  const int segw = 32 * cpl;
+  const int seg = j / segw, r = j - seg * segw;
+  const int g = r / (32 * gw), r2 = r - g * 32 * gw;
+  const int l = r2 / gw, c = r2 - l * gw;
+  return seg * segw + (g * gw + c) * 32 + l;
+}
+
+struct RecOut {  // column-record planes written by the casts
+  float4 *a, *b;
+  int W, cpl;
+};
+
 struct CamView {
   int W, H;
   int n_top;  // rows with v > 0
@@ -86,6 +113,8 @@ struct CamView {
   const double *tc;  // H: (wall_h - cam_h) / v for v > 0 rows
   const double *tf;  // H: -cam_h / v for v < 0 rows
   const RowRec *rows;
+  int cpl;  // record order of rec_pos (0 = identity)
+  float hc, ktop, kbot;  // H/2 - 1/2, focal (wall_h - cam_h), focal cam_h (row estimates)
 };
 
 }  // namespace nvd

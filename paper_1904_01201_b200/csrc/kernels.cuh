@@ -704,19 +704,18 @@ __global__ void __launch_bounds__(128) k_set_poses(EnvView ev, SceneView sc, dou
 __device__ __forceinline__ void column_epilogue(const SceneView &sc, const CamView &cam,
                                                 double s, int k, double dx, double dy,
                                                 ColRec &out) {
-  int a = 0, b = cam.n_top;  // lo = #{i < n_top : tc[i] <= s}
-  while (a < b) {
-    int m = (a + b) >> 1;
-    if (__ldg(cam.tc + m) <= s) a = m + 1; else b = m;
-  }
-  const int lo = a;
-  a = cam.b0;
-  b = cam.H;  // hi = first i >= b0 with tf[i] <= s
-  while (a < b) {
-    int m = (a + b) >> 1;
-    if (__ldg(cam.tf + m) <= s) b = m; else a = m + 1;
-  }
-  const int hi = a;
+  // lo = #{i < n_top : tc[i] <= s} and hi = first i >= b0 with tf[i] <= s.
+  // In exact arithmetic tc_i <= s iff i <= hc - ktop / s and tf_i <= s iff
+  // i >= hc + kbot / s; an f32 estimate of each boundary is settled by the
+  // reference's own FP64 comparisons against the exact tc / tf tables (both
+  // monotone), so the result is exact whatever the estimate's error.
+  const float fs = (float)s;
+  int lo = (int)fminf(fmaxf(floorf(cam.hc - cam.ktop / fs) + 1.0f, 0.0f), (float)cam.n_top);
+  while (lo > 0 && !(__ldg(cam.tc + lo - 1) <= s)) --lo;
+  while (lo < cam.n_top && __ldg(cam.tc + lo) <= s) ++lo;
+  int hi = (int)fminf(fmaxf(ceilf(cam.hc + cam.kbot / fs), (float)cam.b0), (float)cam.H);
+  while (hi > cam.b0 && __ldg(cam.tf + hi - 1) <= s) --hi;
+  while (hi < cam.H && !(__ldg(cam.tf + hi) <= s)) ++hi;
   const bool lit = s < cam.max_range && k >= 0;
   out.lohi = (uint32_t)lo | ((uint32_t)hi << 16);
   float fdx = (float)dx, fdy = (float)dy;
@@ -738,13 +737,20 @@ __device__ __forceinline__ void column_epilogue(const SceneView &sc, const CamVi
   }
 }
 
+__device__ __forceinline__ void put_rec(const RecOut &ro, long long e, int j, const ColRec &r) {
+  const size_t p = (size_t)e * ro.W + rec_pos(j, ro.cpl);
+  const float4 *h = reinterpret_cast<const float4 *>(&r);
+  ro.a[p] = h[0];
+  ro.b[p] = h[1];
+}
+
 // _column_directions (sensors.py:96-102) + raycast_grid + epilogue for one
 // (env, column); column 0 also writes gps_compass (sensors.py:175-180).
 // COH: agent state was written earlier in the same launch (megakernel), so it
 // is read through L2 (ld.global.cg) rather than the non-coherent path.
 template <bool COH>
 __device__ __forceinline__ void cast_column(const EnvView &ev, const SceneView &sc,
-                                            const CamView &cam, int e, int j, ColRec *rec,
+                                            const CamView &cam, int e, int j, const RecOut &ro,
                                             double t_max, double *gps, double *compass) {
   double px, py, c, s;
   if (COH) {
@@ -760,7 +766,7 @@ __device__ __forceinline__ void cast_column(const EnvView &ev, const SceneView &
   ray_grid(sc, px, py, dx, dy, t_max, t, k);
   ColRec r;
   column_epilogue(sc, cam, t, k, dx, dy, r);
-  rec[(size_t)e * cam.W + j] = r;
+  put_rec(ro, e, j, r);
   if (j == 0 && (gps || compass)) {
     double ddx = sub(px, ev.ox[e]), ddy = sub(py, ev.oy[e]);
     double fc = ev.fc[e], fs = ev.fs[e];
@@ -777,14 +783,14 @@ __device__ __forceinline__ void cast_column(const EnvView &ev, const SceneView &
 
 // One thread per (env, column).
 __global__ void __launch_bounds__(128) k_column_cast(EnvView ev, SceneView sc, CamView cam,
-                                                     ColRec *__restrict__ rec, double t_max,
+                                                     RecOut ro, double t_max,
                                                      double *gps, double *compass) {
   const long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   const long long total = (long long)ev.n * cam.W;
   if (g >= total) return;
   const int e = (int)(g / cam.W);
   const int j = (int)(g - (long long)e * cam.W);
-  cast_column<false>(ev, sc, cam, e, j, rec, t_max, gps, compass);
+  cast_column<false>(ev, sc, cam, e, j, ro, t_max, gps, compass);
 }
 
 // ---------------------------------------------------- binned column cast
@@ -936,7 +942,7 @@ __device__ __forceinline__ bool bin_cell(const SceneView &sc, const BinShared &S
 }
 
 __global__ void __launch_bounds__(128) k_cast_binned(EnvView ev, SceneView sc, CamView cam,
-                                                     double focal, ColRec *__restrict__ rec,
+                                                     double focal, RecOut ro,
                                                      double *gps, double *compass) {
   extern __shared__ __align__(128) uint8_t smem[];
   const int W = cam.W;
@@ -1104,7 +1110,7 @@ __global__ void __launch_bounds__(128) k_cast_binned(EnvView ev, SceneView sc, C
       ray_grid(sc, px, py, S.dirx[j], S.diry[j], cam.max_range, t, k);
       ColRec r;
       column_epilogue(sc, cam, t, k, S.dirx[j], S.diry[j], r);
-      rec[(size_t)e * W + j] = r;
+      put_rec(ro, e, j, r);
     }
   } else {
     // pass 2: lowest index among each column's minimal-t hits
@@ -1125,7 +1131,7 @@ __global__ void __launch_bounds__(128) k_cast_binned(EnvView ev, SceneView sc, C
       const int k = key == NV_KEY_INF ? -1 : S.ibest[j];
       ColRec r;
       column_epilogue(sc, cam, t, k, S.dirx[j], S.diry[j], r);
-      rec[(size_t)e * W + j] = r;
+      put_rec(ro, e, j, r);
     }
   }
   if (tid == 0 && (gps || compass)) {
@@ -1157,12 +1163,12 @@ __global__ void k_cols_from_hits(SceneView sc, CamView cam, long long total,
                                  const double *__restrict__ t_col,
                                  const int64_t *__restrict__ i_col,
                                  const double *__restrict__ dirx,
-                                 const double *__restrict__ diry, ColRec *rec) {
+                                 const double *__restrict__ diry, RecOut ro) {
   const long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (g >= total) return;
   ColRec r;
   column_epilogue(sc, cam, t_col[g], (int)i_col[g], dirx[g], diry[g], r);
-  rec[g] = r;
+  put_rec(ro, g / ro.W, (int)(g % ro.W), r);
 }
 
 // Operator entry: raycast_grid / raycast_all over arbitrary rays.
@@ -1223,12 +1229,20 @@ __global__ void __launch_bounds__(128) k_clearance(SceneView sc, const double *p
 //                                              low byte of the f16 result
 // Worst-case error vs the reference's f64 rgb: 0.5 (rounding) + 0.0625 (f16
 // col255) + 255 * 1e-3 (t) < 0.85 of one 8-bit step (tolerance: 1 step).
+//
+// Lane mapping (all fast writers): a warp covers a row segment of 32*CPL
+// columns; lane l owns CPL/GW groups of GW = min(CPL, 4) adjacent columns,
+// group g at segment offset g*32*GW + l*GW.  A warp's group-g stores are then
+// contiguous across lanes (12-byte RGB, 16-byte depth, 8-byte semantic
+// strides: bank-conflict-free shared-memory rows), and its column records are
+// 32 consecutive 16-byte halves (device.cuh rec_pos).
 
 #define NV_H2_POINT2 0x32663266u   // (0.2, 0.2) in f16
 #define NV_H2_1024 0x64006400u     // (1024, 1024): low byte of 1024+x = round(x)
 
 struct FillArgs {
-  const ColRec *rec;
+  const float4 *ra, *rb;  // column-record planes (device.cuh), index env * W + rec_pos
+  int cpl;                // record order
   const RowRec *rows;
   int N, W, H;
   uint8_t *rgb;
@@ -1241,6 +1255,13 @@ struct FillArgs {
   unsigned int *ctr;   // [0] next unit, [1] finished warps (self-resetting)
   const uint16_t *invh;  // ceil(H/2) x W f16 shading table 1/|(d_j, v_i)|, rows
                          // mirrored (v_{H-1-i} = -v_i); env-independent
+};
+
+template <int CPL>
+struct Lanes {
+  static constexpr int GW = CPL < 4 ? CPL : 4;  // columns per group
+  static constexpr int G = CPL / GW;            // groups per lane
+  static constexpr int SEGW = 32 * CPL;         // columns per warp segment
 };
 
 __device__ __forceinline__ uint32_t h2_fma(uint32_t a, uint32_t b, uint32_t c) {
@@ -1289,15 +1310,40 @@ __device__ __forceinline__ uint64_t policy_evict_first() {
   return p;
 }
 
-// L1 prefetch of a lane's CPL column records (the next work unit's).
-template <int CPL>
-__device__ __forceinline__ void prefetch_cols(const ColRec *rp) {
-#pragma unroll
-  for (int k = 0; k < CPL * (int)sizeof(ColRec); k += 128)
-    asm volatile("prefetch.global.L1 [%0];" ::"l"(reinterpret_cast<const char *>(rp) + k));
+__device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_addr(bar)),
+      "r"(parity)
+      : "memory");
+}
+// global -> shared bulk copy completing on an mbarrier (bytes % 16 == 0)
+__device__ __forceinline__ void bulk_load(void *sdst, const void *gsrc, unsigned bytes,
+                                          uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(smem_addr(sdst)),
+      "l"(gsrc), "r"(bytes), "r"(smem_addr(bar))
+      : "memory");
 }
 
-// A lane's CPL columns (CPL/2 pixel pairs) in registers, packed.
+// A lane's CPL columns (CPL/2 pixel pairs, column k = g*GW + c) in registers.
 template <int CPL>
 struct ColRegs {
   float dw[CPL];                 // wall depth (or max_range)
@@ -1306,30 +1352,57 @@ struct ColRegs {
   uint32_t sw[CPL / 2];          // semantic pairs
 };
 
-template <int CPL, bool COH>
-__device__ __forceinline__ void load_cols(const ColRec *rp, ColRegs<CPL> &cr) {
+template <int CPL>
+__device__ __forceinline__ void unpack_cols(const float4 (&A)[CPL], const float4 (&B)[CPL],
+                                            ColRegs<CPL> &cr) {
 #pragma unroll
-  for (int k = 0; k < CPL / 2; ++k) {
-    const float4 *q = reinterpret_cast<const float4 *>(rp + 2 * k);
-    float4 a0, a1, b0, b1;
-    if (COH) {  // written earlier in this launch: read through L2
-      a0 = __ldcg(q); a1 = __ldcg(q + 1); b0 = __ldcg(q + 2); b1 = __ldcg(q + 3);
-    } else {
-      a0 = __ldg(q); a1 = __ldg(q + 1); b0 = __ldg(q + 2); b1 = __ldg(q + 3);
-    }
-    cr.dw[2 * k] = a0.x;
-    cr.dw[2 * k + 1] = b0.x;
-    uint32_t l0 = __float_as_uint(a0.w), l1 = __float_as_uint(b0.w);
-    cr.lo[2 * k] = l0 & 0xffffu;
-    cr.hi[2 * k] = l0 >> 16;
-    cr.lo[2 * k + 1] = l1 & 0xffffu;
-    cr.hi[2 * k + 1] = l1 >> 16;
-    cr.nw[k] = h2_pack(a0.y, b0.y);
-    cr.rw[k] = h2_pack(a1.x, b1.x);
-    cr.gw[k] = h2_pack(a1.y, b1.y);
-    cr.bw[k] = h2_pack(a1.z, b1.z);
-    cr.sw[k] = (__float_as_uint(a1.w) & 0xffffu) | (__float_as_uint(b1.w) << 16);
+  for (int k = 0; k < CPL; ++k) {
+    cr.dw[k] = A[k].x;
+    const uint32_t l = __float_as_uint(A[k].w);
+    cr.lo[k] = l & 0xffffu;
+    cr.hi[k] = l >> 16;
   }
+#pragma unroll
+  for (int m = 0; m < CPL / 2; ++m) {
+    cr.nw[m] = h2_pack(A[2 * m].y, A[2 * m + 1].y);
+    cr.rw[m] = h2_pack(B[2 * m].x, B[2 * m + 1].x);
+    cr.gw[m] = h2_pack(B[2 * m].y, B[2 * m + 1].y);
+    cr.bw[m] = h2_pack(B[2 * m].z, B[2 * m + 1].z);
+    cr.sw[m] = (__float_as_uint(B[2 * m].w) & 0xffffu) | (__float_as_uint(B[2 * m + 1].w) << 16);
+  }
+}
+
+// Global planes; base = env * W + seg * SEGW (records in rec_pos order).
+// COH: written earlier in the same launch (read through L2).
+template <int CPL, bool COH>
+__device__ __forceinline__ void load_cols(const FillArgs &a, size_t base, int lane,
+                                          ColRegs<CPL> &cr) {
+  float4 A[CPL], B[CPL];
+#pragma unroll
+  for (int k = 0; k < CPL; ++k) {
+    const size_t p = base + (size_t)k * 32 + lane;
+    if (COH) {
+      A[k] = __ldcg(a.ra + p);
+      B[k] = __ldcg(a.rb + p);
+    } else {
+      A[k] = __ldg(a.ra + p);
+      B[k] = __ldg(a.rb + p);
+    }
+  }
+  unpack_cols<CPL>(A, B, cr);
+}
+
+// Shared-memory planes of one env: sA/sB + seg * SEGW.
+template <int CPL>
+__device__ __forceinline__ void load_cols_smem(const float4 *sA, const float4 *sB, int lane,
+                                               ColRegs<CPL> &cr) {
+  float4 A[CPL], B[CPL];
+#pragma unroll
+  for (int k = 0; k < CPL; ++k) {
+    A[k] = sA[k * 32 + lane];
+    B[k] = sB[k * 32 + lane];
+  }
+  unpack_cols<CPL>(A, B, cr);
 }
 
 // Shade one pixel pair (columns 2k, 2k+1 of the lane) of row i.
@@ -1368,11 +1441,17 @@ __device__ __forceinline__ void pack_rgb4(const PairOut &p, const PairOut &q, ui
   w2 = __byte_perm(rg1, q.b, 0x6324);                  // b2 r3 g3 b3
 }
 
-// Row record of row i from the CTA's shared-memory copy of the row table.
-__device__ __forceinline__ void load_row(const RowRec *rows_s, uint32_t i, uint4 &q0, uint4 &q1) {
+__device__ __forceinline__ RowRec unpack_row(const RowRec *rows_s, uint32_t i) {
   const uint4 *rq = reinterpret_cast<const uint4 *>(rows_s + i);
-  q0 = rq[0];
-  q1 = rq[1];
+  const uint4 q0 = rq[0], q1 = rq[1];
+  RowRec R;
+  R.depth_p = __uint_as_float(q0.x);
+  R.sem2 = q0.y;
+  R.num2 = q0.z;
+  R.r2 = q0.w;
+  R.g2 = q1.x;
+  R.b2 = q1.y;
+  return R;
 }
 
 // Shading-table row of image row i: the table holds rows [0, ceil(H/2)) and
@@ -1381,17 +1460,69 @@ __device__ __forceinline__ uint32_t inv_row(uint32_t i, int H) {
   return i < (uint32_t)(H >> 1) ? i : (uint32_t)(H - 1) - i;
 }
 
-// The lane's CPL shading-table entries (CPL/2 f16 pairs) from global memory.
+// The lane's shading-table pairs from table row `ip` (+ segment offset).
+template <int CPL, bool GLOBAL>
+__device__ __forceinline__ void load_inv(const uint16_t *ip, int lane, uint32_t (&iv)[CPL / 2]) {
+  using Ln = Lanes<CPL>;
+#pragma unroll
+  for (int g = 0; g < Ln::G; ++g) {
+    const uint16_t *q = ip + g * 32 * Ln::GW + lane * Ln::GW;
+    if constexpr (Ln::GW == 4) {
+      const uint2 v = GLOBAL ? __ldg(reinterpret_cast<const uint2 *>(q))
+                             : *reinterpret_cast<const uint2 *>(q);
+      iv[2 * g] = v.x;
+      iv[2 * g + 1] = v.y;
+    } else {
+      iv[g] = GLOBAL ? __ldg(reinterpret_cast<const uint32_t *>(q))
+                     : *reinterpret_cast<const uint32_t *>(q);
+    }
+  }
+}
+
 template <int CPL>
-__device__ __forceinline__ void load_inv_g(const uint16_t *ip, uint32_t (&iv)[CPL / 2]) {
-  if constexpr (CPL == 8) {
-    const uint4 v = __ldg(reinterpret_cast<const uint4 *>(ip));
-    iv[0] = v.x; iv[1] = v.y; iv[2] = v.z; iv[3] = v.w;
-  } else if constexpr (CPL == 4) {
-    const uint2 v = __ldg(reinterpret_cast<const uint2 *>(ip));
-    iv[0] = v.x; iv[1] = v.y;
-  } else {
-    iv[0] = __ldg(reinterpret_cast<const uint32_t *>(ip));
+__device__ __forceinline__ void shade_row(uint32_t i, const RowRec &R, const ColRegs<CPL> &cr,
+                                          const uint32_t (&iv)[CPL / 2],
+                                          PairOut (&po)[CPL / 2]) {
+#pragma unroll
+  for (int c = 0; c < CPL / 2; ++c)
+    po[c] = shade_pair(i, R, cr.lo[2 * c], cr.hi[2 * c], cr.lo[2 * c + 1], cr.hi[2 * c + 1],
+                       cr.dw[2 * c], cr.dw[2 * c + 1], cr.nw[c], cr.rw[c], cr.gw[c], cr.bw[c],
+                       cr.sw[c], iv[c]);
+}
+
+// Writes the lane's shaded pixels of one row segment into a buffer laid out
+// like the frame (shared-memory stage / slot): px0 = pixel index of the
+// segment's first column in the buffer.
+template <int CPL>
+__device__ __forceinline__ void put_row(const PairOut (&po)[CPL / 2], uint8_t *rgb, float *dep,
+                                        uint16_t *sem, int px0, int lane) {
+  using Ln = Lanes<CPL>;
+#pragma unroll
+  for (int g = 0; g < Ln::G; ++g) {
+    const int px = px0 + g * 32 * Ln::GW + lane * Ln::GW;
+    if constexpr (Ln::GW == 4) {
+      const PairOut &p = po[2 * g], &q = po[2 * g + 1];
+      if (rgb) {
+        uint32_t w0, w1, w2;
+        pack_rgb4(p, q, w0, w1, w2);
+        uint32_t *d = reinterpret_cast<uint32_t *>(rgb + (size_t)px * 3);
+        d[0] = w0;
+        d[1] = w1;
+        d[2] = w2;
+      }
+      if (dep) *reinterpret_cast<float4 *>(dep + px) = make_float4(p.d0, p.d1, q.d0, q.d1);
+      if (sem) *reinterpret_cast<uint2 *>(sem + px) = make_uint2(p.s, q.s);
+    } else {
+      const PairOut &p = po[g];
+      if (rgb) {
+        uint16_t *d16 = reinterpret_cast<uint16_t *>(rgb + (size_t)px * 3);
+        d16[0] = (uint16_t)__byte_perm(p.r, p.g, 0x0040);  // r0 g0
+        d16[1] = (uint16_t)__byte_perm(p.b, p.r, 0x0060);  // b0 r1
+        d16[2] = (uint16_t)__byte_perm(p.g, p.b, 0x0062);  // g1 b1
+      }
+      if (dep) *reinterpret_cast<float2 *>(dep + px) = make_float2(p.d0, p.d1);
+      if (sem) *reinterpret_cast<uint32_t *>(sem + px) = p.s;
+    }
   }
 }
 
@@ -1439,24 +1570,19 @@ struct FillWarp {
 // like global memory, which lane 0 writes out with cp.async.bulk (one copy
 // per channel per stage when a warp covers full rows), evict-first in L2.
 // COH: the column records were written earlier in the same launch.
-// pf: the lane's column records of the warp's next unit (prefetched into L1
-// half-way through this one), or nullptr.
 template <int CPL, int RW, bool COH>
 __device__ __forceinline__ void fill_unit(const FillArgs &a, FillWarp<CPL, RW> &fw, int env,
-                                          int seg, int gidx, const ColRec *pf = nullptr) {
+                                          int seg, int gidx) {
   constexpr int NS = FillWarp<CPL, RW>::NS;
   constexpr int SEGW = FillWarp<CPL, RW>::SEGW;
   const int lane = threadIdx.x & 31;
   const int W = a.W, H = a.H;
-  const int col0 = seg * SEGW + lane * CPL;
   ColRegs<CPL> cr;
-  load_cols<CPL, COH>(a.rec + (size_t)env * W + col0, cr);
+  load_cols<CPL, COH>(a, (size_t)env * W + (size_t)seg * SEGW, lane, cr);
   const int r_begin = gidx * a.rows_per_unit;
   const int r_end = min(H, r_begin + a.rows_per_unit);
-  const int r_pf = r_begin + ((r_end - r_begin) >> 1);
   for (int r0 = r_begin; r0 < r_end; r0 += RW) {
     const int nr = min(RW, r_end - r0);
-    if (pf && r0 <= r_pf && r_pf < r0 + RW) prefetch_cols<CPL>(pf);
     uint8_t *buf = fw.wbase + (fw.k & (NS - 1)) * fw.stage_bytes;
     if (fw.k >= NS) {
       if (lane == 0) bulk_wait_read<NS - 1>();
@@ -1464,66 +1590,15 @@ __device__ __forceinline__ void fill_unit(const FillArgs &a, FillWarp<CPL, RW> &
     }
     for (int rr = 0; rr < nr; ++rr) {
       const uint32_t i = (uint32_t)(r0 + rr);
-      uint4 pq0, pq1;
-      load_row(fw.rows_s, i, pq0, pq1);
-      RowRec R;
-      R.depth_p = __uint_as_float(pq0.x);
-      R.sem2 = pq0.y;
-      R.num2 = pq0.z;
-      R.r2 = pq0.w;
-      R.g2 = pq1.x;
-      R.b2 = pq1.y;
+      const RowRec R = unpack_row(fw.rows_s, i);
       uint32_t iv[CPL / 2];
-      load_inv_g<CPL>(a.invh + (size_t)inv_row(i, H) * W + col0, iv);
+      load_inv<CPL, true>(a.invh + (size_t)inv_row(i, H) * W + seg * SEGW, lane, iv);
       PairOut po[CPL / 2];
-#pragma unroll
-      for (int c = 0; c < CPL / 2; ++c)
-        po[c] = shade_pair(i, R, cr.lo[2 * c], cr.hi[2 * c], cr.lo[2 * c + 1], cr.hi[2 * c + 1],
-                           cr.dw[2 * c], cr.dw[2 * c + 1], cr.nw[c], cr.rw[c], cr.gw[c], cr.bw[c],
-                           cr.sw[c], iv[c]);
-      if (fw.want_rgb) {
-        uint8_t *dst = buf + (rr * SEGW + lane * CPL) * 3;
-        if constexpr (CPL == 2) {
-          uint16_t *d16 = reinterpret_cast<uint16_t *>(dst);
-          d16[0] = (uint16_t)__byte_perm(po[0].r, po[0].g, 0x0040);  // r0 g0
-          d16[1] = (uint16_t)__byte_perm(po[0].b, po[0].r, 0x0060);  // b0 r1
-          d16[2] = (uint16_t)__byte_perm(po[0].g, po[0].b, 0x0062);  // g1 b1
-        } else {
-          uint32_t w[3 * CPL / 4];
-#pragma unroll
-          for (int q = 0; q < CPL / 4; ++q)
-            pack_rgb4(po[2 * q], po[2 * q + 1], w[3 * q], w[3 * q + 1], w[3 * q + 2]);
-          if constexpr (CPL == 4) {
-#pragma unroll
-            for (int q = 0; q < 3; ++q) reinterpret_cast<uint32_t *>(dst)[q] = w[q];
-          } else {  // CPL == 8: three 8-byte chunks
-#pragma unroll
-            for (int q = 0; q < 3; ++q)
-              reinterpret_cast<uint2 *>(dst)[q] = make_uint2(w[2 * q], w[2 * q + 1]);
-          }
-        }
-      }
-      if (fw.want_d) {
-        float *dst = reinterpret_cast<float *>(buf + fw.off_d) + rr * SEGW + lane * CPL;
-        if constexpr (CPL == 2) {
-          *reinterpret_cast<float2 *>(dst) = make_float2(po[0].d0, po[0].d1);
-        } else {
-#pragma unroll
-          for (int q = 0; q < CPL / 4; ++q)
-            reinterpret_cast<float4 *>(dst)[q] =
-                make_float4(po[2 * q].d0, po[2 * q].d1, po[2 * q + 1].d0, po[2 * q + 1].d1);
-        }
-      }
-      if (fw.want_s) {
-        uint16_t *dst = reinterpret_cast<uint16_t *>(buf + fw.off_s) + rr * SEGW + lane * CPL;
-        if constexpr (CPL == 2) {
-          *reinterpret_cast<uint32_t *>(dst) = po[0].s;
-        } else if constexpr (CPL == 4) {
-          *reinterpret_cast<uint2 *>(dst) = make_uint2(po[0].s, po[1].s);
-        } else {
-          *reinterpret_cast<uint4 *>(dst) = make_uint4(po[0].s, po[1].s, po[2].s, po[3].s);
-        }
-      }
+      shade_row<CPL>(i, R, cr, iv, po);
+      put_row<CPL>(po, fw.want_rgb ? buf : nullptr,
+                   fw.want_d ? reinterpret_cast<float *>(buf + fw.off_d) : nullptr,
+                   fw.want_s ? reinterpret_cast<uint16_t *>(buf + fw.off_s) : nullptr,
+                   rr * SEGW, lane);
     }
     fence_proxy_async();
     __syncwarp();
@@ -1568,281 +1643,118 @@ __device__ __forceinline__ void finish_grid(unsigned int *ctr) {
 // k_fill_tma: streaming frame writer over all units of a frame batch; units
 // are pulled from a self-resetting global counter (one prefetched ahead).
 template <int CPL, int RW>
-#ifndef NV_FILL_MINB
-#define NV_FILL_MINB 5
-#endif
-__global__ void __launch_bounds__(128, NV_FILL_MINB) k_fill_tma(FillArgs a) {
+__global__ void __launch_bounds__(128) k_fill_tma(FillArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
   const int lane = threadIdx.x & 31;
   FillWarp<CPL, RW> fw;
   fw.init(a, smem, threadIdx.x >> 5);
-  // Units are claimed two ahead: the current one, the next one (whose column
-  // records are prefetched into L1 during the current one) and, in flight,
-  // the one after.  Row-block-major order: warps across the GPU render the
-  // same rows of different envs at the same time.
-  const long long n_es = (long long)a.N * a.segs_per_row;
-  long long u = 0, nxt = 0;
-  if (lane == 0) {
-    u = atomicAdd(a.ctr, 1u);
-    nxt = atomicAdd(a.ctr, 1u);
-  }
+  long long u = 0;
+  if (lane == 0) u = atomicAdd(a.ctr, 1u);
   u = __shfl_sync(0xffffffffu, u, 0);
-  nxt = __shfl_sync(0xffffffffu, nxt, 0);
   while (u < a.n_units) {
-    long long after = 0;
-    if (lane == 0) after = atomicAdd(a.ctr, 1u);
+    long long nxt = 0;
+    if (lane == 0) nxt = atomicAdd(a.ctr, 1u);
+    // row-block-major order: warps across the GPU render the same rows of
+    // different envs at the same time (shared row records / table rows)
+    const long long n_es = (long long)a.N * a.segs_per_row;
     const int gidx = (int)(u / n_es);
     const long long es = u - (long long)gidx * n_es;
     const int env = (int)(es / a.segs_per_row);
     const int seg = (int)(es - (long long)env * a.segs_per_row);
-    const ColRec *pf = nullptr;
-    if (nxt < a.n_units) {
-      const long long es2 = nxt - (nxt / n_es) * n_es;
-      const int env2 = (int)(es2 / a.segs_per_row);
-      const int seg2 = (int)(es2 - (long long)env2 * a.segs_per_row);
-      pf = a.rec + (size_t)env2 * a.W + seg2 * 32 * CPL + lane * CPL;
-    }
-    fill_unit<CPL, RW, false>(a, fw, env, seg, gidx, pf);
-    u = nxt;
-    nxt = __shfl_sync(0xffffffffu, after, 0);
+    fill_unit<CPL, RW, false>(a, fw, env, seg, gidx);
+    u = __shfl_sync(0xffffffffu, nxt, 0);
   }
   finish_grid(a.ctr);
 }
 
-// ---- CTA-per-frame writer ---------------------------------------------------
-//
-// k_fill_cta: persistent, one CTA of NW warps per SM; a work item is one env's
-// whole frame.  The item's column records (W x 32 B) arrive in shared memory
-// by a TMA bulk copy issued one item ahead (mbarrier completion), so no warp
-// ever waits on L2 for them; the row table and (when it fits) the mirrored
-// half of the env-independent shading table 1/|(d_j, v_i)| sit in shared
-// memory for the whole launch.  Warp w renders column segment w % S, rows
-// [(w / S) * rpw, ...) of the frame through its own double-buffered stage,
-// written out by cp.async.bulk exactly like k_fill_tma.
-
-__device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count)
+// ---- direct-store variant: no smem staging ---------------------------------
+// Each lane stores its pixels of a row straight from registers with
+// evict-first 128/64/32-bit stores; a warp's group-g stores are contiguous.
+__device__ __forceinline__ void st_v4f(float *p, float4 v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.v4.f32 [%0], {%1,%2,%3,%4}, %5;" ::"l"(p), "f"(v.x),
+               "f"(v.y), "f"(v.z), "f"(v.w), "l"(pol)
                : "memory");
 }
-__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
-               "r"(bytes)
+__device__ __forceinline__ void st_v2u(void *p, uint32_t a, uint32_t b, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.v2.b32 [%0], {%1,%2}, %3;" ::"l"(p), "r"(a), "r"(b),
+               "l"(pol)
                : "memory");
 }
-__device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity) {
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      "@!p bra WAIT_%=;\n"
-      "}\n" ::"r"(smem_addr(bar)),
-      "r"(parity)
-      : "memory");
-}
-// global -> shared bulk copy completing on an mbarrier (bytes % 16 == 0)
-__device__ __forceinline__ void bulk_load(void *sdst, const void *gsrc, unsigned bytes,
-                                          uint64_t *bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
-          "r"(smem_addr(sdst)),
-      "l"(gsrc), "r"(bytes), "r"(smem_addr(bar))
-      : "memory");
+__device__ __forceinline__ void st_u(void *p, uint32_t a, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.b32 [%0], %1, %2;" ::"l"(p), "r"(a), "l"(pol)
+               : "memory");
 }
 
-template <int CPL>
-__device__ __forceinline__ void load_cols_smem(const ColRec *rp, ColRegs<CPL> &cr) {
-#pragma unroll
-  for (int k = 0; k < CPL / 2; ++k) {
-    const float4 *q = reinterpret_cast<const float4 *>(rp + 2 * k);
-    const float4 a0 = q[0], a1 = q[1], b0 = q[2], b1 = q[3];
-    cr.dw[2 * k] = a0.x;
-    cr.dw[2 * k + 1] = b0.x;
-    uint32_t l0 = __float_as_uint(a0.w), l1 = __float_as_uint(b0.w);
-    cr.lo[2 * k] = l0 & 0xffffu;
-    cr.hi[2 * k] = l0 >> 16;
-    cr.lo[2 * k + 1] = l1 & 0xffffu;
-    cr.hi[2 * k + 1] = l1 >> 16;
-    cr.nw[k] = h2_pack(a0.y, b0.y);
-    cr.rw[k] = h2_pack(a1.x, b1.x);
-    cr.gw[k] = h2_pack(a1.y, b1.y);
-    cr.bw[k] = h2_pack(a1.z, b1.z);
-    cr.sw[k] = (__float_as_uint(a1.w) & 0xffffu) | (__float_as_uint(b1.w) << 16);
-  }
-}
-
-template <int CPL>
-__device__ __forceinline__ void load_inv_smem(const uint16_t *ip, uint32_t (&iv)[CPL / 2]) {
-  if constexpr (CPL == 8) {
-    const uint4 v = *reinterpret_cast<const uint4 *>(ip);
-    iv[0] = v.x; iv[1] = v.y; iv[2] = v.z; iv[3] = v.w;
-  } else if constexpr (CPL == 4) {
-    const uint2 v = *reinterpret_cast<const uint2 *>(ip);
-    iv[0] = v.x; iv[1] = v.y;
-  } else {
-    iv[0] = *reinterpret_cast<const uint32_t *>(ip);
-  }
-}
-
-struct FillCtaLayout {  // byte offsets into dynamic shared memory
-  int rows, inv, cols, bar, stages, stage_bytes;
-};
-
-template <int CPL, int RW, bool TAB>
-__global__ void __launch_bounds__(512, 1) k_fill_cta(FillArgs a, FillCtaLayout L) {
-  extern __shared__ __align__(128) uint8_t smem[];
-  constexpr int NS = 2;
-  constexpr int SEGW = 32 * CPL;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+template <int CPL, bool COH>
+__device__ __forceinline__ void fill_unit_direct(const FillArgs &a, const RowRec *rows_s,
+                                                 uint64_t pol, int env, int seg, int gidx) {
+  using Ln = Lanes<CPL>;
+  const int lane = threadIdx.x & 31;
   const int W = a.W, H = a.H;
-  const RowRec *rows_s = reinterpret_cast<const RowRec *>(smem + L.rows);
-  const uint16_t *inv_s = reinterpret_cast<const uint16_t *>(smem + L.inv);
-  ColRec *cols_s = reinterpret_cast<ColRec *>(smem + L.cols);  // 2 x W
-  uint64_t *bar = reinterpret_cast<uint64_t *>(smem + L.bar);   // 2
-  const unsigned col_bytes = (unsigned)W * sizeof(ColRec);
-  int e = blockIdx.x;
-  if (threadIdx.x == 0) {
-    mbar_init(bar, 1);
-    mbar_init(bar + 1, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    if (e < a.N) {
-      mbar_expect_tx(bar, col_bytes);
-      bulk_load(cols_s, a.rec + (size_t)e * W, col_bytes, bar);
+  ColRegs<CPL> cr;
+  load_cols<CPL, COH>(a, (size_t)env * W + (size_t)seg * Ln::SEGW, lane, cr);
+  const int r_begin = gidx * a.rows_per_unit;
+  const int r_end = min(H, r_begin + a.rows_per_unit);
+  for (int r = r_begin; r < r_end; ++r) {
+    const uint32_t i = (uint32_t)r;
+    const RowRec R = unpack_row(rows_s, i);
+    uint32_t iv[CPL / 2];
+    load_inv<CPL, true>(a.invh + (size_t)inv_row(i, H) * W + seg * Ln::SEGW, lane, iv);
+    PairOut po[CPL / 2];
+    shade_row<CPL>(i, R, cr, iv, po);
+    const size_t row0 = ((size_t)env * H + r) * W + (size_t)seg * Ln::SEGW;
+#pragma unroll
+    for (int g = 0; g < Ln::G; ++g) {
+      const size_t px = row0 + g * 32 * Ln::GW + lane * Ln::GW;
+      if constexpr (Ln::GW == 4) {
+        const PairOut &p = po[2 * g], &q = po[2 * g + 1];
+        if (a.rgb) {
+          uint32_t w0, w1, w2;
+          pack_rgb4(p, q, w0, w1, w2);
+          uint8_t *d = a.rgb + px * 3;
+          st_u(d, w0, pol);
+          st_u(d + 4, w1, pol);
+          st_u(d + 8, w2, pol);
+        }
+        if (a.depth) st_v4f(a.depth + px, make_float4(p.d0, p.d1, q.d0, q.d1), pol);
+        if (a.sem) st_v2u(a.sem + px, p.s, q.s, pol);
+      } else {
+        const PairOut &p = po[g];
+        if (a.rgb) {
+          uint16_t *d16 = reinterpret_cast<uint16_t *>(a.rgb + px * 3);
+          d16[0] = (uint16_t)__byte_perm(p.r, p.g, 0x0040);
+          d16[1] = (uint16_t)__byte_perm(p.b, p.r, 0x0060);
+          d16[2] = (uint16_t)__byte_perm(p.g, p.b, 0x0062);
+        }
+        if (a.depth) *reinterpret_cast<float2 *>(a.depth + px) = make_float2(p.d0, p.d1);
+        if (a.sem) *reinterpret_cast<uint32_t *>(a.sem + px) = p.s;
+      }
     }
   }
-  {
-    const uint4 *src = reinterpret_cast<const uint4 *>(a.rows);
-    uint4 *dst = reinterpret_cast<uint4 *>(smem + L.rows);
-    for (int k = threadIdx.x; k < H * 2; k += blockDim.x) dst[k] = __ldg(src + k);
-    if (TAB) {
-      const uint4 *s2 = reinterpret_cast<const uint4 *>(a.invh);
-      uint4 *d2 = reinterpret_cast<uint4 *>(smem + L.inv);
-      const int n16 = ((H + 1) / 2) * W * 2 / 16;
-      for (int k = threadIdx.x; k < n16; k += blockDim.x) d2[k] = __ldg(s2 + k);
-    }
-  }
-  __syncthreads();
-  const bool want_rgb = a.rgb != nullptr, want_d = a.depth != nullptr, want_s = a.sem != nullptr;
-  const int off_d = want_rgb ? RW * SEGW * 3 : 0;
-  const int off_s = off_d + (want_d ? RW * SEGW * 4 : 0);
-  uint8_t *wbase = smem + L.stages + (size_t)warp * NS * L.stage_bytes;
+}
+
+template <int CPL>
+__global__ void __launch_bounds__(128) k_fill_direct(FillArgs a) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  stage_rows(a, smem);
+  const RowRec *rows_s = reinterpret_cast<const RowRec *>(smem);
+  const int lane = threadIdx.x & 31;
   const uint64_t pol = policy_evict_first();
-  const int S = a.segs_per_row;
-  const int seg = warp % S;
-  const int rpw = (H * S + nw - 1) / nw;
-  const int r_begin = (warp / S) * rpw;
-  const int r_end = min(H, r_begin + rpw);
-  const int col0 = seg * SEGW + lane * CPL;
-  int kst = 0;  // stages issued by this warp
-  for (int it = 0; e < a.N; ++it, e += gridDim.x) {
-    const int en = e + gridDim.x;
-    if (threadIdx.x == 0 && en < a.N) {  // prefetch the next item's column records
-      uint64_t *b = bar + ((it + 1) & 1);
-      mbar_expect_tx(b, col_bytes);
-      bulk_load(cols_s + ((it + 1) & 1) * W, a.rec + (size_t)en * W, col_bytes, b);
-    }
-    mbar_wait(bar + (it & 1), (unsigned)((it >> 1) & 1));
-    ColRegs<CPL> cr;
-    load_cols_smem<CPL>(cols_s + (it & 1) * W + col0, cr);
-    for (int r0 = r_begin; r0 < r_end; r0 += RW) {
-      const int nr = min(RW, r_end - r0);
-      uint8_t *buf = wbase + (kst & (NS - 1)) * L.stage_bytes;
-      if (kst >= NS) {
-        if (lane == 0) bulk_wait_read<NS - 1>();
-        __syncwarp();
-      }
-      for (int rr = 0; rr < nr; ++rr) {
-        const uint32_t i = (uint32_t)(r0 + rr);
-        uint4 pq0, pq1;
-        load_row(rows_s, i, pq0, pq1);
-        RowRec R;
-        R.depth_p = __uint_as_float(pq0.x);
-        R.sem2 = pq0.y;
-        R.num2 = pq0.z;
-        R.r2 = pq0.w;
-        R.g2 = pq1.x;
-        R.b2 = pq1.y;
-        uint32_t iv[CPL / 2];
-        if constexpr (TAB)
-          load_inv_smem<CPL>(inv_s + (size_t)inv_row(i, H) * W + col0, iv);
-        else
-          load_inv_g<CPL>(a.invh + (size_t)inv_row(i, H) * W + col0, iv);
-        PairOut po[CPL / 2];
-#pragma unroll
-        for (int c = 0; c < CPL / 2; ++c)
-          po[c] = shade_pair(i, R, cr.lo[2 * c], cr.hi[2 * c], cr.lo[2 * c + 1],
-                             cr.hi[2 * c + 1], cr.dw[2 * c], cr.dw[2 * c + 1], cr.nw[c], cr.rw[c],
-                             cr.gw[c], cr.bw[c], cr.sw[c], iv[c]);
-        if (want_rgb) {
-          uint8_t *dst = buf + (rr * SEGW + lane * CPL) * 3;
-          if constexpr (CPL == 2) {
-            uint16_t *d16 = reinterpret_cast<uint16_t *>(dst);
-            d16[0] = (uint16_t)__byte_perm(po[0].r, po[0].g, 0x0040);
-            d16[1] = (uint16_t)__byte_perm(po[0].b, po[0].r, 0x0060);
-            d16[2] = (uint16_t)__byte_perm(po[0].g, po[0].b, 0x0062);
-          } else {
-            uint32_t w[3 * CPL / 4];
-#pragma unroll
-            for (int q = 0; q < CPL / 4; ++q)
-              pack_rgb4(po[2 * q], po[2 * q + 1], w[3 * q], w[3 * q + 1], w[3 * q + 2]);
-            if constexpr (CPL == 4) {
-#pragma unroll
-              for (int q = 0; q < 3; ++q) reinterpret_cast<uint32_t *>(dst)[q] = w[q];
-            } else {
-#pragma unroll
-              for (int q = 0; q < 3; ++q)
-                reinterpret_cast<uint2 *>(dst)[q] = make_uint2(w[2 * q], w[2 * q + 1]);
-            }
-          }
-        }
-        if (want_d) {
-          float *dst = reinterpret_cast<float *>(buf + off_d) + rr * SEGW + lane * CPL;
-          if constexpr (CPL == 2) {
-            *reinterpret_cast<float2 *>(dst) = make_float2(po[0].d0, po[0].d1);
-          } else {
-#pragma unroll
-            for (int q = 0; q < CPL / 4; ++q)
-              reinterpret_cast<float4 *>(dst)[q] =
-                  make_float4(po[2 * q].d0, po[2 * q].d1, po[2 * q + 1].d0, po[2 * q + 1].d1);
-          }
-        }
-        if (want_s) {
-          uint16_t *dst = reinterpret_cast<uint16_t *>(buf + off_s) + rr * SEGW + lane * CPL;
-          if constexpr (CPL == 2) {
-            *reinterpret_cast<uint32_t *>(dst) = po[0].s;
-          } else if constexpr (CPL == 4) {
-            *reinterpret_cast<uint2 *>(dst) = make_uint2(po[0].s, po[1].s);
-          } else {
-            *reinterpret_cast<uint4 *>(dst) = make_uint4(po[0].s, po[1].s, po[2].s, po[3].s);
-          }
-        }
-      }
-      fence_proxy_async();
-      __syncwarp();
-      if (lane == 0) {
-        if (S == 1) {
-          const size_t pix0 = ((size_t)e * H + r0) * W;
-          if (want_rgb) bulk_store(a.rgb + pix0 * 3, buf, (unsigned)(nr * W * 3), pol);
-          if (want_d) bulk_store(a.depth + pix0, buf + off_d, (unsigned)(nr * W * 4), pol);
-          if (want_s) bulk_store(a.sem + pix0, buf + off_s, (unsigned)(nr * W * 2), pol);
-        } else {
-          for (int rr = 0; rr < nr; ++rr) {
-            const size_t pix0 = ((size_t)e * H + r0 + rr) * W + (size_t)seg * SEGW;
-            if (want_rgb)
-              bulk_store(a.rgb + pix0 * 3, buf + rr * SEGW * 3, (unsigned)(SEGW * 3), pol);
-            if (want_d)
-              bulk_store(a.depth + pix0, buf + off_d + rr * SEGW * 4, (unsigned)(SEGW * 4), pol);
-            if (want_s)
-              bulk_store(a.sem + pix0, buf + off_s + rr * SEGW * 2, (unsigned)(SEGW * 2), pol);
-          }
-        }
-        bulk_commit();
-      }
-      ++kst;
-    }
-    __syncthreads();  // column buffer (it & 1) is free for item it + 2
+  long long u = 0;
+  if (lane == 0) u = atomicAdd(a.ctr, 1u);
+  u = __shfl_sync(0xffffffffu, u, 0);
+  while (u < a.n_units) {
+    long long nxt = 0;
+    if (lane == 0) nxt = atomicAdd(a.ctr, 1u);
+    const long long n_es = (long long)a.N * a.segs_per_row;
+    const int gidx = (int)(u / n_es);
+    const long long es = u - (long long)gidx * n_es;
+    const int env = (int)(es / a.segs_per_row);
+    const int seg = (int)(es - (long long)env * a.segs_per_row);
+    fill_unit_direct<CPL, false>(a, rows_s, pol, env, seg, gidx);
+    u = __shfl_sync(0xffffffffu, nxt, 0);
   }
-  if (lane == 0) bulk_wait_all();
+  finish_grid(a.ctr);
 }
 
 // ---- warp-specialised frame writer ------------------------------------------
@@ -1854,10 +1766,9 @@ __global__ void __launch_bounds__(512, 1) k_fill_cta(FillArgs a, FillCtaLayout L
 // the store warp's elected lane waits on the slot's `full` mbarrier, issues
 // the cp.async.bulk stores (evict-first), and releases the previous slot
 // through its `empty` mbarrier once the bulk engine has read it.  The same
-// lane prefetches the next item's column records into a double buffer with a
-// bulk copy.  Producers never touch L2 except through the store path: row
-// records, the shading table and column records are all shared-memory reads.
-
+// lane prefetches the next item's column-record planes into a double buffer
+// with bulk copies.  Producers never touch L2: row records, the shading table
+// and column records are all shared-memory reads.
 #ifndef NV_WS_DEBUG
 #define NV_WS_DEBUG 0  // 1: producers skip rendering, 2: no bulk stores (bound studies)
 #endif
@@ -1866,26 +1777,22 @@ struct FillWsLayout {  // byte offsets into dynamic shared memory + ring geometr
   int slot_bytes, nslot, slot_rows;
 };
 
-__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
-}
-
 template <int CPL, bool TAB, int RPW>
 __global__ void __launch_bounds__(544, 1) k_fill_ws(FillArgs a, FillWsLayout L) {
   extern __shared__ __align__(128) uint8_t smem[];
-  constexpr int SEGW = 32 * CPL;
+  using Ln = Lanes<CPL>;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nw = (blockDim.x >> 5) - 1;  // producer warps
   const int W = a.W, H = a.H, S = a.segs_per_row, R = L.slot_rows, NSLOT = L.nslot;
   const RowRec *rows_s = reinterpret_cast<const RowRec *>(smem + L.rows);
   const uint16_t *inv_s = reinterpret_cast<const uint16_t *>(smem + L.inv);
-  ColRec *cols_s = reinterpret_cast<ColRec *>(smem + L.cols);  // 2 x W
+  float4 *cols_s = reinterpret_cast<float4 *>(smem + L.cols);  // [buf][A | B][W]
   uint64_t *full = reinterpret_cast<uint64_t *>(smem + L.bars);
   uint64_t *empty = full + NSLOT;
   uint64_t *colfull = empty + NSLOT;
   uint64_t *colempty = colfull + 2;
   uint8_t *slots = smem + L.slots;
-  const unsigned col_bytes = (unsigned)W * sizeof(ColRec);
+  const unsigned plane_bytes = (unsigned)W * 16u;
   const bool want_rgb = a.rgb != nullptr, want_d = a.depth != nullptr, want_s = a.sem != nullptr;
   const int off_d = want_rgb ? R * W * 3 : 0;
   const int off_s = off_d + (want_d ? R * W * 4 : 0);
@@ -1917,19 +1824,21 @@ __global__ void __launch_bounds__(544, 1) k_fill_ws(FillArgs a, FillWsLayout L) 
     // ------------------------------------------------------------ store warp
     if (lane != 0) return;
     const uint64_t pol = policy_evict_first();
+    auto load_item = [&](int buf, int env) {
+      uint64_t *b = colfull + buf;
+      mbar_expect_tx(b, 2 * plane_bytes);
+      bulk_load(cols_s + (size_t)buf * 2 * W, a.ra + (size_t)env * W, plane_bytes, b);
+      bulk_load(cols_s + (size_t)buf * 2 * W + W, a.rb + (size_t)env * W, plane_bytes, b);
+    };
     int e = blockIdx.x;
-    if (e < a.N) {
-      mbar_expect_tx(colfull, col_bytes);
-      bulk_load(cols_s, a.rec + (size_t)e * W, col_bytes, colfull);
-    }
+    if (e < a.N) load_item(0, e);
     unsigned k = 0, slot = 0, use = 0, prev = 0;
     for (int it = 0; e < a.N; ++it, e += gridDim.x) {
       const int en = e + gridDim.x;
       if (en < a.N) {
         const int j = it + 1;
         if (j >= 2) mbar_wait(colempty + (j & 1), (unsigned)(((j >> 1) - 1) & 1));
-        mbar_expect_tx(colfull + (j & 1), col_bytes);
-        bulk_load(cols_s + (j & 1) * W, a.rec + (size_t)en * W, col_bytes, colfull + (j & 1));
+        load_item(j & 1, en);
       }
       for (int sl = 0; sl < slots_per_item; ++sl, ++k) {
         mbar_wait(full + slot, use & 1u);
@@ -1959,15 +1868,15 @@ __global__ void __launch_bounds__(544, 1) k_fill_ws(FillArgs a, FillWsLayout L) 
   }
   // -------------------------------------------------------------- producers
   const int seg = warp % S;
-  const int rsub = warp / S;        // first row of this warp within a slot
-  const int rstride = nw / S;       // row stride between the warp's RPW rows
-  const int col0 = seg * SEGW + lane * CPL;
+  const int rsub = warp / S;   // first row of this warp within a slot
+  const int rstride = nw / S;  // row stride between the warp's RPW rows
   unsigned slot = 0, use = 0;
   int e = blockIdx.x;
   for (int it = 0; e < a.N; ++it, e += gridDim.x) {
     mbar_wait(colfull + (it & 1), (unsigned)((it >> 1) & 1));
     ColRegs<CPL> cr;
-    load_cols_smem<CPL>(cols_s + (it & 1) * W + col0, cr);
+    const float4 *cA = cols_s + (size_t)(it & 1) * 2 * W + seg * Ln::SEGW;
+    load_cols_smem<CPL>(cA, cA + W, lane, cr);
     __syncwarp();
     if (lane == 0) mbar_arrive(colempty + (it & 1));
     for (int sl = 0; sl < slots_per_item; ++sl) {
@@ -1981,70 +1890,18 @@ __global__ void __launch_bounds__(544, 1) k_fill_ws(FillArgs a, FillWsLayout L) 
         (void)buf; (void)i;
         continue;
 #endif
-        uint4 pq0, pq1;
-        load_row(rows_s, i, pq0, pq1);
-        RowRec Rr;
-        Rr.depth_p = __uint_as_float(pq0.x);
-        Rr.sem2 = pq0.y;
-        Rr.num2 = pq0.z;
-        Rr.r2 = pq0.w;
-        Rr.g2 = pq1.x;
-        Rr.b2 = pq1.y;
+        const RowRec Rr = unpack_row(rows_s, i);
         uint32_t iv[CPL / 2];
         if constexpr (TAB)
-          load_inv_smem<CPL>(inv_s + (size_t)inv_row(i, H) * W + col0, iv);
+          load_inv<CPL, false>(inv_s + (size_t)inv_row(i, H) * W + seg * Ln::SEGW, lane, iv);
         else
-          load_inv_g<CPL>(a.invh + (size_t)inv_row(i, H) * W + col0, iv);
+          load_inv<CPL, true>(a.invh + (size_t)inv_row(i, H) * W + seg * Ln::SEGW, lane, iv);
         PairOut po[CPL / 2];
-#pragma unroll
-        for (int c = 0; c < CPL / 2; ++c)
-          po[c] = shade_pair(i, Rr, cr.lo[2 * c], cr.hi[2 * c], cr.lo[2 * c + 1],
-                             cr.hi[2 * c + 1], cr.dw[2 * c], cr.dw[2 * c + 1], cr.nw[c], cr.rw[c],
-                             cr.gw[c], cr.bw[c], cr.sw[c], iv[c]);
-        const int px = rs * W + col0;  // pixel index within the slot
-        if (want_rgb) {
-          uint8_t *dst = buf + (size_t)px * 3;
-          if constexpr (CPL == 2) {
-            uint16_t *d16 = reinterpret_cast<uint16_t *>(dst);
-            d16[0] = (uint16_t)__byte_perm(po[0].r, po[0].g, 0x0040);
-            d16[1] = (uint16_t)__byte_perm(po[0].b, po[0].r, 0x0060);
-            d16[2] = (uint16_t)__byte_perm(po[0].g, po[0].b, 0x0062);
-          } else {
-            uint32_t w[3 * CPL / 4];
-#pragma unroll
-            for (int q = 0; q < CPL / 4; ++q)
-              pack_rgb4(po[2 * q], po[2 * q + 1], w[3 * q], w[3 * q + 1], w[3 * q + 2]);
-            if constexpr (CPL == 4) {
-#pragma unroll
-              for (int q = 0; q < 3; ++q) reinterpret_cast<uint32_t *>(dst)[q] = w[q];
-            } else {
-#pragma unroll
-              for (int q = 0; q < 3; ++q)
-                reinterpret_cast<uint2 *>(dst)[q] = make_uint2(w[2 * q], w[2 * q + 1]);
-            }
-          }
-        }
-        if (want_d) {
-          float *dst = reinterpret_cast<float *>(buf + off_d) + px;
-          if constexpr (CPL == 2) {
-            *reinterpret_cast<float2 *>(dst) = make_float2(po[0].d0, po[0].d1);
-          } else {
-#pragma unroll
-            for (int q = 0; q < CPL / 4; ++q)
-              reinterpret_cast<float4 *>(dst)[q] =
-                  make_float4(po[2 * q].d0, po[2 * q].d1, po[2 * q + 1].d0, po[2 * q + 1].d1);
-          }
-        }
-        if (want_s) {
-          uint16_t *dst = reinterpret_cast<uint16_t *>(buf + off_s) + px;
-          if constexpr (CPL == 2) {
-            *reinterpret_cast<uint32_t *>(dst) = po[0].s;
-          } else if constexpr (CPL == 4) {
-            *reinterpret_cast<uint2 *>(dst) = make_uint2(po[0].s, po[1].s);
-          } else {
-            *reinterpret_cast<uint4 *>(dst) = make_uint4(po[0].s, po[1].s, po[2].s, po[3].s);
-          }
-        }
+        shade_row<CPL>(i, Rr, cr, iv, po);
+        put_row<CPL>(po, want_rgb ? buf : nullptr,
+                     want_d ? reinterpret_cast<float *>(buf + off_d) : nullptr,
+                     want_s ? reinterpret_cast<uint16_t *>(buf + off_s) : nullptr,
+                     rs * W + seg * Ln::SEGW, lane);
       }
       fence_proxy_async();
       __syncwarp();
@@ -2055,136 +1912,6 @@ __global__ void __launch_bounds__(544, 1) k_fill_ws(FillArgs a, FillWsLayout L) 
       }
     }
   }
-}
-
-// ---- direct-store variant: no smem staging ---------------------------------
-// Each lane stores its CPL pixels of a row straight from registers: depth as
-// one 256-bit store (STG.256, sm_100), semantic as 128-bit, RGB as three
-// 64-bit stores; a warp covers W contiguous pixels per row, so every row is a
-// fully coalesced run per channel and partial sectors merge in L2.  Without
-// stage buffers the whole L1 serves the column records.
-__device__ __forceinline__ void st_v8f(float *p, const float (&v)[8], uint64_t pol) {
-  asm volatile(
-      "st.global.L2::cache_hint.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8}, %9;" ::"l"(p),
-      "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7]),
-      "l"(pol)
-      : "memory");
-}
-__device__ __forceinline__ void st_v4u(void *p, uint32_t a, uint32_t b, uint32_t c, uint32_t d,
-                                       uint64_t pol) {
-  asm volatile("st.global.L2::cache_hint.v4.b32 [%0], {%1,%2,%3,%4}, %5;" ::"l"(p), "r"(a),
-               "r"(b), "r"(c), "r"(d), "l"(pol)
-               : "memory");
-}
-__device__ __forceinline__ void st_v2u(void *p, uint32_t a, uint32_t b, uint64_t pol) {
-  asm volatile("st.global.L2::cache_hint.v2.b32 [%0], {%1,%2}, %3;" ::"l"(p), "r"(a), "r"(b),
-               "l"(pol)
-               : "memory");
-}
-
-template <int CPL, bool COH>
-__device__ __forceinline__ void fill_unit_direct(const FillArgs &a, const RowRec *rows_s,
-                                                 uint64_t pol, int env, int seg, int gidx) {
-  constexpr int SEGW = 32 * CPL;
-  const int lane = threadIdx.x & 31;
-  const int W = a.W, H = a.H;
-  const int col0 = seg * SEGW + lane * CPL;
-  ColRegs<CPL> cr;
-  load_cols<CPL, COH>(a.rec + (size_t)env * W + col0, cr);
-  const int r_begin = gidx * a.rows_per_unit;
-  const int r_end = min(H, r_begin + a.rows_per_unit);
-  size_t pix = ((size_t)env * H + r_begin) * W + col0;  // first pixel of this lane's run
-  for (int r = r_begin; r < r_end; ++r, pix += W) {
-    const uint32_t i = (uint32_t)r;
-    uint4 pq0, pq1;
-    load_row(rows_s, i, pq0, pq1);
-    RowRec R;
-    R.depth_p = __uint_as_float(pq0.x);
-    R.sem2 = pq0.y;
-    R.num2 = pq0.z;
-    R.r2 = pq0.w;
-    R.g2 = pq1.x;
-    R.b2 = pq1.y;
-    uint32_t iv[CPL / 2];
-    load_inv_g<CPL>(a.invh + (size_t)inv_row(i, H) * W + col0, iv);
-    PairOut po[CPL / 2];
-#pragma unroll
-    for (int c = 0; c < CPL / 2; ++c)
-      po[c] = shade_pair(i, R, cr.lo[2 * c], cr.hi[2 * c], cr.lo[2 * c + 1], cr.hi[2 * c + 1],
-                         cr.dw[2 * c], cr.dw[2 * c + 1], cr.nw[c], cr.rw[c], cr.gw[c], cr.bw[c],
-                         cr.sw[c], iv[c]);
-    if (a.rgb) {
-      uint8_t *dst = a.rgb + pix * 3;
-      if constexpr (CPL == 2) {
-        uint16_t *d16 = reinterpret_cast<uint16_t *>(dst);
-        d16[0] = (uint16_t)__byte_perm(po[0].r, po[0].g, 0x0040);
-        d16[1] = (uint16_t)__byte_perm(po[0].b, po[0].r, 0x0060);
-        d16[2] = (uint16_t)__byte_perm(po[0].g, po[0].b, 0x0062);
-      } else {
-        uint32_t w[3 * CPL / 4];
-#pragma unroll
-        for (int q = 0; q < CPL / 4; ++q)
-          pack_rgb4(po[2 * q], po[2 * q + 1], w[3 * q], w[3 * q + 1], w[3 * q + 2]);
-        if constexpr (CPL == 4) {
-#pragma unroll
-          for (int q = 0; q < 3; ++q) reinterpret_cast<uint32_t *>(dst)[q] = w[q];
-        } else {
-#pragma unroll
-          for (int q = 0; q < 3; ++q) st_v2u(dst + 8 * q, w[2 * q], w[2 * q + 1], pol);
-        }
-      }
-    }
-    if (a.depth) {
-      float *dst = a.depth + pix;
-      if constexpr (CPL == 8) {
-        const float v[8] = {po[0].d0, po[0].d1, po[1].d0, po[1].d1,
-                            po[2].d0, po[2].d1, po[3].d0, po[3].d1};
-        st_v8f(dst, v, pol);
-      } else if constexpr (CPL == 4) {
-        st_v4u(dst, __float_as_uint(po[0].d0), __float_as_uint(po[0].d1),
-               __float_as_uint(po[1].d0), __float_as_uint(po[1].d1), pol);
-      } else {
-        st_v2u(dst, __float_as_uint(po[0].d0), __float_as_uint(po[0].d1), pol);
-      }
-    }
-    if (a.sem) {
-      uint16_t *dst = a.sem + pix;
-      if constexpr (CPL == 8) {
-        st_v4u(dst, po[0].s, po[1].s, po[2].s, po[3].s, pol);
-      } else if constexpr (CPL == 4) {
-        st_v2u(dst, po[0].s, po[1].s, pol);
-      } else {
-        *reinterpret_cast<uint32_t *>(dst) = po[0].s;
-      }
-    }
-  }
-}
-
-template <int CPL>
-__global__ void __launch_bounds__(128) k_fill_direct(FillArgs a) {
-  extern __shared__ __align__(128) uint8_t smem[];
-  stage_rows(a, smem);
-  const RowRec *rows_s = reinterpret_cast<const RowRec *>(smem);
-  const int lane = threadIdx.x & 31;
-  const uint64_t pol = policy_evict_first();
-  long long u = 0;
-  if (lane == 0) u = atomicAdd(a.ctr, 1u);
-  u = __shfl_sync(0xffffffffu, u, 0);
-  while (u < a.n_units) {
-    long long nxt = 0;
-    if (lane == 0) nxt = atomicAdd(a.ctr, 1u);
-    // row-block-major order: warps across the GPU render the same rows of
-    // different envs at the same time, so the row records and shading-table
-    // slice they share stay hot in every SM's L1
-    const long long n_es = (long long)a.N * a.segs_per_row;
-    const int gidx = (int)(u / n_es);
-    const long long es = u - (long long)gidx * n_es;
-    const int env = (int)(es / a.segs_per_row);
-    const int seg = (int)(es - (long long)env * a.segs_per_row);
-    fill_unit_direct<CPL, false>(a, rows_s, pol, env, seg, gidx);
-    u = __shfl_sync(0xffffffffu, nxt, 0);
-  }
-  finish_grid(a.ctr);
 }
 
 // ----------------------------------------------------------- megakernel
@@ -2209,6 +1936,7 @@ struct MegaArgs {
   CamView cam;
   AgentCfg cfg;
   FillArgs f;
+  RecOut ro;  // the same planes as f.ra / f.rb, writable
   const int8_t *actions;
   uint8_t *collided;
   double *disp;
@@ -2264,8 +1992,7 @@ __global__ void __launch_bounds__(128) k_step_render(MegaArgs m) {
     } else if (type == NV_TASK_CAST) {
       wait_at_least(sync, 1u);
       const int j = sub * 32 + lane;
-      if (j < m.cam.W) cast_column<true>(m.ev, m.sc, m.cam, e, j, const_cast<ColRec *>(m.f.rec),
-                                         m.t_max, m.gps, m.compass);
+      if (j < m.cam.W) cast_column<true>(m.ev, m.sc, m.cam, e, j, m.ro, m.t_max, m.gps, m.compass);
       __syncwarp();
       if (lane == 0) {
         __threadfence();
@@ -2287,8 +2014,8 @@ __global__ void __launch_bounds__(128) k_step_render(MegaArgs m) {
   finish_grid(m.f.ctr);
 }
 
-// One thread per pixel, any W/H; the same f16 arithmetic as k_fill_tma (one
-// half of each pair), so both paths produce identical frames.
+// One thread per pixel, any W/H; the same f16 arithmetic as the fast writers
+// (one half of each pair), so every path produces identical frames.
 __global__ void k_fill_generic(FillArgs a) {
   const long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   const long long total = (long long)a.N * a.H * a.W;
@@ -2297,13 +2024,15 @@ __global__ void k_fill_generic(FillArgs a) {
   const long long ei = p / a.W;
   const uint32_t i = (uint32_t)(ei % a.H);
   const int e = (int)(ei / a.H);
-  const ColRec c = a.rec[(size_t)e * a.W + j];
+  const size_t q = (size_t)e * a.W + rec_pos(j, a.cpl);
+  const float4 A = a.ra[q], B = a.rb[q];
   const RowRec R = a.rows[i];
-  const uint32_t lo = c.lohi & 0xffffu, hi = c.lohi >> 16;
+  const uint32_t l = __float_as_uint(A.w);
+  const uint32_t lo = l & 0xffffu, hi = l >> 16;
   const uint32_t inv = a.invh[(size_t)inv_row(i, a.H) * a.W + j];
-  PairOut o = shade_pair(i, R, lo, hi, lo, hi, c.depth_w, c.depth_w, h2_pack(c.num08_w, 0.f),
-                         h2_pack(c.col_w[0], 0.f), h2_pack(c.col_w[1], 0.f),
-                         h2_pack(c.col_w[2], 0.f), c.sem_w & 0xffffu, inv);
+  PairOut o = shade_pair(i, R, lo, hi, lo, hi, A.x, A.x, h2_pack(A.y, 0.f), h2_pack(B.x, 0.f),
+                         h2_pack(B.y, 0.f), h2_pack(B.z, 0.f), __float_as_uint(B.w) & 0xffffu,
+                         inv);
   if (a.depth) a.depth[p] = o.d0;
   if (a.sem) a.sem[p] = (uint16_t)o.s;
   if (a.rgb) {

@@ -87,6 +87,7 @@ struct Camera {
   int W = 0, H = 0;
   double focal = 0, max_range = 0;
   int n_top = 0, b0 = 0;
+  float ktop = 0.f, kbot = 0.f;
   double tables_cam_h = NAN;
   DevBuf u, tc, tf, rows, invh;
   DevBuf rec;      // ColRec N x W
@@ -292,6 +293,8 @@ int build_camera_tables(nv_ctx *c, Camera &cam, double cam_h) {
   TRY(upload(cam.invh, invh));
   cam.n_top = n_top;
   cam.b0 = b0;
+  cam.ktop = (float)(cam.focal * (c->wall_h - cam_h));
+  cam.kbot = (float)(cam.focal * cam_h);
   TRY(upload(cam.u, u));
   TRY(upload(cam.tc, tc));
   TRY(upload(cam.tf, tf));
@@ -300,8 +303,25 @@ int build_camera_tables(nv_ctx *c, Camera &cam, double cam_h) {
   return NV_OK;
 }
 
+// Record order used by the fast fill writers for a frame width (rec_pos).
+int fast_cpl(int W) { return W % 256 == 0 ? 8 : (W == 128 ? 4 : (W == 64 ? 2 : 0)); }
+
+// Column-record planes of N envs in the camera's record buffer (A then B).
+RecOut rec_out(Camera &cam, int64_t N) {
+  RecOut r;
+  r.a = cam.rec.as<float4>();
+  r.b = r.a + (size_t)N * cam.W;
+  r.W = cam.W;
+  r.cpl = fast_cpl(cam.W);
+  return r;
+}
+
 CamView cam_view(const Camera &cam) {
   CamView v;
+  v.cpl = fast_cpl(cam.W);
+  v.hc = (float)(cam.H * 0.5 - 0.5);
+  v.ktop = cam.ktop;
+  v.kbot = cam.kbot;
   v.W = cam.W; v.H = cam.H; v.n_top = cam.n_top; v.b0 = cam.b0; v.max_range = cam.max_range;
   v.u = cam.u.as<double>(); v.tc = cam.tc.as<double>(); v.tf = cam.tf.as<double>();
   v.rows = cam.rows.as<RowRec>();
@@ -426,7 +446,10 @@ int launch_mega(nv_ctx *c, Camera &cam, const int8_t *actions, uint8_t *rgb, flo
   m.cam = cam_view(cam);
   m.cfg = nvk::AgentCfg{c->radius, c->step, c->turn_rad};
   nvk::FillArgs &a = m.f;
-  a.rec = cam.rec.as<ColRec>();
+  m.ro = rec_out(cam, c->n_envs);
+  a.ra = m.ro.a;
+  a.rb = m.ro.b;
+  a.cpl = m.ro.cpl;
   a.rows = cam.rows.as<RowRec>();
   a.invh = cam.invh.as<uint16_t>();
   a.N = (int)c->n_envs; a.W = cam.W; a.H = cam.H;
@@ -482,56 +505,6 @@ int launch_fill_direct(nv_ctx *c, nvk::FillArgs &a, cudaStream_t st) {
   unsigned grid = (unsigned)std::max<long long>(1, std::min<long long>(want, (long long)per_sm * c->sm_count));
   Prof pf(c, st, 2);
   kern<<<grid, warps * 32, smem, st>>>(a);
-  return check_launch(c);
-}
-
-// CTA-per-frame writer: the widest configuration that fits in shared memory,
-// preferring 16 warps with the shading table resident.
-template <int CPL>
-int launch_fill_cta(nv_ctx *c, nvk::FillArgs &a, cudaStream_t st) {
-  constexpr int RW = 2;
-  const int segw = 32 * CPL;
-  const int S = a.W / segw;
-  const int bpp = (a.rgb ? 3 : 0) + (a.depth ? 4 : 0) + (a.sem ? 2 : 0);
-  auto up = [](size_t x) { return (x + 127) & ~(size_t)127; };
-  nvk::FillCtaLayout L;
-  L.stage_bytes = (int)up((size_t)RW * segw * bpp);
-  const size_t rows_b = up((size_t)a.H * sizeof(RowRec));
-  const size_t inv_b = up((size_t)((a.H + 1) / 2) * a.W * 2);
-  const size_t cols_b = up((size_t)2 * a.W * sizeof(ColRec));
-  static const int cfg_nw[6] = {16, 16, 12, 12, 8, 8};
-  static const bool cfg_tab[6] = {true, false, true, false, true, false};
-  int nw = 0;
-  bool tab = false;
-  size_t smem = 0;
-  for (int k = 0; k < 6; ++k) {
-    if (cfg_nw[k] % S) continue;
-    const size_t tot = rows_b + (cfg_tab[k] ? inv_b : 0) + cols_b + 128 +
-                       (size_t)cfg_nw[k] * 2 * L.stage_bytes;
-    if ((int)tot <= c->max_smem_optin) {
-      nw = cfg_nw[k];
-      tab = cfg_tab[k];
-      smem = tot;
-      break;
-    }
-  }
-  if (!nw) return fail(NV_ERR_ARG, "frame layout too large for the CTA fill writer");
-  L.rows = 0;
-  L.inv = (int)rows_b;
-  L.cols = L.inv + (tab ? (int)inv_b : 0);
-  L.bar = L.cols + (int)cols_b;
-  L.stages = L.bar + 128;
-  a.segs_per_row = S;
-  auto kern = tab ? nvk::k_fill_cta<CPL, RW, true> : nvk::k_fill_cta<CPL, RW, false>;
-  static int configured[2][3] = {{0, 0, 0}, {0, 0, 0}};
-  int &cfgd = configured[tab ? 1 : 0][CPL == 2 ? 0 : (CPL == 4 ? 1 : 2)];
-  if ((int)smem > cfgd) {
-    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    cfgd = (int)smem;
-  }
-  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(a.N, c->sm_count));
-  Prof pf(c, st, 2);
-  kern<<<grid, nw * 32, smem, st>>>(a, L);
   return check_launch(c);
 }
 
@@ -606,7 +579,10 @@ int launch_fill(nv_ctx *c, Camera &cam, int64_t N, uint8_t *rgb, float *depth, u
                 cudaStream_t st) {
   if (!rgb && !depth && !sem) return NV_OK;
   nvk::FillArgs a;
-  a.rec = cam.rec.as<ColRec>();
+  const RecOut ro = rec_out(cam, N);
+  a.ra = ro.a;
+  a.rb = ro.b;
+  a.cpl = ro.cpl;
   a.rows = cam.rows.as<RowRec>();
   a.invh = cam.invh.as<uint16_t>();
   a.N = (int)N; a.W = cam.W; a.H = cam.H;
@@ -623,9 +599,6 @@ int launch_fill(nv_ctx *c, Camera &cam, int64_t N, uint8_t *rgb, float *depth, u
   if (c->fill_mode == 3 && aligned && ws_ok && cam.W % 256 == 0) return launch_fill_ws<8>(c, a, st);
   if (c->fill_mode == 3 && aligned && ws_ok && cam.W == 128) return launch_fill_ws<4>(c, a, st);
   if (c->fill_mode == 3 && aligned && ws_ok && cam.W == 64) return launch_fill_ws<2>(c, a, st);
-  if (c->fill_mode == 2 && aligned && cam.W % 256 == 0) return launch_fill_cta<8>(c, a, st);
-  if (c->fill_mode == 2 && aligned && cam.W == 128) return launch_fill_cta<4>(c, a, st);
-  if (c->fill_mode == 2 && aligned && cam.W == 64) return launch_fill_cta<2>(c, a, st);
   if (aligned && cam.W % 256 == 0) return launch_fill_tma<8>(c, a, st);
   if (aligned && cam.W == 128) return launch_fill_tma<4>(c, a, st);
   if (aligned && cam.W == 64) return launch_fill_tma<2>(c, a, st);
@@ -660,7 +633,7 @@ int do_cast(nv_ctx *c, int cam, double *gps, double *compass, cudaStream_t st) {
     }
     Prof pf(c, st, 1);
     nvk::k_cast_binned<<<(unsigned)c->n_envs, 128, smem, st>>>(
-        c->env_view(), c->scene_view(), cam_view(k), k.focal, k.rec.as<ColRec>(), gps, compass);
+        c->env_view(), c->scene_view(), cam_view(k), k.focal, rec_out(k, c->n_envs), gps, compass);
     return check_launch(c);
   }
   // t_max = max_range: capping the walk is output-identical for rendered
@@ -669,7 +642,7 @@ int do_cast(nv_ctx *c, int cam, double *gps, double *compass, cudaStream_t st) {
   const long long total = c->n_envs * (long long)k.W;
   Prof pf(c, st, 1);
   nvk::k_column_cast<<<blocks_for(total, 128), 128, 0, st>>>(
-      c->env_view(), c->scene_view(), cam_view(k), k.rec.as<ColRec>(), k.max_range, gps,
+      c->env_view(), c->scene_view(), cam_view(k), rec_out(k, c->n_envs), k.max_range, gps,
       compass);
   return check_launch(c);
 }
@@ -973,8 +946,8 @@ int nv_set_cast_mode(nv_ctx *c, int mode) {
 
 int nv_set_fill_mode(nv_ctx *c, int mode) {
   if (!c) return fail(NV_ERR_ARG, "ctx is NULL");
-  if (mode < 0 || mode > 3)
-    return fail(NV_ERR_ARG, "fill mode must be 0 (direct), 1 (tma), 2 (cta) or 3 (ws)");
+  if (mode < 0 || mode > 3 || mode == 2)
+    return fail(NV_ERR_ARG, "fill mode must be 0 (direct), 1 (tma) or 3 (ws)");
   c->fill_mode = mode;
   return NV_OK;
 }
@@ -1098,7 +1071,7 @@ int nv_fill_frames(nv_ctx *c, int cam, int64_t n, const double *t_col, const int
   TRY(k.rec.alloc(sizeof(ColRec) * (size_t)n * k.W));
   long long total = n * (long long)k.W;
   nvk::k_cols_from_hits<<<blocks_for(total, 256), 256, 0, st>>>(
-      c->scene_view(), cam_view(k), total, t_col, i_col, dirx, diry, k.rec.as<ColRec>());
+      c->scene_view(), cam_view(k), total, t_col, i_col, dirx, diry, rec_out(k, n));
   TRY(check_launch(c));
   return launch_fill(c, k, n, rgb, depth, sem, st);
 }
