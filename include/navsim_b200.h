@@ -125,7 +125,9 @@ int nv_set_fused(nv_ctx *ctx, int on);
 /* Column cast: 0 (default) = per-column DDA over the grid (raycast_grid's
  * walk), 1 = binned: one CTA per env projects the frustum's segments to
  * column spans and tests (segment, column) pairs exactly (raycast_all's
- * lexicographic minimum, which the reference defines raycast_grid to equal). */
+ * lexicographic minimum, which the reference defines raycast_grid to equal),
+ * 2 = the DDA of mode 0 fused with the agent step in nv_step_render (one CTA
+ * per env: its first warp steps the agent, then all threads cast). */
 int nv_set_cast_mode(nv_ctx *ctx, int mode);
 /* Frame writer: 0 = 256-bit direct stores from registers,
  * 1 = per-warp shared-memory stages written out by TMA bulk copies,

@@ -29,6 +29,17 @@ struct __align__(16) CellEntry {
   double ex, ey;  // b - a (SegmentIndex.ex/ey, geometry.py:116-117)
 };                // the segment index (tie-break key) is items[q]
 
+// Per grid entry, for the swept-disc casts (disc_cast, _kernels.py:393-465):
+// the segment's endpoints and the per-segment quantities the reference
+// recomputes for every candidate -- seg_len = sqrt(ex^2 + ey^2) and the unit
+// tangent (ex / seg_len, ey / seg_len) -- precomputed on the host with the
+// same IEEE operations (no contraction), so the values are identical.
+struct __align__(16) DiscEntry {
+  double ax, ay, bx, by;
+  double tx, ty, len;
+  int32_t idx, pad;
+};
+
 struct SceneView {
   const double *ax, *ay, *bx, *by, *ex, *ey, *nx, *ny;
   const uint16_t *sem;
@@ -40,6 +51,8 @@ struct SceneView {
   const float *cellb;    // per cell: max |endpoint - X0c|_1 over its items
   const int4 *cells;     // per cell: {starts[c], starts[c+1], bits(bound), first chunk}
   const float4 *chunks;  // per run of NV_CHUNK entries: f32 box (x0, y0, x1, y1), cell-relative
+  const DiscEntry *dent; // per entry (same order as items): disc-cast record
+  const double *stx, *sty;  // per segment: unit tangent (ex, ey) / seg_len (0 if degenerate)
   double x0, y0;
   int gnx, gny;
   int64_t n;

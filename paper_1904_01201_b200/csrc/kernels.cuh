@@ -365,6 +365,55 @@ __device__ __forceinline__ double disc_seg_t(double px, double py, double ux, do
   return best;
 }
 
+// disc_seg_t with the segment's seg_len and unit tangent taken from its
+// DiscEntry (the identical values the reference recomputes per candidate).
+__device__ __forceinline__ double disc_seg_t_pre(double px, double py, double ux, double uy,
+                                                 double radius, double u2, const DiscEntry &d) {
+  double best = NV_INF;
+  const double seg_len = d.len;
+  if (seg_len <= 0.0) return best;
+  const double tx = d.tx, ty = d.ty;
+  const double nx = -ty, ny = tx;
+  const double relx = sub(px, d.ax), rely = sub(py, d.ay);
+  const double d0 = add(mul(relx, nx), mul(rely, ny));
+  const double vn = add(mul(ux, nx), mul(uy, ny));
+  if (fabs(d0) >= radius) {
+    const double side = d0 > 0.0 ? 1.0 : -1.0;
+    if (mul(vn, side) < 0.0) {
+      const double t = div(sub(mul(side, radius), d0), vn);
+      if (0.0 <= t && t <= 1.0) {
+        const double proj = add(mul(add(relx, mul(t, ux)), tx), mul(add(rely, mul(t, uy)), ty));
+        if (0.0 <= proj && proj <= seg_len) {
+          if (t < best) best = t;
+        }
+      }
+    }
+  } else {
+    const double proj = add(mul(relx, tx), mul(rely, ty));
+    if (0.0 <= proj && proj <= seg_len && mul(vn, d0) < 0.0) {
+      if (0.0 < best) best = 0.0;
+    }
+  }
+#pragma unroll
+  for (int e = 0; e < 2; ++e) {
+    const double cxp = e == 0 ? d.ax : d.bx;
+    const double cyp = e == 0 ? d.ay : d.by;
+    const double wx = sub(px, cxp), wy = sub(py, cyp);
+    const double b = add(mul(wx, ux), mul(wy, uy));
+    const double c = sub(add(mul(wx, wx), mul(wy, wy)), mul(radius, radius));
+    if (c < 0.0) {
+      if (b < 0.0 && 0.0 < best) best = 0.0;
+      continue;
+    }
+    if (u2 == 0.0) continue;
+    const double disc = sub(mul(b, b), mul(u2, c));
+    if (disc < 0.0) continue;
+    const double t = div(sub(-b, nvx::sqrt_rn(disc)), u2);
+    if (0.0 <= t && t <= 1.0 && t < best) best = t;
+  }
+  return best;
+}
+
 __device__ __forceinline__ void lex_min(double &t, int &i, double t2, int i2) {
   if (t2 < t || (t2 == t && i2 < i)) {
     t = t2;
@@ -423,32 +472,45 @@ __device__ void warp_cast_disc(const SceneView &sc, double px, double py, double
       if (lane >= o) incl += v;
     }
     const int total = __shfl_sync(0xffffffffu, incl, 31);
-    for (int base = 0; base < total; base += 32) {
-      const int g = min(base + lane, total - 1);
-      int o = 0;
+    // two candidates per lane per round; both records are loaded together
+    for (int base = 0; base < total; base += 64) {
+      int qq[2];
+      bool ok[2];
+      float bx0[2], bx1[2], by0[2], by1[2];
 #pragma unroll
-      for (int b = 16; b > 0; b >>= 1) {
-        const int v = __shfl_sync(0xffffffffu, incl, o + b - 1);
-        if (v <= g) o += b;
+      for (int h = 0; h < 2; ++h) {
+        const int g = min(base + h * 32 + lane, total - 1);
+        int o = 0;
+#pragma unroll
+        for (int b = 16; b > 0; b >>= 1) {
+          const int v = __shfl_sync(0xffffffffu, incl, o + b - 1);
+          if (v <= g) o += b;
+        }
+        const int oq0 = __shfl_sync(0xffffffffu, q0, o);
+        const int oincl = __shfl_sync(0xffffffffu, incl, o);
+        const int ocnt = __shfl_sync(0xffffffffu, cnt, o);
+        const int ocx = __shfl_sync(0xffffffffu, cxk, o);
+        const int ocy = __shfl_sync(0xffffffffu, cyk, o);
+        qq[h] = oq0 + (g - (oincl - ocnt));
+        ok[h] = base + h * 32 + lane < total;
+        const double X0 = add(sc.x0, (double)ocx), Y0 = add(sc.y0, (double)ocy);
+        bx0[h] = (float)sub(lox, X0) - grow;
+        bx1[h] = (float)sub(hix, X0) + grow;
+        by0[h] = (float)sub(loy, Y0) - grow;
+        by1[h] = (float)sub(hiy, Y0) + grow;
       }
-      const int oq0 = __shfl_sync(0xffffffffu, q0, o);
-      const int oincl = __shfl_sync(0xffffffffu, incl, o);
-      const int ocnt = __shfl_sync(0xffffffffu, cnt, o);
-      const int ocx = __shfl_sync(0xffffffffu, cxk, o);
-      const int ocy = __shfl_sync(0xffffffffu, cyk, o);
-      if (base + lane >= total) continue;
-      const int q = oq0 + (g - (oincl - ocnt));
-      const double X0 = add(sc.x0, (double)ocx), Y0 = add(sc.y0, (double)ocy);
-      const float sx0 = (float)sub(lox, X0) - grow, sx1 = (float)sub(hix, X0) + grow;
-      const float sy0 = (float)sub(loy, Y0) - grow, sy1 = (float)sub(hiy, Y0) + grow;
-      const float4 f = __ldg(sc.entf + q);
-      if (fmaxf(f.x, f.z) < sx0 || fminf(f.x, f.z) > sx1 || fmaxf(f.y, f.w) < sy0 ||
-          fminf(f.y, f.w) > sy1)
-        continue;
-      int i = __ldg(sc.items + q);
-      double t = disc_seg_t(px, py, ux, uy, radius, u2, __ldg(sc.ax + i), __ldg(sc.ay + i),
-                            __ldg(sc.bx + i), __ldg(sc.by + i));
-      lex_min(bt, bi, t, i);
+      float4 f[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) f[h] = __ldg(sc.entf + qq[h]);
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        if (!ok[h] || fmaxf(f[h].x, f[h].z) < bx0[h] || fminf(f[h].x, f[h].z) > bx1[h] ||
+            fmaxf(f[h].y, f[h].w) < by0[h] || fminf(f[h].y, f[h].w) > by1[h])
+          continue;
+        const DiscEntry d = sc.dent[qq[h]];
+        const double t = disc_seg_t_pre(px, py, ux, uy, radius, u2, d);
+        lex_min(bt, bi, t, d.idx);
+      }
     }
   } else {
     for (int cy = cy0; cy <= cy1; ++cy)
@@ -464,10 +526,9 @@ __device__ void warp_cast_disc(const SceneView &sc, double px, double py, double
           if (fmaxf(f.x, f.z) < sx0 || fminf(f.x, f.z) > sx1 || fmaxf(f.y, f.w) < sy0 ||
               fminf(f.y, f.w) > sy1)
             continue;
-          int i = __ldg(sc.items + q);
-          double t = disc_seg_t(px, py, ux, uy, radius, u2, __ldg(sc.ax + i), __ldg(sc.ay + i),
-                                __ldg(sc.bx + i), __ldg(sc.by + i));
-          lex_min(bt, bi, t, i);
+          const DiscEntry d = sc.dent[q];
+          const double t = disc_seg_t_pre(px, py, ux, uy, radius, u2, d);
+          lex_min(bt, bi, t, d.idx);
         }
       }
   }
@@ -479,13 +540,11 @@ __device__ void warp_cast_disc(const SceneView &sc, double px, double py, double
     tan_y = 0.0;
     return;
   }
-  double exi = sub(__ldg(sc.bx + bi), __ldg(sc.ax + bi));
-  double eyi = sub(__ldg(sc.by + bi), __ldg(sc.ay + bi));
-  double seg_len = nvx::sqrt_rn(add(mul(exi, exi), mul(eyi, eyi)));
+  // the winner's unit tangent (ex / seg_len, ey / seg_len), precomputed
   t_out = bt;
   i_out = bi;
-  tan_x = div(exi, seg_len);
-  tan_y = div(eyi, seg_len);
+  tan_x = __ldg(sc.stx + bi);
+  tan_y = __ldg(sc.sty + bi);
 }
 
 // min_seg_distance (_kernels.py:468-493), one segment.
@@ -791,6 +850,26 @@ __global__ void __launch_bounds__(128) k_column_cast(EnvView ev, SceneView sc, C
   const int e = (int)(g / cam.W);
   const int j = (int)(g - (long long)e * cam.W);
   cast_column<false>(ev, sc, cam, e, j, ro, t_max, gps, compass);
+}
+
+// Simulator.step + the column casts of one env per CTA: warp 0 runs the
+// agent step (the same warp_agent_step as k_agent_step), then every thread
+// casts columns of the env at its new pose.  CTAs progress independently, so
+// the agent step's long FP64 latency chains of some envs overlap the casts of
+// others (no grid-wide step -> cast barrier).
+__global__ void __launch_bounds__(256) k_step_cast(EnvView ev, SceneView sc, AgentCfg cfg,
+                                                   const int8_t *__restrict__ actions,
+                                                   uint8_t *collided_out, double *disp_out,
+                                                   int32_t *status_out, CamView cam, RecOut ro,
+                                                   double t_max, double *gps, double *compass) {
+  const int e = blockIdx.x;
+  if (threadIdx.x < 32) {
+    warp_agent_step(ev, sc, cfg, e, actions[e], collided_out, disp_out, status_out);
+    __threadfence();
+  }
+  __syncthreads();
+  for (int j = threadIdx.x; j < cam.W; j += blockDim.x)
+    cast_column<true>(ev, sc, cam, e, j, ro, t_max, gps, compass);
 }
 
 // ---------------------------------------------------- binned column cast

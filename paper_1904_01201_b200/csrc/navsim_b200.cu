@@ -114,6 +114,7 @@ struct nv_ctx {
   int gnx = 1, gny = 1;
   int64_t nitems = 0;
   DevBuf ax, ay, bx, by, ex, ey, nx, ny, sem, alb, starts, ent, items, entf, cellb, cells, chunks;
+  DevBuf dent, stx, sty;
   // agent
   double radius = 0.1, step = 0.25, turn_rad = 0.17453292519943295, sensor_h = 1.5;
   // envs
@@ -146,6 +147,7 @@ struct nv_ctx {
     v.starts = starts.as<int32_t>(); v.ent = ent.as<CellEntry>(); v.items = items.as<int32_t>();
     v.entf = entf.as<float4>(); v.cellb = cellb.as<float>(); v.cells = cells.as<int4>();
     v.chunks = chunks.as<float4>();
+    v.dent = dent.as<DiscEntry>(); v.stx = stx.as<double>(); v.sty = sty.as<double>();
     v.x0 = gx0; v.y0 = gy0; v.gnx = gnx; v.gny = gny; v.n = n;
     return v;
   }
@@ -648,7 +650,8 @@ int do_cast(nv_ctx *c, int cam, double *gps, double *compass, cudaStream_t st) {
 }
 
 int nv_set_cast_mode_(nv_ctx *c, int mode) {
-  if (mode < 0 || mode > 1) return fail(NV_ERR_ARG, "cast mode must be 0 (dda) or 1 (binned)");
+  if (mode < 0 || mode > 2)
+    return fail(NV_ERR_ARG, "cast mode must be 0 (dda), 1 (binned) or 2 (dda fused with the step)");
   c->cast_mode = mode;
   return NV_OK;
 }
@@ -778,6 +781,27 @@ int nv_scene_upload(nv_ctx *c, const double *segs, const uint16_t *sem, const do
     cells[k] = make_int4(q0, q1, bi, ch0);
   }
   if (chunks.empty()) chunks.push_back(make_float4(0.f, 0.f, 0.f, 0.f));
+  // disc-cast records: disc_cast's per-candidate seg_len / tangent
+  // (_kernels.py:407-413), host IEEE ops without contraction = device ops
+  std::vector<double> stx(n), sty(n), slen(n);
+  for (int64_t i = 0; i < n; ++i) {
+    const double exi = bx[i] - ax[i], eyi = by[i] - ay[i];
+    slen[i] = std::sqrt(exi * exi + eyi * eyi);
+    stx[i] = slen[i] > 0.0 ? exi / slen[i] : 0.0;
+    sty[i] = slen[i] > 0.0 ? eyi / slen[i] : 0.0;
+  }
+  std::vector<DiscEntry> dent(items.size());
+  for (size_t q = 0; q < items.size(); ++q) {
+    const int32_t i = items[q];
+    DiscEntry d;
+    d.ax = ax[i]; d.ay = ay[i]; d.bx = bx[i]; d.by = by[i];
+    d.tx = stx[i]; d.ty = sty[i]; d.len = slen[i];
+    d.idx = i; d.pad = 0;
+    dent[q] = d;
+  }
+  if (dent.empty()) dent.push_back(DiscEntry{});
+  if (stx.empty()) { stx.push_back(0.0); sty.push_back(0.0); }
+  TRY(upload(c->dent, dent)); TRY(upload(c->stx, stx)); TRY(upload(c->sty, sty));
   TRY(upload(c->cells, cells));
   TRY(upload(c->chunks, chunks));
   c->n = n;
@@ -933,6 +957,18 @@ int nv_step_render(nv_ctx *c, const int8_t *actions, int cam, uint8_t *rgb, floa
     if (k.W == 64)
       return launch_mega<2>(c, k, actions, rgb, depth, sem, gps, compass, collided, displacement,
                             status, st);
+  }
+  if (c->cast_mode == 2) {  // agent step fused with the casts, one CTA per env
+    nvk::AgentCfg cfg{c->radius, c->step, c->turn_rad};
+    const int threads = std::min(256, (k.W + 31) / 32 * 32);
+    {
+      Prof pf(c, st, 1);
+      nvk::k_step_cast<<<(unsigned)c->n_envs, threads, 0, st>>>(
+          c->env_view(), c->scene_view(), cfg, actions, collided, displacement, status,
+          cam_view(k), rec_out(k, c->n_envs), k.max_range, gps, compass);
+    }
+    TRY(check_launch(c));
+    return launch_fill(c, k, c->n_envs, rgb, depth, sem, st);
   }
   TRY(do_step(c, actions, collided, displacement, status, st));
   TRY(do_cast(c, cam, gps, compass, st));

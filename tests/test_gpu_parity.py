@@ -399,3 +399,37 @@ def test_cast_modes_agree(nb, cfg, W, H, n):
         assert torch.equal(outs[0]["depth"], outs[1]["depth"])
         assert torch.equal(outs[0]["rgb"], outs[1]["rgb"])
         assert torch.equal(outs[0]["gps"], outs[1]["gps"])
+
+
+@pytest.mark.parametrize("cfg,W,H,n", [("C1", 256, 64, 24), ("C2", 128, 64, 32), ("C1", 40, 33, 16)])
+def test_step_cast_fused_agrees(nb, cfg, W, H, n):
+    """Cast mode 2 (agent step fused with the column casts, one CTA per env)
+    gives the same poses, step results and frames as the separate step and
+    cast launches over a 10-step random-action episode."""
+    from paper_1904_01201_b200 import _native as nat
+    from paper_1904_01201_b200 import synth
+    sc = synth.config_scene(cfg)
+    suite = (nb.SensorConfig("rgb", W, H), nb.SensorConfig("depth", W, H),
+             nb.SensorConfig("semantic", W, H), nb.SensorConfig("gps_compass"))
+    sims = []
+    for mode in (0, 2):
+        sim = nb.BatchSimulator(sc.segments, sc.semantic_ids, sc.albedo, n, sensor_configs=suite,
+                                floor_color=sc.floor_color, ceiling_color=sc.ceiling_color)
+        nat.check(sim.ctx.lib.nv_set_cast_mode(sim.ctx.handle, mode))
+        poses = synth.sample_poses(sc, n, seed=5)
+        sim.reset(poses[:, :2], poses[:, 2])
+        sims.append(sim)
+    acts = torch.as_tensor(synth.random_actions(n, 10, seed=9), device="cuda:0")
+    for s in range(acts.shape[0]):
+        outs = []
+        for sim in sims:
+            sim.step(acts[s])
+            torch.cuda.synchronize()
+            o = {k: v.clone() for k, v in sim.observations().items()}
+            o["state"] = [t.clone() for t in sim.state()]
+            outs.append(o)
+        for k in ("rgb", "depth", "gps", "compass"):
+            assert torch.equal(outs[0][k], outs[1][k]), (s, k)
+        assert torch.equal(outs[0]["semantic"].view(torch.int16), outs[1]["semantic"].view(torch.int16))
+        for a, b in zip(outs[0]["state"], outs[1]["state"]):
+            assert torch.equal(a, b)
