@@ -668,20 +668,23 @@ __device__ __forceinline__ void warp_agent_step(const EnvView &ev, const SceneVi
   const int lane = threadIdx.x & 31;
   int status = 0, collided = 0;
   double moved = 0.0;
-  if (!ev.reset[e]) {
+  // all of the env's state is loaded up front (one memory round trip)
+  const uint8_t was_reset = ev.reset[e];
+  double x = ev.x[e], y = ev.y[e], h0 = ev.h[e], ch = ev.ch[e], sh = ev.sh[e];
+  const double path = ev.path[e];
+  if (!was_reset) {
     status = 2;  // NV_ENV_NOT_RESET
   } else if (a == 0) {
-    double x = ev.x[e], y = ev.y[e];
-    warp_forward(sc, cfg, x, y, ev.ch[e], ev.sh[e], moved, collided);
+    warp_forward(sc, cfg, x, y, ch, sh, moved, collided);
     if (lane == 0) {
       ev.x[e] = x;
       ev.y[e] = y;
-      ev.path[e] = add(ev.path[e], moved);
+      ev.path[e] = add(path, moved);
       ev.coll[e] += collided;
     }
   } else if (a == 1 || a == 2) {
     // apply_turn (sim.py:83-87): wrap(h + sign * radians(turn)); +-x is exact
-    double h = nvx::wrap_angle(add(ev.h[e], a == 1 ? cfg.turn_rad : -cfg.turn_rad));
+    double h = nvx::wrap_angle(add(h0, a == 1 ? cfg.turn_rad : -cfg.turn_rad));
     if (lane == 0) {
       double s, c;
       nvx::sincos_cr(h, &s, &c);
