@@ -214,6 +214,65 @@ int64_t nv_launch_count(nv_ctx *ctx);
 int nv_profile(nv_ctx *ctx, int enable);
 int nv_profile_read(nv_ctx *ctx, double *ms4, int64_t *counts4);
 
+/* ---- navigation grid + geodesic distance fields ------ */
+
+#define NV_ENV_DONE 4        /* task episode finished: env frozen (task.py:196-197) */
+
+/* Occupancy grid -- replaces nav.rasterize_navigable (nav.py:65-78) /
+ * geometry.navigable_mask (geometry.py:209-250) over HOST bounds
+ * (xmin, ymin, xmax, ymax), NULL = the uploaded scene's Scene.bounds
+ * (scene.py:69-76).  Builds on the device the per-cell wall clearance
+ * (point_segment_distances, geometry.py:76-97) and the navigable mask of
+ * the uploaded segments; returns the grid size and the world position of
+ * cell (0, 0)'s center.  Synchronous. */
+int nv_nav_build(nv_ctx *ctx, const double *bounds, double resolution, double agent_radius,
+                 int64_t *nx, int64_t *ny, double *origin2);
+/* Copies the mask (u8 ny x nx) and clearance (f64 ny x nx) to HOST buffers. */
+int nv_nav_copy(nv_ctx *ctx, uint8_t *mask, double *clearance);
+/* nav._snap_to_navigable (nav.py:103-119) for m HOST points (m x 2); HOST
+ * cells out (m x 2 i32: i, j, or -1, -1 when nothing is within radius). */
+int nv_nav_snap(nv_ctx *ctx, const double *pts, int64_t m, double radius, int32_t *cells);
+/* Distance fields -- nav.distance_field / _kernels.dijkstra_grid
+ * (nav.py:122-132, _kernels.py:210-282) for k goal cells (HOST k x 2 i32),
+ * into DEVICE fields f64[k, ny, nx] (+inf unreachable).  Bit-identical to the
+ * reference's Dijkstra (its output is the least fixed point of the
+ * relaxation, which the device reaches by tiled Bellman-Ford).  Synchronous
+ * on `stream`. */
+int nv_nav_fields(nv_ctx *ctx, const int32_t *goal_cells, int64_t k, double *fields,
+                  void *stream);
+/* nav.geodesic_distance (nav.py:135-166) at m DEVICE points (m x 2) in the
+ * fields fid[q] (DEVICE i32); DEVICE out f64[m], NaN = outside the grid
+ * (the reference's NavError). */
+int nv_nav_geodesic(nv_ctx *ctx, const double *fields, const int32_t *fid, const double *pts,
+                    int64_t m, double *out, void *stream);
+
+/* ---- batched PointGoal task (task.py:123-243) ---------- */
+
+/* MAX_EPISODE_STEPS, SUCCESS_RADIUS (task.py:24-25), RewardParams (task.py:52-55). */
+int nv_task_config(nv_ctx *ctx, int max_steps, double success_radius, double success_reward,
+                   double step_penalty);
+/* Environment.reset's task part for the masked envs (HOST arrays of n_envs;
+ * mask NULL = all): goal xy (n x 2), episode gdsp, field index into the
+ * DEVICE fields (f64[n_fields, ny, nx], caller-owned, must outlive the
+ * episodes).  Call after nv_set_poses.  Writes the initial geodesic distance
+ * d0 (HOST f64[n], may be NULL).  Synchronous. */
+int nv_task_reset(nv_ctx *ctx, const double *goal, const double *gdsp, const int32_t *fid,
+                  const double *fields, int64_t n_fields, const uint8_t *mask, double *d0);
+/* Environment.step's task arithmetic after nv_step / nv_step_render with the
+ * same actions (DEVICE i8[n]) and that call's step status (DEVICE i32[n]):
+ * Environment._distance_to_goal (1-ray line of sight, else the field),
+ * success, SPL, reward, termination.  DEVICE outputs (each may be NULL):
+ * reward f64[n], dist f64[n], done u8[n], outcome: 40-byte EpisodeOutcome
+ * records written when an env terminates {u8 success, u8 terminated_by
+ * (1 stop, 2 step_limit), u8[2], i32 steps, i32 collisions, i32, f64
+ * path_taken, f64 shortest_path, f64 spl}.  Finished envs are frozen: later
+ * steps report NV_ENV_DONE until the next nv_task_reset. */
+int nv_task_step(nv_ctx *ctx, const int8_t *actions, const int32_t *status, double *reward,
+                 double *dist, uint8_t *done, void *outcome, void *stream);
+/* Task state (any pointer may be NULL; host or device memory): steps i32[n],
+ * done u8[n], last distance f64[n]. */
+int nv_task_state(nv_ctx *ctx, int32_t *steps, uint8_t *done, double *d_last, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -18,7 +18,7 @@ NV_ERR_ARG = -1
 NV_ERR_CUDA = -2
 NV_ERR_STATE = -3
 NV_ERR_OOM = -4
-NV_ENV_OK, NV_ENV_TOO_CLOSE, NV_ENV_NOT_RESET, NV_ENV_BAD_ACTION = 0, 1, 2, 3
+NV_ENV_OK, NV_ENV_TOO_CLOSE, NV_ENV_NOT_RESET, NV_ENV_BAD_ACTION, NV_ENV_DONE = 0, 1, 2, 3, 4
 NV_CH_RGB, NV_CH_DEPTH, NV_CH_SEM = 1, 2, 4
 
 # every symbol include/navsim_b200.h declares: (name, restype, argtypes)
@@ -58,6 +58,15 @@ SIGNATURES = {
     "nv_launch_count": (_I64, [_P]),
     "nv_profile": (_I, [_P, _I]),
     "nv_profile_read": (_I, [_P, _P, _P]),
+    "nv_nav_build": (_I, [_P, _P, _D, _D, _P, _P, _P]),
+    "nv_nav_copy": (_I, [_P, _P, _P]),
+    "nv_nav_snap": (_I, [_P, _P, _I64, _D, _P]),
+    "nv_nav_fields": (_I, [_P, _P, _I64, _P, _P]),
+    "nv_nav_geodesic": (_I, [_P, _P, _P, _P, _I64, _P, _P]),
+    "nv_task_config": (_I, [_P, _I, _D, _D, _D]),
+    "nv_task_reset": (_I, [_P, _P, _P, _P, _P, _I64, _P, _P]),
+    "nv_task_step": (_I, [_P, _P, _P, _P, _P, _P, _P, _P]),
+    "nv_task_state": (_I, [_P, _P, _P, _P, _P]),
 }
 
 

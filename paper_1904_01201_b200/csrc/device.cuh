@@ -65,6 +65,7 @@ struct EnvView {
   double *ox, *oy, *oh;        // episode frame (sensors.py:155-172)
   double *fc, *fs;             // cos(-oh), sin(-oh)
   uint8_t *reset;
+  const uint8_t *frozen;       // task layer: finished episodes (nullptr = none)
   int n;
 };
 

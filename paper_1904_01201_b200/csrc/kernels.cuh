@@ -674,6 +674,8 @@ __device__ __forceinline__ void warp_agent_step(const EnvView &ev, const SceneVi
   const double path = ev.path[e];
   if (!was_reset) {
     status = 2;  // NV_ENV_NOT_RESET
+  } else if (ev.frozen && ev.frozen[e]) {
+    status = 4;  // NV_ENV_DONE: the task episode is over (task.py:196-197)
   } else if (a == 0) {
     warp_forward(sc, cfg, x, y, ch, sh, moved, collided);
     if (lane == 0) {

@@ -20,6 +20,7 @@
 #include "device.cuh"
 #include "exact_math.cuh"
 #include "kernels.cuh"
+#include "nav.cuh"
 
 using namespace nvd;
 
@@ -118,6 +119,18 @@ struct nv_ctx {
   // agent
   double radius = 0.1, step = 0.25, turn_rad = 0.17453292519943295, sensor_h = 1.5;
   // envs
+  // navigation grid (nv_nav_build) and PointGoal task state (nv_task_*)
+  bool has_nav = false;
+  int nav_nx = 0, nav_ny = 0;
+  double nav_ox = 0, nav_oy = 0, nav_res = 0, nav_radius = 0;
+  DevBuf nav_mask, nav_dist, nav_tmp0, nav_tmp1, nav_flag;
+  double sbounds[4] = {0, 0, 0, 0};  // Scene.bounds of the uploaded segments
+  bool task_on = false;
+  int t_max_steps = 500;
+  double t_success_radius = 0.2, t_success_reward = 10.0, t_step_penalty = -0.01;
+  DevBuf t_goal, t_gdsp, t_fid, t_dlast, t_steps, t_done;
+  const double *t_fields = nullptr;
+  int64_t t_nfields = 0;
   int64_t n_envs = 0;
   DevBuf x, y, h, path, coll, ch, sh, ox, oy, oh, fc, fs, reset;
   Camera cams[8];
@@ -157,6 +170,7 @@ struct nv_ctx {
     v.coll = coll.as<int64_t>(); v.ch = ch.as<double>(); v.sh = sh.as<double>();
     v.ox = ox.as<double>(); v.oy = oy.as<double>(); v.oh = oh.as<double>();
     v.fc = fc.as<double>(); v.fs = fs.as<double>(); v.reset = reset.as<uint8_t>();
+    v.frozen = task_on ? t_done.as<uint8_t>() : nullptr;
     v.n = (int)n_envs;
     return v;
   }
@@ -704,6 +718,17 @@ int nv_scene_upload(nv_ctx *c, const double *segs, const uint16_t *sem, const do
   if (n >= (1LL << 31)) return fail(NV_ERR_ARG, "too many segments (%lld)", (long long)n);
   CK(cudaSetDevice(c->device));
   HostGrid g = build_grid(segs, n);
+  if (n > 0) {  // Scene.bounds (scene.py:69-76)
+    double b0 = INFINITY, b1 = INFINITY, b2 = -INFINITY, b3 = -INFINITY;
+    for (int64_t i = 0; i < n; ++i) {
+      b0 = std::min(b0, std::min(segs[4 * i], segs[4 * i + 2]));
+      b1 = std::min(b1, std::min(segs[4 * i + 1], segs[4 * i + 3]));
+      b2 = std::max(b2, std::max(segs[4 * i], segs[4 * i + 2]));
+      b3 = std::max(b3, std::max(segs[4 * i + 1], segs[4 * i + 3]));
+    }
+    c->sbounds[0] = b0; c->sbounds[1] = b1; c->sbounds[2] = b2; c->sbounds[3] = b3;
+  }
+  c->has_nav = false;
   if (g.nx * g.ny >= (1LL << 31) || (int64_t)g.items.size() >= (1LL << 31))
     return fail(NV_ERR_ARG, "scene grid too large");
   std::vector<double> ax(n), ay(n), bx(n), by(n), ex(n), ey(n), nx(n), ny(n);
@@ -1168,3 +1193,5 @@ int nv_profile_read(nv_ctx *c, double *ms, int64_t *counts) {
 }
 
 }  // extern "C"
+
+#include "nav_task_abi.inc"

@@ -1,0 +1,185 @@
+"""Parity of the CUDA navigation / task row (nv_nav_* / nv_task_*, SURVEY §8f
+rows 1-2) with the reference, through the C ABI:
+
+* occupancy masks, wall clearances, goal snapping, distance fields and
+  geodesic queries bit-exact against fixtures produced by the unmodified
+  reference (tests/golden/make_golden_task.py);
+* whole PointGoal episodes (per-step distance, reward, done flag, collision,
+  displacement and pose, final EpisodeOutcome) bit-exact, all episodes of a
+  scene stepped together as one batch;
+* larger grids (the C2 apartment) against the live oracle
+  (oracle/navsim_nav_oracle.c, pinned to the same fixtures).
+"""
+import glob
+import hashlib
+import math
+import os
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+FILES = sorted(glob.glob(os.path.join(HERE, "golden", "golden_task_*.npz")))
+
+
+def sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+@pytest.fixture(scope="module")
+def nb():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1904_01201_b200 as nb
+    from paper_1904_01201_b200 import _native
+    _native.load()
+    return nb
+
+
+@pytest.fixture(scope="module", params=FILES, ids=[os.path.basename(f)[12:-4] for f in FILES])
+def gold(request):
+    return dict(np.load(request.param))
+
+
+def grid_for(nb, gold, radius):
+    from paper_1904_01201_b200 import nav
+    return nav.rasterize_navigable(gold["segments"], tuple(gold["bounds"]), 0.05, radius)
+
+
+def test_grid_exact(nb, gold):
+    for key in [k[:-7] for k in gold if k.endswith("_origin")]:
+        r = int(key[1:]) / 1000.0
+        g = grid_for(nb, gold, r)
+        assert np.array_equal(g.origin, gold[f"{key}_origin"])
+        assert np.array_equal(g.navigable.astype(np.uint8), gold[f"{key}_navigable"]), key
+        assert np.array_equal(g.clearance.ravel()[gold[f"{key}_clearance_idx"]],
+                              gold[f"{key}_clearance_val"])
+        assert sha(g.clearance) == str(gold[f"{key}_clearance_sha"])
+
+
+def test_snap_fields_geodesic_exact(nb, gold):
+    from paper_1904_01201_b200 import _native as nat
+    from paper_1904_01201_b200 import nav
+    g = grid_for(nb, gold, 0.1)
+    cells = g.snap(gold["snap_pts"])
+    assert np.array_equal(cells, gold["snap_cells"].astype(np.int32))
+    fields, fc = nav.distance_fields(g, gold["field_goal"])
+    assert np.array_equal(fc, gold["field_cell"].astype(np.int32))
+    host = fields.cpu().numpy()
+    for k in range(len(gold["field_goal"])):
+        assert np.array_equal(host[k].ravel()[gold["field_idx"][k]], gold["field_val"][k])
+        assert sha(host[k]) == str(gold["field_sha"][k])
+    # geodesic queries, all fields at once through nv_nav_geodesic
+    pts = torch.as_tensor(gold["geo_pts"].reshape(-1, 2), device="cuda:0")
+    fid = torch.as_tensor(np.repeat(np.arange(len(gold["field_goal"]), dtype=np.int32),
+                                    gold["geo_pts"].shape[1]), device="cuda:0")
+    out = torch.empty(pts.shape[0], dtype=torch.float64, device="cuda:0")
+    c = g.ctx
+    nat.check(c.lib.nv_nav_geodesic(c.handle, nat.ptr(fields), nat.ptr(fid), nat.ptr(pts),
+                                     pts.shape[0], nat.ptr(out), nat.stream_handle("cuda:0")))
+    got = out.cpu().numpy()
+    want = gold["geo_val"].reshape(-1)
+    both_nan = np.isnan(got) & np.isnan(want)
+    assert np.array_equal(got[~both_nan], want[~both_nan])
+
+
+def test_episodes_batched_exact(nb, gold):
+    if "n_episodes" not in gold:
+        pytest.skip("no episodes in this fixture")
+    from paper_1904_01201_b200 import task
+    from paper_1904_01201_b200.sensors import SensorConfig
+    n = int(gold["n_episodes"])
+    segs = gold["segments"]
+    ns = len(segs)
+    env = task.BatchEnvironment((segs, np.arange(1, ns + 1, dtype=np.uint16), np.full((ns, 3), 0.5)),
+                                n, sensor_configs=(SensorConfig("depth", width=64, height=16),))
+    eps = []
+    for k in range(n):
+        p = f"ep{k}_"
+        sr, goal = gold[p + "start_raw"], gold[p + "goal"]
+        gd = float(gold[p + "gdsp"])
+        eu = math.hypot(goal[0] - sr[0], goal[1] - sr[1])
+        eps.append(task.Episode(f"e{k}", "x", (float(sr[0]), float(sr[1])), float(sr[2]),
+                                (float(goal[0]), float(goal[1])), gd, eu, gd / eu))
+    env.reset(eps)
+    assert np.array_equal(env.d0, np.array([float(gold[f"ep{k}_d0"]) for k in range(n)]))
+    xy, h, _, _ = env.sim.state()
+    for k in range(n):
+        st = gold[f"ep{k}_start"]
+        assert xy[k, 0].item() == st[0] and xy[k, 1].item() == st[1] and h[k].item() == st[2]
+    T = max(len(gold[f"ep{k}_actions"]) for k in range(n))
+    acts = np.zeros((T, n), dtype=np.int8)
+    for k in range(n):
+        a = gold[f"ep{k}_actions"]
+        acts[: len(a), k] = a
+    for t in range(T):
+        _, done, info = env.step(torch.as_tensor(acts[t], device="cuda:0"))
+        torch.cuda.synchronize()
+        xy, h, _, _ = env.sim.state()
+        d, r = info["d"].cpu().numpy(), info["reward"].cpu().numpy()
+        dn, co = done.cpu().numpy(), info["collided"].cpu().numpy()
+        mv, stt = info["displacement"].cpu().numpy(), info["status"].cpu().numpy()
+        xy, h = xy.cpu().numpy(), h.cpu().numpy()
+        for k in range(n):
+            rows = gold[f"ep{k}_rows"]
+            if t < len(rows):
+                row = rows[t]
+                assert (d[k], r[k], float(dn[k]), float(co[k]), mv[k]) == tuple(row[:5]), (k, t)
+                assert (xy[k, 0], xy[k, 1], h[k]) == tuple(row[5:8]), (k, t)
+            else:
+                assert stt[k] == 4 and dn[k] == 1  # NV_ENV_DONE: frozen
+    outs = env.outcomes()
+    for k in range(n):
+        o = gold[f"ep{k}_outcome"]
+        got = outs[k]
+        assert got is not None
+        assert (float(got.success), got.shortest_path, got.path_taken, got.spl, float(got.steps),
+                float(got.collisions), 1.0 if got.terminated_by == "stop" else 2.0) == tuple(o)
+
+
+def test_single_env_facade_matches_batch(nb):
+    """task.Environment (reference API over a one-env batch) on the square scene."""
+    from paper_1904_01201_b200 import scene as sm
+    from paper_1904_01201_b200 import task
+    from paper_1904_01201_b200.sim import Action
+    g = dict(np.load(os.path.join(HERE, "golden", "golden_task_square.npz")))
+    walls = [sm.WallSegment(a=(s[0], s[1]), b=(s[2], s[3]), semantic_id=k + 1,
+                            albedo=(0.5, 0.5, 0.5)) for k, s in enumerate(g["segments"])]
+    scene = sm.Scene(id="square-10", walls=walls, floor_color=(0.3, 0.3, 0.3),
+                     ceiling_color=(0.9, 0.9, 0.9))
+    env = task.Environment(scene)
+    sr, goal, gd = g["ep0_start_raw"], g["ep0_goal"], float(g["ep0_gdsp"])
+    eu = math.hypot(goal[0] - sr[0], goal[1] - sr[1])
+    ep = task.Episode("e0", "square-10", (sr[0], sr[1]), sr[2], (goal[0], goal[1]), gd, eu, gd / eu)
+    codes = [Action.MOVE_FORWARD, Action.TURN_LEFT, Action.TURN_RIGHT, Action.STOP]
+    out = task.run_episode(env, ep, [codes[int(a)] for a in g["ep0_actions"]])
+    o = g["ep0_outcome"]
+    assert (float(out.success), out.path_taken, out.spl, float(out.steps)) == (o[0], o[2], o[3], o[4])
+    with pytest.raises(task.TaskError):
+        env.step(Action.STOP)
+    bad = task.Episode("e1", "other", (sr[0], sr[1]), sr[2], (goal[0], goal[1]), gd, eu, gd / eu)
+    with pytest.raises(task.TaskError):
+        env.reset(bad)
+
+
+def test_apartment_fields_vs_oracle(nb):
+    """C2 apartment (10k segments): device grid + fields bit-exact vs the oracle."""
+    from oracle import nav_oracle as no
+    from paper_1904_01201_b200 import nav, synth
+    sc = synth.config_scene("C2")
+    bnds = no.bounds(sc.segments)
+    g = nav.rasterize_navigable(sc.segments, bnds)
+    og = no.Grid(sc.segments, bnds)
+    assert np.array_equal(g.navigable.astype(np.uint8), og.navigable)
+    assert np.array_equal(g.clearance, og.clearance)
+    rng = np.random.default_rng(3)
+    cells = np.argwhere(og.navigable)
+    goals = [og.center_of(*cells[int(rng.integers(len(cells)))]) for _ in range(3)]
+    fields, fc = nav.distance_fields(g, goals)
+    host = fields.cpu().numpy()
+    for k, goal in enumerate(goals):
+        assert tuple(fc[k]) == og.snap(goal)
+        assert np.array_equal(host[k], og.field(tuple(fc[k])))
