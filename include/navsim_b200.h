@@ -273,6 +273,19 @@ int nv_task_step(nv_ctx *ctx, const int8_t *actions, const int32_t *status, doub
  * done u8[n], last distance f64[n]. */
 int nv_task_state(nv_ctx *ctx, int32_t *steps, uint8_t *done, double *d_last, void *stream);
 
+/* ---- inverse-depth noise ------------------------------ */
+
+/* sensors.apply_inverse_depth_noise (sensors.py:183-205) applied to every
+ * depth frame the context renders from now on: z' = max_range / (max_range /
+ * d + eps), eps ~ N(0, sigma), clamped to [0.05, max_range], saturated pixels
+ * untouched; sigma = 0 turns it off (sigma < 0: NV_ERR_ARG, the reference's
+ * SensorError).  eps comes from a counter-based generator keyed by (seed,
+ * frame counter -- reset here --, env_offset + env, row, pixel pair): the
+ * warp-specialised writer fuses it into the frame fill, the other writers run
+ * it as a pass; every path gives the same frame.  numpy's normal stream is
+ * not reproducible on the device: parity is the reference's moment test. */
+int nv_depth_noise(nv_ctx *ctx, double sigma, uint64_t seed, int64_t env_offset);
+
 #ifdef __cplusplus
 }
 #endif

@@ -67,6 +67,7 @@ SIGNATURES = {
     "nv_task_reset": (_I, [_P, _P, _P, _P, _P, _I64, _P, _P]),
     "nv_task_step": (_I, [_P, _P, _P, _P, _P, _P, _P, _P]),
     "nv_task_state": (_I, [_P, _P, _P, _P, _P]),
+    "nv_depth_noise": (_I, [_P, _D, ctypes.c_uint64, _I64]),
 }
 
 

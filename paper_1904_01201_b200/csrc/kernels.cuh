@@ -1339,7 +1339,48 @@ struct FillArgs {
   unsigned int *ctr;   // [0] next unit, [1] finished warps (self-resetting)
   const uint16_t *invh;  // ceil(H/2) x W f16 shading table 1/|(d_j, v_i)|, rows
                          // mirrored (v_{H-1-i} = -v_i); env-independent
+  // inverse-depth noise (sensors.apply_inverse_depth_noise, sensors.py:183-205)
+  float noise_sigma;     // 0 = off
+  float max_range;
+  unsigned long long noise_seed, noise_frame;
+  long long env_offset;  // global id of env 0 (sharding-invariant streams)
 };
+
+// ---- inverse-depth noise ---------------------------------------------------
+// z' = max_range / (max_range / d + eps), eps ~ N(0, sigma), clamped to
+// [0.05, max_range]; saturated pixels (d >= max_range) pass through
+// (sensors.py:195-205).  eps comes from a counter-based generator: one
+// splitmix64 draw per horizontal pixel pair, keyed by (seed, frame, global
+// env, row, pair), turned into two normals by Box-Muller -- so every fill
+// path produces the same noisy frame.  numpy's Generator.normal stream
+// cannot be reproduced on the device; parity is distributional (the
+// reference's own moment test, tests/test_sensors.py:179-184).
+__device__ __forceinline__ unsigned long long splitmix64(unsigned long long z) {
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+__device__ __forceinline__ float2 noise_pair(const FillArgs &a, int env, int row, int col) {
+  const unsigned long long key =
+      ((((a.noise_frame << 20) ^ (unsigned long long)(env + a.env_offset)) * (unsigned long long)a.H +
+        (unsigned long long)row) * (unsigned long long)a.W + (unsigned long long)col) >> 1;
+  const unsigned long long z = splitmix64(a.noise_seed ^ splitmix64(key));
+  const float u1 = (float)((z >> 40) + 1ull) * 0x1p-24f;           // (0, 1]
+  const float u2 = (float)((z >> 16) & 0xFFFFFFull) * 0x1p-24f;     // [0, 1)
+  const float r = sqrtf(-2.0f * __logf(u1));
+  float sn, cs;
+  __sincosf(6.283185307f * u2, &sn, &cs);
+  return make_float2(r * cs * a.noise_sigma, r * sn * a.noise_sigma);
+}
+
+__device__ __forceinline__ float noisy_depth(float d, float eps, float max_range) {
+  if (!(d < max_range)) return d;
+  const float inv = max_range / d + eps;
+  const float z = inv != 0.0f ? max_range / inv : __int_as_float(0x7f800000);
+  return fminf(fmaxf(z, 0.05f), max_range);
+}
 
 template <int CPL>
 struct Lanes {
@@ -1861,7 +1902,7 @@ struct FillWsLayout {  // byte offsets into dynamic shared memory + ring geometr
   int slot_bytes, nslot, slot_rows;
 };
 
-template <int CPL, bool TAB, int RPW>
+template <int CPL, bool TAB, int RPW, bool NOISE>
 __global__ void __launch_bounds__(544, 1) k_fill_ws(FillArgs a, FillWsLayout L) {
   extern __shared__ __align__(128) uint8_t smem[];
   using Ln = Lanes<CPL>;
@@ -1982,6 +2023,16 @@ __global__ void __launch_bounds__(544, 1) k_fill_ws(FillArgs a, FillWsLayout L) 
           load_inv<CPL, true>(a.invh + (size_t)inv_row(i, H) * W + seg * Ln::SEGW, lane, iv);
         PairOut po[CPL / 2];
         shade_row<CPL>(i, Rr, cr, iv, po);
+        if constexpr (NOISE) {
+#pragma unroll
+          for (int c = 0; c < CPL / 2; ++c) {
+            const int col = seg * Ln::SEGW + (c / (Ln::GW / 2)) * 32 * Ln::GW + lane * Ln::GW +
+                            2 * (c % (Ln::GW / 2));
+            const float2 n = noise_pair(a, e, (int)i, col);
+            po[c].d0 = noisy_depth(po[c].d0, n.x, a.max_range);
+            po[c].d1 = noisy_depth(po[c].d1, n.y, a.max_range);
+          }
+        }
         put_row<CPL>(po, want_rgb ? buf : nullptr,
                      want_d ? reinterpret_cast<float *>(buf + off_d) : nullptr,
                      want_s ? reinterpret_cast<uint16_t *>(buf + off_s) : nullptr,
@@ -2096,6 +2147,22 @@ __global__ void __launch_bounds__(128) k_step_render(MegaArgs m) {
     slot = __shfl_sync(0xffffffffu, nxt, 0);
   }
   finish_grid(m.f.ctr);
+}
+
+// Inverse-depth noise as a separate pass over a written depth batch (the
+// writers other than k_fill_ws); same per-pixel values as the fused path.
+__global__ void k_depth_noise(FillArgs a, float *depth) {
+  const long long p2 = blockIdx.x * (long long)blockDim.x + threadIdx.x;  // pixel pair
+  const int half = (a.W + 1) / 2;
+  const long long total = (long long)a.N * a.H * half;
+  if (p2 >= total) return;
+  const int cp = (int)(p2 % half);
+  const long long er = p2 / half;
+  const int row = (int)(er % a.H), env = (int)(er / a.H);
+  const float2 n = noise_pair(a, env, row, 2 * cp);
+  float *d = depth + ((size_t)env * a.H + row) * a.W + 2 * cp;
+  d[0] = noisy_depth(d[0], n.x, a.max_range);
+  if (2 * cp + 1 < a.W) d[1] = noisy_depth(d[1], n.y, a.max_range);
 }
 
 // One thread per pixel, any W/H; the same f16 arithmetic as the fast writers

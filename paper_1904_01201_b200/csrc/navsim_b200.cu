@@ -131,6 +131,9 @@ struct nv_ctx {
   DevBuf t_goal, t_gdsp, t_fid, t_dlast, t_steps, t_done;
   const double *t_fields = nullptr;
   int64_t t_nfields = 0;
+  double noise_sigma = 0.0;  // inverse-depth noise (nv_depth_noise)
+  unsigned long long noise_seed = 0, noise_frame = 0;
+  long long noise_env_offset = 0;
   int64_t n_envs = 0;
   DevBuf x, y, h, path, coll, ch, sh, ox, oy, oh, fc, fs, reset;
   Camera cams[8];
@@ -530,11 +533,12 @@ int launch_fill_direct(nv_ctx *c, nvk::FillArgs &a, cudaStream_t st) {
 template <int CPL, bool TAB, int RPW>
 int launch_ws_kernel(nv_ctx *c, nvk::FillArgs &a, const nvk::FillWsLayout &L, size_t smem,
                      cudaStream_t st) {
-  auto kern = nvk::k_fill_ws<CPL, TAB, RPW>;
-  static int configured = 0;
-  if ((int)smem > configured) {
+  const bool noise = a.noise_sigma > 0.0f && a.depth;
+  auto kern = noise ? nvk::k_fill_ws<CPL, TAB, RPW, true> : nvk::k_fill_ws<CPL, TAB, RPW, false>;
+  static int configured[2] = {0, 0};
+  if ((int)smem > configured[noise]) {
     CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    configured = (int)smem;
+    configured[noise] = (int)smem;
   }
   const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(a.N, c->sm_count));
   Prof pf(c, st, 2);
@@ -559,7 +563,7 @@ int launch_fill_ws(nv_ctx *c, nvk::FillArgs &a, cudaStream_t st) {
     return e ? atoi(e) : 0;
   }();
   struct Opt { bool tab; int rpw, nmin, nmax; };
-  static const Opt opts[] = {{true, 2, 2, 4}, {true, 1, 2, 4}, {false, 2, 2, 4}, {false, 1, 2, 4}};
+  static const Opt opts[] = {{true, 2, 2, 4}, {false, 2, 2, 4}};
   nvk::FillWsLayout L;
   bool tab = false;
   int rpw = 0;
@@ -585,10 +589,8 @@ int launch_fill_ws(nv_ctx *c, nvk::FillArgs &a, cudaStream_t st) {
   L.bars = L.cols + (int)cols_b;
   L.slots = L.bars + (int)bars_b;
   a.segs_per_row = S;
-  if (tab && rpw == 2) return launch_ws_kernel<CPL, true, 2>(c, a, L, smem, st);
-  if (tab) return launch_ws_kernel<CPL, true, 1>(c, a, L, smem, st);
-  if (rpw == 2) return launch_ws_kernel<CPL, false, 2>(c, a, L, smem, st);
-  return launch_ws_kernel<CPL, false, 1>(c, a, L, smem, st);
+  if (tab) return launch_ws_kernel<CPL, true, 2>(c, a, L, smem, st);
+  return launch_ws_kernel<CPL, false, 2>(c, a, L, smem, st);
 }
 
 int launch_fill(nv_ctx *c, Camera &cam, int64_t N, uint8_t *rgb, float *depth, uint16_t *sem,
@@ -604,24 +606,43 @@ int launch_fill(nv_ctx *c, Camera &cam, int64_t N, uint8_t *rgb, float *depth, u
   a.N = (int)N; a.W = cam.W; a.H = cam.H;
   a.rgb = rgb; a.depth = depth; a.sem = sem;
   a.ctr = cam.ctr.as<unsigned int>();
+  const bool noise = c->noise_sigma > 0.0 && depth;
+  a.noise_sigma = noise ? (float)c->noise_sigma : 0.0f;
+  a.max_range = (float)cam.max_range;
+  a.noise_seed = c->noise_seed;
+  a.noise_frame = noise ? c->noise_frame++ : 0;
+  a.env_offset = c->noise_env_offset;
   auto al16 = [](const void *p) { return ((uintptr_t)p & 15) == 0; };
   bool aligned = al16(rgb) && al16(depth) && al16(sem);
   auto al32 = [](const void *p) { return ((uintptr_t)p & 31) == 0; };
-  if (c->fill_mode == 0 && aligned && al32(depth) && cam.W % 256 == 0)
-    return launch_fill_direct<8>(c, a, st);
-  if (c->fill_mode == 0 && aligned && cam.W == 128) return launch_fill_direct<4>(c, a, st);
   const bool ws_ok = cam.W <= 4096 && (cam.W % 256 == 0 ? cam.H % (16 / std::min(16, cam.W / 256)) == 0
                                                           : cam.H % 16 == 0);
+  // the warp-specialised writer applies the noise itself; the others get a pass
   if (c->fill_mode == 3 && aligned && ws_ok && cam.W % 256 == 0) return launch_fill_ws<8>(c, a, st);
   if (c->fill_mode == 3 && aligned && ws_ok && cam.W == 128) return launch_fill_ws<4>(c, a, st);
   if (c->fill_mode == 3 && aligned && ws_ok && cam.W == 64) return launch_fill_ws<2>(c, a, st);
-  if (aligned && cam.W % 256 == 0) return launch_fill_tma<8>(c, a, st);
-  if (aligned && cam.W == 128) return launch_fill_tma<4>(c, a, st);
-  if (aligned && cam.W == 64) return launch_fill_tma<2>(c, a, st);
-  long long total = N * (long long)cam.W * cam.H;
-  Prof pf(c, st, 2);
-  nvk::k_fill_generic<<<blocks_for(total, 256), 256, 0, st>>>(a);
-  return check_launch(c);
+  if (c->fill_mode == 0 && aligned && al32(depth) && cam.W % 256 == 0)
+    TRY(launch_fill_direct<8>(c, a, st));
+  else if (c->fill_mode == 0 && aligned && cam.W == 128)
+    TRY(launch_fill_direct<4>(c, a, st));
+  else if (aligned && cam.W % 256 == 0)
+    TRY(launch_fill_tma<8>(c, a, st));
+  else if (aligned && cam.W == 128)
+    TRY(launch_fill_tma<4>(c, a, st));
+  else if (aligned && cam.W == 64)
+    TRY(launch_fill_tma<2>(c, a, st));
+  else {
+    long long total = N * (long long)cam.W * cam.H;
+    Prof pf(c, st, 2);
+    nvk::k_fill_generic<<<blocks_for(total, 256), 256, 0, st>>>(a);
+    TRY(check_launch(c));
+  }
+  if (noise) {
+    const long long pairs = N * (long long)cam.H * ((cam.W + 1) / 2);
+    nvk::k_depth_noise<<<blocks_for(pairs, 256), 256, 0, st>>>(a, depth);
+    TRY(check_launch(c));
+  }
+  return NV_OK;
 }
 
 int cam_check(nv_ctx *c, int cam) {
@@ -972,7 +993,7 @@ int nv_step_render(nv_ctx *c, const int8_t *actions, int cam, uint8_t *rgb, floa
   Camera &k = c->cams[cam];
   auto al16 = [](const void *p) { return ((uintptr_t)p & 15) == 0; };
   const bool tma_ok = al16(rgb) && al16(depth) && al16(sem) && (rgb || depth || sem);
-  if (c->fused && tma_ok && c->n_envs < (1 << 24)) {
+  if (c->fused && tma_ok && c->n_envs < (1 << 24) && !(c->noise_sigma > 0.0)) {
     if (k.W % 256 == 0)
       return launch_mega<8>(c, k, actions, rgb, depth, sem, gps, compass, collided, displacement,
                             status, st);

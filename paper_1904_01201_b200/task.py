@@ -137,7 +137,8 @@ class BatchEnvironment:
     def __init__(self, scene, n_envs: int, agent: AgentConfig | None = None,
                  sensor_configs=None, reward_params: RewardParams = RewardParams(),
                  resolution: float = nav.DEFAULT_RESOLUTION, device: int = 0,
-                 max_steps: int = MAX_EPISODE_STEPS):
+                 max_steps: int = MAX_EPISODE_STEPS, depth_noise_sigma: float = 0.0,
+                 noise_seed: int = 0, env_offset: int = 0):
         import torch
         segs, sem, alb, wall_h, floor, ceil, bounds, sid = _scene_arrays(scene)
         self.scene_id = sid
@@ -150,6 +151,14 @@ class BatchEnvironment:
         self.dev = self.sim.dev
         c = self.sim.ctx
         self.grid = nav.build_grid(c, bounds, resolution, self.agent.radius)
+        if depth_noise_sigma < 0.0:
+            from .sensors import SensorError
+            raise SensorError("sigma must be non-negative")
+        self.depth_noise_sigma = float(depth_noise_sigma)
+        self.noise_seed = int(noise_seed)
+        self.env_offset = int(env_offset)
+        nat.check(c.lib.nv_depth_noise(c.handle, self.depth_noise_sigma,
+                                       self.noise_seed & 0xFFFFFFFFFFFFFFFF, self.env_offset))
         nat.check(c.lib.nv_task_config(c.handle, int(max_steps), SUCCESS_RADIUS,
                                        float(reward_params.success_reward),
                                        float(reward_params.step_penalty)))
@@ -288,11 +297,13 @@ class Environment:
 
     def __init__(self, scene, agent: AgentConfig | None = None, sensor_configs=None,
                  reward_params: RewardParams = RewardParams(),
-                 resolution: float = nav.DEFAULT_RESOLUTION, device: int = 0):
+                 resolution: float = nav.DEFAULT_RESOLUTION, field_cache=None,
+                 depth_noise_sigma: float = 0.0, noise_seed: int = 0, device: int = 0):
         self.scene = scene
         self.agent_config = agent or AgentConfig()
         self._b = BatchEnvironment(scene, 1, self.agent_config, sensor_configs, reward_params,
-                                   resolution, device)
+                                   resolution, device, depth_noise_sigma=depth_noise_sigma,
+                                   noise_seed=noise_seed)
         self.grid = self._b.grid
         self.episode = None
         self.steps = 0
@@ -312,6 +323,10 @@ class Environment:
         return obs
 
     def reset(self, episode: Episode) -> Observations:
+        # the noise stream restarts with every episode (task.py:187)
+        c = self._b.sim.ctx
+        nat.check(c.lib.nv_depth_noise(c.handle, self._b.depth_noise_sigma,
+                                       self._b.noise_seed & 0xFFFFFFFFFFFFFFFF, 0))
         obs = self._b.reset([episode])
         self.episode = episode
         self.steps = 0

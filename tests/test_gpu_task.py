@@ -183,3 +183,54 @@ def test_apartment_fields_vs_oracle(nb):
     for k, goal in enumerate(goals):
         assert tuple(fc[k]) == og.snap(goal)
         assert np.array_equal(host[k], og.field(tuple(fc[k])))
+
+
+def test_depth_noise_moments_and_paths(nb):
+    """Inverse-depth noise (nv_depth_noise, sensors.py:183-205): the reference's
+    moment test on the device stream (eps = max_range/d' - max_range/d has std
+    sigma), saturated pixels untouched, clamping, determinism, and the same
+    noisy frame from every fill path (fused in the ws writer, a pass
+    otherwise)."""
+    from paper_1904_01201_b200 import _native as nat
+    from paper_1904_01201_b200 import synth
+    sc = synth.config_scene("C2")
+    W = H = 128
+    n = 48
+    suite = (nb.SensorConfig("depth", W, H),)
+    sim = nb.BatchSimulator(sc.segments, sc.semantic_ids, sc.albedo, n, sensor_configs=suite)
+    poses = synth.sample_poses(sc, n, seed=12)
+    sim.reset(poses[:, :2], poses[:, 2])
+    c = sim.ctx
+    sim.render()
+    torch.cuda.synchronize()
+    clean = sim.observations()["depth"].clone().double()
+    outs = []
+    for mode in (3, 1, 0):
+        nat.check(c.lib.nv_set_fill_mode(c.handle, mode))
+        nat.check(c.lib.nv_depth_noise(c.handle, 0.4, 1234, 0))
+        sim.render()
+        torch.cuda.synchronize()
+        outs.append(sim.observations()["depth"].clone())
+    for o in outs[1:]:
+        assert torch.equal(o, outs[0])
+    noisy = outs[0].double()
+    mr = 10.0
+    void = clean >= mr
+    assert torch.equal(noisy[void], clean[void])
+    live = ~void
+    assert noisy[live].min().item() >= 0.05 - 1e-7 and noisy[live].max().item() <= mr
+    sel = (clean <= 4.0) & (noisy > 0.05) & (noisy < mr)
+    eps = (mr / noisy[sel] - mr / clean[sel]).cpu().numpy()
+    assert eps.size > 100000
+    assert abs(eps.mean()) < 0.01
+    assert eps.std() == pytest.approx(0.4, abs=0.01)
+    # a new seed changes the frame; the same seed reproduces it
+    nat.check(c.lib.nv_depth_noise(c.handle, 0.4, 1234, 0))
+    sim.render()
+    torch.cuda.synchronize()
+    assert torch.equal(sim.observations()["depth"], outs[0])
+    nat.check(c.lib.nv_depth_noise(c.handle, 0.4, 99, 0))
+    sim.render()
+    torch.cuda.synchronize()
+    assert not torch.equal(sim.observations()["depth"], outs[0])
+    assert c.lib.nv_depth_noise(c.handle, -1.0, 0, 0) == nat.NV_ERR_ARG
