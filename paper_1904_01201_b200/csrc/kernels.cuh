@@ -877,6 +877,41 @@ __global__ void __launch_bounds__(256) k_step_cast(EnvView ev, SceneView sc, Age
     cast_column<true>(ev, sc, cam, e, j, ro, t_max, gps, compass);
 }
 
+// Persistent variant: every warp pulls (env, 32-column group) work items from
+// a self-resetting global counter until none are left, so all warp slots stay
+// busy to the end of the launch (no tail of half-empty CTAs); consecutive
+// items are neighbouring column groups of one env (shared cells in L1).
+#ifndef NV_CAST_MINB
+#define NV_CAST_MINB 1
+#endif
+__global__ void __launch_bounds__(128, NV_CAST_MINB) k_column_cast_q(EnvView ev, SceneView sc,
+                                                                     CamView cam, RecOut ro,
+                                                                     double t_max, double *gps,
+                                                                     double *compass,
+                                                                     unsigned int *ctr) {
+  const int lane = threadIdx.x & 31;
+  const int gpe = (cam.W + 31) >> 5;  // column groups per env
+  const long long total = (long long)ev.n * gpe;
+  for (;;) {
+    long long item = 0;
+    if (lane == 0) item = atomicAdd(ctr, 1u);
+    item = __shfl_sync(0xffffffffu, item, 0);
+    if (item >= total) break;
+    const int e = (int)(item / gpe);
+    const int j = (int)(item - (long long)e * gpe) * 32 + lane;
+    if (j < cam.W) cast_column<false>(ev, sc, cam, e, j, ro, t_max, gps, compass);
+  }
+  if (lane == 0) {  // the last warp out resets the counters for the next launch
+    __threadfence();
+    const unsigned total_warps = gridDim.x * (blockDim.x >> 5);
+    if (atomicAdd(ctr + 1, 1u) == total_warps - 1) {
+      ctr[0] = 0;
+      ctr[1] = 0;
+      __threadfence();
+    }
+  }
+}
+
 // ---------------------------------------------------- binned column cast
 //
 // k_cast_binned: one CTA per env computes all W column hits by tile-binned

@@ -93,6 +93,8 @@ struct Camera {
   DevBuf u, tc, tf, rows, invh;
   DevBuf rec;      // ColRec N x W
   DevBuf ctr;      // fill scheduler counters
+  DevBuf cast_ctr; // persistent cast work counter (self-resetting)
+  bool cast_ctr_init = false;
   // fused step+render megakernel task queue (rebuilt when N or layout changes)
   DevBuf tasks, envsync;
   int64_t tasks_n = -1;
@@ -141,6 +143,7 @@ struct nv_ctx {
   DevBuf e_act, e_rgb, e_depth, e_sem, e_gps, e_comp, e_coll, e_disp;
   int64_t launches = 0;
   int cast_mode = 0;  // 0: per-column DDA (default), 1: binned (tile-binned segment setup)
+  bool cast_queue = false;  // column cast by persistent warps over a work counter (opt-in: slower)
   int fill_mode = 3;   // 0 direct stores, 1 per-warp TMA stages, 2 CTA per frame, 3 warp-specialised
   bool fused = false;  // nv_step_render uses the megakernel when the layout allows (opt-in)
   // optional per-kernel CUDA-event timing (bench roofline evidence)
@@ -563,7 +566,7 @@ int launch_fill_ws(nv_ctx *c, nvk::FillArgs &a, cudaStream_t st) {
     return e ? atoi(e) : 0;
   }();
   struct Opt { bool tab; int rpw, nmin, nmax; };
-  static const Opt opts[] = {{true, 2, 2, 4}, {false, 2, 2, 4}};
+  static const Opt opts[] = {{true, 2, 2, 4}, {true, 1, 2, 4}, {false, 2, 2, 4}, {false, 1, 2, 4}};
   nvk::FillWsLayout L;
   bool tab = false;
   int rpw = 0;
@@ -589,8 +592,10 @@ int launch_fill_ws(nv_ctx *c, nvk::FillArgs &a, cudaStream_t st) {
   L.bars = L.cols + (int)cols_b;
   L.slots = L.bars + (int)bars_b;
   a.segs_per_row = S;
-  if (tab) return launch_ws_kernel<CPL, true, 2>(c, a, L, smem, st);
-  return launch_ws_kernel<CPL, false, 2>(c, a, L, smem, st);
+  if (tab && rpw == 2) return launch_ws_kernel<CPL, true, 2>(c, a, L, smem, st);
+  if (tab) return launch_ws_kernel<CPL, true, 1>(c, a, L, smem, st);
+  if (rpw == 2) return launch_ws_kernel<CPL, false, 2>(c, a, L, smem, st);
+  return launch_ws_kernel<CPL, false, 1>(c, a, L, smem, st);
 }
 
 int launch_fill(nv_ctx *c, Camera &cam, int64_t N, uint8_t *rgb, float *depth, uint16_t *sem,
@@ -677,6 +682,23 @@ int do_cast(nv_ctx *c, int cam, double *gps, double *compass, cudaStream_t st) {
   // frames (tests/test_gpu_parity.py checks it against the
   // reference's uncapped t_max = 1e9 render).
   const long long total = c->n_envs * (long long)k.W;
+  if (c->cast_queue) {  // persistent warps over a work counter
+    TRY(k.cast_ctr.alloc(2 * sizeof(unsigned int)));
+    if (!k.cast_ctr_init) {
+      CK(cudaMemset(k.cast_ctr.p, 0, 2 * sizeof(unsigned int)));
+      k.cast_ctr_init = true;
+    }
+    int per_sm = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, nvk::k_column_cast_q, 128, 0));
+    const long long want = (c->n_envs * ((k.W + 31) / 32) + 3) / 4;
+    const unsigned grid = (unsigned)std::max<long long>(
+        1, std::min<long long>(want, (long long)std::max(1, per_sm) * c->sm_count));
+    Prof pf(c, st, 1);
+    nvk::k_column_cast_q<<<grid, 128, 0, st>>>(c->env_view(), c->scene_view(), cam_view(k),
+                                                rec_out(k, c->n_envs), k.max_range, gps, compass,
+                                                k.cast_ctr.as<unsigned int>());
+    return check_launch(c);
+  }
   Prof pf(c, st, 1);
   nvk::k_column_cast<<<blocks_for(total, 128), 128, 0, st>>>(
       c->env_view(), c->scene_view(), cam_view(k), rec_out(k, c->n_envs), k.max_range, gps,
@@ -718,6 +740,7 @@ int nv_create(int device, nv_ctx **out) {
   CK(cudaSetDevice(device));
   nv_ctx *c = new nv_ctx();
   c->device = device;
+  if (const char *q = getenv("NAVSIM_CAST_QUEUE")) c->cast_queue = atoi(q) != 0;  // A/B knob
   cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device);
   cudaDeviceGetAttribute(&c->max_smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
   *out = c;
