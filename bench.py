@@ -318,7 +318,8 @@ def run_gpu(args):
                                   shard.n_local * bytes_per_env_step(W, H, chans),
                                   per["step_render_fused"])
     else:
-        dom, dom_bytes, dom_ms = "k_fill_tma (frame_fill)", frame_bytes, per["frame_fill"]
+        writer = {0: "k_fill_direct", 1: "k_fill_tma", 3: "k_fill_ws"}.get(args.fill_mode, "k_fill")
+        dom, dom_bytes, dom_ms = f"{writer} (frame_fill)", frame_bytes, per["frame_fill"]
     peak, peak_src = measured_peaks()
     achieved = dom_bytes / (dom_ms / 1e3) / 1e9
     step_bytes = shard.n_local * bytes_per_env_step(W, H, chans)
