@@ -414,6 +414,9 @@ __device__ __forceinline__ double disc_seg_t_pre(double px, double py, double ux
   return best;
 }
 
+#ifndef NV_DISC_K
+#define NV_DISC_K 4  // candidates per lane per round of the flat disc-cast pass
+#endif
 __device__ __forceinline__ void lex_min(double &t, int &i, double t2, int i2) {
   if (t2 < t || (t2 == t && i2 < i)) {
     t = t2;
@@ -472,13 +475,18 @@ __device__ void warp_cast_disc(const SceneView &sc, double px, double py, double
       if (lane >= o) incl += v;
     }
     const int total = __shfl_sync(0xffffffffu, incl, 31);
-    // two candidates per lane per round; both records are loaded together
-    for (int base = 0; base < total; base += 64) {
-      int qq[2];
-      bool ok[2];
-      float bx0[2], bx1[2], by0[2], by1[2];
+    // All candidates (up to NV_DISC_K per lane) are located and their f32
+    // endpoint records loaded in one memory round trip; the survivors of the
+    // box test are compacted through shared memory to one lane each, which
+    // loads its disc record (second round trip) and runs disc_cast's math.
+    constexpr int K = NV_DISC_K;
+    __shared__ int s_q[8][32 * K];
+    int *sq = s_q[(threadIdx.x >> 5) & 7];
+    for (int base = 0; base < total; base += 32 * K) {
+      int qq[K];
+      bool sv[K];
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
+      for (int h = 0; h < K; ++h) {
         const int g = min(base + h * 32 + lane, total - 1);
         int o = 0;
 #pragma unroll
@@ -492,25 +500,27 @@ __device__ void warp_cast_disc(const SceneView &sc, double px, double py, double
         const int ocx = __shfl_sync(0xffffffffu, cxk, o);
         const int ocy = __shfl_sync(0xffffffffu, cyk, o);
         qq[h] = oq0 + (g - (oincl - ocnt));
-        ok[h] = base + h * 32 + lane < total;
         const double X0 = add(sc.x0, (double)ocx), Y0 = add(sc.y0, (double)ocy);
-        bx0[h] = (float)sub(lox, X0) - grow;
-        bx1[h] = (float)sub(hix, X0) + grow;
-        by0[h] = (float)sub(loy, Y0) - grow;
-        by1[h] = (float)sub(hiy, Y0) + grow;
+        const float bx0 = (float)sub(lox, X0) - grow, bx1 = (float)sub(hix, X0) + grow;
+        const float by0 = (float)sub(loy, Y0) - grow, by1 = (float)sub(hiy, Y0) + grow;
+        const float4 f = __ldg(sc.entf + qq[h]);
+        sv[h] = base + h * 32 + lane < total && !(fmaxf(f.x, f.z) < bx0 || fminf(f.x, f.z) > bx1 ||
+                                                   fmaxf(f.y, f.w) < by0 || fminf(f.y, f.w) > by1);
       }
-      float4 f[2];
+      int nsurv = 0;
 #pragma unroll
-      for (int h = 0; h < 2; ++h) f[h] = __ldg(sc.entf + qq[h]);
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        if (!ok[h] || fmaxf(f[h].x, f[h].z) < bx0[h] || fminf(f[h].x, f[h].z) > bx1[h] ||
-            fmaxf(f[h].y, f[h].w) < by0[h] || fminf(f[h].y, f[h].w) > by1[h])
-          continue;
-        const DiscEntry d = sc.dent[qq[h]];
+      for (int h = 0; h < K; ++h) {
+        const unsigned m = __ballot_sync(0xffffffffu, sv[h]);
+        if (sv[h]) sq[nsurv + __popc(m & ((1u << lane) - 1u))] = qq[h];
+        nsurv += __popc(m);
+      }
+      __syncwarp();
+      for (int r = lane; r < nsurv; r += 32) {
+        const DiscEntry d = sc.dent[sq[r]];
         const double t = disc_seg_t_pre(px, py, ux, uy, radius, u2, d);
         lex_min(bt, bi, t, d.idx);
       }
+      __syncwarp();
     }
   } else {
     for (int cy = cy0; cy <= cy1; ++cy)

@@ -140,7 +140,17 @@ struct nv_ctx {
   DevBuf x, y, h, path, coll, ch, sh, ox, oy, oh, fc, fs, reset;
   Camera cams[8];
   // host-buffer (e2e) path scratch
-  DevBuf e_act, e_rgb, e_depth, e_sem, e_gps, e_comp, e_coll, e_disp;
+  DevBuf e_act, e_rgb, e_depth, e_sem, e_pack;  // e_pack: gps 16N | compass 8N | disp 8N | coll N
+  // host-buffer path as one CUDA graph: H2D actions -> step+render -> one D2H
+  // of the packed step results, replayed while (cam, channels, N) stay fixed
+  cudaStream_t e_stream = nullptr;
+  cudaEvent_t e_ev = nullptr;
+  cudaGraphExec_t e_graph = nullptr;
+  int e_key[3] = {-1, -1, -1};
+  int64_t e_key_n = -1, e_key_gen = -1;
+  int64_t gen = 0;  // bumped by every call that changes kernel arguments (graph key)
+  void *e_hin = nullptr, *e_hout = nullptr;  // pinned staging (actions in, packed results out)
+  size_t e_hin_bytes = 0, e_hout_bytes = 0;
   int64_t launches = 0;
   int cast_mode = 0;  // 0: per-column DDA (default), 1: binned (tile-binned segment setup)
   bool cast_queue = false;  // column cast by persistent warps over a work counter (opt-in: slower)
@@ -155,6 +165,11 @@ struct nv_ctx {
   int64_t prof_n[4] = {0, 0, 0, 0};
   ~nv_ctx() {
     for (auto e : prof_ev) cudaEventDestroy(e);
+    if (e_graph) cudaGraphExecDestroy(e_graph);
+    if (e_ev) cudaEventDestroy(e_ev);
+    if (e_stream) cudaStreamDestroy(e_stream);
+    if (e_hin) cudaFreeHost(e_hin);
+    if (e_hout) cudaFreeHost(e_hout);
   }
   // launch config
   SceneView scene_view() const {
@@ -266,6 +281,7 @@ uint32_t h2splat(float x) {
 // (column directions have unit forward component, sensors.py:96-102), is the
 // same for every env and heading; rows i >= ceil(H/2) mirror row H-1-i.
 int build_camera_tables(nv_ctx *c, Camera &cam, double cam_h) {
+  c->gen++;
   const int W = cam.W, H = cam.H;
   std::vector<double> u(W), tc(H, 0.0), tf(H, 0.0), vv(H);
   for (int j = 0; j < W; ++j) u[j] = (((double)j + 0.5) - (double)W * 0.5) / cam.focal;
@@ -757,6 +773,7 @@ int nv_destroy(nv_ctx *ctx) {
 int nv_scene_upload(nv_ctx *c, const double *segs, const uint16_t *sem, const double *albedo,
                     int64_t n, double wall_height, const double *floor3, const double *ceil3) {
   if (!c) return fail(NV_ERR_ARG, "ctx is NULL");
+  c->gen++;
   if (n < 0 || (n > 0 && (!segs || !sem || !albedo)))
     return fail(NV_ERR_ARG, "bad scene arrays");
   if (n >= (1LL << 31)) return fail(NV_ERR_ARG, "too many segments (%lld)", (long long)n);
@@ -901,6 +918,7 @@ int nv_scene_grid_info(nv_ctx *c, double *x0, double *y0, int64_t *nx, int64_t *
 int nv_agent_config(nv_ctx *c, double radius, double forward_step, double turn_rad,
                     double sensor_height) {
   if (!c) return fail(NV_ERR_ARG, "ctx is NULL");
+  c->gen++;
   if (!(radius >= 0.0) || !(forward_step > 0.0) || !(turn_rad > 0.0) || !(sensor_height > 0.0))
     return fail(NV_ERR_ARG, "invalid agent config");
   if (c->has_scene && sensor_height > c->wall_h)
@@ -914,6 +932,7 @@ int nv_agent_config(nv_ctx *c, double radius, double forward_step, double turn_r
 
 int nv_envs_alloc(nv_ctx *c, int64_t n_envs) {
   if (!c) return fail(NV_ERR_ARG, "ctx is NULL");
+  c->gen++;
   if (n_envs <= 0 || n_envs >= (1LL << 30)) return fail(NV_ERR_ARG, "bad n_envs %lld", (long long)n_envs);
   CK(cudaSetDevice(c->device));
   size_t d = sizeof(double) * (size_t)n_envs;
@@ -935,6 +954,7 @@ int nv_envs_alloc(nv_ctx *c, int64_t n_envs) {
 
 int nv_camera_config(nv_ctx *c, int cam, int width, int height, double focal, double max_range) {
   if (!c) return fail(NV_ERR_ARG, "ctx is NULL");
+  c->gen++;
   if (cam < 0 || cam >= 8) return fail(NV_ERR_ARG, "camera index %d out of range [0, 8)", cam);
   if (width < 1 || height < 1 || width > 16384 || height > 16384)
     return fail(NV_ERR_ARG, "sensor resolution must be at least 1x1 (got %dx%d)", width, height);
@@ -1046,11 +1066,13 @@ int nv_step_render(nv_ctx *c, const int8_t *actions, int cam, uint8_t *rgb, floa
 
 int nv_set_cast_mode(nv_ctx *c, int mode) {
   if (!c) return fail(NV_ERR_ARG, "ctx is NULL");
+  c->gen++;
   return nv_set_cast_mode_(c, mode);
 }
 
 int nv_set_fill_mode(nv_ctx *c, int mode) {
   if (!c) return fail(NV_ERR_ARG, "ctx is NULL");
+  c->gen++;
   if (mode < 0 || mode > 3 || mode == 2)
     return fail(NV_ERR_ARG, "fill mode must be 0 (direct), 1 (tma) or 3 (ws)");
   c->fill_mode = mode;
@@ -1059,6 +1081,7 @@ int nv_set_fill_mode(nv_ctx *c, int mode) {
 
 int nv_set_fused(nv_ctx *c, int on) {
   if (!c) return fail(NV_ERR_ARG, "ctx is NULL");
+  c->gen++;
   c->fused = on != 0;
   return NV_OK;
 }
@@ -1082,22 +1105,93 @@ int nv_step_render_host(nv_ctx *c, const int8_t *actions_host, int cam, uint32_t
   if (want_rgb) TRY(c->e_rgb.alloc(px * 3));
   if (want_d) TRY(c->e_depth.alloc(px * 4));
   if (want_s) TRY(c->e_sem.alloc(px * 2));
-  TRY(c->e_gps.alloc(16 * N)); TRY(c->e_comp.alloc(8 * N)); TRY(c->e_coll.alloc(N));
-  TRY(c->e_disp.alloc(8 * N));
+  const size_t pack = 33 * N;
+  TRY(c->e_pack.alloc(pack));
+  uint8_t *pk = c->e_pack.as<uint8_t>();
+  double *d_gps = reinterpret_cast<double *>(pk), *d_comp = d_gps + 2 * N, *d_disp = d_comp + N;
+  uint8_t *d_coll = pk + 32 * N;
+  const bool frames_out = rgb_host || depth_host || sem_host;
+  // graph path: no host frames, no profiling, no noise (its frame counter
+  // advances per call) -- the common per-step case
+  const bool graph_ok = !frames_out && !c->prof_on && !(c->noise_sigma > 0.0);
+  if (graph_ok) {
+    if (!c->e_stream) {
+      CK(cudaStreamCreateWithFlags(&c->e_stream, cudaStreamNonBlocking));
+      CK(cudaEventCreateWithFlags(&c->e_ev, cudaEventDisableTiming));
+    }
+    if (c->e_hin_bytes < N) {
+      if (c->e_hin) cudaFreeHost(c->e_hin);
+      CK(cudaMallocHost(&c->e_hin, N));
+      c->e_hin_bytes = N;
+    }
+    if (c->e_hout_bytes < pack) {
+      if (c->e_hout) cudaFreeHost(c->e_hout);
+      CK(cudaMallocHost(&c->e_hout, pack));
+      c->e_hout_bytes = pack;
+      if (c->e_graph) cudaGraphExecDestroy(c->e_graph);
+      c->e_graph = nullptr;
+    }
+    const int key[3] = {cam, (int)(channels | (want_rgb ? 8u : 0u) | (want_d ? 16u : 0u) | (want_s ? 32u : 0u)),
+                        c->fill_mode * 16 + c->cast_mode * 2 + (c->fused ? 1 : 0)};
+    const bool same = c->e_graph && c->e_key_n == c->n_envs && c->e_key_gen == c->gen &&
+                      key[0] == c->e_key[0] &&
+                      key[1] == c->e_key[1] && key[2] == c->e_key[2];
+    cudaStream_t es = c->e_stream;
+    if (!same) {
+      if (c->e_graph) cudaGraphExecDestroy(c->e_graph);
+      c->e_graph = nullptr;
+      CK(cudaStreamBeginCapture(es, cudaStreamCaptureModeThreadLocal));
+      cudaMemcpyAsync(c->e_act.p, c->e_hin, N, cudaMemcpyHostToDevice, es);
+      int rc = nv_step_render(c, c->e_act.as<int8_t>(), cam,
+                              want_rgb ? c->e_rgb.as<uint8_t>() : nullptr,
+                              want_d ? c->e_depth.as<float>() : nullptr,
+                              want_s ? c->e_sem.as<uint16_t>() : nullptr, d_gps, d_comp, d_coll,
+                              d_disp, nullptr, es);
+      cudaMemcpyAsync(c->e_hout, pk, pack, cudaMemcpyDeviceToHost, es);
+      cudaGraph_t g = nullptr;
+      cudaError_t ce = cudaStreamEndCapture(es, &g);
+      if (rc != NV_OK) {
+        if (g) cudaGraphDestroy(g);
+        return rc;
+      }
+      if (ce != cudaSuccess) return fail(NV_ERR_CUDA, "graph capture failed: %s", cudaGetErrorString(ce));
+      ce = cudaGraphInstantiate(&c->e_graph, g, 0);
+      cudaGraphDestroy(g);
+      if (ce != cudaSuccess) return fail(NV_ERR_CUDA, "graph instantiate failed: %s", cudaGetErrorString(ce));
+      std::memcpy(c->e_key, key, sizeof key);
+      c->e_key_n = c->n_envs;
+      c->e_key_gen = c->gen;
+    }
+    std::memcpy(c->e_hin, actions_host, N);
+    CK(cudaEventRecord(c->e_ev, st));  // after the caller's prior work
+    CK(cudaStreamWaitEvent(es, c->e_ev, 0));
+    CK(cudaGraphLaunch(c->e_graph, es));
+    c->launches += 3;
+    CK(cudaStreamSynchronize(es));
+    const uint8_t *h = static_cast<const uint8_t *>(c->e_hout);
+    if (gps_host) std::memcpy(gps_host, h, 16 * N);
+    if (compass_host) std::memcpy(compass_host, h + 16 * N, 8 * N);
+    if (displacement_host) std::memcpy(displacement_host, h + 24 * N, 8 * N);
+    if (collided_host) std::memcpy(collided_host, h + 32 * N, N);
+    return NV_OK;
+  }
   CK(cudaMemcpyAsync(c->e_act.p, actions_host, N, cudaMemcpyHostToDevice, st));
   TRY(nv_step_render(c, c->e_act.as<int8_t>(), cam, want_rgb ? c->e_rgb.as<uint8_t>() : nullptr,
                      want_d ? c->e_depth.as<float>() : nullptr,
-                     want_s ? c->e_sem.as<uint16_t>() : nullptr, c->e_gps.as<double>(),
-                     c->e_comp.as<double>(), c->e_coll.as<uint8_t>(), c->e_disp.as<double>(),
+                     want_s ? c->e_sem.as<uint16_t>() : nullptr, d_gps, d_comp, d_coll, d_disp,
                      nullptr, stream));
   if (rgb_host) CK(cudaMemcpyAsync(rgb_host, c->e_rgb.p, px * 3, cudaMemcpyDeviceToHost, st));
   if (depth_host) CK(cudaMemcpyAsync(depth_host, c->e_depth.p, px * 4, cudaMemcpyDeviceToHost, st));
   if (sem_host) CK(cudaMemcpyAsync(sem_host, c->e_sem.p, px * 2, cudaMemcpyDeviceToHost, st));
-  if (gps_host) CK(cudaMemcpyAsync(gps_host, c->e_gps.p, 16 * N, cudaMemcpyDeviceToHost, st));
-  if (compass_host) CK(cudaMemcpyAsync(compass_host, c->e_comp.p, 8 * N, cudaMemcpyDeviceToHost, st));
-  if (collided_host) CK(cudaMemcpyAsync(collided_host, c->e_coll.p, N, cudaMemcpyDeviceToHost, st));
-  if (displacement_host)
-    CK(cudaMemcpyAsync(displacement_host, c->e_disp.p, 8 * N, cudaMemcpyDeviceToHost, st));
+  if (gps_host || compass_host || collided_host || displacement_host) {
+    std::vector<uint8_t> h(pack);
+    CK(cudaMemcpyAsync(h.data(), pk, pack, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (gps_host) std::memcpy(gps_host, h.data(), 16 * N);
+    if (compass_host) std::memcpy(compass_host, h.data() + 16 * N, 8 * N);
+    if (displacement_host) std::memcpy(displacement_host, h.data() + 24 * N, 8 * N);
+    if (collided_host) std::memcpy(collided_host, h.data() + 32 * N, N);
+  }
   CK(cudaStreamSynchronize(st));
   return NV_OK;
 }

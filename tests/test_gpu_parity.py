@@ -433,3 +433,46 @@ def test_step_cast_fused_agrees(nb, cfg, W, H, n):
         assert torch.equal(outs[0]["semantic"].view(torch.int16), outs[1]["semantic"].view(torch.int16))
         for a, b in zip(outs[0]["state"], outs[1]["state"]):
             assert torch.equal(a, b)
+
+
+def test_host_buffer_path_matches_device_path(nb):
+    """nv_step_render_host (graph-replayed, packed results) gives the same step
+    results as nv_step_render on device buffers, across repeated
+    calls (graph replay), a camera/channel change (re-capture) and a fill-mode
+    change (generation bump)."""
+    from paper_1904_01201_b200 import _native as nat
+    from paper_1904_01201_b200 import synth
+    sc = synth.config_scene("C2")
+    W, H, n = 128, 64, 40
+    suite = (nb.SensorConfig("rgb", W, H), nb.SensorConfig("depth", W, H),
+             nb.SensorConfig("gps_compass"))
+    sims = [nb.BatchSimulator(sc.segments, sc.semantic_ids, sc.albedo, n, sensor_configs=suite)
+            for _ in range(2)]
+    poses = synth.sample_poses(sc, n, seed=31)
+    for s in sims:
+        s.reset(poses[:, :2], poses[:, 2])
+    acts = synth.random_actions(n, 8, seed=32)
+    out = {"gps": np.empty((n, 2)), "compass": np.empty(n), "collided": np.empty(n, np.uint8),
+           "displacement": np.empty(n)}
+    for t in range(acts.shape[0]):
+        if t == 5:
+            for s in sims:
+                nat.check(s.ctx.lib.nv_set_fill_mode(s.ctx.handle, 1))
+        a_host = np.ascontiguousarray(acts[t])
+        sims[0].step_host(a_host, out=out)
+        sims[1].step(torch.as_tensor(a_host, device="cuda:0"))
+        torch.cuda.synchronize()
+        o1 = sims[1].observations()
+        assert np.array_equal(out["gps"], o1["gps"].cpu().numpy())
+        assert np.array_equal(out["compass"], o1["compass"].cpu().numpy())
+        assert np.array_equal(out["collided"], sims[1].collided.cpu().numpy())
+        assert np.array_equal(out["displacement"], sims[1].displacement.cpu().numpy())
+    # the non-graph path (host frames requested) agrees too
+    a_host = np.ascontiguousarray(acts[0])
+    rgb_h = np.empty((n, H, W, 3), np.uint8)
+    out["rgb"] = rgb_h
+    sims[0].step_host(a_host, out=out, frames_to_host=True)
+    sims[1].step(torch.as_tensor(a_host, device="cuda:0"))
+    torch.cuda.synchronize()
+    assert np.array_equal(rgb_h, sims[1].observations()["rgb"].cpu().numpy())
+    assert np.array_equal(out["gps"], sims[1].gps.cpu().numpy())
