@@ -318,7 +318,8 @@ def run_gpu(args):
                                   shard.n_local * bytes_per_env_step(W, H, chans),
                                   per["step_render_fused"])
     else:
-        writer = {0: "k_fill_direct", 1: "k_fill_tma", 3: "k_fill_ws"}.get(args.fill_mode, "k_fill")
+        writer = {0: "k_fill_direct", 1: "k_fill_tma", 2: "k_fill_ws"}.get(
+            args.fill_mode, "k_fill_ws" if shard.n_local >= 74 else "k_fill_tma")
         dom, dom_bytes, dom_ms = f"{writer} (frame_fill)", frame_bytes, per["frame_fill"]
     peak, peak_src = measured_peaks()
     achieved = dom_bytes / (dom_ms / 1e3) / 1e9
@@ -390,7 +391,7 @@ def run_gpu(args):
                        "channels": list(chans), "segments": sc.n_segments,
                        "triangles": sc.n_triangles, "parallelism": f"env-shard x{world}",
                        "cuda_graph": use_graph, "fused_megakernel": fused,
-                       "fill_mode": {0: "direct-stores", 1: "per-warp-tma-stages", 3: "warp-specialised-tma"}.get(args.fill_mode),
+                       "fill_mode": {0: "direct-stores", 1: "per-warp-tma-stages", 2: "warp-specialised-tma", 3: "auto (warp-specialised-tma when envs >= SMs/2, else per-warp-tma-stages)"}.get(args.fill_mode),
                        "cast_mode": ["dda", "binned", "dda-fused-with-agent-step"][args.cast_mode],
                        "l2": f"no flush: frames written per step "
                              f"({step_bytes / 1e6:.0f} MB/GPU) exceed the 126 MB L2"},
@@ -427,7 +428,7 @@ def main():
     ap.add_argument("--envs", type=int, default=0, help="override envs per GPU")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-graph", action="store_true")
-    ap.add_argument("--fill-mode", type=int, default=3, help="0 direct stores, 1 per-warp TMA stages, 3 warp-specialised writer")
+    ap.add_argument("--fill-mode", type=int, default=3, help="0 direct stores, 1 per-warp TMA stages, 2 warp-specialised writer, 3 auto")
     ap.add_argument("--cast-mode", type=int, default=0, help="0 per-column DDA, 1 binned, 2 DDA fused with the agent step")
     ap.add_argument("--fused", action="store_true", help="one megakernel launch per step (experimental)")
     ap.add_argument("--no-e2e", action="store_true")

@@ -131,9 +131,11 @@ int nv_set_fused(nv_ctx *ctx, int on);
 int nv_set_cast_mode(nv_ctx *ctx, int mode);
 /* Frame writer: 0 = 256-bit direct stores from registers,
  * 1 = per-warp shared-memory stages written out by TMA bulk copies,
- * 3 (default) = warp-specialised: 16 producer warps render rows into a ring of
+ * 2 = warp-specialised: 16 producer warps render rows into a ring of
  *     smem slots, one store warp writes each slot with one bulk copy per
- *     channel.  All modes produce identical frames. */
+ *     channel (one CTA per SM, one env frame per work item),
+ * 3 (default) = 2 for batches of at least half the SM count, else 1.
+ * All modes produce identical frames. */
 int nv_set_fill_mode(nv_ctx *ctx, int mode);
 
 /* End-to-end call over HOST buffers (the reference-facing path: host actions

@@ -154,7 +154,7 @@ struct nv_ctx {
   int64_t launches = 0;
   int cast_mode = 0;  // 0: per-column DDA (default), 1: binned (tile-binned segment setup)
   bool cast_queue = false;  // column cast by persistent warps over a work counter (opt-in: slower)
-  int fill_mode = 3;   // 0 direct stores, 1 per-warp TMA stages, 2 CTA per frame, 3 warp-specialised
+  int fill_mode = 3;   // 0 direct stores, 1 per-warp TMA stages, 2 warp-specialised, 3 auto
   bool fused = false;  // nv_step_render uses the megakernel when the layout allows (opt-in)
   // optional per-kernel CUDA-event timing (bench roofline evidence)
   bool prof_on = false;
@@ -638,10 +638,14 @@ int launch_fill(nv_ctx *c, Camera &cam, int64_t N, uint8_t *rgb, float *depth, u
   auto al32 = [](const void *p) { return ((uintptr_t)p & 31) == 0; };
   const bool ws_ok = cam.W <= 4096 && (cam.W % 256 == 0 ? cam.H % (16 / std::min(16, cam.W / 256)) == 0
                                                           : cam.H % 16 == 0);
-  // the warp-specialised writer applies the noise itself; the others get a pass
-  if (c->fill_mode == 3 && aligned && ws_ok && cam.W % 256 == 0) return launch_fill_ws<8>(c, a, st);
-  if (c->fill_mode == 3 && aligned && ws_ok && cam.W == 128) return launch_fill_ws<4>(c, a, st);
-  if (c->fill_mode == 3 && aligned && ws_ok && cam.W == 64) return launch_fill_ws<2>(c, a, st);
+  // mode 2 = warp-specialised writer; mode 3 (default) = the same for batches
+  // that fill the GPU (one CTA per env frame at a time), else the per-warp
+  // writer, which spreads a small batch over every SM.  The warp-specialised
+  // writer applies the depth noise itself; the others get a pass.
+  const bool use_ws = c->fill_mode == 2 || (c->fill_mode == 3 && N >= c->sm_count / 2);
+  if (use_ws && aligned && ws_ok && cam.W % 256 == 0) return launch_fill_ws<8>(c, a, st);
+  if (use_ws && aligned && ws_ok && cam.W == 128) return launch_fill_ws<4>(c, a, st);
+  if (use_ws && aligned && ws_ok && cam.W == 64) return launch_fill_ws<2>(c, a, st);
   if (c->fill_mode == 0 && aligned && al32(depth) && cam.W % 256 == 0)
     TRY(launch_fill_direct<8>(c, a, st));
   else if (c->fill_mode == 0 && aligned && cam.W == 128)
@@ -1073,8 +1077,8 @@ int nv_set_cast_mode(nv_ctx *c, int mode) {
 int nv_set_fill_mode(nv_ctx *c, int mode) {
   if (!c) return fail(NV_ERR_ARG, "ctx is NULL");
   c->gen++;
-  if (mode < 0 || mode > 3 || mode == 2)
-    return fail(NV_ERR_ARG, "fill mode must be 0 (direct), 1 (tma) or 3 (ws)");
+  if (mode < 0 || mode > 3)
+    return fail(NV_ERR_ARG, "fill mode must be 0 (direct), 1 (tma), 2 (ws) or 3 (auto)");
   c->fill_mode = mode;
   return NV_OK;
 }

@@ -203,7 +203,7 @@ def test_fill_paths_agree(nb, W, H):
     sim.reset(poses[:, :2], poses[:, 2])
     c, st = sim.ctx, nat.stream_handle("cuda:0")
     outs = []
-    for mode in (0, 1, 3):
+    for mode in (0, 1, 2, 3):
         nat.check(c.lib.nv_set_fill_mode(c.handle, mode))
         sim.render()
         torch.cuda.synchronize()

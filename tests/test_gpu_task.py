@@ -205,7 +205,7 @@ def test_depth_noise_moments_and_paths(nb):
     torch.cuda.synchronize()
     clean = sim.observations()["depth"].clone().double()
     outs = []
-    for mode in (3, 1, 0):
+    for mode in (2, 1, 0):
         nat.check(c.lib.nv_set_fill_mode(c.handle, mode))
         nat.check(c.lib.nv_depth_noise(c.handle, 0.4, 1234, 0))
         sim.render()
