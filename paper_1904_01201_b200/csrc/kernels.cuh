@@ -205,6 +205,9 @@ __device__ __forceinline__ void test_cell_f32(const SceneView &sc, int q0, int q
 #ifndef NV_CAST_CHUNKS
 #define NV_CAST_CHUNKS 1
 #endif
+#ifndef NV_CAST_NCB
+#define NV_CAST_NCB 4  // run boxes loaded per round
+#endif
 __device__ __forceinline__ void ray_grid(const SceneView &sc, double px, double py,
                                          double dx, double dy, double t_max,
                                          double &out_t, int &out_i) {
@@ -270,13 +273,36 @@ __device__ __forceinline__ void ray_grid(const SceneView &sc, double px, double 
       // s(x, y) = d x ((x, y) - p) is linear, so over a run's box it is
       // bounded by two corners; a run whose box lies beyond +-E on one side
       // holds no entry the per-entry side test would keep.
-      for (int q = rec.x, ch = rec.w; q < rec.y; q += NV_CHUNK, ++ch) {
-        const float4 b = __ldg(sc.chunks + ch);
-        const float smin = fmaf(dxf, pos_dx ? b.y : b.w, -(dyf * (pos_dy ? b.z : b.x))) - cf.cp;
-        const float smax = fmaf(dxf, pos_dx ? b.w : b.y, -(dyf * (pos_dy ? b.x : b.z))) - cf.cp;
-        if (smin > cf.E || smax < -cf.E) continue;
-        test_cell_f32<NV_CAST_NB>(sc, q, min(q + NV_CHUNK, rec.y), cf, px, py, dx, dy, dxf, dyf,
-                                  best_t, best_i);
+      // The boxes of up to NV_CAST_NCB runs are loaded together (one memory
+      // round trip per cell in the common case); a passing run's f64 entries
+      // are prefetched into L1 before its f32 side tests, so the exact tests
+      // of its survivors hit L1.
+      const int nch = (rec.y - rec.x + NV_CHUNK - 1) / NV_CHUNK;
+      for (int c0 = 0; c0 < nch; c0 += NV_CAST_NCB) {
+        float4 bb[NV_CAST_NCB];
+#pragma unroll
+        for (int k = 0; k < NV_CAST_NCB; ++k) bb[k] = __ldg(sc.chunks + rec.w + min(c0 + k, nch - 1));
+        unsigned pass = 0;
+#pragma unroll
+        for (int k = 0; k < NV_CAST_NCB; ++k) {
+          const float4 b = bb[k];
+          const float smin = fmaf(dxf, pos_dx ? b.y : b.w, -(dyf * (pos_dy ? b.z : b.x))) - cf.cp;
+          const float smax = fmaf(dxf, pos_dx ? b.w : b.y, -(dyf * (pos_dy ? b.x : b.z))) - cf.cp;
+          const bool ok = c0 + k < nch && !(smin > cf.E || smax < -cf.E);
+          pass |= (ok ? 1u : 0u) << k;
+        }
+        for (unsigned m = pass; m; m &= m - 1) {  // prefetch first, then test
+          const int q = rec.x + (c0 + __ffs(m) - 1) * NV_CHUNK;
+          const char *p = reinterpret_cast<const char *>(sc.ent + q);
+          asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+          asm volatile("prefetch.global.L1 [%0];" ::"l"(p + 128));
+        }
+        while (pass) {
+          const int q = rec.x + (c0 + __ffs(pass) - 1) * NV_CHUNK;
+          pass &= pass - 1;
+          test_cell_f32<NV_CAST_NB>(sc, q, min(q + NV_CHUNK, rec.y), cf, px, py, dx, dy, dxf,
+                                    dyf, best_t, best_i);
+        }
       }
 #else
       test_cell_f32<NV_CAST_NB>(sc, rec.x, rec.y, cf, px, py, dx, dy, dxf, dyf, best_t, best_i);

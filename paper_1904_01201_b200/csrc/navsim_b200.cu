@@ -403,14 +403,18 @@ unsigned blocks_for(long long work, int per_block) {
 
 // Fill work decomposition shared by k_fill_tma and the megakernel.
 template <int CPL>
-void fill_layout(nvk::FillArgs &a) {
+void fill_layout(nvk::FillArgs &a, int sm_count = 148) {
   a.segs_per_row = a.W / (32 * CPL);
   static const int rpu = [] {  // tuning knob (rows per work unit), default 16
     const char *e = getenv("NAVSIM_FILL_RPU");
     const int v = e ? atoi(e) : 0;
-    return v >= 2 && v <= 256 ? v : 16;
+    return v >= 2 && v <= 256 ? v : 0;
   }();
-  a.rows_per_unit = rpu;
+  // 16-row units, shortened (down to 2 rows) when a small batch would leave
+  // warps idle: aim for >= 4 units per SM
+  long long rows = (long long)a.N * a.segs_per_row * a.H;
+  int r = (int)std::min<long long>(16, std::max<long long>(2, rows / (4LL * sm_count)));
+  a.rows_per_unit = rpu ? rpu : (r & ~1);
   a.units_per_seg = (a.H + a.rows_per_unit - 1) / a.rows_per_unit;
   a.n_units = (long long)a.N * a.segs_per_row * a.units_per_seg;
 }
@@ -438,7 +442,7 @@ int launch_fill_tma(nv_ctx *c, nvk::FillArgs &a, cudaStream_t st) {
   int per_sm = 0;
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, warps * 32, smem));
   per_sm = std::max(1, per_sm);
-  fill_layout<CPL>(a);
+  fill_layout<CPL>(a, c->sm_count);
   long long want = (a.n_units + warps - 1) / warps;
   unsigned grid = (unsigned)std::max<long long>(1, std::min<long long>(want, (long long)per_sm * c->sm_count));
   Prof pf(c, st, 2);
@@ -538,7 +542,7 @@ int launch_fill_direct(nv_ctx *c, nvk::FillArgs &a, cudaStream_t st) {
   int per_sm = 0;
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, warps * 32, smem));
   per_sm = std::max(1, per_sm);
-  fill_layout<CPL>(a);
+  fill_layout<CPL>(a, c->sm_count);
   long long want = (a.n_units + warps - 1) / warps;
   unsigned grid = (unsigned)std::max<long long>(1, std::min<long long>(want, (long long)per_sm * c->sm_count));
   Prof pf(c, st, 2);
