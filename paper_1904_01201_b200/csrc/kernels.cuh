@@ -205,6 +205,9 @@ __device__ __forceinline__ void test_cell_f32(const SceneView &sc, int q0, int q
 #ifndef NV_CAST_CHUNKS
 #define NV_CAST_CHUNKS 1
 #endif
+#ifndef NV_CAST_PF_NEXT
+#define NV_CAST_PF_NEXT 0  // L1 prefetch of the next cell's runs (no gain measured)
+#endif
 #ifndef NV_CAST_NCB
 #define NV_CAST_NCB 4  // run boxes loaded per round
 #endif
@@ -309,6 +312,12 @@ __device__ __forceinline__ void ray_grid(const SceneView &sc, double px, double 
 #endif
     }
     if (best_t <= t_exit || t_exit > t_max) break;
+#if NV_CAST_PF_NEXT
+    if (nrec.y > nrec.x) {  // the next cell's run boxes and first entries -> L1
+      asm volatile("prefetch.global.L1 [%0];" ::"l"(sc.chunks + nrec.w));
+      asm volatile("prefetch.global.L1 [%0];" ::"l"(sc.entf + nrec.x));
+    }
+#endif
     cx = ncx;
     cy = ncy;
     tnx = ntnx;

@@ -723,8 +723,13 @@ int do_cast(nv_ctx *c, int cam, double *gps, double *compass, cudaStream_t st) {
                                                 k.cast_ctr.as<unsigned int>());
     return check_launch(c);
   }
+  static const int cast_block = [] {  // tuning knob: threads per cast CTA (32..128)
+    const char *e = getenv("NAVSIM_CAST_BLOCK");
+    const int v = e ? atoi(e) : 0;
+    return v == 32 || v == 64 || v == 96 || v == 128 ? v : 128;
+  }();
   Prof pf(c, st, 1);
-  nvk::k_column_cast<<<blocks_for(total, 128), 128, 0, st>>>(
+  nvk::k_column_cast<<<blocks_for(total, cast_block), cast_block, 0, st>>>(
       c->env_view(), c->scene_view(), cam_view(k), rec_out(k, c->n_envs), k.max_range, gps,
       compass);
   return check_launch(c);
