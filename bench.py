@@ -392,7 +392,7 @@ def run_gpu(args):
                        "triangles": sc.n_triangles, "parallelism": f"env-shard x{world}",
                        "cuda_graph": use_graph, "fused_megakernel": fused,
                        "fill_mode": {0: "direct-stores", 1: "per-warp-tma-stages", 2: "warp-specialised-tma", 3: "auto (warp-specialised-tma when envs >= SMs/2, else per-warp-tma-stages)"}.get(args.fill_mode),
-                       "cast_mode": ["dda", "binned", "dda-fused-with-agent-step"][args.cast_mode],
+                       "cast_mode": ["dda (thread per ray; warp per ray for <= 16384 rays)", "binned", "dda-fused-with-agent-step", "dda-thread-per-ray", "dda-warp-per-ray"][args.cast_mode],
                        "l2": f"no flush: frames written per step "
                              f"({step_bytes / 1e6:.0f} MB/GPU) exceed the 126 MB L2"},
             "roofline": {"bound": "hbm", "kernel": dom,
@@ -429,7 +429,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--fill-mode", type=int, default=3, help="0 direct stores, 1 per-warp TMA stages, 2 warp-specialised writer, 3 auto")
-    ap.add_argument("--cast-mode", type=int, default=0, help="0 per-column DDA, 1 binned, 2 DDA fused with the agent step")
+    ap.add_argument("--cast-mode", type=int, default=0, help="0 per-column DDA (auto), 1 binned, 2 DDA fused with the agent step, 3 thread/ray, 4 warp/ray")
     ap.add_argument("--fused", action="store_true", help="one megakernel launch per step (experimental)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -485,6 +485,7 @@ __device__ void warp_cast_disc(const SceneView &sc, double px, double py, double
   double u2 = add(mul(ux, ux), mul(uy, uy));
   double bt = NV_INF;
   int bi = 0x7fffffff;
+  double btx = 0.0, bty = 0.0;  // tangent of this lane's best
   // f32 prefilter on the cell-relative endpoints: any contact (face, band or
   // endpoint case of disc_cast) needs a point of the segment within `radius`
   // of a point of the sweep, so the segment's box must meet the sweep's box
@@ -553,7 +554,12 @@ __device__ void warp_cast_disc(const SceneView &sc, double px, double py, double
       for (int r = lane; r < nsurv; r += 32) {
         const DiscEntry d = sc.dent[sq[r]];
         const double t = disc_seg_t_pre(px, py, ux, uy, radius, u2, d);
-        lex_min(bt, bi, t, d.idx);
+        if (t < bt || (t == bt && d.idx < bi)) {
+          bt = t;
+          bi = d.idx;
+          btx = d.tx;
+          bty = d.ty;
+        }
       }
       __syncwarp();
     }
@@ -573,10 +579,17 @@ __device__ void warp_cast_disc(const SceneView &sc, double px, double py, double
             continue;
           const DiscEntry d = sc.dent[q];
           const double t = disc_seg_t_pre(px, py, ux, uy, radius, u2, d);
-          lex_min(bt, bi, t, d.idx);
+          if (t < bt || (t == bt && d.idx < bi)) {
+            bt = t;
+            bi = d.idx;
+            btx = d.tx;
+            bty = d.ty;
+          }
         }
       }
   }
+  const double lt = bt;
+  const int li = bi;
   warp_lex_min(bt, bi);
   if (!(bt < NV_INF) || bi == 0x7fffffff) {  // t is inf whenever nothing hit
     t_out = NV_INF;
@@ -585,11 +598,14 @@ __device__ void warp_cast_disc(const SceneView &sc, double px, double py, double
     tan_y = 0.0;
     return;
   }
-  // the winner's unit tangent (ex / seg_len, ey / seg_len), precomputed
+  // the winner's unit tangent (ex / seg_len, ey / seg_len, precomputed) from
+  // the lane that found it -- no memory round trip
+  const unsigned own = __ballot_sync(0xffffffffu, lt == bt && li == bi);
+  const int src = __ffs(own) - 1;
   t_out = bt;
   i_out = bi;
-  tan_x = __ldg(sc.stx + bi);
-  tan_y = __ldg(sc.sty + bi);
+  tan_x = __shfl_sync(0xffffffffu, btx, src);
+  tan_y = __shfl_sync(0xffffffffu, bty, src);
 }
 
 // min_seg_distance (_kernels.py:468-493), one segment.
@@ -887,6 +903,129 @@ __device__ __forceinline__ void cast_column(const EnvView &ev, const SceneView &
       const double h = COH ? __ldcg(ev.h + e) : ev.h[e];
       compass[e] = nvx::wrap_angle(sub(h, ev.oh[e]));
     }
+  }
+}
+
+// raycast_grid for one ray by a whole warp (small batches: latency, not
+// throughput).  Every lane walks the same DDA (uniform control flow, the
+// reference's visit order and early-out); a cell's entries are spread over
+// the lanes (f32 side test, then the exact FP64 test), and the warp keeps the
+// lexicographic (t, idx) minimum.  Returns the result in every lane.
+__device__ __forceinline__ void ray_grid_warp(const SceneView &sc, double px, double py,
+                                              double dx, double dy, double t_max, double &out_t,
+                                              int &out_i) {
+  const int lane = threadIdx.x & 31;
+  const double cell = 1.0;
+  double best_t = NV_INF;
+  int best_i = -1;
+  if (isnan(px) || isnan(py) || isnan(dx) || isnan(dy)) {
+    out_t = best_t;
+    out_i = best_i;
+    return;
+  }
+  long long cx = (long long)floor(sub(px, sc.x0));
+  long long cy = (long long)floor(sub(py, sc.y0));
+  const int stepx = dx > 0.0 ? 1 : -1;
+  const int stepy = dy > 0.0 ? 1 : -1;
+  double tnx, tdx, tny, tdy;
+  if (dx != 0.0) {
+    double nbx = add(sc.x0, mul((double)(cx + (dx > 0.0 ? 1 : 0)), cell));
+    tnx = div(sub(nbx, px), dx);
+    tdx = fabs(div(cell, dx));
+  } else {
+    tnx = NV_INF;
+    tdx = NV_INF;
+  }
+  if (dy != 0.0) {
+    double nby = add(sc.y0, mul((double)(cy + (dy > 0.0 ? 1 : 0)), cell));
+    tny = div(sub(nby, py), dy);
+    tdy = fabs(div(cell, dy));
+  } else {
+    tny = NV_INF;
+    tdy = NV_INF;
+  }
+  const long long gnx = sc.gnx, gny = sc.gny;
+  const float dxf = (float)dx, dyf = (float)dy;
+  const float sd = (fabsf(dxf) + fabsf(dyf)) * (1.0f + 0x1p-20f);
+  for (int guard = 0; guard < (1 << 24); ++guard) {
+    if (0 <= cx && cx < gnx && 0 <= cy && cy < gny) {
+      const int4 rec = __ldg(sc.cells + (cy * gnx + cx));
+      if (rec.y > rec.x) {
+        const double X0 = add(sc.x0, (double)cx), Y0 = add(sc.y0, (double)cy);
+        const float pxr = (float)sub(px, X0), pyr = (float)sub(py, Y0);
+        const float cp = fmaf(dxf, pyr, -(dyf * pxr));
+        const float E = NV_K32 * sd * (__int_as_float(rec.z) + fabsf(pxr) + fabsf(pyr) + 1e-30f);
+        for (int q = rec.x + lane; q < rec.y; q += 32) {
+          const float4 e = __ldg(sc.entf + q);
+          const float sa = fmaf(dxf, e.y, -(dyf * e.x)) - cp;
+          const float sb = fmaf(dxf, e.w, -(dyf * e.z)) - cp;
+          if (fminf(sa, sb) > E || fmaxf(sa, sb) < -E) continue;
+          const double2 *p2 = reinterpret_cast<const double2 *>(sc.ent + q);
+          const double2 a2 = __ldg(p2), e2 = __ldg(p2 + 1);
+          double den, tn, rn;
+          if (seg_pre(px, py, dx, dy, a2.x, a2.y, e2.x, e2.y, best_t, den, tn, rn))
+            seg_exact(den, tn, rn, __ldg(sc.items + q), best_t, best_i);
+        }
+        // the lexicographic minimum is order-free: combine the lanes
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          const double t2 = __shfl_xor_sync(0xffffffffu, best_t, o);
+          const int i2 = __shfl_xor_sync(0xffffffffu, best_i, o);
+          if (t2 < best_t || (t2 == best_t && (unsigned)i2 < (unsigned)best_i)) {
+            best_t = t2;
+            best_i = i2;
+          }
+        }
+      }
+    }
+    const double t_exit = tnx < tny ? tnx : tny;
+    if (best_t <= t_exit || t_exit > t_max) break;
+    if (tnx < tny) {
+      cx += stepx;
+      tnx = add(tnx, tdx);
+    } else {
+      cy += stepy;
+      tny = add(tny, tdy);
+    }
+    if (cx < 0 || cx >= gnx || cy < 0 || cy >= gny) {
+      bool out_x = (cx < 0 && dx <= 0.0) || (cx >= gnx && dx >= 0.0);
+      bool out_y = (cy < 0 && dy <= 0.0) || (cy >= gny && dy >= 0.0);
+      if (out_x || out_y) break;
+    }
+  }
+  out_t = best_t;
+  out_i = best_i;
+}
+
+// One warp per (env, column): the latency-bound small-batch cast.
+__global__ void __launch_bounds__(128) k_column_cast_warp(EnvView ev, SceneView sc, CamView cam,
+                                                          RecOut ro, double t_max, double *gps,
+                                                          double *compass) {
+  const long long g = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const long long total = (long long)ev.n * cam.W;
+  if (g >= total) return;
+  const int lane = threadIdx.x & 31;
+  const int e = (int)(g / cam.W);
+  const int j = (int)(g - (long long)e * cam.W);
+  const double px = ev.x[e], py = ev.y[e], c = ev.ch[e], s = ev.sh[e];
+  const double u = __ldg(cam.u + j);
+  const double dx = add(c, mul(u, s));
+  const double dy = add(s, mul(u, -c));
+  double t;
+  int k;
+  ray_grid_warp(sc, px, py, dx, dy, t_max, t, k);
+  if (lane != 0) return;
+  ColRec r;
+  column_epilogue(sc, cam, t, k, dx, dy, r);
+  put_rec(ro, e, j, r);
+  if (j == 0 && (gps || compass)) {
+    double ddx = sub(px, ev.ox[e]), ddy = sub(py, ev.oy[e]);
+    double fc = ev.fc[e], fs = ev.fs[e];
+    if (gps) {
+      gps[2 * e] = sub(mul(fc, ddx), mul(fs, ddy));
+      gps[2 * e + 1] = add(mul(fs, ddx), mul(fc, ddy));
+    }
+    if (compass) compass[e] = nvx::wrap_angle(sub(ev.h[e], ev.oh[e]));
   }
 }
 

@@ -723,6 +723,18 @@ int do_cast(nv_ctx *c, int cam, double *gps, double *compass, cudaStream_t st) {
                                                 k.cast_ctr.as<unsigned int>());
     return check_launch(c);
   }
+  // small batches (rays fit in about one wave of warps): one warp per ray
+  static const long long warp_rays = [] {
+    const char *e = getenv("NAVSIM_CAST_WARP_RAYS");
+    return e ? atoll(e) : 16384LL;
+  }();
+  if (c->cast_mode == 4 || (c->cast_mode == 0 && total <= warp_rays)) {
+    Prof pf(c, st, 1);
+    nvk::k_column_cast_warp<<<blocks_for(total * 32, 128), 128, 0, st>>>(
+        c->env_view(), c->scene_view(), cam_view(k), rec_out(k, c->n_envs), k.max_range, gps,
+        compass);
+    return check_launch(c);
+  }
   static const int cast_block = [] {  // tuning knob: threads per cast CTA (32..128)
     const char *e = getenv("NAVSIM_CAST_BLOCK");
     const int v = e ? atoi(e) : 0;
@@ -736,8 +748,9 @@ int do_cast(nv_ctx *c, int cam, double *gps, double *compass, cudaStream_t st) {
 }
 
 int nv_set_cast_mode_(nv_ctx *c, int mode) {
-  if (mode < 0 || mode > 2)
-    return fail(NV_ERR_ARG, "cast mode must be 0 (dda), 1 (binned) or 2 (dda fused with the step)");
+  if (mode < 0 || mode > 4)
+    return fail(NV_ERR_ARG, "cast mode must be 0 (dda, auto), 1 (binned), 2 (dda fused with the "
+                            "step), 3 (dda, thread per ray) or 4 (dda, warp per ray)");
   c->cast_mode = mode;
   return NV_OK;
 }

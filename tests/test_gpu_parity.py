@@ -151,15 +151,18 @@ def _oracle_scene(oracle, sc):
     ("C3", 256, 256, 8, 6),        # TMA path W=256, ~100k segments
     ("C1", 40, 33, 8, 20),         # generic path, odd H
 ])
-def test_batch_step_render_vs_oracle(nb, oracle_mod, cfg, W, H, n_envs, steps):
+@pytest.mark.parametrize("cast_mode", [0, 3])  # warp per ray (small batch), thread per ray
+def test_batch_step_render_vs_oracle(nb, oracle_mod, cfg, W, H, n_envs, steps, cast_mode):
     """Batched step+render (device cos/sin, device DDA, TMA fill) vs the oracle
     run on the same actions: poses 1e-6, frames at the stated tolerances."""
+    from paper_1904_01201_b200 import _native as nat
     from paper_1904_01201_b200 import synth
     sc = synth.config_scene(cfg)
     suite = (nb.SensorConfig("rgb", W, H), nb.SensorConfig("depth", W, H),
              nb.SensorConfig("semantic", W, H), nb.SensorConfig("gps_compass"))
     sim = nb.BatchSimulator(sc.segments, sc.semantic_ids, sc.albedo, n_envs, sensor_configs=suite,
                             floor_color=sc.floor_color, ceiling_color=sc.ceiling_color)
+    nat.check(sim.ctx.lib.nv_set_cast_mode(sim.ctx.handle, cast_mode))
     poses = synth.sample_poses(sc, n_envs, seed=17)
     sim.reset(poses[:, :2], poses[:, 2])
     acts = synth.random_actions(n_envs, steps, seed=5)
@@ -373,8 +376,8 @@ def test_blind_and_gps_only(nb):
 @pytest.mark.parametrize("cfg,W,H,n", [("C1", 256, 64, 32), ("C2", 128, 64, 32), ("C3", 256, 32, 64),
                                        ("C1", 40, 33, 16)])
 def test_cast_modes_agree(nb, cfg, W, H, n):
-    """Binned column cast (default) and the per-column DDA give identical
-    frames (the reference's raycast_grid == raycast_all contract), including
+    """Binned column cast and the per-column DDA (thread and warp per ray) give
+    identical frames (the reference's raycast_grid == raycast_all contract), including
     the 1000-piece room whose shared endpoints exercise the (t, idx) tie rule."""
     from paper_1904_01201_b200 import _native as nat
     from paper_1904_01201_b200 import synth
@@ -390,15 +393,16 @@ def test_cast_modes_agree(nb, cfg, W, H, n):
     for s in range(acts.shape[0]):
         sim.step(acts[s], render=False)
         outs = []
-        for mode in (0, 1):
+        for mode in (0, 1, 3, 4):
             nat.check(c.lib.nv_set_cast_mode(c.handle, mode))
             sim.render()
             torch.cuda.synchronize()
             outs.append({k: v.clone() for k, v in sim.observations().items()})
-        assert torch.equal(outs[0]["semantic"].view(torch.int16), outs[1]["semantic"].view(torch.int16))
-        assert torch.equal(outs[0]["depth"], outs[1]["depth"])
-        assert torch.equal(outs[0]["rgb"], outs[1]["rgb"])
-        assert torch.equal(outs[0]["gps"], outs[1]["gps"])
+        for o in outs[1:]:
+            assert torch.equal(outs[0]["semantic"].view(torch.int16), o["semantic"].view(torch.int16))
+            assert torch.equal(outs[0]["depth"], o["depth"])
+            assert torch.equal(outs[0]["rgb"], o["rgb"])
+            assert torch.equal(outs[0]["gps"], o["gps"])
 
 
 @pytest.mark.parametrize("cfg,W,H,n", [("C1", 256, 64, 24), ("C2", 128, 64, 32), ("C1", 40, 33, 16)])
