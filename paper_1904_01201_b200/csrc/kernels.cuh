@@ -2119,6 +2119,8 @@ __global__ void __launch_bounds__(128) k_fill_direct(FillArgs a) {
 struct FillWsLayout {  // byte offsets into dynamic shared memory + ring geometry
   int rows, inv, cols, bars, slots;
   int slot_bytes, nslot, slot_rows;
+  int depth_direct;  // 1: producers store depth straight from registers (STG),
+                     // the slots carry RGB / semantic only
 };
 
 template <int CPL, bool TAB, int RPW, bool NOISE>
@@ -2138,8 +2140,9 @@ __global__ void __launch_bounds__(544, 1) k_fill_ws(FillArgs a, FillWsLayout L) 
   uint8_t *slots = smem + L.slots;
   const unsigned plane_bytes = (unsigned)W * 16u;
   const bool want_rgb = a.rgb != nullptr, want_d = a.depth != nullptr, want_s = a.sem != nullptr;
+  const bool slot_d = want_d && !L.depth_direct;
   const int off_d = want_rgb ? R * W * 3 : 0;
-  const int off_s = off_d + (want_d ? R * W * 4 : 0);
+  const int off_s = off_d + (slot_d ? R * W * 4 : 0);
   const int slots_per_item = H / R;
   if (threadIdx.x == 0) {
     for (int k = 0; k < NSLOT; ++k) {
@@ -2190,7 +2193,7 @@ __global__ void __launch_bounds__(544, 1) k_fill_ws(FillArgs a, FillWsLayout L) 
         const size_t pix0 = ((size_t)e * H + (size_t)sl * R) * W;
 #if NV_WS_DEBUG != 2
         if (want_rgb) bulk_store(a.rgb + pix0 * 3, buf, (unsigned)(R * W * 3), pol);
-        if (want_d) bulk_store(a.depth + pix0, buf + off_d, (unsigned)(R * W * 4), pol);
+        if (slot_d) bulk_store(a.depth + pix0, buf + off_d, (unsigned)(R * W * 4), pol);
         if (want_s) bulk_store(a.sem + pix0, buf + off_s, (unsigned)(R * W * 2), pol);
 #else
         (void)buf; (void)pix0; (void)pol;
@@ -2211,6 +2214,7 @@ __global__ void __launch_bounds__(544, 1) k_fill_ws(FillArgs a, FillWsLayout L) 
     return;
   }
   // -------------------------------------------------------------- producers
+  const uint64_t dpol = policy_evict_first();
   const int seg = warp % S;
   const int rsub = warp / S;   // first row of this warp within a slot
   const int rstride = nw / S;  // row stride between the warp's RPW rows
@@ -2253,9 +2257,24 @@ __global__ void __launch_bounds__(544, 1) k_fill_ws(FillArgs a, FillWsLayout L) 
           }
         }
         put_row<CPL>(po, want_rgb ? buf : nullptr,
-                     want_d ? reinterpret_cast<float *>(buf + off_d) : nullptr,
+                     slot_d ? reinterpret_cast<float *>(buf + off_d) : nullptr,
                      want_s ? reinterpret_cast<uint16_t *>(buf + off_s) : nullptr,
                      rs * W + seg * Ln::SEGW, lane);
+        if (want_d && !slot_d) {  // depth straight to HBM: 16 B per lane, coalesced
+          float *drow = a.depth + ((size_t)e * H + i) * W + seg * Ln::SEGW;
+#pragma unroll
+          for (int g = 0; g < Ln::G; ++g) {
+            float *dp = drow + g * 32 * Ln::GW + lane * Ln::GW;
+            if constexpr (Ln::GW == 4) {
+              const PairOut &p = po[2 * g], &q = po[2 * g + 1];
+              asm volatile("st.global.L2::cache_hint.v4.f32 [%0], {%1,%2,%3,%4}, %5;" ::"l"(dp),
+                           "f"(p.d0), "f"(p.d1), "f"(q.d0), "f"(q.d1), "l"(dpol)
+                           : "memory");
+            } else {
+              *reinterpret_cast<float2 *>(dp) = make_float2(po[g].d0, po[g].d1);
+            }
+          }
+        }
       }
       fence_proxy_async();
       __syncwarp();

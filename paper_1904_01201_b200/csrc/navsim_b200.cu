@@ -574,7 +574,12 @@ int launch_fill_ws(nv_ctx *c, nvk::FillArgs &a, cudaStream_t st) {
   const int segw = 32 * CPL;
   const int S = a.W / segw;
   const int nw = 16;
-  const int bpp = (a.rgb ? 3 : 0) + (a.depth ? 4 : 0) + (a.sem ? 2 : 0);
+  static const int depth_direct = [] {  // tuning knob: depth by STG instead of the slots
+    const char *e = getenv("NAVSIM_WS_DEPTH_DIRECT");
+    return e ? atoi(e) : 0;
+  }();
+  const bool dd = depth_direct && a.depth;
+  const int bpp = (a.rgb ? 3 : 0) + (a.depth && !dd ? 4 : 0) + (a.sem ? 2 : 0);
   auto up = [](size_t x) { return (x + 127) & ~(size_t)127; };
   if (nw % S) return fail(NV_ERR_ARG, "frame layout unsupported by ws fill");
   const size_t rows_b = up((size_t)a.H * sizeof(RowRec));
@@ -611,6 +616,7 @@ int launch_fill_ws(nv_ctx *c, nvk::FillArgs &a, cudaStream_t st) {
   L.cols = L.inv + (tab ? (int)inv_b : 0);
   L.bars = L.cols + (int)cols_b;
   L.slots = L.bars + (int)bars_b;
+  L.depth_direct = dd ? 1 : 0;
   a.segs_per_row = S;
   if (tab && rpw == 2) return launch_ws_kernel<CPL, true, 2>(c, a, L, smem, st);
   if (tab) return launch_ws_kernel<CPL, true, 1>(c, a, L, smem, st);

@@ -74,12 +74,11 @@ def test_c3_fullsize(nb, oracle_mod):
         has = band.any(dim=1)
         assert bool((dmax[has] == dmin[has]).all())
         # plane pixels: the row's plane depth is the same for every env/column
-        ceil_d = torch.where(ceil, dep, torch.zeros_like(dep))
-        cnt = ceil.sum(dim=(0, 2)).clamp(min=1)
-        row_mean = ceil_d.sum(dim=(0, 2)) / cnt
-        row_max = torch.where(ceil, dep, torch.full_like(dep, -1.0)).amax(dim=(0, 2))
-        rows = ceil.any(dim=2).any(dim=0)
-        assert bool((row_mean[rows] == row_max[rows]).all())
+        for plane in (ceil, floor):
+            row_max = torch.where(plane, dep, torch.full_like(dep, -1.0)).amax(dim=(0, 2))
+            row_min = torch.where(plane, dep, torch.full_like(dep, 1e9)).amin(dim=(0, 2))
+            rows = plane.any(dim=2).any(dim=0)
+            assert bool((row_min[rows] == row_max[rows]).all())
         # --- sampled envs vs the oracle
         rgb_h, dep_h, sem_h = obs["rgb"].cpu().numpy(), dep.cpu().numpy(), \
             obs["semantic"].cpu().numpy()
