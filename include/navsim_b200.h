@@ -290,6 +290,22 @@ int nv_task_state(nv_ctx *ctx, int32_t *steps, uint8_t *done, double *d_last, vo
  * not reproducible on the device: parity is the reference's moment test. */
 int nv_depth_noise(nv_ctx *ctx, double sigma, uint64_t seed, int64_t env_offset);
 
+/* ---- frame codecs ------------------------------------ */
+
+/* sensors.depth_to_png / rgb_to_png / semantic_to_png (sensors.py:211-246),
+ * batched on the device: kind 0 = depth (16-bit gray, round(d / max_range *
+ * 65535) clipped), 1 = RGB (8-bit, round(rgb * 255) clipped; u8 input passes
+ * through), 2 = semantic (16-bit gray).  frames: DEVICE [n, H, W(, 3)] of f32
+ * depth / u8 rgb / u16 semantic, or the reference's f64 arrays with src_f64.
+ * out: DEVICE n x stride bytes, each a complete PNG of nv_png_size(kind, W, H)
+ * bytes (zlib stored blocks: any PNG decoder returns exactly the quantised
+ * samples; Adler-32 and CRC-32 computed on the device).  Asynchronous. */
+int64_t nv_png_size(int kind, int width, int height);
+int nv_png_encode(int kind, int src_f64, const void *frames, int64_t n, int width, int height,
+                  double max_range, uint8_t *out, int64_t stride, void *stream);
+/* Host restatement of the device's chunked CRC-32 combination (tests). */
+uint32_t nv_host_crc32_chunked(const uint8_t *p, int64_t len, int chunks);
+
 #ifdef __cplusplus
 }
 #endif

@@ -21,6 +21,7 @@
 #include "exact_math.cuh"
 #include "kernels.cuh"
 #include "nav.cuh"
+#include "codec.cuh"
 
 using namespace nvd;
 
@@ -1365,3 +1366,4 @@ int nv_profile_read(nv_ctx *c, double *ms, int64_t *counts) {
 }  // extern "C"
 
 #include "nav_task_abi.inc"
+#include "codec_abi.inc"

@@ -214,3 +214,82 @@ class EpisodeFrame:
 def gps_compass(state, frame: EpisodeFrame):
     """Idealised GPS + compass in the episode frame (sensors.py:175-180)."""
     return frame.to_frame(state.position), wrap_angle(state.heading - frame.heading)
+
+
+# ---------------------------------------------------------------------------
+# frame codecs (sensors.py:211-246): PNG encoding on the device, one complete
+# PNG per frame (nv_png_encode: quantisation, scanlines, zlib stored blocks,
+# Adler-32 and CRC-32 on the GPU); decoding is the consumer's side (PIL).
+
+PNG_DEPTH, PNG_RGB, PNG_SEMANTIC = 0, 1, 2
+
+
+def encode_frames(frames, kind: int, max_range: float = 10.0, stream=None):
+    """PNG-encode a batch of frames on the GPU.  ``frames``: a CUDA tensor
+    [n, H, W] (depth f32/f64, semantic u16) or [n, H, W, 3] (rgb u8/f64).
+    Returns (out u8 CUDA tensor [n, size], size): row k is frame k's PNG."""
+    import torch
+    from . import _native as nat
+    if not (isinstance(frames, torch.Tensor) and frames.is_cuda):
+        raise SensorError("frames must be a CUDA tensor")
+    f = frames.contiguous()
+    n, H, W = int(f.shape[0]), int(f.shape[1]), int(f.shape[2])
+    src_f64 = 1 if f.dtype == torch.float64 else 0
+    want = {PNG_DEPTH: (torch.float32, torch.float64), PNG_RGB: (torch.uint8, torch.float64),
+            PNG_SEMANTIC: (torch.uint16, torch.int16)}[kind]
+    if f.dtype not in want:
+        raise SensorError(f"frames of kind {kind} must be {want}, got {f.dtype}")
+    lib = nat.load()
+    size = int(lib.nv_png_size(kind, W, H))
+    out = torch.empty((n, size), dtype=torch.uint8, device=f.device)
+    st = nat.stream_handle(f.device) if stream is None else stream
+    nat.check(lib.nv_png_encode(kind, src_f64, nat.ptr(f), n, W, H, float(max_range),
+                                nat.ptr(out), size, st))
+    return out, size
+
+
+def _encode_one(arr, kind, max_range=10.0) -> bytes:
+    import torch
+    t = torch.as_tensor(np.ascontiguousarray(arr))[None].to("cuda")
+    out, size = encode_frames(t, kind, max_range)
+    return bytes(out[0].cpu().numpy().tobytes())
+
+
+def depth_to_png(depth: np.ndarray, max_range: float = 10.0) -> bytes:
+    """16-bit grayscale PNG; meters scale linearly so max_range -> 65535."""
+    d = np.asarray(depth)
+    if d.dtype != np.float32:
+        d = d.astype(np.float64)
+    return _encode_one(d, PNG_DEPTH, max_range)
+
+
+def rgb_to_png(rgb: np.ndarray) -> bytes:
+    r = np.asarray(rgb)
+    if r.dtype != np.uint8:
+        r = r.astype(np.float64)
+    return _encode_one(r, PNG_RGB)
+
+
+def semantic_to_png(semantic: np.ndarray) -> bytes:
+    return _encode_one(np.asarray(semantic, dtype=np.uint16), PNG_SEMANTIC)
+
+
+def png_to_depth(data: bytes, max_range: float = 10.0) -> np.ndarray:
+    import io
+    from PIL import Image
+    arr = np.asarray(Image.open(io.BytesIO(data)), dtype=np.uint16)
+    return arr.astype(np.float64) / 65535.0 * max_range
+
+
+def png_to_rgb(data: bytes) -> np.ndarray:
+    import io
+    from PIL import Image
+    arr = np.asarray(Image.open(io.BytesIO(data)).convert("RGB"), dtype=np.uint8)
+    return arr.astype(np.float64) / 255.0
+
+
+def png_to_semantic(data: bytes) -> np.ndarray:
+    import io
+    from PIL import Image
+    return np.asarray(Image.open(io.BytesIO(data)), dtype=np.uint16)
+

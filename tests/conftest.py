@@ -18,7 +18,7 @@ def pytest_configure(config):
 def golden_names():
     return sorted(os.path.basename(p)[len("golden_"):-len(".npz")]
                   for p in glob.glob(os.path.join(GOLDEN_DIR, "golden_*.npz"))
-                  if not os.path.basename(p).startswith("golden_task_"))
+                  if not os.path.basename(p).startswith(("golden_task_", "golden_codec")))
 
 
 def load_golden(name):

@@ -100,3 +100,19 @@ def test_env_shards_partition():
         for a, b in zip(shards, shards[1:]):
             assert a.hi == b.lo
         assert sum(s.n_local for s in shards) == n
+
+
+def test_chunked_crc32_matches_zlib():
+    """The device PNG encoder's CRC-32 (per-chunk raw CRCs shifted by
+    x^(8 * bytes after) mod P, then XOR-combined) equals zlib.crc32; checked
+    through the host restatement exported by the library."""
+    import ctypes
+    import zlib
+    from paper_1904_01201_b200 import _native
+    lib = _native.load()
+    rng = np.random.default_rng(1)
+    for n in (0, 1, 7, 4096, 131333):
+        b = rng.integers(0, 256, n).astype(np.uint8)
+        for chunks in (1, 5, 256):
+            got = lib.nv_host_crc32_chunked(b.ctypes.data_as(ctypes.c_void_p), n, chunks)
+            assert got == zlib.crc32(b.tobytes())
