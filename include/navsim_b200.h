@@ -273,6 +273,16 @@ int nv_task_reset(nv_ctx *ctx, const double *goal, const double *gdsp, const int
  * steps report NV_ENV_DONE until the next nv_task_reset. */
 int nv_task_step(nv_ctx *ctx, const int8_t *actions, const int32_t *status, double *reward,
                  double *dist, uint8_t *done, void *outcome, void *stream);
+/* nv_step_render + nv_task_step in one call: the agent step and the task
+ * arithmetic run in one kernel (a warp per env; the line-of-sight ray of
+ * Environment._distance_to_goal is cast by the warp), then the column cast
+ * and the frame fill.  Outputs as in nv_step_render and nv_task_step (the
+ * step status is optional here). */
+int nv_task_step_render(nv_ctx *ctx, const int8_t *actions, int cam, uint8_t *rgb,
+                        float *depth, uint16_t *sem, double *gps, double *compass,
+                        uint8_t *collided, double *displacement, int32_t *status,
+                        double *reward, double *dist, uint8_t *done, void *outcome,
+                        void *stream);
 /* Task state (any pointer may be NULL; host or device memory): steps i32[n],
  * done u8[n], last distance f64[n]. */
 int nv_task_state(nv_ctx *ctx, int32_t *steps, uint8_t *done, double *d_last, void *stream);

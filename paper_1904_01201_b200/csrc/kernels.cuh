@@ -722,10 +722,17 @@ __device__ void warp_forward(const SceneView &sc, const AgentCfg &cfg, double &x
 }
 
 // Simulator.step (sim.py:202-219) for env e, executed by one warp.
+// Post-step agent values, identical in every lane (for fused consumers).
+struct AgentPost {
+  double x, y, path;
+  long long coll;
+  int status;
+};
+
 __device__ __forceinline__ void warp_agent_step(const EnvView &ev, const SceneView &sc,
                                                 const AgentCfg &cfg, int e, int a,
                                                 uint8_t *collided_out, double *disp_out,
-                                                int32_t *status_out) {
+                                                int32_t *status_out, AgentPost *post = nullptr) {
   const int lane = threadIdx.x & 31;
   int status = 0, collided = 0;
   double moved = 0.0;
@@ -733,6 +740,7 @@ __device__ __forceinline__ void warp_agent_step(const EnvView &ev, const SceneVi
   const uint8_t was_reset = ev.reset[e];
   double x = ev.x[e], y = ev.y[e], h0 = ev.h[e], ch = ev.ch[e], sh = ev.sh[e];
   const double path = ev.path[e];
+  const long long coll0 = ev.coll[e];
   if (!was_reset) {
     status = 2;  // NV_ENV_NOT_RESET
   } else if (ev.frozen && ev.frozen[e]) {
@@ -743,7 +751,7 @@ __device__ __forceinline__ void warp_agent_step(const EnvView &ev, const SceneVi
       ev.x[e] = x;
       ev.y[e] = y;
       ev.path[e] = add(path, moved);
-      ev.coll[e] += collided;
+      ev.coll[e] = coll0 + collided;
     }
   } else if (a == 1 || a == 2) {
     // apply_turn (sim.py:83-87): wrap(h + sign * radians(turn)); +-x is exact
@@ -762,6 +770,13 @@ __device__ __forceinline__ void warp_agent_step(const EnvView &ev, const SceneVi
     if (collided_out) collided_out[e] = (uint8_t)collided;
     if (disp_out) disp_out[e] = moved;
     if (status_out) status_out[e] = status;
+  }
+  if (post) {
+    post->x = x;
+    post->y = y;
+    post->path = status == 0 && a == 0 ? add(path, moved) : path;
+    post->coll = coll0 + collided;
+    post->status = status;
   }
 }
 

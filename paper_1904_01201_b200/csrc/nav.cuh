@@ -420,6 +420,82 @@ __global__ void k_task_step(EnvView ev, SceneView sc, NavView nv, TaskView tv,
   if (done_out) done_out[e] = tv.done[e];
 }
 
+// Environment._distance_to_goal by a whole warp (the line-of-sight ray uses
+// the warp DDA); the result is identical in every lane.
+__device__ __forceinline__ double distance_to_goal_warp(const SceneView &sc, const NavView &nv,
+                                                        const TaskView &tv, int e, double px,
+                                                        double py) {
+  const double gx = tv.goal[2 * e], gy = tv.goal[2 * e + 1];
+  const double dx = sub(gx, px), dy = sub(gy, py);
+  const double euclid = nvx::hypot_cr(dx, dy);
+  if (euclid <= 1.0) {
+    if (euclid < 1e-12) return 0.0;
+    double t;
+    int k;
+    ray_grid_warp(sc, px, py, dx, dy, 1e9, t, k);
+    if (!(t <= 1.0)) return euclid;
+  }
+  return geodesic_at(tv.fields + (size_t)tv.fid[e] * nv.nx * nv.ny, nv, px, py);
+}
+
+// Simulator.step + Environment.step's task arithmetic in one warp per env
+// (nv_task_step_render): the agent step, then -- for stepped envs -- the
+// distance to the goal at the new pose, reward, termination and outcome,
+// with no second launch and no re-read of the agent state.
+__global__ void __launch_bounds__(128) k_agent_task_step(EnvView ev, SceneView sc, AgentCfg cfg,
+                                                         const int8_t *__restrict__ actions,
+                                                         uint8_t *collided_out, double *disp_out,
+                                                         int32_t *status_out, NavView nv,
+                                                         TaskView tv, double *reward,
+                                                         double *dist, uint8_t *done_out,
+                                                         OutcomeRec *out) {
+  const int e = (int)((blockIdx.x * (size_t)blockDim.x + threadIdx.x) >> 5);
+  if (e >= ev.n) return;
+  const int lane = threadIdx.x & 31;
+  const int a = actions[e];
+  AgentPost post;
+  warp_agent_step(ev, sc, cfg, e, a, collided_out, disp_out, status_out, &post);
+  if (post.status != 0) {
+    if (lane == 0 && done_out) done_out[e] = tv.done[e];
+    return;
+  }
+  const double d_cur = distance_to_goal_warp(sc, nv, tv, e, post.x, post.y);
+  if (lane != 0) return;
+  const int steps = tv.steps[e] + 1;
+  tv.steps[e] = steps;
+  const double d_prev = tv.d_last[e];
+  tv.d_last[e] = d_cur;
+  int term = 0;
+  bool success = false;
+  if (a == 3) {
+    term = 1;
+    success = d_cur <= tv.success_radius;
+  } else if (steps >= tv.max_steps) {
+    term = 2;
+  }
+  const double base = add(sub(d_prev, d_cur), tv.step_penalty);
+  if (reward) reward[e] = term && success ? add(base, tv.success_reward) : base;
+  if (dist) dist[e] = d_cur;
+  if (term) {
+    tv.done[e] = 1;
+    if (out) {
+      OutcomeRec o;
+      o.success = success;
+      o.terminated_by = (uint8_t)term;
+      o.pad[0] = o.pad[1] = 0;
+      o.steps = steps;
+      o.collisions = (int32_t)post.coll;
+      o.pad2 = 0;
+      o.path_taken = post.path;
+      o.shortest_path = tv.gdsp[e];
+      const double sh = o.shortest_path, tk = o.path_taken;
+      o.spl = success ? div(sh, tk > sh ? tk : sh) : 0.0;
+      out[e] = o;
+    }
+  }
+  if (done_out) done_out[e] = tv.done[e];
+}
+
 // Environment.reset's initial distance (task.py:188) for masked envs.
 __global__ void k_task_reset(EnvView ev, SceneView sc, NavView nv, TaskView tv,
                              const uint8_t *mask) {

@@ -162,6 +162,7 @@ class BatchEnvironment:
         nat.check(c.lib.nv_task_config(c.handle, int(max_steps), SUCCESS_RADIUS,
                                        float(reward_params.success_reward),
                                        float(reward_params.step_penalty)))
+        self.fused_task = True             # agent + task step in one kernel (nv_task_step_render)
         N = self.n_envs
         self.fields = None                 # f64[k, h, w] device fields, one per goal cell
         self._field_of: dict = {}          # goal cell -> field index (FieldCache)
@@ -264,12 +265,28 @@ class BatchEnvironment:
         action codes.  Returns (observations, done, info) as device tensors;
         info["outcome"] holds the 40-byte EpisodeOutcome records (valid for
         envs that terminated).  Finished envs stay frozen until reset."""
-        self.sim.step(actions, render=True, stream=stream)
         c = self.sim.ctx
         st = nat.stream_handle(self.dev) if stream is None else stream
-        nat.check(c.lib.nv_task_step(c.handle, nat.ptr(actions), nat.ptr(self.sim.status),
-                                     nat.ptr(self.reward), nat.ptr(self.dist), nat.ptr(self.done),
-                                     nat.ptr(self.outcome), st))
+        sim = self.sim
+        if sim.groups and self.fused_task:
+            # one call: agent step + task arithmetic (one kernel), cast, fill
+            g0 = sim.groups[0]
+            gps = nat.ptr(sim.gps) if sim.want_gps else None
+            comp = nat.ptr(sim.compass) if sim.want_gps else None
+            nat.check(c.lib.nv_task_step_render(
+                c.handle, nat.ptr(actions), g0["cam"], nat.ptr(g0["rgb"]), nat.ptr(g0["depth"]),
+                nat.ptr(g0["semantic"]), gps, comp, nat.ptr(sim.collided),
+                nat.ptr(sim.displacement), nat.ptr(sim.status), nat.ptr(self.reward),
+                nat.ptr(self.dist), nat.ptr(self.done), nat.ptr(self.outcome), st))
+            for g in sim.groups[1:]:
+                nat.check(c.lib.nv_render(c.handle, g["cam"], nat.ptr(g["rgb"]),
+                                          nat.ptr(g["depth"]), nat.ptr(g["semantic"]), None,
+                                          None, st))
+        else:
+            sim.step(actions, render=True, stream=stream)
+            nat.check(c.lib.nv_task_step(c.handle, nat.ptr(actions), nat.ptr(sim.status),
+                                         nat.ptr(self.reward), nat.ptr(self.dist),
+                                         nat.ptr(self.done), nat.ptr(self.outcome), st))
         obs = self.sim.observations()
         obs["goal"] = self.goal_in_frame
         info = {"d": self.dist, "reward": self.reward, "collided": self.sim.collided,

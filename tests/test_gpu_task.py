@@ -86,7 +86,8 @@ def test_snap_fields_geodesic_exact(nb, gold):
     assert np.array_equal(got[~both_nan], want[~both_nan])
 
 
-def test_episodes_batched_exact(nb, gold):
+@pytest.mark.parametrize("fused", [True, False])  # nv_task_step_render / step + nv_task_step
+def test_episodes_batched_exact(nb, gold, fused):
     if "n_episodes" not in gold:
         pytest.skip("no episodes in this fixture")
     from paper_1904_01201_b200 import task
@@ -96,6 +97,7 @@ def test_episodes_batched_exact(nb, gold):
     ns = len(segs)
     env = task.BatchEnvironment((segs, np.arange(1, ns + 1, dtype=np.uint16), np.full((ns, 3), 0.5)),
                                 n, sensor_configs=(SensorConfig("depth", width=64, height=16),))
+    env.fused_task = fused
     eps = []
     for k in range(n):
         p = f"ep{k}_"
