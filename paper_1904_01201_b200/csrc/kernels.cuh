@@ -1013,15 +1013,11 @@ __device__ __forceinline__ void ray_grid_warp(const SceneView &sc, double px, do
 }
 
 // One warp per (env, column): the latency-bound small-batch cast.
-__global__ void __launch_bounds__(128) k_column_cast_warp(EnvView ev, SceneView sc, CamView cam,
-                                                          RecOut ro, double t_max, double *gps,
-                                                          double *compass) {
-  const long long g = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
-  const long long total = (long long)ev.n * cam.W;
-  if (g >= total) return;
+__device__ __forceinline__ void k_column_cast_warp_body(const EnvView &ev, const SceneView &sc,
+                                                        const CamView &cam, const RecOut &ro,
+                                                        double t_max, double *gps,
+                                                        double *compass, int e, int j) {
   const int lane = threadIdx.x & 31;
-  const int e = (int)(g / cam.W);
-  const int j = (int)(g - (long long)e * cam.W);
   const double px = ev.x[e], py = ev.y[e], c = ev.ch[e], s = ev.sh[e];
   const double u = __ldg(cam.u + j);
   const double dx = add(c, mul(u, s));
@@ -1042,6 +1038,17 @@ __global__ void __launch_bounds__(128) k_column_cast_warp(EnvView ev, SceneView 
     }
     if (compass) compass[e] = nvx::wrap_angle(sub(ev.h[e], ev.oh[e]));
   }
+}
+
+__global__ void __launch_bounds__(128) k_column_cast_warp(EnvView ev, SceneView sc, CamView cam,
+                                                          RecOut ro, double t_max, double *gps,
+                                                          double *compass) {
+  const long long g = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const long long total = (long long)ev.n * cam.W;
+  if (g >= total) return;
+  const int e = (int)(g / cam.W);
+  const int j = (int)(g - (long long)e * cam.W);
+  k_column_cast_warp_body(ev, sc, cam, ro, t_max, gps, compass, e, j);
 }
 
 // One thread per (env, column).

@@ -376,18 +376,15 @@ __device__ __forceinline__ double distance_to_goal(const SceneView &sc, const Na
   return geodesic_at(tv.fields + (size_t)tv.fid[e] * nv.nx * nv.ny, nv, px, py);
 }
 
-// Environment.step's task arithmetic (task.py:193-243) after the agent step.
-__global__ void k_task_step(EnvView ev, SceneView sc, NavView nv, TaskView tv,
-                            const int8_t *__restrict__ actions, const int32_t *step_status,
-                            double *reward, double *dist, uint8_t *done_out, OutcomeRec *out) {
-  const int e = blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= ev.n) return;
-  if (step_status && step_status[e] != 0) return;  // not stepped (not reset / done / bad)
-  const int a = actions[e];
+// Environment.step's task arithmetic (task.py:198-243) for a stepped env e
+// whose new distance is d_cur: step counter, termination (stop / budget),
+// success, reward, EpisodeOutcome.  One thread.
+__device__ __forceinline__ void task_finish(const TaskView &tv, int e, int a, double d_cur,
+                                            double path, long long coll, double *reward,
+                                            double *dist, uint8_t *done_out, OutcomeRec *out) {
   const int steps = tv.steps[e] + 1;
   tv.steps[e] = steps;
   const double d_prev = tv.d_last[e];
-  const double d_cur = distance_to_goal(sc, nv, tv, e, ev.x[e], ev.y[e]);
   tv.d_last[e] = d_cur;
   int term = 0;
   bool success = false;
@@ -408,9 +405,9 @@ __global__ void k_task_step(EnvView ev, SceneView sc, NavView nv, TaskView tv,
       o.terminated_by = (uint8_t)term;
       o.pad[0] = o.pad[1] = 0;
       o.steps = steps;
-      o.collisions = (int32_t)ev.coll[e];
+      o.collisions = (int32_t)coll;
       o.pad2 = 0;
-      o.path_taken = ev.path[e];
+      o.path_taken = path;
       o.shortest_path = tv.gdsp[e];
       const double sh = o.shortest_path, tk = o.path_taken;  // task.spl
       o.spl = success ? div(sh, tk > sh ? tk : sh) : 0.0;
@@ -418,6 +415,20 @@ __global__ void k_task_step(EnvView ev, SceneView sc, NavView nv, TaskView tv,
     }
   }
   if (done_out) done_out[e] = tv.done[e];
+}
+
+// Environment.step's task arithmetic (task.py:193-243) after the agent step.
+__global__ void k_task_step(EnvView ev, SceneView sc, NavView nv, TaskView tv,
+                            const int8_t *__restrict__ actions, const int32_t *step_status,
+                            double *reward, double *dist, uint8_t *done_out, OutcomeRec *out) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= ev.n) return;
+  if (step_status && step_status[e] != 0) {  // not stepped (not reset / done / bad)
+    if (done_out) done_out[e] = tv.done[e];
+    return;
+  }
+  const double d_cur = distance_to_goal(sc, nv, tv, e, ev.x[e], ev.y[e]);
+  task_finish(tv, e, actions[e], d_cur, ev.path[e], ev.coll[e], reward, dist, done_out, out);
 }
 
 // Environment._distance_to_goal by a whole warp (the line-of-sight ray uses
@@ -461,39 +472,65 @@ __global__ void __launch_bounds__(128) k_agent_task_step(EnvView ev, SceneView s
   }
   const double d_cur = distance_to_goal_warp(sc, nv, tv, e, post.x, post.y);
   if (lane != 0) return;
-  const int steps = tv.steps[e] + 1;
-  tv.steps[e] = steps;
-  const double d_prev = tv.d_last[e];
-  tv.d_last[e] = d_cur;
-  int term = 0;
-  bool success = false;
-  if (a == 3) {
-    term = 1;
-    success = d_cur <= tv.success_radius;
-  } else if (steps >= tv.max_steps) {
-    term = 2;
-  }
-  const double base = add(sub(d_prev, d_cur), tv.step_penalty);
-  if (reward) reward[e] = term && success ? add(base, tv.success_reward) : base;
-  if (dist) dist[e] = d_cur;
-  if (term) {
-    tv.done[e] = 1;
-    if (out) {
-      OutcomeRec o;
-      o.success = success;
-      o.terminated_by = (uint8_t)term;
-      o.pad[0] = o.pad[1] = 0;
-      o.steps = steps;
-      o.collisions = (int32_t)post.coll;
-      o.pad2 = 0;
-      o.path_taken = post.path;
-      o.shortest_path = tv.gdsp[e];
-      const double sh = o.shortest_path, tk = o.path_taken;
-      o.spl = success ? div(sh, tk > sh ? tk : sh) : 0.0;
-      out[e] = o;
+  task_finish(tv, e, a, d_cur, post.path, post.coll, reward, dist, done_out, out);
+}
+
+// The task arithmetic riding on the column cast (nv_task_step_render with the
+// DDA casts): the thread (or warp) of column 0 of each env, which is short
+// next to the env's longest ray, computes the env's distance to the goal and
+// the step's task outputs after the agent step of the previous launch.
+struct TaskOut {
+  NavView nv;
+  TaskView tv;
+  const int8_t *actions;
+  const int32_t *status;
+  double *reward, *dist;
+  uint8_t *done;
+  OutcomeRec *out;
+};
+
+__global__ void __launch_bounds__(128) k_column_cast_task(EnvView ev, SceneView sc, CamView cam,
+                                                          RecOut ro, double t_max, double *gps,
+                                                          double *compass, TaskOut to) {
+  const long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const long long total = (long long)ev.n * cam.W;
+  if (g >= total) return;
+  const int e = (int)(g / cam.W);
+  const int j = (int)(g - (long long)e * cam.W);
+  if (j == 0) {  // before the ray: the env's task step
+    if (to.status[e] != 0) {
+      if (to.done) to.done[e] = to.tv.done[e];
+    } else {
+      const double px = ev.x[e], py = ev.y[e];
+      const double d_cur = distance_to_goal(sc, to.nv, to.tv, e, px, py);
+      task_finish(to.tv, e, to.actions[e], d_cur, ev.path[e], ev.coll[e], to.reward, to.dist,
+                  to.done, to.out);
     }
   }
-  if (done_out) done_out[e] = tv.done[e];
+  cast_column<false>(ev, sc, cam, e, j, ro, t_max, gps, compass);
+}
+
+__global__ void __launch_bounds__(128) k_column_cast_warp_task(EnvView ev, SceneView sc,
+                                                               CamView cam, RecOut ro,
+                                                               double t_max, double *gps,
+                                                               double *compass, TaskOut to) {
+  const long long g = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const long long total = (long long)ev.n * cam.W;
+  if (g >= total) return;
+  const int e = (int)(g / cam.W);
+  const int j = (int)(g - (long long)e * cam.W);
+  if (j == 0) {
+    const int lane = threadIdx.x & 31;
+    if (to.status[e] != 0) {
+      if (lane == 0 && to.done) to.done[e] = to.tv.done[e];
+    } else {
+      const double d_cur = distance_to_goal_warp(sc, to.nv, to.tv, e, ev.x[e], ev.y[e]);
+      if (lane == 0)
+        task_finish(to.tv, e, to.actions[e], d_cur, ev.path[e], ev.coll[e], to.reward,
+                    to.dist, to.done, to.out);
+    }
+  }
+  k_column_cast_warp_body(ev, sc, cam, ro, t_max, gps, compass, e, j);
 }
 
 // Environment.reset's initial distance (task.py:188) for masked envs.

@@ -131,7 +131,7 @@ struct nv_ctx {
   bool task_on = false;
   int t_max_steps = 500;
   double t_success_radius = 0.2, t_success_reward = 10.0, t_step_penalty = -0.01;
-  DevBuf t_goal, t_gdsp, t_fid, t_dlast, t_steps, t_done;
+  DevBuf t_goal, t_gdsp, t_fid, t_dlast, t_steps, t_done, t_status;
   const double *t_fields = nullptr;
   int64_t t_nfields = 0;
   double noise_sigma = 0.0;  // inverse-depth noise (nv_depth_noise)
@@ -691,6 +691,15 @@ int cam_check(nv_ctx *c, int cam) {
   return NV_OK;
 }
 
+// small batches (rays fit in about one wave of warps): one warp per ray
+bool use_warp_cast(const nv_ctx *c, long long rays) {
+  static const long long warp_rays = [] {
+    const char *e = getenv("NAVSIM_CAST_WARP_RAYS");
+    return e ? atoll(e) : 16384LL;
+  }();
+  return c->cast_mode == 4 || (c->cast_mode == 0 && rays <= warp_rays);
+}
+
 int do_cast(nv_ctx *c, int cam, double *gps, double *compass, cudaStream_t st) {
   Camera &k = c->cams[cam];
   if (c->cast_mode == 1 && k.W <= 2048) {
@@ -730,12 +739,7 @@ int do_cast(nv_ctx *c, int cam, double *gps, double *compass, cudaStream_t st) {
                                                 k.cast_ctr.as<unsigned int>());
     return check_launch(c);
   }
-  // small batches (rays fit in about one wave of warps): one warp per ray
-  static const long long warp_rays = [] {
-    const char *e = getenv("NAVSIM_CAST_WARP_RAYS");
-    return e ? atoll(e) : 16384LL;
-  }();
-  if (c->cast_mode == 4 || (c->cast_mode == 0 && total <= warp_rays)) {
+  if (use_warp_cast(c, total)) {
     Prof pf(c, st, 1);
     nvk::k_column_cast_warp<<<blocks_for(total * 32, 128), 128, 0, st>>>(
         c->env_view(), c->scene_view(), cam_view(k), rec_out(k, c->n_envs), k.max_range, gps,

@@ -86,8 +86,10 @@ def test_snap_fields_geodesic_exact(nb, gold):
     assert np.array_equal(got[~both_nan], want[~both_nan])
 
 
-@pytest.mark.parametrize("fused", [True, False])  # nv_task_step_render / step + nv_task_step
-def test_episodes_batched_exact(nb, gold, fused):
+# nv_task_step_render with the task riding on the warp / thread cast (cast modes
+# 0 / 3), in the agent kernel (cast mode 1), or step + nv_task_step
+@pytest.mark.parametrize("path", ["cast-warp", "cast-thread", "agent", "separate"])
+def test_episodes_batched_exact(nb, gold, path):
     if "n_episodes" not in gold:
         pytest.skip("no episodes in this fixture")
     from paper_1904_01201_b200 import task
@@ -97,7 +99,10 @@ def test_episodes_batched_exact(nb, gold, fused):
     ns = len(segs)
     env = task.BatchEnvironment((segs, np.arange(1, ns + 1, dtype=np.uint16), np.full((ns, 3), 0.5)),
                                 n, sensor_configs=(SensorConfig("depth", width=64, height=16),))
-    env.fused_task = fused
+    from paper_1904_01201_b200 import _native as nat
+    env.fused_task = path != "separate"
+    mode = {"cast-warp": 0, "cast-thread": 3, "agent": 1, "separate": 0}[path]
+    nat.check(env.sim.ctx.lib.nv_set_cast_mode(env.sim.ctx.handle, mode))
     eps = []
     for k in range(n):
         p = f"ep{k}_"
