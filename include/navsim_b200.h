@@ -120,6 +120,10 @@ int nv_step_render(nv_ctx *ctx, const int8_t *actions, int cam, uint8_t *rgb,
                    uint8_t *collided, double *displacement, int32_t *status,
                    void *stream);
 
+/* Overlap of the agent step and the column cast in nv_step_render
+ * (programmatic dependent launch: each env's casts start as soon as its agent
+ * warp has published the new pose).  Thread-per-ray cast only. */
+int nv_set_overlap(nv_ctx *ctx, int on);
 /* Enable / disable (default) the single-launch megakernel of nv_step_render. */
 int nv_set_fused(nv_ctx *ctx, int on);
 /* Column cast: 0 (default) = per-column DDA over the grid (raycast_grid's

@@ -42,6 +42,7 @@ SIGNATURES = {
     "nv_render": (_I, [_P, _I, _P, _P, _P, _P, _P, _P]),
     "nv_step_render": (_I, [_P, _P, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
     "nv_set_fused": (_I, [_P, _I]),
+    "nv_set_overlap": (_I, [_P, _I]),
     "nv_set_fill_mode": (_I, [_P, _I]),
     "nv_set_cast_mode": (_I, [_P, _I]),
     "nv_step_render_host": (_I, [_P, _P, _I, _U32, _P, _P, _P, _P, _P, _P, _P, _P]),

@@ -780,14 +780,54 @@ __device__ __forceinline__ void warp_agent_step(const EnvView &ev, const SceneVi
   }
 }
 
-// Simulator.step for all envs: one warp per env.
+// Simulator.step for all envs: one warp per env.  With `ready` (programmatic
+// dependent launch of the cast), the dependent grid is released at once and
+// each env's pose is published through ready[e] (release) as soon as its warp
+// is done, so the casts of finished envs overlap the long agent chains.
 __global__ void __launch_bounds__(128) k_agent_step(EnvView ev, SceneView sc, AgentCfg cfg,
                                                     const int8_t *__restrict__ actions,
                                                     uint8_t *collided_out,
-                                                    double *disp_out, int32_t *status_out) {
+                                                    double *disp_out, int32_t *status_out,
+                                                    unsigned *ready) {
+  if (ready) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int e = (int)((blockIdx.x * (size_t)blockDim.x + threadIdx.x) >> 5);
   if (e >= ev.n) return;
   warp_agent_step(ev, sc, cfg, e, actions[e], collided_out, disp_out, status_out);
+  if (ready && (threadIdx.x & 31) == 0) {
+    __threadfence();
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(ready + e), "r"(1u) : "memory");
+  }
+}
+
+// Cast side of the agent->cast overlap: thread 0 of a CTA waits for every env
+// the CTA covers (acquire), then the CTA's last arrival per env resets the
+// env's flag for the next step.  (CTAs of the cast grid cover rays
+// [b*B, (b+1)*B) of the env-major ray order.)
+__device__ __forceinline__ void wait_envs_ready(unsigned *ready, unsigned *arrive, int W,
+                                                long long n_rays) {
+  const long long r0 = (long long)blockIdx.x * blockDim.x;
+  const long long r1 = min(n_rays, r0 + blockDim.x) - 1;
+  const int e0 = (int)(r0 / W), e1 = (int)(r1 / W);
+  if (threadIdx.x == 0) {
+    for (int e = e0; e <= e1; ++e) {
+      unsigned v;
+      do {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ready + e) : "memory");
+        if (!v) __nanosleep(64);
+      } while (!v);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int e = e0; e <= e1; ++e) {
+      // CTAs that cover env e: blocks [first, last] of its ray range
+      const long long f = (long long)e * W / blockDim.x, l = ((long long)(e + 1) * W - 1) / blockDim.x;
+      if (atomicAdd(arrive + e, 1u) == (unsigned)(l - f)) {
+        arrive[e] = 0;
+        ready[e] = 0;
+      }
+    }
+  }
 }
 
 // Simulator.set_agent_state (sim.py:172-184), one warp per env.  Inputs are
@@ -1051,16 +1091,22 @@ __global__ void __launch_bounds__(128) k_column_cast_warp(EnvView ev, SceneView 
   k_column_cast_warp_body(ev, sc, cam, ro, t_max, gps, compass, e, j);
 }
 
-// One thread per (env, column).
+// One thread per (env, column).  With `ready`: launched as a programmatic
+// dependent of k_agent_step; waits per env instead of for the whole step.
 __global__ void __launch_bounds__(128) k_column_cast(EnvView ev, SceneView sc, CamView cam,
                                                      RecOut ro, double t_max,
-                                                     double *gps, double *compass) {
-  const long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+                                                     double *gps, double *compass,
+                                                     unsigned *ready, unsigned *arrive) {
   const long long total = (long long)ev.n * cam.W;
+  if (ready) wait_envs_ready(ready, arrive, cam.W, total);
+  const long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (g >= total) return;
   const int e = (int)(g / cam.W);
   const int j = (int)(g - (long long)e * cam.W);
-  cast_column<false>(ev, sc, cam, e, j, ro, t_max, gps, compass);
+  if (ready)
+    cast_column<true>(ev, sc, cam, e, j, ro, t_max, gps, compass);
+  else
+    cast_column<false>(ev, sc, cam, e, j, ro, t_max, gps, compass);
 }
 
 // Simulator.step + the column casts of one env per CTA: warp 0 runs the

@@ -154,7 +154,10 @@ struct nv_ctx {
   size_t e_hin_bytes = 0, e_hout_bytes = 0;
   int64_t launches = 0;
   int cast_mode = 0;  // 0: per-column DDA (default), 1: binned (tile-binned segment setup)
-  bool cast_queue = false;  // column cast by persistent warps over a work counter (opt-in: slower)
+  bool cast_queue = false;
+  bool pdl = false;        // agent step -> cast programmatic dependent launch
+  bool pdl_armed = false, pdl_init = false;
+  DevBuf pdl_ready, pdl_arrive;  // column cast by persistent warps over a work counter (opt-in: slower)
   int fill_mode = 3;   // 0 direct stores, 1 per-warp TMA stages, 2 warp-specialised, 3 auto
   bool fused = false;  // nv_step_render uses the megakernel when the layout allows (opt-in)
   // optional per-kernel CUDA-event timing (bench roofline evidence)
@@ -752,9 +755,25 @@ int do_cast(nv_ctx *c, int cam, double *gps, double *compass, cudaStream_t st) {
     return v == 32 || v == 64 || v == 96 || v == 128 ? v : 128;
   }();
   Prof pf(c, st, 1);
+  if (c->pdl_armed) {  // programmatic dependent of the agent step just launched
+    c->pdl_armed = false;
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = dim3(blocks_for(total, cast_block));
+    lc.blockDim = dim3(cast_block);
+    lc.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    CK(cudaLaunchKernelEx(&lc, nvk::k_column_cast, c->env_view(), c->scene_view(), cam_view(k),
+                          rec_out(k, c->n_envs), k.max_range, gps, compass,
+                          c->pdl_ready.as<unsigned>(), c->pdl_arrive.as<unsigned>()));
+    return check_launch(c);
+  }
   nvk::k_column_cast<<<blocks_for(total, cast_block), cast_block, 0, st>>>(
       c->env_view(), c->scene_view(), cam_view(k), rec_out(k, c->n_envs), k.max_range, gps,
-      compass);
+      compass, nullptr, nullptr);
   return check_launch(c);
 }
 
@@ -767,13 +786,28 @@ int nv_set_cast_mode_(nv_ctx *c, int mode) {
 }
 
 int do_step(nv_ctx *c, const int8_t *actions, uint8_t *collided, double *disp, int32_t *status,
-            cudaStream_t st) {
+            cudaStream_t st, bool arm_pdl = false) {
   nvk::AgentCfg cfg{c->radius, c->step, c->turn_rad};
   long long threads = c->n_envs * 32;
+  unsigned *ready = nullptr;
+  if (arm_pdl) {
+    const size_t b = sizeof(unsigned) * (size_t)c->n_envs;
+    if (c->pdl_ready.bytes < b || !c->pdl_init) {
+      TRY(c->pdl_ready.alloc(b));
+      TRY(c->pdl_arrive.alloc(b));
+      CK(cudaMemset(c->pdl_ready.p, 0, b));
+      CK(cudaMemset(c->pdl_arrive.p, 0, b));
+      c->pdl_init = true;
+    }
+    ready = c->pdl_ready.as<unsigned>();
+  }
   Prof pf(c, st, 0);
   nvk::k_agent_step<<<blocks_for(threads, 128), 128, 0, st>>>(c->env_view(), c->scene_view(), cfg,
-                                                               actions, collided, disp, status);
-  return check_launch(c);
+                                                               actions, collided, disp, status,
+                                                               ready);
+  TRY(check_launch(c));
+  c->pdl_armed = arm_pdl;
+  return NV_OK;
 }
 
 }  // namespace
@@ -794,6 +828,7 @@ int nv_create(int device, nv_ctx **out) {
   nv_ctx *c = new nv_ctx();
   c->device = device;
   if (const char *q = getenv("NAVSIM_CAST_QUEUE")) c->cast_queue = atoi(q) != 0;  // A/B knob
+  if (const char *q = getenv("NAVSIM_PDL")) c->pdl = atoi(q) != 0;                // A/B knob
   cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device);
   cudaDeviceGetAttribute(&c->max_smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
   *out = c;
@@ -1096,8 +1131,15 @@ int nv_step_render(nv_ctx *c, const int8_t *actions, int cam, uint8_t *rgb, floa
     TRY(check_launch(c));
     return launch_fill(c, k, c->n_envs, rgb, depth, sem, st);
   }
-  TRY(do_step(c, actions, collided, displacement, status, st));
+  // agent step -> cast overlap (programmatic dependent launch) for the
+  // thread-per-ray DDA cast, when profiling events are off (an event between
+  // the two launches would break the programmatic edge)
+  const bool pdl = c->pdl && !c->prof_on && !c->cast_queue &&
+                   (c->cast_mode == 3 ||
+                    (c->cast_mode == 0 && !use_warp_cast(c, c->n_envs * (long long)k.W)));
+  TRY(do_step(c, actions, collided, displacement, status, st, pdl));
   TRY(do_cast(c, cam, gps, compass, st));
+  c->pdl_armed = false;
   return launch_fill(c, k, c->n_envs, rgb, depth, sem, st);
 }
 
@@ -1113,6 +1155,13 @@ int nv_set_fill_mode(nv_ctx *c, int mode) {
   if (mode < 0 || mode > 3)
     return fail(NV_ERR_ARG, "fill mode must be 0 (direct), 1 (tma), 2 (ws) or 3 (auto)");
   c->fill_mode = mode;
+  return NV_OK;
+}
+
+int nv_set_overlap(nv_ctx *c, int on) {
+  if (!c) return fail(NV_ERR_ARG, "ctx is NULL");
+  c->gen++;
+  c->pdl = on != 0;
   return NV_OK;
 }
 

@@ -266,23 +266,34 @@ class BatchEnvironment:
         info["outcome"] holds the 40-byte EpisodeOutcome records (valid for
         envs that terminated).  Finished envs stay frozen until reset."""
         c = self.sim.ctx
-        st = nat.stream_handle(self.dev) if stream is None else stream
         sim = self.sim
         if sim.groups and self.fused_task:
-            # one call: agent step + task arithmetic (one kernel), cast, fill
-            g0 = sim.groups[0]
-            gps = nat.ptr(sim.gps) if sim.want_gps else None
-            comp = nat.ptr(sim.compass) if sim.want_gps else None
-            nat.check(c.lib.nv_task_step_render(
-                c.handle, nat.ptr(actions), g0["cam"], nat.ptr(g0["rgb"]), nat.ptr(g0["depth"]),
-                nat.ptr(g0["semantic"]), gps, comp, nat.ptr(sim.collided),
-                nat.ptr(sim.displacement), nat.ptr(sim.status), nat.ptr(self.reward),
-                nat.ptr(self.dist), nat.ptr(self.done), nat.ptr(self.outcome), st))
+            # one call: agent step + task arithmetic, cast, fill; the argument
+            # tail (all buffers are owned by this object) is built once
+            key = stream
+            cached = getattr(self, "_step_args", None)
+            if cached is None or cached[0] != key:
+                st = nat.stream_handle(self.dev) if stream is None else stream
+                g0 = sim.groups[0]
+                gps = nat.ptr(sim.gps) if sim.want_gps else None
+                comp = nat.ptr(sim.compass) if sim.want_gps else None
+                tail = (nat.ptr(g0["rgb"]), nat.ptr(g0["depth"]), nat.ptr(g0["semantic"]), gps,
+                        comp, nat.ptr(sim.collided), nat.ptr(sim.displacement),
+                        nat.ptr(sim.status), nat.ptr(self.reward), nat.ptr(self.dist),
+                        nat.ptr(self.done), nat.ptr(self.outcome), st)
+                cached = (key, c.lib.nv_task_step_render, c.handle, g0["cam"], tail)
+                self._step_args = cached
+            _, fn, h, cam, tail = cached
+            rc = fn(h, actions.data_ptr(), cam, *tail)
+            if rc:
+                nat.check(rc)
+            st = tail[-1]
             for g in sim.groups[1:]:
                 nat.check(c.lib.nv_render(c.handle, g["cam"], nat.ptr(g["rgb"]),
                                           nat.ptr(g["depth"]), nat.ptr(g["semantic"]), None,
                                           None, st))
         else:
+            st = nat.stream_handle(self.dev) if stream is None else stream
             sim.step(actions, render=True, stream=stream)
             nat.check(c.lib.nv_task_step(c.handle, nat.ptr(actions), nat.ptr(sim.status),
                                          nat.ptr(self.reward), nat.ptr(self.dist),
