@@ -1,0 +1,829 @@
+// fill.cuh -- frame writers (fill_frame, _kernels.py:128-207): shading, the per-warp TMA,
+// direct and warp-specialised writers, depth noise, the generic per-pixel kernel.
+#pragma once
+
+#include "cast.cuh"
+
+namespace nvk {
+
+using nvx::add;
+using nvx::div;
+using nvx::mul;
+using nvx::sub;
+
+// ------------------------------------------------------------ frame fill
+
+// ---- fill: packed-f16 shading --------------------------------------------
+//
+// Per pixel (fill_frame, _kernels.py:171-207): the pixel is a plane pixel
+// (ceiling rows [0, lo), floor rows [hi, H)) or a middle-band pixel (wall, or
+// void when s >= max_range); lo/hi were classified exactly in FP64 by the
+// column epilogue.  Depth (f32) and semantic (u16) are selected exactly.  RGB
+// is shaded in f16 pairs, two pixels per instruction:
+//   t   = 0.2 + (0.8 cos-numerator) * inv      inv = 1/|(d, v)| from the f16 table
+//                                              invh (env-independent; rows mirrored)
+//   c8  = round(col255 * t)                    via HFMA2(col255, t, 1024): the
+//                                              low byte of the f16 result
+// Worst-case error vs the reference's f64 rgb: 0.5 (rounding) + 0.0625 (f16
+// col255) + 255 * 1e-3 (t) < 0.85 of one 8-bit step (tolerance: 1 step).
+//
+// Lane mapping (all fast writers): a warp covers a row segment of 32*CPL
+// columns; lane l owns CPL/GW groups of GW = min(CPL, 4) adjacent columns,
+// group g at segment offset g*32*GW + l*GW.  A warp's group-g stores are then
+// contiguous across lanes (12-byte RGB, 16-byte depth, 8-byte semantic
+// strides: bank-conflict-free shared-memory rows), and its column records are
+// 32 consecutive 16-byte halves (device.cuh rec_pos).
+
+#define NV_H2_POINT2 0x32663266u   // (0.2, 0.2) in f16
+#define NV_H2_1024 0x64006400u     // (1024, 1024): low byte of 1024+x = round(x)
+
+struct FillArgs {
+  const float4 *ra, *rb;  // column-record planes (device.cuh), index env * W + rec_pos
+  int cpl;                // record order
+  const RowRec *rows;
+  int N, W, H;
+  uint8_t *rgb;
+  float *depth;
+  uint16_t *sem;
+  int rows_per_unit;   // rows of one work unit
+  int units_per_seg;   // ceil(H / rows_per_unit)
+  int segs_per_row;    // W / (32 * CPL)
+  long long n_units;   // N * segs_per_row * units_per_seg
+  unsigned int *ctr;   // [0] next unit, [1] finished warps (self-resetting)
+  const uint16_t *invh;  // ceil(H/2) x W f16 shading table 1/|(d_j, v_i)|, rows
+                         // mirrored (v_{H-1-i} = -v_i); env-independent
+  // inverse-depth noise (sensors.apply_inverse_depth_noise, sensors.py:183-205)
+  float noise_sigma;     // 0 = off
+  float max_range;
+  unsigned long long noise_seed, noise_frame;
+  long long env_offset;  // global id of env 0 (sharding-invariant streams)
+};
+
+// ---- inverse-depth noise ---------------------------------------------------
+// z' = max_range / (max_range / d + eps), eps ~ N(0, sigma), clamped to
+// [0.05, max_range]; saturated pixels (d >= max_range) pass through
+// (sensors.py:195-205).  eps comes from a counter-based generator: one
+// splitmix64 draw per horizontal pixel pair, keyed by (seed, frame, global
+// env, row, pair), turned into two normals by Box-Muller -- so every fill
+// path produces the same noisy frame.  numpy's Generator.normal stream
+// cannot be reproduced on the device; parity is distributional (the
+// reference's own moment test, tests/test_sensors.py:179-184).
+__device__ __forceinline__ unsigned long long splitmix64(unsigned long long z) {
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+__device__ __forceinline__ float2 noise_pair(const FillArgs &a, int env, int row, int col) {
+  const unsigned long long key =
+      ((((a.noise_frame << 20) ^ (unsigned long long)(env + a.env_offset)) * (unsigned long long)a.H +
+        (unsigned long long)row) * (unsigned long long)a.W + (unsigned long long)col) >> 1;
+  const unsigned long long z = splitmix64(a.noise_seed ^ splitmix64(key));
+  const float u1 = (float)((z >> 40) + 1ull) * 0x1p-24f;           // (0, 1]
+  const float u2 = (float)((z >> 16) & 0xFFFFFFull) * 0x1p-24f;     // [0, 1)
+  const float r = sqrtf(-2.0f * __logf(u1));
+  float sn, cs;
+  __sincosf(6.283185307f * u2, &sn, &cs);
+  return make_float2(r * cs * a.noise_sigma, r * sn * a.noise_sigma);
+}
+
+__device__ __forceinline__ float noisy_depth(float d, float eps, float max_range) {
+  if (!(d < max_range)) return d;
+  const float inv = max_range / d + eps;
+  const float z = inv != 0.0f ? max_range / inv : __int_as_float(0x7f800000);
+  return fminf(fmaxf(z, 0.05f), max_range);
+}
+
+template <int CPL>
+struct Lanes {
+  static constexpr int GW = CPL < 4 ? CPL : 4;  // columns per group
+  static constexpr int G = CPL / GW;            // groups per lane
+  static constexpr int SEGW = 32 * CPL;         // columns per warp segment
+};
+
+__device__ __forceinline__ uint32_t h2_fma(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t d;
+  asm("fma.rn.f16x2 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
+}
+__device__ __forceinline__ uint32_t h2_pack(float lo, float hi) {
+  uint32_t d;
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(d) : "f"(hi), "f"(lo));
+  return d;
+}
+// (a & m) | (b & ~m): per-half select with a 0xFFFF-granular mask
+__device__ __forceinline__ uint32_t sel_mask(uint32_t a, uint32_t b, uint32_t m) {
+  return (a & m) | (b & ~m);
+}
+
+__device__ __forceinline__ unsigned smem_addr(const void *p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void bulk_store(void *gdst, const void *ssrc, unsigned bytes,
+                                           uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;\n" ::"l"(
+          gdst),
+      "r"(smem_addr(ssrc)), "r"(bytes), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_commit() {
+  asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;\n" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() {
+  asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(p));
+  return p;
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_addr(bar)),
+      "r"(parity)
+      : "memory");
+}
+// global -> shared bulk copy completing on an mbarrier (bytes % 16 == 0)
+__device__ __forceinline__ void bulk_load(void *sdst, const void *gsrc, unsigned bytes,
+                                          uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(smem_addr(sdst)),
+      "l"(gsrc), "r"(bytes), "r"(smem_addr(bar))
+      : "memory");
+}
+
+// A lane's CPL columns (CPL/2 pixel pairs, column k = g*GW + c) in registers.
+template <int CPL>
+struct ColRegs {
+  float dw[CPL];                 // wall depth (or max_range)
+  uint32_t lo[CPL], hi[CPL];     // plane rows: i < lo or i >= hi
+  uint32_t nw[CPL / 2], rw[CPL / 2], gw[CPL / 2], bw[CPL / 2];  // f16 pairs
+  uint32_t sw[CPL / 2];          // semantic pairs
+};
+
+template <int CPL>
+__device__ __forceinline__ void unpack_cols(const float4 (&A)[CPL], const float4 (&B)[CPL],
+                                            ColRegs<CPL> &cr) {
+#pragma unroll
+  for (int k = 0; k < CPL; ++k) {
+    cr.dw[k] = A[k].x;
+    const uint32_t l = __float_as_uint(A[k].w);
+    cr.lo[k] = l & 0xffffu;
+    cr.hi[k] = l >> 16;
+  }
+#pragma unroll
+  for (int m = 0; m < CPL / 2; ++m) {
+    cr.nw[m] = h2_pack(A[2 * m].y, A[2 * m + 1].y);
+    cr.rw[m] = h2_pack(B[2 * m].x, B[2 * m + 1].x);
+    cr.gw[m] = h2_pack(B[2 * m].y, B[2 * m + 1].y);
+    cr.bw[m] = h2_pack(B[2 * m].z, B[2 * m + 1].z);
+    cr.sw[m] = (__float_as_uint(B[2 * m].w) & 0xffffu) | (__float_as_uint(B[2 * m + 1].w) << 16);
+  }
+}
+
+// Global planes; base = env * W + seg * SEGW (records in rec_pos order).
+// COH: written earlier in the same launch (read through L2).
+template <int CPL, bool COH>
+__device__ __forceinline__ void load_cols(const FillArgs &a, size_t base, int lane,
+                                          ColRegs<CPL> &cr) {
+  float4 A[CPL], B[CPL];
+#pragma unroll
+  for (int k = 0; k < CPL; ++k) {
+    const size_t p = base + (size_t)k * 32 + lane;
+    if (COH) {
+      A[k] = __ldcg(a.ra + p);
+      B[k] = __ldcg(a.rb + p);
+    } else {
+      A[k] = __ldg(a.ra + p);
+      B[k] = __ldg(a.rb + p);
+    }
+  }
+  unpack_cols<CPL>(A, B, cr);
+}
+
+// Shared-memory planes of one env: sA/sB + seg * SEGW.
+template <int CPL>
+__device__ __forceinline__ void load_cols_smem(const float4 *sA, const float4 *sB, int lane,
+                                               ColRegs<CPL> &cr) {
+  float4 A[CPL], B[CPL];
+#pragma unroll
+  for (int k = 0; k < CPL; ++k) {
+    A[k] = sA[k * 32 + lane];
+    B[k] = sB[k * 32 + lane];
+  }
+  unpack_cols<CPL>(A, B, cr);
+}
+
+// Shade one pixel pair (columns 2k, 2k+1 of the lane) of row i.
+struct PairOut {
+  uint32_t r, g, b, s;  // f16 pairs (low byte of each half = value), sem pair
+  float d0, d1;
+};
+
+__device__ __forceinline__ PairOut shade_pair(uint32_t i, const RowRec &R, uint32_t lo0,
+                                              uint32_t hi0, uint32_t lo1, uint32_t hi1, float dw0,
+                                              float dw1, uint32_t nw, uint32_t rw, uint32_t gw,
+                                              uint32_t bw, uint32_t sw, uint32_t inv2) {
+  const bool in0 = i >= lo0 && i < hi0;  // middle band (wall / void)
+  const bool in1 = i >= lo1 && i < hi1;
+  const uint32_t m = (in0 ? 0x0000ffffu : 0u) | (in1 ? 0xffff0000u : 0u);
+  PairOut o;
+  o.d0 = in0 ? dw0 : R.depth_p;
+  o.d1 = in1 ? dw1 : R.depth_p;
+  o.s = sel_mask(sw, R.sem2, m);
+  const uint32_t num = sel_mask(nw, R.num2, m);
+  const uint32_t t = h2_fma(num, inv2, NV_H2_POINT2);
+  o.r = h2_fma(sel_mask(rw, R.r2, m), t, NV_H2_1024);
+  o.g = h2_fma(sel_mask(gw, R.g2, m), t, NV_H2_1024);
+  o.b = h2_fma(sel_mask(bw, R.b2, m), t, NV_H2_1024);
+  return o;
+}
+
+// Two pixel pairs (4 pixels) -> 12 interleaved RGB bytes (3 words).
+__device__ __forceinline__ void pack_rgb4(const PairOut &p, const PairOut &q, uint32_t &w0,
+                                          uint32_t &w1, uint32_t &w2) {
+  const uint32_t rg0 = __byte_perm(p.r, p.g, 0x6240);  // r0 g0 r1 g1
+  const uint32_t rg1 = __byte_perm(q.r, q.g, 0x6240);  // r2 g2 r3 g3
+  w0 = __byte_perm(rg0, p.b, 0x2410);                  // r0 g0 b0 r1
+  const uint32_t t = __byte_perm(rg0, p.b, 0x3263);    // g1 b1 . .
+  w1 = __byte_perm(t, rg1, 0x5410);                    // g1 b1 r2 g2
+  w2 = __byte_perm(rg1, q.b, 0x6324);                  // b2 r3 g3 b3
+}
+
+__device__ __forceinline__ RowRec unpack_row(const RowRec *rows_s, uint32_t i) {
+  const uint4 *rq = reinterpret_cast<const uint4 *>(rows_s + i);
+  const uint4 q0 = rq[0], q1 = rq[1];
+  RowRec R;
+  R.depth_p = __uint_as_float(q0.x);
+  R.sem2 = q0.y;
+  R.num2 = q0.z;
+  R.r2 = q0.w;
+  R.g2 = q1.x;
+  R.b2 = q1.y;
+  return R;
+}
+
+// Shading-table row of image row i: the table holds rows [0, ceil(H/2)) and
+// row H-1-i equals row i (v_{H-1-i} = -v_i exactly).
+__device__ __forceinline__ uint32_t inv_row(uint32_t i, int H) {
+  return i < (uint32_t)(H >> 1) ? i : (uint32_t)(H - 1) - i;
+}
+
+// The lane's shading-table pairs from table row `ip` (+ segment offset).
+template <int CPL, bool GLOBAL>
+__device__ __forceinline__ void load_inv(const uint16_t *ip, int lane, uint32_t (&iv)[CPL / 2]) {
+  using Ln = Lanes<CPL>;
+#pragma unroll
+  for (int g = 0; g < Ln::G; ++g) {
+    const uint16_t *q = ip + g * 32 * Ln::GW + lane * Ln::GW;
+    if constexpr (Ln::GW == 4) {
+      const uint2 v = GLOBAL ? __ldg(reinterpret_cast<const uint2 *>(q))
+                             : *reinterpret_cast<const uint2 *>(q);
+      iv[2 * g] = v.x;
+      iv[2 * g + 1] = v.y;
+    } else {
+      iv[g] = GLOBAL ? __ldg(reinterpret_cast<const uint32_t *>(q))
+                     : *reinterpret_cast<const uint32_t *>(q);
+    }
+  }
+}
+
+template <int CPL>
+__device__ __forceinline__ void shade_row(uint32_t i, const RowRec &R, const ColRegs<CPL> &cr,
+                                          const uint32_t (&iv)[CPL / 2],
+                                          PairOut (&po)[CPL / 2]) {
+#pragma unroll
+  for (int c = 0; c < CPL / 2; ++c)
+    po[c] = shade_pair(i, R, cr.lo[2 * c], cr.hi[2 * c], cr.lo[2 * c + 1], cr.hi[2 * c + 1],
+                       cr.dw[2 * c], cr.dw[2 * c + 1], cr.nw[c], cr.rw[c], cr.gw[c], cr.bw[c],
+                       cr.sw[c], iv[c]);
+}
+
+// Writes the lane's shaded pixels of one row segment into a buffer laid out
+// like the frame (shared-memory stage / slot): px0 = pixel index of the
+// segment's first column in the buffer.
+template <int CPL>
+__device__ __forceinline__ void put_row(const PairOut (&po)[CPL / 2], uint8_t *rgb, float *dep,
+                                        uint16_t *sem, int px0, int lane) {
+  using Ln = Lanes<CPL>;
+#pragma unroll
+  for (int g = 0; g < Ln::G; ++g) {
+    const int px = px0 + g * 32 * Ln::GW + lane * Ln::GW;
+    if constexpr (Ln::GW == 4) {
+      const PairOut &p = po[2 * g], &q = po[2 * g + 1];
+      if (rgb) {
+        uint32_t w0, w1, w2;
+        pack_rgb4(p, q, w0, w1, w2);
+        uint32_t *d = reinterpret_cast<uint32_t *>(rgb + (size_t)px * 3);
+        d[0] = w0;
+        d[1] = w1;
+        d[2] = w2;
+      }
+      if (dep) *reinterpret_cast<float4 *>(dep + px) = make_float4(p.d0, p.d1, q.d0, q.d1);
+      if (sem) *reinterpret_cast<uint2 *>(sem + px) = make_uint2(p.s, q.s);
+    } else {
+      const PairOut &p = po[g];
+      if (rgb) {
+        uint16_t *d16 = reinterpret_cast<uint16_t *>(rgb + (size_t)px * 3);
+        d16[0] = (uint16_t)__byte_perm(p.r, p.g, 0x0040);  // r0 g0
+        d16[1] = (uint16_t)__byte_perm(p.b, p.r, 0x0060);  // b0 r1
+        d16[2] = (uint16_t)__byte_perm(p.g, p.b, 0x0062);  // g1 b1
+      }
+      if (dep) *reinterpret_cast<float2 *>(dep + px) = make_float2(p.d0, p.d1);
+      if (sem) *reinterpret_cast<uint32_t *>(sem + px) = p.s;
+    }
+  }
+}
+
+// Copies the camera's row table (H x 32 B) into shared memory; every warp of
+// the CTA reads its rows from there (uniform LDS, no L1/L2 misses under the
+// write stream).  Returns the first byte after the table (16-aligned).
+__device__ __forceinline__ uint8_t *stage_rows(const FillArgs &a, uint8_t *smem) {
+  const uint4 *src = reinterpret_cast<const uint4 *>(a.rows);
+  uint4 *dst = reinterpret_cast<uint4 *>(smem);
+  for (int k = threadIdx.x; k < a.H * 2; k += blockDim.x) dst[k] = __ldg(src + k);
+  __syncthreads();
+  return smem + (size_t)a.H * sizeof(RowRec);
+}
+
+// Per-warp state of the streaming writer: a private ring of NS smem stages.
+template <int CPL, int RW>
+struct FillWarp {
+  static constexpr int NS = 2;
+  static constexpr int SEGW = 32 * CPL;
+  uint8_t *wbase;
+  const RowRec *rows_s;  // shared-memory row table
+  int off_d, off_s, stage_bytes;
+  bool want_rgb, want_d, want_s;
+  uint64_t pol;
+  int k;  // stages issued so far
+  // smem layout: [row table H x 32 B][per-warp stage rings]
+  __device__ __forceinline__ void init(const FillArgs &a, uint8_t *smem, int wib) {
+    rows_s = reinterpret_cast<const RowRec *>(smem);
+    smem = stage_rows(a, smem);
+    want_rgb = a.rgb != nullptr;
+    want_d = a.depth != nullptr;
+    want_s = a.sem != nullptr;
+    off_d = want_rgb ? RW * SEGW * 3 : 0;
+    off_s = off_d + (want_d ? RW * SEGW * 4 : 0);
+    stage_bytes = off_s + (want_s ? RW * SEGW * 2 : 0);
+    wbase = smem + (size_t)wib * NS * stage_bytes;
+    pol = policy_evict_first();
+    k = 0;
+  }
+};
+
+// Render one unit = (env, column segment of 32*CPL columns, rows
+// [gidx*rpu, ...)) of fill_frame: the lane's CPL columns' parameters sit in
+// registers; RW rows at a time are rendered into a smem stage laid out exactly
+// like global memory, which lane 0 writes out with cp.async.bulk (one copy
+// per channel per stage when a warp covers full rows), evict-first in L2.
+// COH: the column records were written earlier in the same launch.
+template <int CPL, int RW, bool COH>
+__device__ __forceinline__ void fill_unit(const FillArgs &a, FillWarp<CPL, RW> &fw, int env,
+                                          int seg, int gidx) {
+  constexpr int NS = FillWarp<CPL, RW>::NS;
+  constexpr int SEGW = FillWarp<CPL, RW>::SEGW;
+  const int lane = threadIdx.x & 31;
+  const int W = a.W, H = a.H;
+  ColRegs<CPL> cr;
+  load_cols<CPL, COH>(a, (size_t)env * W + (size_t)seg * SEGW, lane, cr);
+  const int r_begin = gidx * a.rows_per_unit;
+  const int r_end = min(H, r_begin + a.rows_per_unit);
+  for (int r0 = r_begin; r0 < r_end; r0 += RW) {
+    const int nr = min(RW, r_end - r0);
+    uint8_t *buf = fw.wbase + (fw.k & (NS - 1)) * fw.stage_bytes;
+    if (fw.k >= NS) {
+      if (lane == 0) bulk_wait_read<NS - 1>();
+      __syncwarp();
+    }
+    for (int rr = 0; rr < nr; ++rr) {
+      const uint32_t i = (uint32_t)(r0 + rr);
+      const RowRec R = unpack_row(fw.rows_s, i);
+      uint32_t iv[CPL / 2];
+      load_inv<CPL, true>(a.invh + (size_t)inv_row(i, H) * W + seg * SEGW, lane, iv);
+      PairOut po[CPL / 2];
+      shade_row<CPL>(i, R, cr, iv, po);
+      put_row<CPL>(po, fw.want_rgb ? buf : nullptr,
+                   fw.want_d ? reinterpret_cast<float *>(buf + fw.off_d) : nullptr,
+                   fw.want_s ? reinterpret_cast<uint16_t *>(buf + fw.off_s) : nullptr,
+                   rr * SEGW, lane);
+    }
+    fence_proxy_async();
+    __syncwarp();
+    if (lane == 0) {
+      if (a.segs_per_row == 1) {
+        const size_t pix0 = ((size_t)env * H + r0) * W;
+        if (fw.want_rgb) bulk_store(a.rgb + pix0 * 3, buf, (unsigned)(nr * W * 3), fw.pol);
+        if (fw.want_d) bulk_store(a.depth + pix0, buf + fw.off_d, (unsigned)(nr * W * 4), fw.pol);
+        if (fw.want_s) bulk_store(a.sem + pix0, buf + fw.off_s, (unsigned)(nr * W * 2), fw.pol);
+      } else {
+        for (int rr = 0; rr < nr; ++rr) {
+          const size_t pix0 = ((size_t)env * H + r0 + rr) * W + (size_t)seg * SEGW;
+          if (fw.want_rgb)
+            bulk_store(a.rgb + pix0 * 3, buf + rr * SEGW * 3, (unsigned)(SEGW * 3), fw.pol);
+          if (fw.want_d)
+            bulk_store(a.depth + pix0, buf + fw.off_d + rr * SEGW * 4, (unsigned)(SEGW * 4),
+                       fw.pol);
+          if (fw.want_s)
+            bulk_store(a.sem + pix0, buf + fw.off_s + rr * SEGW * 2, (unsigned)(SEGW * 2), fw.pol);
+        }
+      }
+      bulk_commit();
+    }
+    ++fw.k;
+  }
+}
+
+// Drains this warp's bulk stores and, for the last warp of the grid, resets
+// the self-resetting work counter for the next launch.
+__device__ __forceinline__ void finish_grid(unsigned int *ctr) {
+  if ((threadIdx.x & 31) == 0) {
+    bulk_wait_all();
+    const unsigned total_warps = gridDim.x * (blockDim.x >> 5);
+    if (atomicAdd(ctr + 1, 1u) == total_warps - 1) {
+      ctr[0] = 0;
+      ctr[1] = 0;
+      __threadfence();
+    }
+  }
+}
+
+// k_fill_tma: streaming frame writer over all units of a frame batch; units
+// are pulled from a self-resetting global counter (one prefetched ahead).
+template <int CPL, int RW>
+__global__ void __launch_bounds__(128) k_fill_tma(FillArgs a) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  const int lane = threadIdx.x & 31;
+  FillWarp<CPL, RW> fw;
+  fw.init(a, smem, threadIdx.x >> 5);
+  long long u = 0;
+  if (lane == 0) u = atomicAdd(a.ctr, 1u);
+  u = __shfl_sync(0xffffffffu, u, 0);
+  while (u < a.n_units) {
+    long long nxt = 0;
+    if (lane == 0) nxt = atomicAdd(a.ctr, 1u);
+    // row-block-major order: warps across the GPU render the same rows of
+    // different envs at the same time (shared row records / table rows)
+    const long long n_es = (long long)a.N * a.segs_per_row;
+    const int gidx = (int)(u / n_es);
+    const long long es = u - (long long)gidx * n_es;
+    const int env = (int)(es / a.segs_per_row);
+    const int seg = (int)(es - (long long)env * a.segs_per_row);
+    fill_unit<CPL, RW, false>(a, fw, env, seg, gidx);
+    u = __shfl_sync(0xffffffffu, nxt, 0);
+  }
+  finish_grid(a.ctr);
+}
+
+// ---- direct-store variant: no smem staging ---------------------------------
+// Each lane stores its pixels of a row straight from registers with
+// evict-first 128/64/32-bit stores; a warp's group-g stores are contiguous.
+__device__ __forceinline__ void st_v4f(float *p, float4 v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.v4.f32 [%0], {%1,%2,%3,%4}, %5;" ::"l"(p), "f"(v.x),
+               "f"(v.y), "f"(v.z), "f"(v.w), "l"(pol)
+               : "memory");
+}
+__device__ __forceinline__ void st_v2u(void *p, uint32_t a, uint32_t b, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.v2.b32 [%0], {%1,%2}, %3;" ::"l"(p), "r"(a), "r"(b),
+               "l"(pol)
+               : "memory");
+}
+__device__ __forceinline__ void st_u(void *p, uint32_t a, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.b32 [%0], %1, %2;" ::"l"(p), "r"(a), "l"(pol)
+               : "memory");
+}
+
+template <int CPL, bool COH>
+__device__ __forceinline__ void fill_unit_direct(const FillArgs &a, const RowRec *rows_s,
+                                                 uint64_t pol, int env, int seg, int gidx) {
+  using Ln = Lanes<CPL>;
+  const int lane = threadIdx.x & 31;
+  const int W = a.W, H = a.H;
+  ColRegs<CPL> cr;
+  load_cols<CPL, COH>(a, (size_t)env * W + (size_t)seg * Ln::SEGW, lane, cr);
+  const int r_begin = gidx * a.rows_per_unit;
+  const int r_end = min(H, r_begin + a.rows_per_unit);
+  for (int r = r_begin; r < r_end; ++r) {
+    const uint32_t i = (uint32_t)r;
+    const RowRec R = unpack_row(rows_s, i);
+    uint32_t iv[CPL / 2];
+    load_inv<CPL, true>(a.invh + (size_t)inv_row(i, H) * W + seg * Ln::SEGW, lane, iv);
+    PairOut po[CPL / 2];
+    shade_row<CPL>(i, R, cr, iv, po);
+    const size_t row0 = ((size_t)env * H + r) * W + (size_t)seg * Ln::SEGW;
+#pragma unroll
+    for (int g = 0; g < Ln::G; ++g) {
+      const size_t px = row0 + g * 32 * Ln::GW + lane * Ln::GW;
+      if constexpr (Ln::GW == 4) {
+        const PairOut &p = po[2 * g], &q = po[2 * g + 1];
+        if (a.rgb) {
+          uint32_t w0, w1, w2;
+          pack_rgb4(p, q, w0, w1, w2);
+          uint8_t *d = a.rgb + px * 3;
+          st_u(d, w0, pol);
+          st_u(d + 4, w1, pol);
+          st_u(d + 8, w2, pol);
+        }
+        if (a.depth) st_v4f(a.depth + px, make_float4(p.d0, p.d1, q.d0, q.d1), pol);
+        if (a.sem) st_v2u(a.sem + px, p.s, q.s, pol);
+      } else {
+        const PairOut &p = po[g];
+        if (a.rgb) {
+          uint16_t *d16 = reinterpret_cast<uint16_t *>(a.rgb + px * 3);
+          d16[0] = (uint16_t)__byte_perm(p.r, p.g, 0x0040);
+          d16[1] = (uint16_t)__byte_perm(p.b, p.r, 0x0060);
+          d16[2] = (uint16_t)__byte_perm(p.g, p.b, 0x0062);
+        }
+        if (a.depth) *reinterpret_cast<float2 *>(a.depth + px) = make_float2(p.d0, p.d1);
+        if (a.sem) *reinterpret_cast<uint32_t *>(a.sem + px) = p.s;
+      }
+    }
+  }
+}
+
+template <int CPL>
+__global__ void __launch_bounds__(128) k_fill_direct(FillArgs a) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  stage_rows(a, smem);
+  const RowRec *rows_s = reinterpret_cast<const RowRec *>(smem);
+  const int lane = threadIdx.x & 31;
+  const uint64_t pol = policy_evict_first();
+  long long u = 0;
+  if (lane == 0) u = atomicAdd(a.ctr, 1u);
+  u = __shfl_sync(0xffffffffu, u, 0);
+  while (u < a.n_units) {
+    long long nxt = 0;
+    if (lane == 0) nxt = atomicAdd(a.ctr, 1u);
+    const long long n_es = (long long)a.N * a.segs_per_row;
+    const int gidx = (int)(u / n_es);
+    const long long es = u - (long long)gidx * n_es;
+    const int env = (int)(es / a.segs_per_row);
+    const int seg = (int)(es - (long long)env * a.segs_per_row);
+    fill_unit_direct<CPL, false>(a, rows_s, pol, env, seg, gidx);
+    u = __shfl_sync(0xffffffffu, nxt, 0);
+  }
+  finish_grid(a.ctr);
+}
+
+// ---- warp-specialised frame writer ------------------------------------------
+//
+// k_fill_ws: persistent, one CTA per SM = NW producer warps + 1 store warp; a
+// work item is one env's frame.  Producers render rows into a ring of NSLOT
+// shared-memory slots (a slot = R consecutive frame rows, all channels, laid
+// out exactly like the frame, so ONE bulk copy per channel writes it out);
+// the store warp's elected lane waits on the slot's `full` mbarrier, issues
+// the cp.async.bulk stores (evict-first), and releases the previous slot
+// through its `empty` mbarrier once the bulk engine has read it.  The same
+// lane prefetches the next item's column-record planes into a double buffer
+// with bulk copies.  Producers never touch L2: row records, the shading table
+// and column records are all shared-memory reads.
+#ifndef NV_WS_DEBUG
+#define NV_WS_DEBUG 0  // 1: producers skip rendering, 2: no bulk stores (bound studies)
+#endif
+struct FillWsLayout {  // byte offsets into dynamic shared memory + ring geometry
+  int rows, inv, cols, bars, slots;
+  int slot_bytes, nslot, slot_rows;
+  int depth_direct;  // 1: producers store depth straight from registers (STG),
+                     // the slots carry RGB / semantic only
+};
+
+template <int CPL, bool TAB, int RPW, bool NOISE>
+__global__ void __launch_bounds__(544, 1) k_fill_ws(FillArgs a, FillWsLayout L) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  using Ln = Lanes<CPL>;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nw = (blockDim.x >> 5) - 1;  // producer warps
+  const int W = a.W, H = a.H, S = a.segs_per_row, R = L.slot_rows, NSLOT = L.nslot;
+  const RowRec *rows_s = reinterpret_cast<const RowRec *>(smem + L.rows);
+  const uint16_t *inv_s = reinterpret_cast<const uint16_t *>(smem + L.inv);
+  float4 *cols_s = reinterpret_cast<float4 *>(smem + L.cols);  // [buf][A | B][W]
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + L.bars);
+  uint64_t *empty = full + NSLOT;
+  uint64_t *colfull = empty + NSLOT;
+  uint64_t *colempty = colfull + 2;
+  uint8_t *slots = smem + L.slots;
+  const unsigned plane_bytes = (unsigned)W * 16u;
+  const bool want_rgb = a.rgb != nullptr, want_d = a.depth != nullptr, want_s = a.sem != nullptr;
+  const bool slot_d = want_d && !L.depth_direct;
+  const int off_d = want_rgb ? R * W * 3 : 0;
+  const int off_s = off_d + (slot_d ? R * W * 4 : 0);
+  const int slots_per_item = H / R;
+  if (threadIdx.x == 0) {
+    for (int k = 0; k < NSLOT; ++k) {
+      mbar_init(full + k, (unsigned)nw);
+      mbar_init(empty + k, 1);
+    }
+    for (int k = 0; k < 2; ++k) {
+      mbar_init(colfull + k, 1);
+      mbar_init(colempty + k, (unsigned)nw);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  {
+    const uint4 *src = reinterpret_cast<const uint4 *>(a.rows);
+    uint4 *dst = reinterpret_cast<uint4 *>(smem + L.rows);
+    for (int k = threadIdx.x; k < H * 2; k += blockDim.x) dst[k] = __ldg(src + k);
+    if (TAB) {
+      const uint4 *s2 = reinterpret_cast<const uint4 *>(a.invh);
+      uint4 *d2 = reinterpret_cast<uint4 *>(smem + L.inv);
+      const int n16 = ((H + 1) / 2) * W * 2 / 16;
+      for (int k = threadIdx.x; k < n16; k += blockDim.x) d2[k] = __ldg(s2 + k);
+    }
+  }
+  __syncthreads();
+  if (warp == nw) {
+    // ------------------------------------------------------------ store warp
+    if (lane != 0) return;
+    const uint64_t pol = policy_evict_first();
+    auto load_item = [&](int buf, int env) {
+      uint64_t *b = colfull + buf;
+      mbar_expect_tx(b, 2 * plane_bytes);
+      bulk_load(cols_s + (size_t)buf * 2 * W, a.ra + (size_t)env * W, plane_bytes, b);
+      bulk_load(cols_s + (size_t)buf * 2 * W + W, a.rb + (size_t)env * W, plane_bytes, b);
+    };
+    int e = blockIdx.x;
+    if (e < a.N) load_item(0, e);
+    unsigned k = 0, slot = 0, use = 0, prev = 0;
+    for (int it = 0; e < a.N; ++it, e += gridDim.x) {
+      const int en = e + gridDim.x;
+      if (en < a.N) {
+        const int j = it + 1;
+        if (j >= 2) mbar_wait(colempty + (j & 1), (unsigned)(((j >> 1) - 1) & 1));
+        load_item(j & 1, en);
+      }
+      for (int sl = 0; sl < slots_per_item; ++sl, ++k) {
+        mbar_wait(full + slot, use & 1u);
+        const uint8_t *buf = slots + (size_t)slot * L.slot_bytes;
+        const size_t pix0 = ((size_t)e * H + (size_t)sl * R) * W;
+#if NV_WS_DEBUG != 2
+        if (want_rgb) bulk_store(a.rgb + pix0 * 3, buf, (unsigned)(R * W * 3), pol);
+        if (slot_d) bulk_store(a.depth + pix0, buf + off_d, (unsigned)(R * W * 4), pol);
+        if (want_s) bulk_store(a.sem + pix0, buf + off_s, (unsigned)(R * W * 2), pol);
+#else
+        (void)buf; (void)pix0; (void)pol;
+#endif
+        bulk_commit();
+        if (k >= 1) {
+          bulk_wait_read<1>();
+          mbar_arrive(empty + prev);
+        }
+        prev = slot;
+        if (++slot == (unsigned)NSLOT) {
+          slot = 0;
+          ++use;
+        }
+      }
+    }
+    bulk_wait_all();
+    return;
+  }
+  // -------------------------------------------------------------- producers
+  const uint64_t dpol = policy_evict_first();
+  const int seg = warp % S;
+  const int rsub = warp / S;   // first row of this warp within a slot
+  const int rstride = nw / S;  // row stride between the warp's RPW rows
+  unsigned slot = 0, use = 0;
+  int e = blockIdx.x;
+  for (int it = 0; e < a.N; ++it, e += gridDim.x) {
+    mbar_wait(colfull + (it & 1), (unsigned)((it >> 1) & 1));
+    ColRegs<CPL> cr;
+    const float4 *cA = cols_s + (size_t)(it & 1) * 2 * W + seg * Ln::SEGW;
+    load_cols_smem<CPL>(cA, cA + W, lane, cr);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(colempty + (it & 1));
+    for (int sl = 0; sl < slots_per_item; ++sl) {
+      if (use >= 1) mbar_wait(empty + slot, (use - 1) & 1u);
+      uint8_t *buf = slots + (size_t)slot * L.slot_bytes;
+#pragma unroll
+      for (int rr = 0; rr < RPW; ++rr) {
+        const int rs = rsub + rr * rstride;  // row within the slot
+        const uint32_t i = (uint32_t)(sl * R + rs);
+#if NV_WS_DEBUG == 1
+        (void)buf; (void)i;
+        continue;
+#endif
+        const RowRec Rr = unpack_row(rows_s, i);
+        uint32_t iv[CPL / 2];
+        if constexpr (TAB)
+          load_inv<CPL, false>(inv_s + (size_t)inv_row(i, H) * W + seg * Ln::SEGW, lane, iv);
+        else
+          load_inv<CPL, true>(a.invh + (size_t)inv_row(i, H) * W + seg * Ln::SEGW, lane, iv);
+        PairOut po[CPL / 2];
+        shade_row<CPL>(i, Rr, cr, iv, po);
+        if constexpr (NOISE) {
+#pragma unroll
+          for (int c = 0; c < CPL / 2; ++c) {
+            const int col = seg * Ln::SEGW + (c / (Ln::GW / 2)) * 32 * Ln::GW + lane * Ln::GW +
+                            2 * (c % (Ln::GW / 2));
+            const float2 n = noise_pair(a, e, (int)i, col);
+            po[c].d0 = noisy_depth(po[c].d0, n.x, a.max_range);
+            po[c].d1 = noisy_depth(po[c].d1, n.y, a.max_range);
+          }
+        }
+        put_row<CPL>(po, want_rgb ? buf : nullptr,
+                     slot_d ? reinterpret_cast<float *>(buf + off_d) : nullptr,
+                     want_s ? reinterpret_cast<uint16_t *>(buf + off_s) : nullptr,
+                     rs * W + seg * Ln::SEGW, lane);
+        if (want_d && !slot_d) {  // depth straight to HBM: 16 B per lane, coalesced
+          float *drow = a.depth + ((size_t)e * H + i) * W + seg * Ln::SEGW;
+#pragma unroll
+          for (int g = 0; g < Ln::G; ++g) {
+            float *dp = drow + g * 32 * Ln::GW + lane * Ln::GW;
+            if constexpr (Ln::GW == 4) {
+              const PairOut &p = po[2 * g], &q = po[2 * g + 1];
+              asm volatile("st.global.L2::cache_hint.v4.f32 [%0], {%1,%2,%3,%4}, %5;" ::"l"(dp),
+                           "f"(p.d0), "f"(p.d1), "f"(q.d0), "f"(q.d1), "l"(dpol)
+                           : "memory");
+            } else {
+              *reinterpret_cast<float2 *>(dp) = make_float2(po[g].d0, po[g].d1);
+            }
+          }
+        }
+      }
+      fence_proxy_async();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(full + slot);
+      if (++slot == (unsigned)NSLOT) {
+        slot = 0;
+        ++use;
+      }
+    }
+  }
+}
+
+// Inverse-depth noise as a separate pass over a written depth batch (the
+// writers other than k_fill_ws); same per-pixel values as the fused path.
+__global__ void k_depth_noise(FillArgs a, float *depth) {
+  const long long p2 = blockIdx.x * (long long)blockDim.x + threadIdx.x;  // pixel pair
+  const int half = (a.W + 1) / 2;
+  const long long total = (long long)a.N * a.H * half;
+  if (p2 >= total) return;
+  const int cp = (int)(p2 % half);
+  const long long er = p2 / half;
+  const int row = (int)(er % a.H), env = (int)(er / a.H);
+  const float2 n = noise_pair(a, env, row, 2 * cp);
+  float *d = depth + ((size_t)env * a.H + row) * a.W + 2 * cp;
+  d[0] = noisy_depth(d[0], n.x, a.max_range);
+  if (2 * cp + 1 < a.W) d[1] = noisy_depth(d[1], n.y, a.max_range);
+}
+
+// One thread per pixel, any W/H; the same f16 arithmetic as the fast writers
+// (one half of each pair), so every path produces identical frames.
+__global__ void k_fill_generic(FillArgs a) {
+  const long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const long long total = (long long)a.N * a.H * a.W;
+  if (p >= total) return;
+  const int j = (int)(p % a.W);
+  const long long ei = p / a.W;
+  const uint32_t i = (uint32_t)(ei % a.H);
+  const int e = (int)(ei / a.H);
+  const size_t q = (size_t)e * a.W + rec_pos(j, a.cpl);
+  const float4 A = a.ra[q], B = a.rb[q];
+  const RowRec R = a.rows[i];
+  const uint32_t l = __float_as_uint(A.w);
+  const uint32_t lo = l & 0xffffu, hi = l >> 16;
+  const uint32_t inv = a.invh[(size_t)inv_row(i, a.H) * a.W + j];
+  PairOut o = shade_pair(i, R, lo, hi, lo, hi, A.x, A.x, h2_pack(A.y, 0.f), h2_pack(B.x, 0.f),
+                         h2_pack(B.y, 0.f), h2_pack(B.z, 0.f), __float_as_uint(B.w) & 0xffffu,
+                         inv);
+  if (a.depth) a.depth[p] = o.d0;
+  if (a.sem) a.sem[p] = (uint16_t)o.s;
+  if (a.rgb) {
+    a.rgb[3 * p] = (uint8_t)o.r;
+    a.rgb[3 * p + 1] = (uint8_t)o.g;
+    a.rgb[3 * p + 2] = (uint8_t)o.b;
+  }
+}
+
+
+}  // namespace nvk
