@@ -1,10 +1,10 @@
 // geom.cuh -- shared FP64 geometry of the navsim hot path: the exact segment
-// test, raycast_grid's DDA (thread and warp variants), disc_cast and
+// test, raycast_grid's DDA, disc_cast and
 // min_seg_distance (see kernels.cuh for the kernel overview).
 //
 // Exactness: every FP64 operation that decides coverage, semantics, depth or
 // pose uses the nvx:: _rn helpers (no FMA contraction), replicating the
-// reference's operation order.  Shading is FP32 (RGB tolerance 1/255).
+// reference's operation order.
 #pragma once
 
 #include <cuda_runtime.h>
