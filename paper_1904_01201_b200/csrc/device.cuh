@@ -20,7 +20,9 @@
 
 #include <stdint.h>
 
+#ifndef NV_CHUNK
 #define NV_CHUNK 8  // entries per prefilter box (cast)
+#endif
 
 namespace nvd {
 

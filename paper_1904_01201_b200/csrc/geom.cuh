@@ -65,12 +65,27 @@ __device__ __forceinline__ bool seg_pre(double px, double py, double dx, double 
   return ok;
 }
 
+// The reference's exact path for a prefilter survivor.  `0 <= RN(rn/den) <= 1`
+// is decided without the division: seg_pre already rejected sign(rn) !=
+// sign(den) (so RN(rn/den) >= 0) and |rn| > |den| (1 + 1e-12), and for
+// |den| <= |rn| <= 2 |den| the difference |rn| - |den| is exact (Sterbenz):
+// RN(q) <= 1 iff q <= 1 + 2^-53 (the midpoint rounds to even, 1.0) iff
+// |rn| - |den| <= |den| 2^-53 (an exact power-of-two scaling).
+#ifndef NV_R_DIVFREE
+#define NV_R_DIVFREE 1
+#endif
 __device__ __forceinline__ void seg_exact(double den, double tn, double rn, int i,
                                           double &best_t, int &best_i) {
   double t = div(tn, den);
   if (t < 0.0 || t > best_t) return;
-  double r = div(rn, den);
-  if (0.0 <= r && r <= 1.0) {
+#if NV_R_DIVFREE
+  const double ar = fabs(rn), ad = fabs(den);
+  const bool r_ok = ar <= ad || sub(ar, ad) <= ad * 0x1p-53;
+#else
+  const double r = div(rn, den);
+  const bool r_ok = 0.0 <= r && r <= 1.0;
+#endif
+  if (r_ok) {
     if (t < best_t || i < best_i) {
       best_t = t;
       best_i = i;
