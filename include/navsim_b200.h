@@ -129,7 +129,9 @@ int nv_set_fused(nv_ctx *ctx, int on);
 /* Column cast: 0 (default) = per-column DDA over the grid (raycast_grid's
  * walk) -- one thread per ray, or one warp per ray (lanes split each cell's
  * entries) when the batch has at most 16384 rays (latency-bound sizes);
- * 3 / 4 force the thread / warp variant; 1 = binned: one CTA per env projects the frustum's segments to
+ * 3 / 4 force the thread / warp variant, 5 = the DDA by lanes refilling
+ * from per-warp ray pools (no lane idles behind its warp's longest ray);
+ * 1 = binned: one CTA per env projects the frustum's segments to
  * column spans and tests (segment, column) pairs exactly (raycast_all's
  * lexicographic minimum, which the reference defines raycast_grid to equal),
  * 2 = the DDA of mode 0 fused with the agent step in nv_step_render (one CTA

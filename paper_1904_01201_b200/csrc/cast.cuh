@@ -228,9 +228,162 @@ __global__ void __launch_bounds__(128) k_column_cast_warp(EnvView ev, SceneView 
   k_column_cast_warp_body(ev, sc, cam, ro, t_max, gps, compass, e, j);
 }
 
+// ---- ray-pool cast: lanes refill from a per-warp pool of rays --------------
+//
+// k_column_cast_pool: each warp owns a pool of consecutive rays (env-major,
+// column-minor) and walks them as one DDA cell per loop iteration per lane;
+// a lane whose ray finished writes its column record and takes the next ray
+// of the pool in the same iteration, so lanes do not idle behind the warp's
+// longest ray (the per-ray DDA leaves half the lanes idle on average).  The
+// visit order and early-out of every ray are raycast_grid's.
+struct RayState {
+  double px, py, dx, dy, tnx, tny, tdx, tdy, best_t;
+  long long cx, cy;
+  int stepx, stepy, best_i, e, j;
+  int4 rec;
+  float dxf, dyf, sd;
+};
+
+// _column_directions + the DDA prologue of raycast_grid; false when the ray
+// is already finished (NaN input: the reference would spin, the DDA returns
+// the empty hit).
+__device__ __forceinline__ bool ray_begin(const EnvView &ev, const SceneView &sc,
+                                          const CamView &cam, int e, int j, RayState &r) {
+  r.e = e;
+  r.j = j;
+  r.px = ev.x[e];
+  r.py = ev.y[e];
+  const double c = ev.ch[e], s = ev.sh[e];
+  const double u = __ldg(cam.u + j);
+  r.dx = add(c, mul(u, s));
+  r.dy = add(s, mul(u, -c));
+  r.best_t = NV_INF;
+  r.best_i = -1;
+  if (isnan(r.px) || isnan(r.py) || isnan(r.dx) || isnan(r.dy)) return false;
+  const double cell = 1.0;
+  r.cx = (long long)floor(sub(r.px, sc.x0));
+  r.cy = (long long)floor(sub(r.py, sc.y0));
+  r.stepx = r.dx > 0.0 ? 1 : -1;
+  r.stepy = r.dy > 0.0 ? 1 : -1;
+  if (r.dx != 0.0) {
+    const double nbx = add(sc.x0, mul((double)(r.cx + (r.dx > 0.0 ? 1 : 0)), cell));
+    r.tnx = div(sub(nbx, r.px), r.dx);
+    r.tdx = fabs(div(cell, r.dx));
+  } else {
+    r.tnx = NV_INF;
+    r.tdx = NV_INF;
+  }
+  if (r.dy != 0.0) {
+    const double nby = add(sc.y0, mul((double)(r.cy + (r.dy > 0.0 ? 1 : 0)), cell));
+    r.tny = div(sub(nby, r.py), r.dy);
+    r.tdy = fabs(div(cell, r.dy));
+  } else {
+    r.tny = NV_INF;
+    r.tdy = NV_INF;
+  }
+  r.dxf = (float)r.dx;
+  r.dyf = (float)r.dy;
+  r.sd = (fabsf(r.dxf) + fabsf(r.dyf)) * (1.0f + 0x1p-20f);
+  r.rec = make_int4(0, 0, 0, 0);
+  if (0 <= r.cx && r.cx < sc.gnx && 0 <= r.cy && r.cy < sc.gny)
+    r.rec = __ldg(sc.cells + (r.cy * sc.gnx + r.cx));
+  return true;
+}
+
+// One iteration of raycast_grid's loop (one cell); true when the ray is done.
+__device__ __forceinline__ bool ray_cell(const SceneView &sc, RayState &r, double t_max) {
+  const long long gnx = sc.gnx, gny = sc.gny;
+  const double t_exit = r.tnx < r.tny ? r.tnx : r.tny;
+  long long ncx = r.cx, ncy = r.cy;
+  double ntnx = r.tnx, ntny = r.tny;
+  if (r.tnx < r.tny) {
+    ncx += r.stepx;
+    ntnx = add(r.tnx, r.tdx);
+  } else {
+    ncy += r.stepy;
+    ntny = add(r.tny, r.tdy);
+  }
+  int4 nrec = make_int4(0, 0, 0, 0);
+  if (!(t_exit > t_max) && 0 <= ncx && ncx < gnx && 0 <= ncy && ncy < gny)
+    nrec = __ldg(sc.cells + (ncy * gnx + ncx));
+  cell_tests(sc, r.cx, r.cy, r.rec, r.px, r.py, r.dx, r.dy, r.dxf, r.dyf, r.sd, r.dxf >= 0.0f,
+             r.dyf >= 0.0f, r.best_t, r.best_i);
+  if (r.best_t <= t_exit || t_exit > t_max) return true;
+  r.cx = ncx;
+  r.cy = ncy;
+  r.tnx = ntnx;
+  r.tny = ntny;
+  r.rec = nrec;
+  if (r.cx < 0 || r.cx >= gnx || r.cy < 0 || r.cy >= gny) {
+    const bool out_x = (r.cx < 0 && r.dx <= 0.0) || (r.cx >= gnx && r.dx >= 0.0);
+    const bool out_y = (r.cy < 0 && r.dy <= 0.0) || (r.cy >= gny && r.dy >= 0.0);
+    if (out_x || out_y) return true;
+  }
+  return false;
+}
+
+__device__ __forceinline__ void ray_finish(const EnvView &ev, const SceneView &sc,
+                                           const CamView &cam, const RecOut &ro,
+                                           const RayState &r, double *gps, double *compass) {
+  ColRec rc;
+  column_epilogue(sc, cam, r.best_t, r.best_i, r.dx, r.dy, rc);
+  put_rec(ro, r.e, r.j, rc);
+  if (r.j == 0 && (gps || compass)) {
+    const int e = r.e;
+    const double ddx = sub(r.px, ev.ox[e]), ddy = sub(r.py, ev.oy[e]);
+    const double fc = ev.fc[e], fs = ev.fs[e];
+    if (gps) {
+      gps[2 * e] = sub(mul(fc, ddx), mul(fs, ddy));
+      gps[2 * e + 1] = add(mul(fs, ddx), mul(fc, ddy));
+    }
+    if (compass) compass[e] = nvx::wrap_angle(sub(ev.h[e], ev.oh[e]));
+  }
+}
+
+__global__ void __launch_bounds__(128) k_column_cast_pool(EnvView ev, SceneView sc, CamView cam,
+                                                          RecOut ro, double t_max, double *gps,
+                                                          double *compass, int pool) {
+  const int lane = threadIdx.x & 31;
+  const long long n_rays = (long long)ev.n * cam.W;
+  const long long wid = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const long long lo = wid * pool;
+  if (lo >= n_rays) return;
+  const long long hi = min(n_rays, lo + pool);
+  long long next = lo;  // warp-uniform
+  RayState r;
+  bool active = false;
+  for (;;) {
+    // refill idle lanes from the pool (lane order keeps rays adjacent)
+    const unsigned idle = __ballot_sync(0xffffffffu, !active);
+    const long long avail = hi - next;
+    if (!active) {
+      const int rank = __popc(idle & ((1u << lane) - 1u));
+      if (rank < avail) {
+        const long long g = next + rank;
+        const int e = (int)(g / cam.W);
+        const int j = (int)(g - (long long)e * cam.W);
+        active = ray_begin(ev, sc, cam, e, j, r);
+        if (!active) ray_finish(ev, sc, cam, ro, r, gps, compass);  // NaN pose: empty hit
+      }
+    }
+    next += min((long long)__popc(idle), avail);
+    if (!__any_sync(0xffffffffu, active)) {
+      if (next >= hi) break;
+      continue;
+    }
+    if (active && ray_cell(sc, r, t_max)) {
+      ray_finish(ev, sc, cam, ro, r, gps, compass);
+      active = false;
+    }
+  }
+}
+
 // One thread per (env, column).  With `ready`: launched as a programmatic
 // dependent of k_agent_step; waits per env instead of for the whole step.
-__global__ void __launch_bounds__(128) k_column_cast(EnvView ev, SceneView sc, CamView cam,
+#ifndef NV_CAST_KMINB
+#define NV_CAST_KMINB 1  // min resident CTAs/SM for the thread-per-ray cast (register cap)
+#endif
+__global__ void __launch_bounds__(128, NV_CAST_KMINB) k_column_cast(EnvView ev, SceneView sc, CamView cam,
                                                      RecOut ro, double t_max,
                                                      double *gps, double *compass,
                                                      unsigned *ready, unsigned *arrive) {

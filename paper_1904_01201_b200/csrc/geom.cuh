@@ -196,11 +196,6 @@ __device__ __forceinline__ void test_cell_f32(const SceneView &sc, int q0, int q
   }
 }
 
-// raycast_grid (_kernels.py:51-120), one ray, exact replica of the DDA.
-// The walk is software-pipelined: the next cell's record {q0, q1, bound} is
-// loaded (one 16-byte load) before the current cell's entries are tested, so
-// the cell-to-cell latency overlaps the tests; the visit order and the
-// early-out are the reference's.
 #ifndef NV_CAST_NB
 #define NV_CAST_NB 8
 #endif
@@ -213,6 +208,65 @@ __device__ __forceinline__ void test_cell_f32(const SceneView &sc, int q0, int q
 #ifndef NV_CAST_NCB
 #define NV_CAST_NCB 4  // run boxes loaded per round
 #endif
+// The tests of one DDA cell (record `rec`) for a ray: run boxes, f32 side
+// tests, exact FP64 tests of the survivors; updates (best_t, best_i).
+__device__ __forceinline__ void cell_tests(const SceneView &sc, long long cx, long long cy,
+                                           const int4 &rec, double px, double py, double dx,
+                                           double dy, float dxf, float dyf, float sd,
+                                           bool pos_dx, bool pos_dy, double &best_t,
+                                           int &best_i) {
+  if (rec.y > rec.x) {
+    const double X0 = add(sc.x0, (double)cx), Y0 = add(sc.y0, (double)cy);
+    const float pxr = (float)sub(px, X0), pyr = (float)sub(py, Y0);
+    CellF cf;
+    cf.cp = fmaf(dxf, pyr, -(dyf * pxr));
+    cf.E = NV_K32 * sd * (__int_as_float(rec.z) + fabsf(pxr) + fabsf(pyr) + 1e-30f);
+#if NV_CAST_CHUNKS
+    // s(x, y) = d x ((x, y) - p) is linear, so over a run's box it is
+    // bounded by two corners; a run whose box lies beyond +-E on one side
+    // holds no entry the per-entry side test would keep.
+    // The boxes of up to NV_CAST_NCB runs are loaded together (one memory
+    // round trip per cell in the common case); a passing run's f64 entries
+    // are prefetched into L1 before its f32 side tests, so the exact tests
+    // of its survivors hit L1.
+    const int nch = (rec.y - rec.x + NV_CHUNK - 1) / NV_CHUNK;
+    for (int c0 = 0; c0 < nch; c0 += NV_CAST_NCB) {
+      float4 bb[NV_CAST_NCB];
+#pragma unroll
+      for (int k = 0; k < NV_CAST_NCB; ++k) bb[k] = __ldg(sc.chunks + rec.w + min(c0 + k, nch - 1));
+      unsigned pass = 0;
+#pragma unroll
+      for (int k = 0; k < NV_CAST_NCB; ++k) {
+        const float4 b = bb[k];
+        const float smin = fmaf(dxf, pos_dx ? b.y : b.w, -(dyf * (pos_dy ? b.z : b.x))) - cf.cp;
+        const float smax = fmaf(dxf, pos_dx ? b.w : b.y, -(dyf * (pos_dy ? b.x : b.z))) - cf.cp;
+        const bool ok = c0 + k < nch && !(smin > cf.E || smax < -cf.E);
+        pass |= (ok ? 1u : 0u) << k;
+      }
+      for (unsigned m = pass; m; m &= m - 1) {  // prefetch first, then test
+        const int q = rec.x + (c0 + __ffs(m) - 1) * NV_CHUNK;
+        const char *p = reinterpret_cast<const char *>(sc.ent + q);
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(p + 128));
+      }
+      while (pass) {
+        const int q = rec.x + (c0 + __ffs(pass) - 1) * NV_CHUNK;
+        pass &= pass - 1;
+        test_cell_f32<NV_CAST_NB>(sc, q, min(q + NV_CHUNK, rec.y), cf, px, py, dx, dy, dxf,
+                                  dyf, best_t, best_i);
+      }
+    }
+#else
+    test_cell_f32<NV_CAST_NB>(sc, rec.x, rec.y, cf, px, py, dx, dy, dxf, dyf, best_t, best_i);
+#endif
+  }
+}
+
+// raycast_grid (_kernels.py:51-120), one ray, exact replica of the DDA.
+// The walk is software-pipelined: the next cell's record {q0, q1, bound} is
+// loaded (one 16-byte load) before the current cell's entries are tested, so
+// the cell-to-cell latency overlaps the tests; the visit order and the
+// early-out are the reference's.
 __device__ __forceinline__ void ray_grid(const SceneView &sc, double px, double py,
                                          double dx, double dy, double t_max,
                                          double &out_t, int &out_i) {
@@ -268,51 +322,7 @@ __device__ __forceinline__ void ray_grid(const SceneView &sc, double px, double 
     }
     int4 nrec = make_int4(0, 0, 0, 0);
     if (!(t_exit > t_max) && inb(ncx, ncy)) nrec = __ldg(sc.cells + (ncy * gnx + ncx));
-    if (rec.y > rec.x) {
-      const double X0 = add(sc.x0, (double)cx), Y0 = add(sc.y0, (double)cy);
-      const float pxr = (float)sub(px, X0), pyr = (float)sub(py, Y0);
-      CellF cf;
-      cf.cp = fmaf(dxf, pyr, -(dyf * pxr));
-      cf.E = NV_K32 * sd * (__int_as_float(rec.z) + fabsf(pxr) + fabsf(pyr) + 1e-30f);
-#if NV_CAST_CHUNKS
-      // s(x, y) = d x ((x, y) - p) is linear, so over a run's box it is
-      // bounded by two corners; a run whose box lies beyond +-E on one side
-      // holds no entry the per-entry side test would keep.
-      // The boxes of up to NV_CAST_NCB runs are loaded together (one memory
-      // round trip per cell in the common case); a passing run's f64 entries
-      // are prefetched into L1 before its f32 side tests, so the exact tests
-      // of its survivors hit L1.
-      const int nch = (rec.y - rec.x + NV_CHUNK - 1) / NV_CHUNK;
-      for (int c0 = 0; c0 < nch; c0 += NV_CAST_NCB) {
-        float4 bb[NV_CAST_NCB];
-#pragma unroll
-        for (int k = 0; k < NV_CAST_NCB; ++k) bb[k] = __ldg(sc.chunks + rec.w + min(c0 + k, nch - 1));
-        unsigned pass = 0;
-#pragma unroll
-        for (int k = 0; k < NV_CAST_NCB; ++k) {
-          const float4 b = bb[k];
-          const float smin = fmaf(dxf, pos_dx ? b.y : b.w, -(dyf * (pos_dy ? b.z : b.x))) - cf.cp;
-          const float smax = fmaf(dxf, pos_dx ? b.w : b.y, -(dyf * (pos_dy ? b.x : b.z))) - cf.cp;
-          const bool ok = c0 + k < nch && !(smin > cf.E || smax < -cf.E);
-          pass |= (ok ? 1u : 0u) << k;
-        }
-        for (unsigned m = pass; m; m &= m - 1) {  // prefetch first, then test
-          const int q = rec.x + (c0 + __ffs(m) - 1) * NV_CHUNK;
-          const char *p = reinterpret_cast<const char *>(sc.ent + q);
-          asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
-          asm volatile("prefetch.global.L1 [%0];" ::"l"(p + 128));
-        }
-        while (pass) {
-          const int q = rec.x + (c0 + __ffs(pass) - 1) * NV_CHUNK;
-          pass &= pass - 1;
-          test_cell_f32<NV_CAST_NB>(sc, q, min(q + NV_CHUNK, rec.y), cf, px, py, dx, dy, dxf,
-                                    dyf, best_t, best_i);
-        }
-      }
-#else
-      test_cell_f32<NV_CAST_NB>(sc, rec.x, rec.y, cf, px, py, dx, dy, dxf, dyf, best_t, best_i);
-#endif
-    }
+    cell_tests(sc, cx, cy, rec, px, py, dx, dy, dxf, dyf, sd, pos_dx, pos_dy, best_t, best_i);
     if (best_t <= t_exit || t_exit > t_max) break;
 #if NV_CAST_PF_NEXT
     if (nrec.y > nrec.x) {  // the next cell's run boxes and first entries -> L1

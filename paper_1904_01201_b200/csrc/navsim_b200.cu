@@ -155,6 +155,7 @@ struct nv_ctx {
   int64_t launches = 0;
   int cast_mode = 0;  // 0: per-column DDA (default), 1: binned (tile-binned segment setup)
   bool cast_queue = false;
+  int cast_pool = 0;       // > 0: ray-pool cast with this many rays per warp (cast mode 0)
   bool pdl = false;        // agent step -> cast programmatic dependent launch
   bool pdl_armed = false, pdl_init = false;
   DevBuf pdl_ready, pdl_arrive;  // column cast by persistent warps over a work counter (opt-in: slower)
@@ -749,6 +750,15 @@ int do_cast(nv_ctx *c, int cam, double *gps, double *compass, cudaStream_t st) {
         compass);
     return check_launch(c);
   }
+  if (c->cast_mode == 5 || (c->cast_mode == 0 && c->cast_pool > 0)) {  // ray pools
+    const int pool = c->cast_pool > 0 ? c->cast_pool : 64;
+    const long long warps = (total + pool - 1) / pool;
+    Prof pf(c, st, 1);
+    nvk::k_column_cast_pool<<<blocks_for(warps * 32, 128), 128, 0, st>>>(
+        c->env_view(), c->scene_view(), cam_view(k), rec_out(k, c->n_envs), k.max_range, gps,
+        compass, pool);
+    return check_launch(c);
+  }
   static const int cast_block = [] {  // tuning knob: threads per cast CTA (32..128)
     const char *e = getenv("NAVSIM_CAST_BLOCK");
     const int v = e ? atoi(e) : 0;
@@ -778,7 +788,7 @@ int do_cast(nv_ctx *c, int cam, double *gps, double *compass, cudaStream_t st) {
 }
 
 int nv_set_cast_mode_(nv_ctx *c, int mode) {
-  if (mode < 0 || mode > 4)
+  if (mode < 0 || mode > 5)
     return fail(NV_ERR_ARG, "cast mode must be 0 (dda, auto), 1 (binned), 2 (dda fused with the "
                             "step), 3 (dda, thread per ray) or 4 (dda, warp per ray)");
   c->cast_mode = mode;
@@ -829,6 +839,7 @@ int nv_create(int device, nv_ctx **out) {
   c->device = device;
   if (const char *q = getenv("NAVSIM_CAST_QUEUE")) c->cast_queue = atoi(q) != 0;  // A/B knob
   if (const char *q = getenv("NAVSIM_PDL")) c->pdl = atoi(q) != 0;                // A/B knob
+  if (const char *q = getenv("NAVSIM_CAST_POOL")) c->cast_pool = atoi(q);         // A/B knob
   cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device);
   cudaDeviceGetAttribute(&c->max_smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
   *out = c;

@@ -153,7 +153,7 @@ def _oracle_scene(oracle, sc):
 ])
 # cast: warp per ray (small batch), thread per ray, thread per ray overlapped
 # with the agent step (programmatic dependent launch, per-env ready flags)
-@pytest.mark.parametrize("cast_mode", [0, 3, 5])
+@pytest.mark.parametrize("cast_mode", [0, 3, 5, 6])  # 6: ray-pool cast (mode 5)
 def test_batch_step_render_vs_oracle(nb, oracle_mod, cfg, W, H, n_envs, steps, cast_mode):
     """Batched step+render (device cos/sin, device DDA, TMA fill) vs the oracle
     run on the same actions: poses 1e-6, frames at the stated tolerances."""
@@ -164,7 +164,8 @@ def test_batch_step_render_vs_oracle(nb, oracle_mod, cfg, W, H, n_envs, steps, c
              nb.SensorConfig("semantic", W, H), nb.SensorConfig("gps_compass"))
     sim = nb.BatchSimulator(sc.segments, sc.semantic_ids, sc.albedo, n_envs, sensor_configs=suite,
                             floor_color=sc.floor_color, ceiling_color=sc.ceiling_color)
-    nat.check(sim.ctx.lib.nv_set_cast_mode(sim.ctx.handle, min(cast_mode, 3)))
+    nat.check(sim.ctx.lib.nv_set_cast_mode(sim.ctx.handle,
+                                           {0: 0, 3: 3, 5: 3, 6: 5}[cast_mode]))
     nat.check(sim.ctx.lib.nv_set_overlap(sim.ctx.handle, int(cast_mode == 5)))
     poses = synth.sample_poses(sc, n_envs, seed=17)
     sim.reset(poses[:, :2], poses[:, 2])
@@ -396,7 +397,7 @@ def test_cast_modes_agree(nb, cfg, W, H, n):
     for s in range(acts.shape[0]):
         sim.step(acts[s], render=False)
         outs = []
-        for mode in (0, 1, 3, 4):
+        for mode in (0, 1, 3, 4, 5):
             nat.check(c.lib.nv_set_cast_mode(c.handle, mode))
             sim.render()
             torch.cuda.synchronize()
