@@ -155,7 +155,8 @@ struct nv_ctx {
   int64_t launches = 0;
   int cast_mode = 0;  // 0: per-column DDA (default), 1: binned (tile-binned segment setup)
   bool cast_queue = false;
-  int cast_pool = 0;       // > 0: ray-pool cast with this many rays per warp (cast mode 0)
+  int cast_pool = 0;
+  bool e2e_mapped = true;   // host-buffer graph path: zero-copy actions / results       // > 0: ray-pool cast with this many rays per warp (cast mode 0)
   bool pdl = false;        // agent step -> cast programmatic dependent launch
   bool pdl_armed = false, pdl_init = false;
   DevBuf pdl_ready, pdl_arrive;  // column cast by persistent warps over a work counter (opt-in: slower)
@@ -840,6 +841,7 @@ int nv_create(int device, nv_ctx **out) {
   if (const char *q = getenv("NAVSIM_CAST_QUEUE")) c->cast_queue = atoi(q) != 0;  // A/B knob
   if (const char *q = getenv("NAVSIM_PDL")) c->pdl = atoi(q) != 0;                // A/B knob
   if (const char *q = getenv("NAVSIM_CAST_POOL")) c->cast_pool = atoi(q);         // A/B knob
+  if (const char *q = getenv("NAVSIM_E2E_MAPPED")) c->e2e_mapped = atoi(q) != 0;  // A/B knob
   cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device);
   cudaDeviceGetAttribute(&c->max_smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
   *out = c;
@@ -1216,19 +1218,25 @@ int nv_step_render_host(nv_ctx *c, const int8_t *actions_host, int cam, uint32_t
       CK(cudaStreamCreateWithFlags(&c->e_stream, cudaStreamNonBlocking));
       CK(cudaEventCreateWithFlags(&c->e_ev, cudaEventDisableTiming));
     }
+    // pinned, mapped staging: with e2e_mapped the kernels read the actions
+    // from and write the packed step results to host memory directly (no
+    // copy nodes in the graph)
     if (c->e_hin_bytes < N) {
       if (c->e_hin) cudaFreeHost(c->e_hin);
-      CK(cudaMallocHost(&c->e_hin, N));
+      CK(cudaHostAlloc(&c->e_hin, N, cudaHostAllocMapped));
       c->e_hin_bytes = N;
+      if (c->e_graph) cudaGraphExecDestroy(c->e_graph);
+      c->e_graph = nullptr;
     }
     if (c->e_hout_bytes < pack) {
       if (c->e_hout) cudaFreeHost(c->e_hout);
-      CK(cudaMallocHost(&c->e_hout, pack));
+      CK(cudaHostAlloc(&c->e_hout, pack, cudaHostAllocMapped));
       c->e_hout_bytes = pack;
       if (c->e_graph) cudaGraphExecDestroy(c->e_graph);
       c->e_graph = nullptr;
     }
-    const int key[3] = {cam, (int)(channels | (want_rgb ? 8u : 0u) | (want_d ? 16u : 0u) | (want_s ? 32u : 0u)),
+    const int key[3] = {cam, (int)(channels | (want_rgb ? 8u : 0u) | (want_d ? 16u : 0u) |
+                                   (want_s ? 32u : 0u) | (c->e2e_mapped ? 64u : 0u)),
                         c->fill_mode * 16 + c->cast_mode * 2 + (c->fused ? 1 : 0)};
     const bool same = c->e_graph && c->e_key_n == c->n_envs && c->e_key_gen == c->gen &&
                       key[0] == c->e_key[0] &&
@@ -1237,14 +1245,26 @@ int nv_step_render_host(nv_ctx *c, const int8_t *actions_host, int cam, uint32_t
     if (!same) {
       if (c->e_graph) cudaGraphExecDestroy(c->e_graph);
       c->e_graph = nullptr;
+      const int8_t *acts = c->e_act.as<int8_t>();
+      double *o_gps = d_gps, *o_comp = d_comp, *o_disp = d_disp;
+      uint8_t *o_coll = d_coll;
+      if (c->e2e_mapped) {
+        void *din = nullptr, *dout = nullptr;
+        CK(cudaHostGetDevicePointer(&din, c->e_hin, 0));
+        CK(cudaHostGetDevicePointer(&dout, c->e_hout, 0));
+        acts = static_cast<const int8_t *>(din);
+        o_gps = static_cast<double *>(dout);
+        o_comp = o_gps + 2 * N;
+        o_disp = o_comp + N;
+        o_coll = static_cast<uint8_t *>(dout) + 32 * N;
+      }
       CK(cudaStreamBeginCapture(es, cudaStreamCaptureModeThreadLocal));
-      cudaMemcpyAsync(c->e_act.p, c->e_hin, N, cudaMemcpyHostToDevice, es);
-      int rc = nv_step_render(c, c->e_act.as<int8_t>(), cam,
-                              want_rgb ? c->e_rgb.as<uint8_t>() : nullptr,
+      if (!c->e2e_mapped) cudaMemcpyAsync(c->e_act.p, c->e_hin, N, cudaMemcpyHostToDevice, es);
+      int rc = nv_step_render(c, acts, cam, want_rgb ? c->e_rgb.as<uint8_t>() : nullptr,
                               want_d ? c->e_depth.as<float>() : nullptr,
-                              want_s ? c->e_sem.as<uint16_t>() : nullptr, d_gps, d_comp, d_coll,
-                              d_disp, nullptr, es);
-      cudaMemcpyAsync(c->e_hout, pk, pack, cudaMemcpyDeviceToHost, es);
+                              want_s ? c->e_sem.as<uint16_t>() : nullptr, o_gps, o_comp, o_coll,
+                              o_disp, nullptr, es);
+      if (!c->e2e_mapped) cudaMemcpyAsync(c->e_hout, pk, pack, cudaMemcpyDeviceToHost, es);
       cudaGraph_t g = nullptr;
       cudaError_t ce = cudaStreamEndCapture(es, &g);
       if (rc != NV_OK) {
