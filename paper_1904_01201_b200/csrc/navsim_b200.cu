@@ -153,13 +153,13 @@ struct nv_ctx {
   void *e_hin = nullptr, *e_hout = nullptr;  // pinned staging (actions in, packed results out)
   size_t e_hin_bytes = 0, e_hout_bytes = 0;
   int64_t launches = 0;
-  int cast_mode = 0;  // 0: per-column DDA (default), 1: binned (tile-binned segment setup)
-  bool cast_queue = false;
-  int cast_pool = 0;
-  bool e2e_mapped = true;   // host-buffer graph path: zero-copy actions / results       // > 0: ray-pool cast with this many rays per warp (cast mode 0)
-  bool pdl = false;        // agent step -> cast programmatic dependent launch
+  int cast_mode = 0;         // nv_set_cast_mode (include/navsim_b200.h)
+  bool cast_queue = false;   // column cast by persistent warps over a work counter (opt-in: slower)
+  int cast_pool = 0;         // > 0: ray-pool cast with this many rays per warp (cast mode 0)
+  bool e2e_mapped = true;    // host-buffer graph path: zero-copy actions / results
+  bool pdl = false;          // agent step -> cast programmatic dependent launch
   bool pdl_armed = false, pdl_init = false;
-  DevBuf pdl_ready, pdl_arrive;  // column cast by persistent warps over a work counter (opt-in: slower)
+  DevBuf pdl_ready, pdl_arrive;
   int fill_mode = 3;   // 0 direct stores, 1 per-warp TMA stages, 2 warp-specialised, 3 auto
   bool fused = false;  // nv_step_render uses the megakernel when the layout allows (opt-in)
   // optional per-kernel CUDA-event timing (bench roofline evidence)
