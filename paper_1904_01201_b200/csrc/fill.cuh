@@ -142,9 +142,18 @@ __device__ __forceinline__ void bulk_wait_all() {
 __device__ __forceinline__ void fence_proxy_async() {
   asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
 }
+#ifndef NV_FRAME_POLICY
+#define NV_FRAME_POLICY 0  // L2 policy of frame stores: 0 evict_first, 1 evict_normal, 2 evict_last
+#endif
 __device__ __forceinline__ uint64_t policy_evict_first() {
   uint64_t p;
+#if NV_FRAME_POLICY == 1
+  asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;\n" : "=l"(p));
+#elif NV_FRAME_POLICY == 2
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(p));
+#else
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(p));
+#endif
   return p;
 }
 

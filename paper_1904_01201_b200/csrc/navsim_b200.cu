@@ -569,7 +569,12 @@ int launch_ws_kernel(nv_ctx *c, nvk::FillArgs &a, const nvk::FillWsLayout &L, si
     CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     configured[noise] = (int)smem;
   }
-  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(a.N, c->sm_count));
+  static const int ws_sms = [] {  // study knob: SMs given to the ws writer
+    const char *e = getenv("NAVSIM_WS_SMS");
+    return e ? atoi(e) : 0;
+  }();
+  const int sms = ws_sms > 0 ? std::min(ws_sms, c->sm_count) : c->sm_count;
+  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(a.N, sms));
   Prof pf(c, st, 2);
   kern<<<grid, (16 + 1) * 32, smem, st>>>(a, L);
   return check_launch(c);
