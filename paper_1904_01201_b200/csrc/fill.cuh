@@ -616,6 +616,9 @@ __global__ void __launch_bounds__(128) k_fill_direct(FillArgs a) {
 // lane prefetches the next item's column-record planes into a double buffer
 // with bulk copies.  Producers never touch L2: row records, the shading table
 // and column records are all shared-memory reads.
+#ifndef NV_WS_RELEASE_NOW
+#define NV_WS_RELEASE_NOW 1  // release each slot as soon as its bulk reads are done
+#endif
 #ifndef NV_WS_DEBUG
 #define NV_WS_DEBUG 0  // 1: producers skip rendering, 2: no bulk stores (bound studies)
 #endif
@@ -702,10 +705,17 @@ __global__ void __launch_bounds__(544, 1) k_fill_ws(FillArgs a, FillWsLayout L) 
         (void)buf; (void)pix0; (void)pol;
 #endif
         bulk_commit();
+#if NV_WS_RELEASE_NOW
+        // wait for this slot's smem reads and hand it back at once
+        bulk_wait_read<0>();
+        mbar_arrive(empty + slot);
+        (void)prev;
+#else
         if (k >= 1) {
           bulk_wait_read<1>();
           mbar_arrive(empty + prev);
         }
+#endif
         prev = slot;
         if (++slot == (unsigned)NSLOT) {
           slot = 0;

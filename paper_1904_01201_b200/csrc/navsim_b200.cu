@@ -602,7 +602,7 @@ int launch_fill_ws(nv_ctx *c, nvk::FillArgs &a, cudaStream_t st) {
     return e ? atoi(e) : 0;
   }();
   struct Opt { bool tab; int rpw, nmin, nmax; };
-  static const Opt opts[] = {{true, 2, 2, 4}, {true, 1, 2, 4}, {false, 2, 2, 4}, {false, 1, 2, 4}};
+  static const Opt opts[] = {{true, 1, 2, 4}, {true, 2, 2, 4}, {false, 1, 2, 4}, {false, 2, 2, 4}};
   nvk::FillWsLayout L;
   bool tab = false;
   int rpw = 0;
