@@ -337,6 +337,25 @@ __device__ __forceinline__ void shade_row(uint32_t i, const RowRec &R, const Col
                        cr.sw[c], iv[c]);
 }
 
+// A row that is plane (ceiling / floor / their void) in all of the lane's
+// columns: every pixel takes the row record's depth, semantic, colour and
+// cosine numerator; only the per-pixel 1/|(d, v)| differs.  Same arithmetic
+// as shade_pair with an all-plane mask, so the pixels are identical.
+template <int CPL>
+__device__ __forceinline__ void shade_row_plane(const RowRec &R, const uint32_t (&iv)[CPL / 2],
+                                                PairOut (&po)[CPL / 2]) {
+#pragma unroll
+  for (int c = 0; c < CPL / 2; ++c) {
+    const uint32_t t = h2_fma(R.num2, iv[c], NV_H2_POINT2);
+    po[c].r = h2_fma(R.r2, t, NV_H2_1024);
+    po[c].g = h2_fma(R.g2, t, NV_H2_1024);
+    po[c].b = h2_fma(R.b2, t, NV_H2_1024);
+    po[c].s = R.sem2;
+    po[c].d0 = R.depth_p;
+    po[c].d1 = R.depth_p;
+  }
+}
+
 // Writes the lane's shaded pixels of one row segment into a buffer laid out
 // like the frame (shared-memory stage / slot): px0 = pixel index of the
 // segment's first column in the buffer.
@@ -738,6 +757,14 @@ __global__ void __launch_bounds__(544, 1) k_fill_ws(FillArgs a, FillWsLayout L) 
     ColRegs<CPL> cr;
     const float4 *cA = cols_s + (size_t)(it & 1) * 2 * W + seg * Ln::SEGW;
     load_cols_smem<CPL>(cA, cA + W, lane, cr);
+    // rows [0, plane_lo) are ceiling and rows [plane_hi, H) floor in all of
+    // this lane's columns
+    uint32_t plane_lo = cr.lo[0], plane_hi = cr.hi[0];
+#pragma unroll
+    for (int k = 1; k < CPL; ++k) {
+      plane_lo = min(plane_lo, cr.lo[k]);
+      plane_hi = max(plane_hi, cr.hi[k]);
+    }
     __syncwarp();
     if (lane == 0) mbar_arrive(colempty + (it & 1));
     for (int sl = 0; sl < slots_per_item; ++sl) {
@@ -758,7 +785,10 @@ __global__ void __launch_bounds__(544, 1) k_fill_ws(FillArgs a, FillWsLayout L) 
         else
           load_inv<CPL, true>(a.invh + (size_t)inv_row(i, H) * W + seg * Ln::SEGW, lane, iv);
         PairOut po[CPL / 2];
-        shade_row<CPL>(i, Rr, cr, iv, po);
+        if (i < plane_lo || i >= plane_hi)  // plane in every column of the lane
+          shade_row_plane<CPL>(Rr, iv, po);
+        else
+          shade_row<CPL>(i, Rr, cr, iv, po);
         if constexpr (NOISE) {
 #pragma unroll
           for (int c = 0; c < CPL / 2; ++c) {
