@@ -14,6 +14,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include "../../include/navsim_b200.h"
@@ -160,6 +161,8 @@ struct nv_ctx {
   bool pdl = false;          // agent step -> cast programmatic dependent launch
   bool pdl_armed = false, pdl_init = false;
   DevBuf pdl_ready, pdl_arrive;
+  // dynamic shared memory opted in per kernel on this context's device
+  std::unordered_map<const void *, size_t> smem_cfg;
   int fill_mode = 3;   // 0 direct stores, 1 per-warp TMA stages, 2 warp-specialised, 3 auto
   bool fused = false;  // nv_step_render uses the megakernel when the layout allows (opt-in)
   // optional per-kernel CUDA-event timing (bench roofline evidence)
@@ -403,6 +406,17 @@ int check_launch(nv_ctx *c) {
   return NV_OK;
 }
 
+// Opts kernel `fn` into `smem` bytes of dynamic shared memory on the context's
+// device (once per size increase).
+int set_smem(nv_ctx *c, const void *fn, size_t smem) {
+  size_t &have = c->smem_cfg[fn];
+  if (smem > have) {
+    CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    have = smem;
+  }
+  return NV_OK;
+}
+
 unsigned blocks_for(long long work, int per_block) {
   return (unsigned)std::max<long long>(1, (work + per_block - 1) / per_block);
 }
@@ -439,12 +453,7 @@ int launch_fill_tma(nv_ctx *c, nvk::FillArgs &a, cudaStream_t st) {
   const int warps = 4;
   const size_t smem = (size_t)a.H * sizeof(RowRec) + (size_t)warps * 2 * stage;
   auto kern = nvk::k_fill_tma<CPL, RW>;
-  static int configured_smem[3] = {0, 0, 0};
-  int slot = CPL == 2 ? 0 : (CPL == 4 ? 1 : 2);
-  if ((int)smem > configured_smem[slot]) {
-    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    configured_smem[slot] = (int)smem;
-  }
+  TRY(set_smem(c, (const void *)kern, smem));
   int per_sm = 0;
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, warps * 32, smem));
   per_sm = std::max(1, per_sm);
@@ -520,12 +529,7 @@ int launch_mega(nv_ctx *c, Camera &cam, const int8_t *actions, uint8_t *rgb, flo
   const int warps = 4;
   const size_t smem = (size_t)cam.H * sizeof(RowRec) + (size_t)warps * 2 * RW * segw * std::max(bpp, 1);
   auto kern = nvk::k_step_render<CPL, RW>;
-  static int configured_smem[3] = {0, 0, 0};
-  int slot = CPL == 2 ? 0 : (CPL == 4 ? 1 : 2);
-  if ((int)smem > configured_smem[slot]) {
-    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    configured_smem[slot] = (int)smem;
-  }
+  TRY(set_smem(c, (const void *)kern, smem));
   int per_sm = 0;
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, warps * 32, smem));
   per_sm = std::max(1, per_sm);
@@ -540,11 +544,7 @@ int launch_fill_direct(nv_ctx *c, nvk::FillArgs &a, cudaStream_t st) {
   const int warps = 4;
   auto kern = nvk::k_fill_direct<CPL>;
   const size_t smem = (size_t)a.H * sizeof(RowRec);
-  static int configured = 0;
-  if ((int)smem > configured) {
-    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    configured = (int)smem;
-  }
+  TRY(set_smem(c, (const void *)kern, smem));
   int per_sm = 0;
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, warps * 32, smem));
   per_sm = std::max(1, per_sm);
@@ -564,11 +564,7 @@ int launch_ws_kernel(nv_ctx *c, nvk::FillArgs &a, const nvk::FillWsLayout &L, si
                      cudaStream_t st) {
   const bool noise = a.noise_sigma > 0.0f && a.depth;
   auto kern = noise ? nvk::k_fill_ws<CPL, TAB, RPW, true> : nvk::k_fill_ws<CPL, TAB, RPW, false>;
-  static int configured[2] = {0, 0};
-  if ((int)smem > configured[noise]) {
-    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    configured[noise] = (int)smem;
-  }
+  TRY(set_smem(c, (const void *)kern, smem));
   static const int ws_sms = [] {  // study knob: SMs given to the ws writer
     const char *e = getenv("NAVSIM_WS_SMS");
     return e ? atoi(e) : 0;
@@ -717,12 +713,7 @@ int do_cast(nv_ctx *c, int cam, double *gps, double *compass, cudaStream_t st) {
     const size_t smem = (size_t)k.W * (8 + 8 + 8) + (size_t)NV_BIN_MAXCELLS * (16 + 4) +
                         (size_t)((k.W + 3) & ~3) * 4 + (size_t)((ntiles + 3) & ~3) * 4 +
                         (size_t)NV_HIT_CAP * 8 + 32;
-    static size_t configured = 0;
-    if (smem > configured) {
-      CK(cudaFuncSetAttribute(nvk::k_cast_binned, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              (int)smem));
-      configured = smem;
-    }
+    TRY(set_smem(c, (const void *)nvk::k_cast_binned, smem));
     Prof pf(c, st, 1);
     nvk::k_cast_binned<<<(unsigned)c->n_envs, 128, smem, st>>>(
         c->env_view(), c->scene_view(), cam_view(k), k.focal, rec_out(k, c->n_envs), gps, compass);
