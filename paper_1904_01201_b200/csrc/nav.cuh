@@ -28,7 +28,11 @@
 //                    termination, EpisodeOutcome records.
 #pragma once
 
+#include <cooperative_groups.h>
+
 #include "kernels.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace nvk {
 
@@ -180,24 +184,23 @@ __global__ void k_nav_field_init(double *fields, const int2 *goal_ij, int nx, in
 // global flag.  Update rule = dijkstra_grid's relaxation (_kernels.py:254-270):
 // axial +res, diagonal +res*sqrt(2) only when both axial cells are navigable;
 // only navigable cells carry distances.
-__global__ void __launch_bounds__(256) k_nav_relax(double *fields, NavView nv, double diag,
-                                                   const uint8_t *act_in, uint8_t *act_out,
-                                                   int *changed) {
+// One tile of one field relaxed to local convergence in shared memory (all
+// threads of the CTA).  Tile (and halo) distances are read through L2
+// (ld.cg): in the cooperative kernel other CTAs write them during the launch.
+__device__ __forceinline__ void relax_tile(double *D, const NavView &nv, double diag, int tx,
+                                           int ty, int ntx, int nty, const uint8_t *act_in,
+                                           uint8_t *act_out, int *changed) {
   __shared__ double sd[NV_NT + 2][NV_NT + 2];
   __shared__ uint8_t sm[NV_NT + 2][NV_NT + 2];
-  const int tx = blockIdx.x, ty = blockIdx.y, f = blockIdx.z;
-  const int ntx = gridDim.x, nty = gridDim.y;
-  const size_t tile_base = (size_t)f * ntx * nty;
-  if (!act_in[tile_base + (size_t)ty * ntx + tx]) return;
+  if (!__ldcg(act_in + (size_t)ty * ntx + tx)) return;
   const int nx = nv.nx, ny = nv.ny;
-  double *D = fields + (size_t)f * nx * ny;
   const int bx = tx * NV_NT, by = ty * NV_NT;
   for (int k = threadIdx.x; k < (NV_NT + 2) * (NV_NT + 2); k += blockDim.x) {
     const int ti = k / (NV_NT + 2), tj = k - ti * (NV_NT + 2);
     const int i = by + ti - 1, j = bx + tj - 1;
     const bool in = i >= 0 && i < ny && j >= 0 && j < nx;
     sm[ti][tj] = in ? nv.mask[(size_t)i * nx + j] : 0;
-    sd[ti][tj] = in ? D[(size_t)i * nx + j] : NV_INF;
+    sd[ti][tj] = in ? __ldcg(D + (size_t)i * nx + j) : NV_INF;
   }
   __syncthreads();
   const double res = nv.res;
@@ -241,9 +244,52 @@ __global__ void __launch_bounds__(256) k_nav_relax(double *fields, NavView nv, d
     }
     if (threadIdx.x < 9) {  // this tile and its 8 neighbours run next pass
       const int ay = ty + threadIdx.x / 3 - 1, ax = tx + threadIdx.x % 3 - 1;
-      if (ay >= 0 && ay < nty && ax >= 0 && ax < ntx) act_out[tile_base + (size_t)ay * ntx + ax] = 1;
+      if (ay >= 0 && ay < nty && ax >= 0 && ax < ntx) act_out[(size_t)ay * ntx + ax] = 1;
     }
     if (threadIdx.x == 0) atomicExch(changed, 1);
+  }
+  __syncthreads();  // shared tile buffers are reused by the next tile of this CTA
+}
+
+// One pass over all tiles of all fields (host-driven variant).
+__global__ void __launch_bounds__(256) k_nav_relax(double *fields, NavView nv, double diag,
+                                                   const uint8_t *act_in, uint8_t *act_out,
+                                                   int *changed) {
+  const int tx = blockIdx.x, ty = blockIdx.y, f = blockIdx.z;
+  const int ntx = gridDim.x, nty = gridDim.y;
+  const size_t tb = (size_t)f * ntx * nty;
+  relax_tile(fields + (size_t)f * nv.nx * nv.ny, nv, diag, tx, ty, ntx, nty, act_in + tb,
+             act_out + tb, changed);
+}
+
+// All passes in one cooperative launch: CTAs stride over the (field, tile)
+// list, a grid-wide barrier separates passes, and the run ends when a pass
+// changed nothing.  flags[0..1]: change flags of even / odd passes.
+__global__ void __launch_bounds__(256) k_nav_relax_coop(double *fields, NavView nv, double diag,
+                                                        uint8_t *act_a, uint8_t *act_b, int ntx,
+                                                        int nty, int k, int *flags) {
+  cg::grid_group grid = cg::this_grid();
+  const long long per_field = (long long)ntx * nty;
+  const long long ntiles = per_field * k;
+  for (int pass = 0;; ++pass) {
+    uint8_t *ain = (pass & 1) ? act_b : act_a;
+    uint8_t *aout = (pass & 1) ? act_a : act_b;
+    int *changed = flags + (pass & 1);
+    for (long long t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      const int f = (int)(t / per_field);
+      const long long r = t - (long long)f * per_field;
+      const int ty = (int)(r / ntx), tx = (int)(r - (long long)ty * ntx);
+      relax_tile(fields + (size_t)f * nv.nx * nv.ny, nv, diag, tx, ty, ntx, nty,
+                 ain + (size_t)f * per_field, aout + (size_t)f * per_field, changed);
+    }
+    grid.sync();
+    if (!__ldcg(changed)) break;
+    // this pass's input flags become the next pass's output: clear them
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < ntiles;
+         t += (long long)gridDim.x * blockDim.x)
+      ain[t] = 0;
+    if (blockIdx.x == 0 && threadIdx.x == 0) flags[(pass + 1) & 1] = 0;
+    grid.sync();
   }
 }
 
