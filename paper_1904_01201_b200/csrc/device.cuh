@@ -50,7 +50,6 @@ struct SceneView {
   const CellEntry *ent;  // starts[nc] entries
   const int32_t *items;  // same order, index only (disc casts)
   const float4 *entf;    // same order, f32 endpoints (a - X0c, b - X0c), X0c = x0 + cx
-  const float *cellb;    // per cell: max |endpoint - X0c|_1 over its items
   const int4 *cells;     // per cell: {starts[c], starts[c+1], bits(bound), first chunk}
   const float4 *chunks;  // per run of NV_CHUNK entries: f32 box (x0, y0, x1, y1), cell-relative
   const DiscEntry *dent; // per entry (same order as items): disc-cast record

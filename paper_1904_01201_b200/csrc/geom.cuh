@@ -101,40 +101,6 @@ __device__ __forceinline__ void seg_test(double px, double py, double dx, double
     seg_exact(den, tn, rn, i, best_t, best_i);
 }
 
-// Tests the bucket run [q0, q1) of one cell, NB entries per round with all
-// loads issued up front (memory-level parallelism); indices past the end are
-// clamped to q1-1 -- re-testing a segment cannot change a lexicographic min.
-template <int NB>
-__device__ __forceinline__ void test_cell(const SceneView &sc, int q0, int q1, double px,
-                                          double py, double dx, double dy, double &best_t,
-                                          int &best_i) {
-  for (int q = q0; q < q1; q += NB) {
-    double2 a[NB], e[NB];
-#pragma unroll
-    for (int k = 0; k < NB; ++k) {
-      const int qq = min(q + k, q1 - 1);
-      const double2 *p2 = reinterpret_cast<const double2 *>(sc.ent + qq);
-      a[k] = __ldg(p2);
-      e[k] = __ldg(p2 + 1);
-    }
-    double den[NB], tn[NB], rn[NB];
-    bool ok[NB];
-    bool any = false;
-#pragma unroll
-    for (int k = 0; k < NB; ++k) {
-      ok[k] = seg_pre(px, py, dx, dy, a[k].x, a[k].y, e[k].x, e[k].y, best_t, den[k], tn[k],
-                      rn[k]);
-      any |= ok[k];
-    }
-    if (any) {
-#pragma unroll
-      for (int k = 0; k < NB; ++k)
-        if (ok[k]) seg_exact(den[k], tn[k], rn[k], __ldg(sc.items + min(q + k, q1 - 1)), best_t,
-                             best_i);
-    }
-  }
-}
-
 // FP32 prefilter for one cell of the DDA (side test).  The ray's line
 // crosses segment [a, b] iff a and b are not strictly on the same side:
 // with s_a = d x (a - p) and s_b = d x (b - p), the reference's
@@ -153,16 +119,6 @@ __device__ __forceinline__ void test_cell(const SceneView &sc, int q0, int q1, d
 struct CellF {
   float cp, E;  // d x p_rel, error bound
 };
-
-__device__ __forceinline__ CellF cell_f32(const SceneView &sc, int cx, int cy, int c, double px,
-                                          double py, float dxf, float dyf, float sd) {
-  const double X0 = add(sc.x0, (double)cx), Y0 = add(sc.y0, (double)cy);
-  const float pxr = (float)sub(px, X0), pyr = (float)sub(py, Y0);
-  CellF f;
-  f.cp = fmaf(dxf, pyr, -(dyf * pxr));
-  f.E = NV_K32 * sd * (__ldg(sc.cellb + c) + fabsf(pxr) + fabsf(pyr) + 1e-30f);
-  return f;
-}
 
 // Tests the bucket run [q0, q1) of one cell: NB f32 side tests per round
 // (loads issued up front), then the exact FP64 test for the survivors.
@@ -360,60 +316,11 @@ __device__ __forceinline__ void ray_brute(const SceneView &sc, double px, double
 
 // Per-segment first-contact time of disc_cast (_kernels.py:405-459): the
 // minimum over the face / band / endpoint candidates of one segment, taken in
-// the reference's order with its strict `<`.  The reference's result is then
-// the lexicographic (t, idx) minimum over segments (its scan is ascending in
-// idx with strict `<`), which lets the warp scan candidates in any order.
-__device__ __forceinline__ double disc_seg_t(double px, double py, double ux, double uy,
-                                             double radius, double u2, double axi,
-                                             double ayi, double bxi, double byi) {
-  double best = NV_INF;
-  double exi = sub(bxi, axi), eyi = sub(byi, ayi);
-  double seg_len = nvx::sqrt_rn(add(mul(exi, exi), mul(eyi, eyi)));
-  if (seg_len <= 0.0) return best;
-  double tx = div(exi, seg_len), ty = div(eyi, seg_len);
-  double nx = -ty, ny = tx;
-  double relx = sub(px, axi), rely = sub(py, ayi);
-  double d0 = add(mul(relx, nx), mul(rely, ny));
-  double vn = add(mul(ux, nx), mul(uy, ny));
-  if (fabs(d0) >= radius) {
-    double side = d0 > 0.0 ? 1.0 : -1.0;
-    if (mul(vn, side) < 0.0) {
-      double t = div(sub(mul(side, radius), d0), vn);
-      if (0.0 <= t && t <= 1.0) {
-        double proj = add(mul(add(relx, mul(t, ux)), tx), mul(add(rely, mul(t, uy)), ty));
-        if (0.0 <= proj && proj <= seg_len) {
-          if (t < best) best = t;
-        }
-      }
-    }
-  } else {
-    double proj = add(mul(relx, tx), mul(rely, ty));
-    if (0.0 <= proj && proj <= seg_len && mul(vn, d0) < 0.0) {
-      if (0.0 < best) best = 0.0;
-    }
-  }
-#pragma unroll
-  for (int e = 0; e < 2; ++e) {
-    double cxp = e == 0 ? axi : bxi;
-    double cyp = e == 0 ? ayi : byi;
-    double wx = sub(px, cxp), wy = sub(py, cyp);
-    double b = add(mul(wx, ux), mul(wy, uy));
-    double c = sub(add(mul(wx, wx), mul(wy, wy)), mul(radius, radius));
-    if (c < 0.0) {
-      if (b < 0.0 && 0.0 < best) best = 0.0;
-      continue;
-    }
-    if (u2 == 0.0) continue;
-    double disc = sub(mul(b, b), mul(u2, c));
-    if (disc < 0.0) continue;
-    double t = div(sub(-b, nvx::sqrt_rn(disc)), u2);
-    if (0.0 <= t && t <= 1.0 && t < best) best = t;
-  }
-  return best;
-}
-
-// disc_seg_t with the segment's seg_len and unit tangent taken from its
-// DiscEntry (the identical values the reference recomputes per candidate).
+// the reference's order with its strict `<`; the segment's seg_len and unit
+// tangent come from its DiscEntry (the identical values the reference
+// recomputes per candidate).  The reference's result is then the
+// lexicographic (t, idx) minimum over segments (its scan is ascending in idx
+// with strict `<`), which lets the warp scan candidates in any order.
 __device__ __forceinline__ double disc_seg_t_pre(double px, double py, double ux, double uy,
                                                  double radius, double u2, const DiscEntry &d) {
   double best = NV_INF;

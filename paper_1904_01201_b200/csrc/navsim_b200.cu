@@ -118,7 +118,7 @@ struct nv_ctx {
   double gx0 = -0.5, gy0 = -0.5;
   int gnx = 1, gny = 1;
   int64_t nitems = 0;
-  DevBuf ax, ay, bx, by, ex, ey, nx, ny, sem, alb, starts, ent, items, entf, cellb, cells, chunks;
+  DevBuf ax, ay, bx, by, ex, ey, nx, ny, sem, alb, starts, ent, items, entf, cells, chunks;
   DevBuf dent, stx, sty;
   // agent
   double radius = 0.1, step = 0.25, turn_rad = 0.17453292519943295, sensor_h = 1.5;
@@ -188,7 +188,7 @@ struct nv_ctx {
     v.nx = nx.as<double>(); v.ny = ny.as<double>();
     v.sem = sem.as<uint16_t>(); v.alb255 = alb.as<float4>();
     v.starts = starts.as<int32_t>(); v.ent = ent.as<CellEntry>(); v.items = items.as<int32_t>();
-    v.entf = entf.as<float4>(); v.cellb = cellb.as<float>(); v.cells = cells.as<int4>();
+    v.entf = entf.as<float4>(); v.cells = cells.as<int4>();
     v.chunks = chunks.as<float4>();
     v.dent = dent.as<DiscEntry>(); v.stx = stx.as<double>(); v.sty = sty.as<double>();
     v.x0 = gx0; v.y0 = gy0; v.gnx = gnx; v.gny = gny; v.n = n;
@@ -918,7 +918,7 @@ int nv_scene_upload(nv_ctx *c, const double *segs, const uint16_t *sem, const do
   TRY(upload(c->ex, ex)); TRY(upload(c->ey, ey)); TRY(upload(c->nx, nx)); TRY(upload(c->ny, ny));
   TRY(upload(c->sem, sm)); TRY(upload(c->alb, alb));
   TRY(upload(c->starts, starts)); TRY(upload(c->items, items)); TRY(upload(c->ent, ent));
-  TRY(upload(c->entf, entf)); TRY(upload(c->cellb, cellb));
+  TRY(upload(c->entf, entf));
   // Per cell: runs of NV_CHUNK entries (bucket order) with the f32 bounding box
   // of their cell-relative endpoints; the cast rejects a whole run when the
   // ray's line passes the box on one side (kernels.cuh ray_grid).  The cell
