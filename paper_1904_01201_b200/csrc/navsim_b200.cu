@@ -1211,7 +1211,9 @@ int nv_step_render_host(nv_ctx *c, const int8_t *actions_host, int cam, uint32_t
   const bool graph_ok = !frames_out && !c->prof_on && !(c->noise_sigma > 0.0);
   if (graph_ok) {
     if (!c->e_stream) {
-      CK(cudaStreamCreateWithFlags(&c->e_stream, cudaStreamNonBlocking));
+      // a blocking stream: ordered after the legacy default stream's work
+      // implicitly, so callers on stream 0 need no event handshake
+      CK(cudaStreamCreate(&c->e_stream));
       CK(cudaEventCreateWithFlags(&c->e_ev, cudaEventDisableTiming));
     }
     // pinned, mapped staging: with e2e_mapped the kernels read the actions
@@ -1276,8 +1278,10 @@ int nv_step_render_host(nv_ctx *c, const int8_t *actions_host, int cam, uint32_t
       c->e_key_gen = c->gen;
     }
     std::memcpy(c->e_hin, actions_host, N);
-    CK(cudaEventRecord(c->e_ev, st));  // after the caller's prior work
-    CK(cudaStreamWaitEvent(es, c->e_ev, 0));
+    if (st) {  // after the caller's prior work on its own stream
+      CK(cudaEventRecord(c->e_ev, st));
+      CK(cudaStreamWaitEvent(es, c->e_ev, 0));
+    }
     CK(cudaGraphLaunch(c->e_graph, es));
     c->launches += 3;
     CK(cudaStreamSynchronize(es));
