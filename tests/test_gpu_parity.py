@@ -475,6 +475,20 @@ def test_host_buffer_path_matches_device_path(nb):
         assert np.array_equal(out["compass"], o1["compass"].cpu().numpy())
         assert np.array_equal(out["collided"], sims[1].collided.cpu().numpy())
         assert np.array_equal(out["displacement"], sims[1].displacement.cpu().numpy())
+    # pinned (mapped) output buffers: the kernels write them directly
+    pin = {"gps": torch.empty((n, 2), dtype=torch.float64).pin_memory(),
+           "compass": torch.empty(n, dtype=torch.float64).pin_memory(),
+           "collided": torch.empty(n, dtype=torch.uint8).pin_memory(),
+           "displacement": torch.empty(n, dtype=torch.float64).pin_memory()}
+    for t in range(3):
+        a_host = np.ascontiguousarray(acts[t])
+        sims[0].step_host(a_host, out=pin)
+        sims[1].step(torch.as_tensor(a_host, device="cuda:0"))
+        torch.cuda.synchronize()
+        assert torch.equal(pin["gps"], sims[1].gps.cpu())
+        assert torch.equal(pin["compass"], sims[1].compass.cpu())
+        assert torch.equal(pin["collided"], sims[1].collided.cpu())
+        assert torch.equal(pin["displacement"], sims[1].displacement.cpu())
     # the non-graph path (host frames requested) agrees too
     a_host = np.ascontiguousarray(acts[0])
     rgb_h = np.empty((n, H, W, 3), np.uint8)
