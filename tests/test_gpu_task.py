@@ -241,3 +241,61 @@ def test_depth_noise_moments_and_paths(nb):
     torch.cuda.synchronize()
     assert not torch.equal(sim.observations()["depth"], outs[0])
     assert c.lib.nv_depth_noise(c.handle, -1.0, 0, 0) == nat.NV_ERR_ARG
+
+
+def test_apartment_batch_episodes_vs_oracle(nb):
+    """256 PointGoal envs on the C2 apartment (10k segments) through
+    BatchEnvironment vs the oracle's Environment restatement on a sample of
+    envs: per-step distance, reward, done and pose, and the outcomes --
+    bit-exact."""
+    import math
+    from oracle import nav_oracle as no
+    from oracle import oracle as orc
+    from paper_1904_01201_b200 import synth, task
+    from paper_1904_01201_b200.sensors import SensorConfig
+    sc = synth.config_scene("C2")
+    segs = sc.segments
+    bnds = no.bounds(segs)
+    og = no.Grid(segs, bnds)
+    N = 256
+    env = task.BatchEnvironment((segs, sc.semantic_ids, sc.albedo), N,
+                                sensor_configs=(SensorConfig("depth", 64, 16),))
+    rng = np.random.default_rng(12)
+    cells = np.argwhere(og.navigable)
+    eps, starts, goals = [], [], []
+    while len(eps) < N:
+        s = og.center_of(*cells[int(rng.integers(len(cells)))])
+        g = og.center_of(*cells[int(rng.integers(len(cells)))])
+        eu = math.hypot(*(g - s))
+        if not (1.5 <= eu <= 6.0):
+            continue
+        eps.append(task.Episode(f"e{len(eps)}", "x", (float(s[0]), float(s[1])),
+                                float(rng.uniform(-math.pi, math.pi)), (float(g[0]), float(g[1])),
+                                max(1.0, eu), eu, max(1.0, eu) / eu))
+    env.reset(eps)
+    sample = rng.choice(N, size=6, replace=False)
+    scene = orc.OracleScene(segs, sc.semantic_ids, sc.albedo)
+    oenv = {int(e): no.TaskEnv(scene, og) for e in sample}
+    for e, oe in oenv.items():
+        ep = eps[e]
+        d0 = oe.reset(ep.start_position, ep.start_heading, ep.goal_position, ep.gdsp)
+        assert d0 == env.d0[e]
+    T = 60
+    acts = rng.choice(3, size=(T, N), p=[0.6, 0.2, 0.2]).astype(np.int8)
+    acts[T - 1] = 3  # everyone stops
+    done_o = {e: False for e in oenv}
+    for t in range(T):
+        _, done, info = env.step(torch.as_tensor(acts[t], device="cuda:0"))
+        torch.cuda.synchronize()
+        d, r = info["d"].cpu().numpy(), info["reward"].cpu().numpy()
+        dn = done.cpu().numpy()
+        xy, h, _, _ = (v.cpu().numpy() for v in env.sim.state())
+        for e, oe in oenv.items():
+            if done_o[e]:
+                continue
+            dd, rr, ddone, _, _, out = oe.step(int(acts[t, e]))
+            assert (d[e], r[e], bool(dn[e])) == (dd, rr, ddone), (t, e)
+            assert (xy[e, 0], xy[e, 1], h[e]) == tuple(oe.state[:3])
+            done_o[e] = ddone
+    outs = env.outcomes()
+    assert all(o is not None for o in outs)
