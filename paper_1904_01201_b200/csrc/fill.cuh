@@ -646,6 +646,7 @@ struct FillWsLayout {  // byte offsets into dynamic shared memory + ring geometr
   int slot_bytes, nslot, slot_rows;
   int depth_direct;  // 1: producers store depth straight from registers (STG),
                      // the slots carry RGB / semantic only
+  int nw;            // producer warps (the CTA is nw + 1 warps)
 };
 
 template <int CPL, bool TAB, int RPW, bool NOISE>

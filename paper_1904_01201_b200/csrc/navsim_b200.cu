@@ -576,7 +576,7 @@ int launch_ws_kernel(nv_ctx *c, nvk::FillArgs &a, const nvk::FillWsLayout &L, si
   const int sms = ws_sms > 0 ? std::min(ws_sms, c->sm_count) : c->sm_count;
   const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(a.N, sms));
   Prof pf(c, st, 2);
-  kern<<<grid, (16 + 1) * 32, smem, st>>>(a, L);
+  kern<<<grid, (L.nw + 1) * 32, smem, st>>>(a, L);
   return check_launch(c);
 }
 
@@ -584,7 +584,11 @@ template <int CPL>
 int launch_fill_ws(nv_ctx *c, nvk::FillArgs &a, cudaStream_t st) {
   const int segw = 32 * CPL;
   const int S = a.W / segw;
-  const int nw = 16;
+  static const int nw = [] {  // tuning knob: producer warps (4, 8 or 16)
+    const char *e = getenv("NAVSIM_WS_NW");
+    const int v = e ? atoi(e) : 16;
+    return v == 4 || v == 8 ? v : 16;
+  }();
   static const int depth_direct = [] {  // tuning knob: depth by STG instead of the slots
     const char *e = getenv("NAVSIM_WS_DEPTH_DIRECT");
     return e ? atoi(e) : 0;
@@ -628,6 +632,7 @@ int launch_fill_ws(nv_ctx *c, nvk::FillArgs &a, cudaStream_t st) {
   L.bars = L.cols + (int)cols_b;
   L.slots = L.bars + (int)bars_b;
   L.depth_direct = dd ? 1 : 0;
+  L.nw = nw;
   a.segs_per_row = S;
   if (tab && rpw == 2) return launch_ws_kernel<CPL, true, 2>(c, a, L, smem, st);
   if (tab) return launch_ws_kernel<CPL, true, 1>(c, a, L, smem, st);
