@@ -306,6 +306,15 @@ int nv_task_state(nv_ctx *ctx, int32_t *steps, uint8_t *done, double *d_last, vo
  * not reproducible on the device: parity is the reference's moment test. */
 int nv_depth_noise(nv_ctx *ctx, double sigma, uint64_t seed, int64_t env_offset);
 
+/* sensors.apply_inverse_depth_noise (sensors.py:183-205) on caller frames: n
+ * device f32 depth frames [n, height, width] in place, the same generator
+ * and formula as above with stream key (seed, frame, env_offset + k, row,
+ * pixel pair); stateless (no context).  sigma = 0: untouched; sigma < 0 or
+ * max_range <= 0: NV_ERR_ARG. */
+int nv_depth_noise_apply(float *depth, int64_t n, int height, int width, double sigma,
+                         double max_range, uint64_t seed, uint64_t frame, int64_t env_offset,
+                         void *stream);
+
 /* ---- frame codecs ------------------------------------ */
 
 /* sensors.depth_to_png / rgb_to_png / semantic_to_png (sensors.py:211-246),

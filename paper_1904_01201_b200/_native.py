@@ -70,6 +70,8 @@ SIGNATURES = {
     "nv_task_state": (_I, [_P, _P, _P, _P, _P]),
     "nv_task_step_render": (_I, [_P, _P, _I] + [_P] * 13),
     "nv_depth_noise": (_I, [_P, _D, ctypes.c_uint64, _I64]),
+    "nv_depth_noise_apply": (_I, [_P, _I64, _I, _I, _D, _D, ctypes.c_uint64, ctypes.c_uint64,
+                                  _I64, _P]),
     "nv_png_size": (_I64, [_I, _I, _I]),
     "nv_png_encode": (_I, [_I, _I, _P, _I64, _I, _I, _D, _P, _I64, _P]),
     "nv_host_crc32_chunked": (ctypes.c_uint32, [_P, _I64, _I]),

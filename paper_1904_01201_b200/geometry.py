@@ -138,3 +138,12 @@ class SegmentIndex:
     def clearance(self, pos, search_radius: float = 2.0) -> float:
         """Distance to the nearest segment (geometry.py:194-206)."""
         return float(self.clearance_batch([pos[0]], [pos[1]], search_radius)[0])
+
+
+def navigable_mask(segs, bounds, resolution: float, agent_radius: float):
+    """geometry.navigable_mask (geometry.py:209-250): (mask, origin of cell
+    (0, 0)'s center, per-cell wall distance), built on the device
+    (nav.rasterize_navigable -> nv_nav_build)."""
+    from .nav import rasterize_navigable
+    grid = rasterize_navigable(segs, bounds, resolution, agent_radius)
+    return grid.navigable, np.asarray(grid.origin, dtype=np.float64), grid.clearance

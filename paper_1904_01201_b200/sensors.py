@@ -221,6 +221,31 @@ def gps_compass(state, frame: EpisodeFrame):
 # PNG per frame (nv_png_encode: quantisation, scanlines, zlib stored blocks,
 # Adler-32 and CRC-32 on the GPU); decoding is the consumer's side (PIL).
 
+def apply_inverse_depth_noise(depth, sigma: float, rng: np.random.Generator,
+                              max_range: float = 10.0) -> np.ndarray:
+    """sensors.apply_inverse_depth_noise (sensors.py:183-205): z' = max_range /
+    (max_range / d + eps), eps ~ N(0, sigma), clipped to [0.05, max_range];
+    saturated pixels (d >= max_range) pass through; sigma = 0 is the identity;
+    sigma < 0 raises SensorError.  Runs on the GPU (nv_depth_noise_apply) in
+    f32 with the device's counter-based normals keyed by one draw from
+    ``rng`` -- the same ``rng`` state gives the same frame; numpy's normal
+    stream itself is not reproduced (parity is the moment test)."""
+    if sigma < 0.0:
+        raise SensorError("sigma must be non-negative")
+    d = np.asarray(depth, dtype=np.float64)
+    if sigma == 0.0:
+        return d.copy()
+    import torch
+    seed = int(rng.integers(0, 2 ** 63))
+    H, W = (d.shape[-2], d.shape[-1]) if d.ndim >= 2 else (1, d.shape[-1])
+    n = int(d.size // (H * W))
+    t = torch.as_tensor(d.astype(np.float32)).reshape(n, H, W).to("cuda")
+    lib = nat.load()
+    nat.check(lib.nv_depth_noise_apply(nat.ptr(t), n, H, W, float(sigma), float(max_range),
+                                       seed, 0, 0, nat.stream_handle(t.device)))
+    return t.cpu().numpy().astype(np.float64).reshape(d.shape)
+
+
 PNG_DEPTH, PNG_RGB, PNG_SEMANTIC = 0, 1, 2
 
 
