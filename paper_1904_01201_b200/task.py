@@ -23,7 +23,7 @@ from . import nav
 from . import scene as scene_mod
 from .batch import BatchSimulator
 from .sensors import EpisodeFrame, Observations, default_sensor_suite, frames_to_host
-from .sim import Action, AgentConfig, _CODE
+from .sim import Action, AgentConfig, AgentState, _CODE
 
 MAX_EPISODE_STEPS = 500   # task.py:24
 SUCCESS_RADIUS = 0.2      # task.py:25
@@ -385,6 +385,33 @@ class Environment:
         if self._outcome is None:
             raise TaskError("episode has not terminated")
         return self._outcome
+
+    @property
+    def field(self) -> nav.DistanceField:
+        """The current episode's goal distance field (task.py:140-141)."""
+        if self.episode is None:
+            raise TaskError("environment must be reset first")
+        key = tuple(self.episode.goal_position)
+        if getattr(self, "_field_key", None) != key:
+            self._field = nav.distance_field(self.grid, self.episode.goal_position)
+            self._field_key = key
+        return self._field
+
+    @property
+    def sim(self) -> "_EnvAgentView":
+        """The bound simulator's agent state (``env.sim.state``, task.py:123-135)."""
+        return _EnvAgentView(self._b.sim)
+
+
+class _EnvAgentView:
+    def __init__(self, batch_sim):
+        self._s = batch_sim
+
+    @property
+    def state(self) -> AgentState:
+        xy, h, p, k = (t[0].item() if t.dim() == 1 else t[0].cpu().numpy() for t in self._s.state())
+        return AgentState(position=xy, heading=float(h), cumulative_path_length=float(p),
+                          collision_count=int(k))
 
 
 def run_episode(env: Environment, episode: Episode, actions) -> EpisodeOutcome:
