@@ -638,6 +638,9 @@ __global__ void __launch_bounds__(128) k_fill_direct(FillArgs a) {
 #ifndef NV_WS_RELEASE_NOW
 #define NV_WS_RELEASE_NOW 1  // release each slot as soon as its bulk reads are done
 #endif
+#ifndef NV_WS_PLANE_FAST
+#define NV_WS_PLANE_FAST 0  // 1: rows plane in all of a lane's columns skip the band masks (A/B: lane-divergent, slower at 512^2)
+#endif
 #ifndef NV_WS_DEBUG
 #define NV_WS_DEBUG 0  // 1: producers skip rendering, 2: no bulk stores (bound studies)
 #endif
@@ -786,7 +789,7 @@ __global__ void __launch_bounds__(544, 1) k_fill_ws(FillArgs a, FillWsLayout L) 
         else
           load_inv<CPL, true>(a.invh + (size_t)inv_row(i, H) * W + seg * Ln::SEGW, lane, iv);
         PairOut po[CPL / 2];
-        if (i < plane_lo || i >= plane_hi)  // plane in every column of the lane
+        if (NV_WS_PLANE_FAST && (i < plane_lo || i >= plane_hi))  // plane in every column of the lane
           shade_row_plane<CPL>(Rr, iv, po);
         else
           shade_row<CPL>(i, Rr, cr, iv, po);
