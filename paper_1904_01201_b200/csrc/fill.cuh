@@ -650,9 +650,11 @@ struct FillWsLayout {  // byte offsets into dynamic shared memory + ring geometr
   int depth_direct;  // 1: producers store depth straight from registers (STG),
                      // the slots carry RGB / semantic only
   int nw;            // producer warps (the CTA is nw + 1 warps)
+  int bands;         // work items per env frame (row bands of H / bands rows):
+                     // balances CTAs when envs per CTA is small
 };
 
-template <int CPL, bool TAB, int RPW, bool NOISE>
+template <int CPL, bool TAB, int RPW, bool NOISE, bool BANDED>
 __global__ void __launch_bounds__(544, 1) k_fill_ws(FillArgs a, FillWsLayout L) {
   extern __shared__ __align__(128) uint8_t smem[];
   using Ln = Lanes<CPL>;
@@ -672,7 +674,9 @@ __global__ void __launch_bounds__(544, 1) k_fill_ws(FillArgs a, FillWsLayout L) 
   const bool slot_d = want_d && !L.depth_direct;
   const int off_d = want_rgb ? R * W * 3 : 0;
   const int off_s = off_d + (slot_d ? R * W * 4 : 0);
-  const int slots_per_item = H / R;
+  const int bands = BANDED ? L.bands : 1, band_rows = BANDED ? H / bands : H;
+  const int slots_per_item = band_rows / R;
+  const int n_items = a.N * bands;
   if (threadIdx.x == 0) {
     for (int k = 0; k < NSLOT; ++k) {
       mbar_init(full + k, (unsigned)nw);
@@ -706,20 +710,21 @@ __global__ void __launch_bounds__(544, 1) k_fill_ws(FillArgs a, FillWsLayout L) 
       bulk_load(cols_s + (size_t)buf * 2 * W, a.ra + (size_t)env * W, plane_bytes, b);
       bulk_load(cols_s + (size_t)buf * 2 * W + W, a.rb + (size_t)env * W, plane_bytes, b);
     };
-    int e = blockIdx.x;
-    if (e < a.N) load_item(0, e);
+    int q = blockIdx.x;  // work item = (env, row band)
+    if (q < n_items) load_item(0, q / bands);
     unsigned k = 0, slot = 0, use = 0, prev = 0;
-    for (int it = 0; e < a.N; ++it, e += gridDim.x) {
-      const int en = e + gridDim.x;
-      if (en < a.N) {
+    for (int it = 0; q < n_items; ++it, q += gridDim.x) {
+      const int qn = q + gridDim.x;
+      if (qn < n_items) {
         const int j = it + 1;
         if (j >= 2) mbar_wait(colempty + (j & 1), (unsigned)(((j >> 1) - 1) & 1));
-        load_item(j & 1, en);
+        load_item(j & 1, qn / bands);
       }
+      const int e = q / bands, row0 = (q - e * bands) * band_rows;
       for (int sl = 0; sl < slots_per_item; ++sl, ++k) {
         mbar_wait(full + slot, use & 1u);
         const uint8_t *buf = slots + (size_t)slot * L.slot_bytes;
-        const size_t pix0 = ((size_t)e * H + (size_t)sl * R) * W;
+        const size_t pix0 = ((size_t)e * H + (size_t)row0 + (size_t)sl * R) * W;
 #if NV_WS_DEBUG != 2
         if (want_rgb) bulk_store(a.rgb + pix0 * 3, buf, (unsigned)(R * W * 3), pol);
         if (slot_d) bulk_store(a.depth + pix0, buf + off_d, (unsigned)(R * W * 4), pol);
@@ -755,8 +760,9 @@ __global__ void __launch_bounds__(544, 1) k_fill_ws(FillArgs a, FillWsLayout L) 
   const int rsub = warp / S;   // first row of this warp within a slot
   const int rstride = nw / S;  // row stride between the warp's RPW rows
   unsigned slot = 0, use = 0;
-  int e = blockIdx.x;
-  for (int it = 0; e < a.N; ++it, e += gridDim.x) {
+  int q = blockIdx.x;
+  for (int it = 0; q < n_items; ++it, q += gridDim.x) {
+    const int e = q / bands, row0 = (q - e * bands) * band_rows;
     mbar_wait(colfull + (it & 1), (unsigned)((it >> 1) & 1));
     ColRegs<CPL> cr;
     const float4 *cA = cols_s + (size_t)(it & 1) * 2 * W + seg * Ln::SEGW;
@@ -777,7 +783,7 @@ __global__ void __launch_bounds__(544, 1) k_fill_ws(FillArgs a, FillWsLayout L) 
 #pragma unroll
       for (int rr = 0; rr < RPW; ++rr) {
         const int rs = rsub + rr * rstride;  // row within the slot
-        const uint32_t i = (uint32_t)(sl * R + rs);
+        const uint32_t i = (uint32_t)(row0 + sl * R + rs);
 #if NV_WS_DEBUG == 1
         (void)buf; (void)i;
         continue;

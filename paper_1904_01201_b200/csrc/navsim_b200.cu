@@ -567,14 +567,17 @@ template <int CPL, bool TAB, int RPW>
 int launch_ws_kernel(nv_ctx *c, nvk::FillArgs &a, const nvk::FillWsLayout &L, size_t smem,
                      cudaStream_t st) {
   const bool noise = a.noise_sigma > 0.0f && a.depth;
-  auto kern = noise ? nvk::k_fill_ws<CPL, TAB, RPW, true> : nvk::k_fill_ws<CPL, TAB, RPW, false>;
+  auto kern = L.bands > 1 ? (noise ? nvk::k_fill_ws<CPL, TAB, RPW, true, true>
+                                  : nvk::k_fill_ws<CPL, TAB, RPW, false, true>)
+                         : (noise ? nvk::k_fill_ws<CPL, TAB, RPW, true, false>
+                                  : nvk::k_fill_ws<CPL, TAB, RPW, false, false>);
   TRY(set_smem(c, (const void *)kern, smem));
   static const int ws_sms = [] {  // study knob: SMs given to the ws writer
     const char *e = getenv("NAVSIM_WS_SMS");
     return e ? atoi(e) : 0;
   }();
   const int sms = ws_sms > 0 ? std::min(ws_sms, c->sm_count) : c->sm_count;
-  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(a.N, sms));
+  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(a.N * (int64_t)L.bands, sms));
   Prof pf(c, st, 2);
   kern<<<grid, (L.nw + 1) * 32, smem, st>>>(a, L);
   return check_launch(c);
@@ -611,8 +614,13 @@ int launch_fill_ws(nv_ctx *c, nvk::FillArgs &a, cudaStream_t st) {
   bool tab = false;
   int rpw = 0;
   size_t smem = 0;
+  static const bool no_tab = [] {  // tuning knob: never stage the shading table
+    const char *e = getenv("NAVSIM_WS_NOTAB");
+    return e && atoi(e) != 0;
+  }();
   for (const Opt &o : opts) {
     if (force_rpw && o.rpw != force_rpw) continue;
+    if (no_tab && o.tab) continue;
     const int R = o.rpw * nw / S;
     if (a.H % R) continue;
     const size_t slot = up((size_t)R * a.W * bpp);
@@ -633,6 +641,25 @@ int launch_fill_ws(nv_ctx *c, nvk::FillArgs &a, cudaStream_t st) {
   L.slots = L.bars + (int)bars_b;
   L.depth_direct = dd ? 1 : 0;
   L.nw = nw;
+  {  // row bands per env: minimise the busiest CTA's share, ceil(N b / grid) / b
+    static const int force_bands = [] {  // tuning knob
+      const char *e = getenv("NAVSIM_WS_BANDS");
+      return e ? atoi(e) : 0;
+    }();
+    int best = 1;
+    double best_t = 1e30;
+    for (int b = 1; b <= 8; b *= 2) {
+      if ((a.H / L.slot_rows) % b) break;
+      const int64_t items = a.N * (int64_t)b;
+      const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(items, c->sm_count));
+      const double t = (double)((items + grid - 1) / grid) / b;
+      if (t < best_t * (1.0 - 1e-9)) {
+        best_t = t;
+        best = b;
+      }
+    }
+    L.bands = force_bands > 0 && (a.H / L.slot_rows) % force_bands == 0 ? force_bands : best;
+  }
   a.segs_per_row = S;
   if (tab && rpw == 2) return launch_ws_kernel<CPL, true, 2>(c, a, L, smem, st);
   if (tab) return launch_ws_kernel<CPL, true, 1>(c, a, L, smem, st);
