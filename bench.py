@@ -413,6 +413,10 @@ def run_gpu(args):
         }
         if not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline(cfg, seconds=args.cpu_seconds)
+            # the one-worker figure the north-star's 10,000x target refers to
+            # (SURVEY.md section 8(d)); a reported baseline like the one above
+            line["cpu_baseline_1core"] = cpu_baseline(cfg, seconds=min(5.0, args.cpu_seconds),
+                                                      threads=1)
         print(json.dumps(line))
     if world > 1:
         dist.barrier()
