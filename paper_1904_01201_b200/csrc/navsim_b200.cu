@@ -823,7 +823,8 @@ int do_cast(nv_ctx *c, int cam, double *gps, double *compass, cudaStream_t st) {
 int nv_set_cast_mode_(nv_ctx *c, int mode) {
   if (mode < 0 || mode > 5)
     return fail(NV_ERR_ARG, "cast mode must be 0 (dda, auto), 1 (binned), 2 (dda fused with the "
-                            "step), 3 (dda, thread per ray) or 4 (dda, warp per ray)");
+                            "step), 3 (dda, thread per ray), 4 (dda, warp per ray) or 5 (dda, "
+                            "ray pools)");
   c->cast_mode = mode;
   return NV_OK;
 }
