@@ -641,18 +641,23 @@ int launch_fill_ws(nv_ctx *c, nvk::FillArgs &a, cudaStream_t st) {
   L.slots = L.bars + (int)bars_b;
   L.depth_direct = dd ? 1 : 0;
   L.nw = nw;
-  {  // row bands per env: minimise the busiest CTA's share, ceil(N b / grid) / b
+  {  // row bands per env: minimise the busiest CTA's time, ceil(N b / grid) items
+     // of (1/b frame + a fixed per-item cost).  Per-item cost measured at C3
+     // (2 bands: +8 us over 1024 extra items on 148 CTAs) ~ 1.1 us, i.e. the
+     // time one SM streams ~50 KB at its ~45 GB/s store rate.
     static const int force_bands = [] {  // tuning knob
       const char *e = getenv("NAVSIM_WS_BANDS");
       return e ? atoi(e) : 0;
     }();
+    const double frame_bytes = (double)a.W * a.H * bpp;
+    const double ovh = 49500.0 / std::max(1.0, frame_bytes);
     int best = 1;
     double best_t = 1e30;
-    for (int b = 1; b <= 8; b *= 2) {
+    for (int b = 1; b <= 64; b *= 2) {
       if ((a.H / L.slot_rows) % b) break;
       const int64_t items = a.N * (int64_t)b;
       const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(items, c->sm_count));
-      const double t = (double)((items + grid - 1) / grid) / b;
+      const double t = (double)((items + grid - 1) / grid) * (1.0 / b + ovh);
       if (t < best_t * (1.0 - 1e-9)) {
         best_t = t;
         best = b;
@@ -691,11 +696,13 @@ int launch_fill(nv_ctx *c, Camera &cam, int64_t N, uint8_t *rgb, float *depth, u
   auto al32 = [](const void *p) { return ((uintptr_t)p & 31) == 0; };
   const bool ws_ok = cam.W <= 4096 && (cam.W % 256 == 0 ? cam.H % (16 / std::min(16, cam.W / 256)) == 0
                                                           : cam.H % 16 == 0);
-  // mode 2 = warp-specialised writer; mode 3 (default) = the same for batches
-  // that fill the GPU (one CTA per env frame at a time), else the per-warp
-  // writer, which spreads a small batch over every SM.  The warp-specialised
-  // writer applies the depth noise itself; the others get a pass.
-  const bool use_ws = c->fill_mode == 2 || (c->fill_mode == 3 && N >= c->sm_count / 2);
+  // mode 2 = warp-specialised writer; mode 3 (default) = the same whenever the
+  // frame layout allows it (row bands spread small batches over the SMs),
+  // else the per-warp writer.  The warp-specialised writer applies the depth
+  // noise itself; the others get a pass.
+  // (auto = the ws writer whenever the layout allows: with row bands it also
+  // beats the per-warp writer on small batches -- C2 fill 14.7 -> 9.7 us)
+  const bool use_ws = c->fill_mode == 2 || c->fill_mode == 3;
   if (use_ws && aligned && ws_ok && cam.W % 256 == 0) return launch_fill_ws<8>(c, a, st);
   if (use_ws && aligned && ws_ok && cam.W == 128) return launch_fill_ws<4>(c, a, st);
   if (use_ws && aligned && ws_ok && cam.W == 64) return launch_fill_ws<2>(c, a, st);
