@@ -319,8 +319,10 @@ def run_gpu(args):
                                   shard.n_local * bytes_per_env_step(W, H, chans),
                                   per["step_render_fused"])
     else:
-        writer = {0: "k_fill_direct", 1: "k_fill_tma", 2: "k_fill_ws"}.get(
-            args.fill_mode, "k_fill_ws" if shard.n_local >= 74 else "k_fill_tma")
+        # auto (3) = the warp-specialised writer for every frame layout the
+        # bench configs use (256/128-wide, 16-row multiples)
+        writer = {0: "k_fill_direct", 1: "k_fill_tma", 2: "k_fill_ws"}.get(args.fill_mode,
+                                                                           "k_fill_ws")
         dom, dom_bytes, dom_ms = f"{writer} (frame_fill)", frame_bytes, per["frame_fill"]
     peak, peak_src = measured_peaks()
     achieved = dom_bytes / (dom_ms / 1e3) / 1e9
@@ -392,7 +394,7 @@ def run_gpu(args):
                        "channels": list(chans), "segments": sc.n_segments,
                        "triangles": sc.n_triangles, "parallelism": f"env-shard x{world}",
                        "cuda_graph": use_graph, "fused_megakernel": fused,
-                       "fill_mode": {0: "direct-stores", 1: "per-warp-tma-stages", 2: "warp-specialised-tma", 3: "auto (warp-specialised-tma when envs >= SMs/2, else per-warp-tma-stages)"}.get(args.fill_mode),
+                       "fill_mode": {0: "direct-stores", 1: "per-warp-tma-stages", 2: "warp-specialised-tma", 3: "auto (warp-specialised writer; row bands for small batches)"}.get(args.fill_mode),
                        "cast_mode": ["dda (thread per ray; warp per ray for <= 16384 rays)", "binned", "dda-fused-with-agent-step", "dda-thread-per-ray", "dda-warp-per-ray"][args.cast_mode],
                        "l2": f"no flush: frames written per step "
                              f"({step_bytes / 1e6:.0f} MB/GPU) exceed the 126 MB L2"},
