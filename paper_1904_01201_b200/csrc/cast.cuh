@@ -391,7 +391,8 @@ __global__ void __launch_bounds__(128, NV_CAST_KMINB) k_column_cast(EnvView ev, 
   if (ready) wait_envs_ready(ready, arrive, cam.W, total);
   const long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (g >= total) return;
-  const int e = (int)(g / cam.W);
+  // 32-bit division whenever the ray count fits (always, in practice)
+  const int e = total <= 0xffffffffLL ? (int)((unsigned)g / (unsigned)cam.W) : (int)(g / cam.W);
   const int j = (int)(g - (long long)e * cam.W);
   if (ready)
     cast_column<true>(ev, sc, cam, e, j, ro, t_max, gps, compass);

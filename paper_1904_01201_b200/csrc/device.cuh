@@ -106,12 +106,17 @@ struct __align__(16) ColRec {
 #endif
 NV_HDI int rec_pos(int j, int cpl) {
   if (cpl <= 0) return j;
-  const int gw = cpl < 4 ? cpl : 4;
-  const int segw = 32 * cpl;
-  const int seg = j / segw, r = j - seg * segw;
-  const int g = r / (32 * gw), r2 = r - g * 32 * gw;
-  const int l = r2 / gw, c = r2 - l * gw;
-  return seg * segw + (g * gw + c) * 32 + l;
+  // cpl is a power of two (2, 4, 8): shifts and masks instead of divisions
+#if defined(__CUDA_ARCH__)
+  const int lc = __ffs(cpl) - 1;
+#else
+  const int lc = __builtin_ctz((unsigned)cpl);
+#endif
+  const int lg = lc < 2 ? lc : 2;  // log2 of the group width min(cpl, 4)
+  const int seg = j >> (5 + lc), r = j & ((32 << lc) - 1);
+  const int g = r >> (5 + lg), r2 = r & ((32 << lg) - 1);
+  const int l = r2 >> lg, c = r2 & ((1 << lg) - 1);
+  return (seg << (5 + lc)) + (((g << lg) + c) << 5) + l;
 }
 
 struct RecOut {  // column-record planes written by the casts
