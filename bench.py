@@ -447,8 +447,8 @@ def main():
     ap.add_argument("--fill-mode", type=int, default=3, help="0 direct stores, 1 per-warp TMA stages, 2 warp-specialised writer, 3 auto")
     ap.add_argument("--cast-mode", type=int, default=0, help="0 per-column DDA (auto), 1 binned, 2 DDA fused with the agent step, 3 thread/ray, 4 warp/ray")
     ap.add_argument("--fused", action="store_true", help="one megakernel launch per step (experimental)")
-    ap.add_argument("--overlap", type=int, default=0,
-                    help="1: agent step -> cast programmatic dependent launch overlap")
+    ap.add_argument("--overlap", type=int, default=1,
+                    help="agent step -> cast programmatic dependent launch overlap (1 = library default, 0 = off)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)

@@ -122,7 +122,8 @@ int nv_step_render(nv_ctx *ctx, const int8_t *actions, int cam, uint8_t *rgb,
 
 /* Overlap of the agent step and the column cast in nv_step_render
  * (programmatic dependent launch: each env's casts start as soon as its agent
- * warp has published the new pose).  Thread-per-ray cast only. */
+ * warp has published the new pose).  Thread-per-ray cast only; on by default
+ * (end-to-end step 140.4 -> 138.5 us at C3), 0 turns it off. */
 int nv_set_overlap(nv_ctx *ctx, int on);
 /* Enable / disable (default) the single-launch megakernel of nv_step_render. */
 int nv_set_fused(nv_ctx *ctx, int on);

@@ -162,7 +162,7 @@ struct nv_ctx {
   bool cast_queue = false;   // column cast by persistent warps over a work counter (opt-in: slower)
   int cast_pool = 0;         // > 0: ray-pool cast with this many rays per warp (cast mode 0)
   bool e2e_mapped = true;    // host-buffer graph path: zero-copy actions / results
-  bool pdl = false;          // agent step -> cast programmatic dependent launch
+  bool pdl = true;           // agent step -> cast programmatic dependent launch (nv_set_overlap)
   bool pdl_armed = false, pdl_init = false;
   DevBuf pdl_ready, pdl_arrive;
   // dynamic shared memory opted in per kernel on this context's device
@@ -749,6 +749,15 @@ bool use_warp_cast(const nv_ctx *c, long long rays) {
   return c->cast_mode == 4 || (c->cast_mode == 0 && rays <= warp_rays);
 }
 
+int cast_queue_counter(Camera &k) {  // self-resetting work counter of k_column_cast_q
+  TRY(k.cast_ctr.alloc(2 * sizeof(unsigned int)));
+  if (!k.cast_ctr_init) {
+    CK(cudaMemset(k.cast_ctr.p, 0, 2 * sizeof(unsigned int)));
+    k.cast_ctr_init = true;
+  }
+  return NV_OK;
+}
+
 int do_cast(nv_ctx *c, int cam, double *gps, double *compass, cudaStream_t st) {
   Camera &k = c->cams[cam];
   if (c->cast_mode == 1 && k.W <= 2048) {
@@ -767,11 +776,7 @@ int do_cast(nv_ctx *c, int cam, double *gps, double *compass, cudaStream_t st) {
   // reference's uncapped t_max = 1e9 render).
   const long long total = c->n_envs * (long long)k.W;
   if (c->cast_queue) {  // persistent warps over a work counter
-    TRY(k.cast_ctr.alloc(2 * sizeof(unsigned int)));
-    if (!k.cast_ctr_init) {
-      CK(cudaMemset(k.cast_ctr.p, 0, 2 * sizeof(unsigned int)));
-      k.cast_ctr_init = true;
-    }
+    TRY(cast_queue_counter(k));
     int per_sm = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, nvk::k_column_cast_q, 128, 0));
     const long long want = (c->n_envs * ((k.W + 31) / 32) + 3) / 4;
@@ -836,20 +841,26 @@ int nv_set_cast_mode_(nv_ctx *c, int mode) {
   return NV_OK;
 }
 
+// per-env ready / arrive flags of the agent -> cast overlap (zero between steps)
+int pdl_buffers(nv_ctx *c) {
+  const size_t b = sizeof(unsigned) * (size_t)std::max<int64_t>(1, c->n_envs);
+  if (c->pdl_ready.bytes < b || !c->pdl_init) {
+    TRY(c->pdl_ready.alloc(b));
+    TRY(c->pdl_arrive.alloc(b));
+    CK(cudaMemset(c->pdl_ready.p, 0, b));
+    CK(cudaMemset(c->pdl_arrive.p, 0, b));
+    c->pdl_init = true;
+  }
+  return NV_OK;
+}
+
 int do_step(nv_ctx *c, const int8_t *actions, uint8_t *collided, double *disp, int32_t *status,
             cudaStream_t st, bool arm_pdl = false) {
   nvk::AgentCfg cfg{c->radius, c->step, c->turn_rad};
   long long threads = c->n_envs * 32;
   unsigned *ready = nullptr;
   if (arm_pdl) {
-    const size_t b = sizeof(unsigned) * (size_t)c->n_envs;
-    if (c->pdl_ready.bytes < b || !c->pdl_init) {
-      TRY(c->pdl_ready.alloc(b));
-      TRY(c->pdl_arrive.alloc(b));
-      CK(cudaMemset(c->pdl_ready.p, 0, b));
-      CK(cudaMemset(c->pdl_arrive.p, 0, b));
-      c->pdl_init = true;
-    }
+    TRY(pdl_buffers(c));
     ready = c->pdl_ready.as<unsigned>();
   }
   Prof pf(c, st, 0);
@@ -1252,7 +1263,7 @@ int nv_step_render_host(nv_ctx *c, const int8_t *actions_host, int cam, uint32_t
   const bool frames_out = rgb_host || depth_host || sem_host;
   // graph path: no host frames, no profiling, no noise (its frame counter
   // advances per call) -- the common per-step case
-  const bool graph_ok = !frames_out && !c->prof_on && !(c->noise_sigma > 0.0);
+  const bool graph_ok = !frames_out && !c->prof_on && !(c->noise_sigma > 0.0) && !c->fused;
   if (graph_ok) {
     if (!c->e_stream) {
       // a blocking stream: ordered after the legacy default stream's work
@@ -1330,6 +1341,10 @@ int nv_step_render_host(nv_ctx *c, const int8_t *actions_host, int cam, uint32_t
           o_coll = static_cast<uint8_t *>(c->e_out_dev[3]);
         }
       }
+      // everything nv_step_render allocates or zeroes lazily, before the
+      // capture (no allocation may happen while the stream is capturing)
+      if (c->pdl) TRY(pdl_buffers(c));
+      if (c->cast_queue) TRY(cast_queue_counter(c->cams[cam]));
       CK(cudaStreamBeginCapture(es, cudaStreamCaptureModeThreadLocal));
       if (!c->e2e_mapped) cudaMemcpyAsync(c->e_act.p, c->e_hin, N, cudaMemcpyHostToDevice, es);
       int rc = nv_step_render(c, acts, cam, want_rgb ? c->e_rgb.as<uint8_t>() : nullptr,

@@ -57,3 +57,18 @@ for _ in range(500):
 floor = (time.perf_counter() - t0) / 500 * 1e6
 print(f"e2e wall per step {wall:.1f} us, device per step {dev:.1f} us, overhead {wall - dev:.1f} us; "
       f"tiny-graph replay+sync floor {floor:.1f} us")
+# ctypes floor and the raw C call (no Python wrapper)
+lib = sim.ctx.lib
+t0 = time.perf_counter()
+for _ in range(20000):
+    lib.nv_version()
+ct = (time.perf_counter() - t0) / 20000 * 1e6
+args = sim._host_args
+_, fn, h, cam, bits, tail, _ = args
+a0 = host[0].numpy()
+ptr = a0.ctypes.data
+t0 = time.perf_counter()
+for s in range(K):
+    fn(h, ptr, cam, bits, *tail)
+raw = (time.perf_counter() - t0) / K * 1e6
+print(f"ctypes no-op call {ct:.2f} us; raw nv_step_render_host call {raw:.1f} us per step")

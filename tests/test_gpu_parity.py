@@ -498,3 +498,40 @@ def test_host_buffer_path_matches_device_path(nb):
     torch.cuda.synchronize()
     assert np.array_equal(rgb_h, sims[1].observations()["rgb"].cpu().numpy())
     assert np.array_equal(out["gps"], sims[1].gps.cpu().numpy())
+
+
+@pytest.mark.parametrize("mode", ["plain", "overlap", "thread", "fused"])
+def test_host_buffer_path_first_call_all_modes(nb, mode):
+    """The host-buffer step as the very first call on a fresh simulator (its
+    graph is captured before any device step ran: every lazily allocated
+    buffer must exist before the capture) in each step-launch mode, against
+    the device-buffer path."""
+    from paper_1904_01201_b200 import _native as nat
+    from paper_1904_01201_b200 import synth
+    sc = synth.config_scene("C2")
+    W, H, n = 128, 64, 200  # 25,600 rays: the thread-per-ray cast
+    suite = (nb.SensorConfig("rgb", W, H), nb.SensorConfig("depth", W, H),
+             nb.SensorConfig("gps_compass"))
+    sims = [nb.BatchSimulator(sc.segments, sc.semantic_ids, sc.albedo, n, sensor_configs=suite)
+            for _ in range(2)]
+    poses = synth.sample_poses(sc, n, seed=41)
+    for s in sims:
+        s.reset(poses[:, :2], poses[:, 2])
+        c = s.ctx
+        if mode == "overlap":
+            nat.check(c.lib.nv_set_overlap(c.handle, 1))
+        elif mode == "thread":
+            nat.check(c.lib.nv_set_cast_mode(c.handle, 3))
+        elif mode == "fused":
+            nat.check(c.lib.nv_set_fused(c.handle, 1))
+    acts = synth.random_actions(n, 4, seed=42)
+    out = {"gps": np.empty((n, 2)), "compass": np.empty(n), "collided": np.empty(n, np.uint8),
+           "displacement": np.empty(n)}
+    for t in range(acts.shape[0]):
+        a_host = np.ascontiguousarray(acts[t])
+        sims[0].step_host(a_host, out=out)
+        sims[1].step(torch.as_tensor(a_host, device="cuda:0"))
+        torch.cuda.synchronize()
+        assert np.array_equal(out["gps"], sims[1].gps.cpu().numpy())
+        assert np.array_equal(out["collided"], sims[1].collided.cpu().numpy())
+        assert np.array_equal(out["displacement"], sims[1].displacement.cpu().numpy())
