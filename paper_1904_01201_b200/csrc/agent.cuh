@@ -145,9 +145,10 @@ __global__ void __launch_bounds__(128) k_agent_step(EnvView ev, SceneView sc, Ag
 // env's flag for the next step.  (CTAs of the cast grid cover rays
 // [b*B, (b+1)*B) of the env-major ray order.)
 __device__ __forceinline__ void wait_envs_ready(unsigned *ready, unsigned *arrive, int W,
-                                                long long n_rays) {
-  const long long r0 = (long long)blockIdx.x * blockDim.x;
-  const long long r1 = min(n_rays, r0 + blockDim.x) - 1;
+                                                long long n_rays, int rays_per_block = 0) {
+  const int rpb = rays_per_block > 0 ? rays_per_block : (int)blockDim.x;
+  const long long r0 = (long long)blockIdx.x * rpb;
+  const long long r1 = min(n_rays, r0 + rpb) - 1;
   const int e0 = (int)(r0 / W), e1 = (int)(r1 / W);
   if (threadIdx.x == 0) {
     for (int e = e0; e <= e1; ++e) {
@@ -162,7 +163,7 @@ __device__ __forceinline__ void wait_envs_ready(unsigned *ready, unsigned *arriv
   if (threadIdx.x == 0) {
     for (int e = e0; e <= e1; ++e) {
       // CTAs that cover env e: blocks [first, last] of its ray range
-      const long long f = (long long)e * W / blockDim.x, l = ((long long)(e + 1) * W - 1) / blockDim.x;
+      const long long f = (long long)e * W / rpb, l = ((long long)(e + 1) * W - 1) / rpb;
       if (atomicAdd(arrive + e, 1u) == (unsigned)(l - f)) {
         arrive[e] = 0;
         ready[e] = 0;

@@ -189,13 +189,21 @@ __device__ __forceinline__ void ray_grid_warp(const SceneView &sc, double px, do
   out_i = best_i;
 }
 
-// One warp per (env, column): the latency-bound small-batch cast.
+// One warp per (env, column): the latency-bound small-batch cast.  COH: the
+// agent state was written by a still-running grid (programmatic dependent
+// launch), so it is read through L2 (ld.global.cg).
+template <bool COH = false>
 __device__ __forceinline__ void k_column_cast_warp_body(const EnvView &ev, const SceneView &sc,
                                                         const CamView &cam, const RecOut &ro,
                                                         double t_max, double *gps,
                                                         double *compass, int e, int j) {
   const int lane = threadIdx.x & 31;
-  const double px = ev.x[e], py = ev.y[e], c = ev.ch[e], s = ev.sh[e];
+  double px, py, c, s;
+  if (COH) {
+    px = __ldcg(ev.x + e); py = __ldcg(ev.y + e); c = __ldcg(ev.ch + e); s = __ldcg(ev.sh + e);
+  } else {
+    px = ev.x[e]; py = ev.y[e]; c = ev.ch[e]; s = ev.sh[e];
+  }
   const double u = __ldg(cam.u + j);
   const double dx = add(c, mul(u, s));
   const double dy = add(s, mul(u, -c));
@@ -213,19 +221,25 @@ __device__ __forceinline__ void k_column_cast_warp_body(const EnvView &ev, const
       gps[2 * e] = sub(mul(fc, ddx), mul(fs, ddy));
       gps[2 * e + 1] = add(mul(fs, ddx), mul(fc, ddy));
     }
-    if (compass) compass[e] = nvx::wrap_angle(sub(ev.h[e], ev.oh[e]));
+    if (compass) compass[e] = nvx::wrap_angle(sub(COH ? __ldcg(ev.h + e) : ev.h[e], ev.oh[e]));
   }
 }
 
+// With `ready`: a programmatic dependent of k_agent_step, waiting per env.
 __global__ void __launch_bounds__(128) k_column_cast_warp(EnvView ev, SceneView sc, CamView cam,
                                                           RecOut ro, double t_max, double *gps,
-                                                          double *compass) {
-  const long long g = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+                                                          double *compass, unsigned *ready,
+                                                          unsigned *arrive) {
   const long long total = (long long)ev.n * cam.W;
+  if (ready) wait_envs_ready(ready, arrive, cam.W, total, (int)(blockDim.x >> 5));
+  const long long g = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
   if (g >= total) return;
   const int e = (int)(g / cam.W);
   const int j = (int)(g - (long long)e * cam.W);
-  k_column_cast_warp_body(ev, sc, cam, ro, t_max, gps, compass, e, j);
+  if (ready)
+    k_column_cast_warp_body<true>(ev, sc, cam, ro, t_max, gps, compass, e, j);
+  else
+    k_column_cast_warp_body<false>(ev, sc, cam, ro, t_max, gps, compass, e, j);
 }
 
 // ---- ray-pool cast: lanes refill from a per-warp pool of rays --------------

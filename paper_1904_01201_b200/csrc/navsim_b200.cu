@@ -790,9 +790,25 @@ int do_cast(nv_ctx *c, int cam, double *gps, double *compass, cudaStream_t st) {
   }
   if (use_warp_cast(c, total)) {
     Prof pf(c, st, 1);
+    if (c->pdl_armed) {  // programmatic dependent of the agent step just launched
+      c->pdl_armed = false;
+      cudaLaunchConfig_t lc = {};
+      lc.gridDim = dim3(blocks_for(total * 32, 128));
+      lc.blockDim = dim3(128);
+      lc.stream = st;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      at[0].val.programmaticStreamSerializationAllowed = 1;
+      lc.attrs = at;
+      lc.numAttrs = 1;
+      CK(cudaLaunchKernelEx(&lc, nvk::k_column_cast_warp, c->env_view(), c->scene_view(),
+                            cam_view(k), rec_out(k, c->n_envs), k.max_range, gps, compass,
+                            c->pdl_ready.as<unsigned>(), c->pdl_arrive.as<unsigned>()));
+      return check_launch(c);
+    }
     nvk::k_column_cast_warp<<<blocks_for(total * 32, 128), 128, 0, st>>>(
         c->env_view(), c->scene_view(), cam_view(k), rec_out(k, c->n_envs), k.max_range, gps,
-        compass);
+        compass, nullptr, nullptr);
     return check_launch(c);
   }
   if (c->cast_mode == 5 || (c->cast_mode == 0 && c->cast_pool > 0)) {  // ray pools
@@ -1199,8 +1215,8 @@ int nv_step_render(nv_ctx *c, const int8_t *actions, int cam, uint8_t *rgb, floa
   // thread-per-ray DDA cast, when profiling events are off (an event between
   // the two launches would break the programmatic edge)
   const bool pdl = c->pdl && !c->prof_on && !c->cast_queue &&
-                   (c->cast_mode == 3 ||
-                    (c->cast_mode == 0 && !use_warp_cast(c, c->n_envs * (long long)k.W)));
+                   (c->cast_mode == 3 || c->cast_mode == 4 ||
+                    (c->cast_mode == 0 && c->cast_pool <= 0));
   TRY(do_step(c, actions, collided, displacement, status, st, pdl));
   TRY(do_cast(c, cam, gps, compass, st));
   c->pdl_armed = false;
