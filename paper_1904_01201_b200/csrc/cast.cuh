@@ -395,7 +395,7 @@ __global__ void __launch_bounds__(128) k_column_cast_pool(EnvView ev, SceneView 
 // One thread per (env, column).  With `ready`: launched as a programmatic
 // dependent of k_agent_step; waits per env instead of for the whole step.
 #ifndef NV_CAST_KMINB
-#define NV_CAST_KMINB 1  // min resident CTAs/SM for the thread-per-ray cast (register cap)
+#define NV_CAST_KMINB 5  // min resident CTAs/SM for the thread-per-ray cast (register cap: <= 96)
 #endif
 __global__ void __launch_bounds__(128, NV_CAST_KMINB) k_column_cast(EnvView ev, SceneView sc, CamView cam,
                                                      RecOut ro, double t_max,
