@@ -122,8 +122,9 @@ int nv_step_render(nv_ctx *ctx, const int8_t *actions, int cam, uint8_t *rgb,
 
 /* Overlap of the agent step and the column cast in nv_step_render
  * (programmatic dependent launch: each env's casts start as soon as its agent
- * warp has published the new pose).  Thread-per-ray cast only; on by default
- * (end-to-end step 140.4 -> 138.5 us at C3), 0 turns it off. */
+ * warp has published the new pose).  DDA casts (thread or warp per ray); on
+ * by default (C2 32.3 -> 30.1 us/step, C3 end to end 140.4 -> 138.5 us), 0
+ * turns it off. */
 int nv_set_overlap(nv_ctx *ctx, int on);
 /* Enable / disable (default) the single-launch megakernel of nv_step_render. */
 int nv_set_fused(nv_ctx *ctx, int on);
@@ -143,7 +144,8 @@ int nv_set_cast_mode(nv_ctx *ctx, int mode);
  * 2 = warp-specialised: 16 producer warps render rows into a ring of
  *     smem slots, one store warp writes each slot with one bulk copy per
  *     channel (one CTA per SM, one env frame per work item),
- * 3 (default) = 2 for batches of at least half the SM count, else 1.
+ * 3 (default) = 2 whenever the frame layout allows it (small batches split
+ * each frame into row bands to spread over the SMs), else 1.
  * All modes produce identical frames. */
 int nv_set_fill_mode(nv_ctx *ctx, int mode);
 
