@@ -635,6 +635,9 @@ __global__ void __launch_bounds__(128) k_fill_direct(FillArgs a) {
 // lane prefetches the next item's column-record planes into a double buffer
 // with bulk copies.  Producers never touch L2: row records, the shading table
 // and column records are all shared-memory reads.
+#ifndef NV_WS_CBUF
+#define NV_WS_CBUF 2  // record-plane buffers (prefetch distance CBUF - 1 items)
+#endif
 #ifndef NV_WS_RELEASE_NOW
 #define NV_WS_RELEASE_NOW 1  // release each slot as soon as its bulk reads are done
 #endif
@@ -667,7 +670,7 @@ __global__ void __launch_bounds__(544, 1) k_fill_ws(FillArgs a, FillWsLayout L) 
   uint64_t *full = reinterpret_cast<uint64_t *>(smem + L.bars);
   uint64_t *empty = full + NSLOT;
   uint64_t *colfull = empty + NSLOT;
-  uint64_t *colempty = colfull + 2;
+  uint64_t *colempty = colfull + NV_WS_CBUF;
   uint8_t *slots = smem + L.slots;
   const unsigned plane_bytes = (unsigned)W * 16u;
   const bool want_rgb = a.rgb != nullptr, want_d = a.depth != nullptr, want_s = a.sem != nullptr;
@@ -682,7 +685,7 @@ __global__ void __launch_bounds__(544, 1) k_fill_ws(FillArgs a, FillWsLayout L) 
       mbar_init(full + k, (unsigned)nw);
       mbar_init(empty + k, 1);
     }
-    for (int k = 0; k < 2; ++k) {
+    for (int k = 0; k < NV_WS_CBUF; ++k) {
       mbar_init(colfull + k, 1);
       mbar_init(colempty + k, (unsigned)nw);
     }
@@ -711,14 +714,18 @@ __global__ void __launch_bounds__(544, 1) k_fill_ws(FillArgs a, FillWsLayout L) 
       bulk_load(cols_s + (size_t)buf * 2 * W + W, a.rb + (size_t)env * W, plane_bytes, b);
     };
     int q = blockIdx.x;  // work item = (env, row band)
-    if (q < n_items) load_item(0, q / bands);
+    // record planes run NV_WS_CBUF - 1 items ahead of the item being stored
+#pragma unroll
+    for (int j = 0; j < NV_WS_CBUF - 1; ++j)
+      if (q + j * (int)gridDim.x < n_items) load_item(j, (q + j * (int)gridDim.x) / bands);
     unsigned k = 0, slot = 0, use = 0, prev = 0;
     for (int it = 0; q < n_items; ++it, q += gridDim.x) {
-      const int qn = q + gridDim.x;
+      const int qn = q + (NV_WS_CBUF - 1) * (int)gridDim.x;
       if (qn < n_items) {
-        const int j = it + 1;
-        if (j >= 2) mbar_wait(colempty + (j & 1), (unsigned)(((j >> 1) - 1) & 1));
-        load_item(j & 1, qn / bands);
+        const int j = it + NV_WS_CBUF - 1;  // item to post; buffer j % CBUF last held item j - CBUF
+        if (j >= NV_WS_CBUF)
+          mbar_wait(colempty + (j % NV_WS_CBUF), (unsigned)(((j / NV_WS_CBUF) - 1) & 1));
+        load_item(j % NV_WS_CBUF, qn / bands);
       }
       const int e = q / bands, row0 = (q - e * bands) * band_rows;
       for (int sl = 0; sl < slots_per_item; ++sl, ++k) {
@@ -763,9 +770,9 @@ __global__ void __launch_bounds__(544, 1) k_fill_ws(FillArgs a, FillWsLayout L) 
   int q = blockIdx.x;
   for (int it = 0; q < n_items; ++it, q += gridDim.x) {
     const int e = q / bands, row0 = (q - e * bands) * band_rows;
-    mbar_wait(colfull + (it & 1), (unsigned)((it >> 1) & 1));
+    mbar_wait(colfull + (it % NV_WS_CBUF), (unsigned)((it / NV_WS_CBUF) & 1));
     ColRegs<CPL> cr;
-    const float4 *cA = cols_s + (size_t)(it & 1) * 2 * W + seg * Ln::SEGW;
+    const float4 *cA = cols_s + (size_t)(it % NV_WS_CBUF) * 2 * W + seg * Ln::SEGW;
     load_cols_smem<CPL>(cA, cA + W, lane, cr);
     // rows [0, plane_lo) are ceiling and rows [plane_hi, H) floor in all of
     // this lane's columns
@@ -776,7 +783,7 @@ __global__ void __launch_bounds__(544, 1) k_fill_ws(FillArgs a, FillWsLayout L) 
       plane_hi = max(plane_hi, cr.hi[k]);
     }
     __syncwarp();
-    if (lane == 0) mbar_arrive(colempty + (it & 1));
+    if (lane == 0) mbar_arrive(colempty + (it % NV_WS_CBUF));
     for (int sl = 0; sl < slots_per_item; ++sl) {
       if (use >= 1) mbar_wait(empty + slot, (use - 1) & 1u);
       uint8_t *buf = slots + (size_t)slot * L.slot_bytes;

@@ -602,7 +602,7 @@ int launch_fill_ws(nv_ctx *c, nvk::FillArgs &a, cudaStream_t st) {
   if (nw % S) return fail(NV_ERR_ARG, "frame layout unsupported by ws fill");
   const size_t rows_b = up((size_t)a.H * sizeof(RowRec));
   const size_t inv_b = up((size_t)((a.H + 1) / 2) * a.W * 2);
-  const size_t cols_b = up((size_t)2 * a.W * sizeof(ColRec));
+  const size_t cols_b = up((size_t)NV_WS_CBUF * a.W * sizeof(ColRec));
   const size_t bars_b = 128;
   static const int force_rpw = [] {
     const char *e = getenv("NAVSIM_WS_RPW");
