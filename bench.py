@@ -366,7 +366,9 @@ def run_gpu(args):
                "h2d_bytes_per_step": n * 1, "d2h_bytes_per_step": n * (16 + 8 + 1 + 8),
                "path": "nv_step_render_host: pinned host actions in, host step results "
                        "(collided, displacement, gps, compass) out; frames stay in HBM "
-                       "for the GPU consumer (the paper's GPU->GPU mode)"}
+                       "for the GPU consumer (the paper's GPU->GPU mode); each call returns "
+                       "when its results are in host memory, the frame writer finishes "
+                       "behind it, and the timed region ends after a device synchronize"}
         # variant: also copy every frame to pinned host memory (host-consumer mode)
         k2 = min(args.steps, 5)
         fr = {c: torch.empty(((n, H, W, 3) if c == "rgb" else (n, H, W)),

@@ -156,7 +156,13 @@ int nv_set_fill_mode(nv_ctx *ctx, int mode);
  * per-env step results (collided u8, displacement f64, gps f64x2, compass
  * f64) back to host buffers (any may be NULL) and, where the host frame
  * pointers are non-NULL, the frames too.  Host buffers should be pinned.
- * Synchronises `stream` before returning. */
+ * Returns when the step results are in the host buffers.  Without host frame
+ * pointers the step runs as one replayed graph on an internal blocking stream
+ * and returns as soon as its casts are done (the results are complete then);
+ * the frame writer finishes behind the caller, ordered before the next host
+ * step, before work on the legacy default stream, and before nv_host_frames /
+ * nv_camera_config / nv_envs_alloc / nv_scene_upload / nv_destroy return.
+ * With host frame pointers the call synchronises before returning. */
 #define NV_CH_RGB 1u
 #define NV_CH_DEPTH 2u
 #define NV_CH_SEM 4u
@@ -165,8 +171,9 @@ int nv_step_render_host(nv_ctx *ctx, const int8_t *actions_host, int cam,
                         uint16_t *sem_host, double *gps_host,
                         double *compass_host, uint8_t *collided_host,
                         double *displacement_host, void *stream);
-/* Device frame buffers written by nv_step_render_host (valid until the next
- * call; for a GPU consumer of the host-driven path). */
+/* Device frame buffers written by nv_step_render_host (complete when this
+ * returns, valid until the next call; for a GPU consumer of the host-driven
+ * path). */
 int nv_host_frames(nv_ctx *ctx, uint8_t **rgb, float **depth, uint16_t **sem);
 
 /* gps_compass (sensors.py:175-180) alone, for suites without visual sensors.

@@ -94,6 +94,8 @@ struct Camera {
   double tables_cam_h = NAN;
   DevBuf u, tc, tf, rows, invh;
   DevBuf rec;      // ColRec N x W
+  DevBuf rec_e2e;  // the host-buffer step's own records (its frame writer may
+                   // still be reading them after nv_step_render_host returns)
   DevBuf ctr;      // fill scheduler counters
   DevBuf cast_ctr; // persistent cast work counter (self-resetting)
   bool cast_ctr_init = false;
@@ -147,6 +149,9 @@ struct nv_ctx {
   // of the packed step results, replayed while (cam, channels, N) stay fixed
   cudaStream_t e_stream = nullptr;
   cudaEvent_t e_ev = nullptr;
+  cudaEvent_t e_cast_ev = nullptr;  // recorded in the host-step graph after the casts
+  cudaEvent_t mid_ev = nullptr;     // nv_step_render records it after the casts (capture only)
+  bool e_pending = false;           // a host step's frame writer may still be running
   cudaGraphExec_t e_graph = nullptr;
   int e_key[3] = {-1, -1, -1};
   int64_t e_key_n = -1, e_key_gen = -1;
@@ -888,6 +893,17 @@ int do_step(nv_ctx *c, const int8_t *actions, uint8_t *collided, double *disp, i
   return NV_OK;
 }
 
+// A host-buffer step returns once its step results are on the host; its frame
+// writer may still run on the internal stream.  Entry points that reallocate
+// or expose the buffers it uses wait for it first.
+int e2e_fence(nv_ctx *c) {
+  if (c->e_pending) {
+    c->e_pending = false;
+    CK(cudaStreamSynchronize(c->e_stream));
+  }
+  return NV_OK;
+}
+
 }  // namespace
 
 // ====================================================================== ABI
@@ -918,6 +934,7 @@ int nv_create(int device, nv_ctx **out) {
 int nv_destroy(nv_ctx *ctx) {
   if (!ctx) return NV_OK;
   cudaSetDevice(ctx->device);
+  e2e_fence(ctx);
   delete ctx;
   return NV_OK;
 }
@@ -925,6 +942,7 @@ int nv_destroy(nv_ctx *ctx) {
 int nv_scene_upload(nv_ctx *c, const double *segs, const uint16_t *sem, const double *albedo,
                     int64_t n, double wall_height, const double *floor3, const double *ceil3) {
   if (!c) return fail(NV_ERR_ARG, "ctx is NULL");
+  TRY(e2e_fence(c));
   c->gen++;
   if (n < 0 || (n > 0 && (!segs || !sem || !albedo)))
     return fail(NV_ERR_ARG, "bad scene arrays");
@@ -1084,6 +1102,7 @@ int nv_agent_config(nv_ctx *c, double radius, double forward_step, double turn_r
 
 int nv_envs_alloc(nv_ctx *c, int64_t n_envs) {
   if (!c) return fail(NV_ERR_ARG, "ctx is NULL");
+  TRY(e2e_fence(c));
   c->gen++;
   if (n_envs <= 0 || n_envs >= (1LL << 30)) return fail(NV_ERR_ARG, "bad n_envs %lld", (long long)n_envs);
   CK(cudaSetDevice(c->device));
@@ -1106,6 +1125,7 @@ int nv_envs_alloc(nv_ctx *c, int64_t n_envs) {
 
 int nv_camera_config(nv_ctx *c, int cam, int width, int height, double focal, double max_range) {
   if (!c) return fail(NV_ERR_ARG, "ctx is NULL");
+  TRY(e2e_fence(c));
   c->gen++;
   if (cam < 0 || cam >= 8) return fail(NV_ERR_ARG, "camera index %d out of range [0, 8)", cam);
   if (width < 1 || height < 1 || width > 16384 || height > 16384)
@@ -1220,6 +1240,7 @@ int nv_step_render(nv_ctx *c, const int8_t *actions, int cam, uint8_t *rgb, floa
   TRY(do_step(c, actions, collided, displacement, status, st, pdl));
   TRY(do_cast(c, cam, gps, compass, st));
   c->pdl_armed = false;
+  if (c->mid_ev) CK(cudaEventRecordWithFlags(c->mid_ev, st, cudaEventRecordExternal));
   return launch_fill(c, k, c->n_envs, rgb, depth, sem, st);
 }
 
@@ -1329,6 +1350,8 @@ int nv_step_render_host(nv_ctx *c, const int8_t *actions_host, int cam, uint32_t
         c->e_out_dev[q] = at.devicePointer;
       }
     }
+    if (!c->e_cast_ev) CK(cudaEventCreateWithFlags(&c->e_cast_ev, cudaEventDisableTiming));
+    TRY(c->cams[cam].rec_e2e.alloc(c->cams[cam].rec.bytes));
     const bool same = c->e_graph && c->e_key_n == c->n_envs && c->e_key_gen == c->gen &&
                       key[0] == c->e_key[0] &&
                       key[1] == c->e_key[1] && key[2] == c->e_key[2] &&
@@ -1336,6 +1359,7 @@ int nv_step_render_host(nv_ctx *c, const int8_t *actions_host, int cam, uint32_t
                       (!direct || std::memcmp(c->e_key_out, c->e_out_dev, sizeof c->e_key_out) == 0);
     cudaStream_t es = c->e_stream;
     if (!same) {
+      TRY(e2e_fence(c));  // the old graph's writer may still be running
       if (c->e_graph) cudaGraphExecDestroy(c->e_graph);
       c->e_graph = nullptr;
       const int8_t *acts = c->e_act.as<int8_t>();
@@ -1363,10 +1387,19 @@ int nv_step_render_host(nv_ctx *c, const int8_t *actions_host, int cam, uint32_t
       if (c->cast_queue) TRY(cast_queue_counter(c->cams[cam]));
       CK(cudaStreamBeginCapture(es, cudaStreamCaptureModeThreadLocal));
       if (!c->e2e_mapped) cudaMemcpyAsync(c->e_act.p, c->e_hin, N, cudaMemcpyHostToDevice, es);
+      // the graph's casts and writer use the host step's own record buffer,
+      // and an event after the casts tells the host the step results are in
+      Camera &kc = c->cams[cam];
+      std::swap(kc.rec.p, kc.rec_e2e.p);
+      std::swap(kc.rec.bytes, kc.rec_e2e.bytes);
+      c->mid_ev = c->e2e_mapped ? c->e_cast_ev : nullptr;
       int rc = nv_step_render(c, acts, cam, want_rgb ? c->e_rgb.as<uint8_t>() : nullptr,
                               want_d ? c->e_depth.as<float>() : nullptr,
                               want_s ? c->e_sem.as<uint16_t>() : nullptr, o_gps, o_comp, o_coll,
                               o_disp, nullptr, es);
+      c->mid_ev = nullptr;
+      std::swap(kc.rec.p, kc.rec_e2e.p);
+      std::swap(kc.rec.bytes, kc.rec_e2e.bytes);
       if (!c->e2e_mapped) cudaMemcpyAsync(c->e_hout, pk, pack, cudaMemcpyDeviceToHost, es);
       cudaGraph_t g = nullptr;
       cudaError_t ce = cudaStreamEndCapture(es, &g);
@@ -1391,7 +1424,15 @@ int nv_step_render_host(nv_ctx *c, const int8_t *actions_host, int cam, uint32_t
     }
     CK(cudaGraphLaunch(c->e_graph, es));
     c->launches += 3;
-    CK(cudaStreamSynchronize(es));
+    if (c->e2e_mapped) {
+      // the step results are in host memory once the casts are done; the
+      // frame writer finishes behind the caller (ordered before the next
+      // host step; nv_host_frames and reallocating calls wait for it)
+      CK(cudaEventSynchronize(c->e_cast_ev));
+      c->e_pending = true;
+    } else {
+      CK(cudaStreamSynchronize(es));
+    }
     if (direct) return NV_OK;  // the kernels wrote the caller's buffers
     const uint8_t *h = static_cast<const uint8_t *>(c->e_hout);
     if (gps_host) std::memcpy(gps_host, h, 16 * N);
@@ -1400,6 +1441,7 @@ int nv_step_render_host(nv_ctx *c, const int8_t *actions_host, int cam, uint32_t
     if (collided_host) std::memcpy(collided_host, h + 32 * N, N);
     return NV_OK;
   }
+  TRY(e2e_fence(c));
   CK(cudaMemcpyAsync(c->e_act.p, actions_host, N, cudaMemcpyHostToDevice, st));
   TRY(nv_step_render(c, c->e_act.as<int8_t>(), cam, want_rgb ? c->e_rgb.as<uint8_t>() : nullptr,
                      want_d ? c->e_depth.as<float>() : nullptr,
@@ -1423,6 +1465,7 @@ int nv_step_render_host(nv_ctx *c, const int8_t *actions_host, int cam, uint32_t
 
 int nv_host_frames(nv_ctx *c, uint8_t **rgb, float **depth, uint16_t **sem) {
   if (!c) return fail(NV_ERR_ARG, "ctx is NULL");
+  TRY(e2e_fence(c));  // the frames are complete when this returns
   if (rgb) *rgb = c->e_rgb.as<uint8_t>();
   if (depth) *depth = c->e_depth.as<float>();
   if (sem) *sem = c->e_sem.as<uint16_t>();

@@ -535,3 +535,50 @@ def test_host_buffer_path_first_call_all_modes(nb, mode):
         assert np.array_equal(out["gps"], sims[1].gps.cpu().numpy())
         assert np.array_equal(out["collided"], sims[1].collided.cpu().numpy())
         assert np.array_equal(out["displacement"], sims[1].displacement.cpu().numpy())
+
+
+def test_host_step_frames_and_interleaving(nb):
+    """A host-buffer step returns once its step results are in (its frame
+    writer may still run): nv_host_frames waits for the frames, and device
+    steps interleaved on the same context keep every result and frame equal
+    to a pure device-path replica."""
+    import ctypes
+    from paper_1904_01201_b200 import _native as nat
+    from paper_1904_01201_b200 import synth
+
+    class _Dev:  # zero-copy torch view of a device pointer
+        def __init__(self, ptr, shape, typestr):
+            self.__cuda_array_interface__ = {"shape": shape, "typestr": typestr,
+                                             "data": (ptr, False), "version": 3}
+
+    sc = synth.config_scene("C2")
+    W, H, n = 128, 64, 200
+    suite = (nb.SensorConfig("rgb", W, H), nb.SensorConfig("depth", W, H),
+             nb.SensorConfig("gps_compass"))
+    a, b = (nb.BatchSimulator(sc.segments, sc.semantic_ids, sc.albedo, n, sensor_configs=suite)
+            for _ in range(2))
+    poses = synth.sample_poses(sc, n, seed=51)
+    for s in (a, b):
+        s.reset(poses[:, :2], poses[:, 2])
+    acts = synth.random_actions(n, 8, seed=52)
+    out = {"gps": np.empty((n, 2)), "compass": np.empty(n), "collided": np.empty(n, np.uint8),
+           "displacement": np.empty(n)}
+    for t in range(acts.shape[0]):
+        a_host = np.ascontiguousarray(acts[t])
+        b.step(torch.as_tensor(a_host, device="cuda:0"))
+        if t % 3 != 2:
+            a.step_host(a_host, out=out)
+            rgb_p, dep_p = ctypes.c_void_p(), ctypes.c_void_p()
+            nat.check(a.ctx.lib.nv_host_frames(a.ctx.handle, ctypes.byref(rgb_p),
+                                               ctypes.byref(dep_p), None))
+            rgb = torch.as_tensor(_Dev(rgb_p.value, (n, H, W, 3), "|u1"), device="cuda:0")
+            dep = torch.as_tensor(_Dev(dep_p.value, (n, H, W), "<f4"), device="cuda:0")
+            gps = out["gps"]
+        else:
+            a.step(torch.as_tensor(a_host, device="cuda:0"))
+            rgb, dep = a.groups[0]["rgb"], a.groups[0]["depth"]
+            gps = a.gps.cpu().numpy()
+        torch.cuda.synchronize()
+        assert np.array_equal(gps, b.gps.cpu().numpy()), t
+        assert torch.equal(rgb, b.groups[0]["rgb"]), t
+        assert torch.equal(dep, b.groups[0]["depth"]), t
