@@ -1182,6 +1182,7 @@ int nv_set_poses(nv_ctx *c, const double *xy, const double *heading, const uint8
 int nv_step(nv_ctx *c, const int8_t *actions, uint8_t *collided, double *displacement,
             int32_t *status, void *stream) {
   if (!c) return fail(NV_ERR_ARG, "ctx is NULL");
+  if (c->e_pending && (cudaStream_t)stream != c->e_stream) TRY(e2e_fence(c));
   TRY(ensure_envs(c));
   if (!actions) return fail(NV_ERR_ARG, "actions is NULL");
   return do_step(c, actions, collided, displacement, status, (cudaStream_t)stream);
@@ -1190,6 +1191,7 @@ int nv_step(nv_ctx *c, const int8_t *actions, uint8_t *collided, double *displac
 int nv_render(nv_ctx *c, int cam, uint8_t *rgb, float *depth, uint16_t *sem, double *gps,
               double *compass, void *stream) {
   if (!c) return fail(NV_ERR_ARG, "ctx is NULL");
+  if (c->e_pending && (cudaStream_t)stream != c->e_stream) TRY(e2e_fence(c));
   TRY(ensure_envs(c));
   TRY(cam_check(c, cam));
   cudaStream_t st = (cudaStream_t)stream;
@@ -1201,6 +1203,7 @@ int nv_step_render(nv_ctx *c, const int8_t *actions, int cam, uint8_t *rgb, floa
                    uint16_t *sem, double *gps, double *compass, uint8_t *collided,
                    double *displacement, int32_t *status, void *stream) {
   if (!c) return fail(NV_ERR_ARG, "ctx is NULL");
+  if (c->e_pending && (cudaStream_t)stream != c->e_stream) TRY(e2e_fence(c));
   TRY(ensure_envs(c));
   TRY(cam_check(c, cam));
   if (!actions) return fail(NV_ERR_ARG, "actions is NULL");
@@ -1525,6 +1528,7 @@ int nv_fill_frames(nv_ctx *c, int cam, int64_t n, const double *t_col, const int
                    const double *dirx, const double *diry, double sensor_height, uint8_t *rgb,
                    float *depth, uint16_t *sem, void *stream) {
   if (!c) return fail(NV_ERR_ARG, "ctx is NULL");
+  if (c->e_pending && (cudaStream_t)stream != c->e_stream) TRY(e2e_fence(c));
   TRY(ensure_scene(c));
   if (cam < 0 || cam >= 8 || !c->cams[cam].on) return fail(NV_ERR_STATE, "camera %d not configured", cam);
   if (n <= 0) return NV_OK;
