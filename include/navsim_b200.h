@@ -159,8 +159,9 @@ int nv_set_fill_mode(nv_ctx *ctx, int mode);
  * Returns when the step results are in the host buffers.  Without host frame
  * pointers the step runs as one replayed graph on an internal blocking stream
  * and returns as soon as its casts are done (the results are complete then);
- * the frame writer finishes behind the caller, ordered before the next host
- * step, before work on the legacy default stream, and before nv_host_frames /
+ * the frame writer finishes behind the caller on the step's own record
+ * buffer and counters (device steps on any stream may follow at once),
+ * ordered before the next host step and before nv_host_frames /
  * nv_camera_config / nv_envs_alloc / nv_scene_upload / nv_destroy return.
  * With host frame pointers the call synchronises before returning. */
 #define NV_CH_RGB 1u

@@ -94,8 +94,9 @@ struct Camera {
   double tables_cam_h = NAN;
   DevBuf u, tc, tf, rows, invh;
   DevBuf rec;      // ColRec N x W
-  DevBuf rec_e2e;  // the host-buffer step's own records (its frame writer may
-                   // still be reading them after nv_step_render_host returns)
+  DevBuf rec_e2e;  // the host-buffer step's own records and writer counters
+  DevBuf ctr_e2e;  // (its frame writer may still run after nv_step_render_host
+                   // returns, concurrently with device steps on other streams)
   DevBuf ctr;      // fill scheduler counters
   DevBuf cast_ctr; // persistent cast work counter (self-resetting)
   bool cast_ctr_init = false;
@@ -1182,7 +1183,6 @@ int nv_set_poses(nv_ctx *c, const double *xy, const double *heading, const uint8
 int nv_step(nv_ctx *c, const int8_t *actions, uint8_t *collided, double *displacement,
             int32_t *status, void *stream) {
   if (!c) return fail(NV_ERR_ARG, "ctx is NULL");
-  if (c->e_pending && (cudaStream_t)stream != c->e_stream) TRY(e2e_fence(c));
   TRY(ensure_envs(c));
   if (!actions) return fail(NV_ERR_ARG, "actions is NULL");
   return do_step(c, actions, collided, displacement, status, (cudaStream_t)stream);
@@ -1191,7 +1191,6 @@ int nv_step(nv_ctx *c, const int8_t *actions, uint8_t *collided, double *displac
 int nv_render(nv_ctx *c, int cam, uint8_t *rgb, float *depth, uint16_t *sem, double *gps,
               double *compass, void *stream) {
   if (!c) return fail(NV_ERR_ARG, "ctx is NULL");
-  if (c->e_pending && (cudaStream_t)stream != c->e_stream) TRY(e2e_fence(c));
   TRY(ensure_envs(c));
   TRY(cam_check(c, cam));
   cudaStream_t st = (cudaStream_t)stream;
@@ -1203,7 +1202,6 @@ int nv_step_render(nv_ctx *c, const int8_t *actions, int cam, uint8_t *rgb, floa
                    uint16_t *sem, double *gps, double *compass, uint8_t *collided,
                    double *displacement, int32_t *status, void *stream) {
   if (!c) return fail(NV_ERR_ARG, "ctx is NULL");
-  if (c->e_pending && (cudaStream_t)stream != c->e_stream) TRY(e2e_fence(c));
   TRY(ensure_envs(c));
   TRY(cam_check(c, cam));
   if (!actions) return fail(NV_ERR_ARG, "actions is NULL");
@@ -1355,6 +1353,10 @@ int nv_step_render_host(nv_ctx *c, const int8_t *actions_host, int cam, uint32_t
     }
     if (!c->e_cast_ev) CK(cudaEventCreateWithFlags(&c->e_cast_ev, cudaEventDisableTiming));
     TRY(c->cams[cam].rec_e2e.alloc(c->cams[cam].rec.bytes));
+    if (!c->cams[cam].ctr_e2e.p) {
+      TRY(c->cams[cam].ctr_e2e.alloc(16));
+      CK(cudaMemset(c->cams[cam].ctr_e2e.p, 0, 16));
+    }
     const bool same = c->e_graph && c->e_key_n == c->n_envs && c->e_key_gen == c->gen &&
                       key[0] == c->e_key[0] &&
                       key[1] == c->e_key[1] && key[2] == c->e_key[2] &&
@@ -1395,6 +1397,8 @@ int nv_step_render_host(nv_ctx *c, const int8_t *actions_host, int cam, uint32_t
       Camera &kc = c->cams[cam];
       std::swap(kc.rec.p, kc.rec_e2e.p);
       std::swap(kc.rec.bytes, kc.rec_e2e.bytes);
+      std::swap(kc.ctr.p, kc.ctr_e2e.p);
+      std::swap(kc.ctr.bytes, kc.ctr_e2e.bytes);
       c->mid_ev = c->e2e_mapped ? c->e_cast_ev : nullptr;
       int rc = nv_step_render(c, acts, cam, want_rgb ? c->e_rgb.as<uint8_t>() : nullptr,
                               want_d ? c->e_depth.as<float>() : nullptr,
@@ -1403,6 +1407,8 @@ int nv_step_render_host(nv_ctx *c, const int8_t *actions_host, int cam, uint32_t
       c->mid_ev = nullptr;
       std::swap(kc.rec.p, kc.rec_e2e.p);
       std::swap(kc.rec.bytes, kc.rec_e2e.bytes);
+      std::swap(kc.ctr.p, kc.ctr_e2e.p);
+      std::swap(kc.ctr.bytes, kc.ctr_e2e.bytes);
       if (!c->e2e_mapped) cudaMemcpyAsync(c->e_hout, pk, pack, cudaMemcpyDeviceToHost, es);
       cudaGraph_t g = nullptr;
       cudaError_t ce = cudaStreamEndCapture(es, &g);
@@ -1528,7 +1534,6 @@ int nv_fill_frames(nv_ctx *c, int cam, int64_t n, const double *t_col, const int
                    const double *dirx, const double *diry, double sensor_height, uint8_t *rgb,
                    float *depth, uint16_t *sem, void *stream) {
   if (!c) return fail(NV_ERR_ARG, "ctx is NULL");
-  if (c->e_pending && (cudaStream_t)stream != c->e_stream) TRY(e2e_fence(c));
   TRY(ensure_scene(c));
   if (cam < 0 || cam >= 8 || !c->cams[cam].on) return fail(NV_ERR_STATE, "camera %d not configured", cam);
   if (n <= 0) return NV_OK;
