@@ -1,6 +1,6 @@
 # parity tests + A/B runs; usage: RUNS='name|ENV=1 ENV2=2|--bench-args;...' bash scripts/gpu_ab.sh TAG
 TAG=${1:-ab}
-timeout 600 python -m pytest tests -m gpu -x -q -p no:cacheprovider 2>&1 | tail -4
+[ -z "$NO_PYTEST" ] && timeout 600 python -m pytest tests -m gpu -x -q -p no:cacheprovider 2>&1 | tail -4
 run() {  # name, env string, bench args
   local name=$1 envs=$2 args=$3
   env $envs timeout 300 python bench.py --steps 30 --warmup 5 --no-cpu-baseline --no-e2e $args > gpurun_out/${TAG}_${name}.json 2>gpurun_out/${TAG}_${name}.err

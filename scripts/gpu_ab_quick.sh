@@ -1,1 +1,2 @@
-sed '/pytest/d' scripts/gpu_ab.sh > /tmp/ab.sh; RUNS="$RUNS" bash /tmp/ab.sh "$1"
+# the A/B runs of gpu_ab.sh without the parity tests
+NO_PYTEST=1 RUNS="$RUNS" bash scripts/gpu_ab.sh "$1"
