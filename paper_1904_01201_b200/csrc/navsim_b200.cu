@@ -633,7 +633,12 @@ int launch_fill_ws(nv_ctx *c, nvk::FillArgs &a, cudaStream_t st) {
     const int R = o.rpw * nw / S;
     if (a.H % R) continue;
     const size_t slot = up((size_t)R * a.W * bpp);
-    for (int ns = o.nmax; ns >= o.nmin && !rpw; --ns) {
+    static const int slots_max = [] {  // tuning knob: ring slots (2..6; barriers fit 6)
+      const char *e = getenv("NAVSIM_WS_SLOTS");
+      const int v = e ? atoi(e) : 0;
+      return v >= 2 && v <= 6 ? v : 0;
+    }();
+    for (int ns = slots_max ? slots_max : o.nmax; ns >= o.nmin && !rpw; --ns) {
       const size_t tot = rows_b + (o.tab ? inv_b : 0) + cols_b + bars_b + (size_t)ns * slot;
       if ((int)tot <= c->max_smem_optin) {
         tab = o.tab; rpw = o.rpw; smem = tot;
