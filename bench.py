@@ -106,12 +106,15 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def ncu_traffic():
+def ncu_traffic(cfg: str):
     """dram read+write bytes per launch of the dominant kernel from the committed
-    ncu capture (profiles/r01_fill_traffic.json), or None."""
+    ncu capture (profiles/r01_fill_traffic.json) when it was taken on this
+    config, else None."""
     try:
         with open(os.path.join(ROOT, "profiles", "r01_fill_traffic.json")) as f:
             d = json.load(f)
+        if d.get("config", "C3") != cfg:
+            return None
         return int(d["dram_bytes_read"]) + int(d["dram_bytes_write"])
     except (OSError, KeyError, ValueError):
         return None
@@ -410,7 +413,7 @@ def run_gpu(args):
             "roofline": {"bound": "hbm", "kernel": dom,
                          "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak,
-                         "traffic": ncu_traffic() if not fused else None,
+                         "traffic": ncu_traffic(cfg) if not fused else None,
                          "traffic_source": "profiles/r01_fill_traffic.json (ncu --set full)",
                          "peak_source": peak_src,
                          "bytes_per_launch": dom_bytes,
