@@ -186,6 +186,7 @@ struct nv_ctx {
     for (auto e : prof_ev) cudaEventDestroy(e);
     if (e_graph) cudaGraphExecDestroy(e_graph);
     if (e_ev) cudaEventDestroy(e_ev);
+    if (e_cast_ev) cudaEventDestroy(e_cast_ev);
     if (e_stream) cudaStreamDestroy(e_stream);
     if (e_hin) cudaFreeHost(e_hin);
     if (e_hout) cudaFreeHost(e_hout);
