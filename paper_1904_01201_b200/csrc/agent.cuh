@@ -145,9 +145,11 @@ __global__ void __launch_bounds__(128) k_agent_step(EnvView ev, SceneView sc, Ag
 // env's flag for the next step.  (CTAs of the cast grid cover rays
 // [b*B, (b+1)*B) of the env-major ray order.)
 __device__ __forceinline__ void wait_envs_ready(unsigned *ready, unsigned *arrive, int W,
-                                                long long n_rays, int rays_per_block = 0) {
+                                                long long n_rays, int rays_per_block = 0,
+                                                long long block = -1) {
   const int rpb = rays_per_block > 0 ? rays_per_block : (int)blockDim.x;
-  const long long r0 = (long long)blockIdx.x * rpb;
+  const long long blk = block >= 0 ? block : (long long)blockIdx.x;
+  const long long r0 = blk * rpb;
   const long long r1 = min(n_rays, r0 + rpb) - 1;
   const int e0 = (int)(r0 / W), e1 = (int)(r1 / W);
   if (threadIdx.x == 0) {

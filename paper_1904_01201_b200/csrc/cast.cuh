@@ -400,18 +400,68 @@ __global__ void __launch_bounds__(128) k_column_cast_pool(EnvView ev, SceneView 
 __global__ void __launch_bounds__(128, NV_CAST_KMINB) k_column_cast(EnvView ev, SceneView sc, CamView cam,
                                                      RecOut ro, double t_max,
                                                      double *gps, double *compass,
-                                                     unsigned *ready, unsigned *arrive) {
+                                                     unsigned *ready, unsigned *arrive,
+                                                     const unsigned *order, unsigned *cost) {
+  // With `order`: CTA b casts ray block order[b] (blocks the previous step
+  // found slowest first -- longest-processing-time order, so the grid's last
+  // wave is made of short blocks) and records its block's duration in
+  // cost[] for the next step's ordering.  The rays, their results and the
+  // visit order inside each ray are unchanged.
+  const long long blk = order ? (long long)__ldg(order + blockIdx.x) : (long long)blockIdx.x;
+  long long t0 = 0;
+  if (order && threadIdx.x == 0) t0 = clock64();
   const long long total = (long long)ev.n * cam.W;
-  if (ready) wait_envs_ready(ready, arrive, cam.W, total);
-  const long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (g >= total) return;
-  // 32-bit division whenever the ray count fits (always, in practice)
-  const int e = total <= 0xffffffffLL ? (int)((unsigned)g / (unsigned)cam.W) : (int)(g / cam.W);
-  const int j = (int)(g - (long long)e * cam.W);
-  if (ready)
-    cast_column<true>(ev, sc, cam, e, j, ro, t_max, gps, compass);
-  else
-    cast_column<false>(ev, sc, cam, e, j, ro, t_max, gps, compass);
+  if (ready) wait_envs_ready(ready, arrive, cam.W, total, 0, blk);
+  const long long g = blk * (long long)blockDim.x + threadIdx.x;
+  if (g < total) {
+    // 32-bit division whenever the ray count fits (always, in practice)
+    const int e = total <= 0xffffffffLL ? (int)((unsigned)g / (unsigned)cam.W) : (int)(g / cam.W);
+    const int j = (int)(g - (long long)e * cam.W);
+    if (ready)
+      cast_column<true>(ev, sc, cam, e, j, ro, t_max, gps, compass);
+    else
+      cast_column<false>(ev, sc, cam, e, j, ro, t_max, gps, compass);
+  }
+  if (order) {
+    __syncthreads();
+    if (threadIdx.x == 0) cost[blk] = (unsigned)min(clock64() - t0, 0xffffffffLL);
+  }
+}
+
+__global__ void k_lpt_init(unsigned *order, unsigned *cost, unsigned n) {
+  const unsigned i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) {
+    order[i] = i;
+    cost[i] = 0;
+  }
+}
+
+// Longest-first order of the cast's ray blocks from their last durations:
+// a one-CTA counting sort over 256 log-spaced buckets (descending), run on
+// a side stream beside the frame writer.
+__global__ void __launch_bounds__(1024) k_cast_order(const unsigned *cost, unsigned *order,
+                                                     int nblk) {
+  __shared__ unsigned hist[256], base[256], mx;
+  const int t = threadIdx.x;
+  if (t == 0) mx = 0;
+  for (int k = t; k < 256; k += blockDim.x) hist[k] = 0;
+  __syncthreads();
+  for (int b = t; b < nblk; b += blockDim.x) atomicMax(&mx, cost[b]);
+  __syncthreads();
+  const int top = 32 - __clz(mx | 1u);          // bits of the largest cost
+  const int shift = top > 8 ? top - 8 : 0;
+  auto bucket = [&](unsigned c) { return 255 - (int)min(255u, c >> shift); };  // slow first
+  for (int b = t; b < nblk; b += blockDim.x) atomicAdd(&hist[bucket(cost[b])], 1u);
+  __syncthreads();
+  if (t == 0) {
+    unsigned acc = 0;
+    for (int k = 0; k < 256; ++k) {
+      base[k] = acc;
+      acc += hist[k];
+    }
+  }
+  __syncthreads();
+  for (int b = t; b < nblk; b += blockDim.x) order[atomicAdd(&base[bucket(cost[b])], 1u)] = (unsigned)b;
 }
 
 // Simulator.step + the column casts of one env per CTA: warp 0 runs the

@@ -94,6 +94,10 @@ struct Camera {
   double tables_cam_h = NAN;
   DevBuf u, tc, tf, rows, invh;
   DevBuf rec;      // ColRec N x W
+  DevBuf lpt_order, lpt_cost;  // thread-per-ray cast: block order (slowest first) + durations
+  int64_t lpt_n = -1;           // blocks the order is valid for
+  DevBuf lpt_order_e2e, lpt_cost_e2e;  // the host-buffer step's own copies
+  int64_t lpt_n_e2e = -1;
   DevBuf rec_e2e;  // the host-buffer step's own records and writer counters
   DevBuf ctr_e2e;  // (its frame writer may still run after nv_step_render_host
                    // returns, concurrently with device steps on other streams)
@@ -153,6 +157,10 @@ struct nv_ctx {
   cudaEvent_t e_cast_ev = nullptr;  // recorded in the host-step graph after the casts
   cudaEvent_t mid_ev = nullptr;     // nv_step_render records it after the casts (capture only)
   bool e_pending = false;           // a host step's frame writer may still be running
+  bool cast_lpt = true;             // longest-first ordering of the thread-per-ray cast
+  cudaStream_t o_stream = nullptr;  // side stream of the ordering kernel (beside the writer)
+  cudaEvent_t o_ev0 = nullptr, o_ev1 = nullptr;
+  bool o_fork = false;              // an ordering kernel was forked in this step
   cudaGraphExec_t e_graph = nullptr;
   int e_key[3] = {-1, -1, -1};
   int64_t e_key_n = -1, e_key_gen = -1;
@@ -187,6 +195,9 @@ struct nv_ctx {
     if (e_graph) cudaGraphExecDestroy(e_graph);
     if (e_ev) cudaEventDestroy(e_ev);
     if (e_cast_ev) cudaEventDestroy(e_cast_ev);
+    if (o_ev0) cudaEventDestroy(o_ev0);
+    if (o_ev1) cudaEventDestroy(o_ev1);
+    if (o_stream) cudaStreamDestroy(o_stream);
     if (e_stream) cudaStreamDestroy(e_stream);
     if (e_hin) cudaFreeHost(e_hin);
     if (e_hout) cudaFreeHost(e_hout);
@@ -773,6 +784,19 @@ int cast_queue_counter(Camera &k) {  // self-resetting work counter of k_column_
   return NV_OK;
 }
 
+// block order (identity) and durations (zero) for `nblk` cast blocks
+int lpt_buffers(nv_ctx *c, DevBuf &order, DevBuf &cost, int64_t &n, unsigned nblk,
+                cudaStream_t st) {
+  if (n == (int64_t)nblk) return NV_OK;
+  TRY(order.alloc(sizeof(unsigned) * nblk));
+  TRY(cost.alloc(sizeof(unsigned) * nblk));
+  nvk::k_lpt_init<<<blocks_for(nblk, 256), 256, 0, st>>>(order.as<unsigned>(),
+                                                          cost.as<unsigned>(), nblk);
+  TRY(check_launch(c));
+  n = nblk;
+  return NV_OK;
+}
+
 int do_cast(nv_ctx *c, int cam, double *gps, double *compass, cudaStream_t st) {
   Camera &k = c->cams[cam];
   if (c->cast_mode == 1 && k.W <= 2048) {
@@ -840,11 +864,18 @@ int do_cast(nv_ctx *c, int cam, double *gps, double *compass, cudaStream_t st) {
     const int v = e ? atoi(e) : 0;
     return v == 32 || v == 64 || v == 96 || v == 128 ? v : 128;
   }();
+  const unsigned nblk = blocks_for(total, cast_block);
+  unsigned *order = nullptr, *cost = nullptr;
+  if (c->cast_lpt) {
+    TRY(lpt_buffers(c, k.lpt_order, k.lpt_cost, k.lpt_n, nblk, st));
+    order = k.lpt_order.as<unsigned>();
+    cost = k.lpt_cost.as<unsigned>();
+  }
   Prof pf(c, st, 1);
   if (c->pdl_armed) {  // programmatic dependent of the agent step just launched
     c->pdl_armed = false;
     cudaLaunchConfig_t lc = {};
-    lc.gridDim = dim3(blocks_for(total, cast_block));
+    lc.gridDim = dim3(nblk);
     lc.blockDim = dim3(cast_block);
     lc.stream = st;
     cudaLaunchAttribute at[1];
@@ -854,13 +885,36 @@ int do_cast(nv_ctx *c, int cam, double *gps, double *compass, cudaStream_t st) {
     lc.numAttrs = 1;
     CK(cudaLaunchKernelEx(&lc, nvk::k_column_cast, c->env_view(), c->scene_view(), cam_view(k),
                           rec_out(k, c->n_envs), k.max_range, gps, compass,
-                          c->pdl_ready.as<unsigned>(), c->pdl_arrive.as<unsigned>()));
-    return check_launch(c);
+                          c->pdl_ready.as<unsigned>(), c->pdl_arrive.as<unsigned>(),
+                          (const unsigned *)order, cost));
+  } else {
+    nvk::k_column_cast<<<nblk, cast_block, 0, st>>>(
+        c->env_view(), c->scene_view(), cam_view(k), rec_out(k, c->n_envs), k.max_range, gps,
+        compass, nullptr, nullptr, order, cost);
   }
-  nvk::k_column_cast<<<blocks_for(total, cast_block), cast_block, 0, st>>>(
-      c->env_view(), c->scene_view(), cam_view(k), rec_out(k, c->n_envs), k.max_range, gps,
-      compass, nullptr, nullptr);
-  return check_launch(c);
+  TRY(check_launch(c));
+  if (order) {  // next step's order, on a side stream beside the frame writer
+    if (!c->o_stream) {
+      CK(cudaStreamCreateWithFlags(&c->o_stream, cudaStreamNonBlocking));
+      CK(cudaEventCreateWithFlags(&c->o_ev0, cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&c->o_ev1, cudaEventDisableTiming));
+    }
+    CK(cudaEventRecord(c->o_ev0, st));
+    CK(cudaStreamWaitEvent(c->o_stream, c->o_ev0, 0));
+    nvk::k_cast_order<<<1, 1024, 0, c->o_stream>>>(cost, order, (int)nblk);
+    TRY(check_launch(c));
+    CK(cudaEventRecord(c->o_ev1, c->o_stream));
+    c->o_fork = true;  // joined into `st` after the frame writer is launched
+  }
+  return NV_OK;
+}
+
+// join of the ordering kernel forked by do_cast
+int lpt_join(nv_ctx *c, cudaStream_t st) {
+  if (!c->o_fork) return NV_OK;
+  c->o_fork = false;
+  CK(cudaStreamWaitEvent(st, c->o_ev1, 0));
+  return NV_OK;
 }
 
 int nv_set_cast_mode_(nv_ctx *c, int mode) {
@@ -933,6 +987,7 @@ int nv_create(int device, nv_ctx **out) {
   c->device = device;
   if (const char *q = getenv("NAVSIM_CAST_QUEUE")) c->cast_queue = atoi(q) != 0;  // A/B knob
   if (const char *q = getenv("NAVSIM_PDL")) c->pdl = atoi(q) != 0;                // A/B knob
+  if (const char *q = getenv("NAVSIM_CAST_LPT")) c->cast_lpt = atoi(q) != 0;      // A/B knob
   if (const char *q = getenv("NAVSIM_CAST_POOL")) c->cast_pool = atoi(q);         // A/B knob
   if (const char *q = getenv("NAVSIM_E2E_MAPPED")) c->e2e_mapped = atoi(q) != 0;  // A/B knob
   cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device);
@@ -1204,7 +1259,9 @@ int nv_render(nv_ctx *c, int cam, uint8_t *rgb, float *depth, uint16_t *sem, dou
   TRY(cam_check(c, cam));
   cudaStream_t st = (cudaStream_t)stream;
   TRY(do_cast(c, cam, gps, compass, st));
-  return launch_fill(c, c->cams[cam], c->n_envs, rgb, depth, sem, st);
+  const int rc = launch_fill(c, c->cams[cam], c->n_envs, rgb, depth, sem, st);
+  TRY(lpt_join(c, st));
+  return rc;
 }
 
 int nv_step_render(nv_ctx *c, const int8_t *actions, int cam, uint8_t *rgb, float *depth,
@@ -1251,7 +1308,9 @@ int nv_step_render(nv_ctx *c, const int8_t *actions, int cam, uint8_t *rgb, floa
   TRY(do_cast(c, cam, gps, compass, st));
   c->pdl_armed = false;
   if (c->mid_ev) CK(cudaEventRecordWithFlags(c->mid_ev, st, cudaEventRecordExternal));
-  return launch_fill(c, k, c->n_envs, rgb, depth, sem, st);
+  const int rc = launch_fill(c, k, c->n_envs, rgb, depth, sem, st);
+  TRY(lpt_join(c, st));
+  return rc;
 }
 
 int nv_set_cast_mode(nv_ctx *c, int mode) {
@@ -1399,6 +1458,17 @@ int nv_step_render_host(nv_ctx *c, const int8_t *actions_host, int cam, uint32_t
       // capture (no allocation may happen while the stream is capturing)
       if (c->pdl) TRY(pdl_buffers(c));
       if (c->cast_queue) TRY(cast_queue_counter(c->cams[cam]));
+      if (c->cast_lpt) {  // the graph's own block order (thread-per-ray cast)
+        Camera &kk = c->cams[cam];
+        static const int cb = [] {
+          const char *e = getenv("NAVSIM_CAST_BLOCK");
+          const int v = e ? atoi(e) : 0;
+          return v == 32 || v == 64 || v == 96 || v == 128 ? v : 128;
+        }();
+        TRY(lpt_buffers(c, kk.lpt_order_e2e, kk.lpt_cost_e2e, kk.lpt_n_e2e,
+                        blocks_for(c->n_envs * (long long)kk.W, cb), nullptr));
+        CK(cudaDeviceSynchronize());
+      }
       CK(cudaStreamBeginCapture(es, cudaStreamCaptureModeThreadLocal));
       if (!c->e2e_mapped) cudaMemcpyAsync(c->e_act.p, c->e_hin, N, cudaMemcpyHostToDevice, es);
       // the graph's casts and writer use the host step's own record buffer,
@@ -1408,6 +1478,11 @@ int nv_step_render_host(nv_ctx *c, const int8_t *actions_host, int cam, uint32_t
       std::swap(kc.rec.bytes, kc.rec_e2e.bytes);
       std::swap(kc.ctr.p, kc.ctr_e2e.p);
       std::swap(kc.ctr.bytes, kc.ctr_e2e.bytes);
+      std::swap(kc.lpt_order.p, kc.lpt_order_e2e.p);
+      std::swap(kc.lpt_order.bytes, kc.lpt_order_e2e.bytes);
+      std::swap(kc.lpt_cost.p, kc.lpt_cost_e2e.p);
+      std::swap(kc.lpt_cost.bytes, kc.lpt_cost_e2e.bytes);
+      std::swap(kc.lpt_n, kc.lpt_n_e2e);
       c->mid_ev = c->e2e_mapped ? c->e_cast_ev : nullptr;
       int rc = nv_step_render(c, acts, cam, want_rgb ? c->e_rgb.as<uint8_t>() : nullptr,
                               want_d ? c->e_depth.as<float>() : nullptr,
@@ -1418,6 +1493,11 @@ int nv_step_render_host(nv_ctx *c, const int8_t *actions_host, int cam, uint32_t
       std::swap(kc.rec.bytes, kc.rec_e2e.bytes);
       std::swap(kc.ctr.p, kc.ctr_e2e.p);
       std::swap(kc.ctr.bytes, kc.ctr_e2e.bytes);
+      std::swap(kc.lpt_order.p, kc.lpt_order_e2e.p);
+      std::swap(kc.lpt_order.bytes, kc.lpt_order_e2e.bytes);
+      std::swap(kc.lpt_cost.p, kc.lpt_cost_e2e.p);
+      std::swap(kc.lpt_cost.bytes, kc.lpt_cost_e2e.bytes);
+      std::swap(kc.lpt_n, kc.lpt_n_e2e);
       if (!c->e2e_mapped) cudaMemcpyAsync(c->e_hout, pk, pack, cudaMemcpyDeviceToHost, es);
       cudaGraph_t g = nullptr;
       cudaError_t ce = cudaStreamEndCapture(es, &g);
