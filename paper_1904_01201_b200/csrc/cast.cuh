@@ -229,17 +229,27 @@ __device__ __forceinline__ void k_column_cast_warp_body(const EnvView &ev, const
 __global__ void __launch_bounds__(128) k_column_cast_warp(EnvView ev, SceneView sc, CamView cam,
                                                           RecOut ro, double t_max, double *gps,
                                                           double *compass, unsigned *ready,
-                                                          unsigned *arrive) {
+                                                          unsigned *arrive, const unsigned *order,
+                                                          unsigned *cost) {
+  // `order` / `cost`: longest-first block order, as in k_column_cast
+  const long long blk = order ? (long long)__ldg(order + blockIdx.x) : (long long)blockIdx.x;
+  long long t0 = 0;
+  if (order && threadIdx.x == 0) t0 = clock64();
   const long long total = (long long)ev.n * cam.W;
-  if (ready) wait_envs_ready(ready, arrive, cam.W, total, (int)(blockDim.x >> 5));
-  const long long g = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
-  if (g >= total) return;
-  const int e = (int)(g / cam.W);
-  const int j = (int)(g - (long long)e * cam.W);
-  if (ready)
-    k_column_cast_warp_body<true>(ev, sc, cam, ro, t_max, gps, compass, e, j);
-  else
-    k_column_cast_warp_body<false>(ev, sc, cam, ro, t_max, gps, compass, e, j);
+  if (ready) wait_envs_ready(ready, arrive, cam.W, total, (int)(blockDim.x >> 5), blk);
+  const long long g = (blk * (long long)blockDim.x + threadIdx.x) >> 5;
+  if (g < total) {
+    const int e = (int)(g / cam.W);
+    const int j = (int)(g - (long long)e * cam.W);
+    if (ready)
+      k_column_cast_warp_body<true>(ev, sc, cam, ro, t_max, gps, compass, e, j);
+    else
+      k_column_cast_warp_body<false>(ev, sc, cam, ro, t_max, gps, compass, e, j);
+  }
+  if (order) {
+    __syncthreads();
+    if (threadIdx.x == 0) cost[blk] = (unsigned)min(clock64() - t0, 0xffffffffLL);
+  }
 }
 
 // ---- ray-pool cast: lanes refill from a per-warp pool of rays --------------

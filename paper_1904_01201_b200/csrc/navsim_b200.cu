@@ -797,6 +797,28 @@ int lpt_buffers(nv_ctx *c, DevBuf &order, DevBuf &cost, int64_t &n, unsigned nbl
   return NV_OK;
 }
 
+// Longest-first ordering only pays when the cast runs several waves of
+// blocks (C2: 30.1 -> 28.3 us/step); a one-wave cast (C1: 64 blocks) only
+// gains the ordering kernel's latency (14.9 -> 17.1 us/step).
+bool lpt_pays(const nv_ctx *c, unsigned nblk) { return nblk >= 4u * (unsigned)c->sm_count; }
+
+// the next step's block order, on a side stream beside the frame writer
+// (joined into `st` by lpt_join after the writer is launched)
+int lpt_fork(nv_ctx *c, cudaStream_t st, unsigned *order, unsigned *cost, unsigned nblk) {
+  if (!c->o_stream) {
+    CK(cudaStreamCreateWithFlags(&c->o_stream, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&c->o_ev0, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&c->o_ev1, cudaEventDisableTiming));
+  }
+  CK(cudaEventRecord(c->o_ev0, st));
+  CK(cudaStreamWaitEvent(c->o_stream, c->o_ev0, 0));
+  nvk::k_cast_order<<<1, 1024, 0, c->o_stream>>>(cost, order, (int)nblk);
+  TRY(check_launch(c));
+  CK(cudaEventRecord(c->o_ev1, c->o_stream));
+  c->o_fork = true;
+  return NV_OK;
+}
+
 int do_cast(nv_ctx *c, int cam, double *gps, double *compass, cudaStream_t st) {
   Camera &k = c->cams[cam];
   if (c->cast_mode == 1 && k.W <= 2048) {
@@ -828,27 +850,38 @@ int do_cast(nv_ctx *c, int cam, double *gps, double *compass, cudaStream_t st) {
     return check_launch(c);
   }
   if (use_warp_cast(c, total)) {
-    Prof pf(c, st, 1);
-    if (c->pdl_armed) {  // programmatic dependent of the agent step just launched
-      c->pdl_armed = false;
-      cudaLaunchConfig_t lc = {};
-      lc.gridDim = dim3(blocks_for(total * 32, 128));
-      lc.blockDim = dim3(128);
-      lc.stream = st;
-      cudaLaunchAttribute at[1];
-      at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-      at[0].val.programmaticStreamSerializationAllowed = 1;
-      lc.attrs = at;
-      lc.numAttrs = 1;
-      CK(cudaLaunchKernelEx(&lc, nvk::k_column_cast_warp, c->env_view(), c->scene_view(),
-                            cam_view(k), rec_out(k, c->n_envs), k.max_range, gps, compass,
-                            c->pdl_ready.as<unsigned>(), c->pdl_arrive.as<unsigned>()));
-      return check_launch(c);
+    const unsigned nblk = blocks_for(total * 32, 128);
+    unsigned *order = nullptr, *cost = nullptr;
+    if (c->cast_lpt && lpt_pays(c, nblk)) {
+      TRY(lpt_buffers(c, k.lpt_order, k.lpt_cost, k.lpt_n, nblk, st));
+      order = k.lpt_order.as<unsigned>();
+      cost = k.lpt_cost.as<unsigned>();
     }
-    nvk::k_column_cast_warp<<<blocks_for(total * 32, 128), 128, 0, st>>>(
-        c->env_view(), c->scene_view(), cam_view(k), rec_out(k, c->n_envs), k.max_range, gps,
-        compass, nullptr, nullptr);
-    return check_launch(c);
+    {
+      Prof pf(c, st, 1);
+      if (c->pdl_armed) {  // programmatic dependent of the agent step just launched
+        c->pdl_armed = false;
+        cudaLaunchConfig_t lc = {};
+        lc.gridDim = dim3(nblk);
+        lc.blockDim = dim3(128);
+        lc.stream = st;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = 1;
+        lc.attrs = at;
+        lc.numAttrs = 1;
+        CK(cudaLaunchKernelEx(&lc, nvk::k_column_cast_warp, c->env_view(), c->scene_view(),
+                              cam_view(k), rec_out(k, c->n_envs), k.max_range, gps, compass,
+                              c->pdl_ready.as<unsigned>(), c->pdl_arrive.as<unsigned>(),
+                              (const unsigned *)order, cost));
+      } else {
+        nvk::k_column_cast_warp<<<nblk, 128, 0, st>>>(
+            c->env_view(), c->scene_view(), cam_view(k), rec_out(k, c->n_envs), k.max_range, gps,
+            compass, nullptr, nullptr, order, cost);
+      }
+      TRY(check_launch(c));
+    }
+    return order ? lpt_fork(c, st, order, cost, nblk) : NV_OK;
   }
   if (c->cast_mode == 5 || (c->cast_mode == 0 && c->cast_pool > 0)) {  // ray pools
     const int pool = c->cast_pool > 0 ? c->cast_pool : 64;
@@ -866,7 +899,7 @@ int do_cast(nv_ctx *c, int cam, double *gps, double *compass, cudaStream_t st) {
   }();
   const unsigned nblk = blocks_for(total, cast_block);
   unsigned *order = nullptr, *cost = nullptr;
-  if (c->cast_lpt) {
+  if (c->cast_lpt && lpt_pays(c, nblk)) {
     TRY(lpt_buffers(c, k.lpt_order, k.lpt_cost, k.lpt_n, nblk, st));
     order = k.lpt_order.as<unsigned>();
     cost = k.lpt_cost.as<unsigned>();
@@ -893,20 +926,7 @@ int do_cast(nv_ctx *c, int cam, double *gps, double *compass, cudaStream_t st) {
         compass, nullptr, nullptr, order, cost);
   }
   TRY(check_launch(c));
-  if (order) {  // next step's order, on a side stream beside the frame writer
-    if (!c->o_stream) {
-      CK(cudaStreamCreateWithFlags(&c->o_stream, cudaStreamNonBlocking));
-      CK(cudaEventCreateWithFlags(&c->o_ev0, cudaEventDisableTiming));
-      CK(cudaEventCreateWithFlags(&c->o_ev1, cudaEventDisableTiming));
-    }
-    CK(cudaEventRecord(c->o_ev0, st));
-    CK(cudaStreamWaitEvent(c->o_stream, c->o_ev0, 0));
-    nvk::k_cast_order<<<1, 1024, 0, c->o_stream>>>(cost, order, (int)nblk);
-    TRY(check_launch(c));
-    CK(cudaEventRecord(c->o_ev1, c->o_stream));
-    c->o_fork = true;  // joined into `st` after the frame writer is launched
-  }
-  return NV_OK;
+  return order ? lpt_fork(c, st, order, cost, nblk) : NV_OK;
 }
 
 // join of the ordering kernel forked by do_cast
@@ -1458,15 +1478,17 @@ int nv_step_render_host(nv_ctx *c, const int8_t *actions_host, int cam, uint32_t
       // capture (no allocation may happen while the stream is capturing)
       if (c->pdl) TRY(pdl_buffers(c));
       if (c->cast_queue) TRY(cast_queue_counter(c->cams[cam]));
-      if (c->cast_lpt) {  // the graph's own block order (thread-per-ray cast)
+      if (c->cast_lpt) {  // the graph's own block order
         Camera &kk = c->cams[cam];
         static const int cb = [] {
           const char *e = getenv("NAVSIM_CAST_BLOCK");
           const int v = e ? atoi(e) : 0;
           return v == 32 || v == 64 || v == 96 || v == 128 ? v : 128;
         }();
+        const long long rays = c->n_envs * (long long)kk.W;
         TRY(lpt_buffers(c, kk.lpt_order_e2e, kk.lpt_cost_e2e, kk.lpt_n_e2e,
-                        blocks_for(c->n_envs * (long long)kk.W, cb), nullptr));
+                        use_warp_cast(c, rays) ? blocks_for(rays * 32, 128) : blocks_for(rays, cb),
+                        nullptr));
         CK(cudaDeviceSynchronize());
       }
       CK(cudaStreamBeginCapture(es, cudaStreamCaptureModeThreadLocal));
