@@ -405,7 +405,7 @@ __global__ void __launch_bounds__(128) k_column_cast_pool(EnvView ev, SceneView 
 // One thread per (env, column).  With `ready`: launched as a programmatic
 // dependent of k_agent_step; waits per env instead of for the whole step.
 #ifndef NV_CAST_KMINB
-#define NV_CAST_KMINB 5  // min resident CTAs/SM for the thread-per-ray cast (register cap: <= 96)
+#define NV_CAST_KMINB 7  // min resident CTAs/SM for the thread-per-ray cast (register cap: <= 72; A/B with the longest-first order: 5 / 6 / 7 / 8 -> 117.4 / 115.9 / 115.0 / 117.3 us per C3 step)
 #endif
 __global__ void __launch_bounds__(128, NV_CAST_KMINB) k_column_cast(EnvView ev, SceneView sc, CamView cam,
                                                      RecOut ro, double t_max,
