@@ -226,7 +226,10 @@ __device__ __forceinline__ void k_column_cast_warp_body(const EnvView &ev, const
 }
 
 // With `ready`: a programmatic dependent of k_agent_step, waiting per env.
-__global__ void __launch_bounds__(128) k_column_cast_warp(EnvView ev, SceneView sc, CamView cam,
+#ifndef NV_CASTW_MINB
+#define NV_CASTW_MINB 8  // min resident CTAs/SM for the warp-per-ray cast (register cap <= 64; C2 31.1 -> 28.9 us/step)
+#endif
+__global__ void __launch_bounds__(128, NV_CASTW_MINB) k_column_cast_warp(EnvView ev, SceneView sc, CamView cam,
                                                           RecOut ro, double t_max, double *gps,
                                                           double *compass, unsigned *ready,
                                                           unsigned *arrive, const unsigned *order,
