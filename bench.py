@@ -425,7 +425,7 @@ def run_gpu(args):
             "e2e_host_frames": e2e_frames,
             "episode_stats": stats,
         }
-        if not args.no_cpu_baseline:
+        if not args.no_cpu_baseline and world == 1:  # reported at N=1 only
             line["cpu_baseline"] = cpu_baseline(cfg, seconds=args.cpu_seconds)
             # the one-worker figure the north-star's 10,000x target refers to
             # (SURVEY.md section 8(d)); a reported baseline like the one above
