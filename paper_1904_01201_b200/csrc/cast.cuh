@@ -466,12 +466,24 @@ __global__ void __launch_bounds__(1024) k_cast_order(const unsigned *cost, unsig
   auto bucket = [&](unsigned c) { return 255 - (int)min(255u, c >> shift); };  // slow first
   for (int b = t; b < nblk; b += blockDim.x) atomicAdd(&hist[bucket(cost[b])], 1u);
   __syncthreads();
-  if (t == 0) {
-    unsigned acc = 0;
-    for (int k = 0; k < 256; ++k) {
-      base[k] = acc;
-      acc += hist[k];
+  // exclusive prefix over the 256 buckets: 8 warps scan 32 each, then offsets
+  __shared__ unsigned wsum[8];
+  if (t < 256) {
+    const int lane = t & 31, w = t >> 5;
+    unsigned v = hist[t];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned u = __shfl_up_sync(0xffffffffu, v, o);
+      if (lane >= o) v += u;
     }
+    if (lane == 31) wsum[w] = v;
+    base[t] = v - hist[t];
+  }
+  __syncthreads();
+  if (t < 256) {
+    unsigned off = 0;
+    for (int w = 0; w < (t >> 5); ++w) off += wsum[w];
+    base[t] += off;
   }
   __syncthreads();
   for (int b = t; b < nblk; b += blockDim.x) order[atomicAdd(&base[bucket(cost[b])], 1u)] = (unsigned)b;
