@@ -236,7 +236,6 @@ def run_gpu(args):
                          floor_color=sc.floor_color, ceiling_color=sc.ceiling_color, device=local)
     poses = synth.sample_poses(sc, shard.n_total, seed=1)[shard.lo:shard.hi]
     sim.reset(poses[:, :2], poses[:, 2])
-    nat.check(sim.ctx.lib.nv_set_fused(sim.ctx.handle, 1 if args.fused else 0))
     nat.check(sim.ctx.lib.nv_set_overlap(sim.ctx.handle, 1 if args.overlap else 0))
     nat.check(sim.ctx.lib.nv_set_fill_mode(sim.ctx.handle, args.fill_mode))
     nat.check(sim.ctx.lib.nv_set_cast_mode(sim.ctx.handle, args.cast_mode))
@@ -317,22 +316,13 @@ def run_gpu(args):
     cnt = np.zeros(4, dtype=np.int64)
     nat.check(lib.nv_profile_read(h, nat.ptr(msk), nat.ptr(cnt)))
     nat.check(lib.nv_profile(h, 0))
-    names = ["agent_step", "column_cast", "frame_fill", "step_render_fused"]
+    names = ["agent_step", "column_cast", "frame_fill", "other"]
     per = {k: (msk[i] / cnt[i]) for i, k in enumerate(names) if cnt[i] > 0}
-    fused = "step_render_fused" in per
     frame_bytes = shard.n_local * W * H * sum(BYTES_PER_PX[c] for c in chans)
-    # dominant kernel: the fused step+render megakernel (algorithmic bytes = the
-    # frames it writes + the per-env step I/O), else the frame fill
-    if fused:
-        dom, dom_bytes, dom_ms = ("k_step_render (fused agent step + column cast + frame fill)",
-                                  shard.n_local * bytes_per_env_step(W, H, chans),
-                                  per["step_render_fused"])
-    else:
-        # auto (3) = the warp-specialised writer for every frame layout the
-        # bench configs use (256/128-wide, 16-row multiples)
-        writer = {0: "k_fill_direct", 1: "k_fill_tma", 2: "k_fill_ws"}.get(args.fill_mode,
-                                                                           "k_fill_ws")
-        dom, dom_bytes, dom_ms = f"{writer} (frame_fill)", frame_bytes, per["frame_fill"]
+    # dominant kernel: the frame writer (auto = the warp-specialised writer for
+    # every frame layout the bench configs use: 256/128-wide, 16-row multiples)
+    writer = "k_fill_generic" if args.fill_mode == 1 else "k_fill_ws"
+    dom, dom_bytes, dom_ms = f"{writer} (frame_fill)", frame_bytes, per["frame_fill"]
     peak, peak_src = measured_peaks()
     achieved = dom_bytes / (dom_ms / 1e3) / 1e9
     step_bytes = shard.n_local * bytes_per_env_step(W, H, chans)
@@ -405,15 +395,17 @@ def run_gpu(args):
                        "channels": list(chans), "segments": sc.n_segments,
                        "triangles": sc.n_triangles, "parallelism": f"env-shard x{world}",
                        "cuda_graph": use_graph,
-                       "graph_warm_replay": bool(use_graph and not args.cold_graph), "fused_megakernel": fused,
-                       "fill_mode": {0: "direct-stores", 1: "per-warp-tma-stages", 2: "warp-specialised-tma", 3: "auto (warp-specialised writer; row bands for small batches)"}.get(args.fill_mode),
-                       "cast_mode": ["dda (thread per ray; warp per ray for <= 16384 rays)", "binned", "dda-fused-with-agent-step", "dda-thread-per-ray", "dda-warp-per-ray"][args.cast_mode],
+                       "graph_warm_replay": bool(use_graph and not args.cold_graph),
+                       "fill_mode": ["auto (warp-specialised TMA writer; row bands for small batches)",
+                                     "per-pixel kernel"][args.fill_mode],
+                       "cast_mode": ["dda (thread per ray; warp per ray for <= 16384 rays)",
+                                     "dda-thread-per-ray", "dda-warp-per-ray"][args.cast_mode],
                        "l2": f"no flush: frames written per step "
                              f"({step_bytes / 1e6:.0f} MB/GPU) exceed the 126 MB L2"},
             "roofline": {"bound": "hbm", "kernel": dom,
                          "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak,
-                         "traffic": ncu_traffic(cfg) if not fused else None,
+                         "traffic": ncu_traffic(cfg),
                          "traffic_source": "profiles/r01_fill_traffic.json (ncu --set full)",
                          "peak_source": peak_src,
                          "bytes_per_launch": dom_bytes,
@@ -449,9 +441,10 @@ def main():
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--cold-graph", action="store_true",
                     help="time the graph's first replay (no untimed upload replay)")
-    ap.add_argument("--fill-mode", type=int, default=3, help="0 direct stores, 1 per-warp TMA stages, 2 warp-specialised writer, 3 auto")
-    ap.add_argument("--cast-mode", type=int, default=0, help="0 per-column DDA (auto), 1 binned, 2 DDA fused with the agent step, 3 thread/ray, 4 warp/ray")
-    ap.add_argument("--fused", action="store_true", help="one megakernel launch per step (experimental)")
+    ap.add_argument("--fill-mode", type=int, default=0, choices=[0, 1],
+                    help="0 auto (warp-specialised TMA writer), 1 per-pixel kernel")
+    ap.add_argument("--cast-mode", type=int, default=0, choices=[0, 1, 2],
+                    help="0 auto, 1 thread per ray, 2 warp per ray")
     ap.add_argument("--overlap", type=int, default=1,
                     help="agent step -> cast programmatic dependent launch overlap (1 = library default, 0 = off)")
     ap.add_argument("--no-e2e", action="store_true")

@@ -77,7 +77,10 @@ int nv_scene_grid_info(nv_ctx *ctx, double *x0, double *y0, int64_t *nx,
 int nv_agent_config(nv_ctx *ctx, double radius, double forward_step,
                     double turn_rad, double sensor_height);
 
-/* Allocate device state for n_envs environments (all un-reset). */
+/* Allocate device state for n_envs environments (all un-reset: origin,
+ * heading 0, the reference Simulator's initial AgentState, sim.py:159).  May
+ * be called again; it drops the PointGoal episodes of the previous batch
+ * (nv_task_reset starts new ones). */
 int nv_envs_alloc(nv_ctx *ctx, int64_t n_envs);
 
 /* Camera (sensor group sharing one traversal, sensors.py:121-123).
@@ -111,10 +114,14 @@ int nv_step(nv_ctx *ctx, const int8_t *actions, uint8_t *collided,
 int nv_render(nv_ctx *ctx, int cam, uint8_t *rgb, float *depth, uint16_t *sem,
               double *gps, double *compass, void *stream);
 
-/* Fused step + render: one call per simulator step for all envs.  When the
- * frame layout allows (W in {64, 128, 256k}, 16-byte aligned outputs) this is
- * ONE persistent kernel launch (step, cast and fill tasks overlapped through
- * a dependency-tracked queue); otherwise three launches. */
+/* Step + render: one call per simulator step for all envs -- nv_step then
+ * nv_render for camera `cam`, enqueued as three launches on `stream`: the
+ * agent step (k_agent_step, a warp per env), the column cast (a programmatic
+ * dependent of the agent step that starts each env's rays as soon as its new
+ * pose is published, see nv_set_overlap) and the frame writer (the
+ * warp-specialised TMA writer k_fill_ws when the frame layout allows it:
+ * W in {64, 128, 256k <= 4096}, whole 16-row slots, 16-byte aligned outputs;
+ * else the per-pixel k_fill_generic). */
 int nv_step_render(nv_ctx *ctx, const int8_t *actions, int cam, uint8_t *rgb,
                    float *depth, uint16_t *sem, double *gps, double *compass,
                    uint8_t *collided, double *displacement, int32_t *status,
@@ -122,37 +129,36 @@ int nv_step_render(nv_ctx *ctx, const int8_t *actions, int cam, uint8_t *rgb,
 
 /* Overlap of the agent step and the column cast in nv_step_render
  * (programmatic dependent launch: each env's casts start as soon as its agent
- * warp has published the new pose).  DDA casts (thread or warp per ray); on
- * by default (C2 32.3 -> 30.1 us/step, C3 end to end 140.4 -> 138.5 us), 0
- * turns it off. */
+ * warp has published the new pose); on by default (C2 32.3 -> 30.1 us/step,
+ * C3 end to end 140.4 -> 138.5 us), 0 turns it off. */
 int nv_set_overlap(nv_ctx *ctx, int on);
-/* Enable / disable (default) the single-launch megakernel of nv_step_render. */
-int nv_set_fused(nv_ctx *ctx, int on);
-/* Column cast: 0 (default) = per-column DDA over the grid (raycast_grid's
- * walk) -- one thread per ray, or one warp per ray (lanes split each cell's
- * entries) when the batch has at most 16384 rays (latency-bound sizes);
- * 3 / 4 force the thread / warp variant, 5 = the DDA by lanes refilling
- * from per-warp ray pools (no lane idles behind its warp's longest ray);
- * 1 = binned: one CTA per env projects the frustum's segments to
- * column spans and tests (segment, column) pairs exactly (raycast_all's
- * lexicographic minimum, which the reference defines raycast_grid to equal),
- * 2 = the DDA of mode 0 fused with the agent step in nv_step_render (one CTA
- * per env: its first warp steps the agent, then all threads cast). */
+/* Column cast (raycast_grid's DDA over the grid, bit-exact in every mode):
+ * NV_CAST_AUTO (default) = one thread per ray, or one warp per ray (lanes
+ * split each cell's entries) when the batch has at most 16384 rays
+ * (latency-bound sizes); NV_CAST_THREAD / NV_CAST_WARP force one of the two
+ * (parity tests compare them). */
+#define NV_CAST_AUTO 0
+#define NV_CAST_THREAD 1
+#define NV_CAST_WARP 2
 int nv_set_cast_mode(nv_ctx *ctx, int mode);
-/* Frame writer: 0 = 256-bit direct stores from registers,
- * 1 = per-warp shared-memory stages written out by TMA bulk copies,
- * 2 = warp-specialised: 16 producer warps render rows into a ring of
- *     smem slots, one store warp writes each slot with one bulk copy per
- *     channel (one CTA per SM, one env frame per work item),
- * 3 (default) = 2 whenever the frame layout allows it (small batches split
- * each frame into row bands to spread over the SMs), else 1.
- * All modes produce identical frames. */
+/* Frame writer: NV_FILL_AUTO (default) = the warp-specialised TMA writer
+ * (16 producer warps render rows into a ring of smem slots, one store warp
+ * writes each slot with one bulk copy per channel; one CTA per SM, small
+ * batches split each frame into row bands) whenever the frame layout allows
+ * it, else the per-pixel kernel; NV_FILL_GENERIC forces the per-pixel kernel.
+ * Both produce identical frames. */
+#define NV_FILL_AUTO 0
+#define NV_FILL_GENERIC 1
 int nv_set_fill_mode(nv_ctx *ctx, int mode);
 
 /* End-to-end call over HOST buffers (the reference-facing path: host actions
  * in, host results out).  Copies actions (host, n i8) in, runs
  * nv_step_render into device frames owned by the context (channels: bitmask
- * of NV_CH_*; a non-NULL host frame pointer implies its channel), copies the
+ * of NV_CH_*; a non-NULL host frame pointer implies its channel) -- for
+ * camera `cam`, or with cam = NV_ALL_CAMERAS for every camera k whose
+ * channel bits (channels >> 3k) & 7 are non-zero (the first such camera
+ * carries the step and gps/compass, the others are rendered after it; host
+ * frame pointers need a single camera) -- copies the
  * per-env step results (collided u8, displacement f64, gps f64x2, compass
  * f64) back to host buffers (any may be NULL) and, where the host frame
  * pointers are non-NULL, the frames too.  Host buffers should be pinned.
@@ -167,15 +173,16 @@ int nv_set_fill_mode(nv_ctx *ctx, int mode);
 #define NV_CH_RGB 1u
 #define NV_CH_DEPTH 2u
 #define NV_CH_SEM 4u
+#define NV_ALL_CAMERAS (-1)
 int nv_step_render_host(nv_ctx *ctx, const int8_t *actions_host, int cam,
                         uint32_t channels, uint8_t *rgb_host, float *depth_host,
                         uint16_t *sem_host, double *gps_host,
                         double *compass_host, uint8_t *collided_host,
                         double *displacement_host, void *stream);
-/* Device frame buffers written by nv_step_render_host (complete when this
- * returns, valid until the next call; for a GPU consumer of the host-driven
- * path). */
-int nv_host_frames(nv_ctx *ctx, uint8_t **rgb, float **depth, uint16_t **sem);
+/* Device frame buffers of camera `cam` written by nv_step_render_host
+ * (complete when this returns, valid until the next call; for a GPU consumer
+ * of the host-driven path; NULL for channels never rendered). */
+int nv_host_frames(nv_ctx *ctx, int cam, uint8_t **rgb, float **depth, uint16_t **sem);
 
 /* gps_compass (sensors.py:175-180) alone, for suites without visual sensors.
  * DEVICE outputs gps f64[n,2], compass f64[n] (either may be NULL). */
@@ -283,18 +290,21 @@ int nv_task_reset(nv_ctx *ctx, const double *goal, const double *gdsp, const int
  * same actions (DEVICE i8[n]) and that call's step status (DEVICE i32[n]):
  * Environment._distance_to_goal (1-ray line of sight, else the field),
  * success, SPL, reward, termination.  DEVICE outputs (each may be NULL):
- * reward f64[n], dist f64[n], done u8[n], outcome: 40-byte EpisodeOutcome
+ * reward f64[n], dist f64[n] (envs the step did not advance -- status != 0 --
+ * get reward 0 and their unchanged distance), done u8[n], outcome: 40-byte
+ * EpisodeOutcome
  * records written when an env terminates {u8 success, u8 terminated_by
  * (1 stop, 2 step_limit), u8[2], i32 steps, i32 collisions, i32, f64
  * path_taken, f64 shortest_path, f64 spl}.  Finished envs are frozen: later
  * steps report NV_ENV_DONE until the next nv_task_reset. */
 int nv_task_step(nv_ctx *ctx, const int8_t *actions, const int32_t *status, double *reward,
                  double *dist, uint8_t *done, void *outcome, void *stream);
-/* nv_step_render + nv_task_step in one call: the agent step and the task
- * arithmetic run in one kernel (a warp per env; the line-of-sight ray of
- * Environment._distance_to_goal is cast by the warp), then the column cast
- * and the frame fill.  Outputs as in nv_step_render and nv_task_step (the
- * step status is optional here). */
+/* nv_step_render + nv_task_step in one call: the agent step, then the
+ * column cast with the task arithmetic of each env (distance to goal with
+ * Environment._distance_to_goal's line-of-sight ray, reward, termination,
+ * outcome) riding on its column-0 thread (or warp), then the frame fill.
+ * Outputs as in nv_step_render and nv_task_step (the step status is
+ * optional here). */
 int nv_task_step_render(nv_ctx *ctx, const int8_t *actions, int cam, uint8_t *rgb,
                         float *depth, uint16_t *sem, double *gps, double *compass,
                         uint8_t *collided, double *displacement, int32_t *status,

@@ -20,6 +20,9 @@ NV_ERR_STATE = -3
 NV_ERR_OOM = -4
 NV_ENV_OK, NV_ENV_TOO_CLOSE, NV_ENV_NOT_RESET, NV_ENV_BAD_ACTION, NV_ENV_DONE = 0, 1, 2, 3, 4
 NV_CH_RGB, NV_CH_DEPTH, NV_CH_SEM = 1, 2, 4
+NV_ALL_CAMERAS = -1
+NV_CAST_AUTO, NV_CAST_THREAD, NV_CAST_WARP = 0, 1, 2
+NV_FILL_AUTO, NV_FILL_GENERIC = 0, 1
 
 # every symbol include/navsim_b200.h declares: (name, restype, argtypes)
 _P = ctypes.c_void_p
@@ -41,12 +44,11 @@ SIGNATURES = {
     "nv_step": (_I, [_P, _P, _P, _P, _P, _P]),
     "nv_render": (_I, [_P, _I, _P, _P, _P, _P, _P, _P]),
     "nv_step_render": (_I, [_P, _P, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
-    "nv_set_fused": (_I, [_P, _I]),
     "nv_set_overlap": (_I, [_P, _I]),
     "nv_set_fill_mode": (_I, [_P, _I]),
     "nv_set_cast_mode": (_I, [_P, _I]),
     "nv_step_render_host": (_I, [_P, _P, _I, _U32, _P, _P, _P, _P, _P, _P, _P, _P]),
-    "nv_host_frames": (_I, [_P, _P, _P, _P]),
+    "nv_host_frames": (_I, [_P, _I, _P, _P, _P]),
     "nv_gps_compass": (_I, [_P, _P, _P, _P]),
     "nv_get_state": (_I, [_P, _P, _P, _P, _P, _P]),
     "nv_get_frame": (_I, [_P, _P, _P, _P]),

@@ -22,6 +22,14 @@ class SimError(Exception):
     pass
 
 
+class _DevArray:
+    """Zero-copy view of a device buffer (``__cuda_array_interface__``)."""
+
+    def __init__(self, ptr: int, shape, typestr: str):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr,
+                                         "data": (ptr, False), "version": 3}
+
+
 ACTION_CODES = {"move_forward": 0, "turn_left": 1, "turn_right": 2, "stop": 3}
 
 
@@ -183,27 +191,38 @@ class BatchSimulator:
                   out=None, stream=None):
         """End-to-end step through the host-buffer C ABI (nv_step_render_host):
         host actions in, host step results out (and host frames if asked).
-        Only the first camera group is rendered on this path."""
+        Every camera group is rendered (the first one carries the step and
+        gps/compass); the frames stay in context-owned device buffers
+        (``host_step_frames``).  ``frames_to_host`` copies them into
+        ``out['rgb'|'depth'|'semantic']`` and needs a single camera group;
+        ``channels`` (NV_CH_* bits) restricts a single group's channels."""
         o = out or {}
         key = (id(o), frames_to_host, channels, stream)
         args = getattr(self, "_host_args", None)
         if args is None or args[0] != key:
             # the argument tuple is built once per (out buffers, mode); a step
             # then costs one pointer conversion and the C call
-            g = self.groups[0]
-            bits = 0
-            for k in g["kinds"]:
-                bits |= _CHANNEL_BIT[k]
-            if channels is not None:
-                bits = channels
+            if not self.groups:
+                raise SensorError("the host-buffer step renders at least one camera sensor")
+            if frames_to_host and len(self.groups) > 1:
+                raise SensorError("frames_to_host needs a single camera group")
             c = self.ctx
             st = nat.stream_handle(self.dev) if stream is None else stream
+            if len(self.groups) == 1:
+                g = self.groups[0]
+                cam = g["cam"]
+                bits = channels if channels is not None else self._group_bits(g)
+            else:
+                cam = nat.NV_ALL_CAMERAS
+                bits = 0
+                for g in self.groups:
+                    bits |= self._group_bits(g) << (3 * g["cam"])
             tail = (nat.ptr(o.get("rgb")) if frames_to_host else None,
                     nat.ptr(o.get("depth")) if frames_to_host else None,
                     nat.ptr(o.get("semantic")) if frames_to_host else None,
                     nat.ptr(o.get("gps")), nat.ptr(o.get("compass")), nat.ptr(o.get("collided")),
                     nat.ptr(o.get("displacement")), st)
-            args = (key, c.lib.nv_step_render_host, c.handle, g["cam"], bits, tail, o)
+            args = (key, c.lib.nv_step_render_host, c.handle, cam, bits, tail, o)
             self._host_args = args
         _, fn, h, cam, bits, tail, _ = args
         rc = fn(h, actions_host.ctypes.data if hasattr(actions_host, "ctypes") else nat.ptr(actions_host),
@@ -211,6 +230,31 @@ class BatchSimulator:
         if rc:
             nat.check(rc)
         return o
+
+    @staticmethod
+    def _group_bits(g) -> int:
+        bits = 0
+        for k in g["kinds"]:
+            bits |= _CHANNEL_BIT[k]
+        return bits
+
+    def host_step_frames(self) -> dict:
+        """Device frames written by the last ``step_host`` (all camera
+        groups; waits for the frame writers): {kind: torch tensor view}."""
+        import ctypes
+        import torch
+        out = {}
+        for g in self.groups:
+            p = [ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_void_p()]
+            nat.check(self.ctx.lib.nv_host_frames(self.ctx.handle, g["cam"], *(ctypes.byref(x) for x in p)))
+            N, h, w = self.n_envs, g["height"], g["width"]
+            for kind, ptr_, shape, typestr, dt in (
+                    ("rgb", p[0], (N, h, w, 3), "|u1", torch.uint8),
+                    ("depth", p[1], (N, h, w), "<f4", torch.float32),
+                    ("semantic", p[2], (N, h, w), "<u2", torch.uint16)):
+                if kind in g["kinds"] and ptr_.value:
+                    out[kind] = torch.as_tensor(_DevArray(ptr_.value, shape, typestr), device=self.dev)
+        return out
 
     def launches(self) -> int:
         return self.ctx.launches()

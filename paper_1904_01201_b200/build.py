@@ -11,7 +11,7 @@ SRC = os.path.join(HERE, "csrc", "navsim_b200.cu")
 OUT = os.path.join(HERE, "_lib", "libnavsim_b200.so")
 DEPS = [os.path.join(HERE, "csrc", f) for f in
         ("navsim_b200.cu", "kernels.cuh", "geom.cuh", "agent.cuh", "cast.cuh", "fill.cuh",
-         "mega.cuh", "device.cuh", "exact_math.cuh", "nav.cuh",
+         "device.cuh", "exact_math.cuh", "nav.cuh",
          "codec.cuh", "nav_task_abi.inc", "codec_abi.inc")] + [
     os.path.join(HERE, "..", "include", "navsim_b200.h")]
 

@@ -1,5 +1,5 @@
-// fill.cuh -- frame writers (fill_frame, _kernels.py:128-207): shading, the per-warp TMA,
-// direct and warp-specialised writers, depth noise, the generic per-pixel kernel.
+// fill.cuh -- frame writers (fill_frame, _kernels.py:128-207): packed-f16 shading, the
+// warp-specialised TMA writer, depth noise, the generic per-pixel kernel.
 #pragma once
 
 #include "cast.cuh"
@@ -45,11 +45,7 @@ struct FillArgs {
   uint8_t *rgb;
   float *depth;
   uint16_t *sem;
-  int rows_per_unit;   // rows of one work unit
-  int units_per_seg;   // ceil(H / rows_per_unit)
   int segs_per_row;    // W / (32 * CPL)
-  long long n_units;   // N * segs_per_row * units_per_seg
-  unsigned int *ctr;   // [0] next unit, [1] finished warps (self-resetting)
   const uint16_t *invh;  // ceil(H/2) x W f16 shading table 1/|(d_j, v_i)|, rows
                          // mirrored (v_{H-1-i} = -v_i); env-independent
   // inverse-depth noise (sensors.apply_inverse_depth_noise, sensors.py:183-205)
@@ -76,9 +72,11 @@ __device__ __forceinline__ unsigned long long splitmix64(unsigned long long z) {
 }
 
 __device__ __forceinline__ float2 noise_pair(const FillArgs &a, int env, int row, int col) {
+  // key (frame, global env, row, pair): a pair never straddles two rows, even
+  // for odd W
   const unsigned long long key =
-      ((((a.noise_frame << 20) ^ (unsigned long long)(env + a.env_offset)) * (unsigned long long)a.H +
-        (unsigned long long)row) * (unsigned long long)a.W + (unsigned long long)col) >> 1;
+      (((a.noise_frame << 20) ^ (unsigned long long)(env + a.env_offset)) * (unsigned long long)a.H +
+       (unsigned long long)row) * (unsigned long long)((a.W + 1) >> 1) + (unsigned long long)(col >> 1);
   const unsigned long long z = splitmix64(a.noise_seed ^ splitmix64(key));
   const float u1 = (float)((z >> 40) + 1ull) * 0x1p-24f;           // (0, 1]
   const float u2 = (float)((z >> 16) & 0xFFFFFFull) * 0x1p-24f;     // [0, 1)
@@ -337,25 +335,6 @@ __device__ __forceinline__ void shade_row(uint32_t i, const RowRec &R, const Col
                        cr.sw[c], iv[c]);
 }
 
-// A row that is plane (ceiling / floor / their void) in all of the lane's
-// columns: every pixel takes the row record's depth, semantic, colour and
-// cosine numerator; only the per-pixel 1/|(d, v)| differs.  Same arithmetic
-// as shade_pair with an all-plane mask, so the pixels are identical.
-template <int CPL>
-__device__ __forceinline__ void shade_row_plane(const RowRec &R, const uint32_t (&iv)[CPL / 2],
-                                                PairOut (&po)[CPL / 2]) {
-#pragma unroll
-  for (int c = 0; c < CPL / 2; ++c) {
-    const uint32_t t = h2_fma(R.num2, iv[c], NV_H2_POINT2);
-    po[c].r = h2_fma(R.r2, t, NV_H2_1024);
-    po[c].g = h2_fma(R.g2, t, NV_H2_1024);
-    po[c].b = h2_fma(R.b2, t, NV_H2_1024);
-    po[c].s = R.sem2;
-    po[c].d0 = R.depth_p;
-    po[c].d1 = R.depth_p;
-  }
-}
-
 // Writes the lane's shaded pixels of one row segment into a buffer laid out
 // like the frame (shared-memory stage / slot): px0 = pixel index of the
 // segment's first column in the buffer.
@@ -392,237 +371,6 @@ __device__ __forceinline__ void put_row(const PairOut (&po)[CPL / 2], uint8_t *r
   }
 }
 
-// Copies the camera's row table (H x 32 B) into shared memory; every warp of
-// the CTA reads its rows from there (uniform LDS, no L1/L2 misses under the
-// write stream).  Returns the first byte after the table (16-aligned).
-__device__ __forceinline__ uint8_t *stage_rows(const FillArgs &a, uint8_t *smem) {
-  const uint4 *src = reinterpret_cast<const uint4 *>(a.rows);
-  uint4 *dst = reinterpret_cast<uint4 *>(smem);
-  for (int k = threadIdx.x; k < a.H * 2; k += blockDim.x) dst[k] = __ldg(src + k);
-  __syncthreads();
-  return smem + (size_t)a.H * sizeof(RowRec);
-}
-
-// Per-warp state of the streaming writer: a private ring of NS smem stages.
-template <int CPL, int RW>
-struct FillWarp {
-  static constexpr int NS = 2;
-  static constexpr int SEGW = 32 * CPL;
-  uint8_t *wbase;
-  const RowRec *rows_s;  // shared-memory row table
-  int off_d, off_s, stage_bytes;
-  bool want_rgb, want_d, want_s;
-  uint64_t pol;
-  int k;  // stages issued so far
-  // smem layout: [row table H x 32 B][per-warp stage rings]
-  __device__ __forceinline__ void init(const FillArgs &a, uint8_t *smem, int wib) {
-    rows_s = reinterpret_cast<const RowRec *>(smem);
-    smem = stage_rows(a, smem);
-    want_rgb = a.rgb != nullptr;
-    want_d = a.depth != nullptr;
-    want_s = a.sem != nullptr;
-    off_d = want_rgb ? RW * SEGW * 3 : 0;
-    off_s = off_d + (want_d ? RW * SEGW * 4 : 0);
-    stage_bytes = off_s + (want_s ? RW * SEGW * 2 : 0);
-    wbase = smem + (size_t)wib * NS * stage_bytes;
-    pol = policy_evict_first();
-    k = 0;
-  }
-};
-
-// Render one unit = (env, column segment of 32*CPL columns, rows
-// [gidx*rpu, ...)) of fill_frame: the lane's CPL columns' parameters sit in
-// registers; RW rows at a time are rendered into a smem stage laid out exactly
-// like global memory, which lane 0 writes out with cp.async.bulk (one copy
-// per channel per stage when a warp covers full rows), evict-first in L2.
-// COH: the column records were written earlier in the same launch.
-template <int CPL, int RW, bool COH>
-__device__ __forceinline__ void fill_unit(const FillArgs &a, FillWarp<CPL, RW> &fw, int env,
-                                          int seg, int gidx) {
-  constexpr int NS = FillWarp<CPL, RW>::NS;
-  constexpr int SEGW = FillWarp<CPL, RW>::SEGW;
-  const int lane = threadIdx.x & 31;
-  const int W = a.W, H = a.H;
-  ColRegs<CPL> cr;
-  load_cols<CPL, COH>(a, (size_t)env * W + (size_t)seg * SEGW, lane, cr);
-  const int r_begin = gidx * a.rows_per_unit;
-  const int r_end = min(H, r_begin + a.rows_per_unit);
-  for (int r0 = r_begin; r0 < r_end; r0 += RW) {
-    const int nr = min(RW, r_end - r0);
-    uint8_t *buf = fw.wbase + (fw.k & (NS - 1)) * fw.stage_bytes;
-    if (fw.k >= NS) {
-      if (lane == 0) bulk_wait_read<NS - 1>();
-      __syncwarp();
-    }
-    for (int rr = 0; rr < nr; ++rr) {
-      const uint32_t i = (uint32_t)(r0 + rr);
-      const RowRec R = unpack_row(fw.rows_s, i);
-      uint32_t iv[CPL / 2];
-      load_inv<CPL, true>(a.invh + (size_t)inv_row(i, H) * W + seg * SEGW, lane, iv);
-      PairOut po[CPL / 2];
-      shade_row<CPL>(i, R, cr, iv, po);
-      put_row<CPL>(po, fw.want_rgb ? buf : nullptr,
-                   fw.want_d ? reinterpret_cast<float *>(buf + fw.off_d) : nullptr,
-                   fw.want_s ? reinterpret_cast<uint16_t *>(buf + fw.off_s) : nullptr,
-                   rr * SEGW, lane);
-    }
-    fence_proxy_async();
-    __syncwarp();
-    if (lane == 0) {
-      if (a.segs_per_row == 1) {
-        const size_t pix0 = ((size_t)env * H + r0) * W;
-        if (fw.want_rgb) bulk_store(a.rgb + pix0 * 3, buf, (unsigned)(nr * W * 3), fw.pol);
-        if (fw.want_d) bulk_store(a.depth + pix0, buf + fw.off_d, (unsigned)(nr * W * 4), fw.pol);
-        if (fw.want_s) bulk_store(a.sem + pix0, buf + fw.off_s, (unsigned)(nr * W * 2), fw.pol);
-      } else {
-        for (int rr = 0; rr < nr; ++rr) {
-          const size_t pix0 = ((size_t)env * H + r0 + rr) * W + (size_t)seg * SEGW;
-          if (fw.want_rgb)
-            bulk_store(a.rgb + pix0 * 3, buf + rr * SEGW * 3, (unsigned)(SEGW * 3), fw.pol);
-          if (fw.want_d)
-            bulk_store(a.depth + pix0, buf + fw.off_d + rr * SEGW * 4, (unsigned)(SEGW * 4),
-                       fw.pol);
-          if (fw.want_s)
-            bulk_store(a.sem + pix0, buf + fw.off_s + rr * SEGW * 2, (unsigned)(SEGW * 2), fw.pol);
-        }
-      }
-      bulk_commit();
-    }
-    ++fw.k;
-  }
-}
-
-// Drains this warp's bulk stores and, for the last warp of the grid, resets
-// the self-resetting work counter for the next launch.
-__device__ __forceinline__ void finish_grid(unsigned int *ctr) {
-  if ((threadIdx.x & 31) == 0) {
-    bulk_wait_all();
-    const unsigned total_warps = gridDim.x * (blockDim.x >> 5);
-    if (atomicAdd(ctr + 1, 1u) == total_warps - 1) {
-      ctr[0] = 0;
-      ctr[1] = 0;
-      __threadfence();
-    }
-  }
-}
-
-// k_fill_tma: streaming frame writer over all units of a frame batch; units
-// are pulled from a self-resetting global counter (one prefetched ahead).
-template <int CPL, int RW>
-__global__ void __launch_bounds__(128) k_fill_tma(FillArgs a) {
-  extern __shared__ __align__(128) uint8_t smem[];
-  const int lane = threadIdx.x & 31;
-  FillWarp<CPL, RW> fw;
-  fw.init(a, smem, threadIdx.x >> 5);
-  long long u = 0;
-  if (lane == 0) u = atomicAdd(a.ctr, 1u);
-  u = __shfl_sync(0xffffffffu, u, 0);
-  while (u < a.n_units) {
-    long long nxt = 0;
-    if (lane == 0) nxt = atomicAdd(a.ctr, 1u);
-    // row-block-major order: warps across the GPU render the same rows of
-    // different envs at the same time (shared row records / table rows)
-    const long long n_es = (long long)a.N * a.segs_per_row;
-    const int gidx = (int)(u / n_es);
-    const long long es = u - (long long)gidx * n_es;
-    const int env = (int)(es / a.segs_per_row);
-    const int seg = (int)(es - (long long)env * a.segs_per_row);
-    fill_unit<CPL, RW, false>(a, fw, env, seg, gidx);
-    u = __shfl_sync(0xffffffffu, nxt, 0);
-  }
-  finish_grid(a.ctr);
-}
-
-// ---- direct-store variant: no smem staging ---------------------------------
-// Each lane stores its pixels of a row straight from registers with
-// evict-first 128/64/32-bit stores; a warp's group-g stores are contiguous.
-__device__ __forceinline__ void st_v4f(float *p, float4 v, uint64_t pol) {
-  asm volatile("st.global.L2::cache_hint.v4.f32 [%0], {%1,%2,%3,%4}, %5;" ::"l"(p), "f"(v.x),
-               "f"(v.y), "f"(v.z), "f"(v.w), "l"(pol)
-               : "memory");
-}
-__device__ __forceinline__ void st_v2u(void *p, uint32_t a, uint32_t b, uint64_t pol) {
-  asm volatile("st.global.L2::cache_hint.v2.b32 [%0], {%1,%2}, %3;" ::"l"(p), "r"(a), "r"(b),
-               "l"(pol)
-               : "memory");
-}
-__device__ __forceinline__ void st_u(void *p, uint32_t a, uint64_t pol) {
-  asm volatile("st.global.L2::cache_hint.b32 [%0], %1, %2;" ::"l"(p), "r"(a), "l"(pol)
-               : "memory");
-}
-
-template <int CPL, bool COH>
-__device__ __forceinline__ void fill_unit_direct(const FillArgs &a, const RowRec *rows_s,
-                                                 uint64_t pol, int env, int seg, int gidx) {
-  using Ln = Lanes<CPL>;
-  const int lane = threadIdx.x & 31;
-  const int W = a.W, H = a.H;
-  ColRegs<CPL> cr;
-  load_cols<CPL, COH>(a, (size_t)env * W + (size_t)seg * Ln::SEGW, lane, cr);
-  const int r_begin = gidx * a.rows_per_unit;
-  const int r_end = min(H, r_begin + a.rows_per_unit);
-  for (int r = r_begin; r < r_end; ++r) {
-    const uint32_t i = (uint32_t)r;
-    const RowRec R = unpack_row(rows_s, i);
-    uint32_t iv[CPL / 2];
-    load_inv<CPL, true>(a.invh + (size_t)inv_row(i, H) * W + seg * Ln::SEGW, lane, iv);
-    PairOut po[CPL / 2];
-    shade_row<CPL>(i, R, cr, iv, po);
-    const size_t row0 = ((size_t)env * H + r) * W + (size_t)seg * Ln::SEGW;
-#pragma unroll
-    for (int g = 0; g < Ln::G; ++g) {
-      const size_t px = row0 + g * 32 * Ln::GW + lane * Ln::GW;
-      if constexpr (Ln::GW == 4) {
-        const PairOut &p = po[2 * g], &q = po[2 * g + 1];
-        if (a.rgb) {
-          uint32_t w0, w1, w2;
-          pack_rgb4(p, q, w0, w1, w2);
-          uint8_t *d = a.rgb + px * 3;
-          st_u(d, w0, pol);
-          st_u(d + 4, w1, pol);
-          st_u(d + 8, w2, pol);
-        }
-        if (a.depth) st_v4f(a.depth + px, make_float4(p.d0, p.d1, q.d0, q.d1), pol);
-        if (a.sem) st_v2u(a.sem + px, p.s, q.s, pol);
-      } else {
-        const PairOut &p = po[g];
-        if (a.rgb) {
-          uint16_t *d16 = reinterpret_cast<uint16_t *>(a.rgb + px * 3);
-          d16[0] = (uint16_t)__byte_perm(p.r, p.g, 0x0040);
-          d16[1] = (uint16_t)__byte_perm(p.b, p.r, 0x0060);
-          d16[2] = (uint16_t)__byte_perm(p.g, p.b, 0x0062);
-        }
-        if (a.depth) *reinterpret_cast<float2 *>(a.depth + px) = make_float2(p.d0, p.d1);
-        if (a.sem) *reinterpret_cast<uint32_t *>(a.sem + px) = p.s;
-      }
-    }
-  }
-}
-
-template <int CPL>
-__global__ void __launch_bounds__(128) k_fill_direct(FillArgs a) {
-  extern __shared__ __align__(128) uint8_t smem[];
-  stage_rows(a, smem);
-  const RowRec *rows_s = reinterpret_cast<const RowRec *>(smem);
-  const int lane = threadIdx.x & 31;
-  const uint64_t pol = policy_evict_first();
-  long long u = 0;
-  if (lane == 0) u = atomicAdd(a.ctr, 1u);
-  u = __shfl_sync(0xffffffffu, u, 0);
-  while (u < a.n_units) {
-    long long nxt = 0;
-    if (lane == 0) nxt = atomicAdd(a.ctr, 1u);
-    const long long n_es = (long long)a.N * a.segs_per_row;
-    const int gidx = (int)(u / n_es);
-    const long long es = u - (long long)gidx * n_es;
-    const int env = (int)(es / a.segs_per_row);
-    const int seg = (int)(es - (long long)env * a.segs_per_row);
-    fill_unit_direct<CPL, false>(a, rows_s, pol, env, seg, gidx);
-    u = __shfl_sync(0xffffffffu, nxt, 0);
-  }
-  finish_grid(a.ctr);
-}
-
 // ---- warp-specialised frame writer ------------------------------------------
 //
 // k_fill_ws: persistent, one CTA per SM = NW producer warps + 1 store warp; a
@@ -638,20 +386,12 @@ __global__ void __launch_bounds__(128) k_fill_direct(FillArgs a) {
 #ifndef NV_WS_CBUF
 #define NV_WS_CBUF 2  // record-plane buffers (prefetch distance CBUF - 1 items)
 #endif
-#ifndef NV_WS_RELEASE_NOW
-#define NV_WS_RELEASE_NOW 1  // release each slot as soon as its bulk reads are done
-#endif
-#ifndef NV_WS_PLANE_FAST
-#define NV_WS_PLANE_FAST 0  // 1: rows plane in all of a lane's columns skip the band masks (A/B: lane-divergent, slower at 512^2)
-#endif
 #ifndef NV_WS_DEBUG
 #define NV_WS_DEBUG 0  // 1: producers skip rendering, 2: no bulk stores (bound studies)
 #endif
 struct FillWsLayout {  // byte offsets into dynamic shared memory + ring geometry
   int rows, inv, cols, bars, slots;
   int slot_bytes, nslot, slot_rows;
-  int depth_direct;  // 1: producers store depth straight from registers (STG),
-                     // the slots carry RGB / semantic only
   int nw;            // producer warps (the CTA is nw + 1 warps)
   int bands;         // work items per env frame (row bands of H / bands rows):
                      // balances CTAs when envs per CTA is small
@@ -674,9 +414,8 @@ __global__ void __launch_bounds__(544, 1) k_fill_ws(FillArgs a, FillWsLayout L) 
   uint8_t *slots = smem + L.slots;
   const unsigned plane_bytes = (unsigned)W * 16u;
   const bool want_rgb = a.rgb != nullptr, want_d = a.depth != nullptr, want_s = a.sem != nullptr;
-  const bool slot_d = want_d && !L.depth_direct;
   const int off_d = want_rgb ? R * W * 3 : 0;
-  const int off_s = off_d + (slot_d ? R * W * 4 : 0);
+  const int off_s = off_d + (want_d ? R * W * 4 : 0);
   const int bands = BANDED ? L.bands : 1, band_rows = BANDED ? H / bands : H;
   const int slots_per_item = band_rows / R;
   const int n_items = a.N * bands;
@@ -718,7 +457,7 @@ __global__ void __launch_bounds__(544, 1) k_fill_ws(FillArgs a, FillWsLayout L) 
 #pragma unroll
     for (int j = 0; j < NV_WS_CBUF - 1; ++j)
       if (q + j * (int)gridDim.x < n_items) load_item(j, (q + j * (int)gridDim.x) / bands);
-    unsigned k = 0, slot = 0, use = 0, prev = 0;
+    unsigned slot = 0, use = 0;
     for (int it = 0; q < n_items; ++it, q += gridDim.x) {
       const int qn = q + (NV_WS_CBUF - 1) * (int)gridDim.x;
       if (qn < n_items) {
@@ -728,30 +467,21 @@ __global__ void __launch_bounds__(544, 1) k_fill_ws(FillArgs a, FillWsLayout L) 
         load_item(j % NV_WS_CBUF, qn / bands);
       }
       const int e = q / bands, row0 = (q - e * bands) * band_rows;
-      for (int sl = 0; sl < slots_per_item; ++sl, ++k) {
+      for (int sl = 0; sl < slots_per_item; ++sl) {
         mbar_wait(full + slot, use & 1u);
         const uint8_t *buf = slots + (size_t)slot * L.slot_bytes;
         const size_t pix0 = ((size_t)e * H + (size_t)row0 + (size_t)sl * R) * W;
 #if NV_WS_DEBUG != 2
         if (want_rgb) bulk_store(a.rgb + pix0 * 3, buf, (unsigned)(R * W * 3), pol);
-        if (slot_d) bulk_store(a.depth + pix0, buf + off_d, (unsigned)(R * W * 4), pol);
+        if (want_d) bulk_store(a.depth + pix0, buf + off_d, (unsigned)(R * W * 4), pol);
         if (want_s) bulk_store(a.sem + pix0, buf + off_s, (unsigned)(R * W * 2), pol);
 #else
         (void)buf; (void)pix0; (void)pol;
 #endif
         bulk_commit();
-#if NV_WS_RELEASE_NOW
         // wait for this slot's smem reads and hand it back at once
         bulk_wait_read<0>();
         mbar_arrive(empty + slot);
-        (void)prev;
-#else
-        if (k >= 1) {
-          bulk_wait_read<1>();
-          mbar_arrive(empty + prev);
-        }
-#endif
-        prev = slot;
         if (++slot == (unsigned)NSLOT) {
           slot = 0;
           ++use;
@@ -762,7 +492,6 @@ __global__ void __launch_bounds__(544, 1) k_fill_ws(FillArgs a, FillWsLayout L) 
     return;
   }
   // -------------------------------------------------------------- producers
-  const uint64_t dpol = policy_evict_first();
   const int seg = warp % S;
   const int rsub = warp / S;   // first row of this warp within a slot
   const int rstride = nw / S;  // row stride between the warp's RPW rows
@@ -774,14 +503,6 @@ __global__ void __launch_bounds__(544, 1) k_fill_ws(FillArgs a, FillWsLayout L) 
     ColRegs<CPL> cr;
     const float4 *cA = cols_s + (size_t)(it % NV_WS_CBUF) * 2 * W + seg * Ln::SEGW;
     load_cols_smem<CPL>(cA, cA + W, lane, cr);
-    // rows [0, plane_lo) are ceiling and rows [plane_hi, H) floor in all of
-    // this lane's columns
-    uint32_t plane_lo = cr.lo[0], plane_hi = cr.hi[0];
-#pragma unroll
-    for (int k = 1; k < CPL; ++k) {
-      plane_lo = min(plane_lo, cr.lo[k]);
-      plane_hi = max(plane_hi, cr.hi[k]);
-    }
     __syncwarp();
     if (lane == 0) mbar_arrive(colempty + (it % NV_WS_CBUF));
     for (int sl = 0; sl < slots_per_item; ++sl) {
@@ -802,10 +523,7 @@ __global__ void __launch_bounds__(544, 1) k_fill_ws(FillArgs a, FillWsLayout L) 
         else
           load_inv<CPL, true>(a.invh + (size_t)inv_row(i, H) * W + seg * Ln::SEGW, lane, iv);
         PairOut po[CPL / 2];
-        if (NV_WS_PLANE_FAST && (i < plane_lo || i >= plane_hi))  // plane in every column of the lane
-          shade_row_plane<CPL>(Rr, iv, po);
-        else
-          shade_row<CPL>(i, Rr, cr, iv, po);
+        shade_row<CPL>(i, Rr, cr, iv, po);
         if constexpr (NOISE) {
 #pragma unroll
           for (int c = 0; c < CPL / 2; ++c) {
@@ -817,24 +535,9 @@ __global__ void __launch_bounds__(544, 1) k_fill_ws(FillArgs a, FillWsLayout L) 
           }
         }
         put_row<CPL>(po, want_rgb ? buf : nullptr,
-                     slot_d ? reinterpret_cast<float *>(buf + off_d) : nullptr,
+                     want_d ? reinterpret_cast<float *>(buf + off_d) : nullptr,
                      want_s ? reinterpret_cast<uint16_t *>(buf + off_s) : nullptr,
                      rs * W + seg * Ln::SEGW, lane);
-        if (want_d && !slot_d) {  // depth straight to HBM: 16 B per lane, coalesced
-          float *drow = a.depth + ((size_t)e * H + i) * W + seg * Ln::SEGW;
-#pragma unroll
-          for (int g = 0; g < Ln::G; ++g) {
-            float *dp = drow + g * 32 * Ln::GW + lane * Ln::GW;
-            if constexpr (Ln::GW == 4) {
-              const PairOut &p = po[2 * g], &q = po[2 * g + 1];
-              asm volatile("st.global.L2::cache_hint.v4.f32 [%0], {%1,%2,%3,%4}, %5;" ::"l"(dp),
-                           "f"(p.d0), "f"(p.d1), "f"(q.d0), "f"(q.d1), "l"(dpol)
-                           : "memory");
-            } else {
-              *reinterpret_cast<float2 *>(dp) = make_float2(po[g].d0, po[g].d1);
-            }
-          }
-        }
       }
       fence_proxy_async();
       __syncwarp();
@@ -847,8 +550,9 @@ __global__ void __launch_bounds__(544, 1) k_fill_ws(FillArgs a, FillWsLayout L) 
   }
 }
 
-// Inverse-depth noise as a separate pass over a written depth batch (the
-// writers other than k_fill_ws); same per-pixel values as the fused path.
+// Inverse-depth noise as a separate pass over a written depth batch (after
+// k_fill_generic, and nv_depth_noise_apply); same per-pixel values as the
+// fused path of k_fill_ws.
 __global__ void k_depth_noise(FillArgs a, float *depth) {
   const long long p2 = blockIdx.x * (long long)blockDim.x + threadIdx.x;  // pixel pair
   const int half = (a.W + 1) / 2;

@@ -10,18 +10,16 @@
 //   cast.cuh   the column casts: _column_directions + raycast_grid + the exact
 //              row classification of fill_frame -> column records
 //              (k_column_cast thread per ray, k_column_cast_warp warp per ray
-//              for small batches, the binned and queue variants, the agent-fused
-//              k_step_cast) and the operator-level kernels (raycast, disc casts,
-//              clearance, fill from given hits).
+//              for small batches) and the operator-level kernels (raycast,
+//              disc casts, clearance, fill from given hits).
 //   fill.cuh   fill_frame's per-pixel resolve (_kernels.py:128-207) as HBM
 //              writers: k_fill_ws (warp-specialised: producer warps -> smem slots
-//              -> one TMA store warp), k_fill_tma (per-warp TMA stages),
-//              k_fill_direct (STG), k_fill_generic (any size), inverse-depth noise.
-//   mega.cuh   k_step_render, the opt-in persistent step+render megakernel.
+//              -> one TMA store warp), k_fill_generic (any size), inverse-depth
+//              noise.
 //
 // Exactness: every FP64 operation that decides coverage, semantics, depth or
 // pose uses the nvx:: _rn helpers (no FMA contraction), replicating the
 // reference's operation order.  Shading is packed f16 (RGB tolerance 1/255).
 #pragma once
 
-#include "mega.cuh"  // geom -> agent -> cast -> fill -> mega
+#include "fill.cuh"  // geom -> agent -> cast -> fill

@@ -463,6 +463,17 @@ __device__ __forceinline__ void task_finish(const TaskView &tv, int e, int a, do
   if (done_out) done_out[e] = tv.done[e];
 }
 
+// An env the step did not advance (not reset, episode over, bad action:
+// status != 0) earns nothing this step: reward 0, distance unchanged (the
+// reference raises instead of stepping it, task.py:196-197), so a caller
+// summing rewards over batch steps never counts a terminal reward twice.
+__device__ __forceinline__ void task_skip(const TaskView &tv, int e, double *reward, double *dist,
+                                          uint8_t *done_out) {
+  if (reward) reward[e] = 0.0;
+  if (dist) dist[e] = tv.d_last[e];
+  if (done_out) done_out[e] = tv.done[e];
+}
+
 // Environment.step's task arithmetic (task.py:193-243) after the agent step.
 __global__ void k_task_step(EnvView ev, SceneView sc, NavView nv, TaskView tv,
                             const int8_t *__restrict__ actions, const int32_t *step_status,
@@ -470,7 +481,7 @@ __global__ void k_task_step(EnvView ev, SceneView sc, NavView nv, TaskView tv,
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= ev.n) return;
   if (step_status && step_status[e] != 0) {  // not stepped (not reset / done / bad)
-    if (done_out) done_out[e] = tv.done[e];
+    task_skip(tv, e, reward, dist, done_out);
     return;
   }
   const double d_cur = distance_to_goal(sc, nv, tv, e, ev.x[e], ev.y[e]);
@@ -493,32 +504,6 @@ __device__ __forceinline__ double distance_to_goal_warp(const SceneView &sc, con
     if (!(t <= 1.0)) return euclid;
   }
   return geodesic_at(tv.fields + (size_t)tv.fid[e] * nv.nx * nv.ny, nv, px, py);
-}
-
-// Simulator.step + Environment.step's task arithmetic in one warp per env
-// (nv_task_step_render): the agent step, then -- for stepped envs -- the
-// distance to the goal at the new pose, reward, termination and outcome,
-// with no second launch and no re-read of the agent state.
-__global__ void __launch_bounds__(128) k_agent_task_step(EnvView ev, SceneView sc, AgentCfg cfg,
-                                                         const int8_t *__restrict__ actions,
-                                                         uint8_t *collided_out, double *disp_out,
-                                                         int32_t *status_out, NavView nv,
-                                                         TaskView tv, double *reward,
-                                                         double *dist, uint8_t *done_out,
-                                                         OutcomeRec *out) {
-  const int e = (int)((blockIdx.x * (size_t)blockDim.x + threadIdx.x) >> 5);
-  if (e >= ev.n) return;
-  const int lane = threadIdx.x & 31;
-  const int a = actions[e];
-  AgentPost post;
-  warp_agent_step(ev, sc, cfg, e, a, collided_out, disp_out, status_out, &post);
-  if (post.status != 0) {
-    if (lane == 0 && done_out) done_out[e] = tv.done[e];
-    return;
-  }
-  const double d_cur = distance_to_goal_warp(sc, nv, tv, e, post.x, post.y);
-  if (lane != 0) return;
-  task_finish(tv, e, a, d_cur, post.path, post.coll, reward, dist, done_out, out);
 }
 
 // The task arithmetic riding on the column cast (nv_task_step_render with the
@@ -545,7 +530,7 @@ __global__ void __launch_bounds__(128) k_column_cast_task(EnvView ev, SceneView 
   const int j = (int)(g - (long long)e * cam.W);
   if (j == 0) {  // before the ray: the env's task step
     if (to.status[e] != 0) {
-      if (to.done) to.done[e] = to.tv.done[e];
+      task_skip(to.tv, e, to.reward, to.dist, to.done);
     } else {
       const double px = ev.x[e], py = ev.y[e];
       const double d_cur = distance_to_goal(sc, to.nv, to.tv, e, px, py);
@@ -568,7 +553,7 @@ __global__ void __launch_bounds__(128) k_column_cast_warp_task(EnvView ev, Scene
   if (j == 0) {
     const int lane = threadIdx.x & 31;
     if (to.status[e] != 0) {
-      if (lane == 0 && to.done) to.done[e] = to.tv.done[e];
+      if (lane == 0) task_skip(to.tv, e, to.reward, to.dist, to.done);
     } else {
       const double d_cur = distance_to_goal_warp(sc, to.nv, to.tv, e, ev.x[e], ev.y[e]);
       if (lane == 0)

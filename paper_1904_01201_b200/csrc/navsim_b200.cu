@@ -26,6 +26,40 @@
 
 using namespace nvd;
 
+// Compile-time study switches (A/B builds with -D...).  The shipped library
+// is built with these defaults; its behaviour does not depend on the
+// environment.  A/B numbers: profiles/r01_fill_ab_history.json, DESIGN.md.
+#ifndef NV_CAST_WARP_RAYS
+#define NV_CAST_WARP_RAYS 16384  // batches with at most this many rays cast one warp per ray
+#endif
+#ifndef NV_CAST_BLOCK
+#define NV_CAST_BLOCK 128  // threads per CTA of the thread-per-ray cast (32/64/96/128 within noise)
+#endif
+#ifndef NV_CAST_LPT
+#define NV_CAST_LPT 1  // longest-first order of the cast's blocks (C3 -2 us/step)
+#endif
+#ifndef NV_WS_NW
+#define NV_WS_NW 16  // producer warps of the ws writer (4 / 8 / 16)
+#endif
+#ifndef NV_WS_SLOTS
+#define NV_WS_SLOTS 0  // ring slots of the ws writer (0: as many as fit, <= 4)
+#endif
+#ifndef NV_WS_TAB
+#define NV_WS_TAB 0  // 1: stage the shading table in shared memory
+#endif
+#ifndef NV_WS_BANDS
+#define NV_WS_BANDS 0  // row bands per env frame (0: cost model)
+#endif
+#ifndef NV_WS_RPW
+#define NV_WS_RPW 0  // rows per producer warp per slot (0: auto)
+#endif
+#ifndef NV_E2E_MAPPED
+#define NV_E2E_MAPPED 1  // host-buffer step: kernels read actions / write results in mapped pinned memory
+#endif
+#ifndef NV_NAV_HOSTLOOP
+#define NV_NAV_HOSTLOOP 0  // 1: distance-field relaxation as host-driven launches
+#endif
+
 namespace {
 
 thread_local std::string g_err;
@@ -96,19 +130,12 @@ struct Camera {
   DevBuf rec;      // ColRec N x W
   DevBuf lpt_order, lpt_cost;  // thread-per-ray cast: block order (slowest first) + durations
   int64_t lpt_n = -1;           // blocks the order is valid for
-  DevBuf lpt_order_e2e, lpt_cost_e2e;  // the host-buffer step's own copies
+  // The host-buffer step's own record buffer and block order (its frame
+  // writer may still run after nv_step_render_host returns, concurrently with
+  // device steps on other streams) and its device frames (nv_host_frames).
+  DevBuf rec_e2e, lpt_order_e2e, lpt_cost_e2e;
   int64_t lpt_n_e2e = -1;
-  DevBuf rec_e2e;  // the host-buffer step's own records and writer counters
-  DevBuf ctr_e2e;  // (its frame writer may still run after nv_step_render_host
-                   // returns, concurrently with device steps on other streams)
-  DevBuf ctr;      // fill scheduler counters
-  DevBuf cast_ctr; // persistent cast work counter (self-resetting)
-  bool cast_ctr_init = false;
-  // fused step+render megakernel task queue (rebuilt when N or layout changes)
-  DevBuf tasks, envsync;
-  int64_t tasks_n = -1;
-  int tasks_key = -1;
-  int n_tasks = 0, n_cast = 0, n_fill = 0;
+  DevBuf e_rgb, e_depth, e_sem;
 };
 
 }  // namespace
@@ -149,7 +176,7 @@ struct nv_ctx {
   DevBuf x, y, h, path, coll, ch, sh, ox, oy, oh, fc, fs, reset;
   Camera cams[8];
   // host-buffer (e2e) path scratch
-  DevBuf e_act, e_rgb, e_depth, e_sem, e_pack;  // e_pack: gps 16N | compass 8N | disp 8N | coll N
+  DevBuf e_act, e_pack;  // e_pack: gps 16N | compass 8N | disp 8N | coll N
   // host-buffer path as one CUDA graph: H2D actions -> step+render -> one D2H
   // of the packed step results, replayed while (cam, channels, N) stay fixed
   cudaStream_t e_stream = nullptr;
@@ -157,32 +184,25 @@ struct nv_ctx {
   cudaEvent_t e_cast_ev = nullptr;  // recorded in the host-step graph after the casts
   cudaEvent_t mid_ev = nullptr;     // nv_step_render records it after the casts (capture only)
   bool e_pending = false;           // a host step's frame writer may still be running
-  bool cast_lpt = true;             // longest-first ordering of the thread-per-ray cast
   cudaStream_t o_stream = nullptr;  // side stream of the ordering kernel (beside the writer)
   cudaEvent_t o_ev0 = nullptr, o_ev1 = nullptr;
   bool o_fork = false;              // an ordering kernel was forked in this step
   cudaGraphExec_t e_graph = nullptr;
-  int e_key[3] = {-1, -1, -1};
-  int64_t e_key_n = -1, e_key_gen = -1;
-  bool e_key_direct = false;
-  void *e_key_out[4] = {nullptr, nullptr, nullptr, nullptr};
+  std::vector<uint64_t> e_key;  // everything the captured graph depends on (HostStepKey)
   void *e_out_host[4] = {nullptr, nullptr, nullptr, nullptr};  // last caller buffers
   void *e_out_dev[4] = {nullptr, nullptr, nullptr, nullptr};   // their device aliases
   int64_t gen = 0;  // bumped by every call that changes kernel arguments (graph key)
   void *e_hin = nullptr, *e_hout = nullptr;  // pinned staging (actions in, packed results out)
   size_t e_hin_bytes = 0, e_hout_bytes = 0;
   int64_t launches = 0;
-  int cast_mode = 0;         // nv_set_cast_mode (include/navsim_b200.h)
-  bool cast_queue = false;   // column cast by persistent warps over a work counter (opt-in: slower)
-  int cast_pool = 0;         // > 0: ray-pool cast with this many rays per warp (cast mode 0)
-  bool e2e_mapped = true;    // host-buffer graph path: zero-copy actions / results
+  int cast_mode = NV_CAST_AUTO;  // nv_set_cast_mode (include/navsim_b200.h)
+  bool e2e_mapped = NV_E2E_MAPPED != 0;  // host-buffer graph path: zero-copy actions / results
   bool pdl = true;           // agent step -> cast programmatic dependent launch (nv_set_overlap)
   bool pdl_armed = false, pdl_init = false;
   DevBuf pdl_ready, pdl_arrive;
   // dynamic shared memory opted in per kernel on this context's device
   std::unordered_map<const void *, size_t> smem_cfg;
-  int fill_mode = 3;   // 0 direct stores, 1 per-warp TMA stages, 2 warp-specialised, 3 auto
-  bool fused = false;  // nv_step_render uses the megakernel when the layout allows (opt-in)
+  int fill_mode = NV_FILL_AUTO;  // nv_set_fill_mode
   // optional per-kernel CUDA-event timing (bench roofline evidence)
   bool prof_on = false;
   std::vector<cudaEvent_t> prof_ev;   // pool, pairs
@@ -443,144 +463,12 @@ unsigned blocks_for(long long work, int per_block) {
   return (unsigned)std::max<long long>(1, (work + per_block - 1) / per_block);
 }
 
-// Fill work decomposition shared by k_fill_tma and the megakernel.
-template <int CPL>
-void fill_layout(nvk::FillArgs &a, int sm_count = 148) {
-  a.segs_per_row = a.W / (32 * CPL);
-  static const int rpu = [] {  // tuning knob (rows per work unit), default 16
-    const char *e = getenv("NAVSIM_FILL_RPU");
-    const int v = e ? atoi(e) : 0;
-    return v >= 2 && v <= 256 ? v : 0;
-  }();
-  // 16-row units, shortened (down to 2 rows) when a small batch would leave
-  // warps idle: aim for >= 4 units per SM
-  long long rows = (long long)a.N * a.segs_per_row * a.H;
-  int r = (int)std::min<long long>(16, std::max<long long>(2, rows / (4LL * sm_count)));
-  a.rows_per_unit = rpu ? rpu : (r & ~1);
-  a.units_per_seg = (a.H + a.rows_per_unit - 1) / a.rows_per_unit;
-  a.n_units = (long long)a.N * a.segs_per_row * a.units_per_seg;
-}
-
-// Fill launch: TMA streaming writer when the row layout allows 16-byte bulk
-// copies, else the generic per-pixel kernel.
-#ifndef NV_FILL_RW
-#define NV_FILL_RW 2
-#endif
-template <int CPL>
-int launch_fill_tma(nv_ctx *c, nvk::FillArgs &a, cudaStream_t st) {
-  constexpr int RW = NV_FILL_RW;
-  const int segw = 32 * CPL;
-  const int bpp = (a.rgb ? 3 : 0) + (a.depth ? 4 : 0) + (a.sem ? 2 : 0);
-  const int stage = RW * segw * bpp;
-  const int warps = 4;
-  const size_t smem = (size_t)a.H * sizeof(RowRec) + (size_t)warps * 2 * stage;
-  auto kern = nvk::k_fill_tma<CPL, RW>;
-  TRY(set_smem(c, (const void *)kern, smem));
-  int per_sm = 0;
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, warps * 32, smem));
-  per_sm = std::max(1, per_sm);
-  fill_layout<CPL>(a, c->sm_count);
-  long long want = (a.n_units + warps - 1) / warps;
-  unsigned grid = (unsigned)std::max<long long>(1, std::min<long long>(want, (long long)per_sm * c->sm_count));
-  Prof pf(c, st, 2);
-  kern<<<grid, warps * 32, smem, st>>>(a);
-  return check_launch(c);
-}
-
-// Task queue of the megakernel: STEP(e + LS + LC), CAST(e + LC, *), FILL(e, *)
-// per round, so every dependency is dequeued before its dependents.
-int build_tasks(Camera &cam, int64_t N, int n_cast, int n_fill, int key) {
-  if (cam.tasks_n == N && cam.tasks_key == key) return NV_OK;
-  const int64_t LS = std::min<int64_t>(32, N), LC = std::min<int64_t>(96, N);
-  std::vector<int2> t;
-  t.reserve((size_t)N * (1 + n_cast + n_fill));
-  for (int64_t r = 0; r < N + LS + LC; ++r) {
-    if (r < N) t.push_back(make_int2(nvk::NV_TASK_STEP << 24, (int)r));
-    const int64_t ec = r - LS;
-    if (ec >= 0 && ec < N)
-      for (int k = 0; k < n_cast; ++k) t.push_back(make_int2((nvk::NV_TASK_CAST << 24) | k, (int)ec));
-    const int64_t ef = r - LS - LC;
-    if (ef >= 0 && ef < N)
-      for (int k = 0; k < n_fill; ++k) t.push_back(make_int2((nvk::NV_TASK_FILL << 24) | k, (int)ef));
-  }
-  TRY(upload(cam.tasks, t));
-  TRY(cam.envsync.alloc(sizeof(uint32_t) * 3 * (size_t)N));
-  CK(cudaMemset(cam.envsync.p, 0, sizeof(uint32_t) * 3 * (size_t)N));
-  cam.n_tasks = (int)t.size();
-  cam.n_cast = n_cast;
-  cam.n_fill = n_fill;
-  cam.tasks_n = N;
-  cam.tasks_key = key;
-  return NV_OK;
-}
-
-template <int CPL>
-int launch_mega(nv_ctx *c, Camera &cam, const int8_t *actions, uint8_t *rgb, float *depth,
-                uint16_t *sem, double *gps, double *compass, uint8_t *collided, double *disp,
-                int32_t *status, cudaStream_t st) {
-  constexpr int RW = 2;
-  nvk::MegaArgs m;
-  m.ev = c->env_view();
-  m.sc = c->scene_view();
-  m.cam = cam_view(cam);
-  m.cfg = nvk::AgentCfg{c->radius, c->step, c->turn_rad};
-  nvk::FillArgs &a = m.f;
-  m.ro = rec_out(cam, c->n_envs);
-  a.ra = m.ro.a;
-  a.rb = m.ro.b;
-  a.cpl = m.ro.cpl;
-  a.rows = cam.rows.as<RowRec>();
-  a.invh = cam.invh.as<uint16_t>();
-  a.N = (int)c->n_envs; a.W = cam.W; a.H = cam.H;
-  a.rgb = rgb; a.depth = depth; a.sem = sem;
-  a.ctr = cam.ctr.as<unsigned int>();
-  fill_layout<CPL>(a);
-  const int n_cast = (cam.W + 31) / 32;
-  const int n_fill = a.segs_per_row * a.units_per_seg;
-  TRY(build_tasks(cam, c->n_envs, n_cast, n_fill, CPL * 1000 + a.rows_per_unit));
-  m.actions = actions; m.collided = collided; m.disp = disp; m.status = status;
-  m.gps = gps; m.compass = compass;
-  m.t_max = cam.max_range;
-  m.tasks = cam.tasks.as<int2>();
-  m.n_tasks = cam.n_tasks;
-  m.n_cast = cam.n_cast;
-  m.n_fill = cam.n_fill;
-  m.envsync = cam.envsync.as<unsigned int>();
-  const int segw = 32 * CPL;
-  const int bpp = (rgb ? 3 : 0) + (depth ? 4 : 0) + (sem ? 2 : 0);
-  const int warps = 4;
-  const size_t smem = (size_t)cam.H * sizeof(RowRec) + (size_t)warps * 2 * RW * segw * std::max(bpp, 1);
-  auto kern = nvk::k_step_render<CPL, RW>;
-  TRY(set_smem(c, (const void *)kern, smem));
-  int per_sm = 0;
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, warps * 32, smem));
-  per_sm = std::max(1, per_sm);
-  unsigned grid = (unsigned)((long long)per_sm * c->sm_count);
-  Prof pf(c, st, 3);
-  kern<<<grid, warps * 32, smem, st>>>(m);
-  return check_launch(c);
-}
-
-template <int CPL>
-int launch_fill_direct(nv_ctx *c, nvk::FillArgs &a, cudaStream_t st) {
-  const int warps = 4;
-  auto kern = nvk::k_fill_direct<CPL>;
-  const size_t smem = (size_t)a.H * sizeof(RowRec);
-  TRY(set_smem(c, (const void *)kern, smem));
-  int per_sm = 0;
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, warps * 32, smem));
-  per_sm = std::max(1, per_sm);
-  fill_layout<CPL>(a, c->sm_count);
-  long long want = (a.n_units + warps - 1) / warps;
-  unsigned grid = (unsigned)std::max<long long>(1, std::min<long long>(want, (long long)per_sm * c->sm_count));
-  Prof pf(c, st, 2);
-  kern<<<grid, warps * 32, smem, st>>>(a);
-  return check_launch(c);
-}
-
-// Warp-specialised writer: 16 producer warps + 1 store warp.  Preference
-// order: shading table resident, RPW (rows per producer warp per slot) = 2
-// with a ring of >= 2 slots, then RPW = 1 with 2..4 slots, then no table.
+// Warp-specialised writer: NV_WS_NW producer warps + 1 store warp.
+// Preference order: RPW (rows per producer warp per slot) = 1 then 2, the
+// shading table read through L1 (staging it in shared memory measured slower
+// at C1/C2/C3: C3 fill 76.9 vs 75.7 us; NV_WS_TAB=1 builds the staged
+// variant), with as many ring slots as fit (<= 4; A/B at C3: 3 / 4 / 5 / 6
+// slots -> 75.5 / 75.2 / 76.6 / 76.4 us).
 template <int CPL, bool TAB, int RPW>
 int launch_ws_kernel(nv_ctx *c, nvk::FillArgs &a, const nvk::FillWsLayout &L, size_t smem,
                      cudaStream_t st) {
@@ -590,12 +478,8 @@ int launch_ws_kernel(nv_ctx *c, nvk::FillArgs &a, const nvk::FillWsLayout &L, si
                          : (noise ? nvk::k_fill_ws<CPL, TAB, RPW, true, false>
                                   : nvk::k_fill_ws<CPL, TAB, RPW, false, false>);
   TRY(set_smem(c, (const void *)kern, smem));
-  static const int ws_sms = [] {  // study knob: SMs given to the ws writer
-    const char *e = getenv("NAVSIM_WS_SMS");
-    return e ? atoi(e) : 0;
-  }();
-  const int sms = ws_sms > 0 ? std::min(ws_sms, c->sm_count) : c->sm_count;
-  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(a.N * (int64_t)L.bands, sms));
+  const unsigned grid =
+      (unsigned)std::max<int64_t>(1, std::min<int64_t>(a.N * (int64_t)L.bands, c->sm_count));
   Prof pf(c, st, 2);
   kern<<<grid, (L.nw + 1) * 32, smem, st>>>(a, L);
   return check_launch(c);
@@ -605,52 +489,27 @@ template <int CPL>
 int launch_fill_ws(nv_ctx *c, nvk::FillArgs &a, cudaStream_t st) {
   const int segw = 32 * CPL;
   const int S = a.W / segw;
-  static const int nw = [] {  // tuning knob: producer warps (4, 8 or 16)
-    const char *e = getenv("NAVSIM_WS_NW");
-    const int v = e ? atoi(e) : 16;
-    return v == 4 || v == 8 ? v : 16;
-  }();
-  static const int depth_direct = [] {  // tuning knob: depth by STG instead of the slots
-    const char *e = getenv("NAVSIM_WS_DEPTH_DIRECT");
-    return e ? atoi(e) : 0;
-  }();
-  const bool dd = depth_direct && a.depth;
-  const int bpp = (a.rgb ? 3 : 0) + (a.depth && !dd ? 4 : 0) + (a.sem ? 2 : 0);
+  constexpr int nw = NV_WS_NW;
+  const int bpp = (a.rgb ? 3 : 0) + (a.depth ? 4 : 0) + (a.sem ? 2 : 0);
   auto up = [](size_t x) { return (x + 127) & ~(size_t)127; };
   if (nw % S) return fail(NV_ERR_ARG, "frame layout unsupported by ws fill");
   const size_t rows_b = up((size_t)a.H * sizeof(RowRec));
   const size_t inv_b = up((size_t)((a.H + 1) / 2) * a.W * 2);
   const size_t cols_b = up((size_t)NV_WS_CBUF * a.W * sizeof(ColRec));
   const size_t bars_b = 128;
-  static const int force_rpw = [] {
-    const char *e = getenv("NAVSIM_WS_RPW");
-    return e ? atoi(e) : 0;
-  }();
   struct Opt { bool tab; int rpw, nmin, nmax; };
   static const Opt opts[] = {{true, 1, 2, 4}, {true, 2, 2, 4}, {false, 1, 2, 4}, {false, 2, 2, 4}};
   nvk::FillWsLayout L;
   bool tab = false;
   int rpw = 0;
   size_t smem = 0;
-  // The shading table is read from L1/L2 by default: staging it in shared
-  // memory measured slower at C1/C2/C3 (C3 fill 76.9 vs 75.7 us) and only
-  // 0.6 us faster at C4 (knob NAVSIM_WS_TAB=1 stages it).
-  static const bool no_tab = [] {
-    const char *e = getenv("NAVSIM_WS_TAB");
-    return !(e && atoi(e) != 0);
-  }();
   for (const Opt &o : opts) {
-    if (force_rpw && o.rpw != force_rpw) continue;
-    if (no_tab && o.tab) continue;
+    if (NV_WS_RPW && o.rpw != NV_WS_RPW) continue;
+    if (!NV_WS_TAB && o.tab) continue;
     const int R = o.rpw * nw / S;
     if (a.H % R) continue;
     const size_t slot = up((size_t)R * a.W * bpp);
-    static const int slots_max = [] {  // tuning knob: ring slots (2..6; barriers fit 6)
-      const char *e = getenv("NAVSIM_WS_SLOTS");
-      const int v = e ? atoi(e) : 0;
-      return v >= 2 && v <= 6 ? v : 0;
-    }();
-    for (int ns = slots_max ? slots_max : o.nmax; ns >= o.nmin && !rpw; --ns) {
+    for (int ns = NV_WS_SLOTS ? NV_WS_SLOTS : o.nmax; ns >= o.nmin && !rpw; --ns) {
       const size_t tot = rows_b + (o.tab ? inv_b : 0) + cols_b + bars_b + (size_t)ns * slot;
       if ((int)tot <= c->max_smem_optin) {
         tab = o.tab; rpw = o.rpw; smem = tot;
@@ -665,16 +524,11 @@ int launch_fill_ws(nv_ctx *c, nvk::FillArgs &a, cudaStream_t st) {
   L.cols = L.inv + (tab ? (int)inv_b : 0);
   L.bars = L.cols + (int)cols_b;
   L.slots = L.bars + (int)bars_b;
-  L.depth_direct = dd ? 1 : 0;
   L.nw = nw;
   {  // row bands per env: minimise the busiest CTA's time, ceil(N b / grid) items
      // of (1/b frame + a fixed per-item cost).  Per-item cost measured at C3
      // (2 bands: +8 us over 1024 extra items on 148 CTAs) ~ 1.1 us, i.e. the
      // time one SM streams ~50 KB at its ~45 GB/s store rate.
-    static const int force_bands = [] {  // tuning knob
-      const char *e = getenv("NAVSIM_WS_BANDS");
-      return e ? atoi(e) : 0;
-    }();
     const double frame_bytes = (double)a.W * a.H * bpp;
     const double ovh = 49500.0 / std::max(1.0, frame_bytes);
     int best = 1;
@@ -689,13 +543,23 @@ int launch_fill_ws(nv_ctx *c, nvk::FillArgs &a, cudaStream_t st) {
         best = b;
       }
     }
-    L.bands = force_bands > 0 && (a.H / L.slot_rows) % force_bands == 0 ? force_bands : best;
+    constexpr int force_bands = NV_WS_BANDS > 0 ? NV_WS_BANDS : 1;
+    L.bands = NV_WS_BANDS > 0 && (a.H / L.slot_rows) % force_bands == 0 ? force_bands : best;
   }
   a.segs_per_row = S;
   if (tab && rpw == 2) return launch_ws_kernel<CPL, true, 2>(c, a, L, smem, st);
   if (tab) return launch_ws_kernel<CPL, true, 1>(c, a, L, smem, st);
   if (rpw == 2) return launch_ws_kernel<CPL, false, 2>(c, a, L, smem, st);
   return launch_ws_kernel<CPL, false, 1>(c, a, L, smem, st);
+}
+
+// Whether the warp-specialised writer takes this frame layout: W in {64, 128,
+// 256k <= 4096}, whole slots of rows, 16-byte aligned outputs (bulk copies).
+bool ws_layout_ok(const Camera &cam, const void *rgb, const void *depth, const void *sem) {
+  auto al16 = [](const void *p) { return ((uintptr_t)p & 15) == 0; };
+  if (!(al16(rgb) && al16(depth) && al16(sem))) return false;
+  if (cam.W % 256 == 0) return cam.W <= 4096 && cam.H % (16 / std::min(16, cam.W / 256)) == 0;
+  return (cam.W == 128 || cam.W == 64) && cam.H % 16 == 0;
 }
 
 int launch_fill(nv_ctx *c, Camera &cam, int64_t N, uint8_t *rgb, float *depth, uint16_t *sem,
@@ -710,40 +574,24 @@ int launch_fill(nv_ctx *c, Camera &cam, int64_t N, uint8_t *rgb, float *depth, u
   a.invh = cam.invh.as<uint16_t>();
   a.N = (int)N; a.W = cam.W; a.H = cam.H;
   a.rgb = rgb; a.depth = depth; a.sem = sem;
-  a.ctr = cam.ctr.as<unsigned int>();
+  a.segs_per_row = 1;
   const bool noise = c->noise_sigma > 0.0 && depth;
   a.noise_sigma = noise ? (float)c->noise_sigma : 0.0f;
   a.max_range = (float)cam.max_range;
   a.noise_seed = c->noise_seed;
   a.noise_frame = noise ? c->noise_frame++ : 0;
   a.env_offset = c->noise_env_offset;
-  auto al16 = [](const void *p) { return ((uintptr_t)p & 15) == 0; };
-  bool aligned = al16(rgb) && al16(depth) && al16(sem);
-  auto al32 = [](const void *p) { return ((uintptr_t)p & 31) == 0; };
-  const bool ws_ok = cam.W <= 4096 && (cam.W % 256 == 0 ? cam.H % (16 / std::min(16, cam.W / 256)) == 0
-                                                          : cam.H % 16 == 0);
-  // mode 2 = warp-specialised writer; mode 3 (default) = the same whenever the
-  // frame layout allows it (row bands spread small batches over the SMs),
-  // else the per-warp writer.  The warp-specialised writer applies the depth
-  // noise itself; the others get a pass.
-  // (auto = the ws writer whenever the layout allows: with row bands it also
-  // beats the per-warp writer on small batches -- C2 fill 14.7 -> 9.7 us)
-  const bool use_ws = c->fill_mode == 2 || c->fill_mode == 3;
-  if (use_ws && aligned && ws_ok && cam.W % 256 == 0) return launch_fill_ws<8>(c, a, st);
-  if (use_ws && aligned && ws_ok && cam.W == 128) return launch_fill_ws<4>(c, a, st);
-  if (use_ws && aligned && ws_ok && cam.W == 64) return launch_fill_ws<2>(c, a, st);
-  if (c->fill_mode == 0 && aligned && al32(depth) && cam.W % 256 == 0)
-    TRY(launch_fill_direct<8>(c, a, st));
-  else if (c->fill_mode == 0 && aligned && cam.W == 128)
-    TRY(launch_fill_direct<4>(c, a, st));
-  else if (aligned && cam.W % 256 == 0)
-    TRY(launch_fill_tma<8>(c, a, st));
-  else if (aligned && cam.W == 128)
-    TRY(launch_fill_tma<4>(c, a, st));
-  else if (aligned && cam.W == 64)
-    TRY(launch_fill_tma<2>(c, a, st));
-  else {
-    long long total = N * (long long)cam.W * cam.H;
+  // auto: the warp-specialised writer whenever the frame layout allows it
+  // (row bands spread small batches over the SMs), else the per-pixel
+  // kernel; both produce identical frames.  The ws writer applies the depth
+  // noise itself, the per-pixel kernel gets a pass.
+  if (c->fill_mode != NV_FILL_GENERIC && ws_layout_ok(cam, rgb, depth, sem)) {
+    if (cam.W % 256 == 0) return launch_fill_ws<8>(c, a, st);
+    if (cam.W == 128) return launch_fill_ws<4>(c, a, st);
+    return launch_fill_ws<2>(c, a, st);
+  }
+  {
+    const long long total = N * (long long)cam.W * cam.H;
     Prof pf(c, st, 2);
     nvk::k_fill_generic<<<blocks_for(total, 256), 256, 0, st>>>(a);
     TRY(check_launch(c));
@@ -768,20 +616,12 @@ int cam_check(nv_ctx *c, int cam) {
 
 // small batches (rays fit in about one wave of warps): one warp per ray
 bool use_warp_cast(const nv_ctx *c, long long rays) {
-  static const long long warp_rays = [] {
-    const char *e = getenv("NAVSIM_CAST_WARP_RAYS");
-    return e ? atoll(e) : 16384LL;
-  }();
-  return c->cast_mode == 4 || (c->cast_mode == 0 && rays <= warp_rays);
+  return c->cast_mode == NV_CAST_WARP || (c->cast_mode == NV_CAST_AUTO && rays <= NV_CAST_WARP_RAYS);
 }
 
-int cast_queue_counter(Camera &k) {  // self-resetting work counter of k_column_cast_q
-  TRY(k.cast_ctr.alloc(2 * sizeof(unsigned int)));
-  if (!k.cast_ctr_init) {
-    CK(cudaMemset(k.cast_ctr.p, 0, 2 * sizeof(unsigned int)));
-    k.cast_ctr_init = true;
-  }
-  return NV_OK;
+// CTAs of the column cast for `rays` rays (warp or thread per ray)
+unsigned cast_blocks(const nv_ctx *c, long long rays) {
+  return use_warp_cast(c, rays) ? blocks_for(rays * 32, 128) : blocks_for(rays, NV_CAST_BLOCK);
 }
 
 // block order (identity) and durations (zero) for `nblk` cast blocks
@@ -821,111 +661,42 @@ int lpt_fork(nv_ctx *c, cudaStream_t st, unsigned *order, unsigned *cost, unsign
 
 int do_cast(nv_ctx *c, int cam, double *gps, double *compass, cudaStream_t st) {
   Camera &k = c->cams[cam];
-  if (c->cast_mode == 1 && k.W <= 2048) {
-    const int ntiles = (k.W + NV_COLTILE - 1) / NV_COLTILE;
-    const size_t smem = (size_t)k.W * (8 + 8 + 8) + (size_t)NV_BIN_MAXCELLS * (16 + 4) +
-                        (size_t)((k.W + 3) & ~3) * 4 + (size_t)((ntiles + 3) & ~3) * 4 +
-                        (size_t)NV_HIT_CAP * 8 + 32;
-    TRY(set_smem(c, (const void *)nvk::k_cast_binned, smem));
-    Prof pf(c, st, 1);
-    nvk::k_cast_binned<<<(unsigned)c->n_envs, 128, smem, st>>>(
-        c->env_view(), c->scene_view(), cam_view(k), k.focal, rec_out(k, c->n_envs), gps, compass);
-    return check_launch(c);
-  }
   // t_max = max_range: capping the walk is output-identical for rendered
   // frames (tests/test_gpu_parity.py checks it against the
   // reference's uncapped t_max = 1e9 render).
   const long long total = c->n_envs * (long long)k.W;
-  if (c->cast_queue) {  // persistent warps over a work counter
-    TRY(cast_queue_counter(k));
-    int per_sm = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, nvk::k_column_cast_q, 128, 0));
-    const long long want = (c->n_envs * ((k.W + 31) / 32) + 3) / 4;
-    const unsigned grid = (unsigned)std::max<long long>(
-        1, std::min<long long>(want, (long long)std::max(1, per_sm) * c->sm_count));
-    Prof pf(c, st, 1);
-    nvk::k_column_cast_q<<<grid, 128, 0, st>>>(c->env_view(), c->scene_view(), cam_view(k),
-                                                rec_out(k, c->n_envs), k.max_range, gps, compass,
-                                                k.cast_ctr.as<unsigned int>());
-    return check_launch(c);
-  }
-  if (use_warp_cast(c, total)) {
-    const unsigned nblk = blocks_for(total * 32, 128);
-    unsigned *order = nullptr, *cost = nullptr;
-    if (c->cast_lpt && lpt_pays(c, nblk)) {
-      TRY(lpt_buffers(c, k.lpt_order, k.lpt_cost, k.lpt_n, nblk, st));
-      order = k.lpt_order.as<unsigned>();
-      cost = k.lpt_cost.as<unsigned>();
-    }
-    {
-      Prof pf(c, st, 1);
-      if (c->pdl_armed) {  // programmatic dependent of the agent step just launched
-        c->pdl_armed = false;
-        cudaLaunchConfig_t lc = {};
-        lc.gridDim = dim3(nblk);
-        lc.blockDim = dim3(128);
-        lc.stream = st;
-        cudaLaunchAttribute at[1];
-        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-        at[0].val.programmaticStreamSerializationAllowed = 1;
-        lc.attrs = at;
-        lc.numAttrs = 1;
-        CK(cudaLaunchKernelEx(&lc, nvk::k_column_cast_warp, c->env_view(), c->scene_view(),
-                              cam_view(k), rec_out(k, c->n_envs), k.max_range, gps, compass,
-                              c->pdl_ready.as<unsigned>(), c->pdl_arrive.as<unsigned>(),
-                              (const unsigned *)order, cost));
-      } else {
-        nvk::k_column_cast_warp<<<nblk, 128, 0, st>>>(
-            c->env_view(), c->scene_view(), cam_view(k), rec_out(k, c->n_envs), k.max_range, gps,
-            compass, nullptr, nullptr, order, cost);
-      }
-      TRY(check_launch(c));
-    }
-    return order ? lpt_fork(c, st, order, cost, nblk) : NV_OK;
-  }
-  if (c->cast_mode == 5 || (c->cast_mode == 0 && c->cast_pool > 0)) {  // ray pools
-    const int pool = c->cast_pool > 0 ? c->cast_pool : 64;
-    const long long warps = (total + pool - 1) / pool;
-    Prof pf(c, st, 1);
-    nvk::k_column_cast_pool<<<blocks_for(warps * 32, 128), 128, 0, st>>>(
-        c->env_view(), c->scene_view(), cam_view(k), rec_out(k, c->n_envs), k.max_range, gps,
-        compass, pool);
-    return check_launch(c);
-  }
-  static const int cast_block = [] {  // tuning knob: threads per cast CTA (32..128)
-    const char *e = getenv("NAVSIM_CAST_BLOCK");
-    const int v = e ? atoi(e) : 0;
-    return v == 32 || v == 64 || v == 96 || v == 128 ? v : 128;
-  }();
-  const unsigned nblk = blocks_for(total, cast_block);
+  const bool warp = use_warp_cast(c, total);
+  const unsigned nblk = cast_blocks(c, total);
+  const unsigned threads = warp ? 128u : (unsigned)NV_CAST_BLOCK;
   unsigned *order = nullptr, *cost = nullptr;
-  if (c->cast_lpt && lpt_pays(c, nblk)) {
+  if (NV_CAST_LPT && lpt_pays(c, nblk)) {
     TRY(lpt_buffers(c, k.lpt_order, k.lpt_cost, k.lpt_n, nblk, st));
     order = k.lpt_order.as<unsigned>();
     cost = k.lpt_cost.as<unsigned>();
   }
-  Prof pf(c, st, 1);
-  if (c->pdl_armed) {  // programmatic dependent of the agent step just launched
-    c->pdl_armed = false;
+  {
+    Prof pf(c, st, 1);
+    auto kern = warp ? nvk::k_column_cast_warp : nvk::k_column_cast;
+    unsigned *ready = nullptr, *arrive = nullptr;
     cudaLaunchConfig_t lc = {};
     lc.gridDim = dim3(nblk);
-    lc.blockDim = dim3(cast_block);
+    lc.blockDim = dim3(threads);
     lc.stream = st;
     cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    at[0].val.programmaticStreamSerializationAllowed = 1;
-    lc.attrs = at;
-    lc.numAttrs = 1;
-    CK(cudaLaunchKernelEx(&lc, nvk::k_column_cast, c->env_view(), c->scene_view(), cam_view(k),
-                          rec_out(k, c->n_envs), k.max_range, gps, compass,
-                          c->pdl_ready.as<unsigned>(), c->pdl_arrive.as<unsigned>(),
+    if (c->pdl_armed) {  // programmatic dependent of the agent step just launched
+      c->pdl_armed = false;
+      ready = c->pdl_ready.as<unsigned>();
+      arrive = c->pdl_arrive.as<unsigned>();
+      at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      at[0].val.programmaticStreamSerializationAllowed = 1;
+      lc.attrs = at;
+      lc.numAttrs = 1;
+    }
+    CK(cudaLaunchKernelEx(&lc, kern, c->env_view(), c->scene_view(), cam_view(k),
+                          rec_out(k, c->n_envs), k.max_range, gps, compass, ready, arrive,
                           (const unsigned *)order, cost));
-  } else {
-    nvk::k_column_cast<<<nblk, cast_block, 0, st>>>(
-        c->env_view(), c->scene_view(), cam_view(k), rec_out(k, c->n_envs), k.max_range, gps,
-        compass, nullptr, nullptr, order, cost);
+    TRY(check_launch(c));
   }
-  TRY(check_launch(c));
   return order ? lpt_fork(c, st, order, cost, nblk) : NV_OK;
 }
 
@@ -934,15 +705,6 @@ int lpt_join(nv_ctx *c, cudaStream_t st) {
   if (!c->o_fork) return NV_OK;
   c->o_fork = false;
   CK(cudaStreamWaitEvent(st, c->o_ev1, 0));
-  return NV_OK;
-}
-
-int nv_set_cast_mode_(nv_ctx *c, int mode) {
-  if (mode < 0 || mode > 5)
-    return fail(NV_ERR_ARG, "cast mode must be 0 (dda, auto), 1 (binned), 2 (dda fused with the "
-                            "step), 3 (dda, thread per ray), 4 (dda, warp per ray) or 5 (dda, "
-                            "ray pools)");
-  c->cast_mode = mode;
   return NV_OK;
 }
 
@@ -1005,11 +767,6 @@ int nv_create(int device, nv_ctx **out) {
   CK(cudaSetDevice(device));
   nv_ctx *c = new nv_ctx();
   c->device = device;
-  if (const char *q = getenv("NAVSIM_CAST_QUEUE")) c->cast_queue = atoi(q) != 0;  // A/B knob
-  if (const char *q = getenv("NAVSIM_PDL")) c->pdl = atoi(q) != 0;                // A/B knob
-  if (const char *q = getenv("NAVSIM_CAST_LPT")) c->cast_lpt = atoi(q) != 0;      // A/B knob
-  if (const char *q = getenv("NAVSIM_CAST_POOL")) c->cast_pool = atoi(q);         // A/B knob
-  if (const char *q = getenv("NAVSIM_E2E_MAPPED")) c->e2e_mapped = atoi(q) != 0;  // A/B knob
   cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device);
   cudaDeviceGetAttribute(&c->max_smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
   *out = c;
@@ -1204,6 +961,25 @@ int nv_envs_alloc(nv_ctx *c, int64_t n_envs) {
   c->reset.release();
   TRY(c->reset.alloc((size_t)n_envs));
   CK(cudaMemset(c->reset.p, 0, (size_t)n_envs));
+  // The un-reset pose is the reference Simulator's initial AgentState
+  // (origin, heading 0; sim.py:159): cos(heading) = 1 so observations()
+  // before set_agent_state renders like the reference (sim.py:192-200).
+  {
+    const std::vector<double> ones((size_t)n_envs, 1.0);
+    CK(cudaMemcpy(c->ch.p, ones.data(), d, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(c->fc.p, ones.data(), d, cudaMemcpyHostToDevice));
+  }
+  // PointGoal episodes belong to the old env batch: drop them (a stale done
+  // flag would freeze the new envs; a smaller buffer would be read past its
+  // end) -- nv_task_reset starts new ones
+  c->task_on = false;
+  for (DevBuf *b : {&c->t_goal, &c->t_gdsp, &c->t_fid, &c->t_dlast, &c->t_steps, &c->t_done,
+                    &c->t_status})
+    b->release();
+  c->t_fields = nullptr;
+  c->t_nfields = 0;
+  // the agent -> cast ready flags are sized per env
+  c->pdl_init = false;
   c->n_envs = n_envs;
   return NV_OK;
 }
@@ -1225,8 +1001,6 @@ int nv_camera_config(nv_ctx *c, int cam, int width, int height, double focal, do
   k.focal = focal;
   k.max_range = max_range;
   TRY(build_camera_tables(c, k, c->sensor_h));
-  TRY(k.ctr.alloc(16));
-  CK(cudaMemset(k.ctr.p, 0, 16));
   k.on = true;
   return NV_OK;
 }
@@ -1293,37 +1067,10 @@ int nv_step_render(nv_ctx *c, const int8_t *actions, int cam, uint8_t *rgb, floa
   if (!actions) return fail(NV_ERR_ARG, "actions is NULL");
   cudaStream_t st = (cudaStream_t)stream;
   Camera &k = c->cams[cam];
-  auto al16 = [](const void *p) { return ((uintptr_t)p & 15) == 0; };
-  const bool tma_ok = al16(rgb) && al16(depth) && al16(sem) && (rgb || depth || sem);
-  if (c->fused && tma_ok && c->n_envs < (1 << 24) && !(c->noise_sigma > 0.0)) {
-    if (k.W % 256 == 0)
-      return launch_mega<8>(c, k, actions, rgb, depth, sem, gps, compass, collided, displacement,
-                            status, st);
-    if (k.W == 128)
-      return launch_mega<4>(c, k, actions, rgb, depth, sem, gps, compass, collided, displacement,
-                            status, st);
-    if (k.W == 64)
-      return launch_mega<2>(c, k, actions, rgb, depth, sem, gps, compass, collided, displacement,
-                            status, st);
-  }
-  if (c->cast_mode == 2) {  // agent step fused with the casts, one CTA per env
-    nvk::AgentCfg cfg{c->radius, c->step, c->turn_rad};
-    const int threads = std::min(256, (k.W + 31) / 32 * 32);
-    {
-      Prof pf(c, st, 1);
-      nvk::k_step_cast<<<(unsigned)c->n_envs, threads, 0, st>>>(
-          c->env_view(), c->scene_view(), cfg, actions, collided, displacement, status,
-          cam_view(k), rec_out(k, c->n_envs), k.max_range, gps, compass);
-    }
-    TRY(check_launch(c));
-    return launch_fill(c, k, c->n_envs, rgb, depth, sem, st);
-  }
-  // agent step -> cast overlap (programmatic dependent launch) for the
-  // thread-per-ray DDA cast, when profiling events are off (an event between
-  // the two launches would break the programmatic edge)
-  const bool pdl = c->pdl && !c->prof_on && !c->cast_queue &&
-                   (c->cast_mode == 3 || c->cast_mode == 4 ||
-                    (c->cast_mode == 0 && c->cast_pool <= 0));
+  // agent step -> cast overlap (programmatic dependent launch), unless
+  // profiling events are on (an event between the two launches would break
+  // the programmatic edge)
+  const bool pdl = c->pdl && !c->prof_on;
   TRY(do_step(c, actions, collided, displacement, status, st, pdl));
   TRY(do_cast(c, cam, gps, compass, st));
   c->pdl_armed = false;
@@ -1335,15 +1082,19 @@ int nv_step_render(nv_ctx *c, const int8_t *actions, int cam, uint8_t *rgb, floa
 
 int nv_set_cast_mode(nv_ctx *c, int mode) {
   if (!c) return fail(NV_ERR_ARG, "ctx is NULL");
+  if (mode != NV_CAST_AUTO && mode != NV_CAST_THREAD && mode != NV_CAST_WARP)
+    return fail(NV_ERR_ARG, "cast mode must be NV_CAST_AUTO (0), NV_CAST_THREAD (1) or "
+                            "NV_CAST_WARP (2)");
   c->gen++;
-  return nv_set_cast_mode_(c, mode);
+  c->cast_mode = mode;
+  return NV_OK;
 }
 
 int nv_set_fill_mode(nv_ctx *c, int mode) {
   if (!c) return fail(NV_ERR_ARG, "ctx is NULL");
+  if (mode != NV_FILL_AUTO && mode != NV_FILL_GENERIC)
+    return fail(NV_ERR_ARG, "fill mode must be NV_FILL_AUTO (0) or NV_FILL_GENERIC (1)");
   c->gen++;
-  if (mode < 0 || mode > 3)
-    return fail(NV_ERR_ARG, "fill mode must be 0 (direct), 1 (tma), 2 (ws) or 3 (auto)");
   c->fill_mode = mode;
   return NV_OK;
 }
@@ -1355,41 +1106,59 @@ int nv_set_overlap(nv_ctx *c, int on) {
   return NV_OK;
 }
 
-int nv_set_fused(nv_ctx *c, int on) {
-  if (!c) return fail(NV_ERR_ARG, "ctx is NULL");
-  c->gen++;
-  c->fused = on != 0;
-  return NV_OK;
-}
-
 int nv_step_render_host(nv_ctx *c, const int8_t *actions_host, int cam, uint32_t channels,
                         uint8_t *rgb_host, float *depth_host, uint16_t *sem_host,
                         double *gps_host, double *compass_host, uint8_t *collided_host,
                         double *displacement_host, void *stream) {
   if (!c) return fail(NV_ERR_ARG, "ctx is NULL");
   TRY(ensure_envs(c));
-  TRY(cam_check(c, cam));
   if (!actions_host) return fail(NV_ERR_ARG, "actions is NULL");
+  const bool frames_out = rgb_host || depth_host || sem_host;
+  // the cameras this step renders, in order; the first one carries the step
+  // (nv_step_render) and gps/compass, the others are nv_render calls
+  int cams[8], ncam = 0;
+  uint32_t chans[8];
+  if (cam == NV_ALL_CAMERAS) {
+    if (frames_out) return fail(NV_ERR_ARG, "host frame pointers need a single camera");
+    for (int k = 0; k < 8; ++k) {
+      const uint32_t b = (channels >> (3 * k)) & 7u;
+      if (!b) continue;
+      if (!c->cams[k].on) return fail(NV_ERR_STATE, "camera %d not configured (nv_camera_config)", k);
+      cams[ncam] = k;
+      chans[ncam++] = b;
+    }
+    if (!ncam) return fail(NV_ERR_ARG, "no camera channels requested");
+  } else {
+    cams[0] = cam;
+    chans[0] = (channels & 7u) | (rgb_host ? NV_CH_RGB : 0u) | (depth_host ? NV_CH_DEPTH : 0u) |
+               (sem_host ? NV_CH_SEM : 0u);
+    ncam = 1;
+  }
+  for (int q = 0; q < ncam; ++q) TRY(cam_check(c, cams[q]));
   cudaStream_t st = (cudaStream_t)stream;
   const size_t N = (size_t)c->n_envs;
-  const Camera &k = c->cams[cam];
-  const size_t px = N * k.W * k.H;
-  const bool want_rgb = (channels & NV_CH_RGB) || rgb_host;
-  const bool want_d = (channels & NV_CH_DEPTH) || depth_host;
-  const bool want_s = (channels & NV_CH_SEM) || sem_host;
+  for (int q = 0; q < ncam; ++q) {
+    Camera &k = c->cams[cams[q]];
+    const size_t px = N * k.W * k.H;
+    if (chans[q] & NV_CH_RGB) TRY(k.e_rgb.alloc(px * 3));
+    if (chans[q] & NV_CH_DEPTH) TRY(k.e_depth.alloc(px * 4));
+    if (chans[q] & NV_CH_SEM) TRY(k.e_sem.alloc(px * 2));
+  }
+  auto frame_ptrs = [&](int q, uint8_t *&r, float *&d, uint16_t *&s) {
+    Camera &k = c->cams[cams[q]];
+    r = (chans[q] & NV_CH_RGB) ? k.e_rgb.as<uint8_t>() : nullptr;
+    d = (chans[q] & NV_CH_DEPTH) ? k.e_depth.as<float>() : nullptr;
+    s = (chans[q] & NV_CH_SEM) ? k.e_sem.as<uint16_t>() : nullptr;
+  };
   TRY(c->e_act.alloc(N));
-  if (want_rgb) TRY(c->e_rgb.alloc(px * 3));
-  if (want_d) TRY(c->e_depth.alloc(px * 4));
-  if (want_s) TRY(c->e_sem.alloc(px * 2));
   const size_t pack = 33 * N;
   TRY(c->e_pack.alloc(pack));
   uint8_t *pk = c->e_pack.as<uint8_t>();
   double *d_gps = reinterpret_cast<double *>(pk), *d_comp = d_gps + 2 * N, *d_disp = d_comp + N;
   uint8_t *d_coll = pk + 32 * N;
-  const bool frames_out = rgb_host || depth_host || sem_host;
   // graph path: no host frames, no profiling, no noise (its frame counter
   // advances per call) -- the common per-step case
-  const bool graph_ok = !frames_out && !c->prof_on && !(c->noise_sigma > 0.0) && !c->fused;
+  const bool graph_ok = !frames_out && !c->prof_on && !(c->noise_sigma > 0.0);
   if (graph_ok) {
     if (!c->e_stream) {
       // a blocking stream: ordered after the legacy default stream's work
@@ -1401,22 +1170,17 @@ int nv_step_render_host(nv_ctx *c, const int8_t *actions_host, int cam, uint32_t
     // from and write the packed step results to host memory directly (no
     // copy nodes in the graph)
     if (c->e_hin_bytes < N) {
+      TRY(e2e_fence(c));
       if (c->e_hin) cudaFreeHost(c->e_hin);
       CK(cudaHostAlloc(&c->e_hin, N, cudaHostAllocMapped));
       c->e_hin_bytes = N;
-      if (c->e_graph) cudaGraphExecDestroy(c->e_graph);
-      c->e_graph = nullptr;
     }
     if (c->e_hout_bytes < pack) {
+      TRY(e2e_fence(c));
       if (c->e_hout) cudaFreeHost(c->e_hout);
       CK(cudaHostAlloc(&c->e_hout, pack, cudaHostAllocMapped));
       c->e_hout_bytes = pack;
-      if (c->e_graph) cudaGraphExecDestroy(c->e_graph);
-      c->e_graph = nullptr;
     }
-    const int key[3] = {cam, (int)(channels | (want_rgb ? 8u : 0u) | (want_d ? 16u : 0u) |
-                                   (want_s ? 32u : 0u) | (c->e2e_mapped ? 64u : 0u)),
-                        c->fill_mode * 16 + c->cast_mode * 2 + (c->fused ? 1 : 0)};
     // step results straight into the caller's buffers when all four are
     // pinned (mapped) host memory: no staging copy after the step
     void *const outs[4] = {gps_host, compass_host, displacement_host, collided_host};
@@ -1440,21 +1204,43 @@ int nv_step_render_host(nv_ctx *c, const int8_t *actions_host, int cam, uint32_t
       }
     }
     if (!c->e_cast_ev) CK(cudaEventCreateWithFlags(&c->e_cast_ev, cudaEventDisableTiming));
-    TRY(c->cams[cam].rec_e2e.alloc(c->cams[cam].rec.bytes));
-    if (!c->cams[cam].ctr_e2e.p) {
-      TRY(c->cams[cam].ctr_e2e.alloc(16));
-      CK(cudaMemset(c->cams[cam].ctr_e2e.p, 0, 16));
+    // everything the graph's kernels touch exists before the key is taken
+    // (a reallocated buffer changes the key: the graph is never replayed
+    // into freed memory)
+    for (int q = 0; q < ncam; ++q) {
+      Camera &k = c->cams[cams[q]];
+      TRY(k.rec_e2e.alloc(k.rec.bytes));
+      const unsigned nblk = cast_blocks(c, c->n_envs * (long long)k.W);
+      if (NV_CAST_LPT && lpt_pays(c, nblk) && k.lpt_n_e2e != (int64_t)nblk) {
+        TRY(e2e_fence(c));
+        TRY(lpt_buffers(c, k.lpt_order_e2e, k.lpt_cost_e2e, k.lpt_n_e2e, nblk, nullptr));
+        CK(cudaDeviceSynchronize());
+      }
     }
-    const bool same = c->e_graph && c->e_key_n == c->n_envs && c->e_key_gen == c->gen &&
-                      key[0] == c->e_key[0] &&
-                      key[1] == c->e_key[1] && key[2] == c->e_key[2] &&
-                      c->e_key_direct == direct &&
-                      (!direct || std::memcmp(c->e_key_out, c->e_out_dev, sizeof c->e_key_out) == 0);
+    if (c->pdl) TRY(pdl_buffers(c));
+    std::vector<uint64_t> key = {(uint64_t)c->n_envs, (uint64_t)c->gen, (uint64_t)ncam,
+                                 (uint64_t)c->e2e_mapped, (uint64_t)direct,
+                                 (uint64_t)(uintptr_t)c->e_hin, (uint64_t)(uintptr_t)c->e_hout,
+                                 (uint64_t)(uintptr_t)c->e_act.p, (uint64_t)(uintptr_t)c->e_pack.p,
+                                 (uint64_t)(uintptr_t)c->pdl_ready.p};
+    if (direct)
+      for (int q = 0; q < 4; ++q) key.push_back((uint64_t)(uintptr_t)c->e_out_dev[q]);
+    for (int q = 0; q < ncam; ++q) {
+      const Camera &k = c->cams[cams[q]];
+      uint8_t *r; float *d; uint16_t *sm;
+      frame_ptrs(q, r, d, sm);
+      for (uint64_t v : {(uint64_t)cams[q], (uint64_t)chans[q], (uint64_t)(uintptr_t)k.rec_e2e.p,
+                         (uint64_t)(uintptr_t)k.lpt_order_e2e.p, (uint64_t)(uintptr_t)k.lpt_cost_e2e.p,
+                         (uint64_t)(uintptr_t)r, (uint64_t)(uintptr_t)d, (uint64_t)(uintptr_t)sm})
+        key.push_back(v);
+    }
+    const bool same = c->e_graph && key == c->e_key;
     cudaStream_t es = c->e_stream;
     if (!same) {
       TRY(e2e_fence(c));  // the old graph's writer may still be running
       if (c->e_graph) cudaGraphExecDestroy(c->e_graph);
       c->e_graph = nullptr;
+      c->e_key.clear();
       const int8_t *acts = c->e_act.as<int8_t>();
       double *o_gps = d_gps, *o_comp = d_comp, *o_disp = d_disp;
       uint8_t *o_coll = d_coll;
@@ -1474,52 +1260,34 @@ int nv_step_render_host(nv_ctx *c, const int8_t *actions_host, int cam, uint32_t
           o_coll = static_cast<uint8_t *>(c->e_out_dev[3]);
         }
       }
-      // everything nv_step_render allocates or zeroes lazily, before the
-      // capture (no allocation may happen while the stream is capturing)
-      if (c->pdl) TRY(pdl_buffers(c));
-      if (c->cast_queue) TRY(cast_queue_counter(c->cams[cam]));
-      if (c->cast_lpt) {  // the graph's own block order
-        Camera &kk = c->cams[cam];
-        static const int cb = [] {
-          const char *e = getenv("NAVSIM_CAST_BLOCK");
-          const int v = e ? atoi(e) : 0;
-          return v == 32 || v == 64 || v == 96 || v == 128 ? v : 128;
-        }();
-        const long long rays = c->n_envs * (long long)kk.W;
-        TRY(lpt_buffers(c, kk.lpt_order_e2e, kk.lpt_cost_e2e, kk.lpt_n_e2e,
-                        use_warp_cast(c, rays) ? blocks_for(rays * 32, 128) : blocks_for(rays, cb),
-                        nullptr));
-        CK(cudaDeviceSynchronize());
-      }
+      // the graph's casts and writers use the host step's own record buffers
+      // and block orders; an event after the first camera's casts tells the
+      // host the step results are in
+      auto swap_e2e = [&]() {
+        for (int q = 0; q < ncam; ++q) {
+          Camera &k = c->cams[cams[q]];
+          std::swap(k.rec.p, k.rec_e2e.p);
+          std::swap(k.rec.bytes, k.rec_e2e.bytes);
+          std::swap(k.lpt_order.p, k.lpt_order_e2e.p);
+          std::swap(k.lpt_order.bytes, k.lpt_order_e2e.bytes);
+          std::swap(k.lpt_cost.p, k.lpt_cost_e2e.p);
+          std::swap(k.lpt_cost.bytes, k.lpt_cost_e2e.bytes);
+          std::swap(k.lpt_n, k.lpt_n_e2e);
+        }
+      };
       CK(cudaStreamBeginCapture(es, cudaStreamCaptureModeThreadLocal));
       if (!c->e2e_mapped) cudaMemcpyAsync(c->e_act.p, c->e_hin, N, cudaMemcpyHostToDevice, es);
-      // the graph's casts and writer use the host step's own record buffer,
-      // and an event after the casts tells the host the step results are in
-      Camera &kc = c->cams[cam];
-      std::swap(kc.rec.p, kc.rec_e2e.p);
-      std::swap(kc.rec.bytes, kc.rec_e2e.bytes);
-      std::swap(kc.ctr.p, kc.ctr_e2e.p);
-      std::swap(kc.ctr.bytes, kc.ctr_e2e.bytes);
-      std::swap(kc.lpt_order.p, kc.lpt_order_e2e.p);
-      std::swap(kc.lpt_order.bytes, kc.lpt_order_e2e.bytes);
-      std::swap(kc.lpt_cost.p, kc.lpt_cost_e2e.p);
-      std::swap(kc.lpt_cost.bytes, kc.lpt_cost_e2e.bytes);
-      std::swap(kc.lpt_n, kc.lpt_n_e2e);
+      swap_e2e();
       c->mid_ev = c->e2e_mapped ? c->e_cast_ev : nullptr;
-      int rc = nv_step_render(c, acts, cam, want_rgb ? c->e_rgb.as<uint8_t>() : nullptr,
-                              want_d ? c->e_depth.as<float>() : nullptr,
-                              want_s ? c->e_sem.as<uint16_t>() : nullptr, o_gps, o_comp, o_coll,
-                              o_disp, nullptr, es);
+      uint8_t *r; float *d; uint16_t *sm;
+      frame_ptrs(0, r, d, sm);
+      int rc = nv_step_render(c, acts, cams[0], r, d, sm, o_gps, o_comp, o_coll, o_disp, nullptr, es);
       c->mid_ev = nullptr;
-      std::swap(kc.rec.p, kc.rec_e2e.p);
-      std::swap(kc.rec.bytes, kc.rec_e2e.bytes);
-      std::swap(kc.ctr.p, kc.ctr_e2e.p);
-      std::swap(kc.ctr.bytes, kc.ctr_e2e.bytes);
-      std::swap(kc.lpt_order.p, kc.lpt_order_e2e.p);
-      std::swap(kc.lpt_order.bytes, kc.lpt_order_e2e.bytes);
-      std::swap(kc.lpt_cost.p, kc.lpt_cost_e2e.p);
-      std::swap(kc.lpt_cost.bytes, kc.lpt_cost_e2e.bytes);
-      std::swap(kc.lpt_n, kc.lpt_n_e2e);
+      for (int q = 1; q < ncam && rc == NV_OK; ++q) {
+        frame_ptrs(q, r, d, sm);
+        rc = nv_render(c, cams[q], r, d, sm, nullptr, nullptr, es);
+      }
+      swap_e2e();
       if (!c->e2e_mapped) cudaMemcpyAsync(c->e_hout, pk, pack, cudaMemcpyDeviceToHost, es);
       cudaGraph_t g = nullptr;
       cudaError_t ce = cudaStreamEndCapture(es, &g);
@@ -1531,11 +1299,7 @@ int nv_step_render_host(nv_ctx *c, const int8_t *actions_host, int cam, uint32_t
       ce = cudaGraphInstantiate(&c->e_graph, g, 0);
       cudaGraphDestroy(g);
       if (ce != cudaSuccess) return fail(NV_ERR_CUDA, "graph instantiate failed: %s", cudaGetErrorString(ce));
-      std::memcpy(c->e_key, key, sizeof key);
-      c->e_key_n = c->n_envs;
-      c->e_key_gen = c->gen;
-      c->e_key_direct = direct;
-      std::memcpy(c->e_key_out, c->e_out_dev, sizeof c->e_key_out);
+      c->e_key = key;
     }
     std::memcpy(c->e_hin, actions_host, N);
     if (st) {  // after the caller's prior work on its own stream
@@ -1543,7 +1307,7 @@ int nv_step_render_host(nv_ctx *c, const int8_t *actions_host, int cam, uint32_t
       CK(cudaStreamWaitEvent(es, c->e_ev, 0));
     }
     CK(cudaGraphLaunch(c->e_graph, es));
-    c->launches += 3;
+    c->launches += 3 * ncam;
     if (c->e2e_mapped) {
       // the step results are in host memory once the casts are done; the
       // frame writer finishes behind the caller (ordered before the next
@@ -1563,13 +1327,23 @@ int nv_step_render_host(nv_ctx *c, const int8_t *actions_host, int cam, uint32_t
   }
   TRY(e2e_fence(c));
   CK(cudaMemcpyAsync(c->e_act.p, actions_host, N, cudaMemcpyHostToDevice, st));
-  TRY(nv_step_render(c, c->e_act.as<int8_t>(), cam, want_rgb ? c->e_rgb.as<uint8_t>() : nullptr,
-                     want_d ? c->e_depth.as<float>() : nullptr,
-                     want_s ? c->e_sem.as<uint16_t>() : nullptr, d_gps, d_comp, d_coll, d_disp,
-                     nullptr, stream));
-  if (rgb_host) CK(cudaMemcpyAsync(rgb_host, c->e_rgb.p, px * 3, cudaMemcpyDeviceToHost, st));
-  if (depth_host) CK(cudaMemcpyAsync(depth_host, c->e_depth.p, px * 4, cudaMemcpyDeviceToHost, st));
-  if (sem_host) CK(cudaMemcpyAsync(sem_host, c->e_sem.p, px * 2, cudaMemcpyDeviceToHost, st));
+  {
+    uint8_t *r; float *d; uint16_t *sm;
+    frame_ptrs(0, r, d, sm);
+    TRY(nv_step_render(c, c->e_act.as<int8_t>(), cams[0], r, d, sm, d_gps, d_comp, d_coll, d_disp,
+                       nullptr, stream));
+    for (int q = 1; q < ncam; ++q) {
+      frame_ptrs(q, r, d, sm);
+      TRY(nv_render(c, cams[q], r, d, sm, nullptr, nullptr, stream));
+    }
+  }
+  {
+    const Camera &k = c->cams[cams[0]];
+    const size_t px = N * k.W * k.H;
+    if (rgb_host) CK(cudaMemcpyAsync(rgb_host, k.e_rgb.p, px * 3, cudaMemcpyDeviceToHost, st));
+    if (depth_host) CK(cudaMemcpyAsync(depth_host, k.e_depth.p, px * 4, cudaMemcpyDeviceToHost, st));
+    if (sem_host) CK(cudaMemcpyAsync(sem_host, k.e_sem.p, px * 2, cudaMemcpyDeviceToHost, st));
+  }
   if (gps_host || compass_host || collided_host || displacement_host) {
     std::vector<uint8_t> h(pack);
     CK(cudaMemcpyAsync(h.data(), pk, pack, cudaMemcpyDeviceToHost, st));
@@ -1583,12 +1357,14 @@ int nv_step_render_host(nv_ctx *c, const int8_t *actions_host, int cam, uint32_t
   return NV_OK;
 }
 
-int nv_host_frames(nv_ctx *c, uint8_t **rgb, float **depth, uint16_t **sem) {
+int nv_host_frames(nv_ctx *c, int cam, uint8_t **rgb, float **depth, uint16_t **sem) {
   if (!c) return fail(NV_ERR_ARG, "ctx is NULL");
+  if (cam < 0 || cam >= 8) return fail(NV_ERR_ARG, "camera index %d out of range [0, 8)", cam);
   TRY(e2e_fence(c));  // the frames are complete when this returns
-  if (rgb) *rgb = c->e_rgb.as<uint8_t>();
-  if (depth) *depth = c->e_depth.as<float>();
-  if (sem) *sem = c->e_sem.as<uint16_t>();
+  const Camera &k = c->cams[cam];
+  if (rgb) *rgb = k.e_rgb.as<uint8_t>();
+  if (depth) *depth = k.e_depth.as<float>();
+  if (sem) *sem = k.e_sem.as<uint16_t>();
   return NV_OK;
 }
 

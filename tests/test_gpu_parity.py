@@ -151,9 +151,10 @@ def _oracle_scene(oracle, sc):
     ("C3", 256, 256, 8, 6),        # TMA path W=256, ~100k segments
     ("C1", 40, 33, 8, 20),         # generic path, odd H
 ])
-# cast: warp per ray (small batch), thread per ray, thread per ray overlapped
-# with the agent step (programmatic dependent launch, per-env ready flags)
-@pytest.mark.parametrize("cast_mode", [0, 3, 5, 6])  # 6: ray-pool cast (mode 5)
+# cast: auto (warp per ray at these small batches), thread per ray, thread per
+# ray overlapped with the agent step (programmatic dependent launch, per-env
+# ready flags), warp per ray overlapped
+@pytest.mark.parametrize("cast_mode", ["auto", "thread", "thread-overlap", "warp-overlap"])
 def test_batch_step_render_vs_oracle(nb, oracle_mod, cfg, W, H, n_envs, steps, cast_mode):
     """Batched step+render (device cos/sin, device DDA, TMA fill) vs the oracle
     run on the same actions: poses 1e-6, frames at the stated tolerances."""
@@ -164,9 +165,11 @@ def test_batch_step_render_vs_oracle(nb, oracle_mod, cfg, W, H, n_envs, steps, c
              nb.SensorConfig("semantic", W, H), nb.SensorConfig("gps_compass"))
     sim = nb.BatchSimulator(sc.segments, sc.semantic_ids, sc.albedo, n_envs, sensor_configs=suite,
                             floor_color=sc.floor_color, ceiling_color=sc.ceiling_color)
-    nat.check(sim.ctx.lib.nv_set_cast_mode(sim.ctx.handle,
-                                           {0: 0, 3: 3, 5: 3, 6: 5}[cast_mode]))
-    nat.check(sim.ctx.lib.nv_set_overlap(sim.ctx.handle, int(cast_mode == 5)))
+    nat.check(sim.ctx.lib.nv_set_cast_mode(
+        sim.ctx.handle, {"auto": nat.NV_CAST_AUTO, "thread": nat.NV_CAST_THREAD,
+                         "thread-overlap": nat.NV_CAST_THREAD,
+                         "warp-overlap": nat.NV_CAST_WARP}[cast_mode]))
+    nat.check(sim.ctx.lib.nv_set_overlap(sim.ctx.handle, int(cast_mode.endswith("overlap"))))
     poses = synth.sample_poses(sc, n_envs, seed=17)
     sim.reset(poses[:, :2], poses[:, 2])
     acts = synth.random_actions(n_envs, steps, seed=5)
@@ -196,9 +199,9 @@ def test_batch_step_render_vs_oracle(nb, oracle_mod, cfg, W, H, n_envs, steps, c
 
 @pytest.mark.parametrize("W,H", [(256, 64), (128, 40), (512, 32)])
 def test_fill_paths_agree(nb, W, H):
-    """Identical frames from every frame writer: direct 256-bit stores (default),
-    smem stages + TMA bulk stores, the per-pixel kernel (forced by misaligned
-    outputs) and the fused megakernel."""
+    """Identical frames from every frame writer: the warp-specialised TMA
+    writer (auto), the per-pixel kernel (forced, and chosen for misaligned
+    outputs)."""
     from paper_1904_01201_b200 import _native as nat
     from paper_1904_01201_b200 import synth
     sc = synth.config_scene("C2")
@@ -210,7 +213,7 @@ def test_fill_paths_agree(nb, W, H):
     sim.reset(poses[:, :2], poses[:, 2])
     c, st = sim.ctx, nat.stream_handle("cuda:0")
     outs = []
-    for mode in (0, 1, 2, 3):
+    for mode in (nat.NV_FILL_AUTO, nat.NV_FILL_GENERIC):
         nat.check(c.lib.nv_set_fill_mode(c.handle, mode))
         sim.render()
         torch.cuda.synchronize()
@@ -219,6 +222,7 @@ def test_fill_paths_agree(nb, W, H):
     raw_d = torch.empty(n * H * W + 1, dtype=torch.float32, device="cuda:0")
     raw_s = torch.empty(n * H * W + 1, dtype=torch.int16, device="cuda:0")
     rgb, dep, sem = raw_rgb[1:], raw_d[1:], raw_s[1:]
+    nat.check(c.lib.nv_set_fill_mode(c.handle, nat.NV_FILL_AUTO))
     nat.check(c.lib.nv_render(c.handle, 0, nat.ptr(rgb), nat.ptr(dep), nat.ptr(sem), None, None, st))
     torch.cuda.synchronize()
     outs.append({"rgb": rgb.view(n, H, W, 3), "depth": dep.view(n, H, W),
@@ -227,20 +231,6 @@ def test_fill_paths_agree(nb, W, H):
         assert torch.equal(o["rgb"], outs[0]["rgb"])
         assert torch.equal(o["depth"], outs[0]["depth"])
         assert torch.equal(o["semantic"].view(torch.int16), outs[0]["semantic"].view(torch.int16))
-    # fused megakernel vs three launches on the same actions from the same state
-    acts = torch.as_tensor(synth.random_actions(n, 3, seed=4), device="cuda:0")
-    res = []
-    for fused in (0, 1):
-        s2 = nb.BatchSimulator(sc.segments, sc.semantic_ids, sc.albedo, n, sensor_configs=suite)
-        s2.reset(poses[:, :2], poses[:, 2])
-        nat.check(s2.ctx.lib.nv_set_fused(s2.ctx.handle, fused))
-        for s in range(3):
-            s2.step(acts[s])
-        torch.cuda.synchronize()
-        res.append(({k: v.clone() for k, v in s2.observations().items()}, s2.state()[0].clone()))
-    for k in ("rgb", "depth"):
-        assert torch.equal(res[0][0][k], res[1][0][k])
-    assert torch.equal(res[0][1], res[1][1])
 
 
 def test_full_size_properties(nb):
@@ -380,9 +370,9 @@ def test_blind_and_gps_only(nb):
 @pytest.mark.parametrize("cfg,W,H,n", [("C1", 256, 64, 32), ("C2", 128, 64, 32), ("C3", 256, 32, 64),
                                        ("C1", 40, 33, 16)])
 def test_cast_modes_agree(nb, cfg, W, H, n):
-    """Binned column cast and the per-column DDA (thread and warp per ray) give
-    identical frames (the reference's raycast_grid == raycast_all contract), including
-    the 1000-piece room whose shared endpoints exercise the (t, idx) tie rule."""
+    """The per-column DDA by one thread and by one warp per ray give identical
+    frames, including the 1000-piece room whose shared endpoints exercise the
+    (t, idx) tie rule."""
     from paper_1904_01201_b200 import _native as nat
     from paper_1904_01201_b200 import synth
     sc = synth.config_scene(cfg)
@@ -397,7 +387,7 @@ def test_cast_modes_agree(nb, cfg, W, H, n):
     for s in range(acts.shape[0]):
         sim.step(acts[s], render=False)
         outs = []
-        for mode in (0, 1, 3, 4, 5):
+        for mode in (nat.NV_CAST_AUTO, nat.NV_CAST_THREAD, nat.NV_CAST_WARP):
             nat.check(c.lib.nv_set_cast_mode(c.handle, mode))
             sim.render()
             torch.cuda.synchronize()
@@ -410,20 +400,23 @@ def test_cast_modes_agree(nb, cfg, W, H, n):
 
 
 @pytest.mark.parametrize("cfg,W,H,n", [("C1", 256, 64, 24), ("C2", 128, 64, 32), ("C1", 40, 33, 16)])
-def test_step_cast_fused_agrees(nb, cfg, W, H, n):
-    """Cast mode 2 (agent step fused with the column casts, one CTA per env)
-    gives the same poses, step results and frames as the separate step and
-    cast launches over a 10-step random-action episode."""
+@pytest.mark.parametrize("cast", ["thread", "warp"])
+def test_overlap_agrees(nb, cfg, W, H, n, cast):
+    """The agent step -> cast overlap (programmatic dependent launch with
+    per-env ready flags) gives the same poses, step results and frames as the
+    serialised launches over a 10-step random-action episode."""
     from paper_1904_01201_b200 import _native as nat
     from paper_1904_01201_b200 import synth
     sc = synth.config_scene(cfg)
     suite = (nb.SensorConfig("rgb", W, H), nb.SensorConfig("depth", W, H),
              nb.SensorConfig("semantic", W, H), nb.SensorConfig("gps_compass"))
     sims = []
-    for mode in (0, 2):
+    for overlap in (0, 1):
         sim = nb.BatchSimulator(sc.segments, sc.semantic_ids, sc.albedo, n, sensor_configs=suite,
                                 floor_color=sc.floor_color, ceiling_color=sc.ceiling_color)
-        nat.check(sim.ctx.lib.nv_set_cast_mode(sim.ctx.handle, mode))
+        nat.check(sim.ctx.lib.nv_set_cast_mode(
+            sim.ctx.handle, nat.NV_CAST_THREAD if cast == "thread" else nat.NV_CAST_WARP))
+        nat.check(sim.ctx.lib.nv_set_overlap(sim.ctx.handle, overlap))
         poses = synth.sample_poses(sc, n, seed=5)
         sim.reset(poses[:, :2], poses[:, 2])
         sims.append(sim)
@@ -435,11 +428,13 @@ def test_step_cast_fused_agrees(nb, cfg, W, H, n):
             torch.cuda.synchronize()
             o = {k: v.clone() for k, v in sim.observations().items()}
             o["state"] = [t.clone() for t in sim.state()]
+            o["step"] = (sim.collided.clone(), sim.displacement.clone(), sim.status.clone())
             outs.append(o)
         for k in ("rgb", "depth", "gps", "compass"):
             assert torch.equal(outs[0][k], outs[1][k]), (s, k)
         assert torch.equal(outs[0]["semantic"].view(torch.int16), outs[1]["semantic"].view(torch.int16))
-        for a, b in zip(outs[0]["state"], outs[1]["state"]):
+        for a, b in zip(outs[0]["state"] + list(outs[0]["step"]),
+                        outs[1]["state"] + list(outs[1]["step"])):
             assert torch.equal(a, b)
 
 
@@ -465,7 +460,7 @@ def test_host_buffer_path_matches_device_path(nb):
     for t in range(acts.shape[0]):
         if t == 5:
             for s in sims:
-                nat.check(s.ctx.lib.nv_set_fill_mode(s.ctx.handle, 1))
+                nat.check(s.ctx.lib.nv_set_fill_mode(s.ctx.handle, nat.NV_FILL_GENERIC))
         a_host = np.ascontiguousarray(acts[t])
         sims[0].step_host(a_host, out=out)
         sims[1].step(torch.as_tensor(a_host, device="cuda:0"))
@@ -500,7 +495,7 @@ def test_host_buffer_path_matches_device_path(nb):
     assert np.array_equal(out["gps"], sims[1].gps.cpu().numpy())
 
 
-@pytest.mark.parametrize("mode", ["plain", "overlap", "thread", "fused"])
+@pytest.mark.parametrize("mode", ["plain", "no-overlap", "thread", "warp"])
 def test_host_buffer_path_first_call_all_modes(nb, mode):
     """The host-buffer step as the very first call on a fresh simulator (its
     graph is captured before any device step ran: every lazily allocated
@@ -518,12 +513,12 @@ def test_host_buffer_path_first_call_all_modes(nb, mode):
     for s in sims:
         s.reset(poses[:, :2], poses[:, 2])
         c = s.ctx
-        if mode == "overlap":
-            nat.check(c.lib.nv_set_overlap(c.handle, 1))
+        if mode == "no-overlap":
+            nat.check(c.lib.nv_set_overlap(c.handle, 0))
         elif mode == "thread":
-            nat.check(c.lib.nv_set_cast_mode(c.handle, 3))
-        elif mode == "fused":
-            nat.check(c.lib.nv_set_fused(c.handle, 1))
+            nat.check(c.lib.nv_set_cast_mode(c.handle, nat.NV_CAST_THREAD))
+        elif mode == "warp":
+            nat.check(c.lib.nv_set_cast_mode(c.handle, nat.NV_CAST_WARP))
     acts = synth.random_actions(n, 4, seed=42)
     out = {"gps": np.empty((n, 2)), "compass": np.empty(n), "collided": np.empty(n, np.uint8),
            "displacement": np.empty(n)}
@@ -569,7 +564,7 @@ def test_host_step_frames_and_interleaving(nb):
         if t % 3 != 2:
             a.step_host(a_host, out=out)
             rgb_p, dep_p = ctypes.c_void_p(), ctypes.c_void_p()
-            nat.check(a.ctx.lib.nv_host_frames(a.ctx.handle, ctypes.byref(rgb_p),
+            nat.check(a.ctx.lib.nv_host_frames(a.ctx.handle, 0, ctypes.byref(rgb_p),
                                                ctypes.byref(dep_p), None))
             rgb = torch.as_tensor(_Dev(rgb_p.value, (n, H, W, 3), "|u1"), device="cuda:0")
             dep = torch.as_tensor(_Dev(dep_p.value, (n, H, W), "<f4"), device="cuda:0")

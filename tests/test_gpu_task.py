@@ -86,9 +86,9 @@ def test_snap_fields_geodesic_exact(nb, gold):
     assert np.array_equal(got[~both_nan], want[~both_nan])
 
 
-# nv_task_step_render with the task riding on the warp / thread cast (cast modes
-# 0 / 3), in the agent kernel (cast mode 1), or step + nv_task_step
-@pytest.mark.parametrize("path", ["cast-warp", "cast-thread", "agent", "separate"])
+# nv_task_step_render with the task riding on the warp / thread cast, or
+# step + nv_task_step
+@pytest.mark.parametrize("path", ["cast-warp", "cast-thread", "separate"])
 def test_episodes_batched_exact(nb, gold, path):
     if "n_episodes" not in gold:
         pytest.skip("no episodes in this fixture")
@@ -101,7 +101,8 @@ def test_episodes_batched_exact(nb, gold, path):
                                 n, sensor_configs=(SensorConfig("depth", width=64, height=16),))
     from paper_1904_01201_b200 import _native as nat
     env.fused_task = path != "separate"
-    mode = {"cast-warp": 0, "cast-thread": 3, "agent": 1, "separate": 0}[path]
+    mode = {"cast-warp": nat.NV_CAST_WARP, "cast-thread": nat.NV_CAST_THREAD,
+            "separate": nat.NV_CAST_AUTO}[path]
     nat.check(env.sim.ctx.lib.nv_set_cast_mode(env.sim.ctx.handle, mode))
     eps = []
     for k in range(n):
@@ -137,7 +138,10 @@ def test_episodes_batched_exact(nb, gold, path):
                 assert (d[k], r[k], float(dn[k]), float(co[k]), mv[k]) == tuple(row[:5]), (k, t)
                 assert (xy[k, 0], xy[k, 1], h[k]) == tuple(row[5:8]), (k, t)
             else:
-                assert stt[k] == 4 and dn[k] == 1  # NV_ENV_DONE: frozen
+                # NV_ENV_DONE: frozen; a finished env earns nothing more and
+                # keeps its last distance (no terminal reward counted twice)
+                assert stt[k] == 4 and dn[k] == 1
+                assert r[k] == 0.0 and d[k] == rows[-1][0], (k, t)
     outs = env.outcomes()
     for k in range(n):
         o = gold[f"ep{k}_outcome"]
@@ -192,6 +196,49 @@ def test_apartment_fields_vs_oracle(nb):
         assert np.array_equal(host[k], og.field(tuple(fc[k])))
 
 
+def test_envs_realloc_drops_task_state(nb, gold):
+    """nv_envs_alloc after PointGoal episodes (here: a larger batch) starts
+    from un-reset, un-frozen envs: no stale done flag freezes the new envs
+    and the task buffers of the old batch are never read (nv_task_step
+    refuses until nv_task_reset)."""
+    if "n_episodes" not in gold:
+        pytest.skip("no episodes in this fixture")
+    from paper_1904_01201_b200 import _native as nat
+    from paper_1904_01201_b200 import task
+    from paper_1904_01201_b200.sensors import SensorConfig
+    n = int(gold["n_episodes"])
+    segs = gold["segments"]
+    ns = len(segs)
+    env = task.BatchEnvironment((segs, np.arange(1, ns + 1, dtype=np.uint16), np.full((ns, 3), 0.5)),
+                                n, sensor_configs=(SensorConfig("depth", width=64, height=16),))
+    eps = []
+    for k in range(n):
+        p = f"ep{k}_"
+        sr, goal = gold[p + "start_raw"], gold[p + "goal"]
+        gd = float(gold[p + "gdsp"])
+        eu = math.hypot(goal[0] - sr[0], goal[1] - sr[1])
+        eps.append(task.Episode(f"e{k}", "x", (float(sr[0]), float(sr[1])), float(sr[2]),
+                                (float(goal[0]), float(goal[1])), gd, eu, gd / eu))
+    env.reset(eps)
+    _, done, _ = env.step(torch.full((n,), 3, dtype=torch.int8, device="cuda:0"))  # STOP: all done
+    assert bool(done.all())
+    c = env.sim.ctx
+    m = 4 * n + 3
+    nat.check(c.lib.nv_envs_alloc(c.handle, m))
+    xy = np.ascontiguousarray(np.repeat(gold["ep0_start"][None, :2], m, axis=0))
+    hd = np.full(m, float(gold["ep0_start"][2]))
+    st = np.zeros(m, dtype=np.int32)
+    nat.check(c.lib.nv_set_poses(c.handle, nat.ptr(xy), nat.ptr(hd), None, nat.ptr(st), None))
+    acts = torch.zeros(m, dtype=torch.int8, device="cuda:0")
+    status = torch.full((m,), -1, dtype=torch.int32, device="cuda:0")
+    nat.check(c.lib.nv_step(c.handle, nat.ptr(acts), None, None, nat.ptr(status),
+                            nat.stream_handle("cuda:0")))
+    torch.cuda.synchronize()
+    assert bool((status == 0).all())
+    assert c.lib.nv_task_step(c.handle, nat.ptr(acts), nat.ptr(status), None, None, None, None,
+                              None) == nat.NV_ERR_STATE
+
+
 def test_depth_noise_moments_and_paths(nb):
     """Inverse-depth noise (nv_depth_noise, sensors.py:183-205): the reference's
     moment test on the device stream (eps = max_range/d' - max_range/d has std
@@ -212,7 +259,7 @@ def test_depth_noise_moments_and_paths(nb):
     torch.cuda.synchronize()
     clean = sim.observations()["depth"].clone().double()
     outs = []
-    for mode in (2, 1, 0):
+    for mode in (nat.NV_FILL_AUTO, nat.NV_FILL_GENERIC):
         nat.check(c.lib.nv_set_fill_mode(c.handle, mode))
         nat.check(c.lib.nv_depth_noise(c.handle, 0.4, 1234, 0))
         sim.render()
