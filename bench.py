@@ -107,17 +107,22 @@ class ClockSampler:
 
 
 def ncu_traffic(cfg: str):
-    """dram read+write bytes per launch of the dominant kernel from the committed
-    ncu capture (profiles/r01_fill_traffic.json) when it was taken on this
-    config, else None."""
-    try:
-        with open(os.path.join(ROOT, "profiles", "r01_fill_traffic.json")) as f:
-            d = json.load(f)
-        if d.get("config", "C3") != cfg:
-            return None
-        return int(d["dram_bytes_read"]) + int(d["dram_bytes_write"])
-    except (OSError, KeyError, ValueError):
-        return None
+    """dram read+write bytes per launch of the dominant kernel from the newest
+    committed ncu capture of this config (profiles/r*_fill_traffic*.json),
+    else None."""
+    import glob
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_fill_traffic*.json")),
+                       reverse=True):
+        try:
+            with open(path) as f:
+                d = json.load(f)
+            if d.get("config", "C3") != cfg:
+                continue
+            return int(d["dram_bytes_read"]) + int(d["dram_bytes_write"]), \
+                os.path.relpath(path, ROOT)
+        except (OSError, KeyError, ValueError):
+            continue
+    return None, None
 
 
 def measured_peaks():
@@ -165,6 +170,7 @@ def cpu_baseline(cfg: str, seconds: float = 10.0, threads: int | None = None, n_
         if el >= seconds:
             break
     return {"value": frames / el, "unit": "frames/s", "cores": threads, "kind": "port",
+            "envs": n,
             "sample": f"{n} envs x {steps} steps of {WORKLOAD[cfg]} ({el:.1f} s, "
                       f"oracle/navsim_oracle.c, f64 frames like the reference)",
             "cpu_model": _cpu_model()}
@@ -181,11 +187,45 @@ def _cpu_model():
     return "unknown"
 
 
+def world_info():
+    return (int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")),
+            int(os.environ.get("LOCAL_RANK", "0")))
+
+
+def shard_for(args, world, rank):
+    """This rank's env range: weak scaling = N envs per GPU (the config's
+    per-GPU batch, or --envs), strong scaling = N envs in total split over
+    the GPUs."""
+    from paper_1904_01201_b200.dist import EnvShard
+    N = args.envs or CONFIGS[args.config][0]
+    n_total = N * world if args.scaling == "weak" else N
+    return EnvShard(n_total=n_total, world=world, rank=rank)
+
+
+def workload_config(args, shard, world, n_segments, n_triangles):
+    """The workload description shared by both arms (same dict: the driver
+    compares them)."""
+    N_cfg, W, H, chans, _ = CONFIGS[args.config]
+    step_bytes = shard.n_local * bytes_per_env_step(W, H, chans)
+    return {"workload": WORKLOAD[args.config], "config": args.config,
+            "envs_per_gpu": shard.n_local, "envs_total": shard.n_total, "width": W, "height": H,
+            "channels": list(chans), "segments": n_segments, "triangles": n_triangles,
+            "parallelism": f"env-shard x{world}", "scaling": args.scaling,
+            "l2": f"no flush: frames written per step ({step_bytes / 1e6:.0f} MB/GPU) "
+                  f"{'exceed' if step_bytes > 126e6 else 'stay below'} the 126 MB L2"}
+
+
 def run_reference(args):
-    rank = int(os.environ.get("RANK", "0"))
+    """The reference arm: rank 0 alone times the reference's CPU path (the
+    oracle port of Simulator.step + observations) on all host threads, on
+    the GPU arm's workload; the other ranks exit without work."""
+    world, rank, _ = world_info()
     if rank != 0:
         return 0
+    from paper_1904_01201_b200 import synth
     cfg = args.config
+    shard = shard_for(args, world, 0)
+    sc = synth.config_scene(CONFIGS[cfg][4])
     per_step = []
     res = None
     for s in range(args.warmup + args.steps):
@@ -195,16 +235,82 @@ def run_reference(args):
             per_step.append(r["value"])
             res = r
     v = statistics.median(per_step)
-    N_cfg, W, H, chans, _ = CONFIGS[cfg]
     line = {"impl": "reference", "metric": METRIC,
-            "value": v, "unit": "frames/s", "n_gpus": args.gpus, "steps": args.steps,
-            "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
+            "value": v, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "higher_is_better": True, "scaling": args.scaling,
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": WORKLOAD[cfg], "config": cfg},
+            "config": workload_config(args, shard, world, sc.n_segments, sc.n_triangles),
+            "sampled_envs": res["envs"],
             "cpu_baseline": dict(res, value=v),
             "e2e": {"value": v, "unit": "frames/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
+    return 0
+
+
+# ------------------------------------------------------------ multi-rank launch
+
+def _free_port():
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def spawn_ranks(args, argv):
+    """`bench.py --gpus N` outside torchrun: launch N ranks of this script
+    under torch.distributed.run (one process per GPU, rendezvous on
+    127.0.0.1) and return its exit code; rank 0's JSON line reaches our
+    stdout.  None when no spawn is needed (N = 1 or already under torchrun)."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return None
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           f"--master-port={_free_port()}", os.path.abspath(__file__), *argv]
+    env = dict(os.environ)
+    if not args.dry_run:
+        env.setdefault("NCCL_DEBUG", "INFO")  # rank / channel setup in the log
+    return subprocess.call(cmd, env=env)
+
+
+def run_dry(args):
+    """The multi-rank plumbing with the GPU parts stubbed (CPU, gloo): rank
+    setup, barrier + max-over-ranks timing, the EpisodeOutcome all-gather of
+    synthetic 40-byte records; rank 0 prints the contract's line."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1904_01201_b200.dist import gather_records
+    world, rank, _ = world_info()
+    if world != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+        return 2
+    if world > 1:
+        dist.init_process_group("gloo")
+    shard = shard_for(args, world, rank)
+    t0 = time.perf_counter()
+    if world > 1:
+        dist.barrier()
+    ms = torch.tensor([(time.perf_counter() - t0) * 1e3], dtype=torch.float64)
+    rec = torch.zeros((shard.n_local, 40), dtype=torch.uint8)
+    rec[:, 4] = 1  # steps = 1 in every record
+    rec[:, 8:12] = torch.arange(shard.lo, shard.hi, dtype=torch.int32).view(-1, 1).view(torch.uint8)
+    if world > 1:
+        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    gathered = gather_records(rec, world)
+    if rank == 0:
+        ids = gathered[:, 8:12].contiguous().view(torch.int32).reshape(-1).tolist()
+        print(json.dumps({
+            "metric": METRIC, "value": None, "unit": "frames/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": None,
+            "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
+            "dtype": None, "data": "dry run: GPU parts stubbed",
+            "config": workload_config(args, shard, world, None, None), "dry_run": True,
+            "gathered_records": int(gathered.shape[0]),
+            "gathered_in_env_order": ids == list(range(shard.n_total))}))
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
     return 0
 
 
@@ -214,34 +320,34 @@ def run_gpu(args):
     import torch
     import torch.distributed as dist
 
-    from paper_1904_01201_b200 import BatchSimulator, SensorConfig, synth
+    from paper_1904_01201_b200 import BatchSimulator, SensorConfig, synth, task
     from paper_1904_01201_b200 import _native as nat
-    from paper_1904_01201_b200.dist import EnvShard, gather_episode_stats
+    from paper_1904_01201_b200.dist import pointgoal_eval
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    world, rank, local = world_info()
+    if world != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+        return 2
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     cfg = args.config
-    N, W, H, chans, scene_key = CONFIGS[cfg]
-    if args.envs:
-        N = args.envs
-    shard = EnvShard(n_total=N * world, world=world, rank=rank)
+    _, W, H, chans, scene_key = CONFIGS[cfg]
+    shard = shard_for(args, world, rank)
     sc = synth.config_scene(scene_key)
     suite = tuple(SensorConfig(c, W, H) for c in chans) + (SensorConfig("gps_compass"),)
     sim = BatchSimulator(sc.segments, sc.semantic_ids, sc.albedo, shard.n_local,
                          sensor_configs=suite, wall_height=sc.wall_height,
                          floor_color=sc.floor_color, ceiling_color=sc.ceiling_color, device=local)
-    poses = synth.sample_poses(sc, shard.n_total, seed=1)[shard.lo:shard.hi]
+    # per-env start poses and actions derive from the global env id
+    poses = synth.sample_poses(sc, shard.n_local, seed=1, first=shard.lo)
     sim.reset(poses[:, :2], poses[:, 2])
     nat.check(sim.ctx.lib.nv_set_overlap(sim.ctx.handle, 1 if args.overlap else 0))
     nat.check(sim.ctx.lib.nv_set_fill_mode(sim.ctx.handle, args.fill_mode))
     nat.check(sim.ctx.lib.nv_set_cast_mode(sim.ctx.handle, args.cast_mode))
     total_steps = args.warmup + args.steps
-    acts = torch.as_tensor(synth.random_actions(shard.n_total, total_steps, seed=2)[:, shard.lo:shard.hi].copy(),
-                           device=f"cuda:{local}")
+    acts = torch.as_tensor(synth.random_actions(shard.n_total, total_steps, seed=2)
+                           [:, shard.lo:shard.hi].copy(), device=f"cuda:{local}")
     stream = torch.cuda.current_stream()
 
     def barrier():
@@ -304,8 +410,6 @@ def run_gpu(args):
     ms_max = float(t.item())
     frames = shard.n_total * args.steps
     value = frames / (ms_max / 1e3)
-    # episode statistics: the one collective of the path (NCCL all-gather)
-    stats = gather_episode_stats(sim, shard, world)
 
     # ---- kernel breakdown: per-kernel CUDA events over a second run of K steps
     lib, h = sim.ctx.lib, sim.ctx.handle
@@ -327,6 +431,7 @@ def run_gpu(args):
     achieved = dom_bytes / (dom_ms / 1e3) / 1e9
     step_bytes = shard.n_local * bytes_per_env_step(W, H, chans)
     step_gbs = step_bytes / (ms_max / args.steps / 1e3) / 1e9
+    traffic, traffic_src = ncu_traffic(cfg)
 
     # ---- e2e: host-buffer C-ABI path, pinned host actions in, results out
     e2e = None
@@ -380,6 +485,21 @@ def run_gpu(args):
                       "h2d_bytes_per_step": n, "d2h_bytes_per_step":
                           n * (W * H * sum(BYTES_PER_PX[c] for c in chans) + 33),
                       "steps": k2}
+        del fr
+
+    # ---- PointGoal evaluation + the path's one collective: the NCCL
+    # all-gather of the task layer's 40-byte EpisodeOutcome records
+    outcomes = None
+    if not args.no_eval:
+        t0 = time.perf_counter()
+        env = task.BatchEnvironment((sc.segments, sc.semantic_ids, sc.albedo), shard.n_local,
+                                    sensor_configs=suite, device=local,
+                                    max_steps=task.MAX_EPISODE_STEPS)
+        outcomes, _, _ = pointgoal_eval(env, sc, shard, world, n_steps=args.eval_steps, seed=11)
+        outcomes["wall_s"] = time.perf_counter() - t0
+        outcomes["collective"] = (f"{'NCCL' if world > 1 else 'none (1 rank)'} all-gather of "
+                                  f"{shard.n_total} x 40-byte EpisodeOutcome records")
+        del env
 
     line = None
     if rank == 0:
@@ -387,26 +507,23 @@ def run_gpu(args):
             "metric": METRIC,
             "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None,
+            "scaling": args.scaling, "vs_baseline": None,
             "dtype": "f64 geometry/kinematics; u8 rgb, f32 depth, u16 semantic outputs",
             "data": "synthetic (procedural scene, seeded poses/actions)",
-            "config": {"workload": WORKLOAD[cfg], "config": cfg, "envs_per_gpu": shard.n_local,
-                       "envs_total": shard.n_total, "width": W, "height": H,
-                       "channels": list(chans), "segments": sc.n_segments,
-                       "triangles": sc.n_triangles, "parallelism": f"env-shard x{world}",
-                       "cuda_graph": use_graph,
-                       "graph_warm_replay": bool(use_graph and not args.cold_graph),
-                       "fill_mode": ["auto (warp-specialised TMA writer; row bands for small batches)",
-                                     "per-pixel kernel"][args.fill_mode],
-                       "cast_mode": ["dda (thread per ray; warp per ray for <= 16384 rays)",
-                                     "dda-thread-per-ray", "dda-warp-per-ray"][args.cast_mode],
-                       "l2": f"no flush: frames written per step "
-                             f"({step_bytes / 1e6:.0f} MB/GPU) exceed the 126 MB L2"},
+            "config": workload_config(args, shard, world, sc.n_segments, sc.n_triangles),
+            "impl_config": {
+                "cuda_graph": use_graph,
+                "graph_warm_replay": bool(use_graph and not args.cold_graph),
+                "fill_mode": ["auto (warp-specialised TMA writer; row bands for small batches)",
+                              "per-pixel kernel"][args.fill_mode],
+                "cast_mode": ["dda (thread per ray; warp per ray for <= 16384 rays)",
+                              "dda-thread-per-ray", "dda-warp-per-ray"][args.cast_mode],
+                "overlap": bool(args.overlap)},
             "roofline": {"bound": "hbm", "kernel": dom,
                          "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak,
-                         "traffic": ncu_traffic(cfg),
-                         "traffic_source": "profiles/r01_fill_traffic.json (ncu --set full)",
+                         "traffic": traffic,
+                         "traffic_source": traffic_src and f"{traffic_src} (ncu --set full)",
                          "peak_source": peak_src,
                          "bytes_per_launch": dom_bytes,
                          "kernel_ms": per,
@@ -415,7 +532,7 @@ def run_gpu(args):
             "gpu_launches": int(launches_timed),
             "e2e": e2e,
             "e2e_host_frames": e2e_frames,
-            "episode_stats": stats,
+            "episode_outcomes": outcomes,
         }
         if not args.no_cpu_baseline and world == 1:  # reported at N=1 only
             line["cpu_baseline"] = cpu_baseline(cfg, seconds=args.cpu_seconds)
@@ -430,14 +547,21 @@ def run_gpu(args):
     return 0
 
 
-def main():
+def main(argv=None):
+    argv = sys.argv[1:] if argv is None else argv
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="C3", choices=sorted(CONFIGS))
-    ap.add_argument("--envs", type=int, default=0, help="override envs per GPU")
+    ap.add_argument("--envs", type=int, default=0,
+                    help="override the env count (per GPU when weak, total when strong)")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="weak: the config's envs on every GPU; strong: that many envs in "
+                         "total over the GPUs")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--dry-run", action="store_true",
+                    help="multi-rank plumbing only, GPU parts stubbed (CPU, gloo)")
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--cold-graph", action="store_true",
                     help="time the graph's first replay (no untimed upload replay)")
@@ -448,15 +572,23 @@ def main():
     ap.add_argument("--overlap", type=int, default=1,
                     help="agent step -> cast programmatic dependent launch overlap (1 = library default, 0 = off)")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-eval", action="store_true",
+                    help="skip the PointGoal evaluation + EpisodeOutcome all-gather")
+    ap.add_argument("--eval-steps", type=int, default=64)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--ref-seconds", type=float, default=60.0)
     ap.add_argument("--ref-envs", type=int, default=0)
-    args = ap.parse_args()
+    args = ap.parse_args(argv)
     if args.warmup < 3:
         args.warmup = 3
+    rc = spawn_ranks(args, argv)
+    if rc is not None:
+        return rc
     if args.impl == "reference":
         return run_reference(args)
+    if args.dry_run:
+        return run_dry(args)
     return run_gpu(args)
 
 

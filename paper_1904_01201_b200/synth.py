@@ -217,16 +217,17 @@ def _free_raster(scene: SynthScene, clearance: float, res: float = 0.05):
     return ~grown, x0, y0, res
 
 
-def sample_poses(scene: SynthScene, n: int, seed: int, clearance: float = 0.15):
-    """n start poses inside the rooms, >= clearance from every wall (conservative
-    raster test; the simulator re-checks exactly on reset).  Heading uniform on
-    (-pi, pi].  Per-env streams derive from (seed, env id) so sharding over
-    ranks does not change any env's pose (src/seeding.py:13-23 idea)."""
+def sample_poses(scene: SynthScene, n: int, seed: int, clearance: float = 0.15, first: int = 0):
+    """Start poses of envs first .. first+n-1 inside the rooms, >= clearance
+    from every wall (conservative raster test; the simulator re-checks exactly
+    on reset).  Heading uniform on (-pi, pi].  Per-env streams derive from
+    (seed, global env id) so sharding over ranks does not change any env's
+    pose (src/seeding.py:13-23 idea)."""
     free, x0, y0, res = _free_raster(scene, clearance)
     ny, nx = free.shape
     out = np.empty((n, 3))
     for e in range(n):
-        rng = np.random.default_rng(np.random.SeedSequence([seed, e]))
+        rng = np.random.default_rng(np.random.SeedSequence([seed, first + e]))
         for _ in range(10_000):
             r = scene.rooms[int(rng.integers(len(scene.rooms)))]
             x = rng.uniform(r[0] + 0.2, r[2] - 0.2)
@@ -245,3 +246,48 @@ def random_actions(n_envs: int, n_steps: int, seed: int) -> np.ndarray:
     (tests/test_acceptance.py:91-92 policy)."""
     rng = np.random.default_rng(np.random.SeedSequence([seed, 0xAC7]))
     return rng.integers(0, 3, size=(n_steps, n_envs)).astype(np.int8)
+
+
+def pointgoal_episodes(env, scene: SynthScene, n: int, seed: int, first: int = 0,
+                       n_goals: int = 16):
+    """PointGoal episodes for envs first .. first+n-1 of ``env`` (a
+    task.BatchEnvironment on ``scene``): goals from a shared pool of
+    ``n_goals`` seeded navigable points, starts from ``sample_poses``; each
+    env takes the first goal of its own seeded order whose geodesic distance
+    gdsp (nav.geodesic_distance on the goal's device field, like the
+    reference's episode generator, episodes.py) satisfies Episode.validate
+    (1 <= gdsp <= 30 m, gdsp >= euclidean - 2 res).  Everything derives from
+    (seed, global env id): sharding does not change an env's episode.
+    Returns a list with None for envs no goal fits."""
+    import torch
+
+    from . import _native as nat
+    from . import nav, task
+    grid = env.grid
+    goals = sample_poses(scene, n_goals, seed=seed ^ 0x6F41, first=0)[:, :2]
+    fields, _ = nav.distance_fields(grid, goals)
+    starts = sample_poses(scene, n, seed=seed, first=first)
+    k = len(goals)
+    pts = torch.as_tensor(np.repeat(starts[:, :2], k, axis=0), device=env.dev)
+    fid = torch.as_tensor(np.tile(np.arange(k, dtype=np.int32), n), device=env.dev)
+    gd = torch.empty(n * k, dtype=torch.float64, device=env.dev)
+    c = grid.ctx
+    nat.check(c.lib.nv_nav_geodesic(c.handle, nat.ptr(fields), nat.ptr(fid), nat.ptr(pts), n * k,
+                                     nat.ptr(gd), nat.stream_handle(env.dev)))
+    gd = gd.cpu().numpy().reshape(n, k)
+    out = []
+    for e in range(n):
+        rng = np.random.default_rng(np.random.SeedSequence([seed, 0x60A1, first + e]))
+        ep = None
+        for g in rng.permutation(k):
+            d = float(gd[e, g])
+            eu = float(np.hypot(goals[g, 0] - starts[e, 0], goals[g, 1] - starts[e, 1]))
+            if not (math.isfinite(d) and 1.0 <= d <= 30.0 and eu > 0.0
+                    and d >= eu - 2.0 * grid.resolution):
+                continue
+            ep = task.Episode(f"ep{first + e}", env.scene_id or "synthetic",
+                              (float(starts[e, 0]), float(starts[e, 1])), float(starts[e, 2]),
+                              (float(goals[g, 0]), float(goals[g, 1])), d, eu, d / eu)
+            break
+        out.append(ep)
+    return out

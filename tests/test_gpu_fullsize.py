@@ -1,6 +1,11 @@
-"""Parity at BASELINE.json's full size (C3: 1024 envs x 256x256 RGB-D on the
-~200k-triangle apartment), the bench's own workload and default paths
-(warp-specialised writer, thread-per-ray DDA):
+"""Parity at BASELINE.json's full sizes, the bench's own workloads and default
+paths (warp-specialised writer, thread-per-ray DDA):
+
+* C3: 1024 envs x 256x256 RGB-D(-S) on the ~200k-triangle apartment;
+* C5: 512 envs (4096 over 8 GPUs) x 512x512 RGB-D(-S) on the ~1M-triangle
+  scene (~500k segments, 161x155 grid; two warp segments per frame row in
+  the writer, row-banded work items), plus a small C5 batch compared with
+  the oracle in every env at every step;
 
 * a seeded sample of envs against the oracle at every step (poses 1e-6,
   semantic/coverage exact, depth 1e-5 rel, RGB 1/255);
@@ -31,21 +36,20 @@ def nb():
     return nb
 
 
-def test_c3_fullsize(nb, oracle_mod):
+def _check_batch(nb, oracle_mod, cfg, N, W, H, steps, n_sample, seed):
     from paper_1904_01201_b200 import synth
-    sc = synth.config_scene("C3")
-    N, W, H = 1024, 256, 256
+    sc = synth.config_scene(cfg)
     suite = (nb.SensorConfig("rgb", W, H), nb.SensorConfig("depth", W, H),
              nb.SensorConfig("semantic", W, H))
     sim = nb.BatchSimulator(sc.segments, sc.semantic_ids, sc.albedo, N, sensor_configs=suite,
                             floor_color=sc.floor_color, ceiling_color=sc.ceiling_color)
-    poses = synth.sample_poses(sc, N, seed=41)
+    poses = synth.sample_poses(sc, N, seed=seed)
     sim.reset(poses[:, :2], poses[:, 2])
-    acts = synth.random_actions(N, 4, seed=42)
+    acts = synth.random_actions(N, steps, seed=seed + 1)
     osc = oracle_mod.OracleScene(sc.segments, sc.semantic_ids, sc.albedo, sc.wall_height,
                                  sc.floor_color, sc.ceiling_color)
-    rng = np.random.default_rng(43)
-    sample = rng.choice(N, size=12, replace=False)
+    rng = np.random.default_rng(seed + 2)
+    sample = rng.choice(N, size=min(n_sample, N), replace=False)
     states = {int(e): [poses[e, 0], poses[e, 1], oracle_mod.wrap_angle(poses[e, 2]), 0.0, 0]
               for e in sample}
     focal = suite[0].focal
@@ -93,6 +97,11 @@ def test_c3_fullsize(nb, oracle_mod):
             rel = np.abs(dep_h[e].astype(np.float64) - d) / np.maximum(np.abs(d), 1e-12)
             assert rel.max() <= DEPTH_RTOL
             assert np.abs(rgb_h[e].astype(np.float64) / 255.0 - rgb).max() <= RGB_ATOL
+    return sim
+
+
+def test_c3_fullsize(nb, oracle_mod):
+    sim = _check_batch(nb, oracle_mod, "C3", 1024, 256, 256, steps=4, n_sample=12, seed=41)
     # determinism: render again from the same state -> identical frames
     first = {k: v.clone() for k, v in sim.observations().items()}
     sim.render()
@@ -100,3 +109,15 @@ def test_c3_fullsize(nb, oracle_mod):
     again = sim.observations()
     for k in first:
         assert torch.equal(first[k].view(torch.uint8), again[k].view(torch.uint8))
+
+
+def test_c5_fullsize(nb, oracle_mod):
+    """C5 at full per-GPU size: 512 envs x 512x512 on the ~1M-triangle scene,
+    a seeded sample of envs against the oracle at every step."""
+    _check_batch(nb, oracle_mod, "C5", 512, 512, 512, steps=3, n_sample=10, seed=51)
+
+
+def test_c5_small_batch_every_env(nb, oracle_mod):
+    """C5's scene and resolution with every env compared at every step (8 envs
+    x 6 steps: the warp-per-ray cast and the row-banded writer)."""
+    _check_batch(nb, oracle_mod, "C5", 8, 512, 512, steps=6, n_sample=8, seed=61)
