@@ -255,8 +255,10 @@ int nv_profile_read(nv_ctx *ctx, double *ms4, int64_t *counts4);
  * cell (0, 0)'s center.  Synchronous. */
 int nv_nav_build(nv_ctx *ctx, const double *bounds, double resolution, double agent_radius,
                  int64_t *nx, int64_t *ny, double *origin2);
-/* Copies the mask (u8 ny x nx) and clearance (f64 ny x nx) to HOST buffers. */
-int nv_nav_copy(nv_ctx *ctx, uint8_t *mask, double *clearance);
+/* Copies the mask (u8 ny x nx) and clearance (f64 ny x nx) to HOST buffers
+ * sized for an nx x ny grid; NV_ERR_STATE if the context's current grid has
+ * another size (it was rebuilt since the caller's nv_nav_build). */
+int nv_nav_copy(nv_ctx *ctx, int64_t nx, int64_t ny, uint8_t *mask, double *clearance);
 /* nav._snap_to_navigable (nav.py:103-119) for m HOST points (m x 2); HOST
  * cells out (m x 2 i32: i, j, or -1, -1 when nothing is within radius). */
 int nv_nav_snap(nv_ctx *ctx, const double *pts, int64_t m, double radius, int32_t *cells);

@@ -62,7 +62,7 @@ SIGNATURES = {
     "nv_profile": (_I, [_P, _I]),
     "nv_profile_read": (_I, [_P, _P, _P]),
     "nv_nav_build": (_I, [_P, _P, _D, _D, _P, _P, _P]),
-    "nv_nav_copy": (_I, [_P, _P, _P]),
+    "nv_nav_copy": (_I, [_P, _I64, _I64, _P, _P]),
     "nv_nav_snap": (_I, [_P, _P, _I64, _D, _P]),
     "nv_nav_fields": (_I, [_P, _P, _I64, _P, _P]),
     "nv_nav_geodesic": (_I, [_P, _P, _P, _P, _I64, _P, _P]),

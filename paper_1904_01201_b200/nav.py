@@ -41,12 +41,21 @@ class OccupancyGrid:
     height: int
     ctx: object = field(repr=False)
     _host: dict = field(default_factory=dict, repr=False)
+    gen: int = 0  # the context's grid generation this object describes
+
+    def _check(self):
+        """The context holds one grid; a rebuild invalidates older grid objects
+        (their sizes would no longer match the device buffers)."""
+        if getattr(self.ctx, "_nav_gen", 0) != self.gen:
+            raise NavError("occupancy grid was rebuilt on its context; use the new grid")
 
     def _pull(self):
+        self._check()
         if not self._host:
             m = np.empty((self.height, self.width), dtype=np.uint8)
             d = np.empty((self.height, self.width), dtype=np.float64)
-            nat.check(self.ctx.lib.nv_nav_copy(self.ctx.handle, nat.ptr(m), nat.ptr(d)))
+            nat.check(self.ctx.lib.nv_nav_copy(self.ctx.handle, self.width, self.height,
+                                               nat.ptr(m), nat.ptr(d)))
             self._host["navigable"] = m.astype(bool)
             self._host["clearance"] = d
         return self._host
@@ -76,6 +85,7 @@ class OccupancyGrid:
     def snap(self, points, radius: float = SNAP_RADIUS) -> np.ndarray:
         """_snap_to_navigable for many points: (m, 2) i32 cells, -1 rows when
         nothing navigable lies within radius (nav.py:103-119)."""
+        self._check()
         pts = np.ascontiguousarray(np.asarray(points, dtype=np.float64).reshape(-1, 2))
         cells = np.empty((len(pts), 2), dtype=np.int32)
         nat.check(self.ctx.lib.nv_nav_snap(self.ctx.handle, nat.ptr(pts), len(pts),
@@ -105,8 +115,9 @@ def build_grid(ctx, bounds=None, resolution: float = DEFAULT_RESOLUTION,
     nat.check(ctx.lib.nv_nav_build(ctx.handle, nat.ptr(b), float(resolution),
                                    float(agent_radius), nat.ptr(nx), nat.ptr(ny),
                                    nat.ptr(origin)))
+    ctx._nav_gen = getattr(ctx, "_nav_gen", 0) + 1
     return OccupancyGrid(origin=origin, resolution=float(resolution), width=int(nx[0]),
-                         height=int(ny[0]), ctx=ctx)
+                         height=int(ny[0]), ctx=ctx, gen=ctx._nav_gen)
 
 
 def rasterize_navigable(segments, bounds, resolution: float = DEFAULT_RESOLUTION,
@@ -184,6 +195,7 @@ def geodesic_distance(field: DistanceField, p) -> float:
     fid = torch.zeros(1, dtype=torch.int32, device=dev)
     out = torch.empty(1, dtype=torch.float64, device=dev)
     ctx = field.grid.ctx
+    field.grid._check()
     nat.check(ctx.lib.nv_nav_geodesic(ctx.handle, nat.ptr(field.dist_device), nat.ptr(fid),
                                       nat.ptr(pts), 1, nat.ptr(out), nat.stream_handle(dev)))
     v = float(out.item())

@@ -346,3 +346,24 @@ def test_apartment_batch_episodes_vs_oracle(nb):
             done_o[e] = ddone
     outs = env.outcomes()
     assert all(o is not None for o in outs)
+
+
+def test_rebuilt_grid_invalidates_old_grid_objects(nb):
+    """A context holds one navigation grid: after a rebuild with other bounds,
+    the old OccupancyGrid refuses host copies / snaps (its sizes no longer
+    match the device buffers) and nv_nav_copy refuses mismatched buffers."""
+    from paper_1904_01201_b200 import _native as nat
+    from paper_1904_01201_b200 import nav, synth
+    sc = synth.single_room(20)
+    g1 = nav.rasterize_navigable(sc.segments, (0.0, 0.0, 10.0, 10.0))
+    assert g1.navigable.shape == (g1.height, g1.width)
+    g2 = nav.build_grid(g1.ctx, (0.0, 0.0, 5.0, 10.0))
+    assert (g2.width, g2.height) != (g1.width, g1.height)
+    with pytest.raises(nav.NavError):
+        _ = g1.clearance if not g1._host else nav.distance_fields(g1, [(2.0, 2.0)])
+    with pytest.raises(nav.NavError):
+        g1.snap([(2.0, 2.0)])
+    assert g2.navigable.shape == (g2.height, g2.width)
+    m = np.empty((g1.height, g1.width), np.uint8)
+    rc = g1.ctx.lib.nv_nav_copy(g1.ctx.handle, g1.width, g1.height, nat.ptr(m), None)
+    assert rc == nat.NV_ERR_STATE
