@@ -152,18 +152,22 @@ def cpu_baseline(cfg: str, seconds: float = 10.0, threads: int | None = None, n_
     h = np.array([oracle.wrap_angle(v) for v in poses[:, 2]])
     path = np.zeros(n)
     coll = np.zeros(n, dtype=np.int64)
-    depth = np.empty((n, H, W)) if "depth" in chans else None
-    rgb = np.empty((n, H, W, 3)) if "rgb" in chans else None
-    sem = np.empty((n, H, W), dtype=np.uint16) if "semantic" in chans else None
+    # one frame per worker thread, reused for every env it steps: the
+    # reference's bench workers each step one env and discard its frames
+    # (bench.py:128-137), so a worker's frame arrays stay cache-resident
+    depth = np.empty((threads, H, W)) if "depth" in chans else None
+    rgb = np.empty((threads, H, W, 3)) if "rgb" in chans else None
+    sem = np.empty((threads, H, W), dtype=np.uint16) if "semantic" in chans else None
     focal = (W * 0.5) / math.tan(math.radians(90.0) * 0.5)
     acts = synth.random_actions(n, 10_000, seed=2)
     frames, steps, t0 = 0, 0, time.perf_counter()
     osc.batch_step_render(x, y, h, path, coll, acts[0], 0.1, 0.25, 10.0, 1.5, W, H, focal, 10.0,
-                          depth, rgb, sem, threads)  # warm-up
+                          depth, rgb, sem, threads, per_thread_frames=True)  # warm-up
     t0 = time.perf_counter()
     while True:
         osc.batch_step_render(x, y, h, path, coll, acts[(steps + 1) % len(acts)], 0.1, 0.25, 10.0,
-                              1.5, W, H, focal, 10.0, depth, rgb, sem, threads)
+                              1.5, W, H, focal, 10.0, depth, rgb, sem, threads,
+                              per_thread_frames=True)
         steps += 1
         frames += n
         el = time.perf_counter() - t0

@@ -108,6 +108,11 @@ int64_t or_grid_build(const double *segs, int64_t n, double x0, double y0,
   return total;
 }
 
+static int cmp_i64(const void *a, const void *b) {
+  const int64_t x = *(const int64_t *)a, y = *(const int64_t *)b;
+  return (x > y) - (x < y);
+}
+
 /* SegmentIndex.query_aabb, src/geometry.py:151-163: sorted unique ids.
  * mark is scratch of n bytes (zeroed on entry and on exit). Returns count. */
 int64_t or_query_aabb(double xmin, double ymin, double xmax, double ymax,
@@ -116,17 +121,22 @@ int64_t or_query_aabb(double xmin, double ymin, double xmax, double ymax,
                       uint8_t *mark, int64_t *out) {
   int64_t cx0 = cell_coord(xmin, x0, nx), cy0 = cell_coord(ymin, y0, ny);
   int64_t cx1 = cell_coord(xmax, x0, nx), cy1 = cell_coord(ymax, y0, ny);
+  /* np.unique(np.concatenate(buckets)): the marked ids in ascending order,
+     gathered from the buckets and sorted (O(k log k) like np.unique, not a
+     scan over all n segments) */
   int64_t m = 0;
+  (void)n;
   for (int64_t cy = cy0; cy <= cy1; ++cy)
     for (int64_t cx = cx0; cx <= cx1; ++cx) {
       int64_t k = cy * nx + cx;
-      for (int64_t q = starts[k]; q < starts[k + 1]; ++q) mark[items[q]] = 1;
+      for (int64_t q = starts[k]; q < starts[k + 1]; ++q)
+        if (!mark[items[q]]) {
+          mark[items[q]] = 1;
+          out[m++] = items[q];
+        }
     }
-  for (int64_t i = 0; i < n; ++i)
-    if (mark[i]) {
-      out[m++] = i;
-      mark[i] = 0;
-    }
+  qsort(out, (size_t)m, sizeof(int64_t), cmp_i64);
+  for (int64_t i = 0; i < m; ++i) mark[out[i]] = 0;
   return m;
 }
 
@@ -458,6 +468,14 @@ typedef struct {
   int64_t gnx, gny;
   int64_t *starts, *items;
   double wall_h, floor_color[3], ceil_color[3];
+  /* per-worker scratch of or_batch_step_render, kept across calls (a
+     per-call malloc/free of the candidate arrays means mmap/munmap and TLB
+     shootdowns in every worker: the baseline would not scale with threads) */
+  int npool;
+  int64_t pool_w;
+  uint8_t **p_mark;
+  int64_t **p_cand, **p_isc;
+  double **p_scratch;
 } or_scene;
 
 /* RenderGeometry.__init__, src/sensors.py:81-93 */
@@ -501,6 +519,10 @@ void or_scene_destroy(void *p) {
   free(s->ax); free(s->ay); free(s->bx); free(s->by); free(s->ex); free(s->ey);
   free(s->nx); free(s->ny); free(s->albedo); free(s->sem);
   free(s->starts); free(s->items);
+  for (int k = 0; k < s->npool; ++k) {
+    free(s->p_mark[k]); free(s->p_cand[k]); free(s->p_isc[k]); free(s->p_scratch[k]);
+  }
+  free(s->p_mark); free(s->p_cand); free(s->p_isc); free(s->p_scratch);
   free(s);
 }
 
@@ -736,16 +758,22 @@ typedef struct {
   double *depth, *rgb;
   uint16_t *sem;
   int64_t next; /* atomic work counter */
+  int per_thread; /* frames: one per worker thread (reused), not one per env */
 } or_batch_job;
 
+typedef struct {
+  or_batch_job *j;
+  int64_t tid;
+} or_batch_arg;
+
 static void *batch_worker(void *arg) {
-  or_batch_job *j = (or_batch_job *)arg;
+  or_batch_job *j = ((or_batch_arg *)arg)->j;
+  const int64_t tid = ((or_batch_arg *)arg)->tid;
   or_scene *s = j->s;
-  size_t nn = (size_t)(s->n > 0 ? s->n : 1);
-  uint8_t *mark = calloc(nn, 1);
-  int64_t *cand = malloc(nn * 8);
-  double *scratch = malloc(sizeof(double) * 4 * (size_t)j->W);
-  int64_t *isc = malloc(sizeof(int64_t) * (size_t)j->W);
+  uint8_t *mark = s->p_mark[tid];
+  int64_t *cand = s->p_cand[tid];
+  double *scratch = s->p_scratch[tid];
+  int64_t *isc = s->p_isc[tid];
   size_t px = (size_t)(j->W * j->H);
   for (;;) {
     int64_t e = __atomic_fetch_add(&j->next, 1, __ATOMIC_RELAXED);
@@ -762,17 +790,38 @@ static void *batch_worker(void *arg) {
       a.heading = or_wrap_angle(a.heading + (-j->turn_rad));
     j->x[e] = a.x; j->y[e] = a.y; j->heading[e] = a.heading;
     j->path_len[e] = a.path_len; j->collisions[e] = a.collisions;
+    const size_t f = (size_t)(j->per_thread ? tid : e);  /* frame slot */
     scene_render(s, a.x, a.y, a.heading, j->sensor_h, j->W, j->H, j->focal,
                  j->max_range, 1e9, 0, scratch, isc,
-                 j->depth ? j->depth + px * (size_t)e : NULL,
-                 j->rgb ? j->rgb + 3 * px * (size_t)e : NULL,
-                 j->sem ? j->sem + px * (size_t)e : NULL);
+                 j->depth ? j->depth + px * f : NULL,
+                 j->rgb ? j->rgb + 3 * px * f : NULL,
+                 j->sem ? j->sem + px * f : NULL);
   }
-  free(mark);
-  free(cand);
-  free(scratch);
-  free(isc);
   return NULL;
+}
+
+/* per-thread scratch for nthreads workers and width W (grown, never shrunk) */
+static void scratch_pool(or_scene *s, int nthreads, int64_t W) {
+  size_t nn = (size_t)(s->n > 0 ? s->n : 1);
+  if (nthreads <= s->npool && W <= s->pool_w) return;
+  for (int k = 0; k < s->npool; ++k) {
+    free(s->p_mark[k]); free(s->p_cand[k]); free(s->p_isc[k]); free(s->p_scratch[k]);
+  }
+  free(s->p_mark); free(s->p_cand); free(s->p_isc); free(s->p_scratch);
+  int np = nthreads > s->npool ? nthreads : s->npool;
+  int64_t w = W > s->pool_w ? W : s->pool_w;
+  s->p_mark = malloc(sizeof(uint8_t *) * (size_t)np);
+  s->p_cand = malloc(sizeof(int64_t *) * (size_t)np);
+  s->p_isc = malloc(sizeof(int64_t *) * (size_t)np);
+  s->p_scratch = malloc(sizeof(double *) * (size_t)np);
+  for (int k = 0; k < np; ++k) {
+    s->p_mark[k] = calloc(nn, 1);  /* scene_forward leaves it all zero again */
+    s->p_cand[k] = malloc(nn * 8);
+    s->p_isc[k] = malloc(sizeof(int64_t) * (size_t)w);
+    s->p_scratch[k] = malloc(sizeof(double) * 4 * (size_t)w);
+  }
+  s->npool = np;
+  s->pool_w = w;
 }
 
 void or_batch_step_render(void *p, int64_t N, double *x, double *y,
@@ -780,14 +829,25 @@ void or_batch_step_render(void *p, int64_t N, double *x, double *y,
                           const int8_t *actions, double radius, double step,
                           double turn_rad, double sensor_h, int64_t W, int64_t H,
                           double focal, double max_range, double *depth,
-                          double *rgb, uint16_t *sem, int nthreads) {
+                          double *rgb, uint16_t *sem, int nthreads, int per_thread) {
+  /* per_thread != 0: depth/rgb/sem hold one frame per worker thread, reused
+     for every env the thread steps -- the memory behaviour of the
+     reference's bench workers (one env per process, bench.py:128-137, whose
+     fresh per-call frame arrays reuse the same freed block) */
   or_batch_job j = {(or_scene *)p, N, x, y, heading, path_len, collisions,
                     actions, radius, step, turn_rad, sensor_h, focal, max_range,
-                    W, H, depth, rgb, sem, 0};
+                    W, H, depth, rgb, sem, 0, per_thread};
   if (nthreads < 1) nthreads = 1;
+  scratch_pool((or_scene *)p, nthreads, W);
   pthread_t *th = malloc(sizeof(pthread_t) * (size_t)nthreads);
-  for (int k = 1; k < nthreads; ++k) pthread_create(&th[k], NULL, batch_worker, &j);
-  batch_worker(&j);
+  or_batch_arg *args = malloc(sizeof(or_batch_arg) * (size_t)nthreads);
+  for (int k = 0; k < nthreads; ++k) {
+    args[k].j = &j;
+    args[k].tid = k;
+  }
+  for (int k = 1; k < nthreads; ++k) pthread_create(&th[k], NULL, batch_worker, &args[k]);
+  batch_worker(&args[0]);
   for (int k = 1; k < nthreads; ++k) pthread_join(th[k], NULL);
   free(th);
+  free(args);
 }

@@ -57,7 +57,8 @@ def _load():
     lib.or_column_directions.argtypes = [_D, _I64, _D, _P, _P]
     lib.or_gps_compass.argtypes = [_D, _D, _D, _D, _D, _D, _P, _P]
     lib.or_batch_step_render.argtypes = [_P, _I64, _P, _P, _P, _P, _P, _P, _D, _D, _D,
-                                         _D, _I64, _I64, _D, _D, _P, _P, _P, ctypes.c_int]
+                                         _D, _I64, _I64, _D, _D, _P, _P, _P, ctypes.c_int,
+                                         ctypes.c_int]
     return lib
 
 
@@ -159,13 +160,14 @@ class OracleScene:
 
     def batch_step_render(self, x, y, h, path, coll, actions, radius, forward_step,
                           turn_angle, sensor_height, width, height, focal, max_range,
-                          depth, rgb, sem, nthreads):
-        """CPU baseline: N envs step + render, nthreads workers."""
+                          depth, rgb, sem, nthreads, per_thread_frames=False):
+        """CPU baseline: N envs step + render, nthreads workers; frames one
+        per env, or (per_thread_frames) one per worker thread, reused."""
         lib().or_batch_step_render(self._h, len(x), _ptr(x), _ptr(y), _ptr(h), _ptr(path),
                                    _ptr(coll), _ptr(actions), radius, forward_step,
                                    math.radians(turn_angle), sensor_height, width, height,
                                    focal, max_range, _ptr(depth), _ptr(rgb), _ptr(sem),
-                                   int(nthreads))
+                                   int(nthreads), int(bool(per_thread_frames)))
 
 
 def wrap_angle(theta: float) -> float:

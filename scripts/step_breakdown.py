@@ -68,6 +68,8 @@ def main():
     run("forward_only", lambda k: sim.step(const[0]))
     run("turn_only", lambda k: sim.step(const[1]))
     run("stop_only", lambda k: sim.step(const[3]))
+    run("step_only_forward", lambda k: sim.step(const[0], render=False))
+    run("step_only_turn", lambda k: sim.step(const[1], render=False))
     print(json.dumps(out))
 
 

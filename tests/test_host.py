@@ -63,10 +63,18 @@ def test_host_sincos_matches_mpmath():
     mpmath.mp.prec = 200
     rng = np.random.default_rng(2)
     s, c = ctypes.c_double(), ctypes.c_double()
-    for x in rng.uniform(-math.pi, math.pi, 300):
+    # random headings, the table-reduction breakpoints j/64 and the midpoints
+    # between them (largest |t|), quadrant boundaries k pi/2, tiny and large
+    xs = np.concatenate([rng.uniform(-math.pi, math.pi, 4000),
+                         [j / 64 for j in range(-60, 61)], [(j + 0.5) / 64 for j in range(-60, 61)],
+                         [k * math.pi / 2 for k in range(-4, 5)],
+                         [math.nextafter(k * math.pi / 2, 9) for k in range(-4, 5)],
+                         rng.uniform(-1e-3, 1e-3, 200), rng.uniform(-100.0, 100.0, 300)])
+    for x in xs:
         lib.nv_host_sincos(float(x), ctypes.byref(s), ctypes.byref(c))
-        assert s.value == float(mpmath.sin(mpmath.mpf(float(x))))
-        assert c.value == float(mpmath.cos(mpmath.mpf(float(x))))
+        assert s.value == float(mpmath.sin(mpmath.mpf(float(x)))), x
+        assert c.value == float(mpmath.cos(mpmath.mpf(float(x)))), x
+    for _ in range(300):
         a, b = rng.uniform(-0.3, 0.3, 2)
         h = lib.nv_host_hypot(float(a), float(b))
         assert h == float(mpmath.sqrt(mpmath.mpf(float(a)) ** 2 + mpmath.mpf(float(b)) ** 2))
