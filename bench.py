@@ -137,8 +137,11 @@ def measured_peaks():
 # --------------------------------------------------------------- CPU baseline
 
 def cpu_baseline(cfg: str, seconds: float = 10.0, threads: int | None = None, n_envs=None):
-    """The reference's CPU path (oracle port of Simulator.step + observations,
-    f64 frames like fill_frame) on the host cores, time-bounded sample."""
+    """The reference's CPU path on the host cores, run like the reference's own
+    harness (src/bench.py:128-177): ``threads`` workers, each stepping one env
+    (Simulator.step + observations, f64 frames like fill_frame) for a bounded
+    time, released by a barrier; aggregate frames/s = sum(frames) / (max end -
+    min start).  The C port of the path (oracle/navsim_oracle.c)."""
     from oracle import oracle
     from paper_1904_01201_b200 import synth
     N_cfg, W, H, chans, scene_key = CONFIGS[cfg]
@@ -146,36 +149,19 @@ def cpu_baseline(cfg: str, seconds: float = 10.0, threads: int | None = None, n_
     sc = synth.config_scene(scene_key)
     osc = oracle.OracleScene(sc.segments, sc.semantic_ids, sc.albedo, sc.wall_height,
                              sc.floor_color, sc.ceiling_color)
-    n = n_envs or max(1, min(N_cfg, 4 * threads))
+    # starts / action columns as scripts/ref_anchor.py gives the unmodified
+    # reference's workers: worker w steps env w % 64
+    n = n_envs or max(1, min(N_cfg, 64))
     poses = synth.sample_poses(sc, n, seed=1)
-    x, y = poses[:, 0].copy(), poses[:, 1].copy()
-    h = np.array([oracle.wrap_angle(v) for v in poses[:, 2]])
-    path = np.zeros(n)
-    coll = np.zeros(n, dtype=np.int64)
-    # one frame per worker thread, reused for every env it steps: the
-    # reference's bench workers each step one env and discard its frames
-    # (bench.py:128-137), so a worker's frame arrays stay cache-resident
-    depth = np.empty((threads, H, W)) if "depth" in chans else None
-    rgb = np.empty((threads, H, W, 3)) if "rgb" in chans else None
-    sem = np.empty((threads, H, W), dtype=np.uint16) if "semantic" in chans else None
+    acts = synth.random_actions(n, 4096, seed=2)
     focal = (W * 0.5) / math.tan(math.radians(90.0) * 0.5)
-    acts = synth.random_actions(n, 10_000, seed=2)
-    frames, steps, t0 = 0, 0, time.perf_counter()
-    osc.batch_step_render(x, y, h, path, coll, acts[0], 0.1, 0.25, 10.0, 1.5, W, H, focal, 10.0,
-                          depth, rgb, sem, threads, per_thread_frames=True)  # warm-up
-    t0 = time.perf_counter()
-    while True:
-        osc.batch_step_render(x, y, h, path, coll, acts[(steps + 1) % len(acts)], 0.1, 0.25, 10.0,
-                              1.5, W, H, focal, 10.0, depth, rgb, sem, threads,
-                              per_thread_frames=True)
-        steps += 1
-        frames += n
-        el = time.perf_counter() - t0
-        if el >= seconds:
-            break
-    return {"value": frames / el, "unit": "frames/s", "cores": threads, "kind": "port",
+    # warm-up (page-in, caches), then the timed cell
+    oracle.bench_cell(osc, poses, acts, W, H, focal, chans, threads, min(1.0, seconds / 10))
+    fps, frames = oracle.bench_cell(osc, poses, acts, W, H, focal, chans, threads, seconds)
+    return {"value": fps, "unit": "frames/s", "cores": threads, "kind": "port",
             "envs": n,
-            "sample": f"{n} envs x {steps} steps of {WORKLOAD[cfg]} ({el:.1f} s, "
+            "sample": f"{threads} workers x 1 env each, {frames} frames in {seconds:.1f} s of "
+                      f"{WORKLOAD[cfg]} (the reference harness's worker cell, bench.py:128-177; "
                       f"oracle/navsim_oracle.c, f64 frames like the reference)",
             "cpu_model": _cpu_model()}
 

@@ -851,3 +851,105 @@ void or_batch_step_render(void *p, int64_t N, double *x, double *y,
   free(th);
   free(args);
 }
+
+/* ---------------------------------------------- CPU baseline harness (bench)
+ * The reference harness's cell (bench.py:128-177): `nthreads` workers, each
+ * stepping ONE env (its own start pose, its own column of the action table)
+ * with Simulator.step + observations for `seconds`, rendering into its own
+ * reused frame, released together by a barrier; aggregate frames/s =
+ * sum(frames) / (max end - min start) (bench.py:170-174).  Threads stand in
+ * for the harness's forked processes (no shared mutable state). */
+#include <time.h>
+
+typedef struct {
+  or_scene *s;
+  int64_t N, n_steps;
+  const double *x0, *y0, *h0;
+  const int8_t *actions; /* n_steps x N */
+  double radius, step, turn_rad, sensor_h, focal, max_range, seconds;
+  int64_t W, H;
+  int want_rgb, want_depth, want_sem;
+  pthread_barrier_t bar;
+} or_cell_job;
+
+typedef struct {
+  or_cell_job *j;
+  int64_t wid;
+  double t0, t1;
+  int64_t frames;
+} or_cell_arg;
+
+static double now_s(void) {
+  struct timespec ts;
+  clock_gettime(CLOCK_MONOTONIC, &ts);
+  return (double)ts.tv_sec + 1e-9 * (double)ts.tv_nsec;
+}
+
+static void *cell_worker(void *arg) {
+  or_cell_arg *w = (or_cell_arg *)arg;
+  or_cell_job *j = w->j;
+  or_scene *s = j->s;
+  size_t nn = (size_t)(s->n > 0 ? s->n : 1);
+  size_t px = (size_t)(j->W * j->H);
+  uint8_t *mark = calloc(nn, 1);
+  int64_t *cand = malloc(nn * 8);
+  double *scratch = malloc(sizeof(double) * 4 * (size_t)j->W);
+  int64_t *isc = malloc(sizeof(int64_t) * (size_t)j->W);
+  double *depth = j->want_depth ? malloc(sizeof(double) * px) : NULL;
+  double *rgb = j->want_rgb ? malloc(sizeof(double) * 3 * px) : NULL;
+  uint16_t *sem = j->want_sem ? malloc(sizeof(uint16_t) * px) : NULL;
+  const int64_t e = w->wid % j->N;
+  or_agent a = {j->x0[e], j->y0[e], or_wrap_angle(j->h0[e]), 0.0, 0};
+  pthread_barrier_wait(&j->bar);
+  w->t0 = now_s();
+  int64_t k = 0;
+  for (;; ++k) {
+    const int act = j->actions[(k % j->n_steps) * j->N + e];
+    double moved;
+    if (act == 0)
+      scene_forward(s, &a, j->radius, j->step, mark, cand, &moved);
+    else if (act == 1)
+      a.heading = or_wrap_angle(a.heading + j->turn_rad);
+    else if (act == 2)
+      a.heading = or_wrap_angle(a.heading + (-j->turn_rad));
+    scene_render(s, a.x, a.y, a.heading, j->sensor_h, j->W, j->H, j->focal, j->max_range, 1e9,
+                 0, scratch, isc, depth, rgb, sem);
+    if ((k & 7) == 7 && now_s() - w->t0 >= j->seconds) break;
+  }
+  w->t1 = now_s();
+  w->frames = k + 1;
+  free(mark); free(cand); free(scratch); free(isc); free(depth); free(rgb); free(sem);
+  return NULL;
+}
+
+double or_bench_cell(void *p, int64_t N, const double *x0, const double *y0, const double *h0,
+                     const int8_t *actions, int64_t n_steps, double radius, double step,
+                     double turn_rad, double sensor_h, int64_t W, int64_t H, double focal,
+                     double max_range, int want_rgb, int want_depth, int want_sem,
+                     int nthreads, double seconds, int64_t *frames_out) {
+  if (nthreads < 1) nthreads = 1;
+  or_cell_job j = {(or_scene *)p, N, n_steps, x0, y0, h0, actions, radius, step, turn_rad,
+                   sensor_h, focal, max_range, seconds, W, H, want_rgb, want_depth, want_sem};
+  pthread_barrier_init(&j.bar, NULL, (unsigned)nthreads);
+  pthread_t *th = malloc(sizeof(pthread_t) * (size_t)nthreads);
+  or_cell_arg *args = calloc((size_t)nthreads, sizeof(or_cell_arg));
+  for (int k = 0; k < nthreads; ++k) {
+    args[k].j = &j;
+    args[k].wid = k;
+  }
+  for (int k = 1; k < nthreads; ++k) pthread_create(&th[k], NULL, cell_worker, &args[k]);
+  cell_worker(&args[0]);
+  for (int k = 1; k < nthreads; ++k) pthread_join(th[k], NULL);
+  double t0 = args[0].t0, t1 = args[0].t1;
+  int64_t frames = 0;
+  for (int k = 0; k < nthreads; ++k) {
+    if (args[k].t0 < t0) t0 = args[k].t0;
+    if (args[k].t1 > t1) t1 = args[k].t1;
+    frames += args[k].frames;
+  }
+  pthread_barrier_destroy(&j.bar);
+  free(th);
+  free(args);
+  if (frames_out) *frames_out = frames;
+  return (double)frames / (t1 - t0);
+}

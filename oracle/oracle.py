@@ -59,6 +59,10 @@ def _load():
     lib.or_batch_step_render.argtypes = [_P, _I64, _P, _P, _P, _P, _P, _P, _D, _D, _D,
                                          _D, _I64, _I64, _D, _D, _P, _P, _P, ctypes.c_int,
                                          ctypes.c_int]
+    lib.or_bench_cell.restype = _D
+    lib.or_bench_cell.argtypes = [_P, _I64, _P, _P, _P, _P, _I64, _D, _D, _D, _D, _I64, _I64, _D,
+                                  _D, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, _D,
+                                  _P]
     return lib
 
 
@@ -168,6 +172,27 @@ class OracleScene:
                                    math.radians(turn_angle), sensor_height, width, height,
                                    focal, max_range, _ptr(depth), _ptr(rgb), _ptr(sem),
                                    int(nthreads), int(bool(per_thread_frames)))
+
+
+def bench_cell(scene: "OracleScene", poses, actions, width, height, focal, channels, threads,
+               seconds, radius=0.1, forward_step=0.25, turn_angle=10.0, sensor_height=1.5,
+               max_range=10.0):
+    """The reference harness's cell (src/bench.py:128-177) on the C port:
+    ``threads`` workers, one env each (start pose poses[w % N], actions
+    column w % N of the (steps, N) table, cycled), Simulator.step + render
+    for ``seconds``; returns (aggregate frames/s = sum(frames) / (max end -
+    min start), frames)."""
+    poses = np.ascontiguousarray(np.asarray(poses, dtype=np.float64))
+    acts = np.ascontiguousarray(np.asarray(actions, dtype=np.int8))
+    x0, y0, h0 = (np.ascontiguousarray(poses[:, k]) for k in range(3))
+    frames = np.zeros(1, dtype=np.int64)
+    fps = lib().or_bench_cell(scene._h, len(poses), _ptr(x0), _ptr(y0), _ptr(h0), _ptr(acts),
+                              acts.shape[0], radius, forward_step, math.radians(turn_angle),
+                              sensor_height, width, height, focal, max_range,
+                              int("rgb" in channels), int("depth" in channels),
+                              int("semantic" in channels), int(threads), float(seconds),
+                              _ptr(frames))
+    return fps, int(frames[0])
 
 
 def wrap_angle(theta: float) -> float:
