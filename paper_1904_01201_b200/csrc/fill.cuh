@@ -397,8 +397,16 @@ struct FillWsLayout {  // byte offsets into dynamic shared memory + ring geometr
                      // balances CTAs when envs per CTA is small
 };
 
+#ifndef NV_FILL_MAXREG
+#define NV_FILL_MAXREG 0  // > 0: register cap of the ws writer (room for co-resident cast CTAs)
+#endif
+#if NV_FILL_MAXREG > 0
+#define NV_FILL_BOUNDS __maxnreg__(NV_FILL_MAXREG)
+#else
+#define NV_FILL_BOUNDS __launch_bounds__(544, 1)
+#endif
 template <int CPL, bool TAB, int RPW, bool NOISE, bool BANDED>
-__global__ void __launch_bounds__(544, 1) k_fill_ws(FillArgs a, FillWsLayout L) {
+__global__ void NV_FILL_BOUNDS k_fill_ws(FillArgs a, FillWsLayout L) {
   extern __shared__ __align__(128) uint8_t smem[];
   using Ln = Lanes<CPL>;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;

@@ -393,7 +393,10 @@ int build_camera_tables(nv_ctx *c, Camera &cam, double cam_h) {
 }
 
 // Record order used by the fast fill writers for a frame width (rec_pos).
-int fast_cpl(int W) { return W % 256 == 0 ? 8 : (W == 128 ? 4 : (W == 64 ? 2 : 0)); }
+#ifndef NV_CPL256
+#define NV_CPL256 8  // columns per lane of the ws writer for W a multiple of 256 (8 or 4)
+#endif
+int fast_cpl(int W) { return W % 256 == 0 ? NV_CPL256 : (W == 128 ? 4 : (W == 64 ? 2 : 0)); }
 
 // Column-record planes of N envs in the camera's record buffer (A then B).
 RecOut rec_out(Camera &cam, int64_t N) {
@@ -586,7 +589,7 @@ int launch_fill(nv_ctx *c, Camera &cam, int64_t N, uint8_t *rgb, float *depth, u
   // kernel; both produce identical frames.  The ws writer applies the depth
   // noise itself, the per-pixel kernel gets a pass.
   if (c->fill_mode != NV_FILL_GENERIC && ws_layout_ok(cam, rgb, depth, sem)) {
-    if (cam.W % 256 == 0) return launch_fill_ws<8>(c, a, st);
+    if (cam.W % 256 == 0) return launch_fill_ws<NV_CPL256>(c, a, st);
     if (cam.W == 128) return launch_fill_ws<4>(c, a, st);
     return launch_fill_ws<2>(c, a, st);
   }
