@@ -104,7 +104,9 @@ def load():
             "`python -c 'import __graft_entry__ as g; g.build()'`")
     lib = ctypes.CDLL(LIB_PATH)
     for name, (res, args) in SIGNATURES.items():
-        fn = getattr(lib, name)
+        fn = getattr(lib, name, None)
+        if fn is None:  # an older study build (NAVSIM_B200_LIB); tests check the shipped one
+            continue
         fn.restype = res
         fn.argtypes = args
     _lib = lib
