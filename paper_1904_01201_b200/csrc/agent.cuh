@@ -147,11 +147,13 @@ __global__ void __launch_bounds__(128) k_agent_step(EnvView ev, SceneView sc, Ag
 __device__ __forceinline__ void wait_envs_ready(unsigned *ready, unsigned *arrive, int W,
                                                 long long n_rays, int rays_per_block = 0,
                                                 long long block = -1) {
-  const int rpb = rays_per_block > 0 ? rays_per_block : (int)blockDim.x;
-  const long long blk = block >= 0 ? block : (long long)blockIdx.x;
-  const long long r0 = blk * rpb;
-  const long long r1 = min(n_rays, r0 + rpb) - 1;
-  const int e0 = (int)(r0 / W), e1 = (int)(r1 / W);
+  const unsigned rpb = rays_per_block > 0 ? (unsigned)rays_per_block : blockDim.x;
+  const unsigned blk = block >= 0 ? (unsigned)block : blockIdx.x;
+  // 32-bit arithmetic: the ray count of a batch fits (n_envs * W < 2^32)
+  const unsigned r0 = blk * rpb;
+  const unsigned r1 = (unsigned)min(n_rays, (long long)r0 + rpb) - 1u;
+  const unsigned w = (unsigned)W;
+  const int e0 = (int)(r0 / w), e1 = (int)(r1 / w);
   if (threadIdx.x == 0) {
     for (int e = e0; e <= e1; ++e) {
       unsigned v;
@@ -165,8 +167,8 @@ __device__ __forceinline__ void wait_envs_ready(unsigned *ready, unsigned *arriv
   if (threadIdx.x == 0) {
     for (int e = e0; e <= e1; ++e) {
       // CTAs that cover env e: blocks [first, last] of its ray range
-      const long long f = (long long)e * W / rpb, l = ((long long)(e + 1) * W - 1) / rpb;
-      if (atomicAdd(arrive + e, 1u) == (unsigned)(l - f)) {
+      const unsigned f = (unsigned)e * w / rpb, l = ((unsigned)(e + 1) * w - 1u) / rpb;
+      if (atomicAdd(arrive + e, 1u) == l - f) {
         arrive[e] = 0;
         ready[e] = 0;
       }

@@ -130,7 +130,7 @@ __device__ __forceinline__ void test_cell_f32(const SceneView &sc, int q0, int q
   for (int q = q0; q < q1; q += NB) {
     float4 e[NB];
 #pragma unroll
-    for (int k = 0; k < NB; ++k) e[k] = __ldg(sc.entf + min(q + k, q1 - 1));
+    for (int k = 0; k < NB; ++k) e[k] = __ldg(sc.entf + (unsigned)min(q + k, q1 - 1));
     unsigned keep = 0;
 #pragma unroll
     for (int k = 0; k < NB; ++k) {
@@ -142,7 +142,7 @@ __device__ __forceinline__ void test_cell_f32(const SceneView &sc, int q0, int q
     while (keep) {
       const int k = __ffs(keep) - 1;
       keep &= keep - 1;
-      const int qq = min(q + k, q1 - 1);
+      const unsigned qq = (unsigned)min(q + k, q1 - 1);
       const double2 *p2 = reinterpret_cast<const double2 *>(sc.ent + qq);
       const double2 a2 = __ldg(p2), e2 = __ldg(p2 + 1);
       double den, tn, rn;
@@ -166,7 +166,8 @@ __device__ __forceinline__ void test_cell_f32(const SceneView &sc, int q0, int q
 #endif
 // The tests of one DDA cell (record `rec`) for a ray: run boxes, f32 side
 // tests, exact FP64 tests of the survivors; updates (best_t, best_i).
-__device__ __forceinline__ void cell_tests(const SceneView &sc, long long cx, long long cy,
+template <typename IT>
+__device__ __forceinline__ void cell_tests(const SceneView &sc, IT cx, IT cy,
                                            const int4 &rec, double px, double py, double dx,
                                            double dy, float dxf, float dyf, float sd,
                                            bool pos_dx, bool pos_dy, double &best_t,
@@ -189,7 +190,8 @@ __device__ __forceinline__ void cell_tests(const SceneView &sc, long long cx, lo
     for (int c0 = 0; c0 < nch; c0 += NV_CAST_NCB) {
       float4 bb[NV_CAST_NCB];
 #pragma unroll
-      for (int k = 0; k < NV_CAST_NCB; ++k) bb[k] = __ldg(sc.chunks + rec.w + min(c0 + k, nch - 1));
+      for (int k = 0; k < NV_CAST_NCB; ++k)
+        bb[k] = __ldg(sc.chunks + (unsigned)(rec.w + min(c0 + k, nch - 1)));
       unsigned pass = 0;
 #pragma unroll
       for (int k = 0; k < NV_CAST_NCB; ++k) {
@@ -200,7 +202,7 @@ __device__ __forceinline__ void cell_tests(const SceneView &sc, long long cx, lo
         pass |= (ok ? 1u : 0u) << k;
       }
       for (unsigned m = pass; m; m &= m - 1) {  // prefetch first, then test
-        const int q = rec.x + (c0 + __ffs(m) - 1) * NV_CHUNK;
+        const unsigned q = (unsigned)(rec.x + (c0 + __ffs(m) - 1) * NV_CHUNK);
         const char *p = reinterpret_cast<const char *>(sc.ent + q);
         asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
         asm volatile("prefetch.global.L1 [%0];" ::"l"(p + 128));
@@ -222,24 +224,19 @@ __device__ __forceinline__ void cell_tests(const SceneView &sc, long long cx, lo
 // The walk is software-pipelined: the next cell's record {q0, q1, bound} is
 // loaded (one 16-byte load) before the current cell's entries are tested, so
 // the cell-to-cell latency overlaps the tests; the visit order and the
-// early-out are the reference's.
-__device__ __forceinline__ void ray_grid(const SceneView &sc, double px, double py,
-                                         double dx, double dy, double t_max,
-                                         double &out_t, int &out_i) {
+// early-out are the reference's.  IT: the cell-coordinate type (32-bit: the
+// start cell lies within +-2^30 cells of the grid origin, see ray_grid).
+template <typename IT>
+__device__ __forceinline__ void ray_grid_walk(const SceneView &sc, double px, double py,
+                                              double dx, double dy, double t_max, IT cx, IT cy,
+                                              double &out_t, int &out_i) {
   const double cell = 1.0;
   double best_t = NV_INF;
   int best_i = -1;
-  if (isnan(px) || isnan(py) || isnan(dx) || isnan(dy)) {  // reference would spin
-    out_t = best_t;
-    out_i = best_i;
-    return;
-  }
-  // (p - x0) / cell with cell = 1.0 is exact without the division
-  long long cx = (long long)floor(sub(px, sc.x0));
-  long long cy = (long long)floor(sub(py, sc.y0));
   const int stepx = dx > 0.0 ? 1 : -1;
   const int stepy = dy > 0.0 ? 1 : -1;
   double tnx, tdx, tny, tdy;
+  // |cell / d| = |RN(1 / d)|: the correctly rounded reciprocal is the same value
   if (dx != 0.0) {
     double nbx = add(sc.x0, mul((double)(cx + (dx > 0.0 ? 1 : 0)), cell));
     tnx = div(sub(nbx, px), dx);
@@ -256,18 +253,20 @@ __device__ __forceinline__ void ray_grid(const SceneView &sc, double px, double 
     tny = NV_INF;
     tdy = NV_INF;
   }
-  const long long gnx = sc.gnx, gny = sc.gny;
+  const IT gnx = sc.gnx, gny = sc.gny;
   const float dxf = (float)dx, dyf = (float)dy;
   const float sd = (fabsf(dxf) + fabsf(dyf)) * (1.0f + 0x1p-20f);
   const bool pos_dx = dxf >= 0.0f, pos_dy = dyf >= 0.0f;
-  (void)pos_dx; (void)pos_dy;
-  auto inb = [&](long long x, long long y) { return 0 <= x && x < gnx && 0 <= y && y < gny; };
+  auto inb = [&](IT x, IT y) { return 0 <= x && x < gnx && 0 <= y && y < gny; };
+  auto cell_rec = [&](IT x, IT y) {
+    return __ldg(sc.cells + (unsigned)((int)y * sc.gnx + (int)x));  // in the grid: < 2^31
+  };
   int4 rec = make_int4(0, 0, 0, 0);
-  if (inb(cx, cy)) rec = __ldg(sc.cells + (cy * gnx + cx));
+  if (inb(cx, cy)) rec = cell_rec(cx, cy);
   for (int guard = 0; guard < (1 << 24); ++guard) {
     const double t_exit = tnx < tny ? tnx : tny;
     // the cell after this one (the reference advances to it unless it stops)
-    long long ncx = cx, ncy = cy;
+    IT ncx = cx, ncy = cy;
     double ntnx = tnx, ntny = tny;
     if (tnx < tny) {
       ncx += stepx;
@@ -277,8 +276,8 @@ __device__ __forceinline__ void ray_grid(const SceneView &sc, double px, double 
       ntny = add(tny, tdy);
     }
     int4 nrec = make_int4(0, 0, 0, 0);
-    if (!(t_exit > t_max) && inb(ncx, ncy)) nrec = __ldg(sc.cells + (ncy * gnx + ncx));
-    cell_tests(sc, cx, cy, rec, px, py, dx, dy, dxf, dyf, sd, pos_dx, pos_dy, best_t, best_i);
+    if (!(t_exit > t_max) && inb(ncx, ncy)) nrec = cell_rec(ncx, ncy);
+    cell_tests<IT>(sc, cx, cy, rec, px, py, dx, dy, dxf, dyf, sd, pos_dx, pos_dy, best_t, best_i);
     if (best_t <= t_exit || t_exit > t_max) break;
 #if NV_CAST_PF_NEXT
     if (nrec.y > nrec.x) {  // the next cell's run boxes and first entries -> L1
@@ -299,6 +298,26 @@ __device__ __forceinline__ void ray_grid(const SceneView &sc, double px, double 
   }
   out_t = best_t;
   out_i = best_i;
+}
+
+__device__ __forceinline__ void ray_grid(const SceneView &sc, double px, double py,
+                                         double dx, double dy, double t_max,
+                                         double &out_t, int &out_i) {
+  if (isnan(px) || isnan(py) || isnan(dx) || isnan(dy)) {  // reference would spin
+    out_t = NV_INF;
+    out_i = -1;
+    return;
+  }
+  // (p - x0) / cell with cell = 1.0 is exact without the division
+  const double fx = floor(sub(px, sc.x0)), fy = floor(sub(py, sc.y0));
+  if (!(fabs(fx) < 0x1p30 && fabs(fy) < 0x1p30)) {
+    // >= 2^30 cells from the grid origin: the walk's 2^24-step guard ends it
+    // long before it could reach a grid cell (grids are < 2^31 cells in all)
+    out_t = NV_INF;
+    out_i = -1;
+    return;
+  }
+  ray_grid_walk<int>(sc, px, py, dx, dy, t_max, (int)fx, (int)fy, out_t, out_i);
 }
 
 // raycast_all (_kernels.py:16-48)

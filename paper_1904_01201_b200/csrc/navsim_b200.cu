@@ -612,6 +612,9 @@ int cam_check(nv_ctx *c, int cam) {
     return fail(NV_ERR_STATE, "camera %d not configured (nv_camera_config)", cam);
   Camera &k = c->cams[cam];
   if (c->sensor_h > c->wall_h) return fail(NV_ERR_ARG, "sensor height must stay below wall height");
+  if (c->n_envs * (int64_t)k.W >= (1LL << 31))  // ray indices are 32-bit in the casts
+    return fail(NV_ERR_ARG, "n_envs * W = %lld rays per camera exceeds 2^31",
+                (long long)(c->n_envs * (int64_t)k.W));
   if (k.tables_cam_h != c->sensor_h) TRY(build_camera_tables(c, k, c->sensor_h));
   TRY(k.rec.alloc(sizeof(ColRec) * (size_t)std::max<int64_t>(1, c->n_envs) * k.W));
   return NV_OK;
