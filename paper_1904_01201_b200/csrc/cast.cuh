@@ -149,10 +149,10 @@ __device__ __forceinline__ void ray_grid_warp(const SceneView &sc, double px, do
         const float cp = fmaf(dxf, pyr, -(dyf * pxr));
         const float E = NV_K32 * sd * (__int_as_float(rec.z) + fabsf(pxr) + fabsf(pyr) + 1e-30f);
         for (int q = rec.x + lane; q < rec.y; q += 32) {
-          const float4 e = __ldg(sc.entf + q);
-          const float sa = fmaf(dxf, e.y, -(dyf * e.x)) - cp;
-          const float sb = fmaf(dxf, e.w, -(dyf * e.z)) - cp;
-          if (fminf(sa, sb) > E || fmaxf(sa, sb) < -E) continue;
+          const float4 e = __ldg(sc.entm + q);  // side test as in test_cell_f32
+          const float sm = fmaf(dxf, e.y, -(dyf * e.x)) - cp;
+          const float sh = fmaf(dxf, e.w, -(dyf * e.z));
+          if (fabsf(sm) > fabsf(sh) + E) continue;
           const double2 *p2 = reinterpret_cast<const double2 *>(sc.ent + q);
           const double2 a2 = __ldg(p2), e2 = __ldg(p2 + 1);
           double den, tn, rn;

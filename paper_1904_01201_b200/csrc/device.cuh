@@ -50,8 +50,10 @@ struct SceneView {
   const CellEntry *ent;  // starts[nc] entries
   const int32_t *items;  // same order, index only (disc casts)
   const float4 *entf;    // same order, f32 endpoints (a - X0c, b - X0c), X0c = x0 + cx
+  const float4 *entm;    // same order, f32 midpoint and half-vector (m - X0c, (b - a) / 2)
   const int4 *cells;     // per cell: {starts[c], starts[c+1], bits(bound), first chunk}
-  const float4 *chunks;  // per run of NV_CHUNK entries: f32 box (x0, y0, x1, y1), cell-relative
+  const float4 *chunks;  // per run of NV_CHUNK entries: f32 box as centre and half-extents
+                         // (xc, yc, hx, hy), cell-relative, containing every endpoint
   const DiscEntry *dent; // per entry (same order as items): disc-cast record
   const double *stx, *sty;  // per segment: unit tangent (ex, ey) / seg_len (0 if degenerate)
   double x0, y0;

@@ -107,17 +107,22 @@ __device__ __forceinline__ void seg_test(double px, double py, double dx, double
 // r = rn/den = s_a / (s_a - s_b), so both s_a, s_b > 0 (or both < 0) means
 // r < 0 or r > 1 (or den == 0) and the reference skips the segment.
 // Entries are stored in f32 relative to the cell anchor (X0c, Y0c) =
-// (x0 + cx, y0 + cy); the ray origin is rebased to the same anchor in f64
-// and rounded once.  E = 2^-18 |d|_1 (A + |p_rel|_1) bounds the f32 error of
-// s_a, s_b (conversions, products, sums; ~8x over the worst case) and the
-// reference's own f64 rounding, so a segment is skipped only when it is
-// certain that the reference skips it.  Survivors -- the segments the ray's
-// line actually crosses, plus a hairline margin -- take the exact FP64 test,
-// so the result is bit-identical to the unfiltered DDA.
+// (x0 + cx, y0 + cy) as midpoint m and half-vector h (a = m - h, b = m + h,
+// each within 2^-23 A of the stored f32 endpoints); the ray origin is rebased
+// to the same anchor in f64 and rounded once.  Then s_a, s_b = s_m -+ s_h with
+// s_m = d x (m - p), s_h = d x h, and both lie strictly on one side iff
+// |s_m| > |s_h|: the entry is skipped when |s_m| > |s_h| + E.
+// E = 2^-18 |d|_1 (A + |p_rel|_1) bounds the f32 error of these sums
+// (conversions, products, sums, the midpoint form; > 4x over the worst case)
+// and the reference's own f64 rounding, so a segment is skipped only when it
+// is certain that the reference skips it.  Survivors -- the segments the
+// ray's line actually crosses, plus a hairline margin -- take the exact FP64
+// test, so the result is bit-identical to the unfiltered DDA.
 #define NV_K32 0x1p-18f
 
 struct CellF {
   float cp, E;  // d x p_rel, error bound
+  float adx, ady;  // |d| components (box half-extent term)
 };
 
 // Tests the bucket run [q0, q1) of one cell: NB f32 side tests per round
@@ -130,13 +135,13 @@ __device__ __forceinline__ void test_cell_f32(const SceneView &sc, int q0, int q
   for (int q = q0; q < q1; q += NB) {
     float4 e[NB];
 #pragma unroll
-    for (int k = 0; k < NB; ++k) e[k] = __ldg(sc.entf + (unsigned)min(q + k, q1 - 1));
+    for (int k = 0; k < NB; ++k) e[k] = __ldg(sc.entm + (unsigned)min(q + k, q1 - 1));
     unsigned keep = 0;
 #pragma unroll
     for (int k = 0; k < NB; ++k) {
-      const float sa = fmaf(dxf, e[k].y, -(dyf * e[k].x)) - cf.cp;
-      const float sb = fmaf(dxf, e[k].w, -(dyf * e[k].z)) - cf.cp;
-      const bool skip = fminf(sa, sb) > cf.E || fmaxf(sa, sb) < -cf.E;
+      const float sm = fmaf(dxf, e[k].y, -(dyf * e[k].x)) - cf.cp;
+      const float sh = fmaf(dxf, e[k].w, -(dyf * e[k].z));
+      const bool skip = fabsf(sm) > fabsf(sh) + cf.E;
       keep |= (skip ? 0u : 1u) << k;
     }
     while (keep) {
@@ -178,14 +183,16 @@ __device__ __forceinline__ void cell_tests(const SceneView &sc, IT cx, IT cy,
     CellF cf;
     cf.cp = fmaf(dxf, pyr, -(dyf * pxr));
     cf.E = NV_K32 * sd * (__int_as_float(rec.z) + fabsf(pxr) + fabsf(pyr) + 1e-30f);
+    cf.adx = fabsf(dxf);
+    cf.ady = fabsf(dyf);
 #if NV_CAST_CHUNKS
-    // s(x, y) = d x ((x, y) - p) is linear, so over a run's box it is
-    // bounded by two corners; a run whose box lies beyond +-E on one side
-    // holds no entry the per-entry side test would keep.
-    // The boxes of up to NV_CAST_NCB runs are loaded together (one memory
-    // round trip per cell in the common case); a passing run's f64 entries
-    // are prefetched into L1 before its f32 side tests, so the exact tests
-    // of its survivors hit L1.
+    // s(x, y) = d x ((x, y) - p) is linear, so over a run's box (centre c,
+    // half-extents h) it spans s(c) +- (|dx| h_y + |dy| h_x); a run whose box
+    // lies beyond +-E on one side holds no entry the per-entry side test
+    // would keep.  The boxes of up to NV_CAST_NCB runs are loaded together
+    // (one memory round trip per cell in the common case); a passing run's
+    // f64 entries are prefetched into L1 before its f32 side tests, so the
+    // exact tests of its survivors hit L1.
     const int nch = (rec.y - rec.x + NV_CHUNK - 1) / NV_CHUNK;
     for (int c0 = 0; c0 < nch; c0 += NV_CAST_NCB) {
       float4 bb[NV_CAST_NCB];
@@ -196,9 +203,9 @@ __device__ __forceinline__ void cell_tests(const SceneView &sc, IT cx, IT cy,
 #pragma unroll
       for (int k = 0; k < NV_CAST_NCB; ++k) {
         const float4 b = bb[k];
-        const float smin = fmaf(dxf, pos_dx ? b.y : b.w, -(dyf * (pos_dy ? b.z : b.x))) - cf.cp;
-        const float smax = fmaf(dxf, pos_dx ? b.w : b.y, -(dyf * (pos_dy ? b.x : b.z))) - cf.cp;
-        const bool ok = c0 + k < nch && !(smin > cf.E || smax < -cf.E);
+        const float sc_ = fmaf(dxf, b.y, -(dyf * b.x)) - cf.cp;
+        const float hr = fmaf(cf.adx, b.w, cf.ady * b.z);
+        const bool ok = c0 + k < nch && !(fabsf(sc_) > hr + cf.E);
         pass |= (ok ? 1u : 0u) << k;
       }
       for (unsigned m = pass; m; m &= m - 1) {  // prefetch first, then test

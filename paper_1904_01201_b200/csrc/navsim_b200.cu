@@ -152,7 +152,7 @@ struct nv_ctx {
   double gx0 = -0.5, gy0 = -0.5;
   int gnx = 1, gny = 1;
   int64_t nitems = 0;
-  DevBuf ax, ay, bx, by, ex, ey, nx, ny, sem, alb, starts, ent, items, entf, cells, chunks;
+  DevBuf ax, ay, bx, by, ex, ey, nx, ny, sem, alb, starts, ent, items, entf, entm, cells, chunks;
   DevBuf dent, stx, sty;
   // agent
   double radius = 0.1, step = 0.25, turn_rad = 0.17453292519943295, sensor_h = 1.5;
@@ -230,7 +230,7 @@ struct nv_ctx {
     v.nx = nx.as<double>(); v.ny = ny.as<double>();
     v.sem = sem.as<uint16_t>(); v.alb255 = alb.as<float4>();
     v.starts = starts.as<int32_t>(); v.ent = ent.as<CellEntry>(); v.items = items.as<int32_t>();
-    v.entf = entf.as<float4>(); v.cells = cells.as<int4>();
+    v.entf = entf.as<float4>(); v.entm = entm.as<float4>(); v.cells = cells.as<int4>();
     v.chunks = chunks.as<float4>();
     v.dent = dent.as<DiscEntry>(); v.stx = stx.as<double>(); v.sty = sty.as<double>();
     v.x0 = gx0; v.y0 = gy0; v.gnx = gnx; v.gny = gny; v.n = n;
@@ -827,7 +827,7 @@ int nv_scene_upload(nv_ctx *c, const double *segs, const uint16_t *sem, const do
   }
   std::vector<int32_t> starts(g.starts.size()), items(g.items.size());
   std::vector<CellEntry> ent(g.items.size());
-  std::vector<float4> entf(g.items.size());
+  std::vector<float4> entf(g.items.size()), entm(g.items.size());
   std::vector<float> cellb((size_t)(g.nx * g.ny), 0.f);
   for (size_t k = 0; k < g.starts.size(); ++k) starts[k] = (int32_t)g.starts[k];
   for (int64_t cy = 0; cy < g.ny; ++cy)
@@ -846,7 +846,14 @@ int nv_scene_upload(nv_ctx *c, const double *segs, const uint16_t *sem, const do
         float4 f = make_float4((float)(ax[i] - X0), (float)(ay[i] - Y0),
                                (float)(ax[i] + ex[i] - X0), (float)(ay[i] + ey[i] - Y0));
         entf[q] = f;
+        // midpoint / half-vector form of the same f32 endpoints (the cast's side test)
+        const float4 m = make_float4((float)(0.5 * ((double)f.x + (double)f.z)),
+                                     (float)(0.5 * ((double)f.y + (double)f.w)),
+                                     (float)(0.5 * ((double)f.z - (double)f.x)),
+                                     (float)(0.5 * ((double)f.w - (double)f.y)));
+        entm[q] = m;
         amax = std::max(amax, std::max(std::fabs(f.x) + std::fabs(f.y), std::fabs(f.z) + std::fabs(f.w)));
+        amax = std::max(amax, std::fabs(m.x) + std::fabs(m.z) + std::fabs(m.y) + std::fabs(m.w));
       }
       // 2^-20 relative slack covers the f32 rounding of the stored values
       cellb[c] = amax * (1.0f + 0x1p-20f);
@@ -856,10 +863,13 @@ int nv_scene_upload(nv_ctx *c, const double *segs, const uint16_t *sem, const do
   TRY(upload(c->sem, sm)); TRY(upload(c->alb, alb));
   TRY(upload(c->starts, starts)); TRY(upload(c->items, items)); TRY(upload(c->ent, ent));
   TRY(upload(c->entf, entf));
+  TRY(upload(c->entm, entm));
   // Per cell: runs of NV_CHUNK entries (bucket order) with the f32 bounding box
-  // of their cell-relative endpoints; the cast rejects a whole run when the
-  // ray's line passes the box on one side (kernels.cuh ray_grid).  The cell
-  // bound grows to cover the box corners, so one error bound E serves both.
+  // of their cell-relative endpoints, stored as centre + half-extents rounded
+  // outwards (the stored box contains every endpoint); the cast rejects a
+  // whole run when the ray's line passes the box on one side (geom.cuh
+  // cell_tests).  The cell bound grows to cover the box, so one error bound
+  // E serves both.
   std::vector<int4> cells((size_t)(g.nx * g.ny));
   std::vector<float4> chunks;
   for (size_t k = 0; k < cells.size(); ++k) {
@@ -875,9 +885,19 @@ int nv_scene_upload(nv_ctx *c, const double *segs, const uint16_t *sem, const do
         bx.z = std::max(bx.z, std::max(f.x, f.z));
         bx.w = std::max(bx.w, std::max(f.y, f.w));
       }
-      chunks.push_back(bx);
-      const float cb = std::max(std::fabs(bx.x), std::fabs(bx.z)) +
-                       std::max(std::fabs(bx.y), std::fabs(bx.w));
+      // centre (rounded) and half-extent (rounded up) so [c - h, c + h] covers [lo, hi]
+      auto centre_half = [](float lo, float hi, float &cc, float &hh) {
+        cc = (float)(0.5 * ((double)lo + (double)hi));
+        const double h = std::max((double)hi - (double)cc, (double)cc - (double)lo);
+        hh = (float)h;
+        if ((double)hh < h) hh = std::nextafter(hh, INFINITY);
+      };
+      float4 cm;
+      centre_half(bx.x, bx.z, cm.x, cm.z);
+      centre_half(bx.y, bx.w, cm.y, cm.w);
+      chunks.push_back(cm);
+      const float cb = std::max(std::max(std::fabs(bx.x), std::fabs(bx.z)), std::fabs(cm.x) + cm.z) +
+                       std::max(std::max(std::fabs(bx.y), std::fabs(bx.w)), std::fabs(cm.y) + cm.w);
       b = std::max(b, cb * (1.0f + 0x1p-20f));
     }
     int bi;
