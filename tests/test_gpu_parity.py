@@ -315,6 +315,52 @@ def test_raycast_stress_vs_oracle(nb, oracle_mod, cfg):
             assert np.array_equal(tg, to)
 
 
+@pytest.mark.parametrize("cfg", ["C2", "C3"])
+def test_raycast_prefilter_edges_vs_oracle(nb, oracle_mod, cfg):
+    """Cases aimed at the f32 prefilters' error margin and the DDA's integer
+    path: origins exactly on cell lines and outside the grid, rays aimed one
+    ulp either side of segment endpoints and along cell lines, and origins
+    far (>= 2^30 cells) from the grid -- bit-identical (t, idx) to the
+    oracle's raycast_grid."""
+    from paper_1904_01201_b200 import synth
+    sc = synth.config_scene(cfg)
+    osc = _oracle_scene(oracle_mod, sc)
+    idx = nb.SegmentIndex(sc.segments)
+    segs = sc.segments
+    rng = np.random.default_rng(5)
+    lo = segs[:, :2].min(0).tolist()
+    hi = segs[:, :2].max(0).tolist()
+    poses = synth.sample_poses(sc, 12, seed=123)
+    origins = []
+    for (x, y, _) in poses:
+        origins += [(x, y), (math.floor(x), y), (x, math.floor(y)), (math.floor(x), math.floor(y))]
+    origins += [(lo[0] - 3.25, 0.5 * (lo[1] + hi[1])), (0.5 * (lo[0] + hi[0]), hi[1] + 7.0)]
+    for (x, y) in origins:
+        near = segs[np.argsort(np.hypot(segs[:, 0] - x, segs[:, 1] - y))[:128]]
+        d = []
+        for end in (near[:, 0:2], near[:, 2:4]):
+            v = end - [x, y]
+            d += [v, np.nextafter(v, np.inf), np.nextafter(v, -np.inf),
+                  np.stack([np.nextafter(v[:, 0], np.inf), np.nextafter(v[:, 1], -np.inf)], 1)]
+        th = rng.uniform(-math.pi, math.pi, 256)
+        d.append(np.stack([np.cos(th), np.sin(th)], 1))
+        d.append(np.array([[1, 0], [0, 1], [-1, 0], [0, -1]], float))
+        d = np.concatenate(d)
+        d = d[np.hypot(d[:, 0], d[:, 1]) > 0]
+        for t_max in (1e9, 10.0):
+            tg, ig = idx.raycast((x, y), d, t_max=t_max)
+            to, io = osc.raycast((x, y), d, t_max=t_max)
+            assert np.array_equal(ig, io), (x, y, t_max)
+            assert np.array_equal(tg, to), (x, y, t_max)
+    # far from the grid (>= 2^30 cells): nothing is reachable
+    for (x, y) in ((2.0 ** 31, 0.5), (-3e12, 4.0), (10.0, 5e11)):
+        d = np.array([[1.0, 0.0], [-1.0, 0.0], [0.3, -0.9], [-0.7, 0.2]])
+        tg, ig = idx.raycast((x, y), d, t_max=10.0)
+        assert np.all(ig == -1) and np.all(np.isinf(tg))
+        to, io = osc.raycast((x, y), d, t_max=10.0)
+        assert np.array_equal(ig, io) and np.array_equal(tg, to)
+
+
 def _graph_from_golden(nb, g):
     walls = [nb.WallSegment(a=(s[0], s[1]), b=(s[2], s[3]), semantic_id=int(i),
                             albedo=tuple(float(c) for c in a))
