@@ -116,9 +116,13 @@ int nv_render(nv_ctx *ctx, int cam, uint8_t *rgb, float *depth, uint16_t *sem,
 
 /* Step + render: one call per simulator step for all envs -- nv_step then
  * nv_render for camera `cam`, enqueued as three launches on `stream`: the
- * agent step (k_agent_step, a warp per env), the column cast (a programmatic
- * dependent of the agent step that starts each env's rays as soon as its new
- * pose is published, see nv_set_overlap) and the frame writer (the
+ * agent step (k_agent_step, a warp per env; a programmatic dependent of the
+ * previous step's frame writer, which it never reads from -- consecutive
+ * renders alternate between two column-record buffers -- so it starts on
+ * the SMs the writer's tail leaves idle and completes after it), the column
+ * cast (a programmatic dependent of the agent step that starts each env's
+ * rays as soon as its new pose is published, see nv_set_overlap) and the
+ * frame writer (the
  * warp-specialised TMA writer k_fill_ws when the frame layout allows it:
  * W in {64, 128, 256k <= 4096}, whole 16-row slots, 16-byte aligned outputs;
  * else the per-pixel k_fill_generic). */

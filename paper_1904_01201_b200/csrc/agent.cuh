@@ -132,12 +132,16 @@ __global__ void __launch_bounds__(128) k_agent_step(EnvView ev, SceneView sc, Ag
                                                     unsigned *ready) {
   if (ready) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int e = (int)((blockIdx.x * (size_t)blockDim.x + threadIdx.x) >> 5);
-  if (e >= ev.n) return;
-  warp_agent_step(ev, sc, cfg, e, actions[e], collided_out, disp_out, status_out);
-  if (ready && (threadIdx.x & 31) == 0) {
-    __threadfence();
-    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(ready + e), "r"(1u) : "memory");
+  if (e < ev.n) {
+    warp_agent_step(ev, sc, cfg, e, actions[e], collided_out, disp_out, status_out);
+    if (ready && (threadIdx.x & 31) == 0) {
+      __threadfence();
+      asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(ready + e), "r"(1u) : "memory");
+    }
   }
+  // launched as a programmatic dependent of the previous frame writer: this
+  // grid completes only after it, so stream order still holds for what follows
+  asm volatile("griddepcontrol.wait;" ::: "memory");
 }
 
 // Cast side of the agent->cast overlap: thread 0 of a CTA waits for every env

@@ -254,6 +254,7 @@ __global__ void __launch_bounds__(128, NV_CASTW_MINB) k_column_cast_warp(EnvView
     __syncthreads();
     if (threadIdx.x == 0) cost[blk] = (unsigned)min(clock64() - t0, 0xffffffffLL);
   }
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // completes after the agent step
 }
 
 // One thread per (env, column).  With `ready`: launched as a programmatic
@@ -290,6 +291,7 @@ __global__ void __launch_bounds__(128, NV_CAST_KMINB) k_column_cast(EnvView ev, 
     __syncthreads();
     if (threadIdx.x == 0) cost[blk] = (unsigned)min(clock64() - t0, 0xffffffffLL);
   }
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // completes after the agent step
 }
 
 __global__ void k_lpt_init(unsigned *order, unsigned *cost, unsigned n) {

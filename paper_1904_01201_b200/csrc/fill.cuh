@@ -407,6 +407,9 @@ struct FillWsLayout {  // byte offsets into dynamic shared memory + ring geometr
 #endif
 template <int CPL, bool TAB, int RPW, bool NOISE, bool BANDED>
 __global__ void NV_FILL_BOUNDS k_fill_ws(FillArgs a, FillWsLayout L) {
+  // the next step's agent step (a programmatic dependent) may start on SMs
+  // this grid leaves: it touches none of the writer's inputs
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   extern __shared__ __align__(128) uint8_t smem[];
   using Ln = Lanes<CPL>;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;

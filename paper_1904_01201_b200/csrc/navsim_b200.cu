@@ -41,6 +41,9 @@ using namespace nvd;
 #ifndef NV_WS_NW
 #define NV_WS_NW 16  // producer warps of the ws writer (4 / 8 / 16)
 #endif
+#ifndef NV_STEP_CHAIN
+#define NV_STEP_CHAIN 1  // the agent step is a programmatic dependent of the previous frame writer
+#endif
 #ifndef NV_WS_SLOTS
 #define NV_WS_SLOTS 0  // ring slots of the ws writer (0: as many as fit, <= 4)
 #endif
@@ -127,7 +130,10 @@ struct Camera {
   float ktop = 0.f, kbot = 0.f;
   double tables_cam_h = NAN;
   DevBuf u, tc, tf, rows, invh;
-  DevBuf rec;      // ColRec N x W
+  DevBuf rec;      // ColRec, two halves of N x W (A then B planes each): consecutive
+                   // renders alternate (rec_flip), so a step's casts never write
+                   // the records the previous step's writer may still read
+  int rec_half = 0;
   DevBuf lpt_order, lpt_cost;  // thread-per-ray cast: block order (slowest first) + durations
   int64_t lpt_n = -1;           // blocks the order is valid for
   // The host-buffer step's own record buffer and block order (its frame
@@ -398,10 +404,14 @@ int build_camera_tables(nv_ctx *c, Camera &cam, double cam_h) {
 #endif
 int fast_cpl(int W) { return W % 256 == 0 ? NV_CPL256 : (W == 128 ? 4 : (W == 64 ? 2 : 0)); }
 
-// Column-record planes of N envs in the camera's record buffer (A then B).
+// A render's casts write the other half of the record buffer than the last one.
+void rec_flip(Camera &cam) { cam.rec_half ^= 1; }
+
+// Column-record planes of N envs in the current half of the camera's record
+// buffer (A then B).
 RecOut rec_out(Camera &cam, int64_t N) {
   RecOut r;
-  r.a = cam.rec.as<float4>();
+  r.a = cam.rec.as<float4>() + (size_t)cam.rec_half * (cam.rec.bytes / 2 / sizeof(float4));
   r.b = r.a + (size_t)N * cam.W;
   r.W = cam.W;
   r.cpl = fast_cpl(cam.W);
@@ -616,7 +626,7 @@ int cam_check(nv_ctx *c, int cam) {
     return fail(NV_ERR_ARG, "n_envs * W = %lld rays per camera exceeds 2^31",
                 (long long)(c->n_envs * (int64_t)k.W));
   if (k.tables_cam_h != c->sensor_h) TRY(build_camera_tables(c, k, c->sensor_h));
-  TRY(k.rec.alloc(sizeof(ColRec) * (size_t)std::max<int64_t>(1, c->n_envs) * k.W));
+  TRY(k.rec.alloc(2 * sizeof(ColRec) * (size_t)std::max<int64_t>(1, c->n_envs) * k.W));
   return NV_OK;
 }
 
@@ -673,6 +683,7 @@ int do_cast(nv_ctx *c, int cam, double *gps, double *compass, cudaStream_t st) {
   const long long total = c->n_envs * (long long)k.W;
   const bool warp = use_warp_cast(c, total);
   const unsigned nblk = cast_blocks(c, total);
+  rec_flip(k);
   const unsigned threads = warp ? 128u : (unsigned)NV_CAST_BLOCK;
   unsigned *order = nullptr, *cost = nullptr;
   if (NV_CAST_LPT && lpt_pays(c, nblk)) {
@@ -737,9 +748,22 @@ int do_step(nv_ctx *c, const int8_t *actions, uint8_t *collided, double *disp, i
     ready = c->pdl_ready.as<unsigned>();
   }
   Prof pf(c, st, 0);
-  nvk::k_agent_step<<<blocks_for(threads, 128), 128, 0, st>>>(c->env_view(), c->scene_view(), cfg,
-                                                               actions, collided, disp, status,
-                                                               ready);
+  {
+    // a programmatic dependent of whatever kernel precedes it: the previous
+    // step's frame writer releases it early (its records live in the other
+    // half), any other kernel simply completes first
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = dim3(blocks_for(threads, 128));
+    lc.blockDim = dim3(128);
+    lc.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    lc.attrs = at;
+    lc.numAttrs = NV_STEP_CHAIN && c->pdl && !c->prof_on ? 1 : 0;
+    CK(cudaLaunchKernelEx(&lc, nvk::k_agent_step, c->env_view(), c->scene_view(), cfg, actions,
+                          collided, disp, status, ready));
+  }
   TRY(check_launch(c));
   c->pdl_armed = arm_pdl;
   return NV_OK;
@@ -1457,7 +1481,8 @@ int nv_fill_frames(nv_ctx *c, int cam, int64_t n, const double *t_col, const int
     CK(cudaStreamSynchronize(st));
     TRY(build_camera_tables(c, k, sensor_height));
   }
-  TRY(k.rec.alloc(sizeof(ColRec) * (size_t)n * k.W));
+  TRY(k.rec.alloc(2 * sizeof(ColRec) * (size_t)n * k.W));
+  rec_flip(k);
   long long total = n * (long long)k.W;
   nvk::k_cols_from_hits<<<blocks_for(total, 256), 256, 0, st>>>(
       c->scene_view(), cam_view(k), total, t_col, i_col, dirx, diry, rec_out(k, n));
