@@ -236,6 +236,7 @@ __global__ void __launch_bounds__(128, NV_CASTW_MINB) k_column_cast_warp(EnvView
                                                           unsigned *arrive, const unsigned *order,
                                                           unsigned *cost) {
   // `order` / `cost`: longest-first block order, as in k_column_cast
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // see k_column_cast
   const long long blk = order ? (long long)__ldg(order + blockIdx.x) : (long long)blockIdx.x;
   long long t0 = 0;
   if (order && threadIdx.x == 0) t0 = clock64();
@@ -272,6 +273,9 @@ __global__ void __launch_bounds__(128, NV_CAST_KMINB) k_column_cast(EnvView ev, 
   // wave is made of short blocks) and records its block's duration in
   // cost[] for the next step's ordering.  The rays, their results and the
   // visit order inside each ray are unchanged.
+  // the frame writer (a programmatic dependent) may launch once every cast
+  // CTA is running: its set-up then overlaps the cast's tail
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const long long blk = order ? (long long)__ldg(order + blockIdx.x) : (long long)blockIdx.x;
   long long t0 = 0;
   if (order && threadIdx.x == 0) t0 = clock64();

@@ -464,6 +464,10 @@ __global__ void NV_FILL_BOUNDS k_fill_ws(FillArgs a, FillWsLayout L) {
       bulk_load(cols_s + (size_t)buf * 2 * W + W, a.rb + (size_t)env * W, plane_bytes, b);
     };
     int q = blockIdx.x;  // work item = (env, row band)
+    // launched as a programmatic dependent of the column cast: the CTA's
+    // set-up above overlapped the cast's tail; the records are complete and
+    // visible once the cast grid is (a no-op for an ordinary launch)
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     // record planes run NV_WS_CBUF - 1 items ahead of the item being stored
 #pragma unroll
     for (int j = 0; j < NV_WS_CBUF - 1; ++j)

@@ -41,6 +41,9 @@ using namespace nvd;
 #ifndef NV_WS_NW
 #define NV_WS_NW 16  // producer warps of the ws writer (4 / 8 / 16)
 #endif
+#ifndef NV_FILL_PDL
+#define NV_FILL_PDL 1  // the ws writer is a programmatic dependent of the column cast
+#endif
 #ifndef NV_STEP_CHAIN
 #define NV_STEP_CHAIN 1  // the agent step is a programmatic dependent of the previous frame writer
 #endif
@@ -205,6 +208,7 @@ struct nv_ctx {
   bool e2e_mapped = NV_E2E_MAPPED != 0;  // host-buffer graph path: zero-copy actions / results
   bool pdl = true;           // agent step -> cast programmatic dependent launch (nv_set_overlap)
   bool pdl_armed = false, pdl_init = false;
+  bool fill_pdl = false;  // the next ws writer launch follows its column cast (launch_ws_kernel)
   DevBuf pdl_ready, pdl_arrive;
   // dynamic shared memory opted in per kernel on this context's device
   std::unordered_map<const void *, size_t> smem_cfg;
@@ -494,7 +498,21 @@ int launch_ws_kernel(nv_ctx *c, nvk::FillArgs &a, const nvk::FillWsLayout &L, si
   const unsigned grid =
       (unsigned)std::max<int64_t>(1, std::min<int64_t>(a.N * (int64_t)L.bands, c->sm_count));
   Prof pf(c, st, 2);
-  kern<<<grid, (L.nw + 1) * 32, smem, st>>>(a, L);
+  if (c->fill_pdl) {  // a programmatic dependent of the column cast just launched
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = dim3(grid);
+    lc.blockDim = dim3((L.nw + 1) * 32);
+    lc.dynamicSmemBytes = smem;
+    lc.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    CK(cudaLaunchKernelEx(&lc, kern, a, L));
+  } else {
+    kern<<<grid, (L.nw + 1) * 32, smem, st>>>(a, L);
+  }
   return check_launch(c);
 }
 
@@ -1125,7 +1143,11 @@ int nv_step_render(nv_ctx *c, const int8_t *actions, int cam, uint8_t *rgb, floa
   TRY(do_cast(c, cam, gps, compass, st));
   c->pdl_armed = false;
   if (c->mid_ev) CK(cudaEventRecordWithFlags(c->mid_ev, st, cudaEventRecordExternal));
+  // cast -> writer programmatic launch (set-up beside the cast's tail), unless
+  // an event sits between them
+  c->fill_pdl = NV_FILL_PDL && c->pdl && !c->prof_on && !c->mid_ev;
   const int rc = launch_fill(c, k, c->n_envs, rgb, depth, sem, st);
+  c->fill_pdl = false;
   TRY(lpt_join(c, st));
   return rc;
 }
