@@ -226,6 +226,21 @@ __device__ __forceinline__ void k_column_cast_warp_body(const EnvView &ev, const
   }
 }
 
+// Per-env release to the frame writer: after a block's records are written
+// (the caller's __syncthreads), thread 0 adds the block's column count of
+// each env it covers to done[env] (release).  Blocks cover rays
+// [blk * rpb, (blk + 1) * rpb) of the env-major ray order.
+__device__ __forceinline__ void release_envs(unsigned *done, long long blk, int rpb, int W,
+                                             long long n_rays) {
+  const long long r0 = blk * rpb, r1 = min(n_rays, r0 + rpb) - 1;
+  if (r0 > r1) return;
+  __threadfence();
+  for (long long e = r0 / W; e <= r1 / W; ++e) {
+    const long long lo = max(r0, e * W), hi = min(r1, (e + 1) * W - 1);
+    atomicAdd(done + e, (unsigned)(hi - lo + 1));
+  }
+}
+
 // With `ready`: a programmatic dependent of k_agent_step, waiting per env.
 #ifndef NV_CASTW_MINB
 #define NV_CASTW_MINB 8  // min resident CTAs/SM for the warp-per-ray cast (register cap <= 64; C2 31.1 -> 28.9 us/step)
@@ -234,7 +249,7 @@ __global__ void __launch_bounds__(128, NV_CASTW_MINB) k_column_cast_warp(EnvView
                                                           RecOut ro, double t_max, double *gps,
                                                           double *compass, unsigned *ready,
                                                           unsigned *arrive, const unsigned *order,
-                                                          unsigned *cost) {
+                                                          unsigned *cost, unsigned *done) {
   // `order` / `cost`: longest-first block order, as in k_column_cast
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // see k_column_cast
   const long long blk = order ? (long long)__ldg(order + blockIdx.x) : (long long)blockIdx.x;
@@ -251,9 +266,12 @@ __global__ void __launch_bounds__(128, NV_CASTW_MINB) k_column_cast_warp(EnvView
     else
       k_column_cast_warp_body<false>(ev, sc, cam, ro, t_max, gps, compass, e, j);
   }
-  if (order) {
+  if (order || done) {
     __syncthreads();
-    if (threadIdx.x == 0) cost[blk] = (unsigned)min(clock64() - t0, 0xffffffffLL);
+    if (threadIdx.x == 0) {
+      if (order) cost[blk] = (unsigned)min(clock64() - t0, 0xffffffffLL);
+      if (done) release_envs(done, blk, (int)(blockDim.x >> 5), cam.W, total);
+    }
   }
   asm volatile("griddepcontrol.wait;" ::: "memory");  // completes after the agent step
 }
@@ -267,7 +285,8 @@ __global__ void __launch_bounds__(128, NV_CAST_KMINB) k_column_cast(EnvView ev, 
                                                      RecOut ro, double t_max,
                                                      double *gps, double *compass,
                                                      unsigned *ready, unsigned *arrive,
-                                                     const unsigned *order, unsigned *cost) {
+                                                     const unsigned *order, unsigned *cost,
+                                                     unsigned *done) {
   // With `order`: CTA b casts ray block order[b] (blocks the previous step
   // found slowest first -- longest-processing-time order, so the grid's last
   // wave is made of short blocks) and records its block's duration in
@@ -291,9 +310,12 @@ __global__ void __launch_bounds__(128, NV_CAST_KMINB) k_column_cast(EnvView ev, 
     else
       cast_column<false>(ev, sc, cam, e, j, ro, t_max, gps, compass);
   }
-  if (order) {
+  if (order || done) {
     __syncthreads();
-    if (threadIdx.x == 0) cost[blk] = (unsigned)min(clock64() - t0, 0xffffffffLL);
+    if (threadIdx.x == 0) {
+      if (order) cost[blk] = (unsigned)min(clock64() - t0, 0xffffffffLL);
+      if (done) release_envs(done, blk, (int)blockDim.x, cam.W, total);
+    }
   }
   asm volatile("griddepcontrol.wait;" ::: "memory");  // completes after the agent step
 }

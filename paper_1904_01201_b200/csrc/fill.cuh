@@ -53,6 +53,10 @@ struct FillArgs {
   float max_range;
   unsigned long long noise_seed, noise_frame;
   long long env_offset;  // global id of env 0 (sharding-invariant streams)
+  // per-env release from the column cast (the writer is its programmatic
+  // dependent): finished-column counts, band consumers, timeout flag;
+  // nullptr = the records are complete when the writer's loads start
+  unsigned *done, *consumed, *fault;
 };
 
 // ---- inverse-depth noise ---------------------------------------------------
@@ -405,6 +409,41 @@ struct FillWsLayout {  // byte offsets into dynamic shared memory + ring geometr
 #else
 #define NV_FILL_BOUNDS __launch_bounds__(544, 1)
 #endif
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ bool env_cast_done(const unsigned *done, int env, int W) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(done + env) : "memory");
+  return v >= (unsigned)W;
+}
+// Store-warp side of the per-env release: wait (acquire) until env's column
+// records are all written, order the later bulk (async-proxy) reads after it,
+// and let the env's last consumer reset its count (the counts of the other
+// record half serve the next step).  A wait longer than 200 ms raises the
+// fault flag and stops waiting, so a broken launch can never hang the GPU.
+__device__ __forceinline__ void wait_env_cast(unsigned *done, unsigned *consumed,
+                                              unsigned *fault, int env, int W, int bands) {
+  if (!env_cast_done(done, env, W)) {
+    const unsigned long long t0 = global_ns();
+    while (!env_cast_done(done, env, W)) {
+      if (*reinterpret_cast<volatile unsigned *>(fault)) break;
+      if (global_ns() - t0 > 200000000ull) {
+        atomicExch(fault, 1u);
+        break;
+      }
+      __nanosleep(64);
+    }
+  }
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+  if (bands == 1 || atomicAdd(consumed + env, 1u) == (unsigned)(bands - 1)) {
+    if (bands > 1) consumed[env] = 0;
+    done[env] = 0;
+  }
+}
+
 template <int CPL, bool TAB, int RPW, bool NOISE, bool BANDED>
 __global__ void NV_FILL_BOUNDS k_fill_ws(FillArgs a, FillWsLayout L) {
   // the next step's agent step (a programmatic dependent) may start on SMs
@@ -465,22 +504,37 @@ __global__ void NV_FILL_BOUNDS k_fill_ws(FillArgs a, FillWsLayout L) {
     };
     int q = blockIdx.x;  // work item = (env, row band)
     // launched as a programmatic dependent of the column cast: the CTA's
-    // set-up above overlapped the cast's tail; the records are complete and
-    // visible once the cast grid is (a no-op for an ordinary launch)
-    asm volatile("griddepcontrol.wait;" ::: "memory");
-    // record planes run NV_WS_CBUF - 1 items ahead of the item being stored
+    // set-up above overlapped the cast's tail.  With per-env release (a.done)
+    // each item's records are posted as soon as its env is cast (checked
+    // between slots, waited for at the item's end); otherwise they are all
+    // complete and visible once the cast grid is (a no-op for an ordinary
+    // launch).
+    if (!a.done) asm volatile("griddepcontrol.wait;" ::: "memory");
 #pragma unroll
     for (int j = 0; j < NV_WS_CBUF - 1; ++j)
-      if (q + j * (int)gridDim.x < n_items) load_item(j, (q + j * (int)gridDim.x) / bands);
+      if (q + j * (int)gridDim.x < n_items) {
+        const int env = (q + j * (int)gridDim.x) / bands;
+        if (a.done) wait_env_cast(a.done, a.consumed, a.fault, env, W, bands);
+        load_item(j, env);
+      }
     unsigned slot = 0, use = 0;
     for (int it = 0; q < n_items; ++it, q += gridDim.x) {
       const int qn = q + (NV_WS_CBUF - 1) * (int)gridDim.x;
-      if (qn < n_items) {
-        const int j = it + NV_WS_CBUF - 1;  // item to post; buffer j % CBUF last held item j - CBUF
+      const int j = it + NV_WS_CBUF - 1;  // item to post; buffer j % CBUF last held item j - CBUF
+      bool pending = qn < n_items;
+      auto post = [&](bool block) {
+        if (!pending) return;
+        const int env = qn / bands;
+        if (a.done) {
+          if (!block && !env_cast_done(a.done, env, W)) return;
+          wait_env_cast(a.done, a.consumed, a.fault, env, W, bands);
+        }
         if (j >= NV_WS_CBUF)
           mbar_wait(colempty + (j % NV_WS_CBUF), (unsigned)(((j / NV_WS_CBUF) - 1) & 1));
-        load_item(j % NV_WS_CBUF, qn / bands);
-      }
+        load_item(j % NV_WS_CBUF, env);
+        pending = false;
+      };
+      if (!a.done) post(true);
       const int e = q / bands, row0 = (q - e * bands) * band_rows;
       for (int sl = 0; sl < slots_per_item; ++sl) {
         mbar_wait(full + slot, use & 1u);
@@ -494,6 +548,7 @@ __global__ void NV_FILL_BOUNDS k_fill_ws(FillArgs a, FillWsLayout L) {
         (void)buf; (void)pix0; (void)pol;
 #endif
         bulk_commit();
+        if (a.done) post(false);
         // wait for this slot's smem reads and hand it back at once
         bulk_wait_read<0>();
         mbar_arrive(empty + slot);
@@ -502,8 +557,11 @@ __global__ void NV_FILL_BOUNDS k_fill_ws(FillArgs a, FillWsLayout L) {
           ++use;
         }
       }
+      post(true);
     }
     bulk_wait_all();
+    // completes after the cast grid (stream order for what follows)
+    if (a.done) asm volatile("griddepcontrol.wait;" ::: "memory");
     return;
   }
   // -------------------------------------------------------------- producers

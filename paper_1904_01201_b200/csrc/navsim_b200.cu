@@ -44,6 +44,9 @@ using namespace nvd;
 #ifndef NV_FILL_PDL
 #define NV_FILL_PDL 1  // the ws writer is a programmatic dependent of the column cast
 #endif
+#ifndef NV_FILL_RELEASE
+#define NV_FILL_RELEASE 1  // the writer takes each env as soon as its casts are done
+#endif
 #ifndef NV_STEP_CHAIN
 #define NV_STEP_CHAIN 1  // the agent step is a programmatic dependent of the previous frame writer
 #endif
@@ -137,6 +140,10 @@ struct Camera {
                    // renders alternate (rec_flip), so a step's casts never write
                    // the records the previous step's writer may still read
   int rec_half = 0;
+  // per-env release counts (cast -> writer), one set per record half:
+  // [half][done N | consumed N], then the fault flag; zero between steps
+  DevBuf rel, rel_e2e;
+  int64_t rel_n = -1, rel_n_e2e = -1;
   DevBuf lpt_order, lpt_cost;  // thread-per-ray cast: block order (slowest first) + durations
   int64_t lpt_n = -1;           // blocks the order is valid for
   // The host-buffer step's own record buffer and block order (its frame
@@ -411,6 +418,18 @@ int fast_cpl(int W) { return W % 256 == 0 ? NV_CPL256 : (W == 128 ? 4 : (W == 64
 // A render's casts write the other half of the record buffer than the last one.
 void rec_flip(Camera &cam) { cam.rec_half ^= 1; }
 
+// Release counters of the camera for n envs (zeroed when (re)allocated).
+int rel_buffers(DevBuf &b, int64_t &have, int64_t n) {
+  if (have == n) return NV_OK;
+  const size_t bytes = sizeof(unsigned) * (size_t)(4 * n + 1);
+  TRY(b.alloc(bytes));
+  CK(cudaMemset(b.p, 0, bytes));
+  have = n;
+  return NV_OK;
+}
+unsigned *rel_done(Camera &k, int64_t N) { return k.rel.as<unsigned>() + (size_t)k.rec_half * 2 * N; }
+unsigned *rel_fault(Camera &k, int64_t N) { return k.rel.as<unsigned>() + 4 * (size_t)N; }
+
 // Column-record planes of N envs in the current half of the camera's record
 // buffer (A then B).
 RecOut rec_out(Camera &cam, int64_t N) {
@@ -594,9 +613,12 @@ bool ws_layout_ok(const Camera &cam, const void *rgb, const void *depth, const v
 }
 
 int launch_fill(nv_ctx *c, Camera &cam, int64_t N, uint8_t *rgb, float *depth, uint16_t *sem,
-                cudaStream_t st) {
+                cudaStream_t st, bool release = false) {
   if (!rgb && !depth && !sem) return NV_OK;
   nvk::FillArgs a;
+  a.done = release ? rel_done(cam, N) : nullptr;
+  a.consumed = release ? rel_done(cam, N) + N : nullptr;
+  a.fault = release ? rel_fault(cam, N) : nullptr;
   const RecOut ro = rec_out(cam, N);
   a.ra = ro.a;
   a.rb = ro.b;
@@ -645,6 +667,7 @@ int cam_check(nv_ctx *c, int cam) {
                 (long long)(c->n_envs * (int64_t)k.W));
   if (k.tables_cam_h != c->sensor_h) TRY(build_camera_tables(c, k, c->sensor_h));
   TRY(k.rec.alloc(2 * sizeof(ColRec) * (size_t)std::max<int64_t>(1, c->n_envs) * k.W));
+  TRY(rel_buffers(k.rel, k.rel_n, std::max<int64_t>(1, c->n_envs)));
   return NV_OK;
 }
 
@@ -693,7 +716,10 @@ int lpt_fork(nv_ctx *c, cudaStream_t st, unsigned *order, unsigned *cost, unsign
   return NV_OK;
 }
 
-int do_cast(nv_ctx *c, int cam, double *gps, double *compass, cudaStream_t st) {
+// release: publish per-env finished-column counts for a writer launched as
+// this cast's programmatic dependent (k_fill_ws with FillArgs.done)
+int do_cast(nv_ctx *c, int cam, double *gps, double *compass, cudaStream_t st,
+            bool release = false) {
   Camera &k = c->cams[cam];
   // t_max = max_range: capping the walk is output-identical for rendered
   // frames (tests/test_gpu_parity.py checks it against the
@@ -729,7 +755,8 @@ int do_cast(nv_ctx *c, int cam, double *gps, double *compass, cudaStream_t st) {
     }
     CK(cudaLaunchKernelEx(&lc, kern, c->env_view(), c->scene_view(), cam_view(k),
                           rec_out(k, c->n_envs), k.max_range, gps, compass, ready, arrive,
-                          (const unsigned *)order, cost));
+                          (const unsigned *)order, cost,
+                          release ? rel_done(k, c->n_envs) : (unsigned *)nullptr));
     TRY(check_launch(c));
   }
   return order ? lpt_fork(c, st, order, cost, nblk) : NV_OK;
@@ -1140,13 +1167,18 @@ int nv_step_render(nv_ctx *c, const int8_t *actions, int cam, uint8_t *rgb, floa
   // the programmatic edge)
   const bool pdl = c->pdl && !c->prof_on;
   TRY(do_step(c, actions, collided, displacement, status, st, pdl));
-  TRY(do_cast(c, cam, gps, compass, st));
+  // cast -> writer programmatic launch (set-up beside the cast's tail), unless
+  // an event sits between them; with the ws writer, per-env release
+  c->fill_pdl = NV_FILL_PDL && c->pdl && !c->prof_on && !c->mid_ev;
+  // (thread-per-ray batches: with the warp-per-ray cast of small batches the
+  // per-env waits cost more than they overlap, C2 25.7 -> 27.3 us)
+  const bool release = c->fill_pdl && NV_FILL_RELEASE && (rgb || depth || sem) &&
+                       c->fill_mode != NV_FILL_GENERIC && ws_layout_ok(k, rgb, depth, sem) &&
+                       !use_warp_cast(c, c->n_envs * (long long)k.W);
+  TRY(do_cast(c, cam, gps, compass, st, release));
   c->pdl_armed = false;
   if (c->mid_ev) CK(cudaEventRecordWithFlags(c->mid_ev, st, cudaEventRecordExternal));
-  // cast -> writer programmatic launch (set-up beside the cast's tail), unless
-  // an event sits between them
-  c->fill_pdl = NV_FILL_PDL && c->pdl && !c->prof_on && !c->mid_ev;
-  const int rc = launch_fill(c, k, c->n_envs, rgb, depth, sem, st);
+  const int rc = launch_fill(c, k, c->n_envs, rgb, depth, sem, st, release);
   c->fill_pdl = false;
   TRY(lpt_join(c, st));
   return rc;
@@ -1290,6 +1322,10 @@ int nv_step_render_host(nv_ctx *c, const int8_t *actions_host, int cam, uint32_t
       }
     }
     if (c->pdl) TRY(pdl_buffers(c));
+    for (int q = 0; q < ncam; ++q) {
+      Camera &k = c->cams[cams[q]];
+      TRY(rel_buffers(k.rel_e2e, k.rel_n_e2e, c->n_envs));
+    }
     std::vector<uint64_t> key = {(uint64_t)c->n_envs, (uint64_t)c->gen, (uint64_t)ncam,
                                  (uint64_t)c->e2e_mapped, (uint64_t)direct,
                                  (uint64_t)(uintptr_t)c->e_hin, (uint64_t)(uintptr_t)c->e_hout,
@@ -1302,6 +1338,7 @@ int nv_step_render_host(nv_ctx *c, const int8_t *actions_host, int cam, uint32_t
       uint8_t *r; float *d; uint16_t *sm;
       frame_ptrs(q, r, d, sm);
       for (uint64_t v : {(uint64_t)cams[q], (uint64_t)chans[q], (uint64_t)(uintptr_t)k.rec_e2e.p,
+                         (uint64_t)(uintptr_t)k.rel_e2e.p,
                          (uint64_t)(uintptr_t)k.lpt_order_e2e.p, (uint64_t)(uintptr_t)k.lpt_cost_e2e.p,
                          (uint64_t)(uintptr_t)r, (uint64_t)(uintptr_t)d, (uint64_t)(uintptr_t)sm})
         key.push_back(v);
@@ -1340,6 +1377,9 @@ int nv_step_render_host(nv_ctx *c, const int8_t *actions_host, int cam, uint32_t
           Camera &k = c->cams[cams[q]];
           std::swap(k.rec.p, k.rec_e2e.p);
           std::swap(k.rec.bytes, k.rec_e2e.bytes);
+          std::swap(k.rel.p, k.rel_e2e.p);
+          std::swap(k.rel.bytes, k.rel_e2e.bytes);
+          std::swap(k.rel_n, k.rel_n_e2e);
           std::swap(k.lpt_order.p, k.lpt_order_e2e.p);
           std::swap(k.lpt_order.bytes, k.lpt_order_e2e.bytes);
           std::swap(k.lpt_cost.p, k.lpt_cost_e2e.p);
