@@ -444,7 +444,9 @@ __device__ __forceinline__ void wait_env_cast(unsigned *done, unsigned *consumed
   }
 }
 
-template <int CPL, bool TAB, int RPW, bool NOISE, bool BANDED>
+// REL: per-env release from the cast (FillArgs.done); a separate
+// instantiation so the ordinary writer keeps its own code.
+template <int CPL, bool TAB, int RPW, bool NOISE, bool BANDED, bool REL>
 __global__ void NV_FILL_BOUNDS k_fill_ws(FillArgs a, FillWsLayout L) {
   // the next step's agent step (a programmatic dependent) may start on SMs
   // this grid leaves: it touches none of the writer's inputs
@@ -509,12 +511,12 @@ __global__ void NV_FILL_BOUNDS k_fill_ws(FillArgs a, FillWsLayout L) {
     // between slots, waited for at the item's end); otherwise they are all
     // complete and visible once the cast grid is (a no-op for an ordinary
     // launch).
-    if (!a.done) asm volatile("griddepcontrol.wait;" ::: "memory");
+    if constexpr (!REL) asm volatile("griddepcontrol.wait;" ::: "memory");
 #pragma unroll
     for (int j = 0; j < NV_WS_CBUF - 1; ++j)
       if (q + j * (int)gridDim.x < n_items) {
         const int env = (q + j * (int)gridDim.x) / bands;
-        if (a.done) wait_env_cast(a.done, a.consumed, a.fault, env, W, bands);
+        if constexpr (REL) wait_env_cast(a.done, a.consumed, a.fault, env, W, bands);
         load_item(j, env);
       }
     unsigned slot = 0, use = 0;
@@ -525,7 +527,7 @@ __global__ void NV_FILL_BOUNDS k_fill_ws(FillArgs a, FillWsLayout L) {
       auto post = [&](bool block) {
         if (!pending) return;
         const int env = qn / bands;
-        if (a.done) {
+        if constexpr (REL) {
           if (!block && !env_cast_done(a.done, env, W)) return;
           wait_env_cast(a.done, a.consumed, a.fault, env, W, bands);
         }
@@ -534,7 +536,7 @@ __global__ void NV_FILL_BOUNDS k_fill_ws(FillArgs a, FillWsLayout L) {
         load_item(j % NV_WS_CBUF, env);
         pending = false;
       };
-      if (!a.done) post(true);
+      if constexpr (!REL) post(true);
       const int e = q / bands, row0 = (q - e * bands) * band_rows;
       for (int sl = 0; sl < slots_per_item; ++sl) {
         mbar_wait(full + slot, use & 1u);
@@ -548,7 +550,7 @@ __global__ void NV_FILL_BOUNDS k_fill_ws(FillArgs a, FillWsLayout L) {
         (void)buf; (void)pix0; (void)pol;
 #endif
         bulk_commit();
-        if (a.done) post(false);
+        if constexpr (REL) post(false);
         // wait for this slot's smem reads and hand it back at once
         bulk_wait_read<0>();
         mbar_arrive(empty + slot);
@@ -561,7 +563,7 @@ __global__ void NV_FILL_BOUNDS k_fill_ws(FillArgs a, FillWsLayout L) {
     }
     bulk_wait_all();
     // completes after the cast grid (stream order for what follows)
-    if (a.done) asm volatile("griddepcontrol.wait;" ::: "memory");
+    if constexpr (REL) asm volatile("griddepcontrol.wait;" ::: "memory");
     return;
   }
   // -------------------------------------------------------------- producers

@@ -8,6 +8,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <type_traits>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -509,10 +510,14 @@ template <int CPL, bool TAB, int RPW>
 int launch_ws_kernel(nv_ctx *c, nvk::FillArgs &a, const nvk::FillWsLayout &L, size_t smem,
                      cudaStream_t st) {
   const bool noise = a.noise_sigma > 0.0f && a.depth;
-  auto kern = L.bands > 1 ? (noise ? nvk::k_fill_ws<CPL, TAB, RPW, true, true>
-                                  : nvk::k_fill_ws<CPL, TAB, RPW, false, true>)
-                         : (noise ? nvk::k_fill_ws<CPL, TAB, RPW, true, false>
-                                  : nvk::k_fill_ws<CPL, TAB, RPW, false, false>);
+  auto pick = [&](auto rel) {
+    constexpr bool R = decltype(rel)::value;
+    return L.bands > 1 ? (noise ? nvk::k_fill_ws<CPL, TAB, RPW, true, true, R>
+                                : nvk::k_fill_ws<CPL, TAB, RPW, false, true, R>)
+                       : (noise ? nvk::k_fill_ws<CPL, TAB, RPW, true, false, R>
+                                : nvk::k_fill_ws<CPL, TAB, RPW, false, false, R>);
+  };
+  auto kern = a.done ? pick(std::true_type{}) : pick(std::false_type{});
   TRY(set_smem(c, (const void *)kern, smem));
   const unsigned grid =
       (unsigned)std::max<int64_t>(1, std::min<int64_t>(a.N * (int64_t)L.bands, c->sm_count));
@@ -597,8 +602,10 @@ int launch_fill_ws(nv_ctx *c, nvk::FillArgs &a, cudaStream_t st) {
     L.bands = NV_WS_BANDS > 0 && (a.H / L.slot_rows) % force_bands == 0 ? force_bands : best;
   }
   a.segs_per_row = S;
-  if (tab && rpw == 2) return launch_ws_kernel<CPL, true, 2>(c, a, L, smem, st);
-  if (tab) return launch_ws_kernel<CPL, true, 1>(c, a, L, smem, st);
+  if constexpr (NV_WS_TAB != 0) {  // study builds only (staged shading table)
+    if (tab && rpw == 2) return launch_ws_kernel<CPL, true, 2>(c, a, L, smem, st);
+    if (tab) return launch_ws_kernel<CPL, true, 1>(c, a, L, smem, st);
+  }
   if (rpw == 2) return launch_ws_kernel<CPL, false, 2>(c, a, L, smem, st);
   return launch_ws_kernel<CPL, false, 1>(c, a, L, smem, st);
 }
@@ -701,19 +708,27 @@ bool lpt_pays(const nv_ctx *c, unsigned nblk) { return nblk >= 4u * (unsigned)c-
 
 // the next step's block order, on a side stream beside the frame writer
 // (joined into `st` by lpt_join after the writer is launched)
-int lpt_fork(nv_ctx *c, cudaStream_t st, unsigned *order, unsigned *cost, unsigned nblk) {
+// Side stream beside the frame writer, forked from `st` after the casts
+// (joined by lpt_join after the writer is launched).  In a captured graph the
+// fork is a dependency edge only, so the writer stays a programmatic
+// dependent of the casts.
+int side_fork(nv_ctx *c, cudaStream_t st) {
   if (!c->o_stream) {
     CK(cudaStreamCreateWithFlags(&c->o_stream, cudaStreamNonBlocking));
     CK(cudaEventCreateWithFlags(&c->o_ev0, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&c->o_ev1, cudaEventDisableTiming));
   }
+  if (c->o_fork) return NV_OK;
   CK(cudaEventRecord(c->o_ev0, st));
   CK(cudaStreamWaitEvent(c->o_stream, c->o_ev0, 0));
-  nvk::k_cast_order<<<1, 1024, 0, c->o_stream>>>(cost, order, (int)nblk);
-  TRY(check_launch(c));
-  CK(cudaEventRecord(c->o_ev1, c->o_stream));
   c->o_fork = true;
   return NV_OK;
+}
+
+int lpt_fork(nv_ctx *c, cudaStream_t st, unsigned *order, unsigned *cost, unsigned nblk) {
+  TRY(side_fork(c, st));
+  nvk::k_cast_order<<<1, 1024, 0, c->o_stream>>>(cost, order, (int)nblk);
+  return check_launch(c);
 }
 
 // release: publish per-env finished-column counts for a writer launched as
@@ -766,6 +781,7 @@ int do_cast(nv_ctx *c, int cam, double *gps, double *compass, cudaStream_t st,
 int lpt_join(nv_ctx *c, cudaStream_t st) {
   if (!c->o_fork) return NV_OK;
   c->o_fork = false;
+  CK(cudaEventRecord(c->o_ev1, c->o_stream));
   CK(cudaStreamWaitEvent(st, c->o_ev1, 0));
   return NV_OK;
 }
@@ -1167,9 +1183,9 @@ int nv_step_render(nv_ctx *c, const int8_t *actions, int cam, uint8_t *rgb, floa
   // the programmatic edge)
   const bool pdl = c->pdl && !c->prof_on;
   TRY(do_step(c, actions, collided, displacement, status, st, pdl));
-  // cast -> writer programmatic launch (set-up beside the cast's tail), unless
-  // an event sits between them; with the ws writer, per-env release
-  c->fill_pdl = NV_FILL_PDL && c->pdl && !c->prof_on && !c->mid_ev;
+  // cast -> writer programmatic launch (set-up beside the cast's tail); with
+  // the ws writer, per-env release
+  c->fill_pdl = NV_FILL_PDL && c->pdl && !c->prof_on;
   // (thread-per-ray batches: with the warp-per-ray cast of small batches the
   // per-env waits cost more than they overlap, C2 25.7 -> 27.3 us)
   const bool release = c->fill_pdl && NV_FILL_RELEASE && (rgb || depth || sem) &&
@@ -1177,7 +1193,10 @@ int nv_step_render(nv_ctx *c, const int8_t *actions, int cam, uint8_t *rgb, floa
                        !use_warp_cast(c, c->n_envs * (long long)k.W);
   TRY(do_cast(c, cam, gps, compass, st, release));
   c->pdl_armed = false;
-  if (c->mid_ev) CK(cudaEventRecordWithFlags(c->mid_ev, st, cudaEventRecordExternal));
+  if (c->mid_ev) {  // on the side stream: no node between the casts and the writer
+    TRY(side_fork(c, st));
+    CK(cudaEventRecordWithFlags(c->mid_ev, c->o_stream, cudaEventRecordExternal));
+  }
   const int rc = launch_fill(c, k, c->n_envs, rgb, depth, sem, st, release);
   c->fill_pdl = false;
   TRY(lpt_join(c, st));
