@@ -407,7 +407,7 @@ struct FillWsLayout {  // byte offsets into dynamic shared memory + ring geometr
 #if NV_FILL_MAXREG > 0
 #define NV_FILL_BOUNDS __maxnreg__(NV_FILL_MAXREG)
 #else
-#define NV_FILL_BOUNDS __launch_bounds__(544, 1)
+#define NV_FILL_BOUNDS __launch_bounds__(REL ? 576 : 544, 1)
 #endif
 __device__ __forceinline__ unsigned long long global_ns() {
   unsigned long long t;
@@ -454,7 +454,7 @@ __global__ void NV_FILL_BOUNDS k_fill_ws(FillArgs a, FillWsLayout L) {
   extern __shared__ __align__(128) uint8_t smem[];
   using Ln = Lanes<CPL>;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int nw = (blockDim.x >> 5) - 1;  // producer warps
+  const int nw = L.nw;  // producer warps (then the store warp, then with REL the loader warp)
   const int W = a.W, H = a.H, S = a.segs_per_row, R = L.slot_rows, NSLOT = L.nslot;
   const RowRec *rows_s = reinterpret_cast<const RowRec *>(smem + L.rows);
   const uint16_t *inv_s = reinterpret_cast<const uint16_t *>(smem + L.inv);
@@ -494,49 +494,79 @@ __global__ void NV_FILL_BOUNDS k_fill_ws(FillArgs a, FillWsLayout L) {
     }
   }
   __syncthreads();
-  if (warp == nw) {
+  auto load_item = [&](int buf, int env) {
+    uint64_t *b = colfull + buf;
+    mbar_expect_tx(b, 2 * plane_bytes);
+    bulk_load(cols_s + (size_t)buf * 2 * W, a.ra + (size_t)env * W, plane_bytes, b);
+    bulk_load(cols_s + (size_t)buf * 2 * W + W, a.rb + (size_t)env * W, plane_bytes, b);
+  };
+  if constexpr (REL) {
+    if (warp == nw + 1) {
+      // --------------------------------------------------------- loader warp
+      // per-env release: wait (acquire) for each item's env to be cast, then
+      // bulk-load its record planes into the next free buffer; the store
+      // warp never waits on the cast
+      if (lane != 0) return;
+      int it = 0;
+      for (int q = blockIdx.x; q < n_items; q += gridDim.x, ++it) {
+        wait_env_cast(a.done, a.consumed, a.fault, q / bands, W, bands);
+        if (it >= NV_WS_CBUF)
+          mbar_wait(colempty + (it % NV_WS_CBUF), (unsigned)(((it / NV_WS_CBUF) - 1) & 1));
+        load_item(it % NV_WS_CBUF, q / bands);
+      }
+      return;
+    }
+    if (warp == nw) {
+      // ---------------------------------------------------------- store warp
+      if (lane != 0) return;
+      const uint64_t pol = policy_evict_first();
+      unsigned slot = 0, use = 0;
+      for (int q = blockIdx.x; q < n_items; q += gridDim.x) {
+        const int e = q / bands, row0 = (q - e * bands) * band_rows;
+        for (int sl = 0; sl < slots_per_item; ++sl) {
+          mbar_wait(full + slot, use & 1u);
+          const uint8_t *buf = slots + (size_t)slot * L.slot_bytes;
+          const size_t pix0 = ((size_t)e * H + (size_t)row0 + (size_t)sl * R) * W;
+          if (want_rgb) bulk_store(a.rgb + pix0 * 3, buf, (unsigned)(R * W * 3), pol);
+          if (want_d) bulk_store(a.depth + pix0, buf + off_d, (unsigned)(R * W * 4), pol);
+          if (want_s) bulk_store(a.sem + pix0, buf + off_s, (unsigned)(R * W * 2), pol);
+          bulk_commit();
+          bulk_wait_read<0>();
+          mbar_arrive(empty + slot);
+          if (++slot == (unsigned)NSLOT) {
+            slot = 0;
+            ++use;
+          }
+        }
+      }
+      bulk_wait_all();
+      // completes after the cast grid (stream order for what follows)
+      asm volatile("griddepcontrol.wait;" ::: "memory");
+      return;
+    }
+  }
+  if (!REL && warp == nw) {
     // ------------------------------------------------------------ store warp
     if (lane != 0) return;
     const uint64_t pol = policy_evict_first();
-    auto load_item = [&](int buf, int env) {
-      uint64_t *b = colfull + buf;
-      mbar_expect_tx(b, 2 * plane_bytes);
-      bulk_load(cols_s + (size_t)buf * 2 * W, a.ra + (size_t)env * W, plane_bytes, b);
-      bulk_load(cols_s + (size_t)buf * 2 * W + W, a.rb + (size_t)env * W, plane_bytes, b);
-    };
     int q = blockIdx.x;  // work item = (env, row band)
     // launched as a programmatic dependent of the column cast: the CTA's
-    // set-up above overlapped the cast's tail.  With per-env release (a.done)
-    // each item's records are posted as soon as its env is cast (checked
-    // between slots, waited for at the item's end); otherwise they are all
-    // complete and visible once the cast grid is (a no-op for an ordinary
-    // launch).
-    if constexpr (!REL) asm volatile("griddepcontrol.wait;" ::: "memory");
+    // set-up above overlapped the cast's tail; the records are complete and
+    // visible once the cast grid is (a no-op for an ordinary launch)
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    // record planes run NV_WS_CBUF - 1 items ahead of the item being stored
 #pragma unroll
     for (int j = 0; j < NV_WS_CBUF - 1; ++j)
-      if (q + j * (int)gridDim.x < n_items) {
-        const int env = (q + j * (int)gridDim.x) / bands;
-        if constexpr (REL) wait_env_cast(a.done, a.consumed, a.fault, env, W, bands);
-        load_item(j, env);
-      }
+      if (q + j * (int)gridDim.x < n_items) load_item(j, (q + j * (int)gridDim.x) / bands);
     unsigned slot = 0, use = 0;
     for (int it = 0; q < n_items; ++it, q += gridDim.x) {
       const int qn = q + (NV_WS_CBUF - 1) * (int)gridDim.x;
-      const int j = it + NV_WS_CBUF - 1;  // item to post; buffer j % CBUF last held item j - CBUF
-      bool pending = qn < n_items;
-      auto post = [&](bool block) {
-        if (!pending) return;
-        const int env = qn / bands;
-        if constexpr (REL) {
-          if (!block && !env_cast_done(a.done, env, W)) return;
-          wait_env_cast(a.done, a.consumed, a.fault, env, W, bands);
-        }
+      if (qn < n_items) {
+        const int j = it + NV_WS_CBUF - 1;  // item to post; buffer j % CBUF last held item j - CBUF
         if (j >= NV_WS_CBUF)
           mbar_wait(colempty + (j % NV_WS_CBUF), (unsigned)(((j / NV_WS_CBUF) - 1) & 1));
-        load_item(j % NV_WS_CBUF, env);
-        pending = false;
-      };
-      if constexpr (!REL) post(true);
+        load_item(j % NV_WS_CBUF, qn / bands);
+      }
       const int e = q / bands, row0 = (q - e * bands) * band_rows;
       for (int sl = 0; sl < slots_per_item; ++sl) {
         mbar_wait(full + slot, use & 1u);
@@ -550,7 +580,6 @@ __global__ void NV_FILL_BOUNDS k_fill_ws(FillArgs a, FillWsLayout L) {
         (void)buf; (void)pix0; (void)pol;
 #endif
         bulk_commit();
-        if constexpr (REL) post(false);
         // wait for this slot's smem reads and hand it back at once
         bulk_wait_read<0>();
         mbar_arrive(empty + slot);
@@ -559,11 +588,8 @@ __global__ void NV_FILL_BOUNDS k_fill_ws(FillArgs a, FillWsLayout L) {
           ++use;
         }
       }
-      post(true);
     }
     bulk_wait_all();
-    // completes after the cast grid (stream order for what follows)
-    if constexpr (REL) asm volatile("griddepcontrol.wait;" ::: "memory");
     return;
   }
   // -------------------------------------------------------------- producers

@@ -525,7 +525,7 @@ int launch_ws_kernel(nv_ctx *c, nvk::FillArgs &a, const nvk::FillWsLayout &L, si
   if (c->fill_pdl) {  // a programmatic dependent of the column cast just launched
     cudaLaunchConfig_t lc = {};
     lc.gridDim = dim3(grid);
-    lc.blockDim = dim3((L.nw + 1) * 32);
+    lc.blockDim = dim3((L.nw + (a.done ? 2 : 1)) * 32);
     lc.dynamicSmemBytes = smem;
     lc.stream = st;
     cudaLaunchAttribute at[1];
@@ -535,7 +535,7 @@ int launch_ws_kernel(nv_ctx *c, nvk::FillArgs &a, const nvk::FillWsLayout &L, si
     lc.numAttrs = 1;
     CK(cudaLaunchKernelEx(&lc, kern, a, L));
   } else {
-    kern<<<grid, (L.nw + 1) * 32, smem, st>>>(a, L);
+    kern<<<grid, (L.nw + (a.done ? 2 : 1)) * 32, smem, st>>>(a, L);
   }
   return check_launch(c);
 }
