@@ -131,10 +131,12 @@ int nv_step_render(nv_ctx *ctx, const int8_t *actions, int cam, uint8_t *rgb,
                    uint8_t *collided, double *displacement, int32_t *status,
                    void *stream);
 
-/* Overlap of the agent step and the column cast in nv_step_render
- * (programmatic dependent launch: each env's casts start as soon as its agent
- * warp has published the new pose); on by default (C2 32.3 -> 30.1 us/step,
- * C3 end to end 140.4 -> 138.5 us), 0 turns it off. */
+/* Programmatic-dependent-launch chaining in nv_step_render, on by default:
+ * each env's casts start as soon as its agent warp has published the new
+ * pose; the frame writer takes each env as soon as its casts have published
+ * their column records (thread-per-ray batches); the next step's agent step
+ * starts on the SMs the previous writer's tail frees.  0 turns all of it off
+ * (serialised launches; identical results). */
 int nv_set_overlap(nv_ctx *ctx, int on);
 /* Column cast (raycast_grid's DDA over the grid, bit-exact in every mode):
  * NV_CAST_AUTO (default) = one thread per ray, or one warp per ray (lanes
