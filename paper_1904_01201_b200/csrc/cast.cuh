@@ -329,43 +329,44 @@ __global__ void k_lpt_init(unsigned *order, unsigned *cost, unsigned n) {
 }
 
 // Longest-first order of the cast's ray blocks from their last durations:
-// a one-CTA counting sort over 256 log-spaced buckets (descending), run on
-// a side stream beside the frame writer.
-__global__ void __launch_bounds__(1024) k_cast_order(const unsigned *cost, unsigned *order,
-                                                     int nblk) {
-  __shared__ unsigned hist[256], base[256], mx;
-  const int t = threadIdx.x;
-  if (t == 0) mx = 0;
-  for (int k = t; k < 256; k += blockDim.x) hist[k] = 0;
-  __syncthreads();
-  for (int b = t; b < nblk; b += blockDim.x) atomicMax(&mx, cost[b]);
-  __syncthreads();
+// a counting sort over 256 log-spaced buckets (descending) by ONE warp, run
+// on a side stream beside the frame writer -- a single warp fits an SM next
+// to a writer CTA, so the sort never waits for the writer to drain (the next
+// step's agent step depends on it).
+__global__ void __launch_bounds__(32) k_cast_order(const unsigned *cost, unsigned *order,
+                                                   int nblk) {
+  __shared__ unsigned hist[256];
+  const int lane = threadIdx.x;
+  unsigned mx = 0;
+  for (int k = lane; k < 256; k += 32) hist[k] = 0;
+  for (int b = lane; b < nblk; b += 32) mx = max(mx, cost[b]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  __syncwarp();
   const int top = 32 - __clz(mx | 1u);          // bits of the largest cost
   const int shift = top > 8 ? top - 8 : 0;
   auto bucket = [&](unsigned c) { return 255 - (int)min(255u, c >> shift); };  // slow first
-  for (int b = t; b < nblk; b += blockDim.x) atomicAdd(&hist[bucket(cost[b])], 1u);
-  __syncthreads();
-  // exclusive prefix over the 256 buckets: 8 warps scan 32 each, then offsets
-  __shared__ unsigned wsum[8];
-  if (t < 256) {
-    const int lane = t & 31, w = t >> 5;
-    unsigned v = hist[t];
+  for (int b = lane; b < nblk; b += 32) atomicAdd(&hist[bucket(cost[b])], 1u);
+  __syncwarp();
+  // exclusive prefix over the 256 buckets: 8 consecutive buckets per lane
+  unsigned v[8], run = 0;
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const unsigned u = __shfl_up_sync(0xffffffffu, v, o);
-      if (lane >= o) v += u;
-    }
-    if (lane == 31) wsum[w] = v;
-    base[t] = v - hist[t];
+  for (int k = 0; k < 8; ++k) {
+    v[k] = run;
+    run += hist[lane * 8 + k];
   }
-  __syncthreads();
-  if (t < 256) {
-    unsigned off = 0;
-    for (int w = 0; w < (t >> 5); ++w) off += wsum[w];
-    base[t] += off;
+  unsigned incl = run;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned u = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += u;
   }
-  __syncthreads();
-  for (int b = t; b < nblk; b += blockDim.x) order[atomicAdd(&base[bucket(cost[b])], 1u)] = (unsigned)b;
+  const unsigned base = incl - run;
+  __syncwarp();
+#pragma unroll
+  for (int k = 0; k < 8; ++k) hist[lane * 8 + k] = base + v[k];
+  __syncwarp();
+  for (int b = lane; b < nblk; b += 32) order[atomicAdd(&hist[bucket(cost[b])], 1u)] = (unsigned)b;
 }
 
 // gps_compass (sensors.py:175-180) for all envs (no visual sensors case).

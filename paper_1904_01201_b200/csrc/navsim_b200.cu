@@ -727,7 +727,7 @@ int side_fork(nv_ctx *c, cudaStream_t st) {
 
 int lpt_fork(nv_ctx *c, cudaStream_t st, unsigned *order, unsigned *cost, unsigned nblk) {
   TRY(side_fork(c, st));
-  nvk::k_cast_order<<<1, 1024, 0, c->o_stream>>>(cost, order, (int)nblk);
+  nvk::k_cast_order<<<1, 32, 0, c->o_stream>>>(cost, order, (int)nblk);
   return check_launch(c);
 }
 
