@@ -48,6 +48,9 @@ using namespace nvd;
 #ifndef NV_FILL_RELEASE
 #define NV_FILL_RELEASE 1  // the writer takes each env as soon as its casts are done
 #endif
+#ifndef NV_AGENT_BLOCK
+#define NV_AGENT_BLOCK 128  // threads per CTA of the agent step (a warp per env)
+#endif
 #ifndef NV_STEP_CHAIN
 #define NV_STEP_CHAIN 1  // the agent step is a programmatic dependent of the previous frame writer
 #endif
@@ -814,8 +817,8 @@ int do_step(nv_ctx *c, const int8_t *actions, uint8_t *collided, double *disp, i
     // step's frame writer releases it early (its records live in the other
     // half), any other kernel simply completes first
     cudaLaunchConfig_t lc = {};
-    lc.gridDim = dim3(blocks_for(threads, 128));
-    lc.blockDim = dim3(128);
+    lc.gridDim = dim3(blocks_for(threads, NV_AGENT_BLOCK));
+    lc.blockDim = dim3(NV_AGENT_BLOCK);
     lc.stream = st;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
