@@ -125,7 +125,15 @@ __device__ __forceinline__ void warp_agent_step(const EnvView &ev, const SceneVi
 // dependent launch of the cast), the dependent grid is released at once and
 // each env's pose is published through ready[e] (release) as soon as its warp
 // is done, so the casts of finished envs overlap the long agent chains.
-__global__ void __launch_bounds__(128) k_agent_step(EnvView ev, SceneView sc, AgentCfg cfg,
+#ifndef NV_AGENT_MAXREG
+#define NV_AGENT_MAXREG 0  // > 0: register cap of the agent step (room beside a writer CTA)
+#endif
+#if NV_AGENT_MAXREG > 0
+#define NV_AGENT_BOUNDS __maxnreg__(NV_AGENT_MAXREG)
+#else
+#define NV_AGENT_BOUNDS __launch_bounds__(128)
+#endif
+__global__ void NV_AGENT_BOUNDS k_agent_step(EnvView ev, SceneView sc, AgentCfg cfg,
                                                     const int8_t *__restrict__ actions,
                                                     uint8_t *collided_out,
                                                     double *disp_out, int32_t *status_out,
