@@ -520,25 +520,35 @@ struct TaskOut {
   OutcomeRec *out;
 };
 
+// done: per-env release to the frame writer (its programmatic dependent), as
+// in k_column_cast.
 __global__ void __launch_bounds__(128) k_column_cast_task(EnvView ev, SceneView sc, CamView cam,
                                                           RecOut ro, double t_max, double *gps,
-                                                          double *compass, TaskOut to) {
+                                                          double *compass, TaskOut to,
+                                                          unsigned *done) {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   const long long total = (long long)ev.n * cam.W;
-  if (g >= total) return;
-  const int e = (int)(g / cam.W);
-  const int j = (int)(g - (long long)e * cam.W);
-  if (j == 0) {  // before the ray: the env's task step
-    if (to.status[e] != 0) {
-      task_skip(to.tv, e, to.reward, to.dist, to.done);
-    } else {
-      const double px = ev.x[e], py = ev.y[e];
-      const double d_cur = distance_to_goal(sc, to.nv, to.tv, e, px, py);
-      task_finish(to.tv, e, to.actions[e], d_cur, ev.path[e], ev.coll[e], to.reward, to.dist,
-                  to.done, to.out);
+  if (g < total) {
+    const int e = (int)(g / cam.W);
+    const int j = (int)(g - (long long)e * cam.W);
+    if (j == 0) {  // before the ray: the env's task step
+      if (to.status[e] != 0) {
+        task_skip(to.tv, e, to.reward, to.dist, to.done);
+      } else {
+        const double px = ev.x[e], py = ev.y[e];
+        const double d_cur = distance_to_goal(sc, to.nv, to.tv, e, px, py);
+        task_finish(to.tv, e, to.actions[e], d_cur, ev.path[e], ev.coll[e], to.reward, to.dist,
+                    to.done, to.out);
+      }
     }
+    cast_column<false>(ev, sc, cam, e, j, ro, t_max, gps, compass);
   }
-  cast_column<false>(ev, sc, cam, e, j, ro, t_max, gps, compass);
+  if (done) {
+    __syncthreads();
+    if (threadIdx.x == 0) release_envs(done, blockIdx.x, (int)blockDim.x, cam.W, total);
+  }
+  asm volatile("griddepcontrol.wait;" ::: "memory");
 }
 
 __global__ void __launch_bounds__(128) k_column_cast_warp_task(EnvView ev, SceneView sc,
