@@ -367,3 +367,56 @@ def test_rebuilt_grid_invalidates_old_grid_objects(nb):
     m = np.empty((g1.height, g1.width), np.uint8)
     rc = g1.ctx.lib.nv_nav_copy(g1.ctx.handle, g1.width, g1.height, nat.ptr(m), None)
     assert rc == nat.NV_ERR_STATE
+
+
+def test_task_steps_overlap_agrees_at_scale(nb):
+    """The task-layer step with the cast -> writer release and the chained
+    agent step (thread-per-ray batch: 512 envs x 128 columns) gives the same
+    rewards, distances, done flags, poses, frames and EpisodeOutcome records
+    as the serialised launches (nv_set_overlap 0), bit for bit."""
+    import math
+    from oracle import nav_oracle as no
+    from paper_1904_01201_b200 import _native as nat
+    from paper_1904_01201_b200 import synth, task
+    from paper_1904_01201_b200.sensors import SensorConfig
+    sc = synth.config_scene("C2")
+    segs = sc.segments
+    og = no.Grid(segs, no.bounds(segs))
+    N, T = 512, 24
+    rng = np.random.default_rng(33)
+    cells = np.argwhere(og.navigable)
+    eps = []
+    while len(eps) < N:
+        s = og.center_of(*cells[int(rng.integers(len(cells)))])
+        g = og.center_of(*cells[int(rng.integers(len(cells)))])
+        eu = math.hypot(*(g - s))
+        if not (1.5 <= eu <= 6.0):
+            continue
+        eps.append(task.Episode(f"e{len(eps)}", "x", (float(s[0]), float(s[1])),
+                                float(rng.uniform(-math.pi, math.pi)), (float(g[0]), float(g[1])),
+                                max(1.0, eu), eu, max(1.0, eu) / eu))
+    acts = rng.choice(3, size=(T, N), p=[0.6, 0.2, 0.2]).astype(np.int8)
+    acts[T - 1] = 3
+    envs = []
+    for overlap in (0, 1):
+        env = task.BatchEnvironment((segs, sc.semantic_ids, sc.albedo), N,
+                                    sensor_configs=(SensorConfig("rgb", 128, 32),
+                                                    SensorConfig("depth", 128, 32)))
+        nat.check(env.sim.ctx.lib.nv_set_overlap(env.sim.ctx.handle, overlap))
+        env.reset(eps)
+        envs.append(env)
+    for t in range(T):
+        outs = []
+        for env in envs:
+            obs, done, info = env.step(torch.as_tensor(acts[t], device="cuda:0"))
+            torch.cuda.synchronize()
+            outs.append((done.clone(), info["d"].clone(), info["reward"].clone(),
+                         [v.clone() for v in env.sim.state()],
+                         {k: v.clone() for k, v in env.sim.observations().items()}))
+        (d0, dd0, r0, s0, o0), (d1, dd1, r1, s1, o1) = outs
+        assert torch.equal(d0, d1) and torch.equal(dd0, dd1) and torch.equal(r0, r1), t
+        for a, b in zip(s0, s1):
+            assert torch.equal(a, b), t
+        for k in o0:
+            assert torch.equal(o0[k], o1[k]), (t, k)
+    assert envs[0].outcomes() == envs[1].outcomes()
