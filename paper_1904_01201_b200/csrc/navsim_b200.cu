@@ -69,6 +69,9 @@ using namespace nvd;
 #ifndef NV_E2E_MAPPED
 #define NV_E2E_MAPPED 1  // host-buffer step: kernels read actions / write results in mapped pinned memory
 #endif
+#ifndef NV_E2E_PINGPONG
+#define NV_E2E_PINGPONG 1  // host-buffer steps alternate two graphs / streams / frame sets
+#endif
 #ifndef NV_NAV_HOSTLOOP
 #define NV_NAV_HOSTLOOP 0  // 1: distance-field relaxation as host-driven launches
 #endif
@@ -155,7 +158,10 @@ struct Camera {
   // device steps on other streams) and its device frames (nv_host_frames).
   DevBuf rec_e2e, lpt_order_e2e, lpt_cost_e2e;
   int64_t lpt_n_e2e = -1;
-  DevBuf e_rgb, e_depth, e_sem;
+  // two frame sets: consecutive host steps alternate (NV_E2E_PINGPONG), so a
+  // step's writer never writes the frames the previous step's writer may
+  // still be writing
+  DevBuf e_rgb[2], e_depth[2], e_sem[2];
 };
 
 }  // namespace
@@ -199,15 +205,21 @@ struct nv_ctx {
   DevBuf e_act, e_pack;  // e_pack: gps 16N | compass 8N | disp 8N | coll N
   // host-buffer path as one CUDA graph: H2D actions -> step+render -> one D2H
   // of the packed step results, replayed while (cam, channels, N) stay fixed
-  cudaStream_t e_stream = nullptr;
+  // Two host-step graphs on two streams, used alternately (NV_E2E_PINGPONG):
+  // graph p renders into record half / frame set p, so step t+1's agent step
+  // and casts (stream 1-p) need only step t's casts, not its frame writer --
+  // they take the SMs the writer frees, as in one long graph
+  cudaStream_t e_stream[2] = {nullptr, nullptr};
   cudaEvent_t e_ev = nullptr;
-  cudaEvent_t e_cast_ev = nullptr;  // recorded in the host-step graph after the casts
+  cudaEvent_t e_cast_ev[2] = {nullptr, nullptr};  // recorded in graph p after the casts
+  int e_par = 0;   // graph of the next host step
+  int e_last = 0;  // frame set of the last host step (nv_host_frames)
   cudaEvent_t mid_ev = nullptr;     // nv_step_render records it after the casts (capture only)
   bool e_pending = false;           // a host step's frame writer may still be running
   cudaStream_t o_stream = nullptr;  // side stream of the ordering kernel (beside the writer)
   cudaEvent_t o_ev0 = nullptr, o_ev1 = nullptr;
   bool o_fork = false;              // an ordering kernel was forked in this step
-  cudaGraphExec_t e_graph = nullptr;
+  cudaGraphExec_t e_graph[2] = {nullptr, nullptr};
   std::vector<uint64_t> e_key;  // everything the captured graph depends on (HostStepKey)
   void *e_out_host[4] = {nullptr, nullptr, nullptr, nullptr};  // last caller buffers
   void *e_out_dev[4] = {nullptr, nullptr, nullptr, nullptr};   // their device aliases
@@ -233,13 +245,15 @@ struct nv_ctx {
   int64_t prof_n[4] = {0, 0, 0, 0};
   ~nv_ctx() {
     for (auto e : prof_ev) cudaEventDestroy(e);
-    if (e_graph) cudaGraphExecDestroy(e_graph);
+    for (int p = 0; p < 2; ++p) {
+      if (e_graph[p]) cudaGraphExecDestroy(e_graph[p]);
+      if (e_cast_ev[p]) cudaEventDestroy(e_cast_ev[p]);
+      if (e_stream[p]) cudaStreamDestroy(e_stream[p]);
+    }
     if (e_ev) cudaEventDestroy(e_ev);
-    if (e_cast_ev) cudaEventDestroy(e_cast_ev);
     if (o_ev0) cudaEventDestroy(o_ev0);
     if (o_ev1) cudaEventDestroy(o_ev1);
     if (o_stream) cudaStreamDestroy(o_stream);
-    if (e_stream) cudaStreamDestroy(e_stream);
     if (e_hin) cudaFreeHost(e_hin);
     if (e_hout) cudaFreeHost(e_hout);
   }
@@ -839,7 +853,8 @@ int do_step(nv_ctx *c, const int8_t *actions, uint8_t *collided, double *disp, i
 int e2e_fence(nv_ctx *c) {
   if (c->e_pending) {
     c->e_pending = false;
-    CK(cudaStreamSynchronize(c->e_stream));
+    for (int p = 0; p < 2; ++p)
+      if (c->e_stream[p]) CK(cudaStreamSynchronize(c->e_stream[p]));
   }
   return NV_OK;
 }
@@ -1263,18 +1278,26 @@ int nv_step_render_host(nv_ctx *c, const int8_t *actions_host, int cam, uint32_t
   for (int q = 0; q < ncam; ++q) TRY(cam_check(c, cams[q]));
   cudaStream_t st = (cudaStream_t)stream;
   const size_t N = (size_t)c->n_envs;
+  // graph path: no host frames, no profiling, no noise (its frame counter
+  // advances per call) -- the common per-step case
+  const bool graph_ok = !frames_out && !c->prof_on && !(c->noise_sigma > 0.0);
+  // (one camera: with several, the next step's agent step would have to wait
+  // for every camera's casts, not just the first one's)
+  const int nsets = graph_ok && NV_E2E_PINGPONG && ncam == 1 ? 2 : 1;
   for (int q = 0; q < ncam; ++q) {
     Camera &k = c->cams[cams[q]];
     const size_t px = N * k.W * k.H;
-    if (chans[q] & NV_CH_RGB) TRY(k.e_rgb.alloc(px * 3));
-    if (chans[q] & NV_CH_DEPTH) TRY(k.e_depth.alloc(px * 4));
-    if (chans[q] & NV_CH_SEM) TRY(k.e_sem.alloc(px * 2));
+    for (int f = 0; f < nsets; ++f) {
+      if (chans[q] & NV_CH_RGB) TRY(k.e_rgb[f].alloc(px * 3));
+      if (chans[q] & NV_CH_DEPTH) TRY(k.e_depth[f].alloc(px * 4));
+      if (chans[q] & NV_CH_SEM) TRY(k.e_sem[f].alloc(px * 2));
+    }
   }
-  auto frame_ptrs = [&](int q, uint8_t *&r, float *&d, uint16_t *&s) {
+  auto frame_ptrs = [&](int q, int f, uint8_t *&r, float *&d, uint16_t *&s) {
     Camera &k = c->cams[cams[q]];
-    r = (chans[q] & NV_CH_RGB) ? k.e_rgb.as<uint8_t>() : nullptr;
-    d = (chans[q] & NV_CH_DEPTH) ? k.e_depth.as<float>() : nullptr;
-    s = (chans[q] & NV_CH_SEM) ? k.e_sem.as<uint16_t>() : nullptr;
+    r = (chans[q] & NV_CH_RGB) ? k.e_rgb[f].as<uint8_t>() : nullptr;
+    d = (chans[q] & NV_CH_DEPTH) ? k.e_depth[f].as<float>() : nullptr;
+    s = (chans[q] & NV_CH_SEM) ? k.e_sem[f].as<uint16_t>() : nullptr;
   };
   TRY(c->e_act.alloc(N));
   const size_t pack = 33 * N;
@@ -1282,14 +1305,14 @@ int nv_step_render_host(nv_ctx *c, const int8_t *actions_host, int cam, uint32_t
   uint8_t *pk = c->e_pack.as<uint8_t>();
   double *d_gps = reinterpret_cast<double *>(pk), *d_comp = d_gps + 2 * N, *d_disp = d_comp + N;
   uint8_t *d_coll = pk + 32 * N;
-  // graph path: no host frames, no profiling, no noise (its frame counter
-  // advances per call) -- the common per-step case
-  const bool graph_ok = !frames_out && !c->prof_on && !(c->noise_sigma > 0.0);
   if (graph_ok) {
-    if (!c->e_stream) {
-      // a blocking stream: ordered after the legacy default stream's work
+    if (!c->e_stream[0]) {
+      // blocking streams: ordered after the legacy default stream's work
       // implicitly, so callers on stream 0 need no event handshake
-      CK(cudaStreamCreate(&c->e_stream));
+      for (int p = 0; p < 2; ++p) {
+        CK(cudaStreamCreate(&c->e_stream[p]));
+        CK(cudaEventCreateWithFlags(&c->e_cast_ev[p], cudaEventDisableTiming));
+      }
       CK(cudaEventCreateWithFlags(&c->e_ev, cudaEventDisableTiming));
     }
     // pinned, mapped staging: with e2e_mapped the kernels read the actions
@@ -1329,7 +1352,6 @@ int nv_step_render_host(nv_ctx *c, const int8_t *actions_host, int cam, uint32_t
         c->e_out_dev[q] = at.devicePointer;
       }
     }
-    if (!c->e_cast_ev) CK(cudaEventCreateWithFlags(&c->e_cast_ev, cudaEventDisableTiming));
     // everything the graph's kernels touch exists before the key is taken
     // (a reallocated buffer changes the key: the graph is never replayed
     // into freed memory)
@@ -1357,20 +1379,25 @@ int nv_step_render_host(nv_ctx *c, const int8_t *actions_host, int cam, uint32_t
       for (int q = 0; q < 4; ++q) key.push_back((uint64_t)(uintptr_t)c->e_out_dev[q]);
     for (int q = 0; q < ncam; ++q) {
       const Camera &k = c->cams[cams[q]];
-      uint8_t *r; float *d; uint16_t *sm;
-      frame_ptrs(q, r, d, sm);
       for (uint64_t v : {(uint64_t)cams[q], (uint64_t)chans[q], (uint64_t)(uintptr_t)k.rec_e2e.p,
                          (uint64_t)(uintptr_t)k.rel_e2e.p,
-                         (uint64_t)(uintptr_t)k.lpt_order_e2e.p, (uint64_t)(uintptr_t)k.lpt_cost_e2e.p,
-                         (uint64_t)(uintptr_t)r, (uint64_t)(uintptr_t)d, (uint64_t)(uintptr_t)sm})
+                         (uint64_t)(uintptr_t)k.lpt_order_e2e.p, (uint64_t)(uintptr_t)k.lpt_cost_e2e.p})
         key.push_back(v);
+      for (int f = 0; f < nsets; ++f) {
+        uint8_t *r; float *d; uint16_t *sm;
+        frame_ptrs(q, f, r, d, sm);
+        for (uint64_t v : {(uint64_t)(uintptr_t)r, (uint64_t)(uintptr_t)d, (uint64_t)(uintptr_t)sm})
+          key.push_back(v);
+      }
     }
-    const bool same = c->e_graph && key == c->e_key;
-    cudaStream_t es = c->e_stream;
+    const bool same = c->e_graph[0] && key == c->e_key;
     if (!same) {
-      TRY(e2e_fence(c));  // the old graph's writer may still be running
-      if (c->e_graph) cudaGraphExecDestroy(c->e_graph);
-      c->e_graph = nullptr;
+      TRY(e2e_fence(c));  // the old graphs' writers may still be running
+      for (int p = 0; p < 2; ++p) {
+        if (c->e_graph[p]) cudaGraphExecDestroy(c->e_graph[p]);
+        c->e_graph[p] = nullptr;
+      }
+      c->e_par = 0;
       c->e_key.clear();
       const int8_t *acts = c->e_act.as<int8_t>();
       double *o_gps = d_gps, *o_comp = d_comp, *o_disp = d_disp;
@@ -1409,44 +1436,59 @@ int nv_step_render_host(nv_ctx *c, const int8_t *actions_host, int cam, uint32_t
           std::swap(k.lpt_n, k.lpt_n_e2e);
         }
       };
-      CK(cudaStreamBeginCapture(es, cudaStreamCaptureModeThreadLocal));
-      if (!c->e2e_mapped) cudaMemcpyAsync(c->e_act.p, c->e_hin, N, cudaMemcpyHostToDevice, es);
-      swap_e2e();
-      c->mid_ev = c->e2e_mapped ? c->e_cast_ev : nullptr;
-      uint8_t *r; float *d; uint16_t *sm;
-      frame_ptrs(0, r, d, sm);
-      int rc = nv_step_render(c, acts, cams[0], r, d, sm, o_gps, o_comp, o_coll, o_disp, nullptr, es);
-      c->mid_ev = nullptr;
-      for (int q = 1; q < ncam && rc == NV_OK; ++q) {
-        frame_ptrs(q, r, d, sm);
-        rc = nv_render(c, cams[q], r, d, sm, nullptr, nullptr, es);
+      // graph p: record half and release counters of the p-th render after
+      // the capture began (do_cast alternates them), frame set p
+      for (int p = 0; p < nsets; ++p) {
+        cudaStream_t es = c->e_stream[p];
+        CK(cudaStreamBeginCapture(es, cudaStreamCaptureModeThreadLocal));
+        if (!c->e2e_mapped) cudaMemcpyAsync(c->e_act.p, c->e_hin, N, cudaMemcpyHostToDevice, es);
+        swap_e2e();
+        c->mid_ev = c->e2e_mapped ? c->e_cast_ev[p] : nullptr;
+        uint8_t *r; float *d; uint16_t *sm;
+        frame_ptrs(0, p, r, d, sm);
+        int rc = nv_step_render(c, acts, cams[0], r, d, sm, o_gps, o_comp, o_coll, o_disp, nullptr, es);
+        c->mid_ev = nullptr;
+        for (int q = 1; q < ncam && rc == NV_OK; ++q) {
+          frame_ptrs(q, p, r, d, sm);
+          rc = nv_render(c, cams[q], r, d, sm, nullptr, nullptr, es);
+        }
+        swap_e2e();
+        if (!c->e2e_mapped) cudaMemcpyAsync(c->e_hout, pk, pack, cudaMemcpyDeviceToHost, es);
+        cudaGraph_t g = nullptr;
+        cudaError_t ce = cudaStreamEndCapture(es, &g);
+        if (rc != NV_OK) {
+          if (g) cudaGraphDestroy(g);
+          return rc;
+        }
+        if (ce != cudaSuccess) return fail(NV_ERR_CUDA, "graph capture failed: %s", cudaGetErrorString(ce));
+        ce = cudaGraphInstantiate(&c->e_graph[p], g, 0);
+        cudaGraphDestroy(g);
+        if (ce != cudaSuccess) return fail(NV_ERR_CUDA, "graph instantiate failed: %s", cudaGetErrorString(ce));
       }
-      swap_e2e();
-      if (!c->e2e_mapped) cudaMemcpyAsync(c->e_hout, pk, pack, cudaMemcpyDeviceToHost, es);
-      cudaGraph_t g = nullptr;
-      cudaError_t ce = cudaStreamEndCapture(es, &g);
-      if (rc != NV_OK) {
-        if (g) cudaGraphDestroy(g);
-        return rc;
-      }
-      if (ce != cudaSuccess) return fail(NV_ERR_CUDA, "graph capture failed: %s", cudaGetErrorString(ce));
-      ce = cudaGraphInstantiate(&c->e_graph, g, 0);
-      cudaGraphDestroy(g);
-      if (ce != cudaSuccess) return fail(NV_ERR_CUDA, "graph instantiate failed: %s", cudaGetErrorString(ce));
       c->e_key = key;
     }
+    // the previous host step's casts are complete (the host waited for them)
+    // and its writer uses the other record half and frame set: this step's
+    // agent step and casts may run beside that writer
+    const int p = nsets == 2 ? c->e_par : 0;
+    cudaStream_t es = c->e_stream[p];
     std::memcpy(c->e_hin, actions_host, N);
     if (st) {  // after the caller's prior work on its own stream
       CK(cudaEventRecord(c->e_ev, st));
       CK(cudaStreamWaitEvent(es, c->e_ev, 0));
     }
-    CK(cudaGraphLaunch(c->e_graph, es));
+    // (already complete: stream order made explicit)
+    if (nsets == 2) CK(cudaStreamWaitEvent(es, c->e_cast_ev[p ^ 1], 0));
+    CK(cudaGraphLaunch(c->e_graph[p], es));
     c->launches += 3 * ncam;
+    c->e_last = p;
+    c->e_par = p ^ (nsets - 1);
     if (c->e2e_mapped) {
       // the step results are in host memory once the casts are done; the
-      // frame writer finishes behind the caller (ordered before the next
-      // host step; nv_host_frames and reallocating calls wait for it)
-      CK(cudaEventSynchronize(c->e_cast_ev));
+      // frame writer finishes behind the caller (the next-but-one host step
+      // is ordered after it on its stream; nv_host_frames and reallocating
+      // calls wait for it)
+      CK(cudaEventSynchronize(c->e_cast_ev[p]));
       c->e_pending = true;
     } else {
       CK(cudaStreamSynchronize(es));
@@ -1460,23 +1502,24 @@ int nv_step_render_host(nv_ctx *c, const int8_t *actions_host, int cam, uint32_t
     return NV_OK;
   }
   TRY(e2e_fence(c));
+  c->e_last = 0;
   CK(cudaMemcpyAsync(c->e_act.p, actions_host, N, cudaMemcpyHostToDevice, st));
   {
     uint8_t *r; float *d; uint16_t *sm;
-    frame_ptrs(0, r, d, sm);
+    frame_ptrs(0, 0, r, d, sm);
     TRY(nv_step_render(c, c->e_act.as<int8_t>(), cams[0], r, d, sm, d_gps, d_comp, d_coll, d_disp,
                        nullptr, stream));
     for (int q = 1; q < ncam; ++q) {
-      frame_ptrs(q, r, d, sm);
+      frame_ptrs(q, 0, r, d, sm);
       TRY(nv_render(c, cams[q], r, d, sm, nullptr, nullptr, stream));
     }
   }
   {
     const Camera &k = c->cams[cams[0]];
     const size_t px = N * k.W * k.H;
-    if (rgb_host) CK(cudaMemcpyAsync(rgb_host, k.e_rgb.p, px * 3, cudaMemcpyDeviceToHost, st));
-    if (depth_host) CK(cudaMemcpyAsync(depth_host, k.e_depth.p, px * 4, cudaMemcpyDeviceToHost, st));
-    if (sem_host) CK(cudaMemcpyAsync(sem_host, k.e_sem.p, px * 2, cudaMemcpyDeviceToHost, st));
+    if (rgb_host) CK(cudaMemcpyAsync(rgb_host, k.e_rgb[0].p, px * 3, cudaMemcpyDeviceToHost, st));
+    if (depth_host) CK(cudaMemcpyAsync(depth_host, k.e_depth[0].p, px * 4, cudaMemcpyDeviceToHost, st));
+    if (sem_host) CK(cudaMemcpyAsync(sem_host, k.e_sem[0].p, px * 2, cudaMemcpyDeviceToHost, st));
   }
   if (gps_host || compass_host || collided_host || displacement_host) {
     std::vector<uint8_t> h(pack);
@@ -1496,9 +1539,9 @@ int nv_host_frames(nv_ctx *c, int cam, uint8_t **rgb, float **depth, uint16_t **
   if (cam < 0 || cam >= 8) return fail(NV_ERR_ARG, "camera index %d out of range [0, 8)", cam);
   TRY(e2e_fence(c));  // the frames are complete when this returns
   const Camera &k = c->cams[cam];
-  if (rgb) *rgb = k.e_rgb.as<uint8_t>();
-  if (depth) *depth = k.e_depth.as<float>();
-  if (sem) *sem = k.e_sem.as<uint16_t>();
+  if (rgb) *rgb = k.e_rgb[c->e_last].as<uint8_t>();
+  if (depth) *depth = k.e_depth[c->e_last].as<float>();
+  if (sem) *sem = k.e_sem[c->e_last].as<uint16_t>();
   return NV_OK;
 }
 

@@ -525,6 +525,52 @@ def test_chained_steps_agree_at_scale(nb, cfg, W, H, n, steps):
         assert torch.equal(a, b)
 
 
+@pytest.mark.gpu
+@pytest.mark.parametrize("pinned", [False, True])
+def test_host_steps_back_to_back_at_scale(nb, pinned):
+    """Host-buffer steps issued back to back at the bench's batch size: each
+    step's agent step and casts run beside the previous step's frame writer
+    (alternating graphs, record halves and frame sets), and every step's host
+    results and the final frames equal a serialised device-path replica."""
+    from paper_1904_01201_b200 import synth
+    sc = synth.config_scene("C3")
+    W, H, n, steps = 256, 256, 1024, 7
+    suite = (nb.SensorConfig("rgb", W, H), nb.SensorConfig("depth", W, H),
+             nb.SensorConfig("gps_compass"))
+    a, b = (nb.BatchSimulator(sc.segments, sc.semantic_ids, sc.albedo, n, sensor_configs=suite,
+                              floor_color=sc.floor_color, ceiling_color=sc.ceiling_color)
+            for _ in range(2))
+    poses = synth.sample_poses(sc, n, seed=61)
+    for s in (a, b):
+        s.reset(poses[:, :2], poses[:, 2])
+    acts = synth.random_actions(n, steps, seed=62)
+    if pinned:  # mapped host buffers: the kernels write the caller's arrays
+        out = {"gps": torch.empty((n, 2), dtype=torch.float64).pin_memory(),
+               "compass": torch.empty(n, dtype=torch.float64).pin_memory(),
+               "collided": torch.empty(n, dtype=torch.uint8).pin_memory(),
+               "displacement": torch.empty(n, dtype=torch.float64).pin_memory()}
+    else:
+        out = {"gps": np.empty((n, 2)), "compass": np.empty(n), "collided": np.empty(n, np.uint8),
+               "displacement": np.empty(n)}
+    got = []
+    for t in range(steps):
+        a.step_host(np.ascontiguousarray(acts[t]), out=out)
+        got.append({k: (v.numpy() if hasattr(v, "numpy") else v).copy() for k, v in out.items()})
+    for t in range(steps):
+        b.step(torch.as_tensor(np.ascontiguousarray(acts[t]), device="cuda:0"))
+        torch.cuda.synchronize()
+        assert np.array_equal(got[t]["gps"], b.gps.cpu().numpy()), t
+        assert np.array_equal(got[t]["compass"], b.compass.cpu().numpy()), t
+        assert np.array_equal(got[t]["collided"], b.collided.cpu().numpy()), t
+        assert np.array_equal(got[t]["displacement"], b.displacement.cpu().numpy()), t
+    fr = a.host_step_frames()
+    torch.cuda.synchronize()
+    assert torch.equal(fr["rgb"], b.groups[0]["rgb"])
+    assert torch.equal(fr["depth"], b.groups[0]["depth"])
+    for x, y in zip(a.state(), b.state()):
+        assert torch.equal(x, y)
+
+
 def test_host_buffer_path_matches_device_path(nb):
     """nv_step_render_host (graph-replayed, packed results) gives the same step
     results as nv_step_render on device buffers, across repeated
