@@ -173,8 +173,11 @@ int nv_set_fill_mode(nv_ctx *ctx, int mode);
  * and returns as soon as its casts are done (the results are complete then);
  * the frame writer finishes behind the caller on the step's own record
  * buffer and counters (device steps on any stream may follow at once),
- * ordered before the next host step and before nv_host_frames /
- * nv_camera_config / nv_envs_alloc / nv_scene_upload / nv_destroy return.
+ * before nv_host_frames / nv_camera_config / nv_envs_alloc / nv_scene_upload
+ * / nv_destroy return.  With one camera, consecutive host steps alternate
+ * between two graphs, streams, record halves and frame sets: the next host
+ * step's agent step and casts run beside this step's writer (they depend only
+ * on this step's casts), the next-but-one is ordered after it.
  * With host frame pointers the call synchronises before returning. */
 #define NV_CH_RGB 1u
 #define NV_CH_DEPTH 2u
@@ -185,9 +188,11 @@ int nv_step_render_host(nv_ctx *ctx, const int8_t *actions_host, int cam,
                         uint16_t *sem_host, double *gps_host,
                         double *compass_host, uint8_t *collided_host,
                         double *displacement_host, void *stream);
-/* Device frame buffers of camera `cam` written by nv_step_render_host
- * (complete when this returns, valid until the next call; for a GPU consumer
- * of the host-driven path; NULL for channels never rendered). */
+/* Device frame buffers of camera `cam` written by the last
+ * nv_step_render_host (complete when this returns; for a GPU consumer of the
+ * host-driven path; NULL for channels never rendered).  The pointers
+ * alternate between two frame sets from one host step to the next: the
+ * frames stay valid until the next-but-one host step starts. */
 int nv_host_frames(nv_ctx *ctx, int cam, uint8_t **rgb, float **depth, uint16_t **sem);
 
 /* gps_compass (sensors.py:175-180) alone, for suites without visual sensors.
