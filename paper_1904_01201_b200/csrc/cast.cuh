@@ -241,17 +241,52 @@ __device__ __forceinline__ void release_envs(unsigned *done, long long blk, int 
   }
 }
 
+// Release-mode side of the agent -> cast overlap: lane 0 of each warp
+// acquires the ready flags of the envs of the warp's rays [r0, r1] and the
+// warp proceeds (no CTA barrier, no atomics: the flags of this record half
+// are reset by the frame writer once it has consumed the env, see
+// wait_env_cast).  A wait longer than 200 ms raises `fault` and stops waiting,
+// so a broken launch can never hang the GPU.
+__device__ __forceinline__ void warp_wait_envs_ready(const unsigned *ready, unsigned *fault,
+                                                     unsigned r0, unsigned r1, unsigned W) {
+  if ((threadIdx.x & 31) == 0) {
+    for (unsigned e = r0 / W; e <= r1 / W; ++e) {
+      unsigned v;
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ready + e) : "memory");
+      if (v) continue;
+      unsigned long long t0, t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+      do {
+        __nanosleep(64);
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ready + e) : "memory");
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        if (!v && (t - t0 > 200000000ull || *reinterpret_cast<volatile unsigned *>(fault))) {
+          atomicExch(fault, 1u);
+          v = 1;
+        }
+      } while (!v);
+    }
+  }
+  __syncwarp();
+}
+
 // With `ready`: a programmatic dependent of k_agent_step, waiting per env.
+// `trigger`: a frame writer follows as this grid's programmatic dependent (it
+// may launch once every cast CTA runs); without one the grid does not trigger,
+// so a following agent step (a programmatic dependent of whatever precedes it)
+// cannot start while the casts still read the env state.
 #ifndef NV_CASTW_MINB
 #define NV_CASTW_MINB 8  // min resident CTAs/SM for the warp-per-ray cast (register cap <= 64; C2 31.1 -> 28.9 us/step)
 #endif
 __global__ void __launch_bounds__(128, NV_CASTW_MINB) k_column_cast_warp(EnvView ev, SceneView sc, CamView cam,
                                                           RecOut ro, double t_max, double *gps,
                                                           double *compass, unsigned *ready,
-                                                          unsigned *arrive, const unsigned *order,
-                                                          unsigned *cost, unsigned *done) {
+                                                          unsigned *arrive, unsigned *rfault,
+                                                          const unsigned *order, unsigned *cost,
+                                                          unsigned *done, bool trigger) {
+  (void)rfault;  // the warp cast always resets its ready flags itself (arrive)
   // `order` / `cost`: longest-first block order, as in k_column_cast
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // see k_column_cast
+  if (trigger) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // see k_column_cast
   const long long blk = order ? (long long)__ldg(order + blockIdx.x) : (long long)blockIdx.x;
   long long t0 = 0;
   if (order && threadIdx.x == 0) t0 = clock64();
@@ -285,8 +320,9 @@ __global__ void __launch_bounds__(128, NV_CAST_KMINB) k_column_cast(EnvView ev, 
                                                      RecOut ro, double t_max,
                                                      double *gps, double *compass,
                                                      unsigned *ready, unsigned *arrive,
-                                                     const unsigned *order, unsigned *cost,
-                                                     unsigned *done) {
+                                                     unsigned *rfault, const unsigned *order,
+                                                     unsigned *cost, unsigned *done,
+                                                     bool trigger) {
   // With `order`: CTA b casts ray block order[b] (blocks the previous step
   // found slowest first -- longest-processing-time order, so the grid's last
   // wave is made of short blocks) and records its block's duration in
@@ -294,13 +330,25 @@ __global__ void __launch_bounds__(128, NV_CAST_KMINB) k_column_cast(EnvView ev, 
   // visit order inside each ray are unchanged.
   // the frame writer (a programmatic dependent) may launch once every cast
   // CTA is running: its set-up then overlaps the cast's tail
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  if (trigger) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const long long blk = order ? (long long)__ldg(order + blockIdx.x) : (long long)blockIdx.x;
   long long t0 = 0;
   if (order && threadIdx.x == 0) t0 = clock64();
   const long long total = (long long)ev.n * cam.W;
-  if (ready) wait_envs_ready(ready, arrive, cam.W, total, 0, blk);
+#ifndef NV_STUDY_NOWAIT
+#define NV_STUDY_NOWAIT 0  // 1: timing-only study, the cast does not wait for the agent step
+#endif
   const long long g = blk * (long long)blockDim.x + threadIdx.x;
+  if (ready && !NV_STUDY_NOWAIT) {
+    if (arrive) {
+      wait_envs_ready(ready, arrive, cam.W, total, 0, blk);
+    } else {  // release mode: per warp, flags reset by the writer
+      const long long w0 = blk * (long long)blockDim.x + (threadIdx.x & ~31u);
+      if (w0 < total)
+        warp_wait_envs_ready(ready, rfault, (unsigned)w0, (unsigned)min(total - 1, w0 + 31),
+                             (unsigned)cam.W);
+    }
+  }
   if (g < total) {
     // 32-bit division whenever the ray count fits (always, in practice)
     const int e = total <= 0xffffffffLL ? (int)((unsigned)g / (unsigned)cam.W) : (int)(g / cam.W);

@@ -57,6 +57,9 @@ struct FillArgs {
   // dependent): finished-column counts, band consumers, timeout flag;
   // nullptr = the records are complete when the writer's loads start
   unsigned *done, *consumed, *fault;
+  // agent -> cast ready flags of this record half (release mode of
+  // nv_step_render): reset by the env's last consumer, like done
+  unsigned *ready;
 };
 
 // ---- inverse-depth noise ---------------------------------------------------
@@ -425,7 +428,8 @@ __device__ __forceinline__ bool env_cast_done(const unsigned *done, int env, int
 // record half serve the next step).  A wait longer than 200 ms raises the
 // fault flag and stops waiting, so a broken launch can never hang the GPU.
 __device__ __forceinline__ void wait_env_cast(unsigned *done, unsigned *consumed,
-                                              unsigned *fault, int env, int W, int bands) {
+                                              unsigned *fault, unsigned *ready, int env, int W,
+                                              int bands) {
   if (!env_cast_done(done, env, W)) {
     const unsigned long long t0 = global_ns();
     while (!env_cast_done(done, env, W)) {
@@ -441,6 +445,7 @@ __device__ __forceinline__ void wait_env_cast(unsigned *done, unsigned *consumed
   if (bands == 1 || atomicAdd(consumed + env, 1u) == (unsigned)(bands - 1)) {
     if (bands > 1) consumed[env] = 0;
     done[env] = 0;
+    if (ready) ready[env] = 0;  // every cast CTA of the env is past its wait
   }
 }
 
@@ -509,7 +514,7 @@ __global__ void NV_FILL_BOUNDS k_fill_ws(FillArgs a, FillWsLayout L) {
       if (lane != 0) return;
       int it = 0;
       for (int q = blockIdx.x; q < n_items; q += gridDim.x, ++it) {
-        wait_env_cast(a.done, a.consumed, a.fault, q / bands, W, bands);
+        wait_env_cast(a.done, a.consumed, a.fault, a.ready, q / bands, W, bands);
         if (it >= NV_WS_CBUF)
           mbar_wait(colempty + (it % NV_WS_CBUF), (unsigned)(((it / NV_WS_CBUF) - 1) & 1));
         load_item(it % NV_WS_CBUF, q / bands);

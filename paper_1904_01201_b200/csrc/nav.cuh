@@ -526,7 +526,9 @@ __global__ void __launch_bounds__(128) k_column_cast_task(EnvView ev, SceneView 
                                                           RecOut ro, double t_max, double *gps,
                                                           double *compass, TaskOut to,
                                                           unsigned *done) {
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  // triggers only when the writer follows as its programmatic dependent
+  // (release), see k_column_cast
+  if (done) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   const long long total = (long long)ev.n * cam.W;
   if (g < total) {

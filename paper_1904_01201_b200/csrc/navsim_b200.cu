@@ -69,6 +69,9 @@ using namespace nvd;
 #ifndef NV_E2E_MAPPED
 #define NV_E2E_MAPPED 1  // host-buffer step: kernels read actions / write results in mapped pinned memory
 #endif
+#ifndef NV_READY_BY_HALF
+#define NV_READY_BY_HALF 1  // release mode: per-warp ready waits, flags per record half reset by the writer
+#endif
 #ifndef NV_E2E_PINGPONG
 #define NV_E2E_PINGPONG 1  // host-buffer steps alternate two graphs / streams / frame sets
 #endif
@@ -231,6 +234,10 @@ struct nv_ctx {
   bool e2e_mapped = NV_E2E_MAPPED != 0;  // host-buffer graph path: zero-copy actions / results
   bool pdl = true;           // agent step -> cast programmatic dependent launch (nv_set_overlap)
   bool pdl_armed = false, pdl_init = false;
+  // flags of the armed agent -> cast handshake: ready (per env), arrive
+  // (nullptr in release mode: the writer resets the flags), fault
+  unsigned *pdl_cur_ready = nullptr, *pdl_cur_arrive = nullptr;
+  unsigned *fill_ready = nullptr;  // ready flags the next release writer resets
   bool fill_pdl = false;  // the next ws writer launch follows its column cast (launch_ws_kernel)
   DevBuf pdl_ready, pdl_arrive;
   // dynamic shared memory opted in per kernel on this context's device
@@ -643,6 +650,7 @@ int launch_fill(nv_ctx *c, Camera &cam, int64_t N, uint8_t *rgb, float *depth, u
   a.done = release ? rel_done(cam, N) : nullptr;
   a.consumed = release ? rel_done(cam, N) + N : nullptr;
   a.fault = release ? rel_fault(cam, N) : nullptr;
+  a.ready = release ? c->fill_ready : nullptr;
   const RecOut ro = rec_out(cam, N);
   a.ra = ro.a;
   a.rb = ro.b;
@@ -750,8 +758,11 @@ int lpt_fork(nv_ctx *c, cudaStream_t st, unsigned *order, unsigned *cost, unsign
 
 // release: publish per-env finished-column counts for a writer launched as
 // this cast's programmatic dependent (k_fill_ws with FillArgs.done)
+unsigned *pdl_fault(nv_ctx *c);
+
+// trigger: a frame writer follows as the cast's programmatic dependent
 int do_cast(nv_ctx *c, int cam, double *gps, double *compass, cudaStream_t st,
-            bool release = false) {
+            bool release = false, bool trigger = false) {
   Camera &k = c->cams[cam];
   // t_max = max_range: capping the walk is output-identical for rendered
   // frames (tests/test_gpu_parity.py checks it against the
@@ -770,7 +781,7 @@ int do_cast(nv_ctx *c, int cam, double *gps, double *compass, cudaStream_t st,
   {
     Prof pf(c, st, 1);
     auto kern = warp ? nvk::k_column_cast_warp : nvk::k_column_cast;
-    unsigned *ready = nullptr, *arrive = nullptr;
+    unsigned *ready = nullptr, *arrive = nullptr, *rfault = nullptr;
     cudaLaunchConfig_t lc = {};
     lc.gridDim = dim3(nblk);
     lc.blockDim = dim3(threads);
@@ -778,17 +789,18 @@ int do_cast(nv_ctx *c, int cam, double *gps, double *compass, cudaStream_t st,
     cudaLaunchAttribute at[1];
     if (c->pdl_armed) {  // programmatic dependent of the agent step just launched
       c->pdl_armed = false;
-      ready = c->pdl_ready.as<unsigned>();
-      arrive = c->pdl_arrive.as<unsigned>();
+      ready = c->pdl_cur_ready;
+      arrive = c->pdl_cur_arrive;
+      rfault = pdl_fault(c);
       at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
       at[0].val.programmaticStreamSerializationAllowed = 1;
       lc.attrs = at;
       lc.numAttrs = 1;
     }
     CK(cudaLaunchKernelEx(&lc, kern, c->env_view(), c->scene_view(), cam_view(k),
-                          rec_out(k, c->n_envs), k.max_range, gps, compass, ready, arrive,
+                          rec_out(k, c->n_envs), k.max_range, gps, compass, ready, arrive, rfault,
                           (const unsigned *)order, cost,
-                          release ? rel_done(k, c->n_envs) : (unsigned *)nullptr));
+                          release ? rel_done(k, c->n_envs) : (unsigned *)nullptr, trigger));
     TRY(check_launch(c));
   }
   return order ? lpt_fork(c, st, order, cost, nblk) : NV_OK;
@@ -804,26 +816,45 @@ int lpt_join(nv_ctx *c, cudaStream_t st) {
 }
 
 // per-env ready / arrive flags of the agent -> cast overlap (zero between steps)
+// ready: [release half 0 | release half 1 | arrive mode] x N, then the fault
+// flag of the release-mode waits.  The release-mode flags of a record half are
+// reset by the writer that consumes them, the arrive-mode ones by the casts;
+// separate sets, so mixing the modes between steps never loses a flag.
 int pdl_buffers(nv_ctx *c) {
-  const size_t b = sizeof(unsigned) * (size_t)std::max<int64_t>(1, c->n_envs);
+  const size_t n = (size_t)std::max<int64_t>(1, c->n_envs);
+  const size_t b = sizeof(unsigned) * (3 * n + 1);
   if (c->pdl_ready.bytes < b || !c->pdl_init) {
     TRY(c->pdl_ready.alloc(b));
-    TRY(c->pdl_arrive.alloc(b));
+    TRY(c->pdl_arrive.alloc(sizeof(unsigned) * n));
     CK(cudaMemset(c->pdl_ready.p, 0, b));
-    CK(cudaMemset(c->pdl_arrive.p, 0, b));
+    CK(cudaMemset(c->pdl_arrive.p, 0, sizeof(unsigned) * n));
     c->pdl_init = true;
   }
   return NV_OK;
 }
+// the ready flags of a step: release mode -> the set of the record half the
+// coming casts write, else the arrive-mode set
+unsigned *pdl_ready_set(nv_ctx *c, int release_half) {
+  const size_t n = (size_t)std::max<int64_t>(1, c->n_envs);
+  return c->pdl_ready.as<unsigned>() + (release_half >= 0 ? (size_t)release_half : 2) * n;
+}
+unsigned *pdl_fault(nv_ctx *c) {
+  return c->pdl_ready.as<unsigned>() + 3 * (size_t)std::max<int64_t>(1, c->n_envs);
+}
 
+// arm_pdl: the cast that follows is this agent step's programmatic dependent;
+// release_half >= 0: release mode (the casts write that record half, its
+// frame writer resets the ready flags), -1: the casts reset them (arrive)
 int do_step(nv_ctx *c, const int8_t *actions, uint8_t *collided, double *disp, int32_t *status,
-            cudaStream_t st, bool arm_pdl = false) {
+            cudaStream_t st, bool arm_pdl = false, int release_half = -1) {
   nvk::AgentCfg cfg{c->radius, c->step, c->turn_rad};
   long long threads = c->n_envs * 32;
   unsigned *ready = nullptr;
   if (arm_pdl) {
     TRY(pdl_buffers(c));
-    ready = c->pdl_ready.as<unsigned>();
+    ready = pdl_ready_set(c, release_half);
+    c->pdl_cur_ready = ready;
+    c->pdl_cur_arrive = release_half >= 0 ? nullptr : c->pdl_arrive.as<unsigned>();
   }
   Prof pf(c, st, 0);
   {
@@ -1181,7 +1212,7 @@ int nv_render(nv_ctx *c, int cam, uint8_t *rgb, float *depth, uint16_t *sem, dou
   TRY(ensure_envs(c));
   TRY(cam_check(c, cam));
   cudaStream_t st = (cudaStream_t)stream;
-  TRY(do_cast(c, cam, gps, compass, st));
+  TRY(do_cast(c, cam, gps, compass, st, false, rgb || depth || sem));
   const int rc = launch_fill(c, c->cams[cam], c->n_envs, rgb, depth, sem, st);
   TRY(lpt_join(c, st));
   return rc;
@@ -1200,7 +1231,6 @@ int nv_step_render(nv_ctx *c, const int8_t *actions, int cam, uint8_t *rgb, floa
   // profiling events are on (an event between the two launches would break
   // the programmatic edge)
   const bool pdl = c->pdl && !c->prof_on;
-  TRY(do_step(c, actions, collided, displacement, status, st, pdl));
   // cast -> writer programmatic launch (set-up beside the cast's tail); with
   // the ws writer, per-env release
   c->fill_pdl = NV_FILL_PDL && c->pdl && !c->prof_on;
@@ -1209,7 +1239,12 @@ int nv_step_render(nv_ctx *c, const int8_t *actions, int cam, uint8_t *rgb, floa
   const bool release = c->fill_pdl && NV_FILL_RELEASE && (rgb || depth || sem) &&
                        c->fill_mode != NV_FILL_GENERIC && ws_layout_ok(k, rgb, depth, sem) &&
                        !use_warp_cast(c, c->n_envs * (long long)k.W);
-  TRY(do_cast(c, cam, gps, compass, st, release));
+  // release mode: the agent -> cast ready flags of the record half the casts
+  // are about to write (do_cast flips to it), reset by that half's writer
+  const int rhalf = release && NV_READY_BY_HALF ? (k.rec_half ^ 1) : -1;
+  TRY(do_step(c, actions, collided, displacement, status, st, pdl, rhalf));
+  c->fill_ready = pdl && rhalf >= 0 ? c->pdl_cur_ready : nullptr;
+  TRY(do_cast(c, cam, gps, compass, st, release, rgb || depth || sem));
   c->pdl_armed = false;
   if (c->mid_ev) {  // on the side stream: no node between the casts and the writer
     TRY(side_fork(c, st));
@@ -1217,6 +1252,7 @@ int nv_step_render(nv_ctx *c, const int8_t *actions, int cam, uint8_t *rgb, floa
   }
   const int rc = launch_fill(c, k, c->n_envs, rgb, depth, sem, st, release);
   c->fill_pdl = false;
+  c->fill_ready = nullptr;
   TRY(lpt_join(c, st));
   return rc;
 }

@@ -525,6 +525,45 @@ def test_chained_steps_agree_at_scale(nb, cfg, W, H, n, steps):
         assert torch.equal(a, b)
 
 
+def test_steps_without_frames_back_to_back(nb):
+    """nv_step_render with no frame channels (no writer after the casts),
+    issued back to back at a thread-per-ray batch: the casts then do not
+    trigger the next step's agent step early, so every step's gps / compass
+    and the final state equal the serialised launches (nv_set_overlap 0)."""
+    from paper_1904_01201_b200 import _native as nat
+    from paper_1904_01201_b200 import synth
+    sc = synth.config_scene("C3")
+    W, H, n, steps = 256, 64, 512, 6
+    suite = (nb.SensorConfig("depth", W, H), nb.SensorConfig("gps_compass"))
+    sims = []
+    for overlap in (0, 1):
+        sim = nb.BatchSimulator(sc.segments, sc.semantic_ids, sc.albedo, n, sensor_configs=suite)
+        nat.check(sim.ctx.lib.nv_set_overlap(sim.ctx.handle, overlap))
+        poses = synth.sample_poses(sc, n, seed=71)
+        sim.reset(poses[:, :2], poses[:, 2])
+        sims.append(sim)
+    acts = torch.as_tensor(synth.random_actions(n, steps, seed=72), device="cuda:0")
+    outs = []
+    for k, sim in enumerate(sims):
+        cam = sim.groups[0]["cam"]
+        gps = torch.empty((steps, n, 2), dtype=torch.float64, device="cuda:0")
+        comp = torch.empty((steps, n), dtype=torch.float64, device="cuda:0")
+        st = nat.stream_handle()
+        for s in range(steps):
+            nat.check(sim.ctx.lib.nv_step_render(
+                sim.ctx.handle, nat.ptr(acts[s]), cam, None, None, None, nat.ptr(gps[s]),
+                nat.ptr(comp[s]), None, None, None, st))
+            if k == 0:
+                torch.cuda.synchronize()
+        torch.cuda.synchronize()
+        outs.append((gps, comp, sim.state()))
+    (g0, c0, s0), (g1, c1, s1) = outs
+    assert torch.equal(g0, g1)
+    assert torch.equal(c0, c1)
+    for a, b in zip(s0, s1):
+        assert torch.equal(a, b)
+
+
 @pytest.mark.gpu
 @pytest.mark.parametrize("pinned", [False, True])
 def test_host_steps_back_to_back_at_scale(nb, pinned):
