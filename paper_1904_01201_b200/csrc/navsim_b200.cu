@@ -72,6 +72,9 @@ using namespace nvd;
 #ifndef NV_READY_BY_HALF
 #define NV_READY_BY_HALF 1  // release mode: per-warp ready waits, flags per record half reset by the writer
 #endif
+#ifndef NV_E2E_ACT_COPY
+#define NV_E2E_ACT_COPY 0  // mapped host step: copy the actions in (a graph copy node) instead of reading them over PCIe
+#endif
 #ifndef NV_E2E_PINGPONG
 #define NV_E2E_PINGPONG 1  // host-buffer steps alternate two graphs / streams / frame sets
 #endif
@@ -221,6 +224,14 @@ struct nv_ctx {
   bool e_pending = false;           // a host step's frame writer may still be running
   cudaStream_t o_stream = nullptr;  // side stream of the ordering kernel (beside the writer)
   cudaEvent_t o_ev0 = nullptr, o_ev1 = nullptr;
+  // capture only: a branch of its own for the host event after the casts (the
+  // ordering kernel's branch would hold it back by that kernel's duration),
+  // and the event recorded after the ordering kernel (the next host step's
+  // casts read its order)
+  cudaStream_t m_stream = nullptr;
+  cudaEvent_t m_ev0 = nullptr, m_ev1 = nullptr;
+  cudaEvent_t order_ev = nullptr;
+  cudaEvent_t e_order_ev[2] = {nullptr, nullptr};
   bool o_fork = false;              // an ordering kernel was forked in this step
   cudaGraphExec_t e_graph[2] = {nullptr, nullptr};
   std::vector<uint64_t> e_key;  // everything the captured graph depends on (HostStepKey)
@@ -261,6 +272,11 @@ struct nv_ctx {
     if (o_ev0) cudaEventDestroy(o_ev0);
     if (o_ev1) cudaEventDestroy(o_ev1);
     if (o_stream) cudaStreamDestroy(o_stream);
+    if (m_ev0) cudaEventDestroy(m_ev0);
+    if (m_ev1) cudaEventDestroy(m_ev1);
+    if (m_stream) cudaStreamDestroy(m_stream);
+    for (int p = 0; p < 2; ++p)
+      if (e_order_ev[p]) cudaEventDestroy(e_order_ev[p]);
     if (e_hin) cudaFreeHost(e_hin);
     if (e_hout) cudaFreeHost(e_hout);
   }
@@ -810,6 +826,7 @@ int do_cast(nv_ctx *c, int cam, double *gps, double *compass, cudaStream_t st,
 int lpt_join(nv_ctx *c, cudaStream_t st) {
   if (!c->o_fork) return NV_OK;
   c->o_fork = false;
+  if (c->order_ev) CK(cudaEventRecordWithFlags(c->order_ev, c->o_stream, cudaEventRecordExternal));
   CK(cudaEventRecord(c->o_ev1, c->o_stream));
   CK(cudaStreamWaitEvent(st, c->o_ev1, 0));
   return NV_OK;
@@ -1246,14 +1263,24 @@ int nv_step_render(nv_ctx *c, const int8_t *actions, int cam, uint8_t *rgb, floa
   c->fill_ready = pdl && rhalf >= 0 ? c->pdl_cur_ready : nullptr;
   TRY(do_cast(c, cam, gps, compass, st, release, rgb || depth || sem));
   c->pdl_armed = false;
-  if (c->mid_ev) {  // on the side stream: no node between the casts and the writer
-    TRY(side_fork(c, st));
-    CK(cudaEventRecordWithFlags(c->mid_ev, c->o_stream, cudaEventRecordExternal));
+  if (c->mid_ev) {  // on a branch of its own: no node between the casts and the writer
+    if (!c->m_stream) {
+      CK(cudaStreamCreateWithFlags(&c->m_stream, cudaStreamNonBlocking));
+      CK(cudaEventCreateWithFlags(&c->m_ev0, cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&c->m_ev1, cudaEventDisableTiming));
+    }
+    CK(cudaEventRecord(c->m_ev0, st));
+    CK(cudaStreamWaitEvent(c->m_stream, c->m_ev0, 0));
+    CK(cudaEventRecordWithFlags(c->mid_ev, c->m_stream, cudaEventRecordExternal));
   }
   const int rc = launch_fill(c, k, c->n_envs, rgb, depth, sem, st, release);
   c->fill_pdl = false;
   c->fill_ready = nullptr;
   TRY(lpt_join(c, st));
+  if (c->mid_ev) {
+    CK(cudaEventRecord(c->m_ev1, c->m_stream));
+    CK(cudaStreamWaitEvent(st, c->m_ev1, 0));
+  }
   return rc;
 }
 
@@ -1348,6 +1375,7 @@ int nv_step_render_host(nv_ctx *c, const int8_t *actions_host, int cam, uint32_t
       for (int p = 0; p < 2; ++p) {
         CK(cudaStreamCreate(&c->e_stream[p]));
         CK(cudaEventCreateWithFlags(&c->e_cast_ev[p], cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&c->e_order_ev[p], cudaEventDisableTiming));
       }
       CK(cudaEventCreateWithFlags(&c->e_ev, cudaEventDisableTiming));
     }
@@ -1442,7 +1470,7 @@ int nv_step_render_host(nv_ctx *c, const int8_t *actions_host, int cam, uint32_t
         void *din = nullptr, *dout = nullptr;
         CK(cudaHostGetDevicePointer(&din, c->e_hin, 0));
         CK(cudaHostGetDevicePointer(&dout, c->e_hout, 0));
-        acts = static_cast<const int8_t *>(din);
+        if (!NV_E2E_ACT_COPY) acts = static_cast<const int8_t *>(din);
         o_gps = static_cast<double *>(dout);
         o_comp = o_gps + 2 * N;
         o_disp = o_comp + N;
@@ -1477,13 +1505,16 @@ int nv_step_render_host(nv_ctx *c, const int8_t *actions_host, int cam, uint32_t
       for (int p = 0; p < nsets; ++p) {
         cudaStream_t es = c->e_stream[p];
         CK(cudaStreamBeginCapture(es, cudaStreamCaptureModeThreadLocal));
-        if (!c->e2e_mapped) cudaMemcpyAsync(c->e_act.p, c->e_hin, N, cudaMemcpyHostToDevice, es);
+        if (!c->e2e_mapped || NV_E2E_ACT_COPY)
+          cudaMemcpyAsync(c->e_act.p, c->e_hin, N, cudaMemcpyHostToDevice, es);
         swap_e2e();
         c->mid_ev = c->e2e_mapped ? c->e_cast_ev[p] : nullptr;
+        c->order_ev = nsets == 2 ? c->e_order_ev[p] : nullptr;
         uint8_t *r; float *d; uint16_t *sm;
         frame_ptrs(0, p, r, d, sm);
         int rc = nv_step_render(c, acts, cams[0], r, d, sm, o_gps, o_comp, o_coll, o_disp, nullptr, es);
         c->mid_ev = nullptr;
+        c->order_ev = nullptr;
         for (int q = 1; q < ncam && rc == NV_OK; ++q) {
           frame_ptrs(q, p, r, d, sm);
           rc = nv_render(c, cams[q], r, d, sm, nullptr, nullptr, es);
@@ -1513,8 +1544,10 @@ int nv_step_render_host(nv_ctx *c, const int8_t *actions_host, int cam, uint32_t
       CK(cudaEventRecord(c->e_ev, st));
       CK(cudaStreamWaitEvent(es, c->e_ev, 0));
     }
-    // (already complete: stream order made explicit)
-    if (nsets == 2) CK(cudaStreamWaitEvent(es, c->e_cast_ev[p ^ 1], 0));
+    // the previous step's casts are complete (the host waited for them); its
+    // ordering kernel, which writes the block order this step's casts read,
+    // may still run
+    if (nsets == 2) CK(cudaStreamWaitEvent(es, c->e_order_ev[p ^ 1], 0));
     CK(cudaGraphLaunch(c->e_graph[p], es));
     c->launches += 3 * ncam;
     c->e_last = p;
