@@ -241,6 +241,9 @@ __device__ __forceinline__ void release_envs(unsigned *done, long long blk, int 
   }
 }
 
+#ifndef NV_STUDY_NOWAIT
+#define NV_STUDY_NOWAIT 0  // timing-only studies: 1 the cast does not wait for the agent step, 2 one acquire without spinning
+#endif
 // Release-mode side of the agent -> cast overlap: lane 0 of each warp
 // acquires the ready flags of the envs of the warp's rays [r0, r1] and the
 // warp proceeds (no CTA barrier, no atomics: the flags of this record half
@@ -253,7 +256,7 @@ __device__ __forceinline__ void warp_wait_envs_ready(const unsigned *ready, unsi
     for (unsigned e = r0 / W; e <= r1 / W; ++e) {
       unsigned v;
       asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ready + e) : "memory");
-      if (v) continue;
+      if (v || NV_STUDY_NOWAIT == 2) continue;  // (2: timing-only, one acquire, no spin)
       unsigned long long t0, t;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
       do {
@@ -335,11 +338,8 @@ __global__ void __launch_bounds__(128, NV_CAST_KMINB) k_column_cast(EnvView ev, 
   long long t0 = 0;
   if (order && threadIdx.x == 0) t0 = clock64();
   const long long total = (long long)ev.n * cam.W;
-#ifndef NV_STUDY_NOWAIT
-#define NV_STUDY_NOWAIT 0  // 1: timing-only study, the cast does not wait for the agent step
-#endif
   const long long g = blk * (long long)blockDim.x + threadIdx.x;
-  if (ready && !NV_STUDY_NOWAIT) {
+  if (ready && NV_STUDY_NOWAIT != 1) {
     if (arrive) {
       wait_envs_ready(ready, arrive, cam.W, total, 0, blk);
     } else {  // release mode: per warp, flags reset by the writer
