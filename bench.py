@@ -400,6 +400,9 @@ def run_gpu(args):
     ms_max = float(t.item())
     frames = shard.n_total * args.steps
     value = frames / (ms_max / 1e3)
+    faults = sim.ctx.faults()  # (after timing: synchronises) handshake waits that gave up
+    if faults:
+        print(f"[bench] handshake faults {faults:#x}: the timed frames are not valid", file=sys.stderr)
 
     # ---- kernel breakdown: per-kernel CUDA events over a second run of K steps
     lib, h = sim.ctx.lib, sim.ctx.handle
@@ -520,6 +523,7 @@ def run_gpu(args):
                          "step_achieved_gbs": step_gbs, "step_frac": step_gbs / peak},
             "clocks": clk.summary(),
             "gpu_launches": int(launches_timed),
+            "handshake_faults": int(faults),
             "e2e": e2e,
             "e2e_host_frames": e2e_frames,
             "episode_outcomes": outcomes,

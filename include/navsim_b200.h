@@ -246,6 +246,16 @@ double nv_host_hypot(double x, double y);
 /* Number of kernel launches issued by this context so far (bench evidence). */
 int64_t nv_launch_count(nv_ctx *ctx);
 
+/* Handshake faults since the last call (synchronises the device, then
+ * clears them): bit NV_FAULT_WRITER_WAIT -- a frame writer waited longer than
+ * 200 ms for an env's column records, NV_FAULT_CAST_WAIT -- a column cast
+ * waited longer than 200 ms for an env's agent step.  Either means a broken
+ * launch sequence (the waits give up rather than hang the GPU; the frames of
+ * that step are not valid).  0 in every correct run. */
+#define NV_FAULT_WRITER_WAIT 1u
+#define NV_FAULT_CAST_WAIT 2u
+int nv_faults(nv_ctx *ctx, uint32_t *mask);
+
 /* Per-kernel CUDA-event timing of the hot-path launches (bench roofline
  * evidence).  nv_profile(ctx, 1) clears and enables; nv_profile_read waits
  * for the recorded events and returns accumulated milliseconds and launch

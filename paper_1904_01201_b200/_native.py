@@ -23,6 +23,7 @@ NV_CH_RGB, NV_CH_DEPTH, NV_CH_SEM = 1, 2, 4
 NV_ALL_CAMERAS = -1
 NV_CAST_AUTO, NV_CAST_THREAD, NV_CAST_WARP = 0, 1, 2
 NV_FILL_AUTO, NV_FILL_GENERIC = 0, 1
+NV_FAULT_WRITER_WAIT, NV_FAULT_CAST_WAIT = 1, 2
 
 # every symbol include/navsim_b200.h declares: (name, restype, argtypes)
 _P = ctypes.c_void_p
@@ -59,6 +60,7 @@ SIGNATURES = {
     "nv_host_sincos": (None, [_D, _P, _P]),
     "nv_host_hypot": (_D, [_D, _D]),
     "nv_launch_count": (_I64, [_P]),
+    "nv_faults": (_I, [_P, _P]),
     "nv_profile": (_I, [_P, _I]),
     "nv_profile_read": (_I, [_P, _P, _P]),
     "nv_nav_build": (_I, [_P, _P, _D, _D, _P, _P, _P]),
@@ -169,3 +171,9 @@ class Context:
 
     def launches(self) -> int:
         return int(self.lib.nv_launch_count(self._h))
+
+    def faults(self) -> int:
+        """Handshake faults since the last call (NV_FAULT_* bits; synchronises)."""
+        m = ctypes.c_uint32()
+        check(self.lib.nv_faults(self._h, ctypes.byref(m)))
+        return int(m.value)

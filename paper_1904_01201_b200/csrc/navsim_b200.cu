@@ -1712,6 +1712,31 @@ double nv_host_hypot(double x, double y) { return nvx::hypot_cr(x, y); }
 
 int64_t nv_launch_count(nv_ctx *c) { return c ? c->launches : 0; }
 
+int nv_faults(nv_ctx *c, uint32_t *mask) {
+  if (!c) return fail(NV_ERR_ARG, "ctx is NULL");
+  if (!mask) return fail(NV_ERR_ARG, "mask is NULL");
+  TRY(e2e_fence(c));
+  CK(cudaDeviceSynchronize());
+  uint32_t m = 0;
+  auto take = [&](unsigned *word, uint32_t bit) -> int {
+    unsigned v = 0;
+    CK(cudaMemcpy(&v, word, sizeof v, cudaMemcpyDeviceToHost));
+    if (v) {
+      m |= bit;
+      CK(cudaMemset(word, 0, sizeof v));
+    }
+    return NV_OK;
+  };
+  for (Camera &k : c->cams) {
+    if (k.rel.p && k.rel_n > 0) TRY(take(k.rel.as<unsigned>() + 4 * (size_t)k.rel_n, NV_FAULT_WRITER_WAIT));
+    if (k.rel_e2e.p && k.rel_n_e2e > 0)
+      TRY(take(k.rel_e2e.as<unsigned>() + 4 * (size_t)k.rel_n_e2e, NV_FAULT_WRITER_WAIT));
+  }
+  if (c->pdl_ready.p && c->pdl_init) TRY(take(pdl_fault(c), NV_FAULT_CAST_WAIT));
+  *mask = m;
+  return NV_OK;
+}
+
 int nv_profile(nv_ctx *c, int enable) {
   if (!c) return fail(NV_ERR_ARG, "ctx is NULL");
   c->prof_on = enable != 0;

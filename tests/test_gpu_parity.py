@@ -515,6 +515,7 @@ def test_chained_steps_agree_at_scale(nb, cfg, W, H, n, steps):
         s0.step(acts[s])
         torch.cuda.synchronize()
     torch.cuda.synchronize()
+    assert s1.ctx.faults() == 0  # no handshake wait gave up
     o0, o1 = s0.observations(), s1.observations()
     for k in ("rgb", "depth", "gps", "compass"):
         assert torch.equal(o0[k], o1[k]), k
@@ -557,6 +558,7 @@ def test_steps_without_frames_back_to_back(nb):
                 torch.cuda.synchronize()
         torch.cuda.synchronize()
         outs.append((gps, comp, sim.state()))
+    assert sims[1].ctx.faults() == 0
     (g0, c0, s0), (g1, c1, s1) = outs
     assert torch.equal(g0, g1)
     assert torch.equal(c0, c1)
@@ -603,6 +605,7 @@ def test_host_steps_back_to_back_at_scale(nb, pinned):
         assert np.array_equal(got[t]["collided"], b.collided.cpu().numpy()), t
         assert np.array_equal(got[t]["displacement"], b.displacement.cpu().numpy()), t
     fr = a.host_step_frames()
+    assert a.ctx.faults() == 0
     torch.cuda.synchronize()
     assert torch.equal(fr["rgb"], b.groups[0]["rgb"])
     assert torch.equal(fr["depth"], b.groups[0]["depth"])

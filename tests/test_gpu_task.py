@@ -420,3 +420,4 @@ def test_task_steps_overlap_agrees_at_scale(nb):
         for k in o0:
             assert torch.equal(o0[k], o1[k]), (t, k)
     assert envs[0].outcomes() == envs[1].outcomes()
+    assert envs[1].sim.ctx.faults() == 0  # no handshake wait gave up
