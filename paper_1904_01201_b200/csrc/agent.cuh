@@ -125,6 +125,9 @@ __device__ __forceinline__ void warp_agent_step(const EnvView &ev, const SceneVi
 // dependent launch of the cast), the dependent grid is released at once and
 // each env's pose is published through ready[e] (release) as soon as its warp
 // is done, so the casts of finished envs overlap the long agent chains.
+#ifndef NV_AGENT_FENCE
+#define NV_AGENT_FENCE 0
+#endif
 #ifndef NV_AGENT_MAXREG
 #define NV_AGENT_MAXREG 0  // > 0: register cap of the agent step (room beside a writer CTA)
 #endif
@@ -143,7 +146,10 @@ __global__ void NV_AGENT_BOUNDS k_agent_step(EnvView ev, SceneView sc, AgentCfg 
   if (e < ev.n) {
     warp_agent_step(ev, sc, cfg, e, actions[e], collided_out, disp_out, status_out);
     if (ready && (threadIdx.x & 31) == 0) {
-      __threadfence();
+      // lane 0 made every store of the env's step: its release store orders
+      // them before the flag (NV_AGENT_FENCE: an extra sequentially consistent
+      // fence, the round-2 study baseline)
+      if (NV_AGENT_FENCE) __threadfence();
       asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(ready + e), "r"(1u) : "memory");
     }
   }
