@@ -155,7 +155,7 @@ __global__ void NV_AGENT_BOUNDS k_agent_step(EnvView ev, SceneView sc, AgentCfg 
   }
   // launched as a programmatic dependent of the previous frame writer: this
   // grid completes only after it, so stream order still holds for what follows
-  asm volatile("griddepcontrol.wait;" ::: "memory");
+  grid_completes_after_predecessor();
 }
 
 // Cast side of the agent->cast overlap: thread 0 of a CTA waits for every env

@@ -320,7 +320,7 @@ __global__ void __launch_bounds__(128, NV_CASTW_MINB) k_column_cast_warp(EnvView
       if (done) release_envs(done, blk, (int)(blockDim.x >> 5), cam.W, total);
     }
   }
-  asm volatile("griddepcontrol.wait;" ::: "memory");  // completes after the agent step
+  grid_completes_after_predecessor();  // completes after the agent step
 }
 
 // One thread per (env, column).  With `ready`: launched as a programmatic
@@ -374,7 +374,7 @@ __global__ void __launch_bounds__(128, NV_CAST_KMINB) k_column_cast(EnvView ev, 
       if (done) release_envs(done, blk, (int)blockDim.x, cam.W, total);
     }
   }
-  asm volatile("griddepcontrol.wait;" ::: "memory");  // completes after the agent step
+  grid_completes_after_predecessor();  // completes after the agent step
 }
 
 __global__ void k_lpt_init(unsigned *order, unsigned *cost, unsigned n) {

@@ -26,6 +26,19 @@ using nvx::sub;
 
 // ---------------------------------------------------------------- helpers
 
+// End of a grid launched as a programmatic dependent: the grid must not
+// complete before its predecessor (so stream order holds for whatever
+// follows).  One CTA waiting is enough for that -- a grid completes when its
+// last CTA exits -- so only the last CTA in launch order waits and every
+// other CTA frees its SM slot at once instead of idling until the previous
+// frame writer ends (NV_GDW_ALL: every CTA waits, the round-2 baseline).
+#ifndef NV_GDW_ALL
+#define NV_GDW_ALL 0
+#endif
+__device__ __forceinline__ void grid_completes_after_predecessor() {
+  if (NV_GDW_ALL || blockIdx.x == gridDim.x - 1) asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
 // SegmentIndex._cell_of (geometry.py:146-149): trunc toward zero, clamp.
 __device__ __forceinline__ int cell_coord(double v, double o, int n) {
   double d = sub(v, o);  // (v - o) / CELL with CELL = 1.0: division by 1 is exact

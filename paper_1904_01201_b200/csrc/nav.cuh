@@ -550,7 +550,7 @@ __global__ void __launch_bounds__(128) k_column_cast_task(EnvView ev, SceneView 
     __syncthreads();
     if (threadIdx.x == 0) release_envs(done, blockIdx.x, (int)blockDim.x, cam.W, total);
   }
-  asm volatile("griddepcontrol.wait;" ::: "memory");
+  grid_completes_after_predecessor();
 }
 
 __global__ void __launch_bounds__(128) k_column_cast_warp_task(EnvView ev, SceneView sc,
