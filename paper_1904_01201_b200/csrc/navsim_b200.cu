@@ -49,7 +49,7 @@ using namespace nvd;
 #define NV_FILL_RELEASE 1  // the writer takes each env as soon as its casts are done
 #endif
 #ifndef NV_AGENT_BLOCK
-#define NV_AGENT_BLOCK 128  // threads per CTA of the agent step (a warp per env)
+#define NV_AGENT_BLOCK 32  // threads per CTA of the agent step (a warp per env; one-warp CTAs fit beside a writer CTA)
 #endif
 #ifndef NV_STEP_CHAIN
 #define NV_STEP_CHAIN 1  // the agent step is a programmatic dependent of the previous frame writer
