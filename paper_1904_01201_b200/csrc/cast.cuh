@@ -386,44 +386,58 @@ __global__ void k_lpt_init(unsigned *order, unsigned *cost, unsigned n) {
 }
 
 // Longest-first order of the cast's ray blocks from their last durations:
-// a counting sort over 256 log-spaced buckets (descending) by ONE warp, run
-// on a side stream beside the frame writer -- a single warp fits an SM next
-// to a writer CTA, so the sort never waits for the writer to drain (the next
-// step's agent step depends on it).
-__global__ void __launch_bounds__(32) k_cast_order(const unsigned *cost, unsigned *order,
-                                                   int nblk) {
+// a counting sort over 256 log-spaced buckets (descending), run on a side
+// stream beside the frame writer.  The next step's agent step depends on it,
+// so it must fit an SM next to a writer CTA and end well inside the writer:
+// NV_ORDER_WARPS warps of <= 32 registers (one warp per SM sub-partition
+// fits beside the writer's 18 warps x 96 registers).  Equal-bucket blocks
+// come out in any order (the order only schedules; results do not depend
+// on it).
+#ifndef NV_ORDER_WARPS
+#define NV_ORDER_WARPS 4
+#endif
+__global__ void __launch_bounds__(32 * NV_ORDER_WARPS, 64 / NV_ORDER_WARPS)
+    k_cast_order(const unsigned *cost, unsigned *order, int nblk) {
   __shared__ unsigned hist[256];
-  const int lane = threadIdx.x;
+  __shared__ unsigned wmax[NV_ORDER_WARPS];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int T = 32 * NV_ORDER_WARPS;
   unsigned mx = 0;
-  for (int k = lane; k < 256; k += 32) hist[k] = 0;
-  for (int b = lane; b < nblk; b += 32) mx = max(mx, cost[b]);
+  for (int k = tid; k < 256; k += T) hist[k] = 0;
+  for (int b = tid; b < nblk; b += T) mx = max(mx, cost[b]);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-  __syncwarp();
+  if (lane == 0) wmax[warp] = mx;
+  __syncthreads();
+  mx = 0;
+#pragma unroll
+  for (int w = 0; w < NV_ORDER_WARPS; ++w) mx = max(mx, wmax[w]);
   const int top = 32 - __clz(mx | 1u);          // bits of the largest cost
   const int shift = top > 8 ? top - 8 : 0;
   auto bucket = [&](unsigned c) { return 255 - (int)min(255u, c >> shift); };  // slow first
-  for (int b = lane; b < nblk; b += 32) atomicAdd(&hist[bucket(cost[b])], 1u);
-  __syncwarp();
-  // exclusive prefix over the 256 buckets: 8 consecutive buckets per lane
-  unsigned v[8], run = 0;
+  for (int b = tid; b < nblk; b += T) atomicAdd(&hist[bucket(cost[b])], 1u);
+  __syncthreads();
+  if (warp == 0) {
+    // exclusive prefix over the 256 buckets: 8 consecutive buckets per lane
+    unsigned v[8], run = 0;
 #pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    v[k] = run;
-    run += hist[lane * 8 + k];
+    for (int k = 0; k < 8; ++k) {
+      v[k] = run;
+      run += hist[lane * 8 + k];
+    }
+    unsigned incl = run;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned u = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += u;
+    }
+    const unsigned base = incl - run;
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < 8; ++k) hist[lane * 8 + k] = base + v[k];
   }
-  unsigned incl = run;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const unsigned u = __shfl_up_sync(0xffffffffu, incl, o);
-    if (lane >= o) incl += u;
-  }
-  const unsigned base = incl - run;
-  __syncwarp();
-#pragma unroll
-  for (int k = 0; k < 8; ++k) hist[lane * 8 + k] = base + v[k];
-  __syncwarp();
-  for (int b = lane; b < nblk; b += 32) order[atomicAdd(&hist[bucket(cost[b])], 1u)] = (unsigned)b;
+  __syncthreads();
+  for (int b = tid; b < nblk; b += T) order[atomicAdd(&hist[bucket(cost[b])], 1u)] = (unsigned)b;
 }
 
 // gps_compass (sensors.py:175-180) for all envs (no visual sensors case).

@@ -412,6 +412,12 @@ struct FillWsLayout {  // byte offsets into dynamic shared memory + ring geometr
 #else
 #define NV_FILL_BOUNDS __launch_bounds__(REL ? 576 : 544, 1)
 #endif
+#ifndef NV_STUDY_WAITSTAT
+#define NV_STUDY_WAITSTAT 0  // study build: the REL writer's loader accumulates its wait per item rank
+#endif
+#if NV_STUDY_WAITSTAT
+__device__ unsigned long long g_waitstat[16];
+#endif
 __device__ __forceinline__ unsigned long long global_ns() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -514,7 +520,15 @@ __global__ void NV_FILL_BOUNDS k_fill_ws(FillArgs a, FillWsLayout L) {
       if (lane != 0) return;
       int it = 0;
       for (int q = blockIdx.x; q < n_items; q += gridDim.x, ++it) {
+#if NV_STUDY_WAITSTAT
+        const unsigned long long w0 = global_ns();
+#endif
         wait_env_cast(a.done, a.consumed, a.fault, a.ready, q / bands, W, bands);
+#if NV_STUDY_WAITSTAT
+        // study build: ns the loader waited per item rank, and the items
+        atomicAdd(g_waitstat + min(it, 7), global_ns() - w0);
+        atomicAdd(g_waitstat + 8 + min(it, 7), 1ull);
+#endif
         if (it >= NV_WS_CBUF)
           mbar_wait(colempty + (it % NV_WS_CBUF), (unsigned)(((it / NV_WS_CBUF) - 1) & 1));
         load_item(it % NV_WS_CBUF, q / bands);

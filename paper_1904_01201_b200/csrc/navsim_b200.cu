@@ -34,7 +34,7 @@ using namespace nvd;
 #define NV_CAST_WARP_RAYS 16384  // batches with at most this many rays cast one warp per ray
 #endif
 #ifndef NV_CAST_BLOCK
-#define NV_CAST_BLOCK 128  // threads per CTA of the thread-per-ray cast (32/64/96/128 within noise)
+#define NV_CAST_BLOCK 64  // threads per CTA of the thread-per-ray cast (C3: 64 95.3 / 128 95.7 / 32 96.0 us per step with the 4-warp block-order kernel)
 #endif
 #ifndef NV_CAST_LPT
 #define NV_CAST_LPT 1  // longest-first order of the cast's blocks (C3 -2 us/step)
@@ -768,7 +768,7 @@ int side_fork(nv_ctx *c, cudaStream_t st) {
 
 int lpt_fork(nv_ctx *c, cudaStream_t st, unsigned *order, unsigned *cost, unsigned nblk) {
   TRY(side_fork(c, st));
-  nvk::k_cast_order<<<1, 32, 0, c->o_stream>>>(cost, order, (int)nblk);
+  nvk::k_cast_order<<<1, 32 * NV_ORDER_WARPS, 0, c->o_stream>>>(cost, order, (int)nblk);
   return check_launch(c);
 }
 
