@@ -522,29 +522,55 @@ struct TaskOut {
 
 // done: per-env release to the frame writer (its programmatic dependent), as
 // in k_column_cast.
+// With `ready`: a programmatic dependent of the agent step, waiting per env
+// like k_column_cast (release mode when `arrive` is null); the agent step's
+// outputs are then read through L2.
+template <bool COH>
+__device__ __forceinline__ void task_column(const EnvView &ev, const SceneView &sc,
+                                            const CamView &cam, const RecOut &ro, double t_max,
+                                            double *gps, double *compass, const TaskOut &to, int e,
+                                            int j) {
+  if (j == 0) {  // before the ray: the env's task step
+    const int32_t status = COH ? __ldcg(to.status + e) : to.status[e];
+    if (status != 0) {
+      task_skip(to.tv, e, to.reward, to.dist, to.done);
+    } else {
+      const double px = COH ? __ldcg(ev.x + e) : ev.x[e], py = COH ? __ldcg(ev.y + e) : ev.y[e];
+      const double d_cur = distance_to_goal(sc, to.nv, to.tv, e, px, py);
+      task_finish(to.tv, e, to.actions[e], d_cur, COH ? __ldcg(ev.path + e) : ev.path[e],
+                  COH ? __ldcg(ev.coll + e) : ev.coll[e], to.reward, to.dist, to.done, to.out);
+    }
+  }
+  cast_column<COH>(ev, sc, cam, e, j, ro, t_max, gps, compass);
+}
+
 __global__ void __launch_bounds__(128) k_column_cast_task(EnvView ev, SceneView sc, CamView cam,
                                                           RecOut ro, double t_max, double *gps,
                                                           double *compass, TaskOut to,
-                                                          unsigned *done) {
+                                                          unsigned *done, unsigned *ready,
+                                                          unsigned *arrive, unsigned *rfault) {
   // triggers only when the writer follows as its programmatic dependent
   // (release), see k_column_cast
   if (done) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   const long long total = (long long)ev.n * cam.W;
+  if (ready) {
+    if (arrive) {
+      wait_envs_ready(ready, arrive, cam.W, total);
+    } else {
+      const long long w0 = blockIdx.x * (long long)blockDim.x + (threadIdx.x & ~31u);
+      if (w0 < total)
+        warp_wait_envs_ready(ready, rfault, (unsigned)w0, (unsigned)min(total - 1, w0 + 31),
+                             (unsigned)cam.W);
+    }
+  }
   if (g < total) {
     const int e = (int)(g / cam.W);
     const int j = (int)(g - (long long)e * cam.W);
-    if (j == 0) {  // before the ray: the env's task step
-      if (to.status[e] != 0) {
-        task_skip(to.tv, e, to.reward, to.dist, to.done);
-      } else {
-        const double px = ev.x[e], py = ev.y[e];
-        const double d_cur = distance_to_goal(sc, to.nv, to.tv, e, px, py);
-        task_finish(to.tv, e, to.actions[e], d_cur, ev.path[e], ev.coll[e], to.reward, to.dist,
-                    to.done, to.out);
-      }
-    }
-    cast_column<false>(ev, sc, cam, e, j, ro, t_max, gps, compass);
+    if (ready)
+      task_column<true>(ev, sc, cam, ro, t_max, gps, compass, to, e, j);
+    else
+      task_column<false>(ev, sc, cam, ro, t_max, gps, compass, to, e, j);
   }
   if (done) {
     __syncthreads();

@@ -72,6 +72,9 @@ using namespace nvd;
 #ifndef NV_READY_BY_HALF
 #define NV_READY_BY_HALF 1  // release mode: per-warp ready waits, flags per record half reset by the writer
 #endif
+#ifndef NV_TASK_PDL
+#define NV_TASK_PDL 1  // task-layer step: the task cast as the agent step's programmatic dependent
+#endif
 #ifndef NV_E2E_ACT_COPY
 #define NV_E2E_ACT_COPY 0  // mapped host step: copy the actions in (a graph copy node) instead of reading them over PCIe
 #endif
