@@ -68,7 +68,23 @@ struct AgentPost {
   double x, y, path;
   long long coll;
   int status;
+  double h, c, s;  // heading and its cos / sin after the step (valid in lane 0)
 };
+
+// Per-env pose records of the release-mode agent -> cast handshake
+// (NV_POSE_REC): {x, y, cos h, sin h, h} per env and record half, 64-byte
+// stride.  The frame writer resets a consumed env's record to the sentinel,
+// a signalling-NaN pattern no arithmetic produces; the agent step's lane 0
+// writes the new pose (plain 8-byte stores), and a cast lane reloads the
+// record from L2 until no field is the sentinel -- one memory round trip
+// instead of a flag acquire followed by the pose loads.
+#define NV_POSE_SENTINEL 0x7FF0DEAD00000001ull
+#define NV_POSE_STRIDE 8
+__device__ __forceinline__ double pose_field(double v) {
+  // a user-set pose with the sentinel's exact bits becomes a quiet NaN (the
+  // cast's result for any NaN pose is the same: no hit)
+  return (unsigned long long)__double_as_longlong(v) == NV_POSE_SENTINEL ? __longlong_as_double(0x7FF8000000000000ll) : v;
+}
 
 __device__ __forceinline__ void warp_agent_step(const EnvView &ev, const SceneView &sc,
                                                 const AgentCfg &cfg, int e, int a,
@@ -80,6 +96,7 @@ __device__ __forceinline__ void warp_agent_step(const EnvView &ev, const SceneVi
   // all of the env's state is loaded up front (one memory round trip)
   const uint8_t was_reset = ev.reset[e];
   double x = ev.x[e], y = ev.y[e], h0 = ev.h[e], ch = ev.ch[e], sh = ev.sh[e];
+  double hn = h0, cn = ch, sn = sh;
   const double path = ev.path[e];
   const long long coll0 = ev.coll[e];
   if (!was_reset) {
@@ -103,6 +120,9 @@ __device__ __forceinline__ void warp_agent_step(const EnvView &ev, const SceneVi
       ev.h[e] = h;
       ev.sh[e] = s;
       ev.ch[e] = c;
+      hn = h;
+      sn = s;
+      cn = c;
     }
   } else if (a != 3) {
     status = 3;  // NV_ENV_BAD_ACTION
@@ -118,6 +138,9 @@ __device__ __forceinline__ void warp_agent_step(const EnvView &ev, const SceneVi
     post->path = status == 0 && a == 0 ? add(path, moved) : path;
     post->coll = coll0 + collided;
     post->status = status;
+    post->h = hn;
+    post->c = cn;
+    post->s = sn;
   }
 }
 
@@ -140,11 +163,22 @@ __global__ void NV_AGENT_BOUNDS k_agent_step(EnvView ev, SceneView sc, AgentCfg 
                                                     const int8_t *__restrict__ actions,
                                                     uint8_t *collided_out,
                                                     double *disp_out, int32_t *status_out,
-                                                    unsigned *ready) {
-  if (ready) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+                                                    unsigned *ready, double *posrec) {
+  // ready: per-env flags, posrec: per-env pose records (see NV_POSE_SENTINEL)
+  if (ready || posrec) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int e = (int)((blockIdx.x * (size_t)blockDim.x + threadIdx.x) >> 5);
   if (e < ev.n) {
-    warp_agent_step(ev, sc, cfg, e, actions[e], collided_out, disp_out, status_out);
+    AgentPost post;
+    warp_agent_step(ev, sc, cfg, e, actions[e], collided_out, disp_out, status_out,
+                    posrec ? &post : nullptr);
+    if (posrec && (threadIdx.x & 31) == 0) {
+      double *r = posrec + (size_t)e * NV_POSE_STRIDE;
+      r[0] = pose_field(post.x);
+      r[1] = pose_field(post.y);
+      r[2] = pose_field(post.c);
+      r[3] = pose_field(post.s);
+      r[4] = pose_field(post.h);
+    }
     if (ready && (threadIdx.x & 31) == 0) {
       // lane 0 made every store of the env's step: its release store orders
       // them before the flag (NV_AGENT_FENCE: an extra sequentially consistent

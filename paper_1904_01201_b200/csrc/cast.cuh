@@ -66,16 +66,12 @@ __device__ __forceinline__ void put_rec(const RecOut &ro, long long e, int j, co
 // COH: the agent state was written by a still-running grid (programmatic
 // dependent launch), so it is read through L2 (ld.global.cg) rather than the
 // non-coherent path.
-template <bool COH>
-__device__ __forceinline__ void cast_column(const EnvView &ev, const SceneView &sc,
-                                            const CamView &cam, int e, int j, const RecOut &ro,
-                                            double t_max, double *gps, double *compass) {
-  double px, py, c, s;
-  if (COH) {
-    px = __ldcg(ev.x + e); py = __ldcg(ev.y + e); c = __ldcg(ev.ch + e); s = __ldcg(ev.sh + e);
-  } else {
-    px = ev.x[e]; py = ev.y[e]; c = ev.ch[e]; s = ev.sh[e];
-  }
+// (env e's pose px, py, cos c, sin s, heading h: h only read for column 0)
+__device__ __forceinline__ void cast_column_at(const EnvView &ev, const SceneView &sc,
+                                               const CamView &cam, int e, int j, const RecOut &ro,
+                                               double t_max, double *gps, double *compass,
+                                               double px, double py, double c, double s,
+                                               double heading) {
   const double u = __ldg(cam.u + j);
   const double dx = add(c, mul(u, s));
   const double dy = add(s, mul(u, -c));
@@ -92,10 +88,58 @@ __device__ __forceinline__ void cast_column(const EnvView &ev, const SceneView &
       gps[2 * e] = sub(mul(fc, ddx), mul(fs, ddy));
       gps[2 * e + 1] = add(mul(fs, ddx), mul(fc, ddy));
     }
-    if (compass) {
-      const double h = COH ? __ldcg(ev.h + e) : ev.h[e];
-      compass[e] = nvx::wrap_angle(sub(h, ev.oh[e]));
+    if (compass) compass[e] = nvx::wrap_angle(sub(heading, ev.oh[e]));
+  }
+}
+
+template <bool COH>
+__device__ __forceinline__ void cast_column(const EnvView &ev, const SceneView &sc,
+                                            const CamView &cam, int e, int j, const RecOut &ro,
+                                            double t_max, double *gps, double *compass) {
+  double px, py, c, s, h = 0.0;
+  if (COH) {
+    px = __ldcg(ev.x + e); py = __ldcg(ev.y + e); c = __ldcg(ev.ch + e); s = __ldcg(ev.sh + e);
+    if (j == 0) h = __ldcg(ev.h + e);
+  } else {
+    px = ev.x[e]; py = ev.y[e]; c = ev.ch[e]; s = ev.sh[e];
+    if (j == 0) h = ev.h[e];
+  }
+  cast_column_at(ev, sc, cam, e, j, ro, t_max, gps, compass, px, py, c, s, h);
+}
+
+__device__ __forceinline__ double ld_relaxed_f64(const double *p) {
+  double v;
+  asm volatile("ld.relaxed.gpu.global.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ bool is_pose_sentinel(double v) {
+  return (unsigned long long)__double_as_longlong(v) == NV_POSE_SENTINEL;
+}
+// Release-mode cast side with pose records: reload the env's record from L2
+// until no field is the sentinel (each field is written once per step, after
+// the reset, so five non-sentinel fields are all this step's); a wait longer
+// than 200 ms raises `fault` and casts whatever was read.
+__device__ __forceinline__ void load_pose_record(const double *rec, unsigned *fault, double &px,
+                                                 double &py, double &c, double &s, double &h) {
+  unsigned long long t0 = 0;
+  for (;;) {
+    px = ld_relaxed_f64(rec);
+    py = ld_relaxed_f64(rec + 1);
+    c = ld_relaxed_f64(rec + 2);
+    s = ld_relaxed_f64(rec + 3);
+    h = ld_relaxed_f64(rec + 4);
+    if (!(is_pose_sentinel(px) | is_pose_sentinel(py) | is_pose_sentinel(c) | is_pose_sentinel(s) |
+          is_pose_sentinel(h)))
+      return;
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (!t0) {
+      t0 = t;
+    } else if (t - t0 > 200000000ull || *reinterpret_cast<volatile unsigned *>(fault)) {
+      atomicExch(fault, 1u);
+      return;
     }
+    __nanosleep(64);
   }
 }
 
@@ -295,8 +339,10 @@ __global__ void __launch_bounds__(128, NV_CASTW_MINB) k_column_cast_warp(EnvView
                                                           double *compass, unsigned *ready,
                                                           unsigned *arrive, unsigned *rfault,
                                                           const unsigned *order, unsigned *cost,
-                                                          unsigned *done, bool trigger) {
+                                                          unsigned *done, bool trigger,
+                                                          const double *posrec) {
   (void)rfault;  // the warp cast always resets its ready flags itself (arrive)
+  (void)posrec;  // and never runs in release mode
   // `order` / `cost`: longest-first block order, as in k_column_cast
   if (trigger) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // see k_column_cast
   const long long blk = order ? (long long)__ldg(order + blockIdx.x) : (long long)blockIdx.x;
@@ -334,7 +380,7 @@ __global__ void __launch_bounds__(128, NV_CAST_KMINB) k_column_cast(EnvView ev, 
                                                      unsigned *ready, unsigned *arrive,
                                                      unsigned *rfault, const unsigned *order,
                                                      unsigned *cost, unsigned *done,
-                                                     bool trigger) {
+                                                     bool trigger, const double *posrec) {
   // With `order`: CTA b casts ray block order[b] (blocks the previous step
   // found slowest first -- longest-processing-time order, so the grid's last
   // wave is made of short blocks) and records its block's duration in
@@ -362,7 +408,11 @@ __global__ void __launch_bounds__(128, NV_CAST_KMINB) k_column_cast(EnvView ev, 
     // 32-bit division whenever the ray count fits (always, in practice)
     const int e = total <= 0xffffffffLL ? (int)((unsigned)g / (unsigned)cam.W) : (int)(g / cam.W);
     const int j = (int)(g - (long long)e * cam.W);
-    if (ready)
+    if (posrec) {
+      double px, py, c, s, h;
+      load_pose_record(posrec + (size_t)e * NV_POSE_STRIDE, rfault, px, py, c, s, h);
+      cast_column_at(ev, sc, cam, e, j, ro, t_max, gps, compass, px, py, c, s, h);
+    } else if (ready)
       cast_column<true>(ev, sc, cam, e, j, ro, t_max, gps, compass);
     else
       cast_column<false>(ev, sc, cam, e, j, ro, t_max, gps, compass);
@@ -375,6 +425,12 @@ __global__ void __launch_bounds__(128, NV_CAST_KMINB) k_column_cast(EnvView ev, 
     }
   }
   grid_completes_after_predecessor();  // completes after the agent step
+}
+
+// every field of n pose records -> the sentinel (NV_POSE_SENTINEL)
+__global__ void k_pose_init(unsigned long long *rec, long long n_words) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i < n_words) rec[i] = NV_POSE_SENTINEL;
 }
 
 __global__ void k_lpt_init(unsigned *order, unsigned *cost, unsigned n) {

@@ -60,6 +60,9 @@ struct FillArgs {
   // agent -> cast ready flags of this record half (release mode of
   // nv_step_render): reset by the env's last consumer, like done
   unsigned *ready;
+  // or the pose records of this record half (NV_POSE_REC): reset to the
+  // sentinel by the env's last consumer
+  double *posrec;
 };
 
 // ---- inverse-depth noise ---------------------------------------------------
@@ -434,8 +437,8 @@ __device__ __forceinline__ bool env_cast_done(const unsigned *done, int env, int
 // record half serve the next step).  A wait longer than 200 ms raises the
 // fault flag and stops waiting, so a broken launch can never hang the GPU.
 __device__ __forceinline__ void wait_env_cast(unsigned *done, unsigned *consumed,
-                                              unsigned *fault, unsigned *ready, int env, int W,
-                                              int bands) {
+                                              unsigned *fault, unsigned *ready, double *posrec,
+                                              int env, int W, int bands) {
   if (!env_cast_done(done, env, W)) {
     const unsigned long long t0 = global_ns();
     while (!env_cast_done(done, env, W)) {
@@ -452,6 +455,12 @@ __device__ __forceinline__ void wait_env_cast(unsigned *done, unsigned *consumed
     if (bands > 1) consumed[env] = 0;
     done[env] = 0;
     if (ready) ready[env] = 0;  // every cast CTA of the env is past its wait
+    if (posrec) {
+      unsigned long long *r =
+          reinterpret_cast<unsigned long long *>(posrec + (size_t)env * NV_POSE_STRIDE);
+#pragma unroll
+      for (int k = 0; k < 5; ++k) r[k] = NV_POSE_SENTINEL;
+    }
   }
 }
 
@@ -523,7 +532,7 @@ __global__ void NV_FILL_BOUNDS k_fill_ws(FillArgs a, FillWsLayout L) {
 #if NV_STUDY_WAITSTAT
         const unsigned long long w0 = global_ns();
 #endif
-        wait_env_cast(a.done, a.consumed, a.fault, a.ready, q / bands, W, bands);
+        wait_env_cast(a.done, a.consumed, a.fault, a.ready, a.posrec, q / bands, W, bands);
 #if NV_STUDY_WAITSTAT
         // study build: ns the loader waited per item rank, and the items
         atomicAdd(g_waitstat + min(it, 7), global_ns() - w0);

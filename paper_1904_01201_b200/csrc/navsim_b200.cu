@@ -72,6 +72,9 @@ using namespace nvd;
 #ifndef NV_READY_BY_HALF
 #define NV_READY_BY_HALF 1  // release mode: per-warp ready waits, flags per record half reset by the writer
 #endif
+#ifndef NV_POSE_REC
+#define NV_POSE_REC 1  // release-mode handshake through per-env pose records (else ready flags)
+#endif
 #ifndef NV_TASK_PDL
 #define NV_TASK_PDL 1  // task-layer step: the task cast as the agent step's programmatic dependent
 #endif
@@ -252,6 +255,14 @@ struct nv_ctx {
   // (nullptr in release mode: the writer resets the flags), fault
   unsigned *pdl_cur_ready = nullptr, *pdl_cur_arrive = nullptr;
   unsigned *fill_ready = nullptr;  // ready flags the next release writer resets
+  // pose records of the release-mode handshake (NV_POSE_REC): [half][env][8]
+  DevBuf pose_rec;
+  bool pose_init = false;
+  // the host-buffer step's own handshake buffers (its writer may still run
+  // beside device steps on other streams; swapped in around its captures)
+  DevBuf pdl_ready_e2e, pdl_arrive_e2e, pose_rec_e2e;
+  bool pdl_init_e2e = false, pose_init_e2e = false;
+  double *pdl_cur_posrec = nullptr, *fill_posrec = nullptr;
   bool fill_pdl = false;  // the next ws writer launch follows its column cast (launch_ws_kernel)
   DevBuf pdl_ready, pdl_arrive;
   // dynamic shared memory opted in per kernel on this context's device
@@ -670,6 +681,7 @@ int launch_fill(nv_ctx *c, Camera &cam, int64_t N, uint8_t *rgb, float *depth, u
   a.consumed = release ? rel_done(cam, N) + N : nullptr;
   a.fault = release ? rel_fault(cam, N) : nullptr;
   a.ready = release ? c->fill_ready : nullptr;
+  a.posrec = release ? c->fill_posrec : nullptr;
   const RecOut ro = rec_out(cam, N);
   a.ra = ro.a;
   a.rb = ro.b;
@@ -801,6 +813,7 @@ int do_cast(nv_ctx *c, int cam, double *gps, double *compass, cudaStream_t st,
     Prof pf(c, st, 1);
     auto kern = warp ? nvk::k_column_cast_warp : nvk::k_column_cast;
     unsigned *ready = nullptr, *arrive = nullptr, *rfault = nullptr;
+    const double *posrec = nullptr;
     cudaLaunchConfig_t lc = {};
     lc.gridDim = dim3(nblk);
     lc.blockDim = dim3(threads);
@@ -810,6 +823,7 @@ int do_cast(nv_ctx *c, int cam, double *gps, double *compass, cudaStream_t st,
       c->pdl_armed = false;
       ready = c->pdl_cur_ready;
       arrive = c->pdl_cur_arrive;
+      posrec = c->pdl_cur_posrec;
       rfault = pdl_fault(c);
       at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
       at[0].val.programmaticStreamSerializationAllowed = 1;
@@ -819,7 +833,8 @@ int do_cast(nv_ctx *c, int cam, double *gps, double *compass, cudaStream_t st,
     CK(cudaLaunchKernelEx(&lc, kern, c->env_view(), c->scene_view(), cam_view(k),
                           rec_out(k, c->n_envs), k.max_range, gps, compass, ready, arrive, rfault,
                           (const unsigned *)order, cost,
-                          release ? rel_done(k, c->n_envs) : (unsigned *)nullptr, trigger));
+                          release ? rel_done(k, c->n_envs) : (unsigned *)nullptr, trigger,
+                          posrec));
     TRY(check_launch(c));
   }
   return order ? lpt_fork(c, st, order, cost, nblk) : NV_OK;
@@ -850,6 +865,15 @@ int pdl_buffers(nv_ctx *c) {
     CK(cudaMemset(c->pdl_arrive.p, 0, sizeof(unsigned) * n));
     c->pdl_init = true;
   }
+  const size_t words = 2 * n * NV_POSE_STRIDE;
+  if (NV_POSE_REC && (c->pose_rec.bytes < words * 8 || !c->pose_init)) {
+    TRY(c->pose_rec.alloc(words * 8));
+    nvk::k_pose_init<<<blocks_for((int64_t)words, 256), 256>>>(
+        c->pose_rec.as<unsigned long long>(), (long long)words);
+    TRY(check_launch(c));
+    CK(cudaDeviceSynchronize());
+    c->pose_init = true;
+  }
   return NV_OK;
 }
 // the ready flags of a step: release mode -> the set of the record half the
@@ -865,16 +889,28 @@ unsigned *pdl_fault(nv_ctx *c) {
 // arm_pdl: the cast that follows is this agent step's programmatic dependent;
 // release_half >= 0: release mode (the casts write that record half, its
 // frame writer resets the ready flags), -1: the casts reset them (arrive)
+// pose_rec: release mode with pose records instead of ready flags (the
+// casts load the half's records, its writer resets them)
 int do_step(nv_ctx *c, const int8_t *actions, uint8_t *collided, double *disp, int32_t *status,
-            cudaStream_t st, bool arm_pdl = false, int release_half = -1) {
+            cudaStream_t st, bool arm_pdl = false, int release_half = -1, bool pose_rec = false) {
   nvk::AgentCfg cfg{c->radius, c->step, c->turn_rad};
   long long threads = c->n_envs * 32;
   unsigned *ready = nullptr;
+  double *posrec = nullptr;
+  c->pdl_cur_posrec = nullptr;
   if (arm_pdl) {
     TRY(pdl_buffers(c));
-    ready = pdl_ready_set(c, release_half);
-    c->pdl_cur_ready = ready;
-    c->pdl_cur_arrive = release_half >= 0 ? nullptr : c->pdl_arrive.as<unsigned>();
+    if (pose_rec && release_half >= 0) {
+      posrec = c->pose_rec.as<double>() +
+               (size_t)release_half * std::max<int64_t>(1, c->n_envs) * NV_POSE_STRIDE;
+      c->pdl_cur_posrec = posrec;
+      c->pdl_cur_ready = nullptr;
+      c->pdl_cur_arrive = nullptr;
+    } else {
+      ready = pdl_ready_set(c, release_half);
+      c->pdl_cur_ready = ready;
+      c->pdl_cur_arrive = release_half >= 0 ? nullptr : c->pdl_arrive.as<unsigned>();
+    }
   }
   Prof pf(c, st, 0);
   {
@@ -891,7 +927,7 @@ int do_step(nv_ctx *c, const int8_t *actions, uint8_t *collided, double *disp, i
     lc.attrs = at;
     lc.numAttrs = NV_STEP_CHAIN && c->pdl && !c->prof_on ? 1 : 0;
     CK(cudaLaunchKernelEx(&lc, nvk::k_agent_step, c->env_view(), c->scene_view(), cfg, actions,
-                          collided, disp, status, ready));
+                          collided, disp, status, ready, posrec));
   }
   TRY(check_launch(c));
   c->pdl_armed = arm_pdl;
@@ -1160,8 +1196,12 @@ int nv_envs_alloc(nv_ctx *c, int64_t n_envs) {
   c->t_nfields = 0;
   // the agent -> cast ready flags are sized per env
   c->pdl_init = false;
+  c->pose_init = false;
+  c->pdl_init_e2e = false;
+  c->pose_init_e2e = false;
   c->n_envs = n_envs;
-  return NV_OK;
+  // (now, outside any stream capture a first step might be recorded in)
+  return pdl_buffers(c);
 }
 
 int nv_camera_config(nv_ctx *c, int cam, int width, int height, double focal, double max_range) {
@@ -1262,8 +1302,9 @@ int nv_step_render(nv_ctx *c, const int8_t *actions, int cam, uint8_t *rgb, floa
   // release mode: the agent -> cast ready flags of the record half the casts
   // are about to write (do_cast flips to it), reset by that half's writer
   const int rhalf = release && NV_READY_BY_HALF ? (k.rec_half ^ 1) : -1;
-  TRY(do_step(c, actions, collided, displacement, status, st, pdl, rhalf));
+  TRY(do_step(c, actions, collided, displacement, status, st, pdl, rhalf, NV_POSE_REC != 0));
   c->fill_ready = pdl && rhalf >= 0 ? c->pdl_cur_ready : nullptr;
+  c->fill_posrec = pdl && rhalf >= 0 ? c->pdl_cur_posrec : nullptr;
   TRY(do_cast(c, cam, gps, compass, st, release, rgb || depth || sem));
   c->pdl_armed = false;
   if (c->mid_ev) {  // on a branch of its own: no node between the casts and the writer
@@ -1279,6 +1320,7 @@ int nv_step_render(nv_ctx *c, const int8_t *actions, int cam, uint8_t *rgb, floa
   const int rc = launch_fill(c, k, c->n_envs, rgb, depth, sem, st, release);
   c->fill_pdl = false;
   c->fill_ready = nullptr;
+  c->fill_posrec = nullptr;
   TRY(lpt_join(c, st));
   if (c->mid_ev) {
     CK(cudaEventRecord(c->m_ev1, c->m_stream));
@@ -1432,7 +1474,23 @@ int nv_step_render_host(nv_ctx *c, const int8_t *actions_host, int cam, uint32_t
         CK(cudaDeviceSynchronize());
       }
     }
-    if (c->pdl) TRY(pdl_buffers(c));
+    // the handshake buffers of the device path and of the host steps
+    auto swap_pdl = [&]() {
+      std::swap(c->pdl_ready.p, c->pdl_ready_e2e.p);
+      std::swap(c->pdl_ready.bytes, c->pdl_ready_e2e.bytes);
+      std::swap(c->pdl_arrive.p, c->pdl_arrive_e2e.p);
+      std::swap(c->pdl_arrive.bytes, c->pdl_arrive_e2e.bytes);
+      std::swap(c->pose_rec.p, c->pose_rec_e2e.p);
+      std::swap(c->pose_rec.bytes, c->pose_rec_e2e.bytes);
+      std::swap(c->pdl_init, c->pdl_init_e2e);
+      std::swap(c->pose_init, c->pose_init_e2e);
+    };
+    if (c->pdl) {
+      swap_pdl();
+      const int prc = pdl_buffers(c);
+      swap_pdl();
+      TRY(prc);
+    }
     for (int q = 0; q < ncam; ++q) {
       Camera &k = c->cams[cams[q]];
       TRY(rel_buffers(k.rel_e2e, k.rel_n_e2e, c->n_envs));
@@ -1441,7 +1499,8 @@ int nv_step_render_host(nv_ctx *c, const int8_t *actions_host, int cam, uint32_t
                                  (uint64_t)c->e2e_mapped, (uint64_t)direct,
                                  (uint64_t)(uintptr_t)c->e_hin, (uint64_t)(uintptr_t)c->e_hout,
                                  (uint64_t)(uintptr_t)c->e_act.p, (uint64_t)(uintptr_t)c->e_pack.p,
-                                 (uint64_t)(uintptr_t)c->pdl_ready.p};
+                                 (uint64_t)(uintptr_t)c->pdl_ready_e2e.p,
+                                 (uint64_t)(uintptr_t)c->pose_rec_e2e.p};
     if (direct)
       for (int q = 0; q < 4; ++q) key.push_back((uint64_t)(uintptr_t)c->e_out_dev[q]);
     for (int q = 0; q < ncam; ++q) {
@@ -1502,6 +1561,7 @@ int nv_step_render_host(nv_ctx *c, const int8_t *actions_host, int cam, uint32_t
           std::swap(k.lpt_cost.bytes, k.lpt_cost_e2e.bytes);
           std::swap(k.lpt_n, k.lpt_n_e2e);
         }
+        swap_pdl();
       };
       // graph p: record half and release counters of the p-th render after
       // the capture began (do_cast alternates them), frame set p
@@ -1736,6 +1796,10 @@ int nv_faults(nv_ctx *c, uint32_t *mask) {
       TRY(take(k.rel_e2e.as<unsigned>() + 4 * (size_t)k.rel_n_e2e, NV_FAULT_WRITER_WAIT));
   }
   if (c->pdl_ready.p && c->pdl_init) TRY(take(pdl_fault(c), NV_FAULT_CAST_WAIT));
+  if (c->pdl_ready_e2e.p && c->pdl_init_e2e) {
+    const size_t n = (size_t)std::max<int64_t>(1, c->n_envs);
+    TRY(take(c->pdl_ready_e2e.as<unsigned>() + 3 * n, NV_FAULT_CAST_WAIT));
+  }
   *mask = m;
   return NV_OK;
 }
