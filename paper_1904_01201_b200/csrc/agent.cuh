@@ -72,8 +72,8 @@ struct AgentPost {
 };
 
 // Per-env pose records of the release-mode agent -> cast handshake
-// (NV_POSE_REC): {x, y, cos h, sin h, h} per env and record half, 64-byte
-// stride.  The frame writer resets a consumed env's record to the sentinel,
+// (NV_POSE_REC): {x, y, cos h, sin h, h, path, collisions, status} per env
+// and record half, 64-byte stride.  The frame writer resets a consumed env's record to the sentinel,
 // a signalling-NaN pattern no arithmetic produces; the agent step's lane 0
 // writes the new pose (plain 8-byte stores), and a cast lane reloads the
 // record from L2 until no field is the sentinel -- one memory round trip
@@ -178,6 +178,12 @@ __global__ void NV_AGENT_BOUNDS k_agent_step(EnvView ev, SceneView sc, AgentCfg 
       r[2] = pose_field(post.c);
       r[3] = pose_field(post.s);
       r[4] = pose_field(post.h);
+      // the task cast's inputs too: path length, collision count, step status
+      // (never the sentinel's bits: a path is a finite length or a plain NaN,
+      // counts and statuses are small)
+      r[5] = pose_field(post.path);
+      r[6] = __longlong_as_double(post.coll);
+      r[7] = (double)post.status;
     }
     if (ready && (threadIdx.x & 31) == 0) {
       // lane 0 made every store of the env's step: its release store orders

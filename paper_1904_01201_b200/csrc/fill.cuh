@@ -459,7 +459,7 @@ __device__ __forceinline__ void wait_env_cast(unsigned *done, unsigned *consumed
       unsigned long long *r =
           reinterpret_cast<unsigned long long *>(posrec + (size_t)env * NV_POSE_STRIDE);
 #pragma unroll
-      for (int k = 0; k < 5; ++k) r[k] = NV_POSE_SENTINEL;
+      for (int k = 0; k < NV_POSE_STRIDE; ++k) r[k] = NV_POSE_SENTINEL;
     }
   }
 }

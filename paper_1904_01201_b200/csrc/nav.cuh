@@ -544,11 +544,56 @@ __device__ __forceinline__ void task_column(const EnvView &ev, const SceneView &
   cast_column<COH>(ev, sc, cam, e, j, ro, t_max, gps, compass);
 }
 
+// The task step from a pose record (release mode, NV_POSE_REC): every input
+// the agent step produced comes from the record.
+__device__ __forceinline__ void task_column_rec(const EnvView &ev, const SceneView &sc,
+                                                const CamView &cam, const RecOut &ro,
+                                                double t_max, double *gps, double *compass,
+                                                const TaskOut &to, int e, int j,
+                                                const double *rec, unsigned *fault) {
+  double px, py, c, s, h, path, collb, stat;
+  unsigned long long t0 = 0;
+  for (;;) {
+    px = ld_relaxed_f64(rec);
+    py = ld_relaxed_f64(rec + 1);
+    c = ld_relaxed_f64(rec + 2);
+    s = ld_relaxed_f64(rec + 3);
+    h = ld_relaxed_f64(rec + 4);
+    path = ld_relaxed_f64(rec + 5);
+    collb = ld_relaxed_f64(rec + 6);
+    stat = ld_relaxed_f64(rec + 7);
+    if (!(is_pose_sentinel(px) | is_pose_sentinel(py) | is_pose_sentinel(c) | is_pose_sentinel(s) |
+          is_pose_sentinel(h) | is_pose_sentinel(path) | is_pose_sentinel(collb) |
+          is_pose_sentinel(stat)))
+      break;
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (!t0) {
+      t0 = t;
+    } else if (t - t0 > 200000000ull || *reinterpret_cast<volatile unsigned *>(fault)) {
+      atomicExch(fault, 1u);
+      break;
+    }
+    __nanosleep(64);
+  }
+  if (j == 0) {  // before the ray: the env's task step
+    if ((int)stat != 0) {
+      task_skip(to.tv, e, to.reward, to.dist, to.done);
+    } else {
+      const double d_cur = distance_to_goal(sc, to.nv, to.tv, e, px, py);
+      task_finish(to.tv, e, to.actions[e], d_cur, path, __double_as_longlong(collb), to.reward,
+                  to.dist, to.done, to.out);
+    }
+  }
+  cast_column_at(ev, sc, cam, e, j, ro, t_max, gps, compass, px, py, c, s, h);
+}
+
 __global__ void __launch_bounds__(128) k_column_cast_task(EnvView ev, SceneView sc, CamView cam,
                                                           RecOut ro, double t_max, double *gps,
                                                           double *compass, TaskOut to,
                                                           unsigned *done, unsigned *ready,
-                                                          unsigned *arrive, unsigned *rfault) {
+                                                          unsigned *arrive, unsigned *rfault,
+                                                          const double *posrec) {
   // triggers only when the writer follows as its programmatic dependent
   // (release), see k_column_cast
   if (done) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
@@ -567,7 +612,10 @@ __global__ void __launch_bounds__(128) k_column_cast_task(EnvView ev, SceneView 
   if (g < total) {
     const int e = (int)(g / cam.W);
     const int j = (int)(g - (long long)e * cam.W);
-    if (ready)
+    if (posrec)
+      task_column_rec(ev, sc, cam, ro, t_max, gps, compass, to, e, j,
+                      posrec + (size_t)e * NV_POSE_STRIDE, rfault);
+    else if (ready)
       task_column<true>(ev, sc, cam, ro, t_max, gps, compass, to, e, j);
     else
       task_column<false>(ev, sc, cam, ro, t_max, gps, compass, to, e, j);
