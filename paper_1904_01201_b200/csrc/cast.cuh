@@ -410,7 +410,12 @@ __global__ void __launch_bounds__(128, NV_CAST_KMINB) k_column_cast(EnvView ev, 
     const int j = (int)(g - (long long)e * cam.W);
     if (posrec) {
       double px, py, c, s, h;
-      load_pose_record(posrec + (size_t)e * NV_POSE_STRIDE, rfault, px, py, c, s, h);
+      if (NV_STUDY_NOWAIT == 1) {  // timing-only: the current state, no wait
+        px = __ldcg(ev.x + e); py = __ldcg(ev.y + e); c = __ldcg(ev.ch + e); s = __ldcg(ev.sh + e);
+        h = __ldcg(ev.h + e);
+      } else {
+        load_pose_record(posrec + (size_t)e * NV_POSE_STRIDE, rfault, px, py, c, s, h);
+      }
       cast_column_at(ev, sc, cam, e, j, ro, t_max, gps, compass, px, py, c, s, h);
     } else if (ready)
       cast_column<true>(ev, sc, cam, e, j, ro, t_max, gps, compass);
