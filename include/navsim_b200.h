@@ -116,10 +116,11 @@ int nv_render(nv_ctx *ctx, int cam, uint8_t *rgb, float *depth, uint16_t *sem,
 
 /* Step + render: one call per simulator step for all envs -- nv_step then
  * nv_render for camera `cam`, enqueued as three launches on `stream`: the
- * agent step (k_agent_step, a warp per env; a programmatic dependent of the
- * previous step's frame writer, which it never reads from -- consecutive
- * renders alternate between two column-record buffers -- so it starts on
- * the SMs the writer's tail leaves idle and completes after it), the column
+ * agent step (k_agent_step, a warp per env in one-warp CTAs; a programmatic
+ * dependent of the previous step's frame writer, which it never reads from --
+ * consecutive renders alternate between two column-record buffers -- so it
+ * runs beside the writer and on the SMs its tail frees, and completes after
+ * it), the column
  * cast (a programmatic dependent of the agent step that starts each env's
  * rays as soon as its new pose is published, see nv_set_overlap) and the
  * frame writer (the
@@ -131,12 +132,14 @@ int nv_step_render(nv_ctx *ctx, const int8_t *actions, int cam, uint8_t *rgb,
                    uint8_t *collided, double *displacement, int32_t *status,
                    void *stream);
 
-/* Programmatic-dependent-launch chaining in nv_step_render, on by default:
- * each env's casts start as soon as its agent warp has published the new
- * pose; the frame writer takes each env as soon as its casts have published
- * their column records (thread-per-ray batches); the next step's agent step
- * starts on the SMs the previous writer's tail frees.  0 turns all of it off
- * (serialised launches; identical results). */
+/* Programmatic-dependent-launch chaining in nv_step_render (and in
+ * nv_task_step_render), on by default: each env's casts start as soon as its
+ * agent warp has published the new pose (a per-env pose record the casts
+ * reload until it is complete, or an acquired ready flag); the frame writer
+ * takes each env as soon as its casts have published their column records
+ * (thread-per-ray batches); the next step's agent step runs beside the
+ * previous writer.  0 turns all of it off (serialised launches; identical
+ * results). */
 int nv_set_overlap(nv_ctx *ctx, int on);
 /* Column cast (raycast_grid's DDA over the grid, bit-exact in every mode):
  * NV_CAST_AUTO (default) = one thread per ray, or one warp per ray (lanes
