@@ -613,6 +613,55 @@ def test_host_steps_back_to_back_at_scale(nb, pinned):
         assert torch.equal(x, y)
 
 
+def test_host_and_device_steps_share_a_side_stream(nb):
+    """Host-buffer steps and device steps alternating on one non-default
+    stream with no host synchronisation: a host step's frame writer still
+    runs when the next device step's agent step and casts start, and each
+    path has its own records, counters, pose records and ready flags, so
+    every result equals a serialised device-path replica."""
+    import ctypes
+    from paper_1904_01201_b200 import synth
+    sc = synth.config_scene("C3")
+    W, H, n, steps = 256, 128, 256, 8
+    suite = (nb.SensorConfig("rgb", W, H), nb.SensorConfig("depth", W, H),
+             nb.SensorConfig("gps_compass"))
+    a, b = (nb.BatchSimulator(sc.segments, sc.semantic_ids, sc.albedo, n, sensor_configs=suite,
+                              floor_color=sc.floor_color, ceiling_color=sc.ceiling_color)
+            for _ in range(2))
+    poses = synth.sample_poses(sc, n, seed=81)
+    for s in (a, b):
+        s.reset(poses[:, :2], poses[:, 2])
+    acts = synth.random_actions(n, steps, seed=82)
+    dacts = torch.as_tensor(acts, device="cuda:0")
+    side = torch.cuda.Stream()
+    sh = ctypes.c_void_p(side.cuda_stream)
+    out = {"gps": torch.empty((n, 2), dtype=torch.float64).pin_memory(),
+           "compass": torch.empty(n, dtype=torch.float64).pin_memory(),
+           "collided": torch.empty(n, dtype=torch.uint8).pin_memory(),
+           "displacement": torch.empty(n, dtype=torch.float64).pin_memory()}
+    torch.cuda.synchronize()
+    got = {}
+    for t in range(steps):
+        if t % 2 == 0:
+            a.step_host(np.ascontiguousarray(acts[t]), out=out, stream=sh)
+            got[t] = out["gps"].numpy().copy()
+        else:
+            a.step(dacts[t], stream=sh)
+    side.synchronize()
+    for t in range(steps):
+        b.step(dacts[t])
+        torch.cuda.synchronize()
+        if t in got:
+            assert np.array_equal(got[t], b.gps.cpu().numpy()), t
+    torch.cuda.synchronize()
+    assert a.ctx.faults() == 0
+    assert torch.equal(a.groups[0]["rgb"], b.groups[0]["rgb"])
+    assert torch.equal(a.groups[0]["depth"], b.groups[0]["depth"])
+    assert torch.equal(a.gps, b.gps)
+    for x, y in zip(a.state(), b.state()):
+        assert torch.equal(x, y)
+
+
 def test_host_buffer_path_matches_device_path(nb):
     """nv_step_render_host (graph-replayed, packed results) gives the same step
     results as nv_step_render on device buffers, across repeated
