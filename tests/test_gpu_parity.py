@@ -484,8 +484,12 @@ def test_overlap_agrees(nb, cfg, W, H, n, cast):
             assert torch.equal(a, b)
 
 
-@pytest.mark.parametrize("cfg,W,H,n,steps", [("C3", 256, 256, 512, 24), ("C4", 256, 128, 1024, 16)])
-def test_chained_steps_agree_at_scale(nb, cfg, W, H, n, steps):
+@pytest.mark.parametrize("cfg,W,H,n,steps,mode", [
+    ("C3", 256, 256, 512, 24, 0), ("C4", 256, 128, 1024, 16, 0),
+    # small batches with the thread-per-ray cast forced: per-env release and
+    # pose records with a banded writer (several writer CTAs per env)
+    ("C1", 256, 256, 1, 12, 1), ("C2", 128, 128, 3, 12, 1)])
+def test_chained_steps_agree_at_scale(nb, cfg, W, H, n, steps, mode):
     """At batch sizes where the launches really overlap (thread-per-ray cast,
     per-env release into the writer, the next agent step on the previous
     writer's tail, alternating record halves), a multi-step episode gives
@@ -501,6 +505,7 @@ def test_chained_steps_agree_at_scale(nb, cfg, W, H, n, steps):
         sim = nb.BatchSimulator(sc.segments, sc.semantic_ids, sc.albedo, n, sensor_configs=suite,
                                 floor_color=sc.floor_color, ceiling_color=sc.ceiling_color)
         nat.check(sim.ctx.lib.nv_set_overlap(sim.ctx.handle, overlap))
+        nat.check(sim.ctx.lib.nv_set_cast_mode(sim.ctx.handle, mode))
         poses = synth.sample_poses(sc, n, seed=21)
         sim.reset(poses[:, :2], poses[:, 2])
         sims.append(sim)
