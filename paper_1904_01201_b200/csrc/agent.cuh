@@ -163,7 +163,15 @@ __global__ void NV_AGENT_BOUNDS k_agent_step(EnvView ev, SceneView sc, AgentCfg 
                                                     const int8_t *__restrict__ actions,
                                                     uint8_t *collided_out,
                                                     double *disp_out, int32_t *status_out,
-                                                    unsigned *ready, double *posrec) {
+                                                    unsigned *ready, double *posrec,
+                                                    int wait_first) {
+  // wait_first: the preceding frame writer's grid does not fill the GPU, so
+  // residency no longer keeps this step (and the casts it releases) behind
+  // the previous ones (see "The path" in DESIGN.md): start the step's work,
+  // and let the casts launch, only once that writer -- and with it every
+  // earlier grid of the chain -- has completed.  The launch itself still
+  // overlaps it.
+  if (wait_first) asm volatile("griddepcontrol.wait;" ::: "memory");
   // ready: per-env flags, posrec: per-env pose records (see NV_POSE_SENTINEL)
   if (ready || posrec) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int e = (int)((blockIdx.x * (size_t)blockDim.x + threadIdx.x) >> 5);

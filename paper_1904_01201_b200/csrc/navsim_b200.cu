@@ -263,6 +263,11 @@ struct nv_ctx {
   DevBuf pdl_ready_e2e, pdl_arrive_e2e, pose_rec_e2e;
   bool pdl_init_e2e = false, pose_init_e2e = false;
   double *pdl_cur_posrec = nullptr, *fill_posrec = nullptr;
+  // the last ws writer launched: its stream and whether its grid filled the
+  // GPU (one CTA on every SM) -- only then may the next agent step work
+  // beside it (do_step)
+  cudaStream_t ws_tail_stream = nullptr;
+  bool ws_tail_full = false;
   bool fill_pdl = false;  // the next ws writer launch follows its column cast (launch_ws_kernel)
   DevBuf pdl_ready, pdl_arrive;
   // dynamic shared memory opted in per kernel on this context's device
@@ -575,6 +580,8 @@ int launch_ws_kernel(nv_ctx *c, nvk::FillArgs &a, const nvk::FillWsLayout &L, si
   TRY(set_smem(c, (const void *)kern, smem));
   const unsigned grid =
       (unsigned)std::max<int64_t>(1, std::min<int64_t>(a.N * (int64_t)L.bands, c->sm_count));
+  c->ws_tail_full = grid == (unsigned)c->sm_count;
+  c->ws_tail_stream = st;
   Prof pf(c, st, 2);
   if (c->fill_pdl) {  // a programmatic dependent of the column cast just launched
     cudaLaunchConfig_t lc = {};
@@ -926,8 +933,11 @@ int do_step(nv_ctx *c, const int8_t *actions, uint8_t *collided, double *disp, i
     at[0].val.programmaticStreamSerializationAllowed = 1;
     lc.attrs = at;
     lc.numAttrs = NV_STEP_CHAIN && c->pdl && !c->prof_on ? 1 : 0;
+    // (the agent step is a programmatic dependent of whatever precedes it;
+    // beside a full-grid writer it may work at once, else it waits for it)
+    const int wait_first = !(c->ws_tail_full && c->ws_tail_stream == st);
     CK(cudaLaunchKernelEx(&lc, nvk::k_agent_step, c->env_view(), c->scene_view(), cfg, actions,
-                          collided, disp, status, ready, posrec));
+                          collided, disp, status, ready, posrec, wait_first));
   }
   TRY(check_launch(c));
   c->pdl_armed = arm_pdl;

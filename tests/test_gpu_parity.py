@@ -486,9 +486,11 @@ def test_overlap_agrees(nb, cfg, W, H, n, cast):
 
 @pytest.mark.parametrize("cfg,W,H,n,steps,mode", [
     ("C3", 256, 256, 512, 24, 0), ("C4", 256, 128, 1024, 16, 0),
-    # small batches with the thread-per-ray cast forced: per-env release and
-    # pose records with a banded writer (several writer CTAs per env)
-    ("C1", 256, 256, 1, 12, 1), ("C2", 128, 128, 3, 12, 1)])
+    # small batches (writer grids smaller than the GPU: the agent step waits
+    # for the previous writer), with the thread-per-ray cast forced (per-env
+    # release, pose records, banded writer) and in auto mode (warp casts)
+    ("C1", 256, 256, 1, 120, 1), ("C2", 128, 128, 3, 60, 1),
+    ("C1", 256, 256, 1, 120, 0), ("C2", 128, 128, 16, 60, 0)])
 def test_chained_steps_agree_at_scale(nb, cfg, W, H, n, steps, mode):
     """At batch sizes where the launches really overlap (thread-per-ray cast,
     per-env release into the writer, the next agent step on the previous
