@@ -934,8 +934,10 @@ int do_step(nv_ctx *c, const int8_t *actions, uint8_t *collided, double *disp, i
     lc.attrs = at;
     lc.numAttrs = NV_STEP_CHAIN && c->pdl && !c->prof_on ? 1 : 0;
     // (the agent step is a programmatic dependent of whatever precedes it;
-    // beside a full-grid writer it may work at once, else it waits for it)
-    const int wait_first = !(c->ws_tail_full && c->ws_tail_stream == st);
+    // beside a full-grid writer it may work at once, else it waits for it --
+    // also while a host step's writer may still hold SMs, which voids the
+    // residency argument)
+    const int wait_first = !(c->ws_tail_full && c->ws_tail_stream == st) || c->e_pending;
     CK(cudaLaunchKernelEx(&lc, nvk::k_agent_step, c->env_view(), c->scene_view(), cfg, actions,
                           collided, disp, status, ready, posrec, wait_first));
   }
