@@ -11,8 +11,15 @@ import paper_1904_01201_b200 as nb  # noqa: E402
 from paper_1904_01201_b200 import _native as nat, synth  # noqa: E402
 
 R = int(sys.argv[1]) if len(sys.argv) > 1 else 10
-for cfg, W, H, n, steps, mode in (("C2", 128, 128, 3, 60, 1), ("C1", 256, 256, 1, 60, 1),
-                                  ("C2", 128, 128, 16, 60, 0), ("C1", 256, 256, 1, 60, 0)):
+CASES = (("C2", 128, 128, 3, 60, 1), ("C1", 256, 256, 1, 60, 1),
+         ("C2", 128, 128, 16, 60, 0), ("C1", 256, 256, 1, 60, 0),
+         # full writer grids with thread-per-ray casts (release, pose records)
+         ("C3", 256, 256, 256, 30, 0), ("C2", 256, 128, 160, 30, 0),
+         ("C3", 256, 256, 1024, 20, 0))
+only = sys.argv[2] if len(sys.argv) > 2 else None
+for cfg, W, H, n, steps, mode in CASES:
+    if only == "full" and n < 100:
+        continue
     sc = synth.config_scene(cfg)
     suite = (nb.SensorConfig("rgb", W, H), nb.SensorConfig("depth", W, H),
              nb.SensorConfig("gps_compass"))
