@@ -533,6 +533,44 @@ def test_chained_steps_agree_at_scale(nb, cfg, W, H, n, steps, mode):
         assert torch.equal(a, b)
 
 
+@pytest.mark.parametrize("cfg,W,H,n,mode", [("C2", 128, 128, 3, 1), ("C1", 256, 256, 1, 1),
+                                            ("C2", 128, 128, 16, 0)])
+def test_small_batch_chain_repeated(nb, cfg, W, H, n, mode):
+    """The chained step at small batches (writer grids smaller than the GPU),
+    repeated: eight independent 40-step back-to-back runs must each equal the
+    serialised launches (scripts/chain_stress.py found 1 in 15 runs reading a
+    stale pose record before the agent step waited for small writer grids)."""
+    from paper_1904_01201_b200 import _native as nat
+    from paper_1904_01201_b200 import synth
+    sc = synth.config_scene(cfg)
+    suite = (nb.SensorConfig("rgb", W, H), nb.SensorConfig("depth", W, H),
+             nb.SensorConfig("gps_compass"))
+    steps = 40
+    for r in range(8):
+        sims = []
+        for overlap in (0, 1):
+            sim = nb.BatchSimulator(sc.segments, sc.semantic_ids, sc.albedo, n, sensor_configs=suite)
+            nat.check(sim.ctx.lib.nv_set_overlap(sim.ctx.handle, overlap))
+            nat.check(sim.ctx.lib.nv_set_cast_mode(sim.ctx.handle, mode))
+            poses = synth.sample_poses(sc, n, seed=300 + r)
+            sim.reset(poses[:, :2], poses[:, 2])
+            sims.append(sim)
+        acts = torch.as_tensor(synth.random_actions(n, steps, seed=400 + r), device="cuda:0")
+        s0, s1 = sims
+        for s in range(steps):
+            s1.step(acts[s])
+        for s in range(steps):
+            s0.step(acts[s])
+            torch.cuda.synchronize()
+        torch.cuda.synchronize()
+        assert s1.ctx.faults() == 0, r
+        o0, o1 = s0.observations(), s1.observations()
+        for k in ("rgb", "depth", "gps", "compass"):
+            assert torch.equal(o0[k], o1[k]), (r, k)
+        for a, b in zip(s0.state(), s1.state()):
+            assert torch.equal(a, b), r
+
+
 def test_steps_without_frames_back_to_back(nb):
     """nv_step_render with no frame channels (no writer after the casts),
     issued back to back at a thread-per-ray batch: the casts then do not
