@@ -138,8 +138,11 @@ int nv_step_render(nv_ctx *ctx, const int8_t *actions, int cam, uint8_t *rgb,
  * reload until it is complete, or an acquired ready flag); the frame writer
  * takes each env as soon as its casts have published their column records
  * (thread-per-ray batches); the next step's agent step runs beside the
- * previous writer.  0 turns all of it off (serialised launches; identical
- * results). */
+ * previous writer when that writer's grid fills the GPU (after it
+ * otherwise, and while a host step's writer may still run).  The ordering
+ * across steps assumes the context has the whole GPU: with MPS SM limits or
+ * other contexts running concurrently, turn it off.  0 turns all of it off
+ * (serialised launches; identical results). */
 int nv_set_overlap(nv_ctx *ctx, int on);
 /* Column cast (raycast_grid's DDA over the grid, bit-exact in every mode):
  * NV_CAST_AUTO (default) = one thread per ray, or one warp per ray (lanes
